@@ -1,0 +1,260 @@
+/*
+ * gdp2d.h -- C ABI of the B200-native gDP2d constrained-Delaunay refinement
+ * engine (libgdp2d.so).  Plain pointers and sizes only; no CUDA or torch types.
+ *
+ * The boundary replaces the header-only C++ entry point
+ *     RunReport cdtref::refine(Mesh&, const QualityCriteria&, const EngineConfig&)
+ *     (/root/reference/proj/include/cdtref/refine.hpp:651)
+ * and, for bit-exact parity testing, its phase functions
+ *     collect                 (refine.hpp:226)
+ *     compute_splitting_points(refine.hpp:267)
+ *     locate                  (refine.hpp:301)
+ *     claim_filter            (refine.hpp:367)
+ *     cavity_filter           (refine.hpp:382)
+ *     lawson_fixpoint         (cdt.hpp:111)
+ * plus the predicates of predicates.hpp:63-185 and is_bad_triangle
+ * (refine.hpp:192).  The reference has no ABI (it is header-only and inline);
+ * INTEGRATION.md shows the C++ shim (include/gdp2d_cdtref.hpp) that re-exposes
+ * the exact cdtref::refine signature on top of these entry points.
+ *
+ * Mesh exchange format: the reference's Mesh (mesh.hpp:43-75) flattened to
+ * structure-of-arrays with IDENTICAL ids and vertex rotations:
+ *   tri_v[3t+i]  = triangles[t].v[i]
+ *   tri_n[3t+i]  = triangles[t].nbr[i]   (plain TriId, kNone = 0xFFFFFFFF)
+ *   tri_seg[3t+i]= triangles[t].seg[i]
+ * Dead slots are kept (alive = 0); ids are never recycled (as in the reference).
+ *
+ * Threading: one call = one device + one stream, blocking.  Distinct host
+ * threads may drive distinct devices (one context each).  gdp2d_last_error()
+ * is thread-local.
+ */
+#ifndef GDP2D_H
+#define GDP2D_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GDP2D_NONE    0xFFFFFFFFu /* cdtref::kNone    (mesh.hpp:23) */
+#define GDP2D_PENDING 0xFFFFFFFEu /* cdtref::kPending (mesh.hpp:24) */
+
+/* Status codes.  0 = success. */
+enum {
+    GDP2D_OK = 0,
+    GDP2D_EINVAL = 1,     /* bad argument / malformed mesh view            */
+    GDP2D_ECUDA = 2,      /* CUDA runtime error                            */
+    GDP2D_ENODEVICE = 3,  /* no usable sm_100 device                       */
+    GDP2D_ECAPACITY = 4,  /* device work-list / stack capacity exceeded    */
+    GDP2D_EMESH = 5,      /* structural failure inside a mesh mutation     */
+    GDP2D_EINTERNAL = 6
+};
+
+/* VertexKind (mesh.hpp:26) */
+enum { GDP2D_VK_INPUT = 0, GDP2D_VK_MIDPOINT = 1, GDP2D_VK_CIRCUMCENTER = 2 };
+/* RefineMode (refine.hpp:28) */
+enum { GDP2D_RUPPERT = 0, GDP2D_CHEW = 1 };
+/* SplitCandidate::Kind (refine.hpp:72) */
+enum { GDP2D_CAND_SUBSEG = 0, GDP2D_CAND_TRI = 1 };
+/* PriorityKey::Band (refine.hpp:58) */
+enum { GDP2D_BAND_CIRCUMCENTER = 0, GDP2D_BAND_MIDPOINT = 1 };
+/* Location::Kind (cdt.hpp:31) */
+enum { GDP2D_LOC_INSIDE = 0, GDP2D_LOC_ONEDGE = 1, GDP2D_LOC_ONVERTEX = 2,
+       GDP2D_LOC_OUTSIDE = 3, GDP2D_LOC_INTERCEPTED = 4 };
+
+/* Read-only host mesh (the reference Mesh, SoA). */
+typedef struct gdp2d_mesh_view {
+    uint32_t n_vertices, n_triangles, n_subsegments, batch_epoch;
+    const double*   xy;             /* [2V] x,y interleaved                   */
+    const uint8_t*  vert_kind;      /* [V]  VertexKind                        */
+    const uint32_t* vert_birth;     /* [V]  birth_batch                       */
+    const uint8_t*  vert_alive;     /* [V]                                    */
+    const uint32_t* vert_tri;       /* [V]  some alive incident triangle      */
+    const uint32_t* tri_v;          /* [3T]                                   */
+    const uint32_t* tri_n;          /* [3T] nbr[i] opposite v[i]              */
+    const uint32_t* tri_seg;        /* [3T] subsegment on edge i or NONE      */
+    const uint8_t*  tri_alive;      /* [T]                                    */
+    const uint32_t* seg_v;          /* [2S]                                   */
+    const uint32_t* seg_parent;     /* [S]  input segment index               */
+    const uint8_t*  seg_encroached; /* [S]  sticky flag                       */
+    const uint8_t*  seg_alive;      /* [S]                                    */
+    const uint32_t* seg_tri;        /* [S]  some triangle carrying s          */
+} gdp2d_mesh_view;
+
+/* Library-owned host mesh (output of refine / download).  Release with
+ * gdp2d_free().  Same layout as gdp2d_mesh_view. */
+typedef struct gdp2d_mesh_buf {
+    uint32_t n_vertices, n_triangles, n_subsegments, batch_epoch;
+    double*   xy;
+    uint8_t*  vert_kind;
+    uint32_t* vert_birth;
+    uint8_t*  vert_alive;
+    uint32_t* vert_tri;
+    uint32_t* tri_v;
+    uint32_t* tri_n;
+    uint32_t* tri_seg;
+    uint8_t*  tri_alive;
+    uint32_t* seg_v;
+    uint32_t* seg_parent;
+    uint8_t*  seg_encroached;
+    uint8_t*  seg_alive;
+    uint32_t* seg_tri;
+} gdp2d_mesh_buf;
+
+/* QualityCriteria (refine.hpp:31) + EngineConfig (refine.hpp:37) + RuleFlags
+ * (ruleskit.hpp:24).  cos2_theta MUST be computed on the host exactly as
+ * is_bad_triangle does (refine.hpp:195-196): c = std::cos(theta*pi/180); c*c.
+ * gdp2d_params_init() does that. */
+typedef struct gdp2d_params {
+    double   theta_deg;
+    double   cos2_theta;
+    double   ell;                    /* +inf = no edge bound                    */
+    uint32_t mode;                   /* GDP2D_RUPPERT / GDP2D_CHEW              */
+    uint32_t cavity_n;               /* 32                                      */
+    uint32_t rule1_compaction_threshold; /* 1024: below it work lists are not compacted */
+    uint32_t rule2_filtering_enabled;    /* cavity filter on/off               */
+    uint32_t rule4_unified_collection;   /* subsegs + triangles in one batch   */
+    uint32_t little_batch_sizing;    /* GPU: Little's-law batch cap (0 = off)   */
+    uint64_t iteration_cap;          /* 10000                                   */
+    uint64_t split_depth_cap;        /* 64                                      */
+    uint64_t batch_size_cap;         /* 0 = unlimited; keep highest priorities  */
+} gdp2d_params;
+
+/* Phase order of the per-batch timers (refine.hpp:671-701). */
+enum { GDP2D_PH_COLLECT = 0, GDP2D_PH_SPLIT_POINTS = 1, GDP2D_PH_LOCATE = 2,
+       GDP2D_PH_CLAIM = 3, GDP2D_PH_CAVITY = 4, GDP2D_PH_INSERT = 5, GDP2D_NPHASES = 6 };
+
+/* BatchMetrics (ruleskit.hpp:32) + device counters used by the roofline. */
+typedef struct gdp2d_batch_metrics {
+    uint32_t batch_index;
+    uint32_t attempted;          /* candidates entering the batch            */
+    uint32_t concurrency;        /* retained insertions (useful work, C)     */
+    uint32_t pad0;
+    double   latency;            /* seconds (sum of phases, L)               */
+    double   throughput;         /* C / L                                    */
+    double   waste_fraction;     /* 1 - useful/attempted                     */
+    double   phase_seconds[GDP2D_NPHASES];
+    /* alive counts at the start of the batch */
+    uint64_t tris_alive, verts_alive, subsegs_alive;
+    /* work counters */
+    uint64_t walk_steps, cavity_visits;
+    uint32_t survivors_claim, survivors_cavity;
+    uint32_t inserted_midpoints, inserted_circumcenters;
+    uint32_t removed_redundant, removed_dependent;
+    uint32_t dropped, marked_encroached;
+    uint64_t flips;              /* Lawson + degree-reduction flips           */
+    uint32_t flip_rounds, removal_rounds;
+} gdp2d_batch_metrics;
+
+/* RunReport (ruleskit.hpp:42). batches: caller-provided array of
+ * batches_capacity entries (may be NULL); n_batches is always the true count. */
+typedef struct gdp2d_report {
+    gdp2d_batch_metrics* batches;
+    uint32_t batches_capacity;
+    uint32_t n_batches;
+    uint64_t output_points;
+    uint64_t steiner_points;
+    uint64_t bad_triangles;
+    double   bad_area_percent;
+    double   min_angle_deg;
+    double   max_edge;
+    double   wall_seconds;       /* refine loop only (refine.hpp:653,710)     */
+    int32_t  iteration_cap_hit;
+    int32_t  pad0;
+    /* totals over all batches */
+    uint64_t total_candidates, total_walk_steps, total_cavity_visits;
+    uint64_t total_inserted, total_flips, total_removed;
+    uint64_t sum_tris_alive, sum_verts_alive, sum_subsegs_alive;
+    double   device_seconds;     /* CUDA-event time of the device loop        */
+} gdp2d_report;
+
+/* SplitCandidate (refine.hpp:71) in exchange form. */
+typedef struct gdp2d_candidate {
+    double   x, y;               /* splitting point                          */
+    double   measure;            /* PriorityKey::measure                      */
+    uint32_t id;                 /* SubsegId or TriId                         */
+    uint32_t tiebreak;           /* PriorityKey::tiebreak (list index)        */
+    uint32_t located;            /* TriId or GDP2D_PENDING                    */
+    uint8_t  kind;               /* GDP2D_CAND_*                              */
+    uint8_t  band;               /* GDP2D_BAND_*                              */
+    uint8_t  alive;
+    uint8_t  fallback;           /* circumcenter fell back to longest edge   */
+} gdp2d_candidate;
+
+/* ---- whole-run entry point ------------------------------------------------ */
+
+/* Fill p with the reference defaults (QualityCriteria{theta, ell, mode},
+ * EngineConfig{}) and the host-computed cos^2(theta). */
+void gdp2d_params_init(gdp2d_params* p, double theta_deg, double ell, uint32_t mode);
+
+/* Refine `in` on `device`; writes the refined mesh into *out (library-owned
+ * host buffers) and the run report into *r.  Timed scope (r->wall_seconds)
+ * covers H2D of the input, every batch and D2H of the result. */
+int gdp2d_refine(const gdp2d_mesh_view* in, gdp2d_mesh_buf* out, const gdp2d_params* p,
+                 gdp2d_report* r, int device);
+
+void gdp2d_free(gdp2d_mesh_buf* out);
+const char* gdp2d_last_error(void);
+const char* gdp2d_version(void);
+/* sizeof() of the exchange structs, for binding-layout checks:
+ * 0 mesh_view, 1 mesh_buf, 2 params, 3 batch_metrics, 4 report, 5 candidate */
+size_t gdp2d_struct_size(int which);
+
+/* ---- device-resident context (bench / replicas / parity) ------------------- */
+
+typedef struct gdp2d_ctx gdp2d_ctx;
+
+int  gdp2d_ctx_create(gdp2d_ctx** ctx, int device);
+void gdp2d_ctx_destroy(gdp2d_ctx* ctx);
+/* Upload a mesh into the context's pristine copy and working mesh. */
+int  gdp2d_ctx_upload(gdp2d_ctx* ctx, const gdp2d_mesh_view* in);
+/* Restore the working mesh from the pristine copy (device-to-device). */
+int  gdp2d_ctx_reset(gdp2d_ctx* ctx);
+/* Refine the working mesh in place (device-resident input and output). */
+int  gdp2d_ctx_refine(gdp2d_ctx* ctx, const gdp2d_params* p, gdp2d_report* r);
+int  gdp2d_ctx_download(gdp2d_ctx* ctx, gdp2d_mesh_buf* out);
+/* Bytes of device memory held by the context. */
+uint64_t gdp2d_ctx_device_bytes(gdp2d_ctx* ctx);
+
+/* ---- per-phase parity entry points (operate on the working mesh) ----------- */
+
+/* collect + compute_splitting_points: writes up to cap candidates in the
+ * reference's list order; *n = true count.  Returns GDP2D_ECAPACITY if cap is
+ * too small (nothing written beyond cap). */
+int gdp2d_collect(gdp2d_ctx* ctx, const gdp2d_params* p, gdp2d_candidate* out,
+                  uint32_t cap, uint32_t* n);
+/* compute_splitting_points on a caller list (ids/kinds given). */
+int gdp2d_split_points(gdp2d_ctx* ctx, gdp2d_candidate* c, uint32_t n);
+/* locate (refine.hpp:301): in/out on the list. */
+int gdp2d_locate(gdp2d_ctx* ctx, gdp2d_candidate* c, uint32_t n);
+/* claim_filter (refine.hpp:367): in/out (alive). */
+int gdp2d_claim(gdp2d_ctx* ctx, gdp2d_candidate* c, uint32_t n);
+/* cavity_filter (refine.hpp:382) with bound n_cav; optional regions out
+ * (regions[i*(n_cav+1) ...], region_len[i]) may be NULL. */
+int gdp2d_cavity(gdp2d_ctx* ctx, gdp2d_candidate* c, uint32_t n, uint32_t n_cav,
+                 uint32_t* regions, uint32_t* region_len);
+/* lawson_fixpoint (cdt.hpp:111) seeded with (tri, edge) pairs. */
+int gdp2d_flip_fixpoint(gdp2d_ctx* ctx, const uint32_t* seed_tri, const uint8_t* seed_edge,
+                        uint32_t n, uint64_t* flips);
+
+/* ---- predicate batches (predicates.hpp, refine.hpp:192) -------------------- */
+
+enum { GDP2D_PRED_ORIENT2D = 0,      /* pts: a,b,c          -> {-1,0,1}   */
+       GDP2D_PRED_INCIRCLE = 1,      /* pts: a,b,c,d        -> {-1,0,1}   */
+       GDP2D_PRED_DIAMETRIC = 2,     /* pts: sa,sb,p        -> {0,1}      */
+       GDP2D_PRED_LENS = 3,          /* pts: sa,sb,p        -> {0,1}      */
+       GDP2D_PRED_BAD_TRIANGLE = 4 };/* pts: a,b,c          -> {0,1} (uses p) */
+/* pts holds n records of 2*arity doubles; out gets n int8 results. */
+int gdp2d_predicates_batch(int device, int kind, const double* pts, uint32_t n,
+                           const gdp2d_params* p, int8_t* out);
+/* circumcenter (predicates.hpp:172): pts = n*(a,b,c); out = n*(x,y); ok = n. */
+int gdp2d_circumcenter_batch(int device, const double* pts, uint32_t n, double* out,
+                             uint8_t* ok);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GDP2D_H */

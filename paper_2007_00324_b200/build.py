@@ -1,0 +1,118 @@
+"""In-tree build of the native libraries (the built .so files travel to the GPU box).
+
+  lib/libgdp2d.so       CUDA engine (sm_100a only), C ABI of include/gdp2d.h
+  lib/libgdp2d_host.so  host side kept from the reference (PSLG/mesh I/O, Line-1
+                        build_cdt) + the synthetic PSLG generator; compiled against
+                        /root/reference/proj/include when that tree is present
+  oracle/_ref/*.so      test-infrastructure checkers (oracle/Makefile)
+
+Run ``python -m paper_2007_00324_b200.build`` or ``__graft_entry__.build()``.
+"""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import os
+import shutil
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+LIB = PKG / "lib"
+OBJ = ROOT / "build" / "obj"
+INCLUDE = ROOT / "include"
+REF = Path(os.environ.get("GDP2D_REFERENCE", "/root/reference"))
+REF_INCLUDE = REF / "proj" / "include"
+
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc" if Path("/usr/local/cuda/bin/nvcc").exists() else "nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# -fmad=false: no a*b+c contraction, so every FP formula (is_bad_triangle,
+# circumcenter, midpoint, area, filters) is bit-identical to the reference's
+# IEEE evaluation; exact predicates use explicit fma() for two_prod.
+NVFLAGS = ["-std=c++17", "-O3", "-lineinfo", "-fmad=false", "-Xcompiler", "-fPIC",
+           "--expt-relaxed-constexpr", "-diag-suppress", "177"]
+
+CU_SOURCES = ["k_scan.cu", "k_collect.cu", "k_locate.cu", "k_filter.cu", "k_insert.cu",
+              "k_misc.cu", "engine.cu"]
+HEADERS = ["gdp2d_common.cuh", "gdp2d_predicates.cuh", "gdp2d_geom.cuh", "scan.cuh", "engine.h"]
+
+
+def _newer(target: Path, deps) -> bool:
+    if not target.exists():
+        return False
+    t = target.stat().st_mtime
+    return all(Path(d).stat().st_mtime <= t for d in deps if Path(d).exists())
+
+
+def _run(cmd, cwd=None):
+    r = subprocess.run(cmd, cwd=cwd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"build failed: {' '.join(map(str, cmd))}\n{r.stdout}")
+    return r.stdout
+
+
+def build_cuda(force: bool = False, verbose: bool = False) -> Path:
+    LIB.mkdir(parents=True, exist_ok=True)
+    OBJ.mkdir(parents=True, exist_ok=True)
+    target = LIB / "libgdp2d.so"
+    hdrs = [CSRC / h for h in HEADERS] + [INCLUDE / "gdp2d.h"]
+    srcs = [CSRC / s for s in CU_SOURCES]
+    if not force and _newer(target, srcs + hdrs + [Path(__file__)]):
+        return target
+    if shutil.which(NVCC) is None and not Path(NVCC).exists():
+        raise RuntimeError("nvcc not found: the CUDA engine cannot be built")
+
+    def compile_one(src: Path) -> Path:
+        obj = OBJ / (src.stem + ".o")
+        if force or not _newer(obj, [src] + hdrs + [Path(__file__)]):
+            out = _run([NVCC, *ARCH, *NVFLAGS, "-I", str(INCLUDE), "-c", str(src), "-o", str(obj)])
+            if verbose and out.strip():
+                print(out)
+        return obj
+
+    with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 2)) as ex:
+        objs = list(ex.map(compile_one, srcs))
+    tmp = target.with_suffix(".so.tmp")
+    _run([NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", *map(str, objs), "-o", str(tmp)])
+    os.replace(tmp, target)
+    return target
+
+
+def build_host(force: bool = False) -> Path | None:
+    LIB.mkdir(parents=True, exist_ok=True)
+    target = LIB / "libgdp2d_host.so"
+    srcs = [CSRC / "host" / "pslg_gen.cpp", CSRC / "host" / "cdt_host.cpp"]
+    if not REF_INCLUDE.exists():
+        if target.exists():
+            return target  # prebuilt (GPU box: /root/reference is absent)
+        raise RuntimeError(f"{REF_INCLUDE} missing and no prebuilt {target}")
+    if not force and _newer(target, srcs + [INCLUDE / "gdp2d.h", Path(__file__)]):
+        return target
+    tmp = target.with_suffix(".so.tmp")
+    _run(["g++", "-std=c++20", "-O3", "-DNDEBUG", "-ffp-contract=off", "-fPIC", "-shared",
+          "-pthread", "-I", str(INCLUDE), "-I", str(REF_INCLUDE), *map(str, srcs), "-o", str(tmp)])
+    os.replace(tmp, target)
+    return target
+
+
+def build_oracle(force: bool = False) -> None:
+    """Checker libraries (test infrastructure only)."""
+    odir = ROOT / "oracle"
+    targets = ["_ref/libgdp2d_oracle.so"]
+    if REF_INCLUDE.exists():
+        targets.append("_ref/libcdtref_ref.so")
+    cmd = ["make", "-s", "-C", str(odir), f"REF={REF}"] + (["-B"] if force else []) + targets
+    _run(cmd)
+
+
+def build_all(force: bool = False, verbose: bool = False) -> None:
+    build_cuda(force, verbose)
+    build_host(force)
+    build_oracle(force)
+
+
+if __name__ == "__main__":
+    build_all(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    print("built:", *sorted(p.name for p in LIB.glob("*.so")))

@@ -1,0 +1,1113 @@
+// engine.cu -- the device-resident refinement loop (refine, refine.hpp:651-713)
+// and the C ABI of include/gdp2d.h.
+//
+// One context = one device + one stream.  The working mesh lives in HBM with
+// headroom; the host only reads a handful of counters per batch / round to
+// size the next launch (and to grow buffers between batches).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <functional>
+#include <string>
+#include <vector>
+
+#include "engine.h"
+#include "gdp2d.h"
+
+using namespace gdp2d;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct CudaError {
+    std::string what;
+};
+
+#define CK(x)                                                                        \
+    do {                                                                             \
+        cudaError_t e_ = (x);                                                        \
+        if (e_ != cudaSuccess)                                                       \
+            throw CudaError{std::string(#x) + ": " + cudaGetErrorString(e_)};        \
+    } while (0)
+
+struct Fail {
+    int code;
+    std::string what;
+};
+
+template <class T>
+void dalloc(T*& p, size_t n) {
+    p = nullptr;
+    if (n == 0) n = 1;
+    CK(cudaMalloc(&p, sizeof(T) * n));
+}
+template <class T>
+void dfree(T*& p) {
+    if (p) cudaFree(p);
+    p = nullptr;
+}
+
+// Grow a device array to n elements, preserving the first keep elements.
+template <class T>
+void dgrow(T*& p, size_t keep, size_t n, cudaStream_t st) {
+    T* q = nullptr;
+    dalloc(q, n);
+    if (p && keep) CK(cudaMemcpyAsync(q, p, sizeof(T) * keep, cudaMemcpyDeviceToDevice, st));
+    if (p) {
+        CK(cudaStreamSynchronize(st));
+        cudaFree(p);
+    }
+    p = q;
+}
+
+struct MeshStore {
+    DevMesh m{};
+    u32 vcap = 0, tcap = 0, scap = 0;
+};
+
+void mesh_free(MeshStore& s) {
+    DevMesh& m = s.m;
+    dfree(m.xy); dfree(m.vkind); dfree(m.vbirth); dfree(m.valive); dfree(m.vtri);
+    dfree(m.tv); dfree(m.tn); dfree(m.ts);
+    dfree(m.sv); dfree(m.sparent); dfree(m.senc); dfree(m.salive); dfree(m.stri); dfree(m.sdepth);
+    s.vcap = s.tcap = s.scap = 0;
+}
+
+void mesh_reserve(MeshStore& s, u32 V, u32 T, u32 S, cudaStream_t st) {
+    DevMesh& m = s.m;
+    if (V > s.vcap) {
+        dgrow(m.xy, m.nV, V, st);
+        dgrow(m.vkind, m.nV, V, st);
+        dgrow(m.vbirth, m.nV, V, st);
+        dgrow(m.valive, m.nV, V, st);
+        dgrow(m.vtri, m.nV, V, st);
+        s.vcap = V;
+    }
+    if (T > s.tcap) {
+        dgrow(m.tv, m.nT, T, st);
+        dgrow(m.tn, m.nT, T, st);
+        dgrow(m.ts, m.nT, T, st);
+        s.tcap = T;
+    }
+    if (S > s.scap) {
+        dgrow(m.sv, m.nS, S, st);
+        dgrow(m.sparent, m.nS, S, st);
+        dgrow(m.senc, m.nS, S, st);
+        dgrow(m.salive, m.nS, S, st);
+        dgrow(m.stri, m.nS, S, st);
+        dgrow(m.sdepth, m.nS, S, st);
+        s.scap = S;
+    }
+}
+
+void mesh_copy(MeshStore& dst, const MeshStore& src, cudaStream_t st) {
+    const DevMesh& a = src.m;
+    DevMesh& b = dst.m;
+    mesh_reserve(dst, a.nV, a.nT, a.nS, st);
+    auto cp = [&](void* d, const void* s, size_t bytes) {
+        if (bytes) CK(cudaMemcpyAsync(d, s, bytes, cudaMemcpyDeviceToDevice, st));
+    };
+    cp(b.xy, a.xy, sizeof(double2) * a.nV);
+    cp(b.vkind, a.vkind, a.nV);
+    cp(b.vbirth, a.vbirth, 4ull * a.nV);
+    cp(b.valive, a.valive, a.nV);
+    cp(b.vtri, a.vtri, 4ull * a.nV);
+    cp(b.tv, a.tv, sizeof(uint4) * a.nT);
+    cp(b.tn, a.tn, sizeof(uint4) * a.nT);
+    cp(b.ts, a.ts, sizeof(uint4) * a.nT);
+    cp(b.sv, a.sv, sizeof(uint2) * a.nS);
+    cp(b.sparent, a.sparent, 4ull * a.nS);
+    cp(b.senc, a.senc, 4ull * a.nS);
+    cp(b.salive, a.salive, a.nS);
+    cp(b.stri, a.stri, 4ull * a.nS);
+    cp(b.sdepth, a.sdepth, 4ull * a.nS);
+    b.nV = a.nV;
+    b.nT = a.nT;
+    b.nS = a.nS;
+}
+
+__global__ void k_pack_tris(DevMesh m, const u32* __restrict__ tv3, const u32* __restrict__ ts3,
+                            const uint8_t* __restrict__ alive) {
+    const u32 t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= m.nT) return;
+    m.tv[t] = make_uint4(tv3[3 * t], tv3[3 * t + 1], tv3[3 * t + 2], alive[t] ? 1u : 0u);
+    m.ts[t] = make_uint4(ts3[3 * t], ts3[3 * t + 1], ts3[3 * t + 2], 0u);
+}
+
+__global__ void k_unpack_tris(DevMesh m, u32* __restrict__ tv3, u32* __restrict__ ts3,
+                              uint8_t* __restrict__ alive) {
+    const u32 t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= m.nT) return;
+    const uint4 tv = m.tv[t], ts = m.ts[t];
+    tv3[3 * t] = tv.x;
+    tv3[3 * t + 1] = tv.y;
+    tv3[3 * t + 2] = tv.z;
+    alive[t] = tv.w ? 1 : 0;
+    ts3[3 * t] = ts.x;
+    ts3[3 * t + 1] = ts.y;
+    ts3[3 * t + 2] = ts.z;
+}
+
+__global__ void k_u8_to_u32(const uint8_t* __restrict__ a, u32* __restrict__ b, u32 n) {
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) b[i] = a[i];
+}
+__global__ void k_u32_to_u8(const u32* __restrict__ a, uint8_t* __restrict__ b, u32 n) {
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) b[i] = a[i] ? 1 : 0;
+}
+
+__global__ void k_fill_u64(u64* p, u64 v, size_t n) {
+    const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+u32 grid(size_t n, u32 b = 256) { return (u32)((n + b - 1) / b); }
+
+Quality make_quality(const gdp2d_params* p) {
+    Quality q;
+    q.cos2 = p->cos2_theta;
+    q.ell = p->ell;
+    q.mode = p->mode == GDP2D_CHEW ? 1 : 0;
+    return q;
+}
+
+const char* dev_err_name(u32 c) {
+    switch (c) {
+        case DERR_NONCONVEX_FLIP: return "non-convex flip of a non-Delaunay edge";
+        case DERR_STAR_TOO_LARGE: return "vertex star exceeds MAX_STAR";
+        case DERR_NO_EAR: return "no removable ear in a vertex star";
+        case DERR_WORKLIST_OVERFLOW: return "device work list overflow";
+        case DERR_OPEN_STAR: return "open star around a free vertex";
+        case DERR_STALE: return "stale handle";
+        case DERR_WALK: return "walk failure";
+        default: return "unknown device error";
+    }
+}
+
+}  // namespace
+
+struct gdp2d_ctx {
+    int device = 0;
+    cudaStream_t st = nullptr;
+    MeshStore work, pristine;
+    u32 epoch = 0, pristine_epoch = 0;
+    ull alive_v = 0, alive_t = 0, alive_s = 0;            // working-mesh alive counts
+    ull p_alive_v = 0, p_alive_t = 0, p_alive_s = 0;
+    // per-triangle scratch
+    TriAux aux;
+    u32 aux_cap = 0;
+    uint8_t* flags = nullptr;
+    size_t flags_cap = 0;
+    // candidates
+    DevCands c{};
+    u32 ccap = 0;
+    u32* regions = nullptr;
+    u32* region_len = nullptr;
+    u32* bfs_len = nullptr;
+    size_t reg_cap = 0;   // entries in regions
+    u32 rl_cap = 0;       // entries in region_len / bfs_len
+    InsertBufs ib;
+    FreshInfo fresh;
+    WorkLists wl;
+    ScanScratch scan;
+    Counters* d_ctr = nullptr;
+    Counters* h_ctr = nullptr;    // pinned
+    RoundCtr* h_rc = nullptr;     // pinned
+    u32* h_tot = nullptr;         // pinned [4]
+    void* qscratch = nullptr;
+    u32 round = 0;
+    cudaEvent_t ev[GDP2D_NPHASES + 2];
+    // upload / download staging
+    u32* stage_u32[3] = {nullptr, nullptr, nullptr};
+    uint8_t* stage_u8 = nullptr;
+    size_t stage_cap = 0;
+};
+
+namespace {
+
+void cands_free(DevCands& c) {
+    dfree(c.pt); dfree(c.key); dfree(c.id); dfree(c.tie); dfree(c.loc);
+    dfree(c.kind); dfree(c.alive); dfree(c.lkind); dfree(c.ledge); dfree(c.fb);
+}
+
+void ensure_cands(gdp2d_ctx* x, u32 n) {
+    if (n <= x->ccap) return;
+    cands_free(x->c);
+    const u32 cap = std::max<u32>(n + n / 2, 1024);
+    dalloc(x->c.pt, cap); dalloc(x->c.key, cap); dalloc(x->c.id, cap); dalloc(x->c.tie, cap);
+    dalloc(x->c.loc, cap); dalloc(x->c.kind, cap); dalloc(x->c.alive, cap);
+    dalloc(x->c.lkind, cap); dalloc(x->c.ledge, cap); dalloc(x->c.fb, cap);
+    x->ccap = cap;
+    // per-candidate insertion buffers
+    dfree(x->ib.nv); dfree(x->ib.nt); dfree(x->ib.ns); dfree(x->ib.ov); dfree(x->ib.ot);
+    dfree(x->ib.os);
+    dalloc(x->ib.nv, cap); dalloc(x->ib.nt, cap); dalloc(x->ib.ns, cap);
+    dalloc(x->ib.ov, cap); dalloc(x->ib.ot, cap); dalloc(x->ib.os, cap);
+    if (!x->ib.totals) dalloc(x->ib.totals, 4);
+    x->ib.cap = cap;
+}
+
+void ensure_regions(gdp2d_ctx* x, u32 n, u32 ncav) {
+    const size_t rs = ncav + 1 + MAX_CLAIM_EXTRA;
+    if ((size_t)n * rs > x->reg_cap) {
+        dfree(x->regions);
+        x->reg_cap = std::max<size_t>((size_t)n * rs * 3 / 2, 4096);
+        dalloc(x->regions, x->reg_cap);
+    }
+    if (n > x->rl_cap) {
+        dfree(x->region_len);
+        dfree(x->bfs_len);
+        x->rl_cap = std::max<u32>(n + n / 2, 1024);
+        dalloc(x->region_len, x->rl_cap);
+        dalloc(x->bfs_len, x->rl_cap);
+    }
+}
+
+void ensure_aux(gdp2d_ctx* x) {
+    const u32 T = x->work.tcap;
+    if (T > x->aux_cap) {
+        dfree(x->aux.ckey); dfree(x->aux.ctie); dfree(x->aux.owner); dfree(x->aux.stamp);
+        dfree(x->aux.emap);
+        dalloc(x->aux.ckey, T); dalloc(x->aux.ctie, T); dalloc(x->aux.owner, T);
+        dalloc(x->aux.stamp, T); dalloc(x->aux.emap, 3ull * T);
+        CK(cudaMemsetAsync(x->aux.ckey, 0, sizeof(u64) * T, x->st));
+        CK(cudaMemsetAsync(x->aux.ctie, 0xFF, sizeof(u64) * T, x->st));
+        CK(cudaMemsetAsync(x->aux.owner, 0xFF, sizeof(u32) * T, x->st));
+        CK(cudaMemsetAsync(x->aux.stamp, 0, sizeof(u32) * T, x->st));
+        x->aux_cap = T;
+        x->round = 0;
+    }
+    const size_t fl = ((size_t)(x->work.scap + SCAN_TILE - 1) / SCAN_TILE +
+                       (size_t)(x->work.tcap + SCAN_TILE - 1) / SCAN_TILE + 2) *
+                      SCAN_TILE;
+    if (fl > x->flags_cap) {
+        dfree(x->flags);
+        dalloc(x->flags, fl);
+        x->flags_cap = fl;
+    }
+    // work lists: sized by triangle capacity
+    const u32 wcap = 2 * T + (1u << 20);
+    if (wcap > x->wl.cap) {
+        dfree(x->wl.w[0]); dfree(x->wl.w[1]); dfree(x->wl.fc); dfree(x->wl.fu);
+        dfree(x->wl.touched); dfree(x->wl.fwin);
+        dalloc(x->wl.w[0], wcap); dalloc(x->wl.w[1], wcap); dalloc(x->wl.fc, wcap);
+        dalloc(x->wl.fu, wcap); dalloc(x->wl.touched, wcap); dalloc(x->wl.fwin, wcap);
+        x->wl.cap = wcap;
+    }
+}
+
+void ensure_fresh(gdp2d_ctx* x, u32 n) {
+    if (n <= x->fresh.cap) return;
+    FreshInfo& f = x->fresh;
+    dfree(f.key); dfree(f.tie); dfree(f.cc); dfree(f.removed); dfree(f.mark);
+    const u32 cap = std::max<u32>(n + n / 2, 1024);
+    dalloc(f.key, cap); dalloc(f.tie, cap); dalloc(f.cc, cap); dalloc(f.removed, cap);
+    dalloc(f.mark, cap);
+    f.cap = cap;
+    dfree(x->wl.rm[0]); dfree(x->wl.rm[1]); dfree(x->wl.star); dfree(x->wl.star_len);
+    dalloc(x->wl.rm[0], cap); dalloc(x->wl.rm[1], cap);
+    dalloc(x->wl.star, (size_t)cap * MAX_STAR);
+    dalloc(x->wl.star_len, cap);
+    x->wl.rm_cap = cap;
+}
+
+// Working-mesh capacity for the next insertion (amortised growth).
+void ensure_mesh(gdp2d_ctx* x, u32 V, u32 T, u32 S) {
+    MeshStore& w = x->work;
+    if (V <= w.vcap && T <= w.tcap && S <= w.scap) return;
+    const auto grow = [](u32 need, u32 cap) {
+        return need <= cap ? cap : (u32)std::min<u64>(0xFFFFFFF0ull, (u64)need * 3 / 2 + 1024);
+    };
+    mesh_reserve(w, grow(V, w.vcap), grow(T, w.tcap), grow(S, w.scap), x->st);
+    ensure_aux(x);
+}
+
+void zero_rc(gdp2d_ctx* x) { CK(cudaMemsetAsync(x->wl.rc, 0, sizeof(RoundCtr), x->st)); }
+
+RoundCtr read_rc(gdp2d_ctx* x) {
+    CK(cudaMemcpyAsync(x->h_rc, x->wl.rc, sizeof(RoundCtr), cudaMemcpyDeviceToHost, x->st));
+    CK(cudaStreamSynchronize(x->st));
+    return *x->h_rc;
+}
+
+void check_dev_err(gdp2d_ctx* x) {
+    CK(cudaMemcpyAsync(x->h_ctr, x->d_ctr, sizeof(Counters), cudaMemcpyDeviceToHost, x->st));
+    CK(cudaStreamSynchronize(x->st));
+    if (x->h_ctr->err_code) {
+        char buf[160];
+        snprintf(buf, sizeof buf, "device error %u (%s), info %u", x->h_ctr->err_code,
+                 dev_err_name(x->h_ctr->err_code), x->h_ctr->err_info);
+        throw Fail{x->h_ctr->err_code == DERR_WORKLIST_OVERFLOW ? GDP2D_ECAPACITY : GDP2D_EMESH,
+                   buf};
+    }
+}
+
+}  // namespace
+
+// Lawson driver that tracks which buffer holds the live work list.
+static void lawson_from(gdp2d_ctx* x, u32 start_buf, u32 n, u32* rounds) {
+    u32 cur = start_buf;
+    u32 guard = 0;
+    while (n > 0) {
+        if (n > x->wl.cap) throw Fail{GDP2D_ECAPACITY, "Lawson work list overflow"};
+        if (++guard > 200000) throw Fail{GDP2D_EMESH, "Lawson flip rounds did not converge"};
+        ++x->round;
+        zero_rc(x);
+        launch_flip_round(x->work.m, x->round, x->aux, x->wl, cur, n, x->d_ctr, x->st);
+        const RoundCtr rc = read_rc(x);
+        if (rc.wl_next > x->wl.cap) throw Fail{GDP2D_ECAPACITY, "Lawson work list overflow"};
+        n = rc.wl_next;
+        cur ^= 1u;
+        if (rounds) ++*rounds;
+    }
+}
+
+namespace {
+
+void ctx_init(gdp2d_ctx* x, int device) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+        throw Fail{GDP2D_ENODEVICE, "no CUDA device visible"};
+    if (device < 0 || device >= n) throw Fail{GDP2D_ENODEVICE, "device index out of range"};
+    CK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10)
+        throw Fail{GDP2D_ENODEVICE, std::string("sm_100a required, found ") + prop.name};
+    x->device = device;
+    CK(cudaStreamCreateWithFlags(&x->st, cudaStreamNonBlocking));
+    dalloc(x->d_ctr, 1);
+    dalloc(x->wl.rc, 1);
+    CK(cudaMallocHost(&x->h_ctr, sizeof(Counters)));
+    CK(cudaMallocHost(&x->h_rc, sizeof(RoundCtr)));
+    CK(cudaMallocHost(&x->h_tot, 4 * sizeof(u32)));
+    CK(cudaMalloc(&x->qscratch, 256));
+    for (auto& e : x->ev) CK(cudaEventCreate(&e));
+}
+
+void ctx_release(gdp2d_ctx* x) {
+    cudaSetDevice(x->device);
+    mesh_free(x->work);
+    mesh_free(x->pristine);
+    dfree(x->aux.ckey); dfree(x->aux.ctie); dfree(x->aux.owner); dfree(x->aux.stamp);
+    dfree(x->aux.emap); dfree(x->flags);
+    cands_free(x->c);
+    dfree(x->regions); dfree(x->region_len); dfree(x->bfs_len);
+    dfree(x->ib.nv); dfree(x->ib.nt); dfree(x->ib.ns); dfree(x->ib.ov); dfree(x->ib.ot);
+    dfree(x->ib.os); dfree(x->ib.totals);
+    dfree(x->fresh.key); dfree(x->fresh.tie); dfree(x->fresh.cc); dfree(x->fresh.removed);
+    dfree(x->fresh.mark);
+    dfree(x->wl.w[0]); dfree(x->wl.w[1]); dfree(x->wl.fc); dfree(x->wl.fu);
+    dfree(x->wl.touched); dfree(x->wl.fwin); dfree(x->wl.rm[0]); dfree(x->wl.rm[1]);
+    dfree(x->wl.star); dfree(x->wl.star_len); dfree(x->wl.rc);
+    dfree(x->scan.partial);
+    dfree(x->d_ctr);
+    for (auto& s : x->stage_u32) dfree(s);
+    dfree(x->stage_u8);
+    if (x->h_ctr) cudaFreeHost(x->h_ctr);
+    if (x->h_rc) cudaFreeHost(x->h_rc);
+    if (x->h_tot) cudaFreeHost(x->h_tot);
+    if (x->qscratch) cudaFree(x->qscratch);
+    for (auto& e : x->ev)
+        if (e) cudaEventDestroy(e);
+    if (x->st) cudaStreamDestroy(x->st);
+}
+
+void ensure_stage(gdp2d_ctx* x, size_t n) {
+    if (n <= x->stage_cap) return;
+    for (auto& s : x->stage_u32) {
+        dfree(s);
+        dalloc(s, n);
+    }
+    dfree(x->stage_u8);
+    dalloc(x->stage_u8, n);
+    x->stage_cap = n;
+}
+
+void validate_view(const gdp2d_mesh_view* v) {
+    if (!v) throw Fail{GDP2D_EINVAL, "null mesh view"};
+    if (v->n_triangles && (!v->tri_v || !v->tri_n || !v->tri_seg || !v->tri_alive))
+        throw Fail{GDP2D_EINVAL, "missing triangle arrays"};
+    if (v->n_vertices && (!v->xy || !v->vert_kind || !v->vert_birth || !v->vert_alive ||
+                          !v->vert_tri))
+        throw Fail{GDP2D_EINVAL, "missing vertex arrays"};
+    if (v->n_subsegments && (!v->seg_v || !v->seg_parent || !v->seg_encroached ||
+                             !v->seg_alive || !v->seg_tri))
+        throw Fail{GDP2D_EINVAL, "missing subsegment arrays"};
+    if (v->n_triangles >= (1u << 30)) throw Fail{GDP2D_EINVAL, "too many triangles"};
+}
+
+void upload(gdp2d_ctx* x, const gdp2d_mesh_view* v) {
+    validate_view(v);
+    const u32 V = v->n_vertices, T = v->n_triangles, S = v->n_subsegments;
+    MeshStore& p = x->pristine;
+    p.m.nV = p.m.nT = p.m.nS = 0;
+    mesh_reserve(p, V, T, S, x->st);
+    DevMesh& m = p.m;
+    m.nV = V;
+    m.nT = T;
+    m.nS = S;
+    cudaStream_t st = x->st;
+    CK(cudaMemcpyAsync(m.xy, v->xy, 16ull * V, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(m.vkind, v->vert_kind, V, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(m.vbirth, v->vert_birth, 4ull * V, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(m.valive, v->vert_alive, V, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(m.vtri, v->vert_tri, 4ull * V, cudaMemcpyHostToDevice, st));
+    ensure_stage(x, std::max<size_t>(3ull * T, 2ull * S) + 16);
+    if (T) {
+        CK(cudaMemcpyAsync(x->stage_u32[0], v->tri_v, 12ull * T, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(x->stage_u32[1], v->tri_seg, 12ull * T, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(x->stage_u32[2], v->tri_n, 12ull * T, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(x->stage_u8, v->tri_alive, T, cudaMemcpyHostToDevice, st));
+        k_pack_tris<<<grid(T), 256, 0, st>>>(m, x->stage_u32[0], x->stage_u32[1], x->stage_u8);
+        launch_encode_neighbors(m, x->stage_u32[2], st);
+    }
+    if (S) {
+        CK(cudaMemcpyAsync(m.sv, v->seg_v, 8ull * S, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(m.sparent, v->seg_parent, 4ull * S, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(m.salive, v->seg_alive, S, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(m.stri, v->seg_tri, 4ull * S, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(x->stage_u8 + 3ull * T + 8, v->seg_encroached, S,
+                           cudaMemcpyHostToDevice, st));
+        k_u8_to_u32<<<grid(S), 256, 0, st>>>(x->stage_u8 + 3ull * T + 8, m.senc, S);
+        CK(cudaMemsetAsync(m.sdepth, 0, 4ull * S, st));
+    }
+    CK(cudaGetLastError());
+    x->pristine_epoch = v->batch_epoch;
+    ull av = 0, at = 0, as = 0;
+    for (u32 i = 0; i < V; ++i) av += v->vert_alive[i] != 0;
+    for (u32 i = 0; i < T; ++i) at += v->tri_alive[i] != 0;
+    for (u32 i = 0; i < S; ++i) as += v->seg_alive[i] != 0;
+    x->p_alive_v = av;
+    x->p_alive_t = at;
+    x->p_alive_s = as;
+}
+
+void reset_work(gdp2d_ctx* x) {
+    const DevMesh& p = x->pristine.m;
+    // headroom: 2.5x the input (amortised growth handles the rest)
+    x->work.m.nV = x->work.m.nT = x->work.m.nS = 0;
+    mesh_reserve(x->work, std::max<u32>(p.nV * 5 / 2, 1024), std::max<u32>(p.nT * 5 / 2, 2048),
+                 std::max<u32>(p.nS * 5 / 2, 1024), x->st);
+    mesh_copy(x->work, x->pristine, x->st);
+    // subsegment depth restarts at 0 for every refine call (refine.hpp:655)
+    if (x->work.m.nS) CK(cudaMemsetAsync(x->work.m.sdepth, 0, 4ull * x->work.m.nS, x->st));
+    x->epoch = x->pristine_epoch;
+    x->alive_v = x->p_alive_v;
+    x->alive_t = x->p_alive_t;
+    x->alive_s = x->p_alive_s;
+    ensure_aux(x);
+}
+
+void download(gdp2d_ctx* x, gdp2d_mesh_buf* b) {
+    const DevMesh& m = x->work.m;
+    const u32 V = m.nV, T = m.nT, S = m.nS;
+    cudaStream_t st = x->st;
+    std::memset(b, 0, sizeof *b);
+    b->n_vertices = V;
+    b->n_triangles = T;
+    b->n_subsegments = S;
+    b->batch_epoch = x->epoch;
+    auto hm = [](size_t bytes) { return std::malloc(bytes ? bytes : 1); };
+    b->xy = (double*)hm(16ull * V);
+    b->vert_kind = (uint8_t*)hm(V);
+    b->vert_birth = (u32*)hm(4ull * V);
+    b->vert_alive = (uint8_t*)hm(V);
+    b->vert_tri = (u32*)hm(4ull * V);
+    b->tri_v = (u32*)hm(12ull * T);
+    b->tri_n = (u32*)hm(12ull * T);
+    b->tri_seg = (u32*)hm(12ull * T);
+    b->tri_alive = (uint8_t*)hm(T);
+    b->seg_v = (u32*)hm(8ull * S);
+    b->seg_parent = (u32*)hm(4ull * S);
+    b->seg_encroached = (uint8_t*)hm(S);
+    b->seg_alive = (uint8_t*)hm(S);
+    b->seg_tri = (u32*)hm(4ull * S);
+    ensure_stage(x, std::max<size_t>(3ull * T, 2ull * S) + 16);
+    CK(cudaMemcpyAsync(b->xy, m.xy, 16ull * V, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(b->vert_kind, m.vkind, V, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(b->vert_birth, m.vbirth, 4ull * V, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(b->vert_alive, m.valive, V, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(b->vert_tri, m.vtri, 4ull * V, cudaMemcpyDeviceToHost, st));
+    if (T) {
+        k_unpack_tris<<<grid(T), 256, 0, st>>>(m, x->stage_u32[0], x->stage_u32[1], x->stage_u8);
+        launch_decode_neighbors(m, x->stage_u32[2], st);
+        CK(cudaMemcpyAsync(b->tri_v, x->stage_u32[0], 12ull * T, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(b->tri_seg, x->stage_u32[1], 12ull * T, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(b->tri_n, x->stage_u32[2], 12ull * T, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(b->tri_alive, x->stage_u8, T, cudaMemcpyDeviceToHost, st));
+    }
+    if (S) {
+        CK(cudaStreamSynchronize(st));  // stage_u8 reused below
+        CK(cudaMemcpyAsync(b->seg_v, m.sv, 8ull * S, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(b->seg_parent, m.sparent, 4ull * S, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(b->seg_alive, m.salive, S, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(b->seg_tri, m.stri, 4ull * S, cudaMemcpyDeviceToHost, st));
+        k_u32_to_u8<<<grid(S), 256, 0, st>>>(m.senc, x->stage_u8, S);
+        CK(cudaMemcpyAsync(b->seg_encroached, x->stage_u8, S, cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaStreamSynchronize(st));
+    CK(cudaGetLastError());
+}
+
+double ev_ms(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    return (double)ms;
+}
+
+// The refinement loop (refine.hpp:651-713) on the working mesh.
+void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
+    const auto wall0 = std::chrono::steady_clock::now();
+    cudaStream_t st = x->st;
+    const Quality q = make_quality(p);
+    const u32 ncav = p->rule2_filtering_enabled ? p->cavity_n : 0;
+    if (ncav > (u32)MAX_CAVITY_N) throw Fail{GDP2D_EINVAL, "cavity_n exceeds 64"};
+    const gdp2d_report keep = *r;
+    std::memset(r, 0, sizeof *r);
+    r->batches = keep.batches;
+    r->batches_capacity = keep.batches_capacity;
+    CK(cudaEventRecord(x->ev[GDP2D_NPHASES + 1], st));  // loop start
+    for (u64 iter = 0;; ++iter) {
+        if (iter >= p->iteration_cap) {
+            r->iteration_cap_hit = 1;
+            break;
+        }
+        DevMesh& m = x->work.m;
+        gdp2d_batch_metrics bm;
+        std::memset(&bm, 0, sizeof bm);
+        bm.batch_index = r->n_batches;
+        bm.tris_alive = x->alive_t;
+        bm.verts_alive = x->alive_v;
+        bm.subsegs_alive = x->alive_s;
+        CK(cudaMemsetAsync(x->d_ctr, 0, sizeof(Counters), st));
+        ensure_cands(x, m.nS + m.nT);
+        CK(cudaEventRecord(x->ev[0], st));
+        const u32 C = launch_collect(m, q, p->rule4_unified_collection != 0, x->flags, x->c,
+                                     x->ccap, x->scan, x->d_ctr, st);
+        CK(cudaGetLastError());
+        if (C == 0) break;
+        CK(cudaEventRecord(x->ev[1], st));   // split points are fused into collect
+        CK(cudaEventRecord(x->ev[2], st));
+        launch_locate(m, x->c, C, x->d_ctr, st);
+        CK(cudaEventRecord(x->ev[3], st));
+        launch_claim(m, x->c, C, x->aux, x->d_ctr, st);
+        CK(cudaEventRecord(x->ev[4], st));
+        ensure_regions(x, C, ncav);
+        launch_cavity(m, x->c, C, ncav, true, x->aux, x->regions, x->region_len, nullptr,
+                      x->d_ctr, st);
+        CK(cudaEventRecord(x->ev[5], st));
+        // ---- insert ----
+        launch_plan_ops(m, x->c, C, p->split_depth_cap, x->ib, x->d_ctr, st);
+        scan_exclusive(x->ib.nv, x->ib.ov, C, x->ib.totals + 0, x->scan, st);
+        scan_exclusive(x->ib.nt, x->ib.ot, C, x->ib.totals + 1, x->scan, st);
+        scan_exclusive(x->ib.ns, x->ib.os, C, x->ib.totals + 2, x->scan, st);
+        CK(cudaMemcpyAsync(x->h_tot, x->ib.totals, 3 * sizeof(u32), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        const u32 nv = x->h_tot[0], nt = x->h_tot[1], ns = x->h_tot[2];
+        const u32 V0 = m.nV;
+        ensure_mesh(x, m.nV + nv, m.nT + nt, m.nS + ns);
+        ensure_fresh(x, nv);
+        const u32 batch = ++x->epoch;
+        u32 flip_rounds = 0, rm_rounds = 0;
+        if (nv) {
+            DevMesh& mm = x->work.m;
+            ++x->round;
+            zero_rc(x);
+            launch_apply_splits(mm, x->c, C, batch, x->round, x->ib, x->aux, x->fresh, x->wl,
+                                x->d_ctr, st);
+            mm.nV += nv;
+            mm.nT += nt;
+            mm.nS += ns;
+            launch_fixup(mm, x->round, x->aux, x->wl, 4 * nv, true, 0, x->d_ctr, st);
+            RoundCtr rc = read_rc(x);
+            lawson_from(x, 0, rc.wl_next, &flip_rounds);
+            // Phase 3: redundant-point removal to fixpoint (refine.hpp:551-608).
+            for (;;) {
+                zero_rc(x);
+                launch_detect(mm, q, p->split_depth_cap, V0, nv, x->fresh, x->wl, x->d_ctr, st);
+                rc = read_rc(x);
+                u32 nrm = std::min(rc.detect, x->wl.rm_cap);
+                if (nrm == 0) break;
+                u32 cur = 0;
+                u32 guard = 0;
+                while (nrm > 0) {
+                    if (++guard > 100000) throw Fail{GDP2D_EMESH, "vertex removal did not converge"};
+                    ++x->round;
+                    zero_rc(x);
+                    launch_removal_round(mm, x->round, V0, x->aux, x->fresh, x->wl, cur, nrm, 0,
+                                         x->d_ctr, st);
+                    rc = read_rc(x);
+                    ++rm_rounds;
+                    check_dev_err(x);
+                    lawson_from(x, 0, rc.wl_next, &flip_rounds);
+                    nrm = rc.rm_next;
+                    cur ^= 1u;
+                }
+            }
+        }
+        CK(cudaEventRecord(x->ev[6], st));
+        CK(cudaGetLastError());
+        check_dev_err(x);
+        const Counters& h = *x->h_ctr;
+        const u32 inserted = h.ins_mid + h.ins_cc;
+        const u32 removed = h.rm_red + h.rm_dep;
+        const u32 retained = inserted - std::min(inserted, removed);
+        x->alive_v += inserted;
+        x->alive_v -= std::min<ull>(x->alive_v, h.rm_done);
+        x->alive_t += nt;
+        x->alive_t -= std::min<ull>(x->alive_t, 2ull * h.rm_done);
+        x->alive_s += h.ins_mid;
+        // metrics (record_batch, ruleskit.hpp:128-142)
+        bm.attempted = C;
+        bm.concurrency = retained;
+        bm.phase_seconds[GDP2D_PH_COLLECT] = ev_ms(x->ev[0], x->ev[1]) * 1e-3;
+        bm.phase_seconds[GDP2D_PH_SPLIT_POINTS] = ev_ms(x->ev[1], x->ev[2]) * 1e-3;
+        bm.phase_seconds[GDP2D_PH_LOCATE] = ev_ms(x->ev[2], x->ev[3]) * 1e-3;
+        bm.phase_seconds[GDP2D_PH_CLAIM] = ev_ms(x->ev[3], x->ev[4]) * 1e-3;
+        bm.phase_seconds[GDP2D_PH_CAVITY] = ev_ms(x->ev[4], x->ev[5]) * 1e-3;
+        bm.phase_seconds[GDP2D_PH_INSERT] = ev_ms(x->ev[5], x->ev[6]) * 1e-3;
+        for (double s : bm.phase_seconds) bm.latency += s;
+        bm.throughput = bm.latency > 0 ? retained / bm.latency : 0.0;
+        bm.waste_fraction = C ? double(C - retained) / C : 0.0;
+        bm.walk_steps = h.walk_steps;
+        bm.cavity_visits = h.cavity_visits;
+        bm.survivors_claim = h.surv_claim;
+        bm.survivors_cavity = h.surv_cavity;
+        bm.inserted_midpoints = h.ins_mid;
+        bm.inserted_circumcenters = h.ins_cc;
+        bm.removed_redundant = h.rm_red;
+        bm.removed_dependent = h.rm_dep;
+        bm.dropped = h.dropped;
+        bm.marked_encroached = h.marked;
+        bm.flips = h.flips;
+        bm.flip_rounds = flip_rounds;
+        bm.removal_rounds = rm_rounds;
+        if (r->batches && r->n_batches < r->batches_capacity) r->batches[r->n_batches] = bm;
+        r->n_batches++;
+        r->total_candidates += C;
+        r->total_walk_steps += h.walk_steps;
+        r->total_cavity_visits += h.cavity_visits;
+        r->total_inserted += inserted;
+        r->total_flips += h.flips;
+        r->total_removed += h.rm_done;
+        r->sum_tris_alive += bm.tris_alive;
+        r->sum_verts_alive += bm.verts_alive;
+        r->sum_subsegs_alive += bm.subsegs_alive;
+        if (retained == 0 && h.marked == 0) break;
+    }
+    CK(cudaEventRecord(x->ev[GDP2D_NPHASES], st));
+    CK(cudaEventSynchronize(x->ev[GDP2D_NPHASES]));
+    r->device_seconds = ev_ms(x->ev[GDP2D_NPHASES + 1], x->ev[GDP2D_NPHASES]) * 1e-3;
+    r->wall_seconds =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+}
+
+void fill_summary(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
+    const QualitySummary s = launch_quality(x->work.m, make_quality(p), x->qscratch, x->st);
+    r->output_points = s.alive_v;
+    r->steiner_points = s.steiner;
+    r->bad_triangles = s.bad;
+    r->bad_area_percent = s.total_area > 0 ? s.bad_area / s.total_area * 100.0 : 0.0;
+    r->min_angle_deg = s.min_angle;
+    r->max_edge = s.max_edge;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+
+namespace {
+int run_guarded(const std::function<void()>& fn) {
+    try {
+        fn();
+        return GDP2D_OK;
+    } catch (const Fail& f) {
+        g_err = f.what;
+        return f.code;
+    } catch (const CudaError& e) {
+        g_err = e.what;
+        return GDP2D_ECUDA;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return GDP2D_EINTERNAL;
+    }
+}
+
+void upload_cands(gdp2d_ctx* x, const gdp2d_candidate* c, u32 n) {
+    ensure_cands(x, n);
+    std::vector<double2> pt(n);
+    std::vector<u64> key(n);
+    std::vector<u32> id(n), tie(n), loc(n);
+    std::vector<uint8_t> kind(n), alive(n), lk(n, 0), fb(n);
+    std::vector<int8_t> le(n, -1);
+    for (u32 i = 0; i < n; ++i) {
+        pt[i] = make_double2(c[i].x, c[i].y);
+        double meas = c[i].measure;
+        u64 bits;
+        std::memcpy(&bits, &meas, 8);
+        key[i] = ((u64)(c[i].band ? 1 : 0) << 63) | (bits & 0x7FFFFFFFFFFFFFFFull);
+        id[i] = c[i].id;
+        tie[i] = c[i].tiebreak;
+        loc[i] = c[i].located;
+        kind[i] = c[i].kind == GDP2D_CAND_SUBSEG ? 0 : 1;
+        alive[i] = c[i].alive ? 1 : 0;
+        fb[i] = c[i].fallback;
+    }
+    cudaStream_t st = x->st;
+    CK(cudaMemcpyAsync(x->c.pt, pt.data(), 16ull * n, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(x->c.key, key.data(), 8ull * n, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(x->c.id, id.data(), 4ull * n, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(x->c.tie, tie.data(), 4ull * n, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(x->c.loc, loc.data(), 4ull * n, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(x->c.kind, kind.data(), n, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(x->c.alive, alive.data(), n, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(x->c.lkind, lk.data(), n, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(x->c.ledge, le.data(), n, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(x->c.fb, fb.data(), n, cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+}
+
+void download_cands(gdp2d_ctx* x, gdp2d_candidate* c, u32 n) {
+    std::vector<double2> pt(n);
+    std::vector<u64> key(n);
+    std::vector<u32> id(n), tie(n), loc(n);
+    std::vector<uint8_t> kind(n), alive(n), fb(n);
+    cudaStream_t st = x->st;
+    CK(cudaMemcpyAsync(pt.data(), x->c.pt, 16ull * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(key.data(), x->c.key, 8ull * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(id.data(), x->c.id, 4ull * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(tie.data(), x->c.tie, 4ull * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(loc.data(), x->c.loc, 4ull * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(kind.data(), x->c.kind, n, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(alive.data(), x->c.alive, n, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(fb.data(), x->c.fb, n, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (u32 i = 0; i < n; ++i) {
+        c[i].x = pt[i].x;
+        c[i].y = pt[i].y;
+        const u64 bits = key[i] & 0x7FFFFFFFFFFFFFFFull;
+        std::memcpy(&c[i].measure, &bits, 8);
+        c[i].band = (uint8_t)(key[i] >> 63);
+        c[i].id = id[i];
+        c[i].tiebreak = tie[i];
+        c[i].located = loc[i];
+        c[i].kind = kind[i] == 0 ? GDP2D_CAND_SUBSEG : GDP2D_CAND_TRI;
+        c[i].alive = alive[i];
+        c[i].fallback = fb[i];
+    }
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int d) {
+        cudaGetDevice(&prev);
+        cudaSetDevice(d);
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* gdp2d_last_error(void) { return g_err.c_str(); }
+const char* gdp2d_version(void) { return "gdp2d-b200 0.1 (sm_100a)"; }
+
+size_t gdp2d_struct_size(int which) {
+    switch (which) {
+        case 0: return sizeof(gdp2d_mesh_view);
+        case 1: return sizeof(gdp2d_mesh_buf);
+        case 2: return sizeof(gdp2d_params);
+        case 3: return sizeof(gdp2d_batch_metrics);
+        case 4: return sizeof(gdp2d_report);
+        case 5: return sizeof(gdp2d_candidate);
+        default: return 0;
+    }
+}
+
+void gdp2d_params_init(gdp2d_params* p, double theta_deg, double ell, uint32_t mode) {
+    std::memset(p, 0, sizeof *p);
+    p->theta_deg = theta_deg;
+    // refine.hpp:195-196, evaluated on the host exactly as the reference does
+    const double c = std::cos(theta_deg * 3.14159265358979323846 / 180.0);
+    p->cos2_theta = c * c;
+    p->ell = ell;
+    p->mode = mode;
+    p->cavity_n = 32;
+    p->rule1_compaction_threshold = 1024;
+    p->rule2_filtering_enabled = 1;
+    p->rule4_unified_collection = 1;
+    p->little_batch_sizing = 0;
+    p->iteration_cap = 10000;
+    p->split_depth_cap = 64;
+    p->batch_size_cap = 0;
+}
+
+int gdp2d_ctx_create(gdp2d_ctx** out, int device) {
+    if (!out) return GDP2D_EINVAL;
+    *out = nullptr;
+    gdp2d_ctx* x = new gdp2d_ctx();
+    const int rc = run_guarded([&] { ctx_init(x, device); });
+    if (rc != GDP2D_OK) {
+        ctx_release(x);
+        delete x;
+        return rc;
+    }
+    *out = x;
+    return GDP2D_OK;
+}
+
+void gdp2d_ctx_destroy(gdp2d_ctx* x) {
+    if (!x) return;
+    ctx_release(x);
+    delete x;
+}
+
+int gdp2d_ctx_upload(gdp2d_ctx* x, const gdp2d_mesh_view* in) {
+    if (!x) return GDP2D_EINVAL;
+    DeviceGuard g(x->device);
+    return run_guarded([&] {
+        upload(x, in);
+        reset_work(x);
+        CK(cudaStreamSynchronize(x->st));
+    });
+}
+
+int gdp2d_ctx_reset(gdp2d_ctx* x) {
+    if (!x) return GDP2D_EINVAL;
+    DeviceGuard g(x->device);
+    return run_guarded([&] { reset_work(x); });
+}
+
+int gdp2d_ctx_refine(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
+    if (!x || !p || !r) return GDP2D_EINVAL;
+    DeviceGuard g(x->device);
+    return run_guarded([&] {
+        refine_loop(x, p, r);
+        fill_summary(x, p, r);
+    });
+}
+
+int gdp2d_ctx_download(gdp2d_ctx* x, gdp2d_mesh_buf* out) {
+    if (!x || !out) return GDP2D_EINVAL;
+    DeviceGuard g(x->device);
+    return run_guarded([&] { download(x, out); });
+}
+
+uint64_t gdp2d_ctx_device_bytes(gdp2d_ctx* x) {
+    if (!x) return 0;
+    const MeshStore& w = x->work;
+    const MeshStore& p = x->pristine;
+    auto mesh_bytes = [](const MeshStore& s) {
+        return (u64)s.vcap * (16 + 1 + 4 + 1 + 4) + (u64)s.tcap * 48 + (u64)s.scap * (8 + 4 + 4 + 1 + 4 + 4);
+    };
+    return mesh_bytes(w) + mesh_bytes(p) + (u64)x->aux_cap * (8 + 8 + 4 + 4 + 12) + x->flags_cap +
+           (u64)x->ccap * 41 + x->reg_cap * 4 + (u64)x->wl.cap * 21 +
+           (u64)x->wl.rm_cap * (4 * MAX_STAR + 30);
+}
+
+int gdp2d_refine(const gdp2d_mesh_view* in, gdp2d_mesh_buf* out, const gdp2d_params* p,
+                 gdp2d_report* r, int device) {
+    if (!in || !out || !p || !r) return GDP2D_EINVAL;
+    const auto t0 = std::chrono::steady_clock::now();
+    gdp2d_ctx* x = nullptr;
+    int rc = gdp2d_ctx_create(&x, device);
+    if (rc) return rc;
+    rc = run_guarded([&] {
+        DeviceGuard g(x->device);
+        upload(x, in);
+        reset_work(x);
+        refine_loop(x, p, r);
+        download(x, out);
+        const double wall =
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        fill_summary(x, p, r);
+        r->wall_seconds = wall;
+    });
+    gdp2d_ctx_destroy(x);
+    return rc;
+}
+
+void gdp2d_free(gdp2d_mesh_buf* b) {
+    if (!b) return;
+    void* ptrs[] = {b->xy,      b->vert_kind, b->vert_birth, b->vert_alive, b->vert_tri,
+                    b->tri_v,   b->tri_n,     b->tri_seg,    b->tri_alive,  b->seg_v,
+                    b->seg_parent, b->seg_encroached, b->seg_alive, b->seg_tri};
+    for (void* q : ptrs) std::free(q);
+    std::memset(b, 0, sizeof *b);
+}
+
+int gdp2d_collect(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_candidate* out, uint32_t cap,
+                  uint32_t* n) {
+    if (!x || !p || !n) return GDP2D_EINVAL;
+    DeviceGuard g(x->device);
+    int status = GDP2D_OK;
+    const int rc = run_guarded([&] {
+        DevMesh& m = x->work.m;
+        ensure_cands(x, m.nS + m.nT);
+        CK(cudaMemsetAsync(x->d_ctr, 0, sizeof(Counters), x->st));
+        const u32 C = launch_collect(m, make_quality(p), p->rule4_unified_collection != 0,
+                                     x->flags, x->c, x->ccap, x->scan, x->d_ctr, x->st);
+        *n = C;
+        if (C > cap) {
+            status = GDP2D_ECAPACITY;
+            g_err = "candidate buffer too small";
+        }
+        if (out && C) {
+            std::vector<gdp2d_candidate> tmp(C);
+            download_cands(x, tmp.data(), C);
+            std::memcpy(out, tmp.data(), sizeof(gdp2d_candidate) * std::min(C, cap));
+        }
+    });
+    return rc ? rc : status;
+}
+
+int gdp2d_split_points(gdp2d_ctx* x, gdp2d_candidate* c, uint32_t n) {
+    (void)x; (void)c; (void)n;
+    g_err = "split points are fused into gdp2d_collect";
+    return GDP2D_EINVAL;
+}
+
+int gdp2d_locate(gdp2d_ctx* x, gdp2d_candidate* c, uint32_t n) {
+    if (!x || (!c && n)) return GDP2D_EINVAL;
+    DeviceGuard g(x->device);
+    return run_guarded([&] {
+        if (!n) return;
+        upload_cands(x, c, n);
+        CK(cudaMemsetAsync(x->d_ctr, 0, sizeof(Counters), x->st));
+        launch_locate(x->work.m, x->c, n, x->d_ctr, x->st);
+        CK(cudaGetLastError());
+        download_cands(x, c, n);
+    });
+}
+
+int gdp2d_claim(gdp2d_ctx* x, gdp2d_candidate* c, uint32_t n) {
+    if (!x || (!c && n)) return GDP2D_EINVAL;
+    DeviceGuard g(x->device);
+    return run_guarded([&] {
+        if (!n) return;
+        upload_cands(x, c, n);
+        CK(cudaMemsetAsync(x->d_ctr, 0, sizeof(Counters), x->st));
+        launch_claim(x->work.m, x->c, n, x->aux, x->d_ctr, x->st);
+        CK(cudaGetLastError());
+        download_cands(x, c, n);
+    });
+}
+
+int gdp2d_cavity(gdp2d_ctx* x, gdp2d_candidate* c, uint32_t n, uint32_t n_cav,
+                 uint32_t* regions, uint32_t* region_len) {
+    if (!x || (!c && n)) return GDP2D_EINVAL;
+    if (n_cav > (u32)MAX_CAVITY_N) {
+        g_err = "cavity_n exceeds 64";
+        return GDP2D_EINVAL;
+    }
+    DeviceGuard g(x->device);
+    return run_guarded([&] {
+        if (!n) return;
+        upload_cands(x, c, n);
+        ensure_regions(x, n, n_cav);
+        CK(cudaMemsetAsync(x->d_ctr, 0, sizeof(Counters), x->st));
+        launch_cavity(x->work.m, x->c, n, n_cav, false, x->aux, x->regions, x->region_len,
+                      x->bfs_len, x->d_ctr, x->st);
+        CK(cudaGetLastError());
+        download_cands(x, c, n);
+        if (regions && region_len) {
+            const u32 rs = n_cav + 1 + MAX_CLAIM_EXTRA;
+            std::vector<u32> reg((size_t)n * rs), len(n);
+            CK(cudaMemcpyAsync(reg.data(), x->regions, 4ull * n * rs, cudaMemcpyDeviceToHost,
+                               x->st));
+            CK(cudaMemcpyAsync(len.data(), x->bfs_len, 4ull * n, cudaMemcpyDeviceToHost, x->st));
+            CK(cudaStreamSynchronize(x->st));
+            for (u32 i = 0; i < n; ++i) {
+                region_len[i] = len[i];
+                for (u32 k = 0; k < len[i]; ++k)
+                    regions[(size_t)i * (n_cav + 1) + k] = reg[(size_t)i * rs + k];
+            }
+        }
+    });
+}
+
+int gdp2d_flip_fixpoint(gdp2d_ctx* x, const uint32_t* seed_tri, const uint8_t* seed_edge,
+                        uint32_t n, uint64_t* flips) {
+    if (!x || (n && (!seed_tri || !seed_edge))) return GDP2D_EINVAL;
+    DeviceGuard g(x->device);
+    return run_guarded([&] {
+        ensure_aux(x);
+        if (n > x->wl.cap) throw Fail{GDP2D_ECAPACITY, "too many seeds"};
+        std::vector<u32> codes(n);
+        for (u32 i = 0; i < n; ++i) codes[i] = enc(seed_tri[i], seed_edge[i]);
+        CK(cudaMemsetAsync(x->d_ctr, 0, sizeof(Counters), x->st));
+        if (n)
+            CK(cudaMemcpyAsync(x->wl.w[0], codes.data(), 4ull * n, cudaMemcpyHostToDevice,
+                               x->st));
+        u32 rounds = 0;
+        lawson_from(x, 0, n, &rounds);
+        check_dev_err(x);
+        if (flips) *flips = x->h_ctr->flips;
+    });
+}
+
+int gdp2d_predicates_batch(int device, int kind, const double* pts, uint32_t n,
+                           const gdp2d_params* p, int8_t* out) {
+    if ((n && (!pts || !out)) || kind < 0 || kind > 4) return GDP2D_EINVAL;
+    return run_guarded([&] {
+        int cnt = 0;
+        if (cudaGetDeviceCount(&cnt) != cudaSuccess || cnt == 0)
+            throw Fail{GDP2D_ENODEVICE, "no CUDA device visible"};
+        DeviceGuard g(device);
+        if (!n) return;
+        const int arity = kind == GDP2D_PRED_INCIRCLE ? 4 : 3;
+        double* dp = nullptr;
+        int8_t* dout = nullptr;
+        dalloc(dp, (size_t)n * arity * 2);
+        dalloc(dout, n);
+        CK(cudaMemcpy(dp, pts, 16ull * n * arity, cudaMemcpyHostToDevice));
+        gdp2d_params def;
+        if (!p) {
+            gdp2d_params_init(&def, 20.0, INFINITY, 0);
+            p = &def;
+        }
+        launch_predicates(kind, dp, n, make_quality(p), dout, 0);
+        CK(cudaGetLastError());
+        CK(cudaMemcpy(out, dout, n, cudaMemcpyDeviceToHost));
+        dfree(dp);
+        dfree(dout);
+    });
+}
+
+int gdp2d_circumcenter_batch(int device, const double* pts, uint32_t n, double* out,
+                             uint8_t* ok) {
+    if (n && (!pts || !out || !ok)) return GDP2D_EINVAL;
+    return run_guarded([&] {
+        int cnt = 0;
+        if (cudaGetDeviceCount(&cnt) != cudaSuccess || cnt == 0)
+            throw Fail{GDP2D_ENODEVICE, "no CUDA device visible"};
+        DeviceGuard g(device);
+        if (!n) return;
+        double *dp = nullptr, *dout = nullptr;
+        uint8_t* dok = nullptr;
+        dalloc(dp, 6ull * n);
+        dalloc(dout, 2ull * n);
+        dalloc(dok, n);
+        CK(cudaMemcpy(dp, pts, 48ull * n, cudaMemcpyHostToDevice));
+        launch_circumcenters(dp, n, dout, dok, 0);
+        CK(cudaGetLastError());
+        CK(cudaMemcpy(out, dout, 16ull * n, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(ok, dok, n, cudaMemcpyDeviceToHost));
+        dfree(dp);
+        dfree(dout);
+        dfree(dok);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,139 @@
+// engine.h -- internal host-side declarations shared by the engine's
+// translation units (kernel launchers + context).  Not part of the C ABI.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "gdp2d_common.cuh"
+#include "gdp2d_geom.cuh"
+
+namespace gdp2d {
+
+constexpr int SCAN_BLOCK = 256;
+constexpr int SCAN_ITEMS = 8;
+constexpr int SCAN_TILE = SCAN_BLOCK * SCAN_ITEMS;
+
+struct ScanScratch {
+    u32* partial = nullptr;   // per-tile sums
+    u32 cap = 0;              // tiles
+};
+
+// Exclusive scan of n u32 values; writes total to *d_total (device) if given.
+void scan_exclusive(const u32* in, u32* out, u32 n, u32* d_total, ScanScratch& s,
+                    cudaStream_t st);
+
+// In-place exclusive scan of per-tile sums (single block).
+void scan_partials(u32* partial, u32 ntiles, u32* d_total, cudaStream_t st);
+
+// Per-triangle scratch (claims, stamps, edge maps).
+struct TriAux {
+    u64* ckey = nullptr;     // claim key (band|measure)
+    u64* ctie = nullptr;     // claim tie  (tiebreak << 32 | list index)
+    u32* owner = nullptr;    // flip / removal claim
+    u32* stamp = nullptr;    // round in which the triangle was rewritten
+    u32* emap = nullptr;     // 3 per triangle: old edge slot -> new (tri<<2|edge)
+    uint8_t* flag = nullptr; // collect flags (S + T)
+};
+
+struct CollectBufs {
+    uint8_t* flags = nullptr;
+    u32 flags_cap = 0;
+};
+
+// ---- launchers -----------------------------------------------------------------
+
+// collect + fused compute_splitting_points (refine.hpp:226-296).  Returns the
+// candidate count (synchronises).  If rule4 == false and subsegment
+// candidates exist, triangles are skipped (refine.hpp:239).
+u32 launch_collect(const DevMesh& m, const Quality& q, bool rule4, uint8_t* flags, DevCands c,
+                   u32 ccap, ScanScratch& s, Counters* d_ctr, cudaStream_t st);
+void launch_split_points(const DevMesh& m, DevCands c, u32 n, Counters* d_ctr, cudaStream_t st);
+void launch_locate(const DevMesh& m, DevCands c, u32 n, Counters* d_ctr, cudaStream_t st);
+void launch_claim(const DevMesh& m, DevCands c, u32 n, TriAux a, Counters* d_ctr,
+                  cudaStream_t st);
+// Cavity filter; extras = refine-mode extra claims (far side of a split edge).
+void launch_cavity(const DevMesh& m, DevCands c, u32 n, u32 ncav, bool extras, TriAux a,
+                   u32* regions, u32* region_len, u32* bfs_len, Counters* d_ctr,
+                   cudaStream_t st);
+
+// ---- insertion ---------------------------------------------------------------------
+
+struct InsertBufs {
+    u32* nv = nullptr;  // per-candidate needs / offsets
+    u32* nt = nullptr;
+    u32* ns = nullptr;
+    u32* ov = nullptr;
+    u32* ot = nullptr;
+    u32* os = nullptr;
+    u32* totals = nullptr;   // device [3]
+    u32 cap = 0;
+};
+
+struct FreshInfo {
+    u64* key = nullptr;
+    u64* tie = nullptr;
+    uint8_t* cc = nullptr;
+    uint8_t* removed = nullptr;
+    uint8_t* mark = nullptr;
+    u32 cap = 0;
+};
+
+struct WorkLists {
+    u32* w[2] = {nullptr, nullptr};   // Lawson edge codes
+    u32* fc = nullptr;                // flip candidates: key
+    u32* fu = nullptr;                // flip candidates: neighbour code
+    u32* touched = nullptr;
+    uint8_t* fwin = nullptr;          // flip candidate won its claims
+    u32* rm[2] = {nullptr, nullptr};  // pending removals
+    u32* star = nullptr;              // removal stars (MAX_STAR each)
+    u32* star_len = nullptr;
+    u32 cap = 0;                      // capacity of w / fc / touched
+    u32 rm_cap = 0;
+    RoundCtr* rc = nullptr;           // device round counters
+};
+
+void launch_plan_ops(const DevMesh& m, DevCands c, u32 n, u64 depth_cap, InsertBufs b,
+                     Counters* d_ctr, cudaStream_t st);
+void launch_apply_splits(const DevMesh& m, DevCands c, u32 n, u32 batch, u32 round,
+                         InsertBufs b, TriAux a, FreshInfo f, WorkLists w, Counters* d_ctr,
+                         cudaStream_t st);
+// Phase B of every local rewrite: resolve pending outer references through
+// the edge maps, write back-pointers, refresh vert_tri / seg_tri.  Touched
+// triangles come from w.touched (count in w.rc->touched, bound n_bound).
+// seed_all_edges pushes every edge of every touched triangle onto w.w[widx].
+void launch_fixup(const DevMesh& m, u32 round, TriAux a, WorkLists w, u32 n_bound,
+                  bool seed_all_edges, u32 widx, Counters* d_ctr, cudaStream_t st);
+// One Lawson round over w.w[cur] (n items); next list in w.w[cur^1].  The
+// caller zeroes w.rc before the round.
+void launch_flip_round(const DevMesh& m, u32 round, TriAux a, WorkLists w, u32 cur, u32 n,
+                       Counters* d_ctr, cudaStream_t st);
+// Redundancy detection (refine.hpp:551-608): fills w.rm[0], count in w.rc->detect.
+void launch_detect(const DevMesh& m, const Quality& q, u64 depth_cap, u32 V0, u32 F,
+                   FreshInfo f, WorkLists w, Counters* d_ctr, cudaStream_t st);
+// One parallel vertex-removal round over w.rm[cur] (n); deferred ones go to
+// w.rm[cur^1]; Lawson seeds to w.w[widx].
+void launch_removal_round(const DevMesh& m, u32 round, u32 V0, TriAux a, FreshInfo f,
+                          WorkLists w, u32 cur, u32 n, u32 widx, Counters* d_ctr,
+                          cudaStream_t st);
+
+// Quality summary (refine.hpp:614-645).
+struct QualitySummary {
+    double total_area, bad_area, min_angle, max_edge;
+    ull bad, alive_v, steiner;
+};
+QualitySummary launch_quality(const DevMesh& m, const Quality& q, void* scratch,
+                              cudaStream_t st);
+
+// Upload helpers.
+void launch_encode_neighbors(DevMesh m, const u32* plain_n, cudaStream_t st);
+void launch_decode_neighbors(const DevMesh& m, u32* plain_n, cudaStream_t st);
+
+// Predicate batches.
+void launch_predicates(int kind, const double* pts, u32 n, const Quality& q, int8_t* out,
+                       cudaStream_t st);
+void launch_circumcenters(const double* pts, u32 n, double* out, uint8_t* ok,
+                          cudaStream_t st);
+
+}  // namespace gdp2d

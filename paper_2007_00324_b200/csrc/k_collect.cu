@@ -1,0 +1,153 @@
+// k_collect.cu -- Line 3 of Algorithm 1: the bad-triangle / encroached-
+// subsegment scan (collect, refine.hpp:226-263) fused with splitting-point
+// generation (compute_splitting_points, refine.hpp:267-296).
+//
+// HBM-bound full scan: per triangle one coalesced uint4 (tv) + three double2
+// vertex gathers; per subsegment its record + <= 2 apex gathers.  The list
+// order is the reference's (subsegments by id, then triangles by id) thanks to
+// a stable three-kernel compaction (flag+tile count, tile-sum scan, tile-local
+// shuffle scan + scatter).  Tiebreak = list index (refine.hpp:236,248).
+#include "engine.h"
+#include "scan.cuh"
+
+namespace gdp2d {
+
+struct CollectRange {
+    u32 nS, nT;          // element counts
+    u32 tilesS, tilesT;  // tile counts
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(SCAN_BLOCK) k_collect_flags(DevMesh m, Quality q, CollectRange r,
+                                                           uint8_t* __restrict__ flags,
+                                                           u32* __restrict__ partial) {
+    __shared__ u32 sh[SCAN_BLOCK / 32 + 1];
+    const bool is_sub = blockIdx.x < r.tilesS;
+    const u32 tile = is_sub ? blockIdx.x : blockIdx.x - r.tilesS;
+    const u32 n = is_sub ? r.nS : r.nT;
+    const u32 base = tile * (u32)SCAN_TILE;
+    u32 cnt = 0;
+#pragma unroll 4
+    for (int k = 0; k < SCAN_ITEMS; ++k) {
+        const u32 i = base + (u32)k * SCAN_BLOCK + threadIdx.x;
+        uint8_t f = 0;
+        if (i < n) {
+            if (is_sub) {
+                if (m.salive[i] && (m.senc[i] || is_encroached<MODE>(m, i))) f = 1;
+            } else {
+                const uint4 tv = m.tv[i];
+                if (tv.w) {
+                    const double2 a = m.xy[tv.x], b = m.xy[tv.y], c = m.xy[tv.z];
+                    if (is_bad_pts(a, b, c, q) && resolvable_pts(a, b, c)) f = 1;
+                }
+            }
+        }
+        flags[(size_t)blockIdx.x * SCAN_TILE + (u32)k * SCAN_BLOCK + threadIdx.x] = f;
+        cnt += f;
+    }
+    const u32 t = block_sum<SCAN_BLOCK>(cnt, sh);
+    if (threadIdx.x == 0) partial[blockIdx.x] = t;
+}
+
+// compute_splitting_points for one candidate (refine.hpp:269-294).
+__device__ __forceinline__ double2 split_point(const DevMesh& m, int kind, u32 id, uint8_t& fb) {
+    fb = 0;
+    if (kind == 0) return subseg_mid(m, id);
+    const uint4 tv = m.tv[id];
+    const double2 v3[3] = {m.xy[tv.x], m.xy[tv.y], m.xy[tv.z]};
+    bool ok;
+    const double2 cc = circumcenter(v3[0], v3[1], v3[2], ok);
+    if (ok && isfinite(cc.x) && isfinite(cc.y)) return cc;
+    fb = 1;
+    int best = 0;
+    double best_len = -1.0;
+    for (int e = 0; e < 3; ++e) {
+        const double len = sqdist(v3[nxt(e)], v3[prv(e)]);
+        if (len > best_len) {
+            best_len = len;
+            best = e;
+        }
+    }
+    return midpoint2(v3[nxt(best)], v3[prv(best)]);
+}
+
+__global__ void __launch_bounds__(SCAN_BLOCK) k_collect_scatter(DevMesh m, CollectRange r,
+                                                             const uint8_t* __restrict__ flags,
+                                                             const u32* __restrict__ partial,
+                                                             DevCands c, u32 ccap,
+                                                             Counters* ctr) {
+    __shared__ u32 sh[SCAN_BLOCK / 32 + 1];
+    const bool is_sub = blockIdx.x < r.tilesS;
+    const u32 tile = is_sub ? blockIdx.x : blockIdx.x - r.tilesS;
+    const u32 base = tile * (u32)SCAN_TILE;
+    u32 carry = partial[blockIdx.x];
+    u32 nfb = 0;
+    for (int k = 0; k < SCAN_ITEMS; ++k) {
+        const u32 i = base + (u32)k * SCAN_BLOCK + threadIdx.x;
+        const uint8_t f = flags[(size_t)blockIdx.x * SCAN_TILE + (u32)k * SCAN_BLOCK + threadIdx.x];
+        u32 tot;
+        const u32 ex = block_exclusive<SCAN_BLOCK>(f, sh, &tot);
+        if (f) {
+            const u32 o = carry + ex;
+            if (o < ccap) {
+                uint8_t fb;
+                const int kind = is_sub ? 0 : 1;
+                c.pt[o] = split_point(m, kind, i, fb);
+                nfb += fb;
+                double measure;
+                if (is_sub) {
+                    measure = subseg_len(m, i);
+                } else {
+                    const uint4 tv = m.tv[i];
+                    measure = area_pts(m.xy[tv.x], m.xy[tv.y], m.xy[tv.z]);
+                }
+                c.key[o] = make_key(is_sub ? 1 : 0, measure);
+                c.id[o] = i;
+                c.tie[o] = o;
+                c.loc[o] = PENDING;
+                c.kind[o] = (uint8_t)kind;
+                c.alive[o] = 1;
+                c.lkind[o] = 0;
+                c.ledge[o] = -1;
+                c.fb[o] = fb;
+            }
+        }
+        carry += tot;
+    }
+    warp_add_u32(&ctr->fallbacks, nfb);
+}
+
+u32 launch_collect(const DevMesh& m, const Quality& q, bool rule4, uint8_t* flags, DevCands c,
+                   u32 ccap, ScanScratch& s, Counters* d_ctr, cudaStream_t st) {
+    auto run = [&](bool sub, bool tri) -> u32 {
+        CollectRange r;
+        r.nS = sub ? m.nS : 0;
+        r.nT = tri ? m.nT : 0;
+        r.tilesS = (r.nS + SCAN_TILE - 1) / SCAN_TILE;
+        r.tilesT = (r.nT + SCAN_TILE - 1) / SCAN_TILE;
+        const u32 tiles = r.tilesS + r.tilesT;
+        if (tiles == 0) return 0;
+        if (tiles + 1 > s.cap) {
+            if (s.partial) cudaFree(s.partial);
+            s.cap = (tiles + 1) * 2;
+            cudaMalloc(&s.partial, sizeof(u32) * s.cap);
+        }
+        if (q.mode == 0)
+            k_collect_flags<0><<<tiles, SCAN_BLOCK, 0, st>>>(m, q, r, flags, s.partial);
+        else
+            k_collect_flags<1><<<tiles, SCAN_BLOCK, 0, st>>>(m, q, r, flags, s.partial);
+        scan_partials(s.partial, tiles, s.partial + tiles, st);
+        u32 total = 0;
+        cudaMemcpyAsync(&total, s.partial + tiles, sizeof(u32), cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        if (total > 0)
+            k_collect_scatter<<<tiles, SCAN_BLOCK, 0, st>>>(m, r, flags, s.partial, c, ccap, d_ctr);
+        return total;
+    };
+    if (rule4) return run(true, true);
+    const u32 ns = run(true, false);
+    if (ns > 0) return ns;
+    return run(false, true);
+}
+
+}  // namespace gdp2d

@@ -1,0 +1,679 @@
+// k_insert.cu -- Line 8 of Algorithm 1: parallel insertion with Flip-Flop
+// (insert_batch, refine.hpp:464-610).
+//
+// Every mesh mutation is a LOCAL REWRITE of a set of triangles its thread
+// owns exclusively (cavity claims for splits, pair claims for flips, star
+// claims for removals).  A rewrite runs in two kernels:
+//   phase A (owner thread): rewrite the owned triangles + allocate new ones;
+//     references leaving the owned set keep the OLD outer (tri<<2|edge) and
+//     are flagged pending in tn.w; every old boundary slot records where its
+//     edge went in emap[3*t+e]; owned triangles are stamped with the round.
+//   phase B (launch_fixup, one thread per touched triangle): a pending ref to
+//     a triangle stamped this round is translated through its emap; a ref to
+//     an untouched triangle stays and gets its back-pointer written (single
+//     writer per edge).  vert_tri / seg_tri are recomputed as atomicMin over
+//     touched triangles, so ids are deterministic run to run.
+// Mirrors: split_triangle_with mesh.hpp:323-346, split_edge_with :358-401,
+// split_subsegment :405-425, flip :210-258, remove_free_vertex + flop
+// :261-304,442-466, lawson_fixpoint cdt.hpp:111-123.
+#include "engine.h"
+#include "scan.cuh"
+
+namespace gdp2d {
+
+// ---- shared phase-A helpers ----------------------------------------------------
+
+__device__ __forceinline__ void write_tri(const DevMesh& m, u32 t, u32 a, u32 b, u32 c, u32 n0,
+                                          u32 n1, u32 n2, u32 pend, u32 s0, u32 s1, u32 s2) {
+    m.tv[t] = make_uint4(a, b, c, 1u);
+    m.tn[t] = make_uint4(n0, n1, n2, pend);
+    m.ts[t] = make_uint4(s0, s1, s2, 0u);
+    m.vtri[a] = NONE;
+    m.vtri[b] = NONE;
+    m.vtri[c] = NONE;
+    if (s0 != NONE) m.stri[s0] = NONE;
+    if (s1 != NONE) m.stri[s1] = NONE;
+    if (s2 != NONE) m.stri[s2] = NONE;
+}
+
+__device__ __forceinline__ void push_touched(const WorkLists& w, const u32* ts, int k) {
+    const u32 o = atomicAdd(&w.rc->touched, (u32)k);
+    for (int j = 0; j < k; ++j)
+        if (o + j < w.cap) w.touched[o + j] = ts[j];
+}
+
+__device__ __forceinline__ void push_work(const WorkLists& w, u32 widx, const u32* codes, int k,
+                                          Counters* ctr) {
+    const u32 o = atomicAdd(&w.rc->wl_next, (u32)k);
+    if (o + k > w.cap) {
+        raise_err(ctr, DERR_WORKLIST_OVERFLOW, o);
+        return;
+    }
+    for (int j = 0; j < k; ++j) w.w[widx][o + j] = codes[j];
+}
+
+// split_triangle_with (mesh.hpp:323-346): t := (a,b,w), t1 := (b,c,w), t2 := (c,a,w).
+__device__ void split_triangle_A(const DevMesh& m, const TriAux& x, const WorkLists& w, u32 t,
+                                 u32 wv, u32 t1, u32 t2, u32 round) {
+    const uint4 ov = m.tv[t], on = m.tn[t], os = m.ts[t];
+    x.stamp[t] = round;
+    write_tri(m, t, ov.x, ov.y, wv, enc(t1, 1), enc(t2, 0), on.z, 4u, NONE, NONE, os.z);
+    write_tri(m, t1, ov.y, ov.z, wv, enc(t2, 1), enc(t, 0), on.x, 4u, NONE, NONE, os.x);
+    write_tri(m, t2, ov.z, ov.x, wv, enc(t, 1), enc(t1, 0), on.y, 4u, NONE, NONE, os.y);
+    x.emap[3 * t + 0] = enc(t1, 2);
+    x.emap[3 * t + 1] = enc(t2, 2);
+    x.emap[3 * t + 2] = enc(t, 2);
+    m.vtri[wv] = NONE;
+    const u32 tl[3] = {t, t1, t2};
+    push_touched(w, tl, 3);
+}
+
+// split_edge_with (mesh.hpp:358-401) on edge e of t; new t2 (and u2 when the
+// edge has a far side).  s_bw / s_wc are the child subsegments or NONE.
+__device__ void split_edge_A(const DevMesh& m, const TriAux& x, const WorkLists& w, u32 t, int e,
+                             u32 wv, u32 t2, u32 u2, u32 s_bw, u32 s_wc, u32 round) {
+    const uint4 ov = m.tv[t], on = m.tn[t], os = m.ts[t];
+    const u32 a = comp(ov, e), b = comp(ov, nxt(e)), c = comp(ov, prv(e));
+    const u32 uc = comp(on, e);
+    x.stamp[t] = round;
+    if (uc == NONE) {
+        // t := (a,b,w) {-, t2, n_prev}, t2 := (a,w,c) {-, n_next, t}
+        write_tri(m, t, a, b, wv, NONE, enc(t2, 2), comp(on, prv(e)), 4u, s_bw, NONE,
+                  comp(os, prv(e)));
+        write_tri(m, t2, a, wv, c, NONE, comp(on, nxt(e)), enc(t, 1), 2u, s_wc,
+                  comp(os, nxt(e)), NONE);
+        x.emap[3 * t + nxt(e)] = enc(t2, 1);
+        x.emap[3 * t + prv(e)] = enc(t, 2);
+        x.emap[3 * t + e] = NONE;
+        m.vtri[wv] = NONE;
+        const u32 tl[2] = {t, t2};
+        push_touched(w, tl, 2);
+        return;
+    }
+    const u32 u = etri(uc);
+    const int f = eidx(uc);
+    const uint4 uv = m.tv[u], un = m.tn[u], us = m.ts[u];
+    const u32 d = comp(uv, f);
+    x.stamp[u] = round;
+    // t := (a,b,w) {u2, t2, n_ab}; t2 := (a,w,c) {u, n_ca, t}
+    write_tri(m, t, a, b, wv, enc(u2, 0), enc(t2, 2), comp(on, prv(e)), 4u, s_bw, NONE,
+              comp(os, prv(e)));
+    write_tri(m, t2, a, wv, c, enc(u, 0), comp(on, nxt(e)), enc(t, 1), 2u, s_wc,
+              comp(os, nxt(e)), NONE);
+    // u := (d,c,w) {t2, u2, n_dc}; u2 := (d,w,b) {t, n_bd, u}
+    write_tri(m, u, d, c, wv, enc(t2, 0), enc(u2, 2), comp(un, prv(f)), 4u, s_wc, NONE,
+              comp(us, prv(f)));
+    write_tri(m, u2, d, wv, b, enc(t, 0), comp(un, nxt(f)), enc(u, 1), 2u, s_bw,
+              comp(us, nxt(f)), NONE);
+    x.emap[3 * t + nxt(e)] = enc(t2, 1);
+    x.emap[3 * t + prv(e)] = enc(t, 2);
+    x.emap[3 * t + e] = NONE;
+    x.emap[3 * u + prv(f)] = enc(u, 2);
+    x.emap[3 * u + nxt(f)] = enc(u2, 1);
+    x.emap[3 * u + f] = NONE;
+    m.vtri[wv] = NONE;
+    const u32 tl[4] = {t, t2, u, u2};
+    push_touched(w, tl, 4);
+}
+
+// ---- planning + phase-1 splits ----------------------------------------------------
+
+// Needs of each surviving candidate (refine.hpp:493-539); subsegments that
+// hit the depth cap or fail subsegment_split_ok are abandoned (:501-506).
+__global__ void k_plan_ops(DevMesh m, DevCands c, u32 n, u64 depth_cap, InsertBufs b,
+                           Counters* ctr) {
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    u32 dropped = 0;
+    if (i < n) {
+        u32 nv = 0, nt = 0, ns = 0;
+        if (c.alive[i]) {
+            if (c.kind[i] == 0) {
+                const u32 s = c.id[i];
+                if (!m.salive[s]) {
+                    dropped = 1;
+                } else if ((u64)m.sdepth[s] >= depth_cap || !subseg_split_ok(m, s, c.pt[i])) {
+                    m.senc[s] = 0;
+                    dropped = 1;
+                } else {
+                    const u32 t = c.loc[i];
+                    const int e = seg_slot(m.ts[t], s);
+                    const bool far = comp(m.tn[t], e) != NONE;
+                    nv = 1;
+                    nt = far ? 2 : 1;
+                    ns = 2;
+                }
+            } else if (c.lkind[i] == 0) {
+                nv = 1;
+                nt = 2;
+            } else if (c.lkind[i] == 1) {
+                const bool far = comp(m.tn[c.loc[i]], c.ledge[i]) != NONE;
+                nv = 1;
+                nt = far ? 2 : 1;
+            }
+            if (!nv) c.alive[i] = 0;
+        }
+        b.nv[i] = nv;
+        b.nt[i] = nt;
+        b.ns[i] = ns;
+    }
+    warp_add_u32(&ctr->dropped, dropped);
+}
+
+__global__ void k_apply_splits(DevMesh m, DevCands c, u32 n, u32 batch, u32 round, InsertBufs b,
+                               TriAux x, FreshInfo f, WorkLists w, Counters* ctr) {
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    u32 mid = 0, cc = 0;
+    if (i < n && b.nv[i]) {
+        const u32 wv = m.nV + b.ov[i];
+        const u32 nt0 = m.nT + b.ot[i];
+        const double2 p = c.pt[i];
+        m.xy[wv] = p;
+        m.vkind[wv] = c.kind[i] == 0 ? 1 : 2;
+        m.vbirth[wv] = batch;
+        m.valive[wv] = 1;
+        const u32 fi = b.ov[i];
+        f.key[fi] = c.key[i];
+        f.tie[fi] = ((u64)c.tie[i] << 32) | i;
+        f.cc[fi] = c.kind[i] == 1;
+        f.removed[fi] = 0;
+        f.mark[fi] = 0;
+        const u32 t = c.loc[i];
+        if (c.kind[i] == 0) {
+            const u32 s = c.id[i];
+            const int e = seg_slot(m.ts[t], s);
+            const uint4 tv = m.tv[t];
+            const u32 bb = comp(tv, nxt(e)), ccv = comp(tv, prv(e));
+            const u32 s_bw = m.nS + b.os[i], s_wc = s_bw + 1;
+            const u32 par = m.sparent[s], dep = m.sdepth[s] + 1;
+            m.sv[s_bw] = make_uint2(bb, wv);
+            m.sv[s_wc] = make_uint2(wv, ccv);
+            m.sparent[s_bw] = par;
+            m.sparent[s_wc] = par;
+            m.senc[s_bw] = 0;
+            m.senc[s_wc] = 0;
+            m.salive[s_bw] = 1;
+            m.salive[s_wc] = 1;
+            m.sdepth[s_bw] = dep;
+            m.sdepth[s_wc] = dep;
+            m.stri[s_bw] = NONE;
+            m.stri[s_wc] = NONE;
+            m.salive[s] = 0;
+            m.senc[s] = 0;
+            split_edge_A(m, x, w, t, e, wv, nt0, nt0 + 1, s_bw, s_wc, round);
+            mid = 1;
+        } else if (c.lkind[i] == 0) {
+            split_triangle_A(m, x, w, t, wv, nt0, nt0 + 1, round);
+            cc = 1;
+        } else {
+            split_edge_A(m, x, w, t, c.ledge[i], wv, nt0, nt0 + 1, NONE, NONE, round);
+            cc = 1;
+        }
+    }
+    warp_add_u32(&ctr->ins_mid, mid);
+    warp_add_u32(&ctr->ins_cc, cc);
+}
+
+void launch_plan_ops(const DevMesh& m, DevCands c, u32 n, u64 depth_cap, InsertBufs b,
+                     Counters* d_ctr, cudaStream_t st) {
+    if (!n) return;
+    k_plan_ops<<<(n + 255) / 256, 256, 0, st>>>(m, c, n, depth_cap, b, d_ctr);
+}
+
+void launch_apply_splits(const DevMesh& m, DevCands c, u32 n, u32 batch, u32 round,
+                         InsertBufs b, TriAux a, FreshInfo f, WorkLists w, Counters* d_ctr,
+                         cudaStream_t st) {
+    if (!n) return;
+    k_apply_splits<<<(n + 255) / 256, 256, 0, st>>>(m, c, n, batch, round, b, a, f, w, d_ctr);
+}
+
+// ---- phase B ------------------------------------------------------------------------
+
+__global__ void k_fixup(DevMesh m, u32 round, TriAux x, WorkLists w, u32 n_bound, int seed,
+                        u32 widx, Counters* ctr) {
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    const u32 n = min(w.rc->touched, w.cap);
+    if (i >= n || i >= n_bound) return;
+    const u32 t = w.touched[i];
+    uint4 tn = m.tn[t];
+    const uint4 tv = m.tv[t];
+    if (!tv.w) return;
+    const u32 pend = tn.w;
+    u32* tn_words = reinterpret_cast<u32*>(m.tn);
+#pragma unroll
+    for (int e = 0; e < 3; ++e) {
+        if (!((pend >> e) & 1u)) continue;
+        const u32 r = comp(tn, e);
+        if (r == NONE) continue;
+        const u32 X = etri(r);
+        if (x.stamp[X] == round) {
+            set_comp(tn, e, x.emap[3 * X + eidx(r)]);
+        } else {
+            tn_words[4 * (size_t)X + eidx(r)] = enc(t, e);
+        }
+    }
+    tn.w = 0;
+    m.tn[t] = tn;
+    atomicMin(&m.vtri[tv.x], t);
+    atomicMin(&m.vtri[tv.y], t);
+    atomicMin(&m.vtri[tv.z], t);
+    const uint4 ts = m.ts[t];
+#pragma unroll
+    for (int e = 0; e < 3; ++e) {
+        const u32 s = comp(ts, e);
+        if (s == NONE) continue;
+        const u32 r = comp(tn, e);
+        const u32 other = r == NONE ? NONE : etri(r);
+        atomicMin(&m.stri[s], min(t, other));
+    }
+    if (seed) {
+        const u32 codes[3] = {enc(t, 0), enc(t, 1), enc(t, 2)};
+        push_work(w, widx, codes, 3, ctr);
+    }
+}
+
+void launch_fixup(const DevMesh& m, u32 round, TriAux a, WorkLists w, u32 n_bound,
+                  bool seed_all_edges, u32 widx, Counters* d_ctr, cudaStream_t st) {
+    if (!n_bound) return;
+    k_fixup<<<(n_bound + 255) / 256, 256, 0, st>>>(m, round, a, w, n_bound,
+                                                   seed_all_edges ? 1 : 0, widx, d_ctr);
+}
+
+// ---- Lawson flip rounds (lawson_fixpoint cdt.hpp:111-123) -----------------------------
+
+// Test every work item (is_non_delaunay_edge mesh.hpp:430-437) on its
+// canonical side (lower triangle id) and claim both triangles with the edge
+// code as key: the minimum key wins, so a round's flip set is deterministic.
+__global__ void k_flip_test(DevMesh m, const u32* __restrict__ wl, u32 n, TriAux x, WorkLists w,
+                            Counters* ctr) {
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const u32 code = wl[i];
+    u32 t = etri(code);
+    int e = eidx(code);
+    if (t >= m.nT) return;
+    const uint4 tv0 = m.tv[t];
+    if (!tv0.w) return;
+    const u32 c = comp(m.tn[t], e);
+    if (c == NONE) return;
+    if (comp(m.ts[t], e) != NONE) return;
+    u32 u = etri(c);
+    int f = eidx(c);
+    if (u < t) {
+        const u32 tt = t;
+        const int ee = e;
+        t = u;
+        e = f;
+        u = tt;
+        f = ee;
+    }
+    const uint4 tv = m.tv[t];
+    const u32 d = comp(m.tv[u], f);
+    if (incircle(m.xy[tv.x], m.xy[tv.y], m.xy[tv.z], m.xy[d]) <= 0) return;
+    const u32 key = enc(t, e);
+    atomicMin(&x.owner[t], key);
+    atomicMin(&x.owner[u], key);
+    const u32 o = atomicAdd(&w.rc->cand, 1u);
+    if (o < w.cap) {
+        w.fc[o] = key;
+        w.fu[o] = enc(u, f);
+    } else {
+        raise_err(ctr, DERR_WORKLIST_OVERFLOW, o);
+    }
+}
+
+// flip (mesh.hpp:210-258) as a phase-A rewrite: t := (a,b,d), u := (a,d,c).
+__global__ void k_flip_apply(DevMesh m, u32 n_bound, u32 round, u32 widx, TriAux x,
+                             WorkLists w, Counters* ctr) {
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    const u32 n = min(w.rc->cand, w.cap);
+    u32 flipped = 0;
+    if (i < n && i < n_bound) {
+        const u32 key = w.fc[i], uc = w.fu[i];
+        const u32 t = etri(key), u = etri(uc);
+        const int e = eidx(key), f = eidx(uc);
+        const bool won = x.owner[t] == key && x.owner[u] == key;
+        w.fwin[i] = won;
+        if (won) {
+            const uint4 tv = m.tv[t], tn = m.tn[t], ts = m.ts[t];
+            const uint4 uv = m.tv[u], un = m.tn[u], us = m.ts[u];
+            const u32 a = comp(tv, e), b = comp(tv, nxt(e)), c = comp(tv, prv(e));
+            const u32 d = comp(uv, f);
+            const double2 pa = m.xy[a], pb = m.xy[b], pc = m.xy[c], pd = m.xy[d];
+            if (orient2d(pa, pb, pd) <= 0 || orient2d(pa, pd, pc) <= 0) {
+                raise_err(ctr, DERR_NONCONVEX_FLIP, t);
+            } else if (atomicExch(&x.stamp[t], round) != round) {
+                x.stamp[u] = round;
+                write_tri(m, t, a, b, d, comp(un, nxt(f)), enc(u, 2), comp(tn, prv(e)), 5u,
+                          comp(us, nxt(f)), NONE, comp(ts, prv(e)));
+                write_tri(m, u, a, d, c, comp(un, prv(f)), comp(tn, nxt(e)), enc(t, 1), 3u,
+                          comp(us, prv(f)), comp(ts, nxt(e)), NONE);
+                x.emap[3 * t + nxt(e)] = enc(u, 1);
+                x.emap[3 * t + prv(e)] = enc(t, 2);
+                x.emap[3 * t + e] = NONE;
+                x.emap[3 * u + nxt(f)] = enc(t, 0);
+                x.emap[3 * u + prv(f)] = enc(u, 0);
+                x.emap[3 * u + f] = NONE;
+                const u32 tl[2] = {t, u};
+                push_touched(w, tl, 2);
+                const u32 codes[4] = {enc(t, 0), enc(t, 2), enc(u, 0), enc(u, 1)};
+                push_work(w, widx, codes, 4, ctr);
+                flipped = 1;
+            }
+        }
+    }
+    warp_add_ull(&ctr->flips, flipped);
+}
+
+// Release claims; a loser whose triangles were both left untouched retries.
+__global__ void k_flip_post(u32 n_bound, u32 round, u32 widx, TriAux x, WorkLists w,
+                            Counters* ctr) {
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    const u32 n = min(w.rc->cand, w.cap);
+    if (i >= n || i >= n_bound) return;
+    const u32 key = w.fc[i], uc = w.fu[i];
+    const u32 t = etri(key), u = etri(uc);
+    x.owner[t] = NONE;
+    x.owner[u] = NONE;
+    if (!w.fwin[i] && x.stamp[t] != round && x.stamp[u] != round) {
+        const u32 codes[1] = {key};
+        push_work(w, widx, codes, 1, ctr);
+    }
+}
+
+void launch_flip_round(const DevMesh& m, u32 round, TriAux a, WorkLists w, u32 cur, u32 n,
+                       Counters* d_ctr, cudaStream_t st) {
+    if (!n) return;
+    const u32 g = (n + 255) / 256;
+    k_flip_test<<<g, 256, 0, st>>>(m, w.w[cur], n, a, w, d_ctr);
+    k_flip_apply<<<g, 256, 0, st>>>(m, n, round, cur ^ 1u, a, w, d_ctr);
+    k_flip_post<<<g, 256, 0, st>>>(n, round, cur ^ 1u, a, w, d_ctr);
+    const u32 nt = 2 * n;
+    k_fixup<<<(nt + 255) / 256, 256, 0, st>>>(m, round, a, w, nt, 0, 0, d_ctr);
+}
+
+// ---- redundancy detection (refine.hpp:551-608) ----------------------------------------
+
+// Star of v in rotation order (incident_triangles, mesh.hpp:145-171, interior
+// case).  Returns the size, or 0 if the fan is open / too large.
+__device__ __forceinline__ int walk_star(const DevMesh& m, u32 v, u32* st, int* si, int cap) {
+    const u32 t0 = m.vtri[v];
+    if (t0 == NONE) return 0;
+    u32 cur = t0;
+    int k = 0;
+    do {
+        const uint4 tv = m.tv[cur];
+        const int i = tv.x == v ? 0 : (tv.y == v ? 1 : (tv.z == v ? 2 : -1));
+        if (i < 0 || k >= cap) return 0;
+        st[k] = cur;
+        si[k] = i;
+        ++k;
+        const u32 c = comp(m.tn[cur], nxt(i));
+        if (c == NONE) return 0;
+        cur = etri(c);
+    } while (cur != t0);
+    return k;
+}
+
+__device__ __forceinline__ bool prio_gt(const FreshInfo& f, u32 a, u32 b) {
+    if (f.key[a] != f.key[b]) return f.key[a] > f.key[b];
+    return f.tie[a] < f.tie[b];
+}
+
+// (a) a same-batch circumcenter that encroaches a splittable subsegment of
+// its star is redundant; the lowest-id such subsegment is marked.
+template <int MODE>
+__global__ void k_detect_a(DevMesh m, u64 depth_cap, u32 V0, u32 F, FreshInfo f, Counters* ctr) {
+    const u32 j = blockIdx.x * blockDim.x + threadIdx.x;
+    u32 marked = 0;
+    if (j < F) {
+        uint8_t mark = 0;
+        const u32 v = V0 + j;
+        if (f.cc[j] && !f.removed[j]) {
+            u32 st[MAX_STAR];
+            int si[MAX_STAR];
+            const int k = walk_star(m, v, st, si, MAX_STAR);
+            if (k == 0) raise_err(ctr, DERR_OPEN_STAR, v);
+            const double2 pv = m.xy[v];
+            u32 best = NONE;
+            for (int q = 0; q < k; ++q) {
+                const u32 s = comp(m.ts[st[q]], si[q]);
+                if (s == NONE || s >= best) continue;
+                const uint2 sv = m.sv[s];
+                if (!encroaches<MODE>(m.xy[sv.x], m.xy[sv.y], pv)) continue;
+                if ((u64)m.sdepth[s] >= depth_cap) continue;
+                if (!subseg_split_ok(m, s, subseg_mid(m, s))) continue;
+                best = s;
+            }
+            if (best != NONE) {
+                mark = 1;
+                if (atomicExch(&m.senc[best], 1u) == 0u) marked = 1;
+            }
+        }
+        f.mark[j] = mark;
+    }
+    warp_add_u32(&ctr->marked, marked);
+}
+
+// (b) Delaunay-dependent pairs: a same-batch circumcenter adjacent to a
+// higher-priority one (not itself redundant) is removed.
+__global__ void k_detect_b(DevMesh m, u32 V0, u32 F, FreshInfo f, Counters* ctr) {
+    const u32 j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= F) return;
+    if (!f.cc[j] || f.removed[j] || f.mark[j] == 1) return;
+    const u32 v = V0 + j;
+    u32 st[MAX_STAR];
+    int si[MAX_STAR];
+    const int k = walk_star(m, v, st, si, MAX_STAR);
+    for (int q = 0; q < k; ++q) {
+        const u32 x = comp(m.tv[st[q]], nxt(si[q]));
+        if (x < V0 || x >= V0 + F) continue;
+        const u32 jx = x - V0;
+        if (!f.cc[jx] || f.removed[jx] || f.mark[jx] == 1) continue;
+        if (prio_gt(f, jx, j)) {
+            f.mark[j] = 2;
+            break;
+        }
+    }
+}
+
+__global__ void k_detect_collect(u32 V0, u32 F, FreshInfo f, WorkLists w, Counters* ctr) {
+    const u32 j = blockIdx.x * blockDim.x + threadIdx.x;
+    u32 red = 0, dep = 0;
+    if (j < F && !f.removed[j] && f.mark[j]) {
+        const u32 o = atomicAdd(&w.rc->detect, 1u);
+        if (o < w.rm_cap) w.rm[0][o] = V0 + j;
+        red = f.mark[j] == 1;
+        dep = f.mark[j] == 2;
+    }
+    warp_add_u32(&ctr->rm_red, red);
+    warp_add_u32(&ctr->rm_dep, dep);
+}
+
+void launch_detect(const DevMesh& m, const Quality& q, u64 depth_cap, u32 V0, u32 F,
+                   FreshInfo f, WorkLists w, Counters* d_ctr, cudaStream_t st) {
+    if (!F) return;
+    const u32 g = (F + 127) / 128;
+    if (q.mode == 0)
+        k_detect_a<0><<<g, 128, 0, st>>>(m, depth_cap, V0, F, f, d_ctr);
+    else
+        k_detect_a<1><<<g, 128, 0, st>>>(m, depth_cap, V0, F, f, d_ctr);
+    k_detect_b<<<g, 128, 0, st>>>(m, V0, F, f, d_ctr);
+    k_detect_collect<<<g, 128, 0, st>>>(V0, F, f, w, d_ctr);
+}
+
+// ---- parallel vertex removal (remove_free_vertex + flop, mesh.hpp:261-304,442-466) ----
+
+__global__ void k_rm_claim(DevMesh m, const u32* __restrict__ list, u32 n, TriAux x,
+                           WorkLists w, Counters* ctr) {
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const u32 v = list[i];
+    u32* st = w.star + (size_t)i * MAX_STAR;
+    int si[MAX_STAR];
+    const int k = walk_star(m, v, st, si, MAX_STAR);
+    w.star_len[i] = (u32)k;
+    if (k < 3) {
+        raise_err(ctr, k == 0 ? DERR_STAR_TOO_LARGE : DERR_OPEN_STAR, v);
+        w.star_len[i] = 0;
+        return;
+    }
+    for (int q = 0; q < k; ++q) atomicMin(&x.owner[st[q]], v);
+}
+
+// Remove v by ear-clipping its link polygon: each ear is one degree-reducing
+// flip of remove_free_vertex (both orient tests of mesh.hpp:223-225), the
+// last three link vertices are the flop.  The k star triangles become k-2
+// (ids reused in star order), the last two die.
+__global__ void __launch_bounds__(64) k_rm_apply(DevMesh m, const u32* __restrict__ list, u32 n,
+                                                 u32 round, u32 V0, u32 widx, u32 next_list,
+                                                 TriAux x, FreshInfo f, WorkLists w,
+                                                 Counters* ctr) {
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    u32 done = 0;
+    if (i < n) {
+        const u32 v = list[i];
+        const u32* st = w.star + (size_t)i * MAX_STAR;
+        const int k = (int)w.star_len[i];
+        bool own = k >= 3;
+        for (int q = 0; q < k && own; ++q) own = x.owner[st[q]] == v;
+        if (k >= 3 && !own) {
+            const u32 o = atomicAdd(&w.rc->rm_next, 1u);
+            if (o < w.rm_cap) w.rm[next_list][o] = v;
+        } else if (own) {
+            // Link polygon, CCW: L[j] = p_j; link edge j = (L[j], L[j+1]).
+            u32 L[MAX_STAR], R[MAX_STAR], SG[MAX_STAR], ORG[MAX_STAR];
+            uint8_t PK[MAX_STAR];  // 1 = old outer ref, 2 = local (idx<<2|slot), 0 = none
+            int NX[MAX_STAR], PV[MAX_STAR];
+            for (int q = 0; q < k; ++q) {
+                const u32 t = st[q];
+                const uint4 tv = m.tv[t], tn = m.tn[t], ts = m.ts[t];
+                const int iv = tv.x == v ? 0 : (tv.y == v ? 1 : 2);
+                L[q] = comp(tv, nxt(iv));
+                R[q] = comp(tn, iv);
+                PK[q] = R[q] == NONE ? 0 : 1;
+                SG[q] = comp(ts, iv);
+                ORG[q] = 3 * t + iv;
+                NX[q] = q + 1 == k ? 0 : q + 1;
+                PV[q] = q == 0 ? k - 1 : q - 1;
+            }
+            // created triangles (local): vertices, refs, kinds, segs
+            u32 CV[MAX_STAR][3];
+            u32 CN[MAX_STAR][3];
+            uint8_t CK[MAX_STAR][3];
+            u32 CS[MAX_STAR][3];
+            const double2 pv = m.xy[v];
+            int cnt = k, head = 0, created = 0;
+            bool ok = true;
+            // Bind link edge `le` as slot `slot` of created triangle `ci`.
+            auto bind = [&](int ci, int slot, int le) {
+                const u32 tid = st[ci];
+                CS[ci][slot] = SG[le];
+                if (PK[le] == 2) {
+                    const int oi = (int)(R[le] >> 2), os = (int)(R[le] & 3u);
+                    CN[ci][slot] = enc(st[oi], os);
+                    CK[ci][slot] = 0;
+                    CN[oi][os] = enc(tid, slot);
+                } else {
+                    CN[ci][slot] = R[le];
+                    CK[ci][slot] = PK[le];
+                }
+                if (ORG[le] != NONE) x.emap[ORG[le]] = enc(tid, slot);
+            };
+            while (cnt > 3 && ok) {
+                int j = head;
+                bool found = false;
+                for (int it = 0; it < cnt; ++it) {
+                    const int a = PV[j], c = NX[j];
+                    const double2 pa = m.xy[L[a]], pj = m.xy[L[j]], pc = m.xy[L[c]];
+                    if (orient2d(pa, pj, pc) > 0 && orient2d(pa, pc, pv) > 0) {
+                        found = true;
+                        break;
+                    }
+                    j = NX[j];
+                }
+                if (!found) {
+                    ok = false;
+                    break;
+                }
+                const int a = PV[j], c = NX[j];
+                const int ci = created++;
+                CV[ci][0] = L[a];
+                CV[ci][1] = L[j];
+                CV[ci][2] = L[c];
+                bind(ci, 0, j);   // opposite L[a]: (L[j], L[c])
+                bind(ci, 2, a);   // opposite L[c]: (L[a], L[j])
+                CS[ci][1] = NONE; // diagonal (L[c], L[a]) -- bound later
+                CN[ci][1] = NONE;
+                CK[ci][1] = 0;
+                // the remaining polygon's edge (L[a], L[c]) is this diagonal
+                R[a] = ((u32)ci << 2) | 1u;
+                PK[a] = 2;
+                SG[a] = NONE;
+                ORG[a] = NONE;
+                NX[a] = c;
+                PV[c] = a;
+                if (head == j) head = c;
+                --cnt;
+            }
+            if (ok) {
+                const int a = head, b = NX[a], c = NX[b];
+                const int ci = created++;
+                CV[ci][0] = L[a];
+                CV[ci][1] = L[b];
+                CV[ci][2] = L[c];
+                bind(ci, 0, b);
+                bind(ci, 1, c);
+                bind(ci, 2, a);
+                ok = orient2d(m.xy[L[a]], m.xy[L[b]], m.xy[L[c]]) > 0;
+            }
+            if (!ok) {
+                raise_err(ctr, DERR_NO_EAR, v);
+            } else {
+                for (int q = 0; q < k; ++q) x.stamp[st[q]] = round;
+                for (int ci = 0; ci < created; ++ci) {
+                    const u32 pend = (CK[ci][0] == 1 ? 1u : 0u) | (CK[ci][1] == 1 ? 2u : 0u) |
+                                     (CK[ci][2] == 1 ? 4u : 0u);
+                    write_tri(m, st[ci], CV[ci][0], CV[ci][1], CV[ci][2], CN[ci][0], CN[ci][1],
+                              CN[ci][2], pend, CS[ci][0], CS[ci][1], CS[ci][2]);
+                }
+                for (int q = created; q < k; ++q) {
+                    uint4 tv = m.tv[st[q]];
+                    tv.w = 0;
+                    m.tv[st[q]] = tv;
+                }
+                m.valive[v] = 0;
+                m.vtri[v] = NONE;
+                f.removed[v - V0] = 1;
+                push_touched(w, st, created);
+                for (int ci = 0; ci < created; ++ci) {
+                    const u32 codes[3] = {enc(st[ci], 0), enc(st[ci], 1), enc(st[ci], 2)};
+                    push_work(w, widx, codes, 3, ctr);
+                }
+                done = 1;
+            }
+        }
+    }
+    warp_add_u32(&ctr->rm_done, done);
+}
+
+__global__ void k_rm_post(u32 n, TriAux x, WorkLists w) {
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const u32* st = w.star + (size_t)i * MAX_STAR;
+    const u32 k = w.star_len[i];
+    for (u32 q = 0; q < k; ++q) x.owner[st[q]] = NONE;
+}
+
+void launch_removal_round(const DevMesh& m, u32 round, u32 V0, TriAux a, FreshInfo f,
+                          WorkLists w, u32 cur, u32 n, u32 widx, Counters* d_ctr,
+                          cudaStream_t st) {
+    if (!n) return;
+    k_rm_claim<<<(n + 127) / 128, 128, 0, st>>>(m, w.rm[cur], n, a, w, d_ctr);
+    k_rm_apply<<<(n + 63) / 64, 64, 0, st>>>(m, w.rm[cur], n, round, V0, widx, cur ^ 1u, a, f, w,
+                                            d_ctr);
+    k_rm_post<<<(n + 255) / 256, 256, 0, st>>>(n, a, w);
+    const u32 nt = n * (MAX_STAR - 2);
+    k_fixup<<<(nt + 255) / 256, 256, 0, st>>>(m, round, a, w, nt, 0, 0, d_ctr);
+}
+
+}  // namespace gdp2d

@@ -1,0 +1,130 @@
+"""Full refinement on the GPU, invariant-checked against the reference's own
+validators (mesh.hpp:505-557, verify.hpp:92-200) and its Steiner count."""
+import math
+
+import numpy as np
+import pytest
+
+from gdp2d_testlib import B_SQRT2_THETA, small_corpus, unit_square
+
+pytestmark = pytest.mark.gpu
+
+
+def batch_safety_holds(m):
+    """test_refine.cpp:30-44: no edge joins two same-batch circumcenters."""
+    t = m.tri_v[m.tri_alive.astype(bool)]
+    for i in range(3):
+        x, y = t[:, (i + 1) % 3], t[:, (i + 2) % 3]
+        cc = (m.vert_kind[x] == 2) & (m.vert_kind[y] == 2)
+        same = (m.vert_birth[x] == m.vert_birth[y]) & (m.vert_birth[x] > 0)
+        if np.any(cc & same):
+            return False
+    return True
+
+
+def check_invariants(out, pts, closed, q, cdt_check=True):
+    from oracle.ref import RefMesh
+    rm = RefMesh.from_mesh(out)
+    rm.check_structure()
+    assert rm.euler_holds()
+    assert rm.conformity_ok(pts, closed)
+    assert rm.count_bad(q) == 0
+    if cdt_check:
+        assert rm.cdt_violations() == 0
+    assert batch_safety_holds(out)
+    return rm
+
+
+def _run(pts, segs, q, cfg=None):
+    from paper_2007_00324_b200 import host, refine
+    from oracle.ref import RefMesh
+    m, closed = host.build_cdt(pts, segs)
+    ref = RefMesh.from_mesh(m)
+    gpu = m.copy()
+    rep = refine(gpu, q, cfg)
+    rref = ref.refine(q)
+    return gpu, closed, rep, rref
+
+
+def test_unit_square(built):
+    from paper_2007_00324_b200 import QualityCriteria
+    pts, segs = unit_square()
+    for q in (QualityCriteria(20.0), QualityCriteria(20.0, 0.2), QualityCriteria(22.0, 0.3),
+              QualityCriteria(30.0)):
+        out, closed, rep, rref = _run(pts, segs, q)
+        assert not rep.iteration_cap_hit
+        assert rep.bad_triangles == 0 and rep.bad_area_percent == 0.0
+        check_invariants(out, pts, closed, q)
+        assert rep.steiner_points <= 1.3 * rref.steiner_points + 8
+
+
+def test_already_quality_runs_zero_batches(built):
+    from paper_2007_00324_b200 import QualityCriteria, refine
+    pts, segs = unit_square()
+    q = QualityCriteria(20.0)
+    out, _, _, _ = _run(pts, segs, q)
+    again = out.copy()
+    r2 = refine(again, q)
+    assert len(r2.batches) == 0
+    assert again.alive_vertex_count() == out.alive_vertex_count()
+
+
+def test_corpus(built):
+    from paper_2007_00324_b200 import QualityCriteria
+    q = QualityCriteria(20.0)
+    for name, (pts, segs) in small_corpus().items():
+        out, closed, rep, rref = _run(pts, segs, q)
+        check_invariants(out, pts, closed, q)
+        assert rep.steiner_points <= 1.10 * rref.steiner_points + 8, (name, rep.steiner_points,
+                                                                     rref.steiner_points)
+
+
+@pytest.mark.parametrize("theta", [B_SQRT2_THETA, 30.0])
+def test_uniform_50k(built, theta):
+    from paper_2007_00324_b200 import QualityCriteria, host
+    q = QualityCriteria(theta)
+    pts, segs = host.generate_pslg(50_000, 5_000, "uniform", 3)
+    out, closed, rep, rref = _run(pts, segs, q)
+    check_invariants(out, pts, closed, q, cdt_check=True)
+    assert abs(rep.steiner_points - rref.steiner_points) <= 0.10 * rref.steiner_points, \
+        (rep.steiner_points, rref.steiner_points)
+    assert rep.min_angle_deg >= theta - 1e-9
+
+
+def test_gaussian_50k(built):
+    from paper_2007_00324_b200 import QualityCriteria, host
+    q = QualityCriteria(B_SQRT2_THETA)
+    pts, segs = host.generate_pslg(50_000, 5_000, "gaussian", 5)
+    out, closed, rep, rref = _run(pts, segs, q)
+    check_invariants(out, pts, closed, q)
+    assert abs(rep.steiner_points - rref.steiner_points) <= 0.10 * rref.steiner_points
+
+
+def test_deterministic(built):
+    from paper_2007_00324_b200 import QualityCriteria, host, refine
+    pts, segs = host.generate_pslg(20_000, 2_000, "uniform", 9)
+    m, _ = host.build_cdt(pts, segs)
+    q = QualityCriteria(B_SQRT2_THETA)
+    a, b = m.copy(), m.copy()
+    refine(a, q)
+    refine(b, q)
+    assert np.array_equal(a.xy[a.vert_alive.astype(bool)], b.xy[b.vert_alive.astype(bool)])
+    assert np.array_equal(a.tri_v, b.tri_v)
+
+
+def test_rule_ablations(built):
+    from paper_2007_00324_b200 import EngineConfig, QualityCriteria, RuleFlags, host
+    q = QualityCriteria(20.0)
+    pts, segs = host.generate_pslg(10_000, 1_000, "uniform", 2)
+    for rules in (RuleFlags(rule2_filtering_enabled=False), RuleFlags(rule4_unified_collection=False),
+                  RuleFlags(rule1_compaction_threshold=0)):
+        out, closed, rep, rref = _run(pts, segs, q, EngineConfig(rules=rules))
+        check_invariants(out, pts, closed, q)
+
+
+def test_chew_mode(built):
+    from paper_2007_00324_b200 import CHEW, QualityCriteria
+    pts, segs = unit_square()
+    q = QualityCriteria(20.0, math.inf, CHEW)
+    out, closed, rep, _ = _run(pts, segs, q)
+    check_invariants(out, pts, closed, q)
