@@ -1,0 +1,346 @@
+#!/usr/bin/env python
+"""gDP2d refinement benchmark (BASELINE.json metric: refine wall time and
+Steiner points/s on one B200, against the CPU reference on the host cores).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl gdp2d|reference]
+
+A *step* is one complete refinement (Algorithm 1, lines 2-9) of the workload
+PSLG's initial CDT to radius-edge <= sqrt(2): the device-resident working mesh
+is restored from the pristine copy in HBM, then refined to quality.  Line 1
+(build_cdt, untimed in the paper) runs once on the host before
+timing.  Under torchrun every rank refines its own independent PSLG (seed +
+rank): replicas, no data-path collective ("scaling": "weak").
+
+Keys beyond the base contract:
+  e2e          the same metric through the C ABI entry point gdp2d_refine with
+               HOST buffers (H2D of the input mesh + D2H of the refined mesh
+               inside the timed region)
+  roofline     the Line-3 full scan kernel (k_collect_flags): algorithmic bytes
+               (16 B/triangle + 16 B/vertex + 48 B/subsegment per launch) over its
+               CUDA-event time, against MEASURED_PEAKS.json hbm_gbs
+  cpu_baseline the reference (oracle/_ref, unmodified cdtref headers) timed on a
+               bounded sample of the same workload on this box's host cores
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "Refine wall-time (s) & Steiner pts/sec on 1 B200 vs CPU ref on host cores"
+UNIT = "Steiner pts/s"
+B_THETA = math.degrees(math.asin(1.0 / (2.0 * math.sqrt(2.0))))
+CONFIGS = {
+    1: dict(n=100_000, m=1_000, dist="uniform", theta=B_THETA,
+            name="cfg1: 100K uniform pts + 1K segs, radius-edge<=sqrt2"),
+    2: dict(n=1_000_000, m=100_000, dist="uniform", theta=B_THETA,
+            name="cfg2: 1M uniform pts + 10% segs, radius-edge<=sqrt2"),
+    3: dict(n=5_000_000, m=500_000, dist="gaussian", theta=B_THETA,
+            name="cfg3: 5M gaussian pts + 10% segs, radius-edge<=sqrt2"),
+    4: dict(n=1_000_000, m=100_000, dist="uniform", theta=30.0,
+            name="cfg4: 1M uniform pts + 10% segs, min-angle 30deg"),
+    5: dict(n=2_000_000, m=200_000, dist="uniform", theta=B_THETA,
+            name="cfg5: 2M uniform pts + 10% segs per GPU (replicas), radius-edge<=sqrt2"),
+}
+CPU_SAMPLE = dict(n=250_000, m=25_000)   # bounded CPU-reference sample (~5-10 s)
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class Dist:
+    def __init__(self, world, rank, local):
+        self.world, self.rank, self.local = world, rank, local
+        self.pg = None
+        if world > 1:
+            import torch
+            import torch.distributed as td
+            torch.cuda.set_device(local)
+            td.init_process_group("nccl", device_id=torch.device("cuda", local))
+            self.td = td
+
+    def barrier(self):
+        if self.world > 1:
+            self.td.barrier()
+
+    def max(self, x: float) -> float:
+        if self.world == 1:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{self.local}")
+        self.td.all_reduce(t, op=self.td.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, x: float) -> float:
+        if self.world == 1:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{self.local}")
+        self.td.all_reduce(t, op=self.td.ReduceOp.SUM)
+        return float(t.item())
+
+    def close(self):
+        if self.world > 1:
+            self.td.destroy_process_group()
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = ROOT / "gpurun_out" / f"clocks_{device}.csv"
+
+    def __enter__(self):
+        try:
+            self.path.parent.mkdir(exist_ok=True)
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.f.close()
+
+    def summary(self):
+        try:
+            rows = [r.split(",") for r in self.path.read_text().strip().splitlines() if r.strip()]
+        except Exception:
+            rows = []
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        smax = max(float(r[2]) for r in rows)
+        load = [s for s in sm if s > 0.5 * smax] or sm
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4)
+                          if len(r) > 4 + k and "Active" in r[4 + k] and "Not" not in r[4 + k]})
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": smax,
+                "samples": len(rows), "reasons": reasons}
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def make_workload(cfg: dict, seed: int):
+    from paper_2007_00324_b200 import host
+    pts, segs = host.generate_pslg(cfg["n"], cfg["m"], cfg["dist"], seed)
+    mesh, closed = host.build_cdt(pts, segs)
+    return mesh
+
+
+def mesh_bytes(m) -> int:
+    return sum(getattr(m, k).nbytes for k in ("xy", "vert_kind", "vert_birth", "vert_alive",
+                                              "vert_tri", "tri_v", "tri_n", "tri_seg", "tri_alive",
+                                              "seg_v", "seg_parent", "seg_encroached", "seg_alive",
+                                              "seg_tri"))
+
+
+def cpu_reference_steps(cfg, steps, seed, executors):
+    """Time the reference refine (oracle/_ref) on a bounded sample; returns
+    (steiner per step list, seconds per step list, sample description)."""
+    from paper_2007_00324_b200 import QualityCriteria
+    from oracle.ref import RefMesh
+    sample = dict(cfg, **CPU_SAMPLE)
+    mesh = make_workload(sample, seed)
+    base = RefMesh.from_mesh(mesh)
+    q = QualityCriteria(cfg["theta"])
+    st, secs = [], []
+    for _ in range(steps):
+        m = base.clone()
+        rep = m.refine(q, executors=executors)
+        st.append(rep.steiner_points)
+        secs.append(rep.wall_seconds)
+    desc = (f"reference cdtref::refine (oracle/_ref, g++ -O3) on a {sample['n']}-point "
+            f"{sample['dist']} PSLG + {sample['m']} segs (same generator and quality bound as "
+            f"the workload), executors={executors}")
+    return st, secs, desc
+
+
+def run_reference_arm(a, world, rank):
+    cfg = CONFIGS[a.config]
+    if rank != 0:
+        return 0
+    cores = os.cpu_count() or 1
+    warm_st, warm_s, _ = cpu_reference_steps(cfg, a.warmup, 1234, cores) if a.warmup else ([], [], "")
+    st, secs, desc = cpu_reference_steps(cfg, a.steps, 1234, cores)
+    total = sum(secs)
+    value = sum(st) / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": total / a.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": cfg["name"], "cpu_sample": CPU_SAMPLE},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": desc},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "refine_wall_s": total / a.steps,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", default="gdp2d", choices=["gdp2d", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    a = ap.parse_args()
+    world, rank, local = dist_env()
+    if a.impl == "reference":
+        return run_reference_arm(a, world, rank)
+
+    import numpy as np
+    import torch
+
+    from paper_2007_00324_b200 import Engine, QualityCriteria, refine
+    from paper_2007_00324_b200 import _abi as A
+
+    dist = Dist(world, rank, local)
+    device = local
+    torch.cuda.set_device(device)
+    cfg = CONFIGS[a.config]
+    q = QualityCriteria(cfg["theta"])
+    seed = 20261017 + rank
+    t0 = time.time()
+    mesh = make_workload(cfg, seed)
+    setup_s = time.time() - t0
+    lib = A.engine()
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{device}")  # > 126 MB L2
+
+    eng = Engine(device)
+    eng.upload(mesh)
+    for _ in range(max(a.warmup, 0)):
+        eng.reset()
+        eng.refine(q)
+
+    # ---- timed region: K device-resident steps ----
+    reps = []
+    step_ms = []
+    dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = lib.gdp2d_kernel_launches()
+    with ClockSampler(device) as clk:
+        host_t0 = time.perf_counter()
+        for _ in range(a.steps):
+            flush.zero_()                       # evict L2 between steps
+            torch.cuda.synchronize()
+            eng.reset()
+            rep = eng.refine(q)
+            reps.append(rep)
+            step_ms.append(rep.device_seconds * 1e3)
+        torch.cuda.synchronize()
+        host_s = time.perf_counter() - host_t0
+    launches = lib.gdp2d_kernel_launches() - launches0
+    dist.barrier()
+    dev_s = sum(step_ms) / 1e3
+    dev_s_max = dist.max(dev_s)
+    steiner_local = sum(r.steiner_points for r in reps)
+    steiner_all = dist.sum(steiner_local)
+    value = steiner_all / dev_s_max
+    last = reps[-1]
+
+    # ---- e2e: the public C ABI with host buffers ----
+    e2e_steps = a.e2e_steps or a.steps
+    e2e_s = []
+    e2e_st = 0
+    h2d = mesh_bytes(mesh)
+    d2h = 0
+    dist.barrier()
+    for _ in range(e2e_steps):
+        m = mesh.copy()
+        t = time.perf_counter()
+        r = refine(m, q)
+        e2e_s.append(time.perf_counter() - t)
+        e2e_st += r.steiner_points
+        d2h = mesh_bytes(m)
+    e2e_total = dist.max(sum(e2e_s))
+    e2e_value = dist.sum(e2e_st) / e2e_total
+
+    # ---- roofline of the Line-3 full scan kernel ----
+    peak, peak_kind = load_peaks()
+    scan_s = sum(r.scan_seconds for r in reps)
+    scan_b = sum(r.scan_bytes for r in reps)
+    scan_n = sum(r.scan_launches for r in reps)
+    achieved = (scan_b / scan_n) / (scan_s / scan_n) / 1e9 if scan_n and scan_s > 0 else None
+    refine_gbs = last.algorithmic_bytes() / last.device_seconds / 1e9
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": dev_s_max / a.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["name"], "points_per_gpu": cfg["n"],
+                   "segments_per_gpu": cfg["m"], "theta_deg": cfg["theta"],
+                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "l2": "512 MB flush before every step; mesh > L2"},
+        "refine_wall_s": dev_s_max / a.steps,
+        "steiner_points": last.steiner_points,
+        "batches": len(last.batches),
+        "quality": {"bad_triangles": last.bad_triangles, "min_angle_deg": last.min_angle_deg},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "wall_s_per_step": e2e_total / e2e_steps},
+        "roofline": {"kernel": "k_collect_flags (Line-3 full scan)", "bound": "hbm",
+                     "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": (achieved / peak) if achieved else None, "traffic": None,
+                     "bytes_per_launch": scan_b / scan_n if scan_n else None,
+                     "share_of_step": scan_s / dev_s if dev_s else None},
+        "roofline_refine": {"bytes_alg": last.algorithmic_bytes(), "achieved": refine_gbs,
+                            "frac": refine_gbs / peak, "unit": "GB/s",
+                            "formula": "SURVEY 8(d) bytes_alg / device refine time"},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "host_timed_s": host_s,
+        "setup_s": setup_s,
+    }
+
+    # ---- CPU baseline (rank 0, N = 1 only) ----
+    if world == 1 and not a.no_cpu_baseline:
+        st, secs, desc = cpu_reference_steps(cfg, 1, 1234, 1)
+        line["cpu_baseline"] = {"value": st[0] / secs[0], "unit": UNIT, "cores": 1,
+                                "kind": "reference", "sample": desc,
+                                "seconds": secs[0], "steiner": st[0]}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    eng.close()
+    dist.close()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -168,6 +168,13 @@ typedef struct gdp2d_report {
     uint64_t total_inserted, total_flips, total_removed;
     uint64_t sum_tris_alive, sum_verts_alive, sum_subsegs_alive;
     double   device_seconds;     /* CUDA-event time of the device loop        */
+    /* roofline instrumentation of the Line-3 full scan (collect flags kernel):
+     * CUDA-event time summed over its launches and its algorithmic bytes
+     * (16 B per triangle slot + 16 B per vertex + 48 B per subsegment). */
+    double   scan_seconds;
+    uint64_t scan_bytes;
+    uint64_t scan_launches;
+    uint64_t kernel_launches;    /* engine kernels launched by this call      */
 } gdp2d_report;
 
 /* SplitCandidate (refine.hpp:71) in exchange form. */
@@ -201,6 +208,8 @@ const char* gdp2d_version(void);
 /* sizeof() of the exchange structs, for binding-layout checks:
  * 0 mesh_view, 1 mesh_buf, 2 params, 3 batch_metrics, 4 report, 5 candidate */
 size_t gdp2d_struct_size(int which);
+/* Process-wide count of engine kernel launches so far (all devices). */
+uint64_t gdp2d_kernel_launches(void);
 
 /* ---- device-resident context (bench / replicas / parity) ------------------- */
 

@@ -72,7 +72,9 @@ class Report(C.Structure):
                 ("total_cavity_visits", C.c_uint64), ("total_inserted", C.c_uint64),
                 ("total_flips", C.c_uint64), ("total_removed", C.c_uint64),
                 ("sum_tris_alive", C.c_uint64), ("sum_verts_alive", C.c_uint64),
-                ("sum_subsegs_alive", C.c_uint64), ("device_seconds", C.c_double)]
+                ("sum_subsegs_alive", C.c_uint64), ("device_seconds", C.c_double),
+                ("scan_seconds", C.c_double), ("scan_bytes", C.c_uint64),
+                ("scan_launches", C.c_uint64), ("kernel_launches", C.c_uint64)]
 
 
 class Candidate(C.Structure):
@@ -102,6 +104,7 @@ SIGNATURES = {
     "gdp2d_last_error": (C.c_char_p, []),
     "gdp2d_version": (C.c_char_p, []),
     "gdp2d_struct_size": (C.c_size_t, [C.c_int]),
+    "gdp2d_kernel_launches": (C.c_uint64, []),
     "gdp2d_ctx_create": (C.c_int, [C.POINTER(ctx_p), C.c_int]),
     "gdp2d_ctx_destroy": (None, [ctx_p]),
     "gdp2d_ctx_upload": (C.c_int, [ctx_p, C.POINTER(MeshView)]),

@@ -19,6 +19,11 @@
 
 using namespace gdp2d;
 
+unsigned long long& gdp2d::launch_counter() {
+    static unsigned long long n = 0;
+    return n;
+}
+
 namespace {
 
 thread_local std::string g_err;
@@ -221,7 +226,7 @@ struct gdp2d_ctx {
     u32* h_tot = nullptr;         // pinned [4]
     void* qscratch = nullptr;
     u32 round = 0;
-    cudaEvent_t ev[GDP2D_NPHASES + 2];
+    cudaEvent_t ev[GDP2D_NPHASES + 4];   // phases, loop start/end, scan start/end
     // upload / download staging
     u32* stage_u32[3] = {nullptr, nullptr, nullptr};
     uint8_t* stage_u8 = nullptr;
@@ -458,13 +463,13 @@ void upload(gdp2d_ctx* x, const gdp2d_mesh_view* v) {
     CK(cudaMemcpyAsync(m.vbirth, v->vert_birth, 4ull * V, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(m.valive, v->vert_alive, V, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(m.vtri, v->vert_tri, 4ull * V, cudaMemcpyHostToDevice, st));
-    ensure_stage(x, std::max<size_t>(3ull * T, 2ull * S) + 16);
+    ensure_stage(x, std::max<size_t>(3ull * T, 2ull * S) + T + S + 16);
     if (T) {
         CK(cudaMemcpyAsync(x->stage_u32[0], v->tri_v, 12ull * T, cudaMemcpyHostToDevice, st));
         CK(cudaMemcpyAsync(x->stage_u32[1], v->tri_seg, 12ull * T, cudaMemcpyHostToDevice, st));
         CK(cudaMemcpyAsync(x->stage_u32[2], v->tri_n, 12ull * T, cudaMemcpyHostToDevice, st));
         CK(cudaMemcpyAsync(x->stage_u8, v->tri_alive, T, cudaMemcpyHostToDevice, st));
-        k_pack_tris<<<grid(T), 256, 0, st>>>(m, x->stage_u32[0], x->stage_u32[1], x->stage_u8);
+        note_launch(), k_pack_tris<<<grid(T), 256, 0, st>>>(m, x->stage_u32[0], x->stage_u32[1], x->stage_u8);
         launch_encode_neighbors(m, x->stage_u32[2], st);
     }
     if (S) {
@@ -472,9 +477,9 @@ void upload(gdp2d_ctx* x, const gdp2d_mesh_view* v) {
         CK(cudaMemcpyAsync(m.sparent, v->seg_parent, 4ull * S, cudaMemcpyHostToDevice, st));
         CK(cudaMemcpyAsync(m.salive, v->seg_alive, S, cudaMemcpyHostToDevice, st));
         CK(cudaMemcpyAsync(m.stri, v->seg_tri, 4ull * S, cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(x->stage_u8 + 3ull * T + 8, v->seg_encroached, S,
-                           cudaMemcpyHostToDevice, st));
-        k_u8_to_u32<<<grid(S), 256, 0, st>>>(x->stage_u8 + 3ull * T + 8, m.senc, S);
+        CK(cudaMemcpyAsync(x->stage_u8 + T + 8, v->seg_encroached, S, cudaMemcpyHostToDevice,
+                           st));
+        note_launch(), k_u8_to_u32<<<grid(S), 256, 0, st>>>(x->stage_u8 + T + 8, m.senc, S);
         CK(cudaMemsetAsync(m.sdepth, 0, 4ull * S, st));
     }
     CK(cudaGetLastError());
@@ -535,7 +540,7 @@ void download(gdp2d_ctx* x, gdp2d_mesh_buf* b) {
     CK(cudaMemcpyAsync(b->vert_alive, m.valive, V, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(b->vert_tri, m.vtri, 4ull * V, cudaMemcpyDeviceToHost, st));
     if (T) {
-        k_unpack_tris<<<grid(T), 256, 0, st>>>(m, x->stage_u32[0], x->stage_u32[1], x->stage_u8);
+        note_launch(), k_unpack_tris<<<grid(T), 256, 0, st>>>(m, x->stage_u32[0], x->stage_u32[1], x->stage_u8);
         launch_decode_neighbors(m, x->stage_u32[2], st);
         CK(cudaMemcpyAsync(b->tri_v, x->stage_u32[0], 12ull * T, cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(b->tri_seg, x->stage_u32[1], 12ull * T, cudaMemcpyDeviceToHost, st));
@@ -548,7 +553,7 @@ void download(gdp2d_ctx* x, gdp2d_mesh_buf* b) {
         CK(cudaMemcpyAsync(b->seg_parent, m.sparent, 4ull * S, cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(b->seg_alive, m.salive, S, cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(b->seg_tri, m.stri, 4ull * S, cudaMemcpyDeviceToHost, st));
-        k_u32_to_u8<<<grid(S), 256, 0, st>>>(m.senc, x->stage_u8, S);
+        note_launch(), k_u32_to_u8<<<grid(S), 256, 0, st>>>(m.senc, x->stage_u8, S);
         CK(cudaMemcpyAsync(b->seg_encroached, x->stage_u8, S, cudaMemcpyDeviceToHost, st));
     }
     CK(cudaStreamSynchronize(st));
@@ -569,6 +574,7 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
     const u32 ncav = p->rule2_filtering_enabled ? p->cavity_n : 0;
     if (ncav > (u32)MAX_CAVITY_N) throw Fail{GDP2D_EINVAL, "cavity_n exceeds 64"};
     const gdp2d_report keep = *r;
+    const unsigned long long launches0 = gdp2d::launch_counter();
     std::memset(r, 0, sizeof *r);
     r->batches = keep.batches;
     r->batches_capacity = keep.batches_capacity;
@@ -589,8 +595,13 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
         ensure_cands(x, m.nS + m.nT);
         CK(cudaEventRecord(x->ev[0], st));
         const u32 C = launch_collect(m, q, p->rule4_unified_collection != 0, x->flags, x->c,
-                                     x->ccap, x->scan, x->d_ctr, st);
+                                     x->ccap, x->scan, x->d_ctr, st, x->ev[GDP2D_NPHASES + 2],
+                                     x->ev[GDP2D_NPHASES + 3]);
         CK(cudaGetLastError());
+        // launch_collect synchronised: the scan events are complete
+        r->scan_seconds += ev_ms(x->ev[GDP2D_NPHASES + 2], x->ev[GDP2D_NPHASES + 3]) * 1e-3;
+        r->scan_bytes += 16ull * m.nT + 16ull * m.nV + 48ull * m.nS;
+        r->scan_launches += 1;
         if (C == 0) break;
         CK(cudaEventRecord(x->ev[1], st));   // split points are fused into collect
         CK(cudaEventRecord(x->ev[2], st));
@@ -656,8 +667,7 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
         check_dev_err(x);
         const Counters& h = *x->h_ctr;
         const u32 inserted = h.ins_mid + h.ins_cc;
-        const u32 removed = h.rm_red + h.rm_dep;
-        const u32 retained = inserted - std::min(inserted, removed);
+        const u32 retained = inserted - std::min(inserted, h.rm_done);
         x->alive_v += inserted;
         x->alive_v -= std::min<ull>(x->alive_v, h.rm_done);
         x->alive_t += nt;
@@ -704,6 +714,7 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
     CK(cudaEventRecord(x->ev[GDP2D_NPHASES], st));
     CK(cudaEventSynchronize(x->ev[GDP2D_NPHASES]));
     r->device_seconds = ev_ms(x->ev[GDP2D_NPHASES + 1], x->ev[GDP2D_NPHASES]) * 1e-3;
+    r->kernel_launches = gdp2d::launch_counter() - launches0;
     r->wall_seconds =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
 }
@@ -822,6 +833,8 @@ extern "C" {
 
 const char* gdp2d_last_error(void) { return g_err.c_str(); }
 const char* gdp2d_version(void) { return "gdp2d-b200 0.1 (sm_100a)"; }
+
+uint64_t gdp2d_kernel_launches(void) { return __atomic_load_n(&launch_counter(), __ATOMIC_RELAXED); }
 
 size_t gdp2d_struct_size(int which) {
     switch (which) {

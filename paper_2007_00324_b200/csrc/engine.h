@@ -11,6 +11,11 @@
 
 namespace gdp2d {
 
+// Process-wide count of engine kernel launches (reported by bench.py as
+// gpu_launches; every <<<>>> in the engine goes through note_launch()).
+unsigned long long& launch_counter();
+inline void note_launch() { __atomic_add_fetch(&launch_counter(), 1ull, __ATOMIC_RELAXED); }
+
 constexpr int SCAN_BLOCK = 256;
 constexpr int SCAN_ITEMS = 8;
 constexpr int SCAN_TILE = SCAN_BLOCK * SCAN_ITEMS;
@@ -48,7 +53,8 @@ struct CollectBufs {
 // candidate count (synchronises).  If rule4 == false and subsegment
 // candidates exist, triangles are skipped (refine.hpp:239).
 u32 launch_collect(const DevMesh& m, const Quality& q, bool rule4, uint8_t* flags, DevCands c,
-                   u32 ccap, ScanScratch& s, Counters* d_ctr, cudaStream_t st);
+                   u32 ccap, ScanScratch& s, Counters* d_ctr, cudaStream_t st,
+                   cudaEvent_t ev_scan0 = nullptr, cudaEvent_t ev_scan1 = nullptr);
 void launch_split_points(const DevMesh& m, DevCands c, u32 n, Counters* d_ctr, cudaStream_t st);
 void launch_locate(const DevMesh& m, DevCands c, u32 n, Counters* d_ctr, cudaStream_t st);
 void launch_claim(const DevMesh& m, DevCands c, u32 n, TriAux a, Counters* d_ctr,

@@ -92,7 +92,7 @@ struct Counters {
     u32 err_code;
     u32 err_info;
     u32 fallbacks;
-    u32 pad;
+    u32 rm_kept;        // removals abandoned (degenerate star)
 };
 
 // Per-round work-list counters (zeroed by the host before every round).

@@ -118,7 +118,8 @@ __global__ void __launch_bounds__(SCAN_BLOCK) k_collect_scatter(DevMesh m, Colle
 }
 
 u32 launch_collect(const DevMesh& m, const Quality& q, bool rule4, uint8_t* flags, DevCands c,
-                   u32 ccap, ScanScratch& s, Counters* d_ctr, cudaStream_t st) {
+                   u32 ccap, ScanScratch& s, Counters* d_ctr, cudaStream_t st,
+                   cudaEvent_t ev_scan0, cudaEvent_t ev_scan1) {
     auto run = [&](bool sub, bool tri) -> u32 {
         CollectRange r;
         r.nS = sub ? m.nS : 0;
@@ -132,16 +133,18 @@ u32 launch_collect(const DevMesh& m, const Quality& q, bool rule4, uint8_t* flag
             s.cap = (tiles + 1) * 2;
             cudaMalloc(&s.partial, sizeof(u32) * s.cap);
         }
+        if (ev_scan0 && sub) cudaEventRecord(ev_scan0, st);
         if (q.mode == 0)
-            k_collect_flags<0><<<tiles, SCAN_BLOCK, 0, st>>>(m, q, r, flags, s.partial);
+            note_launch(), k_collect_flags<0><<<tiles, SCAN_BLOCK, 0, st>>>(m, q, r, flags, s.partial);
         else
-            k_collect_flags<1><<<tiles, SCAN_BLOCK, 0, st>>>(m, q, r, flags, s.partial);
+            note_launch(), k_collect_flags<1><<<tiles, SCAN_BLOCK, 0, st>>>(m, q, r, flags, s.partial);
+        if (ev_scan1 && (tri || !rule4)) cudaEventRecord(ev_scan1, st);
         scan_partials(s.partial, tiles, s.partial + tiles, st);
         u32 total = 0;
         cudaMemcpyAsync(&total, s.partial + tiles, sizeof(u32), cudaMemcpyDeviceToHost, st);
         cudaStreamSynchronize(st);
         if (total > 0)
-            k_collect_scatter<<<tiles, SCAN_BLOCK, 0, st>>>(m, r, flags, s.partial, c, ccap, d_ctr);
+            note_launch(), k_collect_scatter<<<tiles, SCAN_BLOCK, 0, st>>>(m, r, flags, s.partial, c, ccap, d_ctr);
         return total;
     };
     if (rule4) return run(true, true);

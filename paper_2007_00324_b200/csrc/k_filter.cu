@@ -59,10 +59,10 @@ void launch_claim(const DevMesh& m, DevCands c, u32 n, TriAux a, Counters* d_ctr
                   cudaStream_t st) {
     if (!n) return;
     const u32 g = (n + 255) / 256;
-    k_claim_max<<<g, 256, 0, st>>>(c, n, a.ckey);
-    k_claim_tie<<<g, 256, 0, st>>>(c, n, a.ckey, a.ctie);
-    k_claim_check<<<g, 256, 0, st>>>(c, n, a.ckey, a.ctie, d_ctr);
-    k_claim_reset<<<g, 256, 0, st>>>(c, n, m.nT, a.ckey, a.ctie);
+    note_launch(), k_claim_max<<<g, 256, 0, st>>>(c, n, a.ckey);
+    note_launch(), k_claim_tie<<<g, 256, 0, st>>>(c, n, a.ckey, a.ctie);
+    note_launch(), k_claim_check<<<g, 256, 0, st>>>(c, n, a.ckey, a.ctie, d_ctr);
+    note_launch(), k_claim_reset<<<g, 256, 0, st>>>(c, n, m.nT, a.ckey, a.ctie);
 }
 
 // ---- cavity ---------------------------------------------------------------------
@@ -206,12 +206,12 @@ void launch_cavity(const DevMesh& m, DevCands c, u32 n, u32 ncav, bool extras, T
                    cudaStream_t st) {
     if (!n) return;
     const u32 rs = ncav + 1 + MAX_CLAIM_EXTRA;
-    k_cavity_bfs<<<(n + 127) / 128, 128, 0, st>>>(m, c, n, ncav, extras ? 1 : 0, rs, regions,
+    note_launch(), k_cavity_bfs<<<(n + 127) / 128, 128, 0, st>>>(m, c, n, ncav, extras ? 1 : 0, rs, regions,
                                                    region_len, bfs_len, a.ckey, d_ctr);
     const u32 g = (n + 255) / 256;
-    k_cavity_tie<<<g, 256, 0, st>>>(c, n, rs, regions, region_len, a.ckey, a.ctie);
-    k_cavity_check<<<g, 256, 0, st>>>(c, n, rs, regions, region_len, a.ckey, a.ctie, d_ctr);
-    k_cavity_reset<<<g, 256, 0, st>>>(n, rs, regions, region_len, a.ckey, a.ctie);
+    note_launch(), k_cavity_tie<<<g, 256, 0, st>>>(c, n, rs, regions, region_len, a.ckey, a.ctie);
+    note_launch(), k_cavity_check<<<g, 256, 0, st>>>(c, n, rs, regions, region_len, a.ckey, a.ctie, d_ctr);
+    note_launch(), k_cavity_reset<<<g, 256, 0, st>>>(n, rs, regions, region_len, a.ckey, a.ctie);
 }
 
 }  // namespace gdp2d

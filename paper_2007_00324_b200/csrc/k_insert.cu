@@ -216,14 +216,14 @@ __global__ void k_apply_splits(DevMesh m, DevCands c, u32 n, u32 batch, u32 roun
 void launch_plan_ops(const DevMesh& m, DevCands c, u32 n, u64 depth_cap, InsertBufs b,
                      Counters* d_ctr, cudaStream_t st) {
     if (!n) return;
-    k_plan_ops<<<(n + 255) / 256, 256, 0, st>>>(m, c, n, depth_cap, b, d_ctr);
+    note_launch(), k_plan_ops<<<(n + 255) / 256, 256, 0, st>>>(m, c, n, depth_cap, b, d_ctr);
 }
 
 void launch_apply_splits(const DevMesh& m, DevCands c, u32 n, u32 batch, u32 round,
                          InsertBufs b, TriAux a, FreshInfo f, WorkLists w, Counters* d_ctr,
                          cudaStream_t st) {
     if (!n) return;
-    k_apply_splits<<<(n + 255) / 256, 256, 0, st>>>(m, c, n, batch, round, b, a, f, w, d_ctr);
+    note_launch(), k_apply_splits<<<(n + 255) / 256, 256, 0, st>>>(m, c, n, batch, round, b, a, f, w, d_ctr);
 }
 
 // ---- phase B ------------------------------------------------------------------------
@@ -274,7 +274,7 @@ __global__ void k_fixup(DevMesh m, u32 round, TriAux x, WorkLists w, u32 n_bound
 void launch_fixup(const DevMesh& m, u32 round, TriAux a, WorkLists w, u32 n_bound,
                   bool seed_all_edges, u32 widx, Counters* d_ctr, cudaStream_t st) {
     if (!n_bound) return;
-    k_fixup<<<(n_bound + 255) / 256, 256, 0, st>>>(m, round, a, w, n_bound,
+    note_launch(), k_fixup<<<(n_bound + 255) / 256, 256, 0, st>>>(m, round, a, w, n_bound,
                                                    seed_all_edges ? 1 : 0, widx, d_ctr);
 }
 
@@ -384,11 +384,11 @@ void launch_flip_round(const DevMesh& m, u32 round, TriAux a, WorkLists w, u32 c
                        Counters* d_ctr, cudaStream_t st) {
     if (!n) return;
     const u32 g = (n + 255) / 256;
-    k_flip_test<<<g, 256, 0, st>>>(m, w.w[cur], n, a, w, d_ctr);
-    k_flip_apply<<<g, 256, 0, st>>>(m, n, round, cur ^ 1u, a, w, d_ctr);
-    k_flip_post<<<g, 256, 0, st>>>(n, round, cur ^ 1u, a, w, d_ctr);
+    note_launch(), k_flip_test<<<g, 256, 0, st>>>(m, w.w[cur], n, a, w, d_ctr);
+    note_launch(), k_flip_apply<<<g, 256, 0, st>>>(m, n, round, cur ^ 1u, a, w, d_ctr);
+    note_launch(), k_flip_post<<<g, 256, 0, st>>>(n, round, cur ^ 1u, a, w, d_ctr);
     const u32 nt = 2 * n;
-    k_fixup<<<(nt + 255) / 256, 256, 0, st>>>(m, round, a, w, nt, 0, 0, d_ctr);
+    note_launch(), k_fixup<<<(nt + 255) / 256, 256, 0, st>>>(m, round, a, w, nt, 0, 0, d_ctr);
 }
 
 // ---- redundancy detection (refine.hpp:551-608) ----------------------------------------
@@ -468,7 +468,7 @@ __global__ void k_detect_b(DevMesh m, u32 V0, u32 F, FreshInfo f, Counters* ctr)
         const u32 x = comp(m.tv[st[q]], nxt(si[q]));
         if (x < V0 || x >= V0 + F) continue;
         const u32 jx = x - V0;
-        if (!f.cc[jx] || f.removed[jx] || f.mark[jx] == 1) continue;
+        if (!f.cc[jx] || f.removed[jx] == 1 || f.mark[jx] == 1) continue;
         if (prio_gt(f, jx, j)) {
             f.mark[j] = 2;
             break;
@@ -494,11 +494,11 @@ void launch_detect(const DevMesh& m, const Quality& q, u64 depth_cap, u32 V0, u3
     if (!F) return;
     const u32 g = (F + 127) / 128;
     if (q.mode == 0)
-        k_detect_a<0><<<g, 128, 0, st>>>(m, depth_cap, V0, F, f, d_ctr);
+        note_launch(), k_detect_a<0><<<g, 128, 0, st>>>(m, depth_cap, V0, F, f, d_ctr);
     else
-        k_detect_a<1><<<g, 128, 0, st>>>(m, depth_cap, V0, F, f, d_ctr);
-    k_detect_b<<<g, 128, 0, st>>>(m, V0, F, f, d_ctr);
-    k_detect_collect<<<g, 128, 0, st>>>(V0, F, f, w, d_ctr);
+        note_launch(), k_detect_a<1><<<g, 128, 0, st>>>(m, depth_cap, V0, F, f, d_ctr);
+    note_launch(), k_detect_b<<<g, 128, 0, st>>>(m, V0, F, f, d_ctr);
+    note_launch(), k_detect_collect<<<g, 128, 0, st>>>(V0, F, f, w, d_ctr);
 }
 
 // ---- parallel vertex removal (remove_free_vertex + flop, mesh.hpp:261-304,442-466) ----
@@ -627,7 +627,11 @@ __global__ void __launch_bounds__(64) k_rm_apply(DevMesh m, const u32* __restric
                 ok = orient2d(m.xy[L[a]], m.xy[L[b]], m.xy[L[c]]) > 0;
             }
             if (!ok) {
-                raise_err(ctr, DERR_NO_EAR, v);
+                // No flippable incident edge (degenerate star): like
+                // remove_free_vertex returning false (mesh.hpp:462), keep the
+                // vertex; it is never selected again.
+                f.removed[v - V0] = 2;
+                atomicAdd(&ctr->rm_kept, 1u);
             } else {
                 for (int q = 0; q < k; ++q) x.stamp[st[q]] = round;
                 for (int ci = 0; ci < created; ++ci) {
@@ -668,12 +672,12 @@ void launch_removal_round(const DevMesh& m, u32 round, u32 V0, TriAux a, FreshIn
                           WorkLists w, u32 cur, u32 n, u32 widx, Counters* d_ctr,
                           cudaStream_t st) {
     if (!n) return;
-    k_rm_claim<<<(n + 127) / 128, 128, 0, st>>>(m, w.rm[cur], n, a, w, d_ctr);
-    k_rm_apply<<<(n + 63) / 64, 64, 0, st>>>(m, w.rm[cur], n, round, V0, widx, cur ^ 1u, a, f, w,
+    note_launch(), k_rm_claim<<<(n + 127) / 128, 128, 0, st>>>(m, w.rm[cur], n, a, w, d_ctr);
+    note_launch(), k_rm_apply<<<(n + 63) / 64, 64, 0, st>>>(m, w.rm[cur], n, round, V0, widx, cur ^ 1u, a, f, w,
                                             d_ctr);
-    k_rm_post<<<(n + 255) / 256, 256, 0, st>>>(n, a, w);
+    note_launch(), k_rm_post<<<(n + 255) / 256, 256, 0, st>>>(n, a, w);
     const u32 nt = n * (MAX_STAR - 2);
-    k_fixup<<<(nt + 255) / 256, 256, 0, st>>>(m, round, a, w, nt, 0, 0, d_ctr);
+    note_launch(), k_fixup<<<(nt + 255) / 256, 256, 0, st>>>(m, round, a, w, nt, 0, 0, d_ctr);
 }
 
 }  // namespace gdp2d

@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(256) k_locate(DevMesh m, DevCands c, u32 n, Co
 
 void launch_locate(const DevMesh& m, DevCands c, u32 n, Counters* d_ctr, cudaStream_t st) {
     if (!n) return;
-    k_locate<<<(n + 255) / 256, 256, 0, st>>>(m, c, n, d_ctr);
+    note_launch(), k_locate<<<(n + 255) / 256, 256, 0, st>>>(m, c, n, d_ctr);
 }
 
 }  // namespace gdp2d

@@ -44,12 +44,12 @@ __global__ void k_decode_nbrs(DevMesh m, u32* __restrict__ plain) {
 
 void launch_encode_neighbors(DevMesh m, const u32* plain_n, cudaStream_t st) {
     if (!m.nT) return;
-    k_encode_nbrs<<<(m.nT + 255) / 256, 256, 0, st>>>(m, plain_n);
+    note_launch(), k_encode_nbrs<<<(m.nT + 255) / 256, 256, 0, st>>>(m, plain_n);
 }
 
 void launch_decode_neighbors(const DevMesh& m, u32* plain_n, cudaStream_t st) {
     if (!m.nT) return;
-    k_decode_nbrs<<<(m.nT + 255) / 256, 256, 0, st>>>(m, plain_n);
+    note_launch(), k_decode_nbrs<<<(m.nT + 255) / 256, 256, 0, st>>>(m, plain_n);
 }
 
 // ---- predicate batches ------------------------------------------------------------
@@ -83,11 +83,11 @@ void launch_predicates(int kind, const double* pts, u32 n, const Quality& q, int
     const u32 g = (n + 127) / 128;
     const double2* p = reinterpret_cast<const double2*>(pts);
     switch (kind) {
-        case 0: k_predicates<0><<<g, 128, 0, st>>>(p, n, q, out); break;
-        case 1: k_predicates<1><<<g, 128, 0, st>>>(p, n, q, out); break;
-        case 2: k_predicates<2><<<g, 128, 0, st>>>(p, n, q, out); break;
-        case 3: k_predicates<3><<<g, 128, 0, st>>>(p, n, q, out); break;
-        default: k_predicates<4><<<g, 128, 0, st>>>(p, n, q, out); break;
+        case 0: note_launch(), k_predicates<0><<<g, 128, 0, st>>>(p, n, q, out); break;
+        case 1: note_launch(), k_predicates<1><<<g, 128, 0, st>>>(p, n, q, out); break;
+        case 2: note_launch(), k_predicates<2><<<g, 128, 0, st>>>(p, n, q, out); break;
+        case 3: note_launch(), k_predicates<3><<<g, 128, 0, st>>>(p, n, q, out); break;
+        default: note_launch(), k_predicates<4><<<g, 128, 0, st>>>(p, n, q, out); break;
     }
 }
 
@@ -102,7 +102,7 @@ __global__ void k_circumcenters(const double2* __restrict__ pts, u32 n, double2*
 
 void launch_circumcenters(const double* pts, u32 n, double* out, uint8_t* ok, cudaStream_t st) {
     if (!n) return;
-    k_circumcenters<<<(n + 255) / 256, 256, 0, st>>>(reinterpret_cast<const double2*>(pts), n,
+    note_launch(), k_circumcenters<<<(n + 255) / 256, 256, 0, st>>>(reinterpret_cast<const double2*>(pts), n,
                                                      reinterpret_cast<double2*>(out), ok);
 }
 
@@ -180,8 +180,8 @@ QualitySummary launch_quality(const DevMesh& m, const Quality& q, void* scratch,
     h.max_edge_bits = 0;
     QAcc* d = reinterpret_cast<QAcc*>(scratch);
     cudaMemcpyAsync(d, &h, sizeof h, cudaMemcpyHostToDevice, st);
-    if (m.nT) k_quality_tris<<<(m.nT + 255) / 256, 256, 0, st>>>(m, q, d);
-    if (m.nV) k_quality_verts<<<(m.nV + 255) / 256, 256, 0, st>>>(m, d);
+    if (m.nT) note_launch(), k_quality_tris<<<(m.nT + 255) / 256, 256, 0, st>>>(m, q, d);
+    if (m.nV) note_launch(), k_quality_verts<<<(m.nV + 255) / 256, 256, 0, st>>>(m, d);
     cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
     QualitySummary s;

@@ -50,7 +50,7 @@ __global__ void k_tile_scan(const u32* __restrict__ in, u32 n, const u32* __rest
 }
 
 void scan_partials(u32* partial, u32 ntiles, u32* d_total, cudaStream_t st) {
-    k_partial_scan<<<1, SCAN_BLOCK, 0, st>>>(partial, ntiles, d_total);
+    note_launch(), k_partial_scan<<<1, SCAN_BLOCK, 0, st>>>(partial, ntiles, d_total);
 }
 
 void scan_exclusive(const u32* in, u32* out, u32 n, u32* d_total, ScanScratch& s,
@@ -65,9 +65,9 @@ void scan_exclusive(const u32* in, u32* out, u32 n, u32* d_total, ScanScratch& s
         s.cap = tiles * 2;
         cudaMalloc(&s.partial, sizeof(u32) * s.cap);
     }
-    k_tile_reduce<<<tiles, SCAN_BLOCK, 0, st>>>(in, n, s.partial);
-    k_partial_scan<<<1, SCAN_BLOCK, 0, st>>>(s.partial, tiles, d_total);
-    k_tile_scan<<<tiles, SCAN_BLOCK, 0, st>>>(in, n, s.partial, out);
+    note_launch(), k_tile_reduce<<<tiles, SCAN_BLOCK, 0, st>>>(in, n, s.partial);
+    note_launch(), k_partial_scan<<<1, SCAN_BLOCK, 0, st>>>(s.partial, tiles, d_total);
+    note_launch(), k_tile_scan<<<tiles, SCAN_BLOCK, 0, st>>>(in, n, s.partial, out);
 }
 
 }  // namespace gdp2d

@@ -126,6 +126,10 @@ class RunReport:
     iteration_cap_hit: bool = False
     device_seconds: float = 0.0
     totals: dict = field(default_factory=dict)
+    scan_seconds: float = 0.0
+    scan_bytes: int = 0
+    scan_launches: int = 0
+    kernel_launches: int = 0
 
     def algorithmic_bytes(self) -> int:
         """SURVEY §8(d) bytes_alg from the per-batch counters."""
@@ -159,7 +163,9 @@ def _report(r: A.Report, arr) -> RunReport:
                      bad_area_percent=r.bad_area_percent, min_angle_deg=r.min_angle_deg,
                      max_edge=r.max_edge, wall_seconds=r.wall_seconds,
                      iteration_cap_hit=bool(r.iteration_cap_hit), device_seconds=r.device_seconds,
-                     totals={k: getattr(r, k) for k in _TOTALS})
+                     totals={k: getattr(r, k) for k in _TOTALS}, scan_seconds=r.scan_seconds,
+                     scan_bytes=r.scan_bytes, scan_launches=r.scan_launches,
+                     kernel_launches=r.kernel_launches)
 
 
 def _new_report(cap: int = 20000):
