@@ -36,6 +36,8 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
+from paper_2007_00324_b200.replicas import Dist, assign, dist_env, replica_seed  # noqa: E402
+
 METRIC = "Refine wall-time (s) & Steiner pts/sec on 1 B200 vs CPU ref on host cores"
 UNIT = "Steiner pts/s"
 B_THETA = math.degrees(math.asin(1.0 / (2.0 * math.sqrt(2.0))))
@@ -52,49 +54,6 @@ CONFIGS = {
             name="cfg5: 2M uniform pts + 10% segs per GPU (replicas), radius-edge<=sqrt2"),
 }
 CPU_SAMPLE = dict(n=250_000, m=25_000)   # bounded CPU-reference sample (~5-10 s)
-
-
-def dist_env():
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return world, rank, local
-
-
-class Dist:
-    def __init__(self, world, rank, local):
-        self.world, self.rank, self.local = world, rank, local
-        self.pg = None
-        if world > 1:
-            import torch
-            import torch.distributed as td
-            torch.cuda.set_device(local)
-            td.init_process_group("nccl", device_id=torch.device("cuda", local))
-            self.td = td
-
-    def barrier(self):
-        if self.world > 1:
-            self.td.barrier()
-
-    def max(self, x: float) -> float:
-        if self.world == 1:
-            return x
-        import torch
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{self.local}")
-        self.td.all_reduce(t, op=self.td.ReduceOp.MAX)
-        return float(t.item())
-
-    def sum(self, x: float) -> float:
-        if self.world == 1:
-            return x
-        import torch
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{self.local}")
-        self.td.all_reduce(t, op=self.td.ReduceOp.SUM)
-        return float(t.item())
-
-    def close(self):
-        if self.world > 1:
-            self.td.destroy_process_group()
 
 
 class ClockSampler:
@@ -237,18 +196,26 @@ def main():
     torch.cuda.set_device(device)
     cfg = CONFIGS[a.config]
     q = QualityCriteria(cfg["theta"])
-    seed = 20261017 + rank
+    # config 5: a batch of 8 independent PSLGs spread round-robin over the
+    # ranks; otherwise one PSLG per rank (weak scaling)
+    items = assign(8, world, rank) if a.config == 5 else [0]
     t0 = time.time()
-    mesh = make_workload(cfg, seed)
+    meshes = [make_workload(cfg, replica_seed(20261017, rank if a.config != 5 else 0, it))
+              for it in items]
     setup_s = time.time() - t0
+    mesh = meshes[0]
     lib = A.engine()
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{device}")  # > 126 MB L2
 
-    eng = Engine(device)
-    eng.upload(mesh)
+    engines = []
+    for mm in meshes:
+        e = Engine(device)
+        e.upload(mm)
+        engines.append(e)
     for _ in range(max(a.warmup, 0)):
-        eng.reset()
-        eng.refine(q)
+        for e in engines:
+            e.reset()
+            e.refine(q)
 
     # ---- timed region: K device-resident steps ----
     reps = []
@@ -259,12 +226,15 @@ def main():
     with ClockSampler(device) as clk:
         host_t0 = time.perf_counter()
         for _ in range(a.steps):
-            flush.zero_()                       # evict L2 between steps
-            torch.cuda.synchronize()
-            eng.reset()
-            rep = eng.refine(q)
-            reps.append(rep)
-            step_ms.append(rep.device_seconds * 1e3)
+            ms = 0.0
+            for e in engines:
+                flush.zero_()                       # evict L2 before every refine
+                torch.cuda.synchronize()
+                e.reset()
+                rep = e.refine(q)
+                reps.append(rep)
+                ms += rep.device_seconds * 1e3
+            step_ms.append(ms)
         torch.cuda.synchronize()
         host_s = time.perf_counter() - host_t0
     launches = lib.gdp2d_kernel_launches() - launches0
@@ -275,21 +245,26 @@ def main():
     steiner_all = dist.sum(steiner_local)
     value = steiner_all / dev_s_max
     last = reps[-1]
+    eng = engines[0]
 
     # ---- e2e: the public C ABI with host buffers ----
     e2e_steps = a.e2e_steps or a.steps
     e2e_s = []
     e2e_st = 0
-    h2d = mesh_bytes(mesh)
+    h2d = sum(mesh_bytes(mm) for mm in meshes)
     d2h = 0
     dist.barrier()
     for _ in range(e2e_steps):
-        m = mesh.copy()
-        t = time.perf_counter()
-        r = refine(m, q)
-        e2e_s.append(time.perf_counter() - t)
-        e2e_st += r.steiner_points
-        d2h = mesh_bytes(m)
+        d2h = 0
+        t_step = 0.0
+        for mm in meshes:
+            m = mm.copy()
+            t = time.perf_counter()
+            r = refine(m, q)          # upload (H2D) + refine + download (D2H)
+            t_step += time.perf_counter() - t
+            e2e_st += r.steiner_points
+            d2h += mesh_bytes(m)
+        e2e_s.append(t_step)
     e2e_total = dist.max(sum(e2e_s))
     e2e_value = dist.sum(e2e_st) / e2e_total
 
@@ -337,7 +312,8 @@ def main():
                                 "seconds": secs[0], "steiner": st[0]}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    eng.close()
+    for e in engines:
+        e.close()
     dist.close()
     return 0
 

@@ -131,7 +131,7 @@ typedef struct gdp2d_batch_metrics {
     uint32_t batch_index;
     uint32_t attempted;          /* candidates entering the batch            */
     uint32_t concurrency;        /* retained insertions (useful work, C)     */
-    uint32_t pad0;
+    uint32_t removals_kept;      /* redundant points whose star had no ear   */
     double   latency;            /* seconds (sum of phases, L)               */
     double   throughput;         /* C / L                                    */
     double   waste_fraction;     /* 1 - useful/attempted                     */
@@ -198,7 +198,9 @@ void gdp2d_params_init(gdp2d_params* p, double theta_deg, double ell, uint32_t m
 
 /* Refine `in` on `device`; writes the refined mesh into *out (library-owned
  * host buffers) and the run report into *r.  Timed scope (r->wall_seconds)
- * covers H2D of the input, every batch and D2H of the result. */
+ * covers H2D of the input, every batch and D2H of the result.  The device
+ * context (HBM buffers, stream) is cached per device and reused by later
+ * calls; concurrent calls on the same device are serialised. */
 int gdp2d_refine(const gdp2d_mesh_view* in, gdp2d_mesh_buf* out, const gdp2d_params* p,
                  gdp2d_report* r, int device);
 
@@ -224,6 +226,14 @@ int  gdp2d_ctx_reset(gdp2d_ctx* ctx);
 /* Refine the working mesh in place (device-resident input and output). */
 int  gdp2d_ctx_refine(gdp2d_ctx* ctx, const gdp2d_params* p, gdp2d_report* r);
 int  gdp2d_ctx_download(gdp2d_ctx* ctx, gdp2d_mesh_buf* out);
+/* Current working-mesh sizes (slots, including dead ones). */
+int  gdp2d_ctx_sizes(gdp2d_ctx* ctx, uint32_t* n_vertices, uint32_t* n_triangles,
+                     uint32_t* n_subsegments);
+/* Download into CALLER-allocated arrays sized from gdp2d_ctx_sizes(); the
+ * pointers in *dst are used as given (nothing is allocated or freed). */
+int  gdp2d_ctx_download_to(gdp2d_ctx* ctx, gdp2d_mesh_buf* dst);
+/* Release the per-device contexts that gdp2d_refine() keeps cached. */
+void gdp2d_release_cached(void);
 /* Bytes of device memory held by the context. */
 uint64_t gdp2d_ctx_device_bytes(gdp2d_ctx* ctx);
 

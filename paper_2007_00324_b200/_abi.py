@@ -48,7 +48,7 @@ class Params(C.Structure):
 
 class BatchMetrics(C.Structure):
     _fields_ = [("batch_index", C.c_uint32), ("attempted", C.c_uint32),
-                ("concurrency", C.c_uint32), ("pad0", C.c_uint32), ("latency", C.c_double),
+                ("concurrency", C.c_uint32), ("removals_kept", C.c_uint32), ("latency", C.c_double),
                 ("throughput", C.c_double), ("waste_fraction", C.c_double),
                 ("phase_seconds", C.c_double * 6), ("tris_alive", C.c_uint64),
                 ("verts_alive", C.c_uint64), ("subsegs_alive", C.c_uint64),
@@ -112,6 +112,10 @@ SIGNATURES = {
     "gdp2d_ctx_refine": (C.c_int, [ctx_p, C.POINTER(Params), C.POINTER(Report)]),
     "gdp2d_ctx_download": (C.c_int, [ctx_p, C.POINTER(MeshBuf)]),
     "gdp2d_ctx_device_bytes": (C.c_uint64, [ctx_p]),
+    "gdp2d_ctx_sizes": (C.c_int, [ctx_p, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
+                                  C.POINTER(C.c_uint32)]),
+    "gdp2d_ctx_download_to": (C.c_int, [ctx_p, C.POINTER(MeshBuf)]),
+    "gdp2d_release_cached": (None, []),
     "gdp2d_collect": (C.c_int, [ctx_p, C.POINTER(Params), C.c_void_p, C.c_uint32,
                                 C.POINTER(C.c_uint32)]),
     "gdp2d_split_points": (C.c_int, [ctx_p, C.c_void_p, C.c_uint32]),

@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -226,6 +227,16 @@ struct gdp2d_ctx {
     u32* h_tot = nullptr;         // pinned [4]
     void* qscratch = nullptr;
     u32 round = 0;
+    bool full_scan = true;        // next collect recomputes every triangle
+    u32 collect_round = 0, collect_nT = 0;
+    bool validate = false;        // GDP2D_VALIDATE=1: check structure after every round
+    bool lawson_rounds = false;   // GDP2D_LAWSON=rounds: per-round launches
+    bool full_collect = false;    // GDP2D_COLLECT=full: never reuse cached flags
+    int lawson_grid = 0;          // persistent Lawson kernel grid (co-resident blocks)
+    RoundCtr* rcs = nullptr;      // per-round counters of the persistent kernel
+    u32* d_res = nullptr;
+    u32* d_val = nullptr;
+    const char* phase = "";
     cudaEvent_t ev[GDP2D_NPHASES + 4];   // phases, loop start/end, scan start/end
     // upload / download staging
     u32* stage_u32[3] = {nullptr, nullptr, nullptr};
@@ -277,9 +288,10 @@ void ensure_aux(gdp2d_ctx* x) {
     const u32 T = x->work.tcap;
     if (T > x->aux_cap) {
         dfree(x->aux.ckey); dfree(x->aux.ctie); dfree(x->aux.owner); dfree(x->aux.stamp);
-        dfree(x->aux.emap);
+        dfree(x->aux.emap); dfree(x->aux.tbad);
         dalloc(x->aux.ckey, T); dalloc(x->aux.ctie, T); dalloc(x->aux.owner, T);
-        dalloc(x->aux.stamp, T); dalloc(x->aux.emap, 3ull * T);
+        dalloc(x->aux.stamp, T); dalloc(x->aux.emap, 3ull * T); dalloc(x->aux.tbad, T);
+        x->full_scan = true;  // stamps restart: the cached flags are unusable
         CK(cudaMemsetAsync(x->aux.ckey, 0, sizeof(u64) * T, x->st));
         CK(cudaMemsetAsync(x->aux.ctie, 0xFF, sizeof(u64) * T, x->st));
         CK(cudaMemsetAsync(x->aux.owner, 0xFF, sizeof(u32) * T, x->st));
@@ -344,20 +356,58 @@ void check_dev_err(gdp2d_ctx* x) {
     CK(cudaMemcpyAsync(x->h_ctr, x->d_ctr, sizeof(Counters), cudaMemcpyDeviceToHost, x->st));
     CK(cudaStreamSynchronize(x->st));
     if (x->h_ctr->err_code) {
-        char buf[160];
-        snprintf(buf, sizeof buf, "device error %u (%s), info %u", x->h_ctr->err_code,
-                 dev_err_name(x->h_ctr->err_code), x->h_ctr->err_info);
+        char buf[512];
+        const double* d = x->h_ctr->dbg;
+        snprintf(buf, sizeof buf,
+                 "device error %u (%s), info %u, dbg [%.17g %.17g %.17g %.17g %.17g %.17g %.17g %.17g]",
+                 x->h_ctr->err_code, dev_err_name(x->h_ctr->err_code), x->h_ctr->err_info, d[0],
+                 d[1], d[2], d[3], d[4], d[5], d[6], d[7]);
         throw Fail{x->h_ctr->err_code == DERR_WORKLIST_OVERFLOW ? GDP2D_ECAPACITY : GDP2D_EMESH,
                    buf};
     }
 }
 
+void validate_now(gdp2d_ctx* x, const char* where) {
+    if (!x->validate) return;
+    launch_validate(x->work.m, x->d_val, x->st);
+    u32 h[4];
+    CK(cudaMemcpyAsync(h, x->d_val, sizeof h, cudaMemcpyDeviceToHost, x->st));
+    CK(cudaStreamSynchronize(x->st));
+    check_dev_err(x);
+    if (h[0]) {
+        char buf[200];
+        snprintf(buf, sizeof buf, "validate after %s (round %u): failure %u at triangle %u edge %d",
+                 where, x->round, h[0], h[1], (int)h[2]);
+        throw Fail{GDP2D_EMESH, buf};
+    }
+}
+
 }  // namespace
 
-// Lawson driver that tracks which buffer holds the live work list.
+// Lawson driver: the persistent cooperative kernel runs every round of the
+// fixpoint in one launch; GDP2D_VALIDATE=1 (or GDP2D_LAWSON=rounds) uses one
+// launch sequence per round so the structure can be checked in between.
 static void lawson_from(gdp2d_ctx* x, u32 start_buf, u32 n, u32* rounds) {
     u32 cur = start_buf;
     u32 guard = 0;
+    if (!x->validate && !x->lawson_rounds) {
+        constexpr u32 kMax = 1024;
+        while (n > 0) {
+            if (n > x->wl.cap) throw Fail{GDP2D_ECAPACITY, "Lawson work list overflow"};
+            if (++guard > 1000) throw Fail{GDP2D_EMESH, "Lawson flip rounds did not converge"};
+            CK(cudaMemsetAsync(x->rcs, 0, sizeof(RoundCtr) * kMax, x->st));
+            launch_lawson_persistent(x->work.m, x->round + 1, cur, n, kMax, x->aux, x->wl, x->rcs,
+                                     x->d_res, x->d_ctr, x->lawson_grid, x->st);
+            CK(cudaGetLastError());
+            CK(cudaMemcpyAsync(x->h_tot, x->d_res, 3 * sizeof(u32), cudaMemcpyDeviceToHost, x->st));
+            CK(cudaStreamSynchronize(x->st));
+            x->round += x->h_tot[0];
+            if (rounds) *rounds += x->h_tot[0];
+            cur = x->h_tot[1];
+            n = x->h_tot[2];
+        }
+        return;
+    }
     while (n > 0) {
         if (n > x->wl.cap) throw Fail{GDP2D_ECAPACITY, "Lawson work list overflow"};
         if (++guard > 200000) throw Fail{GDP2D_EMESH, "Lawson flip rounds did not converge"};
@@ -369,6 +419,7 @@ static void lawson_from(gdp2d_ctx* x, u32 start_buf, u32 n, u32* rounds) {
         n = rc.wl_next;
         cur ^= 1u;
         if (rounds) ++*rounds;
+        validate_now(x, "flip round");
     }
 }
 
@@ -392,6 +443,18 @@ void ctx_init(gdp2d_ctx* x, int device) {
     CK(cudaMallocHost(&x->h_rc, sizeof(RoundCtr)));
     CK(cudaMallocHost(&x->h_tot, 4 * sizeof(u32)));
     CK(cudaMalloc(&x->qscratch, 256));
+    dalloc(x->d_val, 4);
+    dalloc(x->wl.dbg, 4 + 2 * MAX_STAR);
+    CK(cudaMemsetAsync(x->wl.dbg, 0, sizeof(double) * (4 + 2 * MAX_STAR), x->st));
+    const char* ev = std::getenv("GDP2D_VALIDATE");
+    x->validate = ev && ev[0] == '1';
+    const char* lr = std::getenv("GDP2D_LAWSON");
+    x->lawson_rounds = lr && std::string(lr) == "rounds";
+    x->lawson_grid = lawson_persistent_grid(device);
+    const char* fc = std::getenv("GDP2D_COLLECT");
+    x->full_collect = fc && std::string(fc) == "full";
+    dalloc(x->rcs, 1024);
+    dalloc(x->d_res, 4);
     for (auto& e : x->ev) CK(cudaEventCreate(&e));
 }
 
@@ -400,7 +463,7 @@ void ctx_release(gdp2d_ctx* x) {
     mesh_free(x->work);
     mesh_free(x->pristine);
     dfree(x->aux.ckey); dfree(x->aux.ctie); dfree(x->aux.owner); dfree(x->aux.stamp);
-    dfree(x->aux.emap); dfree(x->flags);
+    dfree(x->aux.emap); dfree(x->aux.tbad); dfree(x->flags);
     cands_free(x->c);
     dfree(x->regions); dfree(x->region_len); dfree(x->bfs_len);
     dfree(x->ib.nv); dfree(x->ib.nt); dfree(x->ib.ns); dfree(x->ib.ov); dfree(x->ib.ot);
@@ -418,6 +481,10 @@ void ctx_release(gdp2d_ctx* x) {
     if (x->h_rc) cudaFreeHost(x->h_rc);
     if (x->h_tot) cudaFreeHost(x->h_tot);
     if (x->qscratch) cudaFree(x->qscratch);
+    dfree(x->d_val);
+    dfree(x->wl.dbg);
+    dfree(x->rcs);
+    dfree(x->d_res);
     for (auto& e : x->ev)
         if (e) cudaEventDestroy(e);
     if (x->st) cudaStreamDestroy(x->st);
@@ -507,17 +574,50 @@ void reset_work(gdp2d_ctx* x) {
     x->alive_t = x->p_alive_t;
     x->alive_s = x->p_alive_s;
     ensure_aux(x);
+    x->full_scan = true;
+}
+
+// Copy the working mesh into host arrays already present in *b.
+void download_into(gdp2d_ctx* x, gdp2d_mesh_buf* b) {
+    const DevMesh& m = x->work.m;
+    const u32 V = m.nV, T = m.nT, S = m.nS;
+    cudaStream_t st = x->st;
+    b->n_vertices = V;
+    b->n_triangles = T;
+    b->n_subsegments = S;
+    b->batch_epoch = x->epoch;
+    ensure_stage(x, std::max<size_t>(3ull * T, 2ull * S) + T + S + 16);
+    if (V) {
+        CK(cudaMemcpyAsync(b->xy, m.xy, 16ull * V, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(b->vert_kind, m.vkind, V, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(b->vert_birth, m.vbirth, 4ull * V, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(b->vert_alive, m.valive, V, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(b->vert_tri, m.vtri, 4ull * V, cudaMemcpyDeviceToHost, st));
+    }
+    if (T) {
+        note_launch(), k_unpack_tris<<<grid(T), 256, 0, st>>>(m, x->stage_u32[0], x->stage_u32[1], x->stage_u8);
+        launch_decode_neighbors(m, x->stage_u32[2], st);
+        CK(cudaMemcpyAsync(b->tri_v, x->stage_u32[0], 12ull * T, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(b->tri_seg, x->stage_u32[1], 12ull * T, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(b->tri_n, x->stage_u32[2], 12ull * T, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(b->tri_alive, x->stage_u8, T, cudaMemcpyDeviceToHost, st));
+    }
+    if (S) {
+        CK(cudaMemcpyAsync(b->seg_v, m.sv, 8ull * S, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(b->seg_parent, m.sparent, 4ull * S, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(b->seg_alive, m.salive, S, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(b->seg_tri, m.stri, 4ull * S, cudaMemcpyDeviceToHost, st));
+        note_launch(), k_u32_to_u8<<<grid(S), 256, 0, st>>>(m.senc, x->stage_u8 + T + 8, S);
+        CK(cudaMemcpyAsync(b->seg_encroached, x->stage_u8 + T + 8, S, cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaStreamSynchronize(st));
+    CK(cudaGetLastError());
 }
 
 void download(gdp2d_ctx* x, gdp2d_mesh_buf* b) {
     const DevMesh& m = x->work.m;
     const u32 V = m.nV, T = m.nT, S = m.nS;
-    cudaStream_t st = x->st;
     std::memset(b, 0, sizeof *b);
-    b->n_vertices = V;
-    b->n_triangles = T;
-    b->n_subsegments = S;
-    b->batch_epoch = x->epoch;
     auto hm = [](size_t bytes) { return std::malloc(bytes ? bytes : 1); };
     b->xy = (double*)hm(16ull * V);
     b->vert_kind = (uint8_t*)hm(V);
@@ -533,31 +633,7 @@ void download(gdp2d_ctx* x, gdp2d_mesh_buf* b) {
     b->seg_encroached = (uint8_t*)hm(S);
     b->seg_alive = (uint8_t*)hm(S);
     b->seg_tri = (u32*)hm(4ull * S);
-    ensure_stage(x, std::max<size_t>(3ull * T, 2ull * S) + 16);
-    CK(cudaMemcpyAsync(b->xy, m.xy, 16ull * V, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(b->vert_kind, m.vkind, V, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(b->vert_birth, m.vbirth, 4ull * V, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(b->vert_alive, m.valive, V, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(b->vert_tri, m.vtri, 4ull * V, cudaMemcpyDeviceToHost, st));
-    if (T) {
-        note_launch(), k_unpack_tris<<<grid(T), 256, 0, st>>>(m, x->stage_u32[0], x->stage_u32[1], x->stage_u8);
-        launch_decode_neighbors(m, x->stage_u32[2], st);
-        CK(cudaMemcpyAsync(b->tri_v, x->stage_u32[0], 12ull * T, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(b->tri_seg, x->stage_u32[1], 12ull * T, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(b->tri_n, x->stage_u32[2], 12ull * T, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(b->tri_alive, x->stage_u8, T, cudaMemcpyDeviceToHost, st));
-    }
-    if (S) {
-        CK(cudaStreamSynchronize(st));  // stage_u8 reused below
-        CK(cudaMemcpyAsync(b->seg_v, m.sv, 8ull * S, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(b->seg_parent, m.sparent, 4ull * S, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(b->seg_alive, m.salive, S, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(b->seg_tri, m.stri, 4ull * S, cudaMemcpyDeviceToHost, st));
-        note_launch(), k_u32_to_u8<<<grid(S), 256, 0, st>>>(m.senc, x->stage_u8, S);
-        CK(cudaMemcpyAsync(b->seg_encroached, x->stage_u8, S, cudaMemcpyDeviceToHost, st));
-    }
-    CK(cudaStreamSynchronize(st));
-    CK(cudaGetLastError());
+    download_into(x, b);
 }
 
 double ev_ms(cudaEvent_t a, cudaEvent_t b) {
@@ -594,13 +670,31 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
         CK(cudaMemsetAsync(x->d_ctr, 0, sizeof(Counters), st));
         ensure_cands(x, m.nS + m.nT);
         CK(cudaEventRecord(x->ev[0], st));
+        CollectCache cache;
+        cache.stamp = x->aux.stamp;
+        cache.tbad = x->aux.tbad;
+        cache.last_round = x->collect_round;
+        cache.nT_last = x->collect_nT;
+        cache.full = (x->full_scan || x->full_collect) ? 1 : 0;
         const u32 C = launch_collect(m, q, p->rule4_unified_collection != 0, x->flags, x->c,
-                                     x->ccap, x->scan, x->d_ctr, st, x->ev[GDP2D_NPHASES + 2],
-                                     x->ev[GDP2D_NPHASES + 3]);
+                                     x->ccap, x->scan, x->d_ctr, st, cache,
+                                     x->ev[GDP2D_NPHASES + 2], x->ev[GDP2D_NPHASES + 3]);
+        x->full_scan = false;
+        x->collect_round = x->round;
+        x->collect_nT = m.nT;
         CK(cudaGetLastError());
         // launch_collect synchronised: the scan events are complete
         r->scan_seconds += ev_ms(x->ev[GDP2D_NPHASES + 2], x->ev[GDP2D_NPHASES + 3]) * 1e-3;
-        r->scan_bytes += 16ull * m.nT + 16ull * m.nV + 48ull * m.nS;
+        {
+            // bytes the scan must move: 5 B per clean triangle (stamp + cached
+            // flag), 16 B record + 3 x 16 B corners + 5 B per re-evaluated one,
+            // 48 B per subsegment (SURVEY 8(d) per-unit figure)
+            CK(cudaMemcpyAsync(&x->h_tot[3], &x->d_ctr->scan_dirty, sizeof(u32),
+                               cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            const u64 dirty = x->h_tot[3];
+            r->scan_bytes += 5ull * m.nT + 64ull * dirty + 48ull * m.nS;
+        }
         r->scan_launches += 1;
         if (C == 0) break;
         CK(cudaEventRecord(x->ev[1], st));   // split points are fused into collect
@@ -637,6 +731,7 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
             mm.nS += ns;
             launch_fixup(mm, x->round, x->aux, x->wl, 4 * nv, true, 0, x->d_ctr, st);
             RoundCtr rc = read_rc(x);
+            validate_now(x, "splits");
             lawson_from(x, 0, rc.wl_next, &flip_rounds);
             // Phase 3: redundant-point removal to fixpoint (refine.hpp:551-608).
             for (;;) {
@@ -656,6 +751,7 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
                     rc = read_rc(x);
                     ++rm_rounds;
                     check_dev_err(x);
+                    validate_now(x, "removal round");
                     lawson_from(x, 0, rc.wl_next, &flip_rounds);
                     nrm = rc.rm_next;
                     cur ^= 1u;
@@ -698,6 +794,7 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
         bm.flips = h.flips;
         bm.flip_rounds = flip_rounds;
         bm.removal_rounds = rm_rounds;
+        bm.removals_kept = h.rm_kept;
         if (r->batches && r->n_batches < r->batches_capacity) r->batches[r->n_batches] = bm;
         r->n_batches++;
         r->total_candidates += C;
@@ -713,6 +810,16 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
     }
     CK(cudaEventRecord(x->ev[GDP2D_NPHASES], st));
     CK(cudaEventSynchronize(x->ev[GDP2D_NPHASES]));
+    if (const char* dbg = std::getenv("GDP2D_DEBUG"); dbg && dbg[0] == '1') {
+        double h[4 + 2 * MAX_STAR];
+        CK(cudaMemcpy(h, x->wl.dbg, sizeof h, cudaMemcpyDeviceToHost));
+        if (h[0] != 0.0) {
+            fprintf(stderr, "gdp2d debug: kept removal k=%d v=(%.17g, %.17g) link:", (int)h[1], h[2], h[3]);
+            for (int q = 0; q < (int)h[1] && q < MAX_STAR; ++q)
+                fprintf(stderr, " (%.17g, %.17g)", h[4 + 2 * q], h[5 + 2 * q]);
+            fprintf(stderr, "\n");
+        }
+    }
     r->device_seconds = ev_ms(x->ev[GDP2D_NPHASES + 1], x->ev[GDP2D_NPHASES]) * 1e-3;
     r->kernel_launches = gdp2d::launch_counter() - launches0;
     r->wall_seconds =
@@ -815,6 +922,10 @@ void download_cands(gdp2d_ctx* x, gdp2d_candidate* c, u32 n) {
         c[i].fallback = fb[i];
     }
 }
+
+constexpr int kMaxDevices = 64;
+std::mutex g_cache_mu[kMaxDevices];
+gdp2d_ctx* g_cache[kMaxDevices] = {};
 
 struct DeviceGuard {
     int prev = -1;
@@ -932,11 +1043,15 @@ uint64_t gdp2d_ctx_device_bytes(gdp2d_ctx* x) {
 int gdp2d_refine(const gdp2d_mesh_view* in, gdp2d_mesh_buf* out, const gdp2d_params* p,
                  gdp2d_report* r, int device) {
     if (!in || !out || !p || !r) return GDP2D_EINVAL;
+    if (device < 0 || device >= kMaxDevices) return GDP2D_ENODEVICE;
     const auto t0 = std::chrono::steady_clock::now();
-    gdp2d_ctx* x = nullptr;
-    int rc = gdp2d_ctx_create(&x, device);
-    if (rc) return rc;
-    rc = run_guarded([&] {
+    std::lock_guard<std::mutex> lock(g_cache_mu[device]);
+    if (!g_cache[device]) {
+        const int rc = gdp2d_ctx_create(&g_cache[device], device);
+        if (rc) return rc;
+    }
+    gdp2d_ctx* x = g_cache[device];
+    return run_guarded([&] {
         DeviceGuard g(x->device);
         upload(x, in);
         reset_work(x);
@@ -947,8 +1062,28 @@ int gdp2d_refine(const gdp2d_mesh_view* in, gdp2d_mesh_buf* out, const gdp2d_par
         fill_summary(x, p, r);
         r->wall_seconds = wall;
     });
-    gdp2d_ctx_destroy(x);
-    return rc;
+}
+
+void gdp2d_release_cached(void) {
+    for (int d = 0; d < kMaxDevices; ++d) {
+        std::lock_guard<std::mutex> lock(g_cache_mu[d]);
+        if (g_cache[d]) gdp2d_ctx_destroy(g_cache[d]);
+        g_cache[d] = nullptr;
+    }
+}
+
+int gdp2d_ctx_sizes(gdp2d_ctx* x, uint32_t* v, uint32_t* t, uint32_t* s) {
+    if (!x || !v || !t || !s) return GDP2D_EINVAL;
+    *v = x->work.m.nV;
+    *t = x->work.m.nT;
+    *s = x->work.m.nS;
+    return GDP2D_OK;
+}
+
+int gdp2d_ctx_download_to(gdp2d_ctx* x, gdp2d_mesh_buf* dst) {
+    if (!x || !dst) return GDP2D_EINVAL;
+    DeviceGuard g(x->device);
+    return run_guarded([&] { download_into(x, dst); });
 }
 
 void gdp2d_free(gdp2d_mesh_buf* b) {
@@ -969,8 +1104,12 @@ int gdp2d_collect(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_candidate* out, uin
         DevMesh& m = x->work.m;
         ensure_cands(x, m.nS + m.nT);
         CK(cudaMemsetAsync(x->d_ctr, 0, sizeof(Counters), x->st));
+        CollectCache cache;
+        cache.stamp = x->aux.stamp;
+        cache.tbad = x->aux.tbad;
+        cache.full = 1;
         const u32 C = launch_collect(m, make_quality(p), p->rule4_unified_collection != 0,
-                                     x->flags, x->c, x->ccap, x->scan, x->d_ctr, x->st);
+                                     x->flags, x->c, x->ccap, x->scan, x->d_ctr, x->st, cache);
         *n = C;
         if (C > cap) {
             status = GDP2D_ECAPACITY;

@@ -39,7 +39,7 @@ struct TriAux {
     u32* owner = nullptr;    // flip / removal claim
     u32* stamp = nullptr;    // round in which the triangle was rewritten
     u32* emap = nullptr;     // 3 per triangle: old edge slot -> new (tri<<2|edge)
-    uint8_t* flag = nullptr; // collect flags (S + T)
+    uint8_t* tbad = nullptr; // cached is_bad && resolvable per triangle (incremental collect)
 };
 
 struct CollectBufs {
@@ -52,9 +52,17 @@ struct CollectBufs {
 // collect + fused compute_splitting_points (refine.hpp:226-296).  Returns the
 // candidate count (synchronises).  If rule4 == false and subsegment
 // candidates exist, triangles are skipped (refine.hpp:239).
+struct CollectCache {
+    const u32* stamp = nullptr;   // TriAux::stamp
+    uint8_t* tbad = nullptr;      // cached per-triangle flag
+    u32 last_round = 0;           // round id at the previous collect
+    u32 nT_last = 0;              // triangle count at the previous collect
+    int full = 1;                 // 1 = recompute every triangle
+};
 u32 launch_collect(const DevMesh& m, const Quality& q, bool rule4, uint8_t* flags, DevCands c,
                    u32 ccap, ScanScratch& s, Counters* d_ctr, cudaStream_t st,
-                   cudaEvent_t ev_scan0 = nullptr, cudaEvent_t ev_scan1 = nullptr);
+                   const CollectCache& cache, cudaEvent_t ev_scan0 = nullptr,
+                   cudaEvent_t ev_scan1 = nullptr);
 void launch_split_points(const DevMesh& m, DevCands c, u32 n, Counters* d_ctr, cudaStream_t st);
 void launch_locate(const DevMesh& m, DevCands c, u32 n, Counters* d_ctr, cudaStream_t st);
 void launch_claim(const DevMesh& m, DevCands c, u32 n, TriAux a, Counters* d_ctr,
@@ -98,6 +106,7 @@ struct WorkLists {
     u32 cap = 0;                      // capacity of w / fc / touched
     u32 rm_cap = 0;
     RoundCtr* rc = nullptr;           // device round counters
+    double* dbg = nullptr;            // debug dump: [0]=flag, [1]=k, [2..3]=v, then link xy
 };
 
 void launch_plan_ops(const DevMesh& m, DevCands c, u32 n, u64 depth_cap, InsertBufs b,
@@ -115,6 +124,14 @@ void launch_fixup(const DevMesh& m, u32 round, TriAux a, WorkLists w, u32 n_boun
 // caller zeroes w.rc before the round.
 void launch_flip_round(const DevMesh& m, u32 round, TriAux a, WorkLists w, u32 cur, u32 n,
                        Counters* d_ctr, cudaStream_t st);
+// The whole Lawson fixpoint as one persistent cooperative kernel (see
+// k_insert.cu).  result[0..2] = rounds run, list buffer holding the remaining
+// work, remaining work count.
+constexpr int LAWSON_BLOCK = 256;
+int lawson_persistent_grid(int device);
+void launch_lawson_persistent(const DevMesh& m, u32 round0, u32 cur0, u32 n0, u32 max_rounds,
+                              TriAux a, WorkLists w, RoundCtr* rcs, u32* result, Counters* d_ctr,
+                              int grid, cudaStream_t st);
 // Redundancy detection (refine.hpp:551-608): fills w.rm[0], count in w.rc->detect.
 void launch_detect(const DevMesh& m, const Quality& q, u64 depth_cap, u32 V0, u32 F,
                    FreshInfo f, WorkLists w, Counters* d_ctr, cudaStream_t st);
@@ -131,6 +148,9 @@ struct QualitySummary {
 };
 QualitySummary launch_quality(const DevMesh& m, const Quality& q, void* scratch,
                               cudaStream_t st);
+
+// Debug structural validator (out: 4 u32 device words).
+void launch_validate(const DevMesh& m, u32* out, cudaStream_t st);
 
 // Upload helpers.
 void launch_encode_neighbors(DevMesh m, const u32* plain_n, cudaStream_t st);

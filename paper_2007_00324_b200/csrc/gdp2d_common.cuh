@@ -93,6 +93,8 @@ struct Counters {
     u32 err_info;
     u32 fallbacks;
     u32 rm_kept;        // removals abandoned (degenerate star)
+    u32 scan_dirty;     // triangles re-evaluated by the collect scan
+    double dbg[8];      // coordinates attached to the first device error
 };
 
 // Per-round work-list counters (zeroed by the host before every round).

@@ -17,16 +17,25 @@ struct CollectRange {
     u32 tilesS, tilesT;  // tile counts
 };
 
+// Incremental mode (full == 0): a triangle untouched since the previous
+// collect (stamp <= last_round, id < nT_last) keeps its cached quality flag
+// tbad[t] -- its corners and hence is_bad_triangle are unchanged -- so the
+// scan reads 5 B instead of 16 B + three vertex gathers.  The candidate list is
+// identical to a full scan (same flags, same stable compaction).
 template <int MODE>
 __global__ void __launch_bounds__(SCAN_BLOCK) k_collect_flags(DevMesh m, Quality q, CollectRange r,
                                                            uint8_t* __restrict__ flags,
-                                                           u32* __restrict__ partial) {
+                                                           u32* __restrict__ partial,
+                                                           const u32* __restrict__ stamp,
+                                                           uint8_t* __restrict__ tbad,
+                                                           u32 last_round, u32 nT_last, int full,
+                                                           Counters* ctr) {
     __shared__ u32 sh[SCAN_BLOCK / 32 + 1];
     const bool is_sub = blockIdx.x < r.tilesS;
     const u32 tile = is_sub ? blockIdx.x : blockIdx.x - r.tilesS;
     const u32 n = is_sub ? r.nS : r.nT;
     const u32 base = tile * (u32)SCAN_TILE;
-    u32 cnt = 0;
+    u32 cnt = 0, dirty = 0;
 #pragma unroll 4
     for (int k = 0; k < SCAN_ITEMS; ++k) {
         const u32 i = base + (u32)k * SCAN_BLOCK + threadIdx.x;
@@ -34,17 +43,22 @@ __global__ void __launch_bounds__(SCAN_BLOCK) k_collect_flags(DevMesh m, Quality
         if (i < n) {
             if (is_sub) {
                 if (m.salive[i] && (m.senc[i] || is_encroached<MODE>(m, i))) f = 1;
+            } else if (!full && i < nT_last && stamp[i] <= last_round) {
+                f = tbad[i];
             } else {
                 const uint4 tv = m.tv[i];
                 if (tv.w) {
                     const double2 a = m.xy[tv.x], b = m.xy[tv.y], c = m.xy[tv.z];
                     if (is_bad_pts(a, b, c, q) && resolvable_pts(a, b, c)) f = 1;
                 }
+                tbad[i] = f;
+                ++dirty;
             }
         }
         flags[(size_t)blockIdx.x * SCAN_TILE + (u32)k * SCAN_BLOCK + threadIdx.x] = f;
         cnt += f;
     }
+    warp_add_u32(&ctr->scan_dirty, dirty);
     const u32 t = block_sum<SCAN_BLOCK>(cnt, sh);
     if (threadIdx.x == 0) partial[blockIdx.x] = t;
 }
@@ -119,7 +133,7 @@ __global__ void __launch_bounds__(SCAN_BLOCK) k_collect_scatter(DevMesh m, Colle
 
 u32 launch_collect(const DevMesh& m, const Quality& q, bool rule4, uint8_t* flags, DevCands c,
                    u32 ccap, ScanScratch& s, Counters* d_ctr, cudaStream_t st,
-                   cudaEvent_t ev_scan0, cudaEvent_t ev_scan1) {
+                   const CollectCache& cache, cudaEvent_t ev_scan0, cudaEvent_t ev_scan1) {
     auto run = [&](bool sub, bool tri) -> u32 {
         CollectRange r;
         r.nS = sub ? m.nS : 0;
@@ -135,9 +149,9 @@ u32 launch_collect(const DevMesh& m, const Quality& q, bool rule4, uint8_t* flag
         }
         if (ev_scan0 && sub) cudaEventRecord(ev_scan0, st);
         if (q.mode == 0)
-            note_launch(), k_collect_flags<0><<<tiles, SCAN_BLOCK, 0, st>>>(m, q, r, flags, s.partial);
+            note_launch(), k_collect_flags<0><<<tiles, SCAN_BLOCK, 0, st>>>(m, q, r, flags, s.partial, cache.stamp, cache.tbad, cache.last_round, cache.nT_last, cache.full, d_ctr);
         else
-            note_launch(), k_collect_flags<1><<<tiles, SCAN_BLOCK, 0, st>>>(m, q, r, flags, s.partial);
+            note_launch(), k_collect_flags<1><<<tiles, SCAN_BLOCK, 0, st>>>(m, q, r, flags, s.partial, cache.stamp, cache.tbad, cache.last_round, cache.nT_last, cache.full, d_ctr);
         if (ev_scan1 && (tri || !rule4)) cudaEventRecord(ev_scan1, st);
         scan_partials(s.partial, tiles, s.partial + tiles, st);
         u32 total = 0;

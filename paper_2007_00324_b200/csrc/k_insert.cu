@@ -16,8 +16,14 @@
 // Mirrors: split_triangle_with mesh.hpp:323-346, split_edge_with :358-401,
 // split_subsegment :405-425, flip :210-258, remove_free_vertex + flop
 // :261-304,442-466, lawson_fixpoint cdt.hpp:111-123.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+
 #include "engine.h"
 #include "scan.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace gdp2d {
 
@@ -36,15 +42,16 @@ __device__ __forceinline__ void write_tri(const DevMesh& m, u32 t, u32 a, u32 b,
     if (s2 != NONE) m.stri[s2] = NONE;
 }
 
-__device__ __forceinline__ void push_touched(const WorkLists& w, const u32* ts, int k) {
-    const u32 o = atomicAdd(&w.rc->touched, (u32)k);
+__device__ __forceinline__ void push_touched(const WorkLists& w, const u32* ts, int k,
+                                             RoundCtr* rc = nullptr) {
+    const u32 o = atomicAdd(&(rc ? rc : w.rc)->touched, (u32)k);
     for (int j = 0; j < k; ++j)
         if (o + j < w.cap) w.touched[o + j] = ts[j];
 }
 
 __device__ __forceinline__ void push_work(const WorkLists& w, u32 widx, const u32* codes, int k,
-                                          Counters* ctr) {
-    const u32 o = atomicAdd(&w.rc->wl_next, (u32)k);
+                                          Counters* ctr, RoundCtr* rc = nullptr) {
+    const u32 o = atomicAdd(&(rc ? rc : w.rc)->wl_next, (u32)k);
     if (o + k > w.cap) {
         raise_err(ctr, DERR_WORKLIST_OVERFLOW, o);
         return;
@@ -228,12 +235,9 @@ void launch_apply_splits(const DevMesh& m, DevCands c, u32 n, u32 batch, u32 rou
 
 // ---- phase B ------------------------------------------------------------------------
 
-__global__ void k_fixup(DevMesh m, u32 round, TriAux x, WorkLists w, u32 n_bound, int seed,
-                        u32 widx, Counters* ctr) {
-    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
-    const u32 n = min(w.rc->touched, w.cap);
-    if (i >= n || i >= n_bound) return;
-    const u32 t = w.touched[i];
+__device__ __forceinline__ void fixup_one(const DevMesh& m, u32 round, const TriAux& x,
+                                          const WorkLists& w, u32 t, int seed, u32 widx,
+                                          RoundCtr* rc, Counters* ctr) {
     uint4 tn = m.tn[t];
     const uint4 tv = m.tv[t];
     if (!tv.w) return;
@@ -267,8 +271,16 @@ __global__ void k_fixup(DevMesh m, u32 round, TriAux x, WorkLists w, u32 n_bound
     }
     if (seed) {
         const u32 codes[3] = {enc(t, 0), enc(t, 1), enc(t, 2)};
-        push_work(w, widx, codes, 3, ctr);
+        push_work(w, widx, codes, 3, ctr, rc);
     }
+}
+
+__global__ void k_fixup(DevMesh m, u32 round, TriAux x, WorkLists w, u32 n_bound, int seed,
+                        u32 widx, Counters* ctr) {
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    const u32 n = min(w.rc->touched, w.cap);
+    if (i >= n || i >= n_bound) return;
+    fixup_one(m, round, x, w, w.touched[i], seed, widx, w.rc, ctr);
 }
 
 void launch_fixup(const DevMesh& m, u32 round, TriAux a, WorkLists w, u32 n_bound,
@@ -280,14 +292,11 @@ void launch_fixup(const DevMesh& m, u32 round, TriAux a, WorkLists w, u32 n_boun
 
 // ---- Lawson flip rounds (lawson_fixpoint cdt.hpp:111-123) -----------------------------
 
-// Test every work item (is_non_delaunay_edge mesh.hpp:430-437) on its
-// canonical side (lower triangle id) and claim both triangles with the edge
-// code as key: the minimum key wins, so a round's flip set is deterministic.
-__global__ void k_flip_test(DevMesh m, const u32* __restrict__ wl, u32 n, TriAux x, WorkLists w,
-                            Counters* ctr) {
-    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const u32 code = wl[i];
+// Test one work item (is_non_delaunay_edge mesh.hpp:430-437) on its canonical
+// side (lower triangle id) and claim both triangles with the edge code as key:
+// the minimum key wins, so a round's flip set is deterministic.
+__device__ __forceinline__ void flip_test_one(const DevMesh& m, u32 code, const TriAux& x,
+                                              const WorkLists& w, RoundCtr* rc, Counters* ctr) {
     u32 t = etri(code);
     int e = eidx(code);
     if (t >= m.nT) return;
@@ -312,7 +321,7 @@ __global__ void k_flip_test(DevMesh m, const u32* __restrict__ wl, u32 n, TriAux
     const u32 key = enc(t, e);
     atomicMin(&x.owner[t], key);
     atomicMin(&x.owner[u], key);
-    const u32 o = atomicAdd(&w.rc->cand, 1u);
+    const u32 o = atomicAdd(&rc->cand, 1u);
     if (o < w.cap) {
         w.fc[o] = key;
         w.fu[o] = enc(u, f);
@@ -322,62 +331,82 @@ __global__ void k_flip_test(DevMesh m, const u32* __restrict__ wl, u32 n, TriAux
 }
 
 // flip (mesh.hpp:210-258) as a phase-A rewrite: t := (a,b,d), u := (a,d,c).
-__global__ void k_flip_apply(DevMesh m, u32 n_bound, u32 round, u32 widx, TriAux x,
-                             WorkLists w, Counters* ctr) {
-    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
-    const u32 n = min(w.rc->cand, w.cap);
-    u32 flipped = 0;
-    if (i < n && i < n_bound) {
-        const u32 key = w.fc[i], uc = w.fu[i];
-        const u32 t = etri(key), u = etri(uc);
-        const int e = eidx(key), f = eidx(uc);
-        const bool won = x.owner[t] == key && x.owner[u] == key;
-        w.fwin[i] = won;
-        if (won) {
-            const uint4 tv = m.tv[t], tn = m.tn[t], ts = m.ts[t];
-            const uint4 uv = m.tv[u], un = m.tn[u], us = m.ts[u];
-            const u32 a = comp(tv, e), b = comp(tv, nxt(e)), c = comp(tv, prv(e));
-            const u32 d = comp(uv, f);
-            const double2 pa = m.xy[a], pb = m.xy[b], pc = m.xy[c], pd = m.xy[d];
-            if (orient2d(pa, pb, pd) <= 0 || orient2d(pa, pd, pc) <= 0) {
-                raise_err(ctr, DERR_NONCONVEX_FLIP, t);
-            } else if (atomicExch(&x.stamp[t], round) != round) {
-                x.stamp[u] = round;
-                write_tri(m, t, a, b, d, comp(un, nxt(f)), enc(u, 2), comp(tn, prv(e)), 5u,
-                          comp(us, nxt(f)), NONE, comp(ts, prv(e)));
-                write_tri(m, u, a, d, c, comp(un, prv(f)), comp(tn, nxt(e)), enc(t, 1), 3u,
-                          comp(us, prv(f)), comp(ts, nxt(e)), NONE);
-                x.emap[3 * t + nxt(e)] = enc(u, 1);
-                x.emap[3 * t + prv(e)] = enc(t, 2);
-                x.emap[3 * t + e] = NONE;
-                x.emap[3 * u + nxt(f)] = enc(t, 0);
-                x.emap[3 * u + prv(f)] = enc(u, 0);
-                x.emap[3 * u + f] = NONE;
-                const u32 tl[2] = {t, u};
-                push_touched(w, tl, 2);
-                const u32 codes[4] = {enc(t, 0), enc(t, 2), enc(u, 0), enc(u, 1)};
-                push_work(w, widx, codes, 4, ctr);
-                flipped = 1;
-            }
+__device__ __forceinline__ u32 flip_apply_one(const DevMesh& m, u32 i, u32 round, u32 widx,
+                                              const TriAux& x, const WorkLists& w, RoundCtr* rc,
+                                              Counters* ctr) {
+    const u32 key = w.fc[i], uc = w.fu[i];
+    const u32 t = etri(key), u = etri(uc);
+    const int e = eidx(key), f = eidx(uc);
+    const bool won = x.owner[t] == key && x.owner[u] == key;
+    w.fwin[i] = won;
+    // Duplicate work items carry the same key and all "win"; exactly one
+    // performs the flip -- the stamp exchange comes BEFORE any read, so a
+    // duplicate never sees the half-rewritten pair.
+    if (!won || atomicExch(&x.stamp[t], round) == round) return 0;
+    const uint4 tv = m.tv[t], tn = m.tn[t], ts = m.ts[t];
+    const uint4 uv = m.tv[u], un = m.tn[u], us = m.ts[u];
+    const u32 a = comp(tv, e), b = comp(tv, nxt(e)), c = comp(tv, prv(e));
+    const u32 d = comp(uv, f);
+    const double2 pa = m.xy[a], pb = m.xy[b], pc = m.xy[c], pd = m.xy[d];
+    x.stamp[u] = round;
+    if (orient2d(pa, pb, pd) <= 0 || orient2d(pa, pd, pc) <= 0) {
+        if (atomicCAS(&ctr->err_code, 0u, (u32)DERR_NONCONVEX_FLIP) == 0u) {
+            ctr->err_info = t;
+            ctr->dbg[0] = pa.x; ctr->dbg[1] = pa.y; ctr->dbg[2] = pb.x; ctr->dbg[3] = pb.y;
+            ctr->dbg[4] = pc.x; ctr->dbg[5] = pc.y; ctr->dbg[6] = pd.x; ctr->dbg[7] = pd.y;
         }
+        return 0;
     }
-    warp_add_ull(&ctr->flips, flipped);
+    write_tri(m, t, a, b, d, comp(un, nxt(f)), enc(u, 2), comp(tn, prv(e)), 5u,
+              comp(us, nxt(f)), NONE, comp(ts, prv(e)));
+    write_tri(m, u, a, d, c, comp(un, prv(f)), comp(tn, nxt(e)), enc(t, 1), 3u,
+              comp(us, prv(f)), comp(ts, nxt(e)), NONE);
+    x.emap[3 * t + nxt(e)] = enc(u, 1);
+    x.emap[3 * t + prv(e)] = enc(t, 2);
+    x.emap[3 * t + e] = NONE;
+    x.emap[3 * u + nxt(f)] = enc(t, 0);
+    x.emap[3 * u + prv(f)] = enc(u, 0);
+    x.emap[3 * u + f] = NONE;
+    const u32 tl[2] = {t, u};
+    push_touched(w, tl, 2, rc);
+    const u32 codes[4] = {enc(t, 0), enc(t, 2), enc(u, 0), enc(u, 1)};
+    push_work(w, widx, codes, 4, ctr, rc);
+    return 1;
 }
 
 // Release claims; a loser whose triangles were both left untouched retries.
-__global__ void k_flip_post(u32 n_bound, u32 round, u32 widx, TriAux x, WorkLists w,
-                            Counters* ctr) {
-    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
-    const u32 n = min(w.rc->cand, w.cap);
-    if (i >= n || i >= n_bound) return;
+__device__ __forceinline__ void flip_post_one(u32 i, u32 round, u32 widx, const TriAux& x,
+                                              const WorkLists& w, RoundCtr* rc, Counters* ctr) {
     const u32 key = w.fc[i], uc = w.fu[i];
     const u32 t = etri(key), u = etri(uc);
     x.owner[t] = NONE;
     x.owner[u] = NONE;
     if (!w.fwin[i] && x.stamp[t] != round && x.stamp[u] != round) {
         const u32 codes[1] = {key};
-        push_work(w, widx, codes, 1, ctr);
+        push_work(w, widx, codes, 1, ctr, rc);
     }
+}
+
+__global__ void k_flip_test(DevMesh m, const u32* __restrict__ wl, u32 n, TriAux x, WorkLists w,
+                            Counters* ctr) {
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) flip_test_one(m, wl[i], x, w, w.rc, ctr);
+}
+
+__global__ void k_flip_apply(DevMesh m, u32 n_bound, u32 round, u32 widx, TriAux x,
+                             WorkLists w, Counters* ctr) {
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    const u32 n = min(w.rc->cand, w.cap);
+    u32 flipped = 0;
+    if (i < n && i < n_bound) flipped = flip_apply_one(m, i, round, widx, x, w, w.rc, ctr);
+    warp_add_ull(&ctr->flips, flipped);
+}
+
+__global__ void k_flip_post(u32 n_bound, u32 round, u32 widx, TriAux x, WorkLists w,
+                            Counters* ctr) {
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    const u32 n = min(w.rc->cand, w.cap);
+    if (i < n && i < n_bound) flip_post_one(i, round, widx, x, w, w.rc, ctr);
 }
 
 void launch_flip_round(const DevMesh& m, u32 round, TriAux a, WorkLists w, u32 cur, u32 n,
@@ -389,6 +418,66 @@ void launch_flip_round(const DevMesh& m, u32 round, TriAux a, WorkLists w, u32 c
     note_launch(), k_flip_post<<<g, 256, 0, st>>>(n, round, cur ^ 1u, a, w, d_ctr);
     const u32 nt = 2 * n;
     note_launch(), k_fixup<<<(nt + 255) / 256, 256, 0, st>>>(m, round, a, w, nt, 0, 0, d_ctr);
+}
+
+// Whole Lawson fixpoint in ONE persistent cooperative launch: each round is
+// test+claim | apply | post+fixup separated by grid-wide barriers (which also
+// fence and invalidate L1), so the ~30 rounds of a batch cost no host round
+// trips.  Per-round counters live in rcs[r] (zeroed by the host).  Stops when
+// the next work list is empty or after max_rounds (the host then continues).
+__global__ void __launch_bounds__(LAWSON_BLOCK) k_lawson_persistent(
+    DevMesh m, u32 round0, u32 cur0, u32 n0, u32 max_rounds, TriAux x, WorkLists w,
+    RoundCtr* rcs, u32* result, Counters* ctr) {
+    cg::grid_group g = cg::this_grid();
+    const u32 tid = (u32)g.thread_rank(), nthr = (u32)g.size();
+    u32 n = n0, cur = cur0, r = 0;
+    u32 flipped = 0;
+    for (; r < max_rounds && n > 0; ++r) {
+        RoundCtr* rc = rcs + r;
+        const u32 round = round0 + r;
+        const u32* wl = w.w[cur];
+        for (u32 i = tid; i < n; i += nthr) flip_test_one(m, wl[i], x, w, rc, ctr);
+        g.sync();
+        const u32 nc = min(*(volatile u32*)&rc->cand, w.cap);
+        for (u32 i = tid; i < nc; i += nthr) flipped += flip_apply_one(m, i, round, cur ^ 1u, x, w, rc, ctr);
+        g.sync();
+        for (u32 i = tid; i < nc; i += nthr) flip_post_one(i, round, cur ^ 1u, x, w, rc, ctr);
+        const u32 nt = min(*(volatile u32*)&rc->touched, w.cap);
+        for (u32 i = tid; i < nt; i += nthr) fixup_one(m, round, x, w, w.touched[i], 0, 0, rc, ctr);
+        g.sync();
+        n = *(volatile u32*)&rc->wl_next;
+        if (n > w.cap) {
+            raise_err(ctr, DERR_WORKLIST_OVERFLOW, n);
+            n = 0;
+        }
+        cur ^= 1u;
+    }
+    warp_add_ull(&ctr->flips, flipped);
+    if (tid == 0) {
+        result[0] = r;
+        result[1] = cur;
+        result[2] = n;
+    }
+}
+
+int lawson_persistent_grid(int device) {
+    static int cached[64] = {0};
+    if (device >= 0 && device < 64 && cached[device]) return cached[device];
+    int sms = 0, per_sm = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lawson_persistent, LAWSON_BLOCK, 0);
+    const int g = std::max(1, sms * std::max(1, per_sm));
+    if (device >= 0 && device < 64) cached[device] = g;
+    return g;
+}
+
+void launch_lawson_persistent(const DevMesh& m, u32 round0, u32 cur0, u32 n0, u32 max_rounds,
+                              TriAux a, WorkLists w, RoundCtr* rcs, u32* result, Counters* d_ctr,
+                              int grid, cudaStream_t st) {
+    void* args[] = {(void*)&m, &round0, &cur0, &n0, &max_rounds, &a, &w, &rcs, &result, &d_ctr};
+    note_launch();
+    cudaLaunchCooperativeKernel((void*)k_lawson_persistent, dim3(grid), dim3(LAWSON_BLOCK), args,
+                                0, st);
 }
 
 // ---- redundancy detection (refine.hpp:551-608) ----------------------------------------
@@ -582,14 +671,22 @@ __global__ void __launch_bounds__(64) k_rm_apply(DevMesh m, const u32* __restric
             while (cnt > 3 && ok) {
                 int j = head;
                 bool found = false;
-                for (int it = 0; it < cnt; ++it) {
-                    const int a = PV[j], c = NX[j];
-                    const double2 pa = m.xy[L[a]], pj = m.xy[L[j]], pc = m.xy[L[c]];
-                    if (orient2d(pa, pj, pc) > 0 && orient2d(pa, pc, pv) > 0) {
-                        found = true;
-                        break;
+                // Pass 0: a strict ear = one valid flip of remove_free_vertex.
+                // Pass 1 (degenerate stars only, e.g. a point that was inserted
+                // exactly on an edge): v may lie ON the new diagonal -- the
+                // final hole triangulation is still valid because v leaves.
+                for (int pass = 0; pass < 2 && !found; ++pass) {
+                    j = head;
+                    for (int it = 0; it < cnt; ++it) {
+                        const int a = PV[j], c = NX[j];
+                        const double2 pa = m.xy[L[a]], pj = m.xy[L[j]], pc = m.xy[L[c]];
+                        const int side = orient2d(pa, pc, pv);
+                        if (orient2d(pa, pj, pc) > 0 && (side > 0 || (pass == 1 && side == 0))) {
+                            found = true;
+                            break;
+                        }
+                        j = NX[j];
                     }
-                    j = NX[j];
                 }
                 if (!found) {
                     ok = false;
@@ -632,6 +729,18 @@ __global__ void __launch_bounds__(64) k_rm_apply(DevMesh m, const u32* __restric
                 // vertex; it is never selected again.
                 f.removed[v - V0] = 2;
                 atomicAdd(&ctr->rm_kept, 1u);
+                if (w.dbg && atomicCAS(reinterpret_cast<ull*>(w.dbg), 0ull, 1ull) == 0ull) {
+                    w.dbg[1] = k;
+                    w.dbg[2] = pv.x;
+                    w.dbg[3] = pv.y;
+                    for (int q = 0; q < k; ++q) {
+                        const uint4 tv = m.tv[st[q]];
+                        const int iv = tv.x == v ? 0 : (tv.y == v ? 1 : 2);
+                        const double2 pq = m.xy[comp(tv, nxt(iv))];
+                        w.dbg[4 + 2 * q] = pq.x;
+                        w.dbg[5 + 2 * q] = pq.y;
+                    }
+                }
             } else {
                 for (int q = 0; q < k; ++q) x.stamp[st[q]] = round;
                 for (int ci = 0; ci < created; ++ci) {

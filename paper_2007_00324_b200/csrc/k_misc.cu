@@ -196,3 +196,62 @@ QualitySummary launch_quality(const DevMesh& m, const Quality& q, void* scratch,
 }
 
 }  // namespace gdp2d
+
+namespace gdp2d {
+
+// Debug validator (GDP2D_VALIDATE=1): the structural checks of
+// Mesh::check_structure (mesh.hpp:505-551) on the device.  out[0] = first
+// failure code, out[1] = triangle, out[2] = edge.
+__global__ void k_validate(DevMesh m, u32* out) {
+    const u32 t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= m.nT) return;
+    const uint4 tv = m.tv[t];
+    if (!tv.w) return;
+    auto fail = [&](u32 code, int e) {
+        if (atomicCAS(&out[0], 0u, code) == 0u) {
+            out[1] = t;
+            out[2] = (u32)e;
+        }
+    };
+    if (tv.x >= m.nV || tv.y >= m.nV || tv.z >= m.nV) return fail(1, -1);
+    if (orient2d(m.xy[tv.x], m.xy[tv.y], m.xy[tv.z]) <= 0) return fail(2, -1);
+    const uint4 tn = m.tn[t], ts = m.ts[t];
+    if (tn.w) return fail(3, -1);
+    for (int e = 0; e < 3; ++e) {
+        const u32 c = comp(tn, e);
+        if (c == NONE) continue;
+        const u32 u = etri(c);
+        const int f = eidx(c);
+        if (u >= m.nT || f > 2) return fail(4, e);
+        const uint4 uv = m.tv[u];
+        if (!uv.w) return fail(5, e);
+        if (comp(m.tn[u], f) != enc(t, e)) return fail(6, e);
+        if (comp(uv, nxt(f)) != comp(tv, prv(e)) || comp(uv, prv(f)) != comp(tv, nxt(e)))
+            return fail(7, e);
+        if (comp(m.ts[u], f) != comp(ts, e)) return fail(8, e);
+    }
+    for (int e = 0; e < 3; ++e) {
+        const u32 s = comp(ts, e);
+        if (s == NONE) continue;
+        if (s >= m.nS || !m.salive[s]) return fail(9, e);
+        const uint2 sv = m.sv[s];
+        const u32 x = comp(tv, nxt(e)), y = comp(tv, prv(e));
+        if (!((sv.x == x && sv.y == y) || (sv.x == y && sv.y == x))) return fail(10, e);
+        const u32 st = m.stri[s];
+        if (st == NONE || st >= m.nT || seg_slot(m.ts[st], s) < 0) return fail(11, e);
+    }
+    for (int i = 0; i < 3; ++i) {
+        const u32 v = comp(tv, i);
+        const u32 vt = m.vtri[v];
+        if (vt == NONE || vt >= m.nT || !m.tv[vt].w) return fail(12, i);
+        const uint4 w = m.tv[vt];
+        if (w.x != v && w.y != v && w.z != v) return fail(13, i);
+    }
+}
+
+void launch_validate(const DevMesh& m, u32* out, cudaStream_t st) {
+    cudaMemsetAsync(out, 0, 4 * sizeof(u32), st);
+    if (m.nT) note_launch(), k_validate<<<(m.nT + 255) / 256, 256, 0, st>>>(m, out);
+}
+
+}  // namespace gdp2d

@@ -146,7 +146,7 @@ _TOTALS = ("total_candidates", "total_walk_steps", "total_cavity_visits", "total
 _COUNTERS = ("tris_alive", "verts_alive", "subsegs_alive", "walk_steps", "cavity_visits",
              "survivors_claim", "survivors_cavity", "inserted_midpoints",
              "inserted_circumcenters", "removed_redundant", "removed_dependent", "dropped",
-             "marked_encroached", "flips", "flip_rounds", "removal_rounds")
+             "marked_encroached", "flips", "flip_rounds", "removal_rounds", "removals_kept")
 
 
 def _report(r: A.Report, arr) -> RunReport:
@@ -268,12 +268,37 @@ class Mesh:
 # ---- whole-run entry point ---------------------------------------------------------
 
 
+_ENGINES: dict = {}
+
+
+def _engine_for(device: int) -> "Engine":
+    eng = _ENGINES.get(device)
+    if eng is None:
+        eng = _ENGINES[device] = Engine(device)
+    return eng
+
+
 def refine(m: Mesh, q: QualityCriteria, cfg: Optional[EngineConfig] = None) -> RunReport:
     """cdtref::refine (refine.hpp:651) on the GPU; `m` is replaced by the refined mesh.
 
-    The timed scope (report.wall_seconds) covers H2D of the input mesh, every
-    batch and D2H of the result, through the C ABI with host buffers.
+    Host buffers in, host buffers out, through the C ABI: upload (H2D of the
+    input mesh), device-resident refinement, download straight into freshly
+    allocated numpy arrays (D2H).  The device context is cached per device.
+    report.wall_seconds covers the three steps.
     """
+    import time
+    cfg = cfg or EngineConfig()
+    eng = _engine_for(cfg.device)
+    t0 = time.perf_counter()
+    eng.upload(m)
+    rep = eng.refine(q, cfg)
+    m.assign(eng.download())
+    rep.wall_seconds = time.perf_counter() - t0
+    return rep
+
+
+def refine_c(m: Mesh, q: QualityCriteria, cfg: Optional[EngineConfig] = None) -> RunReport:
+    """The single-call C entry point gdp2d_refine (library-owned output buffers)."""
     cfg = cfg or EngineConfig()
     lib = A.engine()
     p = make_params(q, cfg)
@@ -328,10 +353,27 @@ class Engine:
         _raise(self.lib.gdp2d_ctx_refine(self.ctx, C.byref(p), C.byref(r)), "gdp2d_ctx_refine")
         return _report(r, arr)
 
+    def sizes(self):
+        v, t, s = C.c_uint32(), C.c_uint32(), C.c_uint32()
+        _raise(self.lib.gdp2d_ctx_sizes(self.ctx, C.byref(v), C.byref(t), C.byref(s)),
+               "gdp2d_ctx_sizes")
+        return v.value, t.value, s.value
+
     def download(self) -> Mesh:
-        out = A.MeshBuf()
-        _raise(self.lib.gdp2d_ctx_download(self.ctx, C.byref(out)), "gdp2d_ctx_download")
-        return Mesh.from_buf(out, self.lib.gdp2d_free)
+        """D2H of the working mesh straight into new numpy arrays."""
+        nv, nt, ns = self.sizes()
+        arrays = {}
+        for name, dt, w in _FIELDS:
+            n = nv if name in _VERT else nt if name in _TRI else ns
+            arrays[name] = np.empty((n, w) if w > 1 else n, dtype=dt)
+        mesh = Mesh(**arrays)
+        b = A.MeshBuf()
+        v = mesh.view()
+        for fname, _ in A.MeshView._fields_[4:]:
+            setattr(b, fname, getattr(v, fname))
+        _raise(self.lib.gdp2d_ctx_download_to(self.ctx, C.byref(b)), "gdp2d_ctx_download_to")
+        mesh.batch_epoch = b.batch_epoch
+        return mesh
 
     def device_bytes(self) -> int:
         return int(self.lib.gdp2d_ctx_device_bytes(self.ctx))

@@ -73,3 +73,26 @@ def triangles_near_bound(theta_deg: float, n: int, seed: int = 3) -> np.ndarray:
     tri = np.stack([a, b, c], axis=1)
     rnd = rng.uniform(0, 1, size=(n, 3, 2))
     return np.concatenate([tri, rnd])
+
+
+def mesh_scale_cocircular(n: int, seed: int = 17) -> np.ndarray:
+    """Near-cocircular quadruples at mesh scale: centre in the unit square,
+    radius 1e-2..1e-7, jitter of a few ulps of the coordinates (first three CCW)."""
+    rng = np.random.default_rng(seed)
+    c = rng.uniform(0.0, 1.0, size=(n, 1, 2))
+    r = 10.0 ** rng.uniform(-7, -2, size=(n, 1, 1))
+    t = np.sort(rng.uniform(0.0, 2 * math.pi, size=(n, 4)), axis=1)
+    pts = c + r * np.stack([np.cos(t), np.sin(t)], axis=2)
+    ulp = np.spacing(np.abs(pts) + 1e-300)
+    pts = pts + rng.integers(-2, 3, size=pts.shape) * ulp
+    return pts
+
+
+def mesh_scale_collinear(n: int, seed: int = 19) -> np.ndarray:
+    rng = np.random.default_rng(seed)
+    a = rng.uniform(0.0, 1.0, size=(n, 1, 2))
+    d = rng.normal(size=(n, 1, 2)) * 10.0 ** rng.uniform(-7, -2, size=(n, 1, 1))
+    s = rng.uniform(-1, 2, size=(n, 3, 1))
+    pts = a + s * d
+    ulp = np.spacing(np.abs(pts) + 1e-300)
+    return pts + rng.integers(-1, 2, size=pts.shape) * ulp

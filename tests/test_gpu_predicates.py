@@ -88,3 +88,10 @@ def test_circumcenter_bits(libs):
     assert np.array_equal(gok, rok)
     ok = rok.astype(bool)
     assert np.array_equal(g[ok].view(np.uint64), r[ok].view(np.uint64))
+
+
+def test_mesh_scale_near_degenerate(libs):
+    pts4 = G.mesh_scale_cocircular(200_000)
+    _cmp(libs, 1, pts4)
+    _cmp(libs, 0, pts4[:, :3])
+    _cmp(libs, 0, G.mesh_scale_collinear(200_000))

@@ -50,7 +50,7 @@ def main():
                       f"mid={c['inserted_midpoints']} cc={c['inserted_circumcenters']} "
                       f"red={c['removed_redundant']} dep={c['removed_dependent']} "
                       f"mark={c['marked_encroached']} drop={c['dropped']} flips={c['flips']} "
-                      f"fr={c['flip_rounds']} rr={c['removal_rounds']} | {ph}", flush=True)
+                      f"fr={c['flip_rounds']} rr={c['removal_rounds']} kept={c['removals_kept']} | {ph}", flush=True)
         out = eng.download()
     if a.check or a.ref:
         from oracle.ref import RefMesh
