@@ -1,0 +1,219 @@
+/*
+ * gdp2d_cdtref.hpp -- drop-in C++ shim: the reference's refine entry point
+ *
+ *     RunReport cdtref::refine(Mesh&, const QualityCriteria&, const EngineConfig&)
+ *     (/root/reference/proj/include/cdtref/refine.hpp:651)
+ *
+ * re-exposed with the SAME signature on top of the C ABI of gdp2d.h, so an
+ * existing caller (tools/cdtref.cpp:175, tests/unit/test_refine.cpp:374, ...)
+ * switches by including this header and writing gdp2d::refine instead of
+ * cdtref::refine.  The caller keeps the reference's own Mesh, PSLG/mesh I/O
+ * (pslg_io.hpp) and Line-1 build_cdt (cdt.hpp:483): this header only packs
+ * the AoS Mesh (mesh.hpp:43-75) into the SoA exchange view, runs the whole
+ * refinement loop on the GPU (libgdp2d.so) and unpacks the result in place.
+ *
+ * Include AFTER the reference headers ("cdtref/refine.hpp"); link -lgdp2d.
+ *
+ * Semantics kept from the reference:
+ *   - the mesh is mutated in place; ids of surviving input elements are kept,
+ *     dead slots stay (alive = false), new vertices carry kind
+ *     SteinerMidpoint / SteinerCircumcenter and birth_batch, batch_epoch is
+ *     bumped once per batch (refine.hpp:468);
+ *   - RunReport is filled exactly like refine.hpp:651-713 (per-batch
+ *     BatchMetrics with the six phase names of refine.hpp:671-701,
+ *     iteration_cap_hit, and the quality summary of refine.hpp:614-645);
+ *   - cfg.execution / executor_count / seed are accepted and ignored (the GPU
+ *     is the executor), as rule3_gamma / rule5 are ignored by the reference;
+ *   - errors: a device structural failure throws cdtref::MeshError
+ *     (MeshErrc::StaleHandle), capacity / CUDA / argument failures throw
+ *     std::runtime_error carrying gdp2d_last_error().  There is no CPU
+ *     fallback: without an sm_100 device the call throws.
+ */
+#ifndef GDP2D_CDTREF_HPP
+#define GDP2D_CDTREF_HPP
+
+#include <cmath>
+#include <cstdint>
+#include <cstdlib>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "gdp2d.h"
+
+namespace gdp2d {
+
+namespace detail {
+
+inline const char* const kPhaseNames[GDP2D_NPHASES] = {"collect", "split_points", "locate",
+                                                       "claim", "cavity", "insert"};
+
+inline gdp2d_params make_params(const cdtref::QualityCriteria& q,
+                                const cdtref::EngineConfig& cfg) {
+    gdp2d_params p;
+    // host-computed cos^2(theta), exactly as is_bad_triangle (refine.hpp:195-196)
+    gdp2d_params_init(&p, q.theta, q.ell,
+                      q.mode == cdtref::RefineMode::Chew ? GDP2D_CHEW : GDP2D_RUPPERT);
+    p.cavity_n = static_cast<uint32_t>(cfg.cavity_n);
+    p.rule1_compaction_threshold = static_cast<uint32_t>(cfg.rules.rule1_compaction_threshold);
+    p.rule2_filtering_enabled = cfg.rules.rule2_filtering_enabled ? 1u : 0u;
+    p.rule4_unified_collection = cfg.rules.rule4_unified_collection ? 1u : 0u;
+    p.iteration_cap = cfg.iteration_cap;
+    p.split_depth_cap = cfg.split_depth_cap;
+    p.batch_size_cap = cfg.batch_size_cap;
+    return p;
+}
+
+// AoS Mesh -> SoA staging owned by the caller's stack frame.
+struct Packed {
+    std::vector<double> xy;
+    std::vector<uint8_t> vkind, valive, talive, senc, salive;
+    std::vector<uint32_t> vbirth, tv, tn, ts, sv, sparent;
+    gdp2d_mesh_view view{};
+
+    explicit Packed(const cdtref::Mesh& m) {
+        const size_t V = m.vertices.size(), T = m.triangles.size(), S = m.subsegments.size();
+        xy.resize(2 * V);
+        vkind.resize(V);
+        valive.resize(V);
+        vbirth.resize(V);
+        for (size_t i = 0; i < V; ++i) {
+            const cdtref::Vertex& v = m.vertices[i];
+            xy[2 * i] = v.pos.x;
+            xy[2 * i + 1] = v.pos.y;
+            vkind[i] = static_cast<uint8_t>(v.kind);
+            vbirth[i] = v.birth_batch;
+            valive[i] = v.alive ? 1 : 0;
+        }
+        tv.resize(3 * T);
+        tn.resize(3 * T);
+        ts.resize(3 * T);
+        talive.resize(T);
+        for (size_t t = 0; t < T; ++t) {
+            const cdtref::Triangle& tr = m.triangles[t];
+            for (int i = 0; i < 3; ++i) {
+                tv[3 * t + i] = tr.v[i];
+                tn[3 * t + i] = tr.nbr[i];
+                ts[3 * t + i] = tr.seg[i];
+            }
+            talive[t] = tr.alive ? 1 : 0;
+        }
+        sv.resize(2 * S);
+        sparent.resize(S);
+        senc.resize(S);
+        salive.resize(S);
+        for (size_t s = 0; s < S; ++s) {
+            const cdtref::Subsegment& sg = m.subsegments[s];
+            sv[2 * s] = sg.v[0];
+            sv[2 * s + 1] = sg.v[1];
+            sparent[s] = sg.parent;
+            senc[s] = sg.encroached ? 1 : 0;
+            salive[s] = sg.alive ? 1 : 0;
+        }
+        view.n_vertices = static_cast<uint32_t>(V);
+        view.n_triangles = static_cast<uint32_t>(T);
+        view.n_subsegments = static_cast<uint32_t>(S);
+        view.batch_epoch = m.batch_epoch;
+        view.xy = xy.data();
+        view.vert_kind = vkind.data();
+        view.vert_birth = vbirth.data();
+        view.vert_alive = valive.data();
+        view.vert_tri = m.vert_tri.data();
+        view.tri_v = tv.data();
+        view.tri_n = tn.data();
+        view.tri_seg = ts.data();
+        view.tri_alive = talive.data();
+        view.seg_v = sv.data();
+        view.seg_parent = sparent.data();
+        view.seg_encroached = senc.data();
+        view.seg_alive = salive.data();
+        view.seg_tri = m.seg_tri.data();
+    }
+};
+
+// SoA result -> the caller's Mesh, in place (ids preserved).
+inline void unpack(const gdp2d_mesh_buf& b, cdtref::Mesh& m) {
+    const size_t V = b.n_vertices, T = b.n_triangles, S = b.n_subsegments;
+    m.vertices.resize(V);
+    m.vert_tri.assign(b.vert_tri, b.vert_tri + V);
+    for (size_t i = 0; i < V; ++i) {
+        cdtref::Vertex& v = m.vertices[i];
+        v.pos = cdtref::Point2{b.xy[2 * i], b.xy[2 * i + 1]};
+        v.kind = static_cast<cdtref::VertexKind>(b.vert_kind[i]);
+        v.birth_batch = b.vert_birth[i];
+        v.alive = b.vert_alive[i] != 0;
+    }
+    m.triangles.resize(T);
+    for (size_t t = 0; t < T; ++t) {
+        cdtref::Triangle& tr = m.triangles[t];
+        for (int i = 0; i < 3; ++i) {
+            tr.v[i] = b.tri_v[3 * t + i];
+            tr.nbr[i] = b.tri_n[3 * t + i];
+            tr.seg[i] = b.tri_seg[3 * t + i];
+        }
+        tr.alive = b.tri_alive[t] != 0;
+    }
+    m.subsegments.resize(S);
+    m.seg_tri.assign(b.seg_tri, b.seg_tri + S);
+    for (size_t s = 0; s < S; ++s) {
+        cdtref::Subsegment& sg = m.subsegments[s];
+        sg.v = {b.seg_v[2 * s], b.seg_v[2 * s + 1]};
+        sg.parent = b.seg_parent[s];
+        sg.encroached = b.seg_encroached[s] != 0;
+        sg.alive = b.seg_alive[s] != 0;
+    }
+    m.batch_epoch = b.batch_epoch;
+}
+
+inline void throw_status(int rc) {
+    const std::string what = std::string("gdp2d_refine: ") + gdp2d_last_error();
+    if (rc == GDP2D_EMESH) throw cdtref::MeshError(cdtref::MeshErrc::StaleHandle, what);
+    throw std::runtime_error(what);
+}
+
+}  // namespace detail
+
+// Drop-in for cdtref::refine (refine.hpp:651).  `device` selects the GPU
+// (one call = one device + one stream, blocking; distinct host threads may
+// drive distinct devices).
+inline cdtref::RunReport refine(cdtref::Mesh& m, const cdtref::QualityCriteria& q,
+                                const cdtref::EngineConfig& cfg, int device = 0) {
+    const gdp2d_params p = detail::make_params(q, cfg);
+    detail::Packed in(m);
+    std::vector<gdp2d_batch_metrics> bm(cfg.iteration_cap < 100000 ? cfg.iteration_cap + 1 : 100001);
+    gdp2d_report r{};
+    r.batches = bm.data();
+    r.batches_capacity = static_cast<uint32_t>(bm.size());
+    gdp2d_mesh_buf out{};
+    const int rc = gdp2d_refine(&in.view, &out, &p, &r, device);
+    if (rc != GDP2D_OK) detail::throw_status(rc);
+    detail::unpack(out, m);
+    gdp2d_free(&out);
+
+    cdtref::RunReport rep;
+    const uint32_t nb = r.n_batches < r.batches_capacity ? r.n_batches : r.batches_capacity;
+    for (uint32_t i = 0; i < nb; ++i) {
+        std::map<std::string, double> phases;
+        for (int k = 0; k < GDP2D_NPHASES; ++k) {
+            // the reference records "cavity" only when rule 2 is on (refine.hpp:688)
+            if (k == GDP2D_PH_CAVITY && !cfg.rules.rule2_filtering_enabled) continue;
+            phases[detail::kPhaseNames[k]] = bm[i].phase_seconds[k];
+        }
+        rep.batches.push_back(cdtref::record_batch(bm[i].batch_index, std::move(phases),
+                                                   bm[i].attempted, bm[i].concurrency));
+    }
+    rep.output_points = r.output_points;
+    rep.steiner_points = r.steiner_points;
+    rep.bad_triangles = r.bad_triangles;
+    rep.bad_area_percent = r.bad_area_percent;
+    rep.min_angle_deg = r.min_angle_deg;
+    rep.max_edge = r.max_edge;
+    rep.wall_seconds = r.wall_seconds;
+    rep.iteration_cap_hit = r.iteration_cap_hit != 0;
+    return rep;
+}
+
+}  // namespace gdp2d
+
+#endif  // GDP2D_CDTREF_HPP

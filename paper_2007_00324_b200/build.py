@@ -97,6 +97,26 @@ def build_host(force: bool = False) -> Path | None:
     return target
 
 
+def build_cli(force: bool = False) -> Path | None:
+    """lib/gdp2d_cli: the reference CLI's run_one with cdtref::refine swapped
+    for the drop-in gdp2d::refine (include/gdp2d_cdtref.hpp)."""
+    target = LIB / "gdp2d_cli"
+    src = CSRC / "host" / "gdp2d_cli.cpp"
+    if not REF_INCLUDE.exists():
+        if target.exists():
+            return target
+        raise RuntimeError(f"{REF_INCLUDE} missing and no prebuilt {target}")
+    deps = [src, INCLUDE / "gdp2d.h", INCLUDE / "gdp2d_cdtref.hpp", Path(__file__)]
+    if not force and _newer(target, deps):
+        return target
+    tmp = target.with_name(target.name + ".tmp")
+    _run(["g++", "-std=c++20", "-O3", "-DNDEBUG", "-ffp-contract=off", "-pthread",
+          "-I", str(INCLUDE), "-I", str(REF_INCLUDE), str(src), "-o", str(tmp),
+          "-L", str(LIB), "-lgdp2d", "-Wl,-rpath,$ORIGIN"])
+    os.replace(tmp, target)
+    return target
+
+
 def build_oracle(force: bool = False) -> None:
     """Checker libraries (test infrastructure only)."""
     odir = ROOT / "oracle"
@@ -110,6 +130,7 @@ def build_oracle(force: bool = False) -> None:
 def build_all(force: bool = False, verbose: bool = False) -> None:
     build_cuda(force, verbose)
     build_host(force)
+    build_cli(force)
     build_oracle(force)
 
 

@@ -676,12 +676,16 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
         cache.last_round = x->collect_round;
         cache.nT_last = x->collect_nT;
         cache.full = (x->full_scan || x->full_collect) ? 1 : 0;
+        bool tris_scanned = false;
         const u32 C = launch_collect(m, q, p->rule4_unified_collection != 0, x->flags, x->c,
-                                     x->ccap, x->scan, x->d_ctr, st, cache,
+                                     x->ccap, x->scan, x->d_ctr, st, cache, &tris_scanned,
                                      x->ev[GDP2D_NPHASES + 2], x->ev[GDP2D_NPHASES + 3]);
-        x->full_scan = false;
-        x->collect_round = x->round;
-        x->collect_nT = m.nT;
+        if (tris_scanned) {
+            // the cached triangle flags are current as of this round
+            x->full_scan = false;
+            x->collect_round = x->round;
+            x->collect_nT = m.nT;
+        }
         CK(cudaGetLastError());
         // launch_collect synchronised: the scan events are complete
         r->scan_seconds += ev_ms(x->ev[GDP2D_NPHASES + 2], x->ev[GDP2D_NPHASES + 3]) * 1e-3;
@@ -1108,8 +1112,10 @@ int gdp2d_collect(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_candidate* out, uin
         cache.stamp = x->aux.stamp;
         cache.tbad = x->aux.tbad;
         cache.full = 1;
+        bool tris_scanned = false;
         const u32 C = launch_collect(m, make_quality(p), p->rule4_unified_collection != 0,
-                                     x->flags, x->c, x->ccap, x->scan, x->d_ctr, x->st, cache);
+                                     x->flags, x->c, x->ccap, x->scan, x->d_ctr, x->st, cache,
+                                     &tris_scanned);
         *n = C;
         if (C > cap) {
             status = GDP2D_ECAPACITY;

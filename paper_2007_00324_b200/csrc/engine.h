@@ -51,7 +51,9 @@ struct CollectBufs {
 
 // collect + fused compute_splitting_points (refine.hpp:226-296).  Returns the
 // candidate count (synchronises).  If rule4 == false and subsegment
-// candidates exist, triangles are skipped (refine.hpp:239).
+// candidates exist, triangles are skipped (refine.hpp:239); *tris_scanned
+// then stays false and the caller must not advance the incremental cache
+// (the cached per-triangle flags were not refreshed).
 struct CollectCache {
     const u32* stamp = nullptr;   // TriAux::stamp
     uint8_t* tbad = nullptr;      // cached per-triangle flag
@@ -61,7 +63,7 @@ struct CollectCache {
 };
 u32 launch_collect(const DevMesh& m, const Quality& q, bool rule4, uint8_t* flags, DevCands c,
                    u32 ccap, ScanScratch& s, Counters* d_ctr, cudaStream_t st,
-                   const CollectCache& cache, cudaEvent_t ev_scan0 = nullptr,
+                   const CollectCache& cache, bool* tris_scanned, cudaEvent_t ev_scan0 = nullptr,
                    cudaEvent_t ev_scan1 = nullptr);
 void launch_split_points(const DevMesh& m, DevCands c, u32 n, Counters* d_ctr, cudaStream_t st);
 void launch_locate(const DevMesh& m, DevCands c, u32 n, Counters* d_ctr, cudaStream_t st);

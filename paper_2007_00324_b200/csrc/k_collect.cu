@@ -133,8 +133,11 @@ __global__ void __launch_bounds__(SCAN_BLOCK) k_collect_scatter(DevMesh m, Colle
 
 u32 launch_collect(const DevMesh& m, const Quality& q, bool rule4, uint8_t* flags, DevCands c,
                    u32 ccap, ScanScratch& s, Counters* d_ctr, cudaStream_t st,
-                   const CollectCache& cache, cudaEvent_t ev_scan0, cudaEvent_t ev_scan1) {
+                   const CollectCache& cache, bool* tris_scanned, cudaEvent_t ev_scan0,
+                   cudaEvent_t ev_scan1) {
+    *tris_scanned = false;
     auto run = [&](bool sub, bool tri) -> u32 {
+        if (tri) *tris_scanned = true;
         CollectRange r;
         r.nS = sub ? m.nS : 0;
         r.nT = tri ? m.nT : 0;

@@ -51,6 +51,12 @@ def main():
                       f"red={c['removed_redundant']} dep={c['removed_dependent']} "
                       f"mark={c['marked_encroached']} drop={c['dropped']} flips={c['flips']} "
                       f"fr={c['flip_rounds']} rr={c['removal_rounds']} kept={c['removals_kept']} | {ph}", flush=True)
+        tot = {}
+        for b in rep.batches:
+            for k, v in b.phase_breakdown.items():
+                tot[k] = tot.get(k, 0.0) + v
+        print("phase totals (ms): " + " ".join(f"{k}={v*1e3:.2f}" for k, v in tot.items()),
+              f"sum={sum(tot.values())*1e3:.2f}", flush=True)
         out = eng.download()
     if a.check or a.ref:
         from oracle.ref import RefMesh
