@@ -32,11 +32,13 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # circumcenter, midpoint, area, filters) is bit-identical to the reference's
 # IEEE evaluation; exact predicates use explicit fma() for two_prod.
 NVFLAGS = ["-std=c++17", "-O3", "-lineinfo", "-fmad=false", "-Xcompiler", "-fPIC",
-           "--expt-relaxed-constexpr", "-diag-suppress", "177"]
+           "--expt-relaxed-constexpr", "-diag-suppress", "177"] + \
+    os.environ.get("GDP2D_NVCC_EXTRA", "").split()
 
 CU_SOURCES = ["k_scan.cu", "k_collect.cu", "k_locate.cu", "k_filter.cu", "k_insert.cu",
               "k_misc.cu", "engine.cu"]
-HEADERS = ["gdp2d_common.cuh", "gdp2d_predicates.cuh", "gdp2d_geom.cuh", "scan.cuh", "engine.h"]
+HEADERS = ["gdp2d_common.cuh", "gdp2d_predicates.cuh", "gdp2d_geom.cuh", "gdp2d_phases.cuh",
+           "scan.cuh", "engine.h"]
 
 
 def _newer(target: Path, deps) -> bool:

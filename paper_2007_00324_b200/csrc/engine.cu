@@ -197,8 +197,76 @@ const char* dev_err_name(u32 c) {
 
 }  // namespace
 
+// GDP2D_TRACE=1: CUDA events between the launches of every batch plus the
+// device step trace of the persistent insertion kernel, printed to stderr.
+struct Tracer {
+    bool on = false;
+    cudaEvent_t ev[48] = {};
+    const char* name[48] = {};
+    int n = 0;
+    unsigned long long* d_trace = nullptr;
+    u32* d_trace_n = nullptr;
+    static constexpr u32 kCap = 1u << 16;
+    void init() {
+        for (auto& e : ev) cudaEventCreate(&e);
+        cudaMalloc(&d_trace, sizeof(unsigned long long) * kCap);
+        cudaMalloc(&d_trace_n, sizeof(u32));
+    }
+    void release() {
+        for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
+        if (d_trace) cudaFree(d_trace);
+        if (d_trace_n) cudaFree(d_trace_n);
+    }
+    void mark(const char* what, cudaStream_t st) {
+        if (!on || n >= 48) return;
+        name[n] = what;
+        cudaEventRecord(ev[n++], st);
+    }
+    void flush(u32 batch, cudaStream_t st) {
+        if (!on) return;
+        cudaStreamSynchronize(st);
+        fprintf(stderr, "[trace] batch %u host:", batch);
+        for (int i = 1; i < n; ++i) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+            fprintf(stderr, " %s=%.1f", name[i], ms * 1e3f);
+        }
+        fprintf(stderr, " (us)\n");
+        n = 0;
+        u32 cnt = 0;
+        cudaMemcpy(&cnt, d_trace_n, sizeof cnt, cudaMemcpyDeviceToHost);
+        cnt = std::min(cnt, kCap);
+        if (cnt > 1) {
+            std::vector<unsigned long long> t(cnt);
+            cudaMemcpy(t.data(), d_trace, sizeof(unsigned long long) * cnt, cudaMemcpyDeviceToHost);
+            static const char* tags[] = {"?", "start", "apply", "fixup", "ftest", "fapply", "fpost",
+                                         "detA", "detB", "detC", "rmclaim", "rmapply", "rmpost",
+                                         "blkin", "blkout", "end", "locate", "claim", "cavity",
+                                         "plan"};
+            constexpr u32 NT = sizeof(tags) / sizeof(tags[0]);
+            double sum[NT] = {0};
+            int cntt[NT] = {0};
+            for (u32 i = 1; i < cnt; ++i) {
+                const u32 tag = (u32)(t[i] & 0xFF);
+                const double dt = double((t[i] >> 8) - (t[i - 1] >> 8)) * 1e-3;
+                if (tag < NT) {
+                    sum[tag] += dt;
+                    cntt[tag]++;
+                }
+            }
+            fprintf(stderr, "[trace] batch %u device:", batch);
+            for (u32 k = 2; k < NT; ++k)
+                if (cntt[k]) fprintf(stderr, " %s=%.1f/%d", tags[k], sum[k], cntt[k]);
+            fprintf(stderr, " total=%.1f (us/steps)\n",
+                    double((t[cnt - 1] >> 8) - (t[0] >> 8)) * 1e-3);
+        }
+    }
+};
+
 struct gdp2d_ctx {
     int device = 0;
+    Tracer tr;
     cudaStream_t st = nullptr;
     MeshStore work, pristine;
     u32 epoch = 0, pristine_epoch = 0;
@@ -233,6 +301,17 @@ struct gdp2d_ctx {
     bool lawson_rounds = false;   // GDP2D_LAWSON=rounds: per-round launches
     bool full_collect = false;    // GDP2D_COLLECT=full: never reuse cached flags
     int lawson_grid = 0;          // persistent Lawson kernel grid (co-resident blocks)
+    int insert_grid = 0;          // persistent insertion kernel grid
+    int rollback_grid = 0;        // persistent rollback kernel grid
+    bool legacy_insert = false;   // GDP2D_INSERT=legacy: host-driven insertion rounds
+    RoundCtr* ring = nullptr;     // [4] step counters of the persistent insertion kernel
+    u32* ins_state = nullptr;     // [8] its status words
+    u32* h_state = nullptr;       // pinned copy
+    u32* d_C = nullptr;           // candidate count written by collect (device)
+    u32 small_nv = 256;           // GDP2D_SMALL_NV: block-mode insertion at or below
+    u32 small_wl = 256;           // GDP2D_SMALL_WL: block-mode Lawson below this list size
+    u32 small_c = 256;            // GDP2D_SMALL_C: whole batch in one CTA at or below
+    u32* scan_part = nullptr;     // [3 * insert_grid] plan chunk sums
     RoundCtr* rcs = nullptr;      // per-round counters of the persistent kernel
     u32* d_res = nullptr;
     u32* d_val = nullptr;
@@ -318,6 +397,17 @@ void ensure_aux(gdp2d_ctx* x) {
     }
 }
 
+// Lawson / touched work lists of at least n entries (contents are transient).
+void ensure_worklists(gdp2d_ctx* x, u64 n) {
+    if (n <= x->wl.cap) return;
+    const u32 wcap = (u32)std::min<u64>(0xFFFFFFF0ull, n + n / 2);
+    dfree(x->wl.w[0]); dfree(x->wl.w[1]); dfree(x->wl.fc); dfree(x->wl.fu);
+    dfree(x->wl.touched); dfree(x->wl.fwin);
+    dalloc(x->wl.w[0], wcap); dalloc(x->wl.w[1], wcap); dalloc(x->wl.fc, wcap);
+    dalloc(x->wl.fu, wcap); dalloc(x->wl.touched, wcap); dalloc(x->wl.fwin, wcap);
+    x->wl.cap = wcap;
+}
+
 void ensure_fresh(gdp2d_ctx* x, u32 n) {
     if (n <= x->fresh.cap) return;
     FreshInfo& f = x->fresh;
@@ -352,9 +442,16 @@ RoundCtr read_rc(gdp2d_ctx* x) {
     return *x->h_rc;
 }
 
+void raise_dev_err(gdp2d_ctx* x);
+
 void check_dev_err(gdp2d_ctx* x) {
     CK(cudaMemcpyAsync(x->h_ctr, x->d_ctr, sizeof(Counters), cudaMemcpyDeviceToHost, x->st));
     CK(cudaStreamSynchronize(x->st));
+    raise_dev_err(x);
+}
+
+// Throw if the (already downloaded) device counters carry an error.
+void raise_dev_err(gdp2d_ctx* x) {
     if (x->h_ctr->err_code) {
         char buf[512];
         const double* d = x->h_ctr->dbg;
@@ -451,6 +548,22 @@ void ctx_init(gdp2d_ctx* x, int device) {
     const char* lr = std::getenv("GDP2D_LAWSON");
     x->lawson_rounds = lr && std::string(lr) == "rounds";
     x->lawson_grid = lawson_persistent_grid(device);
+    x->insert_grid = insert_persistent_grid(device);
+    x->rollback_grid = rollback_persistent_grid(device);
+    const char* li = std::getenv("GDP2D_INSERT");
+    x->legacy_insert = (li && std::string(li) == "legacy") || x->validate || x->lawson_rounds;
+    dalloc(x->ring, 4);
+    dalloc(x->d_C, 1);
+    if (const char* e = std::getenv("GDP2D_TRACE"); e && e[0] == '1') {
+        x->tr.on = true;
+        x->tr.init();
+    }
+    if (const char* e = std::getenv("GDP2D_SMALL_NV")) x->small_nv = (u32)std::strtoul(e, nullptr, 10);
+    if (const char* e = std::getenv("GDP2D_SMALL_WL")) x->small_wl = (u32)std::strtoul(e, nullptr, 10);
+    if (const char* e = std::getenv("GDP2D_SMALL_C")) x->small_c = (u32)std::strtoul(e, nullptr, 10);
+    dalloc(x->scan_part, 3ull * x->insert_grid + 3);
+    dalloc(x->ins_state, 8);
+    CK(cudaMallocHost(&x->h_state, 8 * sizeof(u32)));
     const char* fc = std::getenv("GDP2D_COLLECT");
     x->full_collect = fc && std::string(fc) == "full";
     dalloc(x->rcs, 1024);
@@ -485,6 +598,12 @@ void ctx_release(gdp2d_ctx* x) {
     dfree(x->wl.dbg);
     dfree(x->rcs);
     dfree(x->d_res);
+    dfree(x->ring);
+    dfree(x->d_C);
+    dfree(x->scan_part);
+    x->tr.release();
+    dfree(x->ins_state);
+    if (x->h_state) cudaFreeHost(x->h_state);
     for (auto& e : x->ev)
         if (e) cudaEventDestroy(e);
     if (x->st) cudaStreamDestroy(x->st);
@@ -642,6 +761,133 @@ double ev_ms(cudaEvent_t a, cudaEvent_t b) {
     return (double)ms;
 }
 
+// Insertion phase, host-driven (one launch sequence per flip / removal round,
+// a host round trip after each): kept for GDP2D_VALIDATE=1 (structure checked
+// after every round) and GDP2D_INSERT=legacy.
+void insert_legacy(gdp2d_ctx* x, const gdp2d_params* p, const Quality& q, u32 C, u32 batch,
+                   u32& nv, u32& nt, u32& ns, u32& flip_rounds, u32& rm_rounds) {
+    cudaStream_t st = x->st;
+    CK(cudaMemcpyAsync(x->h_tot, x->ib.totals, 3 * sizeof(u32), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    nv = x->h_tot[0];
+    nt = x->h_tot[1];
+    ns = x->h_tot[2];
+    const u32 V0 = x->work.m.nV;
+    ensure_mesh(x, x->work.m.nV + nv, x->work.m.nT + nt, x->work.m.nS + ns);
+    ensure_fresh(x, nv);
+    if (!nv) return;
+    DevMesh& mm = x->work.m;
+    ++x->round;
+    zero_rc(x);
+    launch_apply_splits(mm, x->c, C, batch, x->round, x->ib, x->aux, x->fresh, x->wl, x->d_ctr,
+                        st);
+    mm.nV += nv;
+    mm.nT += nt;
+    mm.nS += ns;
+    launch_fixup(mm, x->round, x->aux, x->wl, 4 * nv, true, 0, x->d_ctr, st);
+    RoundCtr rc = read_rc(x);
+    validate_now(x, "splits");
+    lawson_from(x, 0, rc.wl_next, &flip_rounds);
+    // Phase 3: redundant-point removal to fixpoint (refine.hpp:551-608).
+    for (;;) {
+        zero_rc(x);
+        launch_detect(mm, q, p->split_depth_cap, V0, nv, x->fresh, x->wl, x->d_ctr, st);
+        rc = read_rc(x);
+        u32 nrm = std::min(rc.detect, x->wl.rm_cap);
+        if (nrm == 0) break;
+        u32 cur = 0;
+        u32 guard = 0;
+        while (nrm > 0) {
+            if (++guard > 100000) throw Fail{GDP2D_EMESH, "vertex removal did not converge"};
+            ++x->round;
+            zero_rc(x);
+            launch_removal_round(mm, x->round, V0, x->aux, x->fresh, x->wl, cur, nrm, 0,
+                                 x->d_ctr, st);
+            rc = read_rc(x);
+            ++rm_rounds;
+            check_dev_err(x);
+            validate_now(x, "removal round");
+            lawson_from(x, 0, rc.wl_next, &flip_rounds);
+            nrm = rc.rm_next;
+            cur ^= 1u;
+        }
+    }
+}
+
+// Insertion phase as one persistent cooperative launch (k_insert.cu): no host
+// round trip inside; the capacity check runs on the device and a batch that
+// does not fit is re-launched after growing the buffers (the mesh is not
+// touched by a launch that reports INS_GROW).
+void insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, u32 C, u32 ncav, u32 batch, u32& nv,
+                       u32& nt, u32& ns, u32& flip_rounds, u32& rm_rounds) {
+    (void)C;
+    cudaStream_t st = x->st;
+    for (int attempt = 0;; ++attempt) {
+        CK(cudaMemsetAsync(x->ring, 0, 4 * sizeof(RoundCtr), st));
+        InsertLaunch L;
+        L.m = x->work.m;
+        L.c = x->c;
+        L.b = x->ib;
+        L.x = x->aux;
+        L.f = x->fresh;
+        L.w = x->wl;
+        L.ring = x->ring;
+        L.state = x->ins_state;
+        L.ctr = x->d_ctr;
+        L.d_C = x->d_C;
+        L.depth_cap = p->split_depth_cap;
+        L.batch = batch;
+        L.round0 = x->round + 1;
+        L.vcap = x->work.vcap;
+        L.tcap = x->work.tcap;
+        L.scap = x->work.scap;
+        L.small_nv = x->small_nv;
+        L.small_wl = x->small_wl;
+        L.max_steps = 1u << 20;
+        L.ncav = ncav;
+        L.rs = ncav + 1 + MAX_CLAIM_EXTRA;
+        L.regions = x->regions;
+        L.region_len = x->region_len;
+        L.scan_part = x->scan_part;
+        L.small_c = x->small_c;
+        L.resume = attempt > 0 ? 1 : 0;
+        L.filter = C <= x->small_c ? 1 : 0;
+        if (x->tr.on) {
+            L.trace = x->tr.d_trace;
+            L.trace_n = x->tr.d_trace_n;
+            L.trace_cap = Tracer::kCap;
+            CK(cudaMemsetAsync(x->tr.d_trace_n, 0, sizeof(u32), st));
+        }
+        x->tr.mark("pre_ins", st);
+        launch_insert_persistent(L, p->mode == GDP2D_CHEW ? 1 : 0, x->insert_grid,
+                                 x->rollback_grid, st);
+        x->tr.mark("insert_kernel", st);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(x->h_state, x->ins_state, 8 * sizeof(u32), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(x->h_tot, x->ib.totals, 3 * sizeof(u32), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(x->h_ctr, x->d_ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        nv = x->h_tot[0];
+        nt = x->h_tot[1];
+        ns = x->h_tot[2];
+        if (x->h_state[0] == 1u) {   // INS_GROW
+            if (attempt > 2) throw Fail{GDP2D_ECAPACITY, "insertion does not fit after growth"};
+            ensure_mesh(x, x->work.m.nV + nv, x->work.m.nT + nt, x->work.m.nS + ns);
+            ensure_fresh(x, nv);
+            ensure_worklists(x, 12ull * nv);
+            continue;
+        }
+        if (x->h_state[0] == 2u) throw Fail{GDP2D_EMESH, "insertion exceeded its step bound"};
+        x->round += x->h_state[1] + 1;
+        flip_rounds = x->h_state[2];
+        rm_rounds = x->h_state[3];
+        x->work.m.nV += nv;
+        x->work.m.nT += nt;
+        x->work.m.nS += ns;
+        return;
+    }
+}
+
 // The refinement loop (refine.hpp:651-713) on the working mesh.
 void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
     const auto wall0 = std::chrono::steady_clock::now();
@@ -670,6 +916,7 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
         CK(cudaMemsetAsync(x->d_ctr, 0, sizeof(Counters), st));
         ensure_cands(x, m.nS + m.nT);
         CK(cudaEventRecord(x->ev[0], st));
+        x->tr.mark("start", st);
         CollectCache cache;
         cache.stamp = x->aux.stamp;
         cache.tbad = x->aux.tbad;
@@ -679,7 +926,7 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
         bool tris_scanned = false;
         const u32 C = launch_collect(m, q, p->rule4_unified_collection != 0, x->flags, x->c,
                                      x->ccap, x->scan, x->d_ctr, st, cache, &tris_scanned,
-                                     x->ev[GDP2D_NPHASES + 2], x->ev[GDP2D_NPHASES + 3]);
+                                     x->d_C, x->ev[GDP2D_NPHASES + 2], x->ev[GDP2D_NPHASES + 3]);
         if (tris_scanned) {
             // the cached triangle flags are current as of this round
             x->full_scan = false;
@@ -689,83 +936,69 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
         CK(cudaGetLastError());
         // launch_collect synchronised: the scan events are complete
         r->scan_seconds += ev_ms(x->ev[GDP2D_NPHASES + 2], x->ev[GDP2D_NPHASES + 3]) * 1e-3;
-        {
-            // bytes the scan must move: 5 B per clean triangle (stamp + cached
-            // flag), 16 B record + 3 x 16 B corners + 5 B per re-evaluated one,
-            // 48 B per subsegment (SURVEY 8(d) per-unit figure)
-            CK(cudaMemcpyAsync(&x->h_tot[3], &x->d_ctr->scan_dirty, sizeof(u32),
-                               cudaMemcpyDeviceToHost, st));
-            CK(cudaStreamSynchronize(st));
-            const u64 dirty = x->h_tot[3];
-            r->scan_bytes += 5ull * m.nT + 64ull * dirty + 48ull * m.nS;
-        }
+        // bytes the scan must move: 5 B per clean triangle (stamp + cached
+        // flag), 16 B record + 3 x 16 B corners + 5 B per re-evaluated one,
+        // 48 B per subsegment (SURVEY 8(d) per-unit figure); the dirty count
+        // arrives with the end-of-batch counters
+        const u64 scan_nT = m.nT, scan_nS = m.nS;
         r->scan_launches += 1;
-        if (C == 0) break;
+        x->tr.mark("collect", st);
+        if (C == 0) {
+            check_dev_err(x);
+            r->scan_bytes += 5ull * scan_nT + 64ull * x->h_ctr->scan_dirty + 48ull * scan_nS;
+            break;
+        }
         CK(cudaEventRecord(x->ev[1], st));   // split points are fused into collect
         CK(cudaEventRecord(x->ev[2], st));
-        launch_locate(m, x->c, C, x->d_ctr, st);
-        CK(cudaEventRecord(x->ev[3], st));
-        launch_claim(m, x->c, C, x->aux, x->d_ctr, st);
-        CK(cudaEventRecord(x->ev[4], st));
         ensure_regions(x, C, ncav);
-        launch_cavity(m, x->c, C, ncav, true, x->aux, x->regions, x->region_len, nullptr,
-                      x->d_ctr, st);
-        CK(cudaEventRecord(x->ev[5], st));
-        // ---- insert ----
-        launch_plan_ops(m, x->c, C, p->split_depth_cap, x->ib, x->d_ctr, st);
-        scan_exclusive(x->ib.nv, x->ib.ov, C, x->ib.totals + 0, x->scan, st);
-        scan_exclusive(x->ib.nt, x->ib.ot, C, x->ib.totals + 1, x->scan, st);
-        scan_exclusive(x->ib.ns, x->ib.os, C, x->ib.totals + 2, x->scan, st);
-        CK(cudaMemcpyAsync(x->h_tot, x->ib.totals, 3 * sizeof(u32), cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        const u32 nv = x->h_tot[0], nt = x->h_tot[1], ns = x->h_tot[2];
-        const u32 V0 = m.nV;
-        ensure_mesh(x, m.nV + nv, m.nT + nt, m.nS + ns);
-        ensure_fresh(x, nv);
         const u32 batch = ++x->epoch;
         u32 flip_rounds = 0, rm_rounds = 0;
-        if (nv) {
-            DevMesh& mm = x->work.m;
-            ++x->round;
-            zero_rc(x);
-            launch_apply_splits(mm, x->c, C, batch, x->round, x->ib, x->aux, x->fresh, x->wl,
-                                x->d_ctr, st);
-            mm.nV += nv;
-            mm.nT += nt;
-            mm.nS += ns;
-            launch_fixup(mm, x->round, x->aux, x->wl, 4 * nv, true, 0, x->d_ctr, st);
-            RoundCtr rc = read_rc(x);
-            validate_now(x, "splits");
-            lawson_from(x, 0, rc.wl_next, &flip_rounds);
-            // Phase 3: redundant-point removal to fixpoint (refine.hpp:551-608).
-            for (;;) {
-                zero_rc(x);
-                launch_detect(mm, q, p->split_depth_cap, V0, nv, x->fresh, x->wl, x->d_ctr, st);
-                rc = read_rc(x);
-                u32 nrm = std::min(rc.detect, x->wl.rm_cap);
-                if (nrm == 0) break;
-                u32 cur = 0;
-                u32 guard = 0;
-                while (nrm > 0) {
-                    if (++guard > 100000) throw Fail{GDP2D_EMESH, "vertex removal did not converge"};
-                    ++x->round;
-                    zero_rc(x);
-                    launch_removal_round(mm, x->round, V0, x->aux, x->fresh, x->wl, cur, nrm, 0,
-                                         x->d_ctr, st);
-                    rc = read_rc(x);
-                    ++rm_rounds;
-                    check_dev_err(x);
-                    validate_now(x, "removal round");
-                    lawson_from(x, 0, rc.wl_next, &flip_rounds);
-                    nrm = rc.rm_next;
-                    cur ^= 1u;
-                }
+        u32 nv = 0, nt = 0, ns = 0;
+        if (x->legacy_insert) {
+            launch_locate(m, x->c, C, x->d_ctr, st);
+            x->tr.mark("locate", st);
+            CK(cudaEventRecord(x->ev[3], st));
+            launch_claim(m, x->c, C, x->aux, x->d_ctr, st);
+            x->tr.mark("claim", st);
+            CK(cudaEventRecord(x->ev[4], st));
+            launch_cavity(m, x->c, C, ncav, true, x->aux, x->regions, x->region_len, nullptr,
+                          x->d_ctr, st);
+            x->tr.mark("cavity", st);
+            CK(cudaEventRecord(x->ev[5], st));
+            launch_plan_ops(m, x->c, C, p->split_depth_cap, x->ib, x->d_ctr, st);
+            scan_exclusive(x->ib.nv, x->ib.ov, C, x->ib.totals + 0, x->scan, st);
+            scan_exclusive(x->ib.nt, x->ib.ot, C, x->ib.totals + 1, x->scan, st);
+            scan_exclusive(x->ib.ns, x->ib.os, C, x->ib.totals + 2, x->scan, st);
+            x->tr.mark("plan+scans", st);
+            insert_legacy(x, p, q, C, batch, nv, nt, ns, flip_rounds, rm_rounds);
+        } else {
+            if (C > x->small_c) {
+                // big batch: Lines 5-7 as high-occupancy standalone kernels
+                launch_locate(m, x->c, C, x->d_ctr, st);
+                CK(cudaEventRecord(x->ev[3], st));
+                launch_claim(m, x->c, C, x->aux, x->d_ctr, st);
+                CK(cudaEventRecord(x->ev[4], st));
+                launch_cavity(m, x->c, C, ncav, true, x->aux, x->regions, x->region_len,
+                              nullptr, x->d_ctr, st);
+                CK(cudaEventRecord(x->ev[5], st));
+            } else {
+                // tail batch: everything runs inside the block-mode kernels
+                CK(cudaEventRecord(x->ev[3], st));
+                CK(cudaEventRecord(x->ev[4], st));
+                CK(cudaEventRecord(x->ev[5], st));
             }
+            insert_persistent(x, p, C, ncav, batch, nv, nt, ns, flip_rounds, rm_rounds);
         }
         CK(cudaEventRecord(x->ev[6], st));
+        x->tr.mark("sync", st);
+        x->tr.flush(bm.batch_index, st);
         CK(cudaGetLastError());
-        check_dev_err(x);
+        if (x->legacy_insert)
+            check_dev_err(x);
+        else
+            raise_dev_err(x);   // counters came back with the insertion's status
         const Counters& h = *x->h_ctr;
+        r->scan_bytes += 5ull * scan_nT + 64ull * h.scan_dirty + 48ull * scan_nS;
         const u32 inserted = h.ins_mid + h.ins_cc;
         const u32 retained = inserted - std::min(inserted, h.rm_done);
         x->alive_v += inserted;
@@ -1115,7 +1348,7 @@ int gdp2d_collect(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_candidate* out, uin
         bool tris_scanned = false;
         const u32 C = launch_collect(m, make_quality(p), p->rule4_unified_collection != 0,
                                      x->flags, x->c, x->ccap, x->scan, x->d_ctr, x->st, cache,
-                                     &tris_scanned);
+                                     &tris_scanned, x->d_C);
         *n = C;
         if (C > cap) {
             status = GDP2D_ECAPACITY;

@@ -63,7 +63,8 @@ struct CollectCache {
 };
 u32 launch_collect(const DevMesh& m, const Quality& q, bool rule4, uint8_t* flags, DevCands c,
                    u32 ccap, ScanScratch& s, Counters* d_ctr, cudaStream_t st,
-                   const CollectCache& cache, bool* tris_scanned, cudaEvent_t ev_scan0 = nullptr,
+                   const CollectCache& cache, bool* tris_scanned, u32* d_count,
+                   cudaEvent_t ev_scan0 = nullptr,
                    cudaEvent_t ev_scan1 = nullptr);
 void launch_split_points(const DevMesh& m, DevCands c, u32 n, Counters* d_ctr, cudaStream_t st);
 void launch_locate(const DevMesh& m, DevCands c, u32 n, Counters* d_ctr, cudaStream_t st);
@@ -134,6 +135,42 @@ int lawson_persistent_grid(int device);
 void launch_lawson_persistent(const DevMesh& m, u32 round0, u32 cur0, u32 n0, u32 max_rounds,
                               TriAux a, WorkLists w, RoundCtr* rcs, u32* result, Counters* d_ctr,
                               int grid, cudaStream_t st);
+// The whole insertion phase of a batch (phase 1 splits, Lawson, detect +
+// rollback loops) as one persistent cooperative launch (k_insert.cu).
+constexpr int INSERT_BLOCK = 256;
+struct InsertLaunch {
+    DevMesh m;            // counts before the batch
+    DevCands c;
+    InsertBufs b;
+    TriAux x;
+    FreshInfo f;
+    WorkLists w;
+    RoundCtr* ring;       // [4] zeroed before the launch
+    u32* state;           // [8] status / steps / flip rounds / removal rounds / handoff
+    Counters* ctr;
+    const u32* d_C;
+    u64 depth_cap;
+    u32 batch, round0;
+    u32 vcap, tcap, scap;
+    u32 small_nv, small_wl, max_steps;
+    u32 ncav = 32, rs = 35;
+    u32* regions = nullptr;
+    u32* region_len = nullptr;
+    u32* scan_part = nullptr;   // [3 * grid]
+    u32 small_c = 0;
+    int resume = 0;
+    int filter = 1;
+    unsigned long long* trace = nullptr;   // device step trace (GDP2D_TRACE=1)
+    u32* trace_n = nullptr;
+    u32 trace_cap = 0;
+};
+int insert_persistent_grid(int device);
+int rollback_persistent_grid(int device);
+// Kernel 1 (plan + splits + Lawson, with Lines 5-7 when L.filter) then
+// kernel 2 (detect + rollback loop), both cooperative, no host sync between.
+void launch_insert_persistent(const InsertLaunch& L, int mode, int grid, int grid2,
+                              cudaStream_t st);
+
 // Redundancy detection (refine.hpp:551-608): fills w.rm[0], count in w.rc->detect.
 void launch_detect(const DevMesh& m, const Quality& q, u64 depth_cap, u32 V0, u32 F,
                    FreshInfo f, WorkLists w, Counters* d_ctr, cudaStream_t st);

@@ -13,6 +13,8 @@
 // Edge i of a triangle is opposite corner i: (v[i+1], v[i+2]) (mesh.hpp:115).
 #pragma once
 
+#include <cooperative_groups.h>
+#include <cooperative_groups/scan.h>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -125,6 +127,22 @@ __device__ __forceinline__ void raise_err(Counters* c, u32 code, u32 info) {
 
 __device__ __forceinline__ u64 make_key(int band, double measure) {
     return ((u64)band << 63) | ((u64)__double_as_longlong(measure) & 0x7FFFFFFFFFFFFFFFull);
+}
+
+// Warp-aggregated reservation of k slots on a shared append counter: the
+// lanes that are converged at the call site scan their k, ONE lane issues the
+// atomicAdd and broadcasts the base.  Work lists are appended by every thread
+// of a grid; a same-address atomic per thread serialises in one L2 slice
+// (hundreds of microseconds per round at mesh scale), one per warp does not.
+__device__ __forceinline__ u32 agg_reserve(u32* ctr, u32 k) {
+    namespace cg = cooperative_groups;
+    cg::coalesced_group g = cg::coalesced_threads();
+    const u32 pre = cg::exclusive_scan(g, k);
+    u32 base = 0;
+    const u32 last = g.num_threads() - 1;
+    if (g.thread_rank() == last) base = atomicAdd(ctr, pre + k);
+    base = g.shfl(base, last);
+    return base + pre;
 }
 
 // Warp-aggregated atomic add on a 64-bit counter.  Must be called by all 32

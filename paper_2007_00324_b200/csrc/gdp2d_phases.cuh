@@ -1,0 +1,263 @@
+// gdp2d_phases.cuh -- per-candidate bodies of Lines 5-7 of Algorithm 1, shared
+// by the standalone phase kernels (parity entry points gdp2d_locate /
+// gdp2d_claim / gdp2d_cavity, k_locate.cu / k_filter.cu) and the persistent
+// batch kernel (k_insert.cu), so the code the parity tests check is the code
+// the refinement runs.
+//
+//   locate_one           locate (refine.hpp:301-335) -> locate_point cdt.hpp:68-105
+//   claim_*_one          ClaimTable / claim_filter (refine.hpp:342-376)
+//   cavity_*_one         cavity_filter (refine.hpp:382-429) -> expand (expandlist.hpp:93-157)
+//   plan_one             insert_batch phase-1 needs (refine.hpp:493-539)
+//
+// The reference's ClaimTable keeps, per triangle, the candidate with the
+// maximum priority_less key (band, measure, then LOWER tiebreak).  On the GPU
+// that strict total order is resolved with two atomics per slot, no sort:
+// atomicMax on the 64-bit (band<<63 | bits(measure)) key, then atomicMin on
+// (tiebreak<<32 | list index) among the key holders.  The index term
+// reproduces the sequential first-claimer rule for exact ties.
+#pragma once
+
+#include "engine.h"
+
+namespace gdp2d {
+
+// Returns the walk steps.
+__device__ __forceinline__ u32 locate_one(const DevMesh& m, const DevCands& c, u32 i) {
+    if (!c.alive[i]) return 0;
+    if (c.kind[i] == 0) {
+        c.loc[i] = m.stri[c.id[i]];
+        c.lkind[i] = 4;   // subsegment midpoint: split along the subsegment
+        c.ledge[i] = -1;
+        return 0;
+    }
+    const double2 p = c.pt[i];
+    const Loc loc = locate_point(m, c.id[i], p, true);
+    u32 hit = NONE;
+    bool done = false;
+    switch (loc.kind) {
+        case 0:  // Inside
+            c.loc[i] = loc.tri;
+            c.lkind[i] = 0;
+            c.ledge[i] = -1;
+            done = true;
+            break;
+        case 1: {  // OnEdge
+            const u32 s = comp(m.ts[loc.tri], loc.edge);
+            if (s == NONE) {
+                c.loc[i] = loc.tri;
+                c.lkind[i] = 1;
+                c.ledge[i] = (int8_t)loc.edge;
+                done = true;
+            } else {
+                hit = s;
+            }
+            break;
+        }
+        case 4:
+            hit = loc.seg;
+            break;
+        default:  // OnVertex, OutsideHull
+            c.alive[i] = 0;
+            done = true;
+            break;
+    }
+    if (!done) {
+        // Interception: split the blocking subsegment (refine.hpp:329-334).
+        c.kind[i] = 0;
+        c.id[i] = hit;
+        c.pt[i] = subseg_mid(m, hit);
+        c.key[i] = make_key(1, subseg_len(m, hit));
+        c.loc[i] = m.stri[hit];
+        c.lkind[i] = 4;
+        c.ledge[i] = -1;
+    }
+    return loc.steps;
+}
+
+__device__ __forceinline__ u64 tie_of(const DevCands& c, u32 i) {
+    return ((u64)c.tie[i] << 32) | (u64)i;
+}
+
+__device__ __forceinline__ void claim_max_one(const DevCands& c, u32 i, u64* ckey) {
+    if (c.alive[i]) atomicMax((ull*)&ckey[c.loc[i]], (ull)c.key[i]);
+}
+
+__device__ __forceinline__ void claim_tie_one(const DevCands& c, u32 i, const u64* ckey,
+                                              u64* ctie) {
+    if (c.alive[i]) {
+        const u32 t = c.loc[i];
+        if (ckey[t] == c.key[i]) atomicMin((ull*)&ctie[t], (ull)tie_of(c, i));
+    }
+}
+
+// Returns 1 if the candidate owns its triangle.
+__device__ __forceinline__ u32 claim_check_one(const DevCands& c, u32 i, const u64* ckey,
+                                               const u64* ctie) {
+    if (!c.alive[i]) return 0;
+    const u32 t = c.loc[i];
+    const bool own = ckey[t] == c.key[i] && ctie[t] == tie_of(c, i);
+    if (!own) c.alive[i] = 0;
+    return own ? 1u : 0u;
+}
+
+__device__ __forceinline__ void claim_reset_one(const DevCands& c, u32 i, u32 nT, u64* ckey,
+                                                u64* ctie) {
+    const u32 t = c.loc[i];
+    if (t < nT) {
+        ckey[t] = 0;
+        ctie[t] = ~0ull;
+    }
+}
+
+// Per candidate: FIFO BFS of triangles whose circumcircle strictly contains
+// the point (the located triangle always belongs), never crossing a
+// subsegment, at most ncav+1 triangles.  Processing a FIFO queue item by item
+// with emissions appended in (source, slot) order visits triangles in exactly
+// the window order of expand() (expandlist.hpp:98-152), so the region -- and
+// hence the claim set -- is the reference's, including when the cap binds.
+// extras (refine mode): the triangle across a split edge is claimed too
+// (SURVEY §7 hard part (i)).  Returns the BFS region size (cavity visits).
+__device__ __forceinline__ u32 cavity_bfs_one(const DevMesh& m, const DevCands& c, u32 i,
+                                              u32 ncav, int extras, u32 rs, u32* regions,
+                                              u32* region_len, u32* bfs_len, u64* ckey) {
+    u32 len = 0, blen = 0;
+    if (c.alive[i]) {
+        u32* reg = regions + (size_t)i * rs;
+        u32 queue[1 + 3 * (MAX_CAVITY_N + 1)];
+        u32 head = 0, tail = 0;
+        const u32 located = c.loc[i];
+        const double2 p = c.pt[i];
+        const u64 key = c.key[i];
+        queue[tail++] = located;
+        while (head < tail && len <= ncav) {
+            const u32 t = queue[head++];
+            const uint4 tv = m.tv[t];
+            bool pred = t == located;
+            if (!pred && tv.w) pred = incircle(m.xy[tv.x], m.xy[tv.y], m.xy[tv.z], p) > 0;
+            if (!pred) continue;
+            bool in = false;
+            for (u32 k = 0; k < len; ++k) in |= reg[k] == t;
+            if (in) continue;
+            reg[len++] = t;
+            atomicMax((ull*)&ckey[t], (ull)key);
+            const uint4 tn = m.tn[t];
+            const uint4 ts = m.ts[t];
+            for (int e = 0; e < 3; ++e) {
+                if (comp(ts, e) != NONE) continue;
+                const u32 cc = comp(tn, e);
+                if (cc == NONE) continue;
+                const u32 nb = etri(cc);
+                bool seen = false;
+                for (u32 k = 0; k < len; ++k) seen |= reg[k] == nb;
+                if (seen) continue;
+                queue[tail++] = nb;
+            }
+        }
+        blen = len;
+        if (extras) {
+            u32 far = NONE;
+            if (c.kind[i] == 0) {
+                const u32 s = c.id[i];
+                const int e = seg_slot(m.ts[located], s);
+                if (e >= 0) {
+                    const u32 cc = comp(m.tn[located], e);
+                    if (cc != NONE) far = etri(cc);
+                }
+            } else if (c.lkind[i] == 1) {
+                const u32 cc = comp(m.tn[located], c.ledge[i]);
+                if (cc != NONE) far = etri(cc);
+            }
+            if (far != NONE) {
+                bool in = false;
+                for (u32 k = 0; k < len; ++k) in |= reg[k] == far;
+                if (!in) {
+                    reg[len++] = far;
+                    atomicMax((ull*)&ckey[far], (ull)key);
+                }
+            }
+        }
+    }
+    region_len[i] = len;
+    if (bfs_len) bfs_len[i] = blen;
+    return blen;
+}
+
+__device__ __forceinline__ void cavity_tie_one(const DevCands& c, u32 i, u32 rs,
+                                               const u32* regions, const u32* region_len,
+                                               const u64* ckey, u64* ctie) {
+    const u32 len = region_len[i];
+    if (!len) return;
+    const u64 key = c.key[i];
+    const u64 tie = tie_of(c, i);
+    const u32* reg = regions + (size_t)i * rs;
+    for (u32 k = 0; k < len; ++k) {
+        const u32 t = reg[k];
+        if (ckey[t] == key) atomicMin((ull*)&ctie[t], (ull)tie);
+    }
+}
+
+// Returns 1 if the candidate owns its whole region (refine.hpp:420-428).
+__device__ __forceinline__ u32 cavity_check_one(const DevCands& c, u32 i, u32 rs,
+                                                const u32* regions, const u32* region_len,
+                                                const u64* ckey, const u64* ctie) {
+    const u32 len = region_len[i];
+    if (!len || !c.alive[i]) return 0;
+    const u64 key = c.key[i];
+    const u64 tie = tie_of(c, i);
+    const u32* reg = regions + (size_t)i * rs;
+    bool own = true;
+    for (u32 k = 0; k < len && own; ++k) {
+        const u32 t = reg[k];
+        own = ckey[t] == key && ctie[t] == tie;
+    }
+    if (!own) c.alive[i] = 0;
+    return own ? 1u : 0u;
+}
+
+__device__ __forceinline__ void cavity_reset_one(u32 i, u32 rs, const u32* regions,
+                                                 const u32* region_len, u64* ckey, u64* ctie) {
+    const u32 len = region_len[i];
+    const u32* reg = regions + (size_t)i * rs;
+    for (u32 k = 0; k < len; ++k) {
+        ckey[reg[k]] = 0;
+        ctie[reg[k]] = ~0ull;
+    }
+}
+
+// Needs of one surviving candidate (refine.hpp:493-539): subsegments that hit
+// the depth cap or fail subsegment_split_ok are abandoned (:501-506).
+// Returns 1 if the candidate was dropped.
+__device__ __forceinline__ u32 plan_one(const DevMesh& m, const DevCands& c, u32 i, u64 depth_cap,
+                                        u32& nv, u32& nt, u32& ns) {
+    nv = nt = ns = 0;
+    u32 dropped = 0;
+    if (c.alive[i]) {
+        if (c.kind[i] == 0) {
+            const u32 s = c.id[i];
+            if (!m.salive[s]) {
+                dropped = 1;
+            } else if ((u64)m.sdepth[s] >= depth_cap || !subseg_split_ok(m, s, c.pt[i])) {
+                m.senc[s] = 0;
+                dropped = 1;
+            } else {
+                const u32 t = c.loc[i];
+                const int e = seg_slot(m.ts[t], s);
+                const bool far = comp(m.tn[t], e) != NONE;
+                nv = 1;
+                nt = far ? 2 : 1;
+                ns = 2;
+            }
+        } else if (c.lkind[i] == 0) {
+            nv = 1;
+            nt = 2;
+        } else if (c.lkind[i] == 1) {
+            const bool far = comp(m.tn[c.loc[i]], c.ledge[i]) != NONE;
+            nv = 1;
+            nt = far ? 2 : 1;
+        }
+        if (!nv) c.alive[i] = 0;
+    }
+    return dropped;
+}
+
+}  // namespace gdp2d

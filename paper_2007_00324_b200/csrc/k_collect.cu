@@ -58,9 +58,12 @@ __global__ void __launch_bounds__(SCAN_BLOCK) k_collect_flags(DevMesh m, Quality
         flags[(size_t)blockIdx.x * SCAN_TILE + (u32)k * SCAN_BLOCK + threadIdx.x] = f;
         cnt += f;
     }
-    warp_add_u32(&ctr->scan_dirty, dirty);
-    const u32 t = block_sum<SCAN_BLOCK>(cnt, sh);
-    if (threadIdx.x == 0) partial[blockIdx.x] = t;
+    // one reduction for both: count and dirty are <= SCAN_TILE < 2^16
+    const u32 t = block_sum<SCAN_BLOCK>(cnt | (dirty << 16), sh);
+    if (threadIdx.x == 0) {
+        partial[blockIdx.x] = t & 0xFFFFu;
+        if (t >> 16) atomicAdd(&ctr->scan_dirty, t >> 16);
+    }
 }
 
 // compute_splitting_points for one candidate (refine.hpp:269-294).
@@ -89,12 +92,15 @@ __global__ void __launch_bounds__(SCAN_BLOCK) k_collect_scatter(DevMesh m, Colle
                                                              const uint8_t* __restrict__ flags,
                                                              const u32* __restrict__ partial,
                                                              DevCands c, u32 ccap,
+                                                             const u32* __restrict__ d_total,
                                                              Counters* ctr) {
     __shared__ u32 sh[SCAN_BLOCK / 32 + 1];
     const bool is_sub = blockIdx.x < r.tilesS;
     const u32 tile = is_sub ? blockIdx.x : blockIdx.x - r.tilesS;
     const u32 base = tile * (u32)SCAN_TILE;
     u32 carry = partial[blockIdx.x];
+    const u32 end = blockIdx.x + 1 < r.tilesS + r.tilesT ? partial[blockIdx.x + 1] : *d_total;
+    if (end == carry) return;   // no candidate in this tile (the common case in the tail)
     u32 nfb = 0;
     for (int k = 0; k < SCAN_ITEMS; ++k) {
         const u32 i = base + (u32)k * SCAN_BLOCK + threadIdx.x;
@@ -133,8 +139,8 @@ __global__ void __launch_bounds__(SCAN_BLOCK) k_collect_scatter(DevMesh m, Colle
 
 u32 launch_collect(const DevMesh& m, const Quality& q, bool rule4, uint8_t* flags, DevCands c,
                    u32 ccap, ScanScratch& s, Counters* d_ctr, cudaStream_t st,
-                   const CollectCache& cache, bool* tris_scanned, cudaEvent_t ev_scan0,
-                   cudaEvent_t ev_scan1) {
+                   const CollectCache& cache, bool* tris_scanned, u32* d_count,
+                   cudaEvent_t ev_scan0, cudaEvent_t ev_scan1) {
     *tris_scanned = false;
     auto run = [&](bool sub, bool tri) -> u32 {
         if (tri) *tris_scanned = true;
@@ -144,7 +150,10 @@ u32 launch_collect(const DevMesh& m, const Quality& q, bool rule4, uint8_t* flag
         r.tilesS = (r.nS + SCAN_TILE - 1) / SCAN_TILE;
         r.tilesT = (r.nT + SCAN_TILE - 1) / SCAN_TILE;
         const u32 tiles = r.tilesS + r.tilesT;
-        if (tiles == 0) return 0;
+        if (tiles == 0) {
+            cudaMemsetAsync(d_count, 0, sizeof(u32), st);
+            return 0;
+        }
         if (tiles + 1 > s.cap) {
             if (s.partial) cudaFree(s.partial);
             s.cap = (tiles + 1) * 2;
@@ -156,12 +165,12 @@ u32 launch_collect(const DevMesh& m, const Quality& q, bool rule4, uint8_t* flag
         else
             note_launch(), k_collect_flags<1><<<tiles, SCAN_BLOCK, 0, st>>>(m, q, r, flags, s.partial, cache.stamp, cache.tbad, cache.last_round, cache.nT_last, cache.full, d_ctr);
         if (ev_scan1 && (tri || !rule4)) cudaEventRecord(ev_scan1, st);
-        scan_partials(s.partial, tiles, s.partial + tiles, st);
+        scan_partials(s.partial, tiles, d_count, st);
         u32 total = 0;
-        cudaMemcpyAsync(&total, s.partial + tiles, sizeof(u32), cudaMemcpyDeviceToHost, st);
+        cudaMemcpyAsync(&total, d_count, sizeof(u32), cudaMemcpyDeviceToHost, st);
         cudaStreamSynchronize(st);
         if (total > 0)
-            note_launch(), k_collect_scatter<<<tiles, SCAN_BLOCK, 0, st>>>(m, r, flags, s.partial, c, ccap, d_ctr);
+            note_launch(), k_collect_scatter<<<tiles, SCAN_BLOCK, 0, st>>>(m, r, flags, s.partial, c, ccap, d_count, d_ctr);
         return total;
     };
     if (rule4) return run(true, true);

@@ -1,58 +1,37 @@
-// k_filter.cu -- Lines 6-7 of Algorithm 1: the per-triangle claim
+// k_filter.cu -- Lines 6-7 of Algorithm 1 as standalone kernels for the
+// gdp2d_claim / gdp2d_cavity parity entry points: the per-triangle claim
 // (claim_filter, refine.hpp:367-376) and the cavity-approximation filter
-// (cavity_filter, refine.hpp:382-429 -> expand, expandlist.hpp:93-157).
-//
-// The reference's ClaimTable (refine.hpp:342-361) keeps, per triangle, the
-// candidate with the maximum priority_less key (band, measure, then LOWER
-// tiebreak).  On the GPU that strict total order is resolved with two atomics
-// per slot, no sort: atomicMax on the 64-bit (band<<63 | bits(measure)) key,
-// then atomicMin on (tiebreak<<32 | list index) among the key holders.  The
-// index term reproduces the sequential first-claimer rule for exact ties.
-#include "engine.h"
+// (cavity_filter, refine.hpp:382-429 -> expand, expandlist.hpp:93-157).  The
+// per-candidate bodies live in gdp2d_phases.cuh and are the ones the
+// persistent batch kernel runs.
+#include "gdp2d_phases.cuh"
+#include "scan.cuh"
 
 namespace gdp2d {
 
-__device__ __forceinline__ u64 tie_of(const DevCands& c, u32 i) {
-    return ((u64)c.tie[i] << 32) | (u64)i;
-}
-
 __global__ void k_claim_max(DevCands c, u32 n, u64* __restrict__ ckey) {
     const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n && c.alive[i]) atomicMax((ull*)&ckey[c.loc[i]], (ull)c.key[i]);
+    if (i < n) claim_max_one(c, i, ckey);
 }
 
 __global__ void k_claim_tie(DevCands c, u32 n, const u64* __restrict__ ckey,
                             u64* __restrict__ ctie) {
     const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n && c.alive[i]) {
-        const u32 t = c.loc[i];
-        if (ckey[t] == c.key[i]) atomicMin((ull*)&ctie[t], (ull)tie_of(c, i));
-    }
+    if (i < n) claim_tie_one(c, i, ckey, ctie);
 }
 
 __global__ void k_claim_check(DevCands c, u32 n, const u64* __restrict__ ckey,
                               const u64* __restrict__ ctie, Counters* ctr) {
     const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
     u32 surv = 0;
-    if (i < n && c.alive[i]) {
-        const u32 t = c.loc[i];
-        const bool own = ckey[t] == c.key[i] && ctie[t] == tie_of(c, i);
-        if (!own) c.alive[i] = 0;
-        surv = own;
-    }
-    warp_add_u32(&ctr->surv_claim, surv);
+    if (i < n) surv = claim_check_one(c, i, ckey, ctie);
+    block_add<u32>(&ctr->surv_claim, surv);
 }
 
 __global__ void k_claim_reset(DevCands c, u32 n, u32 nT, u64* __restrict__ ckey,
                               u64* __restrict__ ctie) {
     const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) {
-        const u32 t = c.loc[i];
-        if (t < nT) {
-            ckey[t] = 0;
-            ctie[t] = ~0ull;
-        }
-    }
+    if (i < n) claim_reset_one(c, i, nT, ckey, ctie);
 }
 
 void launch_claim(const DevMesh& m, DevCands c, u32 n, TriAux a, Counters* d_ctr,
@@ -65,14 +44,6 @@ void launch_claim(const DevMesh& m, DevCands c, u32 n, TriAux a, Counters* d_ctr
     note_launch(), k_claim_reset<<<g, 256, 0, st>>>(c, n, m.nT, a.ckey, a.ctie);
 }
 
-// ---- cavity ---------------------------------------------------------------------
-
-// Per candidate: FIFO BFS of triangles whose circumcircle strictly contains
-// the point (the located triangle always belongs), never crossing a
-// subsegment, at most ncav+1 triangles.  Processing a FIFO queue item by item
-// with emissions appended in (source, slot) order visits triangles in exactly
-// the window order of expand() (expandlist.hpp:98-152), so the region -- and
-// hence the claim set -- is the reference's, including when the cap binds.
 __global__ void __launch_bounds__(128) k_cavity_bfs(DevMesh m, DevCands c, u32 n, u32 ncav,
                                                     int extras, u32 rs,
                                                     u32* __restrict__ regions,
@@ -81,88 +52,15 @@ __global__ void __launch_bounds__(128) k_cavity_bfs(DevMesh m, DevCands c, u32 n
                                                     u64* __restrict__ ckey, Counters* ctr) {
     const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
     ull visits = 0;
-    if (i < n) {
-        u32 len = 0, blen = 0;
-        if (c.alive[i]) {
-            u32* reg = regions + (size_t)i * rs;
-            u32 queue[1 + 3 * (MAX_CAVITY_N + 1)];
-            u32 head = 0, tail = 0;
-            const u32 located = c.loc[i];
-            const double2 p = c.pt[i];
-            const u64 key = c.key[i];
-            queue[tail++] = located;
-            while (head < tail && len <= ncav) {
-                const u32 t = queue[head++];
-                const uint4 tv = m.tv[t];
-                bool pred = t == located;
-                if (!pred && tv.w)
-                    pred = incircle(m.xy[tv.x], m.xy[tv.y], m.xy[tv.z], p) > 0;
-                if (!pred) continue;
-                bool in = false;
-                for (u32 k = 0; k < len; ++k) in |= reg[k] == t;
-                if (in) continue;
-                reg[len++] = t;
-                atomicMax((ull*)&ckey[t], (ull)key);
-                const uint4 tn = m.tn[t];
-                const uint4 ts = m.ts[t];
-                for (int e = 0; e < 3; ++e) {
-                    if (comp(ts, e) != NONE) continue;
-                    const u32 cc = comp(tn, e);
-                    if (cc == NONE) continue;
-                    const u32 nb = etri(cc);
-                    bool seen = false;
-                    for (u32 k = 0; k < len; ++k) seen |= reg[k] == nb;
-                    if (seen) continue;
-                    queue[tail++] = nb;
-                }
-            }
-            blen = len;
-            if (extras) {
-                // Refine mode: the insertion also rewrites the triangle across a
-                // split edge, so claim it too (SURVEY §7 hard part (i)).
-                u32 far = NONE;
-                if (c.kind[i] == 0) {
-                    const u32 s = c.id[i];
-                    const int e = seg_slot(m.ts[located], s);
-                    if (e >= 0) {
-                        const u32 cc = comp(m.tn[located], e);
-                        if (cc != NONE) far = etri(cc);
-                    }
-                } else if (c.lkind[i] == 1) {
-                    const u32 cc = comp(m.tn[located], c.ledge[i]);
-                    if (cc != NONE) far = etri(cc);
-                }
-                if (far != NONE) {
-                    bool in = false;
-                    for (u32 k = 0; k < len; ++k) in |= reg[k] == far;
-                    if (!in) {
-                        reg[len++] = far;
-                        atomicMax((ull*)&ckey[far], (ull)key);
-                    }
-                }
-            }
-        }
-        region_len[i] = len;
-        if (bfs_len) bfs_len[i] = blen;
-        visits = blen;
-    }
-    warp_add_ull(&ctr->cavity_visits, visits);
+    if (i < n) visits = cavity_bfs_one(m, c, i, ncav, extras, rs, regions, region_len, bfs_len, ckey);
+    block_add<ull>(&ctr->cavity_visits, visits);
 }
 
 __global__ void k_cavity_tie(DevCands c, u32 n, u32 rs, const u32* __restrict__ regions,
                              const u32* __restrict__ region_len, const u64* __restrict__ ckey,
                              u64* __restrict__ ctie) {
     const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const u32 len = region_len[i];
-    if (!len) return;
-    const u64 key = c.key[i];
-    const u64 tie = tie_of(c, i);
-    const u32* reg = regions + (size_t)i * rs;
-    for (u32 k = 0; k < len; ++k) {
-        const u32 t = reg[k];
-        if (ckey[t] == key) atomicMin((ull*)&ctie[t], (ull)tie);
-    }
+    if (i < n) cavity_tie_one(c, i, rs, regions, region_len, ckey, ctie);
 }
 
 __global__ void k_cavity_check(DevCands c, u32 n, u32 rs, const u32* __restrict__ regions,
@@ -170,35 +68,15 @@ __global__ void k_cavity_check(DevCands c, u32 n, u32 rs, const u32* __restrict_
                                const u64* __restrict__ ctie, Counters* ctr) {
     const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
     u32 surv = 0;
-    if (i < n) {
-        const u32 len = region_len[i];
-        if (len && c.alive[i]) {
-            const u64 key = c.key[i];
-            const u64 tie = tie_of(c, i);
-            const u32* reg = regions + (size_t)i * rs;
-            bool own = true;
-            for (u32 k = 0; k < len && own; ++k) {
-                const u32 t = reg[k];
-                own = ckey[t] == key && ctie[t] == tie;
-            }
-            if (!own) c.alive[i] = 0;
-            surv = own;
-        }
-    }
-    warp_add_u32(&ctr->surv_cavity, surv);
+    if (i < n) surv = cavity_check_one(c, i, rs, regions, region_len, ckey, ctie);
+    block_add<u32>(&ctr->surv_cavity, surv);
 }
 
 __global__ void k_cavity_reset(u32 n, u32 rs, const u32* __restrict__ regions,
                                const u32* __restrict__ region_len, u64* __restrict__ ckey,
                                u64* __restrict__ ctie) {
     const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const u32 len = region_len[i];
-    const u32* reg = regions + (size_t)i * rs;
-    for (u32 k = 0; k < len; ++k) {
-        ckey[reg[k]] = 0;
-        ctie[reg[k]] = ~0ull;
-    }
+    if (i < n) cavity_reset_one(i, rs, regions, region_len, ckey, ctie);
 }
 
 void launch_cavity(const DevMesh& m, DevCands c, u32 n, u32 ncav, bool extras, TriAux a,

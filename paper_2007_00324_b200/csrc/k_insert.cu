@@ -20,10 +20,16 @@
 
 #include <algorithm>
 
-#include "engine.h"
+#include "gdp2d_phases.cuh"
 #include "scan.cuh"
 
 namespace cg = cooperative_groups;
+
+// CTAs per SM the split/Lawson kernel is compiled for (register budget
+// 65536 / (256 * MINB)); measured on B200, see DESIGN.md.
+#ifndef GDP2D_SPLIT_MINB
+#define GDP2D_SPLIT_MINB 2
+#endif
 
 namespace gdp2d {
 
@@ -44,14 +50,14 @@ __device__ __forceinline__ void write_tri(const DevMesh& m, u32 t, u32 a, u32 b,
 
 __device__ __forceinline__ void push_touched(const WorkLists& w, const u32* ts, int k,
                                              RoundCtr* rc = nullptr) {
-    const u32 o = atomicAdd(&(rc ? rc : w.rc)->touched, (u32)k);
+    const u32 o = agg_reserve(&(rc ? rc : w.rc)->touched, (u32)k);
     for (int j = 0; j < k; ++j)
         if (o + j < w.cap) w.touched[o + j] = ts[j];
 }
 
 __device__ __forceinline__ void push_work(const WorkLists& w, u32 widx, const u32* codes, int k,
                                           Counters* ctr, RoundCtr* rc = nullptr) {
-    const u32 o = atomicAdd(&(rc ? rc : w.rc)->wl_next, (u32)k);
+    const u32 o = agg_reserve(&(rc ? rc : w.rc)->wl_next, (u32)k);
     if (o + k > w.cap) {
         raise_err(ctr, DERR_WORKLIST_OVERFLOW, o);
         return;
@@ -60,8 +66,13 @@ __device__ __forceinline__ void push_work(const WorkLists& w, u32 widx, const u3
 }
 
 // split_triangle_with (mesh.hpp:323-346): t := (a,b,w), t1 := (b,c,w), t2 := (c,a,w).
+// seed != 0: push the three link edges (opposite wv) as Lawson seeds.  The
+// spokes (wv, a) need no test: an empty circle through wv and a exists inside
+// the old circumcircle, so they are Delaunay edges (Lawson insertion); the
+// flips that later change a spoke's quad push it again (flip_apply_one).
 __device__ void split_triangle_A(const DevMesh& m, const TriAux& x, const WorkLists& w, u32 t,
-                                 u32 wv, u32 t1, u32 t2, u32 round) {
+                                 u32 wv, u32 t1, u32 t2, u32 round, RoundCtr* rc = nullptr,
+                                 int seed = 0, Counters* ctr = nullptr) {
     const uint4 ov = m.tv[t], on = m.tn[t], os = m.ts[t];
     x.stamp[t] = round;
     write_tri(m, t, ov.x, ov.y, wv, enc(t1, 1), enc(t2, 0), on.z, 4u, NONE, NONE, os.z);
@@ -72,13 +83,20 @@ __device__ void split_triangle_A(const DevMesh& m, const TriAux& x, const WorkLi
     x.emap[3 * t + 2] = enc(t, 2);
     m.vtri[wv] = NONE;
     const u32 tl[3] = {t, t1, t2};
-    push_touched(w, tl, 3);
+    push_touched(w, tl, 3, rc);
+    if (seed) {
+        const u32 codes[3] = {enc(t, 2), enc(t1, 2), enc(t2, 2)};
+        push_work(w, 0, codes, 3, ctr, rc);
+    }
 }
 
 // split_edge_with (mesh.hpp:358-401) on edge e of t; new t2 (and u2 when the
 // edge has a far side).  s_bw / s_wc are the child subsegments or NONE.
+// seed != 0: push every edge of the new triangles (a point on an edge gets no
+// empty-circle guarantee for the edge halves).
 __device__ void split_edge_A(const DevMesh& m, const TriAux& x, const WorkLists& w, u32 t, int e,
-                             u32 wv, u32 t2, u32 u2, u32 s_bw, u32 s_wc, u32 round) {
+                             u32 wv, u32 t2, u32 u2, u32 s_bw, u32 s_wc, u32 round,
+                             RoundCtr* rc = nullptr, int seed = 0, Counters* ctr = nullptr) {
     const uint4 ov = m.tv[t], on = m.tn[t], os = m.ts[t];
     const u32 a = comp(ov, e), b = comp(ov, nxt(e)), c = comp(ov, prv(e));
     const u32 uc = comp(on, e);
@@ -94,7 +112,12 @@ __device__ void split_edge_A(const DevMesh& m, const TriAux& x, const WorkLists&
         x.emap[3 * t + e] = NONE;
         m.vtri[wv] = NONE;
         const u32 tl[2] = {t, t2};
-        push_touched(w, tl, 2);
+        push_touched(w, tl, 2, rc);
+        if (seed) {
+            const u32 codes[6] = {enc(t, 0), enc(t, 1), enc(t, 2), enc(t2, 0), enc(t2, 1),
+                                  enc(t2, 2)};
+            push_work(w, 0, codes, 6, ctr, rc);
+        }
         return;
     }
     const u32 u = etri(uc);
@@ -120,45 +143,25 @@ __device__ void split_edge_A(const DevMesh& m, const TriAux& x, const WorkLists&
     x.emap[3 * u + f] = NONE;
     m.vtri[wv] = NONE;
     const u32 tl[4] = {t, t2, u, u2};
-    push_touched(w, tl, 4);
+    push_touched(w, tl, 4, rc);
+    if (seed) {
+        const u32 codes[12] = {enc(t, 0), enc(t, 1), enc(t, 2), enc(t2, 0), enc(t2, 1),
+                               enc(t2, 2), enc(u, 0), enc(u, 1), enc(u, 2), enc(u2, 0),
+                               enc(u2, 1), enc(u2, 2)};
+        push_work(w, 0, codes, 12, ctr, rc);
+    }
 }
 
 // ---- planning + phase-1 splits ----------------------------------------------------
 
-// Needs of each surviving candidate (refine.hpp:493-539); subsegments that
-// hit the depth cap or fail subsegment_split_ok are abandoned (:501-506).
+// Needs of each surviving candidate (plan_one, gdp2d_phases.cuh).
 __global__ void k_plan_ops(DevMesh m, DevCands c, u32 n, u64 depth_cap, InsertBufs b,
                            Counters* ctr) {
     const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
     u32 dropped = 0;
     if (i < n) {
-        u32 nv = 0, nt = 0, ns = 0;
-        if (c.alive[i]) {
-            if (c.kind[i] == 0) {
-                const u32 s = c.id[i];
-                if (!m.salive[s]) {
-                    dropped = 1;
-                } else if ((u64)m.sdepth[s] >= depth_cap || !subseg_split_ok(m, s, c.pt[i])) {
-                    m.senc[s] = 0;
-                    dropped = 1;
-                } else {
-                    const u32 t = c.loc[i];
-                    const int e = seg_slot(m.ts[t], s);
-                    const bool far = comp(m.tn[t], e) != NONE;
-                    nv = 1;
-                    nt = far ? 2 : 1;
-                    ns = 2;
-                }
-            } else if (c.lkind[i] == 0) {
-                nv = 1;
-                nt = 2;
-            } else if (c.lkind[i] == 1) {
-                const bool far = comp(m.tn[c.loc[i]], c.ledge[i]) != NONE;
-                nv = 1;
-                nt = far ? 2 : 1;
-            }
-            if (!nv) c.alive[i] = 0;
-        }
+        u32 nv, nt, ns;
+        dropped = plan_one(m, c, i, depth_cap, nv, nt, ns);
         b.nv[i] = nv;
         b.nt[i] = nt;
         b.ns[i] = ns;
@@ -166,55 +169,66 @@ __global__ void k_plan_ops(DevMesh m, DevCands c, u32 n, u64 depth_cap, InsertBu
     warp_add_u32(&ctr->dropped, dropped);
 }
 
+// One surviving candidate's phase-1 insertion (refine.hpp:492-539).
+// Returns 1 = midpoint, 2 = circumcenter, 0 = nothing.
+__device__ __forceinline__ int apply_one(const DevMesh& m, const DevCands& c, u32 i, u32 batch,
+                                         u32 round, const InsertBufs& b, const TriAux& x,
+                                         const FreshInfo& f, const WorkLists& w, RoundCtr* rc,
+                                         int seed, Counters* ctr) {
+    if (!b.nv[i]) return 0;
+    const u32 wv = m.nV + b.ov[i];
+    const u32 nt0 = m.nT + b.ot[i];
+    const double2 p = c.pt[i];
+    m.xy[wv] = p;
+    m.vkind[wv] = c.kind[i] == 0 ? 1 : 2;
+    m.vbirth[wv] = batch;
+    m.valive[wv] = 1;
+    const u32 fi = b.ov[i];
+    f.key[fi] = c.key[i];
+    f.tie[fi] = ((u64)c.tie[i] << 32) | i;
+    f.cc[fi] = c.kind[i] == 1;
+    f.removed[fi] = 0;
+    f.mark[fi] = 0;
+    const u32 t = c.loc[i];
+    if (c.kind[i] == 0) {
+        const u32 s = c.id[i];
+        const int e = seg_slot(m.ts[t], s);
+        const uint4 tv = m.tv[t];
+        const u32 bb = comp(tv, nxt(e)), ccv = comp(tv, prv(e));
+        const u32 s_bw = m.nS + b.os[i], s_wc = s_bw + 1;
+        const u32 par = m.sparent[s], dep = m.sdepth[s] + 1;
+        m.sv[s_bw] = make_uint2(bb, wv);
+        m.sv[s_wc] = make_uint2(wv, ccv);
+        m.sparent[s_bw] = par;
+        m.sparent[s_wc] = par;
+        m.senc[s_bw] = 0;
+        m.senc[s_wc] = 0;
+        m.salive[s_bw] = 1;
+        m.salive[s_wc] = 1;
+        m.sdepth[s_bw] = dep;
+        m.sdepth[s_wc] = dep;
+        m.stri[s_bw] = NONE;
+        m.stri[s_wc] = NONE;
+        m.salive[s] = 0;
+        m.senc[s] = 0;
+        split_edge_A(m, x, w, t, e, wv, nt0, nt0 + 1, s_bw, s_wc, round, rc, seed, ctr);
+        return 1;
+    }
+    if (c.lkind[i] == 0)
+        split_triangle_A(m, x, w, t, wv, nt0, nt0 + 1, round, rc, seed, ctr);
+    else
+        split_edge_A(m, x, w, t, c.ledge[i], wv, nt0, nt0 + 1, NONE, NONE, round, rc, seed, ctr);
+    return 2;
+}
+
 __global__ void k_apply_splits(DevMesh m, DevCands c, u32 n, u32 batch, u32 round, InsertBufs b,
                                TriAux x, FreshInfo f, WorkLists w, Counters* ctr) {
     const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
     u32 mid = 0, cc = 0;
-    if (i < n && b.nv[i]) {
-        const u32 wv = m.nV + b.ov[i];
-        const u32 nt0 = m.nT + b.ot[i];
-        const double2 p = c.pt[i];
-        m.xy[wv] = p;
-        m.vkind[wv] = c.kind[i] == 0 ? 1 : 2;
-        m.vbirth[wv] = batch;
-        m.valive[wv] = 1;
-        const u32 fi = b.ov[i];
-        f.key[fi] = c.key[i];
-        f.tie[fi] = ((u64)c.tie[i] << 32) | i;
-        f.cc[fi] = c.kind[i] == 1;
-        f.removed[fi] = 0;
-        f.mark[fi] = 0;
-        const u32 t = c.loc[i];
-        if (c.kind[i] == 0) {
-            const u32 s = c.id[i];
-            const int e = seg_slot(m.ts[t], s);
-            const uint4 tv = m.tv[t];
-            const u32 bb = comp(tv, nxt(e)), ccv = comp(tv, prv(e));
-            const u32 s_bw = m.nS + b.os[i], s_wc = s_bw + 1;
-            const u32 par = m.sparent[s], dep = m.sdepth[s] + 1;
-            m.sv[s_bw] = make_uint2(bb, wv);
-            m.sv[s_wc] = make_uint2(wv, ccv);
-            m.sparent[s_bw] = par;
-            m.sparent[s_wc] = par;
-            m.senc[s_bw] = 0;
-            m.senc[s_wc] = 0;
-            m.salive[s_bw] = 1;
-            m.salive[s_wc] = 1;
-            m.sdepth[s_bw] = dep;
-            m.sdepth[s_wc] = dep;
-            m.stri[s_bw] = NONE;
-            m.stri[s_wc] = NONE;
-            m.salive[s] = 0;
-            m.senc[s] = 0;
-            split_edge_A(m, x, w, t, e, wv, nt0, nt0 + 1, s_bw, s_wc, round);
-            mid = 1;
-        } else if (c.lkind[i] == 0) {
-            split_triangle_A(m, x, w, t, wv, nt0, nt0 + 1, round);
-            cc = 1;
-        } else {
-            split_edge_A(m, x, w, t, c.ledge[i], wv, nt0, nt0 + 1, NONE, NONE, round);
-            cc = 1;
-        }
+    if (i < n) {
+        const int r = apply_one(m, c, i, batch, round, b, x, f, w, w.rc, 0, ctr);
+        mid = r == 1;
+        cc = r == 2;
     }
     warp_add_u32(&ctr->ins_mid, mid);
     warp_add_u32(&ctr->ins_cc, cc);
@@ -321,7 +335,7 @@ __device__ __forceinline__ void flip_test_one(const DevMesh& m, u32 code, const 
     const u32 key = enc(t, e);
     atomicMin(&x.owner[t], key);
     atomicMin(&x.owner[u], key);
-    const u32 o = atomicAdd(&rc->cand, 1u);
+    const u32 o = agg_reserve(&rc->cand, 1u);
     if (o < w.cap) {
         w.fc[o] = key;
         w.fu[o] = enc(u, f);
@@ -511,43 +525,48 @@ __device__ __forceinline__ bool prio_gt(const FreshInfo& f, u32 a, u32 b) {
 // (a) a same-batch circumcenter that encroaches a splittable subsegment of
 // its star is redundant; the lowest-id such subsegment is marked.
 template <int MODE>
+__device__ __noinline__ u32 detect_a_one(const DevMesh& m, u64 depth_cap, u32 V0, u32 j,
+                                         const FreshInfo& f, Counters* ctr) {
+    u32 marked = 0;
+    uint8_t mark = 0;
+    const u32 v = V0 + j;
+    if (f.cc[j] && !f.removed[j]) {
+        u32 st[MAX_STAR];
+        int si[MAX_STAR];
+        const int k = walk_star(m, v, st, si, MAX_STAR);
+        if (k == 0) raise_err(ctr, DERR_OPEN_STAR, v);
+        const double2 pv = m.xy[v];
+        u32 best = NONE;
+        for (int q = 0; q < k; ++q) {
+            const u32 s = comp(m.ts[st[q]], si[q]);
+            if (s == NONE || s >= best) continue;
+            const uint2 sv = m.sv[s];
+            if (!encroaches<MODE>(m.xy[sv.x], m.xy[sv.y], pv)) continue;
+            if ((u64)m.sdepth[s] >= depth_cap) continue;
+            if (!subseg_split_ok(m, s, subseg_mid(m, s))) continue;
+            best = s;
+        }
+        if (best != NONE) {
+            mark = 1;
+            if (atomicExch(&m.senc[best], 1u) == 0u) marked = 1;
+        }
+    }
+    f.mark[j] = mark;
+    return marked;
+}
+
+template <int MODE>
 __global__ void k_detect_a(DevMesh m, u64 depth_cap, u32 V0, u32 F, FreshInfo f, Counters* ctr) {
     const u32 j = blockIdx.x * blockDim.x + threadIdx.x;
     u32 marked = 0;
-    if (j < F) {
-        uint8_t mark = 0;
-        const u32 v = V0 + j;
-        if (f.cc[j] && !f.removed[j]) {
-            u32 st[MAX_STAR];
-            int si[MAX_STAR];
-            const int k = walk_star(m, v, st, si, MAX_STAR);
-            if (k == 0) raise_err(ctr, DERR_OPEN_STAR, v);
-            const double2 pv = m.xy[v];
-            u32 best = NONE;
-            for (int q = 0; q < k; ++q) {
-                const u32 s = comp(m.ts[st[q]], si[q]);
-                if (s == NONE || s >= best) continue;
-                const uint2 sv = m.sv[s];
-                if (!encroaches<MODE>(m.xy[sv.x], m.xy[sv.y], pv)) continue;
-                if ((u64)m.sdepth[s] >= depth_cap) continue;
-                if (!subseg_split_ok(m, s, subseg_mid(m, s))) continue;
-                best = s;
-            }
-            if (best != NONE) {
-                mark = 1;
-                if (atomicExch(&m.senc[best], 1u) == 0u) marked = 1;
-            }
-        }
-        f.mark[j] = mark;
-    }
+    if (j < F) marked = detect_a_one<MODE>(m, depth_cap, V0, j, f, ctr);
     warp_add_u32(&ctr->marked, marked);
 }
 
 // (b) Delaunay-dependent pairs: a same-batch circumcenter adjacent to a
 // higher-priority one (not itself redundant) is removed.
-__global__ void k_detect_b(DevMesh m, u32 V0, u32 F, FreshInfo f, Counters* ctr) {
-    const u32 j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= F) return;
+__device__ __noinline__ void detect_b_one(const DevMesh& m, u32 V0, u32 F, u32 j,
+                                          const FreshInfo& f) {
     if (!f.cc[j] || f.removed[j] || f.mark[j] == 1) return;
     const u32 v = V0 + j;
     u32 st[MAX_STAR];
@@ -565,15 +584,27 @@ __global__ void k_detect_b(DevMesh m, u32 V0, u32 F, FreshInfo f, Counters* ctr)
     }
 }
 
-__global__ void k_detect_collect(u32 V0, u32 F, FreshInfo f, WorkLists w, Counters* ctr) {
+__global__ void k_detect_b(DevMesh m, u32 V0, u32 F, FreshInfo f, Counters* ctr) {
     const u32 j = blockIdx.x * blockDim.x + threadIdx.x;
-    u32 red = 0, dep = 0;
-    if (j < F && !f.removed[j] && f.mark[j]) {
-        const u32 o = atomicAdd(&w.rc->detect, 1u);
+    if (j < F) detect_b_one(m, V0, F, j, f);
+}
+
+// Removal list of a detection pass; returns (redundant, dependent) flags.
+__device__ __forceinline__ void detect_collect_one(u32 V0, u32 j, const FreshInfo& f,
+                                                   const WorkLists& w, RoundCtr* rc, u32& red,
+                                                   u32& dep) {
+    if (!f.removed[j] && f.mark[j]) {
+        const u32 o = agg_reserve(&rc->detect, 1u);
         if (o < w.rm_cap) w.rm[0][o] = V0 + j;
         red = f.mark[j] == 1;
         dep = f.mark[j] == 2;
     }
+}
+
+__global__ void k_detect_collect(u32 V0, u32 F, FreshInfo f, WorkLists w, Counters* ctr) {
+    const u32 j = blockIdx.x * blockDim.x + threadIdx.x;
+    u32 red = 0, dep = 0;
+    if (j < F) detect_collect_one(V0, j, f, w, w.rc, red, dep);
     warp_add_u32(&ctr->rm_red, red);
     warp_add_u32(&ctr->rm_dep, dep);
 }
@@ -592,10 +623,8 @@ void launch_detect(const DevMesh& m, const Quality& q, u64 depth_cap, u32 V0, u3
 
 // ---- parallel vertex removal (remove_free_vertex + flop, mesh.hpp:261-304,442-466) ----
 
-__global__ void k_rm_claim(DevMesh m, const u32* __restrict__ list, u32 n, TriAux x,
-                           WorkLists w, Counters* ctr) {
-    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+__device__ __forceinline__ void rm_claim_one(const DevMesh& m, const u32* __restrict__ list, u32 i,
+                                             const TriAux& x, const WorkLists& w, Counters* ctr) {
     const u32 v = list[i];
     u32* st = w.star + (size_t)i * MAX_STAR;
     int si[MAX_STAR];
@@ -609,24 +638,29 @@ __global__ void k_rm_claim(DevMesh m, const u32* __restrict__ list, u32 n, TriAu
     for (int q = 0; q < k; ++q) atomicMin(&x.owner[st[q]], v);
 }
 
+__global__ void k_rm_claim(DevMesh m, const u32* __restrict__ list, u32 n, TriAux x,
+                           WorkLists w, Counters* ctr) {
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) rm_claim_one(m, list, i, x, w, ctr);
+}
+
 // Remove v by ear-clipping its link polygon: each ear is one degree-reducing
 // flip of remove_free_vertex (both orient tests of mesh.hpp:223-225), the
 // last three link vertices are the flop.  The k star triangles become k-2
 // (ids reused in star order), the last two die.
-__global__ void __launch_bounds__(64) k_rm_apply(DevMesh m, const u32* __restrict__ list, u32 n,
-                                                 u32 round, u32 V0, u32 widx, u32 next_list,
-                                                 TriAux x, FreshInfo f, WorkLists w,
-                                                 Counters* ctr) {
-    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+__device__ __noinline__ u32 rm_apply_one(const DevMesh& m, const u32* __restrict__ list, u32 i,
+                                         u32 round, u32 V0, u32 widx, u32 next_list,
+                                         const TriAux& x, const FreshInfo& f, const WorkLists& w,
+                                         RoundCtr* rc, Counters* ctr) {
     u32 done = 0;
-    if (i < n) {
+    {
         const u32 v = list[i];
         const u32* st = w.star + (size_t)i * MAX_STAR;
         const int k = (int)w.star_len[i];
         bool own = k >= 3;
         for (int q = 0; q < k && own; ++q) own = x.owner[st[q]] == v;
         if (k >= 3 && !own) {
-            const u32 o = atomicAdd(&w.rc->rm_next, 1u);
+            const u32 o = agg_reserve(&rc->rm_next, 1u);
             if (o < w.rm_cap) w.rm[next_list][o] = v;
         } else if (own) {
             // Link polygon, CCW: L[j] = p_j; link edge j = (L[j], L[j+1]).
@@ -757,24 +791,37 @@ __global__ void __launch_bounds__(64) k_rm_apply(DevMesh m, const u32* __restric
                 m.valive[v] = 0;
                 m.vtri[v] = NONE;
                 f.removed[v - V0] = 1;
-                push_touched(w, st, created);
+                push_touched(w, st, created, rc);
                 for (int ci = 0; ci < created; ++ci) {
                     const u32 codes[3] = {enc(st[ci], 0), enc(st[ci], 1), enc(st[ci], 2)};
-                    push_work(w, widx, codes, 3, ctr);
+                    push_work(w, widx, codes, 3, ctr, rc);
                 }
                 done = 1;
             }
         }
     }
+    return done;
+}
+
+__global__ void __launch_bounds__(64) k_rm_apply(DevMesh m, const u32* __restrict__ list, u32 n,
+                                                 u32 round, u32 V0, u32 widx, u32 next_list,
+                                                 TriAux x, FreshInfo f, WorkLists w,
+                                                 Counters* ctr) {
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    u32 done = 0;
+    if (i < n) done = rm_apply_one(m, list, i, round, V0, widx, next_list, x, f, w, w.rc, ctr);
     warp_add_u32(&ctr->rm_done, done);
+}
+
+__device__ __forceinline__ void rm_post_one(u32 i, const TriAux& x, const WorkLists& w) {
+    const u32* st = w.star + (size_t)i * MAX_STAR;
+    const u32 k = w.star_len[i];
+    for (u32 q = 0; q < k; ++q) x.owner[st[q]] = NONE;
 }
 
 __global__ void k_rm_post(u32 n, TriAux x, WorkLists w) {
     const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const u32* st = w.star + (size_t)i * MAX_STAR;
-    const u32 k = w.star_len[i];
-    for (u32 q = 0; q < k; ++q) x.owner[st[q]] = NONE;
+    if (i < n) rm_post_one(i, x, w);
 }
 
 void launch_removal_round(const DevMesh& m, u32 round, u32 V0, TriAux a, FreshInfo f,
@@ -787,6 +834,539 @@ void launch_removal_round(const DevMesh& m, u32 round, u32 V0, TriAux a, FreshIn
     note_launch(), k_rm_post<<<(n + 255) / 256, 256, 0, st>>>(n, a, w);
     const u32 nt = n * (MAX_STAR - 2);
     note_launch(), k_fixup<<<(nt + 255) / 256, 256, 0, st>>>(m, round, a, w, nt, 0, 0, d_ctr);
+}
+
+// =====================================================================================
+// The whole insertion phase (Line 8: refine.hpp:464-610) as ONE persistent
+// cooperative launch per batch: phase-1 splits, fixup, Lawson fixpoint, and
+// the detect / rollback loop of phase 3 with its Lawson passes -- every
+// data-dependent loop runs on the device, so a batch needs no host round
+// trip between its phases.
+//
+// Execution contexts (Exec): grid mode (all CTAs, grid barriers) or block
+// mode (CTA 0 alone, __syncthreads).  Block mode is Rule 1 of the paper
+// applied to the tail: when a batch inserts only a few
+// hundred points, or a Lawson work list drops below a block's worth, the
+// work runs in one CTA and a barrier costs tens of nanoseconds instead of a
+// grid-wide synchronisation.
+//
+// Per-step counters live in a ring of 4 RoundCtr; the leader zeroes the slot
+// of step k+1 at the start of step k (at least one barrier separates that
+// write from its first use, and no slot is read more than one step late).
+// =====================================================================================
+
+struct Exec {
+    u32 tid, nthr;
+    bool block;  // block mode: CTA 0 only
+    __device__ __forceinline__ void sync() const {
+        if (block)
+            __syncthreads();
+        else
+            cg::this_grid().sync();
+    }
+    __device__ __forceinline__ bool leader() const { return tid == 0; }
+};
+
+__device__ __forceinline__ Exec grid_exec() {
+    cg::grid_group g = cg::this_grid();
+    return Exec{(u32)g.thread_rank(), (u32)g.size(), false};
+}
+__device__ __forceinline__ Exec block_exec() { return Exec{threadIdx.x, blockDim.x, true}; }
+
+__device__ __forceinline__ u32 vload(const u32* p) { return *(const volatile u32*)p; }
+
+struct InsertArgs {
+    DevMesh m;            // counts BEFORE this batch's insertions
+    DevCands c;
+    InsertBufs b;
+    TriAux x;
+    FreshInfo f;
+    WorkLists w;
+    RoundCtr* ring;       // [4], zeroed by the host before the launch
+    u32* state;           // [0] status, [1] steps, [2] flip rounds, [3] removal rounds, [4..7] handoff
+    Counters* ctr;
+    const u32* d_C;       // candidate count (collect)
+    u64 depth_cap;
+    u32 batch;            // batch epoch written into vert_birth
+    u32 round0;           // first stamp round of this batch
+    u32 vcap, tcap, scap; // mesh capacities
+    u32 small_nv;         // block mode when the batch inserts <= small_nv points
+    u32 small_wl;         // Lawson switches to block mode below this many work items
+    u32 max_steps;        // safety bound on barrier steps
+    // Lines 5-7 (locate / claim / cavity) + the phase-1 plan and its scan
+    u32 ncav, rs;         // cavity bound and region stride
+    u32* regions;
+    u32* region_len;
+    u32* scan_part;       // [3 * grid] per-CTA chunk sums of the insertion plan
+    u32 small_c;          // block mode for the whole batch when C <= small_c
+    int resume;           // 1: candidates are planned, start at the capacity check
+    int filter;           // 1: run Lines 5-7 in kernel 1 (tiny batches)
+    unsigned long long* trace;   // GDP2D_TRACE: (globaltimer << 8 | tag) per step, or null
+    u32* trace_n;
+    u32 trace_cap;
+};
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Step tags of the device trace (printed by the host under GDP2D_TRACE=1).
+enum : u32 { TR_START = 1, TR_APPLY, TR_FIXUP, TR_FTEST, TR_FAPPLY, TR_FPOST, TR_DET_A, TR_DET_B,
+             TR_DET_C, TR_RM_CLAIM, TR_RM_APPLY, TR_RM_POST, TR_BLOCK_IN, TR_BLOCK_OUT, TR_END,
+             TR_LOCATE, TR_CLAIM, TR_CAVITY, TR_PLAN };
+
+__device__ __forceinline__ void trace(const InsertArgs& a, bool leader, u32 tag) {
+    if (a.trace && leader) {
+        const u32 i = atomicAdd(a.trace_n, 1u);
+        if (i < a.trace_cap) a.trace[i] = (globaltimer() << 8) | tag;
+    }
+}
+
+enum : u32 { INS_OK = 0, INS_GROW = 1, INS_STEPS = 2 };
+
+__device__ __forceinline__ RoundCtr* ring_at(const InsertArgs& a, u32 step) {
+    return a.ring + (step & 3u);
+}
+__device__ __forceinline__ void ring_advance(const InsertArgs& a, const Exec& ex, u32 step) {
+    if (ex.leader()) {
+        RoundCtr* z = a.ring + ((step + 1u) & 3u);
+        z->wl_next = z->cand = z->touched = z->rm_next = z->detect = 0;
+    }
+}
+
+// Lawson rounds (test + claim | apply | post + fixup) until the work list in
+// w.w[cur] (n items) is empty.  step / cur are uniform across ex.
+__device__ void lawson_rounds(const InsertArgs& a, const Exec& ex, const DevMesh& m, u32& step,
+                              u32& cur, u32 n, ull& flipped, u32& rounds) {
+    const WorkLists& w = a.w;
+    while (n > 0 && step < a.max_steps) {
+        RoundCtr* rc = ring_at(a, step);
+        ring_advance(a, ex, step);
+        const u32 round = a.round0 + step;
+        const u32* wl = w.w[cur];
+        for (u32 i = ex.tid; i < n; i += ex.nthr) flip_test_one(m, wl[i], a.x, w, rc, a.ctr);
+        ex.sync();
+        trace(a, ex.leader(), TR_FTEST);
+        const u32 nc = min(vload(&rc->cand), w.cap);
+        for (u32 i = ex.tid; i < nc; i += ex.nthr)
+            flipped += flip_apply_one(m, i, round, cur ^ 1u, a.x, w, rc, a.ctr);
+        ex.sync();
+        trace(a, ex.leader(), TR_FAPPLY);
+        for (u32 i = ex.tid; i < nc; i += ex.nthr)
+            flip_post_one(i, round, cur ^ 1u, a.x, w, rc, a.ctr);
+        const u32 nt = min(vload(&rc->touched), w.cap);
+        for (u32 i = ex.tid; i < nt; i += ex.nthr)
+            fixup_one(m, round, a.x, w, w.touched[i], 0, 0, rc, a.ctr);
+        ex.sync();
+        trace(a, ex.leader(), TR_FPOST);
+        n = vload(&rc->wl_next);
+        if (n > w.cap) {
+            raise_err(a.ctr, DERR_WORKLIST_OVERFLOW, n);
+            n = 0;
+        }
+        cur ^= 1u;
+        ++step;
+        ++rounds;
+    }
+}
+
+// Lawson fixpoint from grid mode: small work lists finish in CTA 0 alone.
+__device__ void lawson_fixpoint_dev(const InsertArgs& a, const Exec& ex, const DevMesh& m,
+                                    u32& step, u32& cur, u32 n, ull& flipped, u32& rounds) {
+    if (ex.block) {
+        lawson_rounds(a, ex, m, step, cur, n, flipped, rounds);
+        return;
+    }
+    while (n > 0 && step < a.max_steps) {
+        if (n <= a.small_wl) {
+            if (blockIdx.x == 0) {
+                const Exec bx = block_exec();
+                trace(a, bx.leader(), TR_BLOCK_IN);
+                u32 s2 = step, c2 = cur, r2 = 0;
+                lawson_rounds(a, bx, m, s2, c2, n, flipped, r2);
+                trace(a, bx.leader(), TR_BLOCK_OUT);
+                if (threadIdx.x == 0) {
+                    a.state[4] = s2;
+                    a.state[5] = c2;
+                    a.state[6] = r2;
+                }
+            }
+            ex.sync();
+            step = vload(&a.state[4]);
+            cur = vload(&a.state[5]);
+            rounds += vload(&a.state[6]);
+            ex.sync();   // everyone has read the handoff before it can be reused
+            return;
+        }
+        // one grid-wide round, then re-evaluate the list size
+        RoundCtr* rc = ring_at(a, step);
+        ring_advance(a, ex, step);
+        const u32 round = a.round0 + step;
+        const u32* wl = a.w.w[cur];
+        for (u32 i = ex.tid; i < n; i += ex.nthr) flip_test_one(m, wl[i], a.x, a.w, rc, a.ctr);
+        ex.sync();
+        trace(a, ex.leader(), TR_FTEST);
+        const u32 nc = min(vload(&rc->cand), a.w.cap);
+        for (u32 i = ex.tid; i < nc; i += ex.nthr)
+            flipped += flip_apply_one(m, i, round, cur ^ 1u, a.x, a.w, rc, a.ctr);
+        ex.sync();
+        trace(a, ex.leader(), TR_FAPPLY);
+        for (u32 i = ex.tid; i < nc; i += ex.nthr)
+            flip_post_one(i, round, cur ^ 1u, a.x, a.w, rc, a.ctr);
+        const u32 nt = min(vload(&rc->touched), a.w.cap);
+        for (u32 i = ex.tid; i < nt; i += ex.nthr)
+            fixup_one(m, round, a.x, a.w, a.w.touched[i], 0, 0, rc, a.ctr);
+        ex.sync();
+        trace(a, ex.leader(), TR_FPOST);
+        n = vload(&rc->wl_next);
+        if (n > a.w.cap) {
+            raise_err(a.ctr, DERR_WORKLIST_OVERFLOW, n);
+            n = 0;
+        }
+        cur ^= 1u;
+        ++step;
+        ++rounds;
+    }
+}
+
+// Lines 5-7 for the whole candidate list (tiny batches; big ones run the
+// high-occupancy standalone kernels of k_locate.cu / k_filter.cu instead),
+// then the phase-1 plan and its exclusive scan (three 0/1 streams packed into one u64 per
+// candidate inside a CTA chunk; chunk sums cross CTAs through scan_part).
+template <int MODE>
+__device__ void filter(const InsertArgs& a, const Exec& ex, u32 C) {
+    const DevMesh& m = a.m;
+    ull steps = 0, visits = 0;
+    u32 surv1 = 0, surv2 = 0;
+    for (u32 i = ex.tid; i < C; i += ex.nthr) steps += locate_one(m, a.c, i);
+    ex.sync();
+    trace(a, ex.leader(), TR_LOCATE);
+    for (u32 i = ex.tid; i < C; i += ex.nthr) claim_max_one(a.c, i, a.x.ckey);
+    ex.sync();
+    for (u32 i = ex.tid; i < C; i += ex.nthr) claim_tie_one(a.c, i, a.x.ckey, a.x.ctie);
+    ex.sync();
+    for (u32 i = ex.tid; i < C; i += ex.nthr) surv1 += claim_check_one(a.c, i, a.x.ckey, a.x.ctie);
+    ex.sync();
+    for (u32 i = ex.tid; i < C; i += ex.nthr) claim_reset_one(a.c, i, m.nT, a.x.ckey, a.x.ctie);
+    ex.sync();
+    trace(a, ex.leader(), TR_CLAIM);
+    for (u32 i = ex.tid; i < C; i += ex.nthr)
+        visits += cavity_bfs_one(m, a.c, i, a.ncav, 1, a.rs, a.regions, a.region_len, nullptr,
+                                 a.x.ckey);
+    ex.sync();
+    for (u32 i = ex.tid; i < C; i += ex.nthr)
+        cavity_tie_one(a.c, i, a.rs, a.regions, a.region_len, a.x.ckey, a.x.ctie);
+    ex.sync();
+    for (u32 i = ex.tid; i < C; i += ex.nthr)
+        surv2 += cavity_check_one(a.c, i, a.rs, a.regions, a.region_len, a.x.ckey, a.x.ctie);
+    ex.sync();
+    for (u32 i = ex.tid; i < C; i += ex.nthr)
+        cavity_reset_one(i, a.rs, a.regions, a.region_len, a.x.ckey, a.x.ctie);
+    trace(a, ex.leader(), TR_CAVITY);
+    warp_add_ull(&a.ctr->walk_steps, steps);
+    warp_add_ull(&a.ctr->cavity_visits, visits);
+    warp_add_u32(&a.ctr->surv_claim, surv1);
+    warp_add_u32(&a.ctr->surv_cavity, surv2);
+}
+
+__device__ void plan_and_scan(const InsertArgs& a, const Exec& ex, u32 C) {
+    const DevMesh& m = a.m;
+    u32 dropped = 0;
+
+    // plan + chunk sums: CTA b owns candidates [b*chunk, (b+1)*chunk)
+    __shared__ unsigned long long sh64[INSERT_BLOCK / 32 + 1];
+    const u32 nblk = ex.block ? 1u : gridDim.x;
+    const u32 b = ex.block ? 0u : blockIdx.x;
+    const u32 chunk = ((C + nblk - 1) / nblk + INSERT_BLOCK - 1) / INSERT_BLOCK * INSERT_BLOCK;
+    const u32 lo = min(C, b * chunk), hi = min(C, lo + chunk);
+    // fields: nv (bits 0-20), far (21-41), mid (42-62); a chunk is < 2^21
+    unsigned long long local = 0;
+    for (u32 i = lo + threadIdx.x; i < hi; i += INSERT_BLOCK) {
+        u32 nv, nt, ns;
+        dropped += plan_one(m, a.c, i, a.depth_cap, nv, nt, ns);
+        a.b.nv[i] = nv;
+        a.b.nt[i] = nt;
+        a.b.ns[i] = ns;
+        local += (unsigned long long)nv | ((unsigned long long)(nt - nv) << 21) |
+                 ((unsigned long long)(ns >> 1) << 42);
+    }
+    unsigned long long tot;
+    block_exclusive_t<INSERT_BLOCK, unsigned long long>(local, sh64, &tot);
+    if (threadIdx.x == 0) {
+        a.scan_part[3 * b + 0] = (u32)(tot & 0x1FFFFF);
+        a.scan_part[3 * b + 1] = (u32)((tot >> 21) & 0x1FFFFF);
+        a.scan_part[3 * b + 2] = (u32)((tot >> 42) & 0x1FFFFF);
+    }
+    ex.sync();
+    // CTA prefix = sum of the chunk sums of the CTAs before it
+    u32 p0 = 0, p1 = 0, p2 = 0;
+    for (u32 k = threadIdx.x; k < b; k += INSERT_BLOCK) {
+        p0 += a.scan_part[3 * k];
+        p1 += a.scan_part[3 * k + 1];
+        p2 += a.scan_part[3 * k + 2];
+    }
+    __shared__ u32 shp[INSERT_BLOCK / 32 + 1];
+    p0 = block_sum<INSERT_BLOCK>(p0, shp);
+    p1 = block_sum<INSERT_BLOCK>(p1, shp);
+    p2 = block_sum<INSERT_BLOCK>(p2, shp);
+    __shared__ u32 pre[3];
+    if (threadIdx.x == 0) {
+        pre[0] = p0;
+        pre[1] = p1;
+        pre[2] = p2;
+    }
+    __syncthreads();
+    u32 c0 = pre[0], c1 = pre[1], c2 = pre[2];
+    for (u32 base = lo; base < hi; base += INSERT_BLOCK) {
+        const u32 i = base + threadIdx.x;
+        unsigned long long v = 0;
+        if (i < hi)
+            v = (unsigned long long)a.b.nv[i] | ((unsigned long long)(a.b.nt[i] - a.b.nv[i]) << 21) |
+                ((unsigned long long)(a.b.ns[i] >> 1) << 42);
+        unsigned long long t;
+        const unsigned long long ex64 = block_exclusive_t<INSERT_BLOCK, unsigned long long>(v, sh64, &t);
+        if (i < hi) {
+            const u32 e0 = (u32)(ex64 & 0x1FFFFF), e1 = (u32)((ex64 >> 21) & 0x1FFFFF),
+                      e2 = (u32)((ex64 >> 42) & 0x1FFFFF);
+            a.b.ov[i] = c0 + e0;
+            a.b.ot[i] = c0 + e0 + c1 + e1;
+            a.b.os[i] = 2u * (c2 + e2);
+        }
+        c0 += (u32)(t & 0x1FFFFF);
+        c1 += (u32)((t >> 21) & 0x1FFFFF);
+        c2 += (u32)((t >> 42) & 0x1FFFFF);
+    }
+    if (b == nblk - 1 && threadIdx.x == 0) {
+        a.b.totals[0] = c0;
+        a.b.totals[1] = c0 + c1;
+        a.b.totals[2] = 2u * c2;
+    }
+    warp_add_u32(&a.ctr->dropped, dropped);
+    ex.sync();
+    trace(a, ex.leader(), TR_PLAN);
+}
+
+// Phase 1 (splits) + the Lawson fixpoint.  step / flip_rounds / flips are
+// left in state[] for the rollback kernel.
+__device__ void split_and_flip(const InsertArgs& a, const Exec& ex, u32 nv, u32 nt, u32 ns) {
+    const u32 C = vload(a.d_C);
+    const WorkLists& w = a.w;
+    DevMesh m = a.m;   // pre-insertion counts: new ids are m.nV + offset, ...
+    u32 step = 0, cur = 0, flip_rounds = 0;
+    ull flipped = 0;
+    u32 mid = 0, cc = 0;
+    RoundCtr* rc = ring_at(a, step);
+    ring_advance(a, ex, step);
+    {
+        const u32 round = a.round0 + step;
+        for (u32 i = ex.tid; i < C; i += ex.nthr) {
+            const int r = apply_one(m, a.c, i, a.batch, round, a.b, a.x, a.f, w, rc, 1, a.ctr);
+            mid += r == 1;
+            cc += r == 2;
+        }
+        m.nV += nv;
+        m.nT += nt;
+        m.nS += ns;
+        ex.sync();
+        trace(a, ex.leader(), TR_APPLY);
+        const u32 ntouch = min(vload(&rc->touched), w.cap);
+        for (u32 i = ex.tid; i < ntouch; i += ex.nthr)
+            fixup_one(m, round, a.x, w, w.touched[i], 0, 0, rc, a.ctr);
+        ex.sync();
+        trace(a, ex.leader(), TR_FIXUP);
+    }
+    const u32 n = vload(&rc->wl_next);
+    ++step;
+    lawson_fixpoint_dev(a, ex, m, step, cur, n, flipped, flip_rounds);
+    warp_add_u32(&a.ctr->ins_mid, mid);
+    warp_add_u32(&a.ctr->ins_cc, cc);
+    warp_add_ull(&a.ctr->flips, flipped);
+    if (ex.leader()) {
+        a.state[0] = step >= a.max_steps ? INS_STEPS : INS_OK;
+        a.state[1] = step;
+        a.state[2] = flip_rounds;
+        a.state[3] = 0;
+    }
+}
+
+// Phase 3 (refine.hpp:551-608): detection + parallel rollback to fixpoint,
+// each removal round followed by its Lawson pass.
+template <int MODE>
+__device__ void rollback_loop(const InsertArgs& a, const Exec& ex, u32 nv, u32 nt, u32 ns) {
+    const WorkLists& w = a.w;
+    DevMesh m = a.m;
+    m.nV += nv;
+    m.nT += nt;
+    m.nS += ns;
+    u32 step = vload(&a.state[1]), cur = 0, flip_rounds = 0, rm_rounds = 0;
+    ull flipped = 0;
+    u32 marked = 0, red = 0, dep = 0, done = 0;
+    const u32 V0 = a.m.nV, F = nv;
+    ex.sync();   // every thread has read state[1] before the leader rewrites it
+    while (step < a.max_steps) {
+        RoundCtr* rc = ring_at(a, step);
+        ring_advance(a, ex, step);
+        for (u32 j = ex.tid; j < F; j += ex.nthr) marked += detect_a_one<MODE>(m, a.depth_cap, V0, j, a.f, a.ctr);
+        ex.sync();
+        trace(a, ex.leader(), TR_DET_A);
+        for (u32 j = ex.tid; j < F; j += ex.nthr) detect_b_one(m, V0, F, j, a.f);
+        ex.sync();
+        trace(a, ex.leader(), TR_DET_B);
+        for (u32 j = ex.tid; j < F; j += ex.nthr) {
+            u32 r1 = 0, r2 = 0;
+            detect_collect_one(V0, j, a.f, w, rc, r1, r2);
+            red += r1;
+            dep += r2;
+        }
+        ex.sync();
+        trace(a, ex.leader(), TR_DET_C);
+        u32 nrm = min(vload(&rc->detect), w.rm_cap);
+        ++step;
+        if (nrm == 0) break;
+        u32 rcur = 0;
+        while (nrm > 0 && step < a.max_steps) {
+            rc = ring_at(a, step);
+            ring_advance(a, ex, step);
+            const u32 round = a.round0 + step;
+            const u32* list = w.rm[rcur];
+            for (u32 i = ex.tid; i < nrm; i += ex.nthr) rm_claim_one(m, list, i, a.x, w, a.ctr);
+            ex.sync();
+            trace(a, ex.leader(), TR_RM_CLAIM);
+            for (u32 i = ex.tid; i < nrm; i += ex.nthr)
+                done += rm_apply_one(m, list, i, round, V0, 0, rcur ^ 1u, a.x, a.f, w, rc, a.ctr);
+            ex.sync();
+            trace(a, ex.leader(), TR_RM_APPLY);
+            for (u32 i = ex.tid; i < nrm; i += ex.nthr) rm_post_one(i, a.x, w);
+            const u32 ntouch = min(vload(&rc->touched), w.cap);
+            for (u32 i = ex.tid; i < ntouch; i += ex.nthr)
+                fixup_one(m, round, a.x, w, w.touched[i], 0, 0, rc, a.ctr);
+            ex.sync();
+            trace(a, ex.leader(), TR_RM_POST);
+            const u32 nl = vload(&rc->wl_next);
+            const u32 nnext = min(vload(&rc->rm_next), w.rm_cap);
+            ++step;
+            ++rm_rounds;
+            cur = 0;
+            lawson_fixpoint_dev(a, ex, m, step, cur, nl, flipped, flip_rounds);
+            nrm = nnext;
+            rcur ^= 1u;
+        }
+    }
+    warp_add_u32(&a.ctr->marked, marked);
+    warp_add_u32(&a.ctr->rm_red, red);
+    warp_add_u32(&a.ctr->rm_dep, dep);
+    warp_add_u32(&a.ctr->rm_done, done);
+    warp_add_ull(&a.ctr->flips, flipped);
+    trace(a, ex.leader(), TR_END);
+    if (ex.leader()) {
+        if (step >= a.max_steps) a.state[0] = INS_STEPS;
+        a.state[1] = step;
+        a.state[2] += flip_rounds;
+        a.state[3] = rm_rounds;
+    }
+}
+
+__device__ __forceinline__ bool fits_and_status(const InsertArgs& a, u32 nv, u32 nt, u32 ns) {
+    const bool fits = (u64)a.m.nV + nv <= a.vcap && (u64)a.m.nT + nt <= a.tcap &&
+                      (u64)a.m.nS + ns <= a.scap && nv <= a.f.cap && nv <= a.w.rm_cap &&
+                      12ull * nv <= a.w.cap;
+    const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+    if (!fits && lead) {
+        a.state[0] = INS_GROW;
+        a.state[1] = 0;
+    }
+    if (fits && nv == 0 && lead) a.state[0] = a.state[1] = a.state[2] = a.state[3] = 0;
+    return fits && nv > 0;
+}
+
+// Kernel 1 of a batch after collect: [Lines 5-7 when the batch is small] +
+// the phase-1 plan + splits + Lawson.  Block mode (CTA 0 alone) when the
+// candidate list is small -- the long tail of the refinement (Rule 1).
+template <int MODE>
+__global__ void __launch_bounds__(INSERT_BLOCK, GDP2D_SPLIT_MINB) k_batch_split(InsertArgs a) {
+    const u32 C = vload(a.d_C);
+    const bool block = C <= a.small_c;
+    if (block && blockIdx.x != 0) return;
+    const Exec ex = block ? block_exec() : grid_exec();
+    if (!a.resume) {
+        trace(a, ex.leader(), TR_START);
+        if (a.filter) filter<MODE>(a, ex, C);
+        plan_and_scan(a, ex, C);
+    }
+    const u32 nv = vload(&a.b.totals[0]), nt = vload(&a.b.totals[1]), ns = vload(&a.b.totals[2]);
+    if (!fits_and_status(a, nv, nt, ns)) return;   // uniform
+    split_and_flip(a, ex, nv, nt, ns);
+}
+
+// Kernel 2: phase 3 rollback (skipped when kernel 1 asked for growth).
+template <int MODE>
+__global__ void __launch_bounds__(INSERT_BLOCK) k_batch_rollback(InsertArgs a) {
+    if (vload(&a.state[0]) != INS_OK) return;
+    const u32 nv = vload(&a.b.totals[0]), nt = vload(&a.b.totals[1]), ns = vload(&a.b.totals[2]);
+    if (nv == 0) return;
+    const bool block = nv <= a.small_c;
+    if (block && blockIdx.x != 0) return;
+    const Exec ex = block ? block_exec() : grid_exec();
+    rollback_loop<MODE>(a, ex, nv, nt, ns);
+}
+
+template <class K0, class K1>
+static int coop_grid(K0 k0, K1 k1, int device) {
+    int sms = 0, per0 = 0, per1 = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per0, k0, INSERT_BLOCK, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per1, k1, INSERT_BLOCK, 0);
+    return std::max(1, sms * std::max(1, std::min(per0, per1)));
+}
+
+int insert_persistent_grid(int device) {
+    return coop_grid(k_batch_split<0>, k_batch_split<1>, device);
+}
+int rollback_persistent_grid(int device) {
+    return coop_grid(k_batch_rollback<0>, k_batch_rollback<1>, device);
+}
+
+void launch_insert_persistent(const InsertLaunch& L, int mode, int grid, int grid2, cudaStream_t st) {
+    InsertArgs a;
+    a.m = L.m;
+    a.c = L.c;
+    a.b = L.b;
+    a.x = L.x;
+    a.f = L.f;
+    a.w = L.w;
+    a.ring = L.ring;
+    a.state = L.state;
+    a.ctr = L.ctr;
+    a.d_C = L.d_C;
+    a.depth_cap = L.depth_cap;
+    a.batch = L.batch;
+    a.round0 = L.round0;
+    a.vcap = L.vcap;
+    a.tcap = L.tcap;
+    a.scap = L.scap;
+    a.small_nv = L.small_nv;
+    a.small_wl = L.small_wl;
+    a.max_steps = L.max_steps;
+    a.ncav = L.ncav;
+    a.rs = L.rs;
+    a.regions = L.regions;
+    a.region_len = L.region_len;
+    a.scan_part = L.scan_part;
+    a.small_c = L.small_c;
+    a.resume = L.resume;
+    a.filter = L.filter;
+    a.trace = L.trace;
+    a.trace_n = L.trace_n;
+    a.trace_cap = L.trace_cap;
+    void* args[] = {&a};
+    note_launch();
+    cudaLaunchCooperativeKernel(mode ? (void*)k_batch_split<1> : (void*)k_batch_split<0>, dim3(grid),
+                                dim3(INSERT_BLOCK), args, 0, st);
+    note_launch();
+    cudaLaunchCooperativeKernel(mode ? (void*)k_batch_rollback<1> : (void*)k_batch_rollback<0>,
+                                dim3(grid2), dim3(INSERT_BLOCK), args, 0, st);
 }
 
 }  // namespace gdp2d

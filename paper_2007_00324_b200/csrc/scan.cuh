@@ -8,36 +8,42 @@
 namespace gdp2d {
 
 // Inclusive warp scan.
-__device__ __forceinline__ u32 warp_inclusive(u32 v) {
+template <class T>
+__device__ __forceinline__ T warp_inclusive_t(T v) {
     const int lane = threadIdx.x & 31;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        const u32 n = __shfl_up_sync(0xFFFFFFFFu, v, o);
+        const T n = __shfl_up_sync(0xFFFFFFFFu, v, o);
         if (lane >= o) v += n;
     }
     return v;
 }
+__device__ __forceinline__ u32 warp_inclusive(u32 v) { return warp_inclusive_t<u32>(v); }
 
 // Exclusive block scan of one value per thread.  `sh` needs BLOCK/32 + 1
-// words.  Returns the exclusive prefix; *total gets the block sum.  All
+// elements.  Returns the exclusive prefix; *total gets the block sum.  All
 // threads of the block must call it.
-template <int BLOCK>
-__device__ __forceinline__ u32 block_exclusive(u32 v, u32* sh, u32* total) {
+template <int BLOCK, class T>
+__device__ __forceinline__ T block_exclusive_t(T v, T* sh, T* total) {
     constexpr int NW = BLOCK / 32;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const u32 inc = warp_inclusive(v);
+    const T inc = warp_inclusive_t<T>(v);
     if (lane == 31) sh[warp] = inc;
     __syncthreads();
     if (warp == 0) {
-        u32 w = lane < NW ? sh[lane] : 0u;
-        w = warp_inclusive(w);
+        T w = lane < NW ? sh[lane] : T(0);
+        w = warp_inclusive_t<T>(w);
         if (lane < NW) sh[lane] = w;
     }
     __syncthreads();
-    const u32 pre = warp ? sh[warp - 1] : 0u;
+    const T pre = warp ? sh[warp - 1] : T(0);
     *total = sh[NW - 1];
     __syncthreads();
     return pre + inc - v;
+}
+template <int BLOCK>
+__device__ __forceinline__ u32 block_exclusive(u32 v, u32* sh, u32* total) {
+    return block_exclusive_t<BLOCK, u32>(v, sh, total);
 }
 
 template <int BLOCK>
@@ -52,6 +58,20 @@ __device__ __forceinline__ u32 block_sum(u32 v, u32* sh) {
         for (int i = 0; i < NW; ++i) t += sh[i];
     __syncthreads();
     return t;  // valid in thread 0 only
+}
+
+// Block-aggregated counter add: one global atomic per CTA instead of one per
+// warp (a same-address atomic per warp still serialises ~10^4 deep at mesh
+// scale).  Every thread of the block must call it.
+template <class T>
+__device__ __forceinline__ void block_add(T* ctr, T v) {
+    __shared__ T acc;
+    if (threadIdx.x == 0) acc = 0;
+    __syncthreads();
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xFFFFFFFFu, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(&acc, v);
+    __syncthreads();
+    if (threadIdx.x == 0 && acc) atomicAdd(ctr, acc);
 }
 
 }  // namespace gdp2d
