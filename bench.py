@@ -15,9 +15,11 @@ Keys beyond the base contract:
   e2e          the same metric through the C ABI entry point gdp2d_refine with
                HOST buffers (H2D of the input mesh + D2H of the refined mesh
                inside the timed region)
-  roofline     the Line-3 full scan kernel (k_collect_flags): algorithmic bytes
-               (16 B/triangle + 16 B/vertex + 48 B/subsegment per launch) over its
-               CUDA-event time, against MEASURED_PEAKS.json hbm_gbs
+  roofline     the engine kernel with the largest share of the step (CUDA events
+               on the engine stream, every launch in the timed region): its
+               algorithmic bytes per launch over its average
+               launch time, against MEASURED_PEAKS.json hbm_gbs; traffic = ncu
+               dram bytes per launch from profiles/traffic.json when present
   cpu_baseline the reference (oracle/_ref, unmodified cdtref headers) timed on a
                bounded sample of the same workload on this box's host cores
 """
@@ -268,12 +270,33 @@ def main():
     e2e_total = dist.max(sum(e2e_s))
     e2e_value = dist.sum(e2e_st) / e2e_total
 
-    # ---- roofline of the Line-3 full scan kernel ----
+    # ---- roofline: the dominant engine kernel (largest share of the step) ----
     peak, peak_kind = load_peaks()
-    scan_s = sum(r.scan_seconds for r in reps)
-    scan_b = sum(r.scan_bytes for r in reps)
-    scan_n = sum(r.scan_launches for r in reps)
-    achieved = (scan_b / scan_n) / (scan_s / scan_n) / 1e9 if scan_n and scan_s > 0 else None
+    kernels = {
+        "k_collect_flags": ("Line-3 scan (incremental bad/encroached flags)",
+                            sum(r.scan_seconds for r in reps), sum(r.scan_bytes for r in reps),
+                            sum(r.scan_launches for r in reps)),
+        "k_batch_split": ("Lines 5-8a: plan + splits + Lawson flips (persistent)",
+                          sum(r.split_seconds for r in reps), sum(r.split_bytes for r in reps),
+                          sum(r.split_launches for r in reps)),
+        "k_batch_rollback": ("Line 8b: redundancy detection + rollback + Lawson (persistent)",
+                             sum(r.rollback_seconds for r in reps),
+                             sum(r.rollback_bytes for r in reps),
+                             sum(r.rollback_launches for r in reps)),
+    }
+    traffic_db = {}
+    tp = ROOT / "profiles" / "traffic.json"
+    if tp.exists():
+        traffic_db = json.loads(tp.read_text()).get(f"config{a.config}", {})
+    per_kernel = {}
+    for name, (what, ks, kb, kn) in kernels.items():
+        ach = (kb / ks / 1e9) if ks > 0 else None
+        per_kernel[name] = {"what": what, "achieved": ach, "frac": (ach / peak) if ach else None,
+                            "bytes_per_launch": kb / kn if kn else None,
+                            "ms_per_launch": ks / kn * 1e3 if kn else None,
+                            "share_of_step": ks / dev_s if dev_s else None,
+                            "traffic": traffic_db.get(name)}
+    dom = max(per_kernel, key=lambda k: per_kernel[k]["share_of_step"] or 0.0)
     refine_gbs = last.algorithmic_bytes() / last.device_seconds / 1e9
 
     line = {
@@ -290,11 +313,13 @@ def main():
         "quality": {"bad_triangles": last.bad_triangles, "min_angle_deg": last.min_angle_deg},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "wall_s_per_step": e2e_total / e2e_steps},
-        "roofline": {"kernel": "k_collect_flags (Line-3 full scan)", "bound": "hbm",
-                     "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": (achieved / peak) if achieved else None, "traffic": None,
-                     "bytes_per_launch": scan_b / scan_n if scan_n else None,
-                     "share_of_step": scan_s / dev_s if dev_s else None},
+        "roofline": {"kernel": dom, "bound": "hbm", "achieved": per_kernel[dom]["achieved"],
+                     "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": per_kernel[dom]["frac"], "traffic": per_kernel[dom]["traffic"],
+                     "bytes_per_launch": per_kernel[dom]["bytes_per_launch"],
+                     "share_of_step": per_kernel[dom]["share_of_step"],
+                     "bytes_formula": "DESIGN.md section 3 / include/gdp2d.h gdp2d_report"},
+        "roofline_kernels": per_kernel,
         "roofline_refine": {"bytes_alg": last.algorithmic_bytes(), "achieved": refine_gbs,
                             "frac": refine_gbs / peak, "unit": "GB/s",
                             "formula": "SURVEY 8(d) bytes_alg / device refine time"},

@@ -175,6 +175,17 @@ typedef struct gdp2d_report {
     uint64_t scan_bytes;
     uint64_t scan_launches;
     uint64_t kernel_launches;    /* engine kernels launched by this call      */
+    /* roofline instrumentation of the persistent batch kernels (k_batch_split:
+     * plan + splits + Lawson; k_batch_rollback: detection + rollback + Lawson):
+     * CUDA-event time summed over launches and algorithmic bytes
+     * (32 B/candidate planned + 128 B/insertion + 128 B/flip; 64 B/fresh vertex
+     * detected + 128 B/flip + 128 B/removal). */
+    double   split_seconds;
+    uint64_t split_bytes;
+    uint64_t split_launches;
+    double   rollback_seconds;
+    uint64_t rollback_bytes;
+    uint64_t rollback_launches;
 } gdp2d_report;
 
 /* SplitCandidate (refine.hpp:71) in exchange form. */

@@ -74,7 +74,10 @@ class Report(C.Structure):
                 ("sum_tris_alive", C.c_uint64), ("sum_verts_alive", C.c_uint64),
                 ("sum_subsegs_alive", C.c_uint64), ("device_seconds", C.c_double),
                 ("scan_seconds", C.c_double), ("scan_bytes", C.c_uint64),
-                ("scan_launches", C.c_uint64), ("kernel_launches", C.c_uint64)]
+                ("scan_launches", C.c_uint64), ("kernel_launches", C.c_uint64),
+                ("split_seconds", C.c_double), ("split_bytes", C.c_uint64),
+                ("split_launches", C.c_uint64), ("rollback_seconds", C.c_double),
+                ("rollback_bytes", C.c_uint64), ("rollback_launches", C.c_uint64)]
 
 
 class Candidate(C.Structure):

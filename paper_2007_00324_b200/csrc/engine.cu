@@ -80,6 +80,7 @@ void mesh_free(MeshStore& s) {
     dfree(m.xy); dfree(m.vkind); dfree(m.vbirth); dfree(m.valive); dfree(m.vtri);
     dfree(m.tv); dfree(m.tn); dfree(m.ts);
     dfree(m.sv); dfree(m.sparent); dfree(m.senc); dfree(m.salive); dfree(m.stri); dfree(m.sdepth);
+    dfree(m.tflag); dfree(m.sflag);
     s.vcap = s.tcap = s.scap = 0;
 }
 
@@ -97,6 +98,7 @@ void mesh_reserve(MeshStore& s, u32 V, u32 T, u32 S, cudaStream_t st) {
         dgrow(m.tv, m.nT, T, st);
         dgrow(m.tn, m.nT, T, st);
         dgrow(m.ts, m.nT, T, st);
+        dgrow(m.tflag, m.nT, T, st);
         s.tcap = T;
     }
     if (S > s.scap) {
@@ -106,6 +108,7 @@ void mesh_reserve(MeshStore& s, u32 V, u32 T, u32 S, cudaStream_t st) {
         dgrow(m.salive, m.nS, S, st);
         dgrow(m.stri, m.nS, S, st);
         dgrow(m.sdepth, m.nS, S, st);
+        dgrow(m.sflag, m.nS, S, st);
         s.scap = S;
     }
 }
@@ -205,17 +208,21 @@ struct Tracer {
     const char* name[48] = {};
     int n = 0;
     unsigned long long* d_trace = nullptr;
+    u32* d_trace_val = nullptr;
     u32* d_trace_n = nullptr;
+    bool rounds = false;   // GDP2D_TRACE=2: also print every Lawson round
     static constexpr u32 kCap = 1u << 16;
     void init() {
         for (auto& e : ev) cudaEventCreate(&e);
         cudaMalloc(&d_trace, sizeof(unsigned long long) * kCap);
+        cudaMalloc(&d_trace_val, sizeof(u32) * kCap);
         cudaMalloc(&d_trace_n, sizeof(u32));
     }
     void release() {
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
         if (d_trace) cudaFree(d_trace);
+        if (d_trace_val) cudaFree(d_trace_val);
         if (d_trace_n) cudaFree(d_trace_n);
     }
     void mark(const char* what, cudaStream_t st) {
@@ -239,7 +246,9 @@ struct Tracer {
         cnt = std::min(cnt, kCap);
         if (cnt > 1) {
             std::vector<unsigned long long> t(cnt);
+            std::vector<u32> val(cnt);
             cudaMemcpy(t.data(), d_trace, sizeof(unsigned long long) * cnt, cudaMemcpyDeviceToHost);
+            cudaMemcpy(val.data(), d_trace_val, sizeof(u32) * cnt, cudaMemcpyDeviceToHost);
             static const char* tags[] = {"?", "start", "apply", "fixup", "ftest", "fapply", "fpost",
                                          "detA", "detB", "detC", "rmclaim", "rmapply", "rmpost",
                                          "blkin", "blkout", "end", "locate", "claim", "cavity",
@@ -260,6 +269,15 @@ struct Tracer {
                 if (cntt[k]) fprintf(stderr, " %s=%.1f/%d", tags[k], sum[k], cntt[k]);
             fprintf(stderr, " total=%.1f (us/steps)\n",
                     double((t[cnt - 1] >> 8) - (t[0] >> 8)) * 1e-3);
+            if (rounds) {
+                fprintf(stderr, "[trace] batch %u steps:", batch);
+                for (u32 i = 1; i < cnt; ++i) {
+                    const u32 tag = (u32)(t[i] & 0xFF);
+                    const double dt = double((t[i] >> 8) - (t[i - 1] >> 8)) * 1e-3;
+                    fprintf(stderr, " %s:%u:%.1f", tag < NT ? tags[tag] : "?", val[i], dt);
+                }
+                fprintf(stderr, "\n");
+            }
         }
     }
 };
@@ -296,7 +314,6 @@ struct gdp2d_ctx {
     void* qscratch = nullptr;
     u32 round = 0;
     bool full_scan = true;        // next collect recomputes every triangle
-    u32 collect_round = 0, collect_nT = 0;
     bool validate = false;        // GDP2D_VALIDATE=1: check structure after every round
     bool lawson_rounds = false;   // GDP2D_LAWSON=rounds: per-round launches
     bool full_collect = false;    // GDP2D_COLLECT=full: never reuse cached flags
@@ -307,6 +324,9 @@ struct gdp2d_ctx {
     RoundCtr* ring = nullptr;     // [4] step counters of the persistent insertion kernel
     u32* ins_state = nullptr;     // [8] its status words
     u32* h_state = nullptr;       // pinned copy
+    cudaEvent_t ev_k[3] = {};     // around the split and rollback kernels
+    double k_split_s = 0, k_rb_s = 0;   // per refine call: roofline accumulators
+    u64 k_split_b = 0, k_rb_b = 0, k_launches = 0;
     u32* d_C = nullptr;           // candidate count written by collect (device)
     u32 small_nv = 256;           // GDP2D_SMALL_NV: block-mode insertion at or below
     u32 small_wl = 256;           // GDP2D_SMALL_WL: block-mode Lawson below this list size
@@ -367,10 +387,9 @@ void ensure_aux(gdp2d_ctx* x) {
     const u32 T = x->work.tcap;
     if (T > x->aux_cap) {
         dfree(x->aux.ckey); dfree(x->aux.ctie); dfree(x->aux.owner); dfree(x->aux.stamp);
-        dfree(x->aux.emap); dfree(x->aux.tbad);
+        dfree(x->aux.emap);
         dalloc(x->aux.ckey, T); dalloc(x->aux.ctie, T); dalloc(x->aux.owner, T);
-        dalloc(x->aux.stamp, T); dalloc(x->aux.emap, 3ull * T); dalloc(x->aux.tbad, T);
-        x->full_scan = true;  // stamps restart: the cached flags are unusable
+        dalloc(x->aux.stamp, T); dalloc(x->aux.emap, 3ull * T);
         CK(cudaMemsetAsync(x->aux.ckey, 0, sizeof(u64) * T, x->st));
         CK(cudaMemsetAsync(x->aux.ctie, 0xFF, sizeof(u64) * T, x->st));
         CK(cudaMemsetAsync(x->aux.owner, 0xFF, sizeof(u32) * T, x->st));
@@ -411,10 +430,10 @@ void ensure_worklists(gdp2d_ctx* x, u64 n) {
 void ensure_fresh(gdp2d_ctx* x, u32 n) {
     if (n <= x->fresh.cap) return;
     FreshInfo& f = x->fresh;
-    dfree(f.key); dfree(f.tie); dfree(f.cc); dfree(f.removed); dfree(f.mark);
+    dfree(f.key); dfree(f.tie); dfree(f.cc); dfree(f.removed); dfree(f.mark); dfree(f.dirty);
     const u32 cap = std::max<u32>(n + n / 2, 1024);
     dalloc(f.key, cap); dalloc(f.tie, cap); dalloc(f.cc, cap); dalloc(f.removed, cap);
-    dalloc(f.mark, cap);
+    dalloc(f.mark, cap); dalloc(f.dirty, cap);
     f.cap = cap;
     dfree(x->wl.rm[0]); dfree(x->wl.rm[1]); dfree(x->wl.star); dfree(x->wl.star_len);
     dalloc(x->wl.rm[0], cap); dalloc(x->wl.rm[1], cap);
@@ -552,10 +571,11 @@ void ctx_init(gdp2d_ctx* x, int device) {
     x->rollback_grid = rollback_persistent_grid(device);
     const char* li = std::getenv("GDP2D_INSERT");
     x->legacy_insert = (li && std::string(li) == "legacy") || x->validate || x->lawson_rounds;
-    dalloc(x->ring, 4);
+    dalloc(x->ring, 5);   // 4-slot step ring + the removal-seed accumulator
     dalloc(x->d_C, 1);
-    if (const char* e = std::getenv("GDP2D_TRACE"); e && e[0] == '1') {
+    if (const char* e = std::getenv("GDP2D_TRACE"); e && (e[0] == '1' || e[0] == '2')) {
         x->tr.on = true;
+        x->tr.rounds = e[0] == '2';
         x->tr.init();
     }
     if (const char* e = std::getenv("GDP2D_SMALL_NV")) x->small_nv = (u32)std::strtoul(e, nullptr, 10);
@@ -569,6 +589,7 @@ void ctx_init(gdp2d_ctx* x, int device) {
     dalloc(x->rcs, 1024);
     dalloc(x->d_res, 4);
     for (auto& e : x->ev) CK(cudaEventCreate(&e));
+    for (auto& e : x->ev_k) CK(cudaEventCreate(&e));
 }
 
 void ctx_release(gdp2d_ctx* x) {
@@ -576,13 +597,13 @@ void ctx_release(gdp2d_ctx* x) {
     mesh_free(x->work);
     mesh_free(x->pristine);
     dfree(x->aux.ckey); dfree(x->aux.ctie); dfree(x->aux.owner); dfree(x->aux.stamp);
-    dfree(x->aux.emap); dfree(x->aux.tbad); dfree(x->flags);
+    dfree(x->aux.emap); dfree(x->flags);
     cands_free(x->c);
     dfree(x->regions); dfree(x->region_len); dfree(x->bfs_len);
     dfree(x->ib.nv); dfree(x->ib.nt); dfree(x->ib.ns); dfree(x->ib.ov); dfree(x->ib.ot);
     dfree(x->ib.os); dfree(x->ib.totals);
     dfree(x->fresh.key); dfree(x->fresh.tie); dfree(x->fresh.cc); dfree(x->fresh.removed);
-    dfree(x->fresh.mark);
+    dfree(x->fresh.mark); dfree(x->fresh.dirty);
     dfree(x->wl.w[0]); dfree(x->wl.w[1]); dfree(x->wl.fc); dfree(x->wl.fu);
     dfree(x->wl.touched); dfree(x->wl.fwin); dfree(x->wl.rm[0]); dfree(x->wl.rm[1]);
     dfree(x->wl.star); dfree(x->wl.star_len); dfree(x->wl.rc);
@@ -605,6 +626,8 @@ void ctx_release(gdp2d_ctx* x) {
     dfree(x->ins_state);
     if (x->h_state) cudaFreeHost(x->h_state);
     for (auto& e : x->ev)
+        if (e) cudaEventDestroy(e);
+    for (auto& e : x->ev_k)
         if (e) cudaEventDestroy(e);
     if (x->st) cudaStreamDestroy(x->st);
 }
@@ -823,7 +846,7 @@ void insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, u32 C, u32 ncav, u32
     (void)C;
     cudaStream_t st = x->st;
     for (int attempt = 0;; ++attempt) {
-        CK(cudaMemsetAsync(x->ring, 0, 4 * sizeof(RoundCtr), st));
+        CK(cudaMemsetAsync(x->ring, 0, 5 * sizeof(RoundCtr), st));
         InsertLaunch L;
         L.m = x->work.m;
         L.c = x->c;
@@ -831,6 +854,9 @@ void insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, u32 C, u32 ncav, u32
         L.x = x->aux;
         L.f = x->fresh;
         L.w = x->wl;
+        L.w.vdirty = x->fresh.dirty;          // fixup flags rewritten fresh stars
+        L.w.fresh_v0 = x->work.m.nV;          // fresh ids start here ...
+        L.w.fresh_n = x->fresh.cap;           // ... and never exceed the buffer
         L.ring = x->ring;
         L.state = x->ins_state;
         L.ctr = x->d_ctr;
@@ -854,13 +880,17 @@ void insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, u32 C, u32 ncav, u32
         L.filter = C <= x->small_c ? 1 : 0;
         if (x->tr.on) {
             L.trace = x->tr.d_trace;
+            L.trace_val = x->tr.d_trace_val;
             L.trace_n = x->tr.d_trace_n;
             L.trace_cap = Tracer::kCap;
             CK(cudaMemsetAsync(x->tr.d_trace_n, 0, sizeof(u32), st));
         }
         x->tr.mark("pre_ins", st);
+        CK(cudaMemsetAsync(x->ins_state, 0, 8 * sizeof(u32), st));
+        CK(cudaEventRecord(x->ev_k[0], st));
         launch_insert_persistent(L, p->mode == GDP2D_CHEW ? 1 : 0, x->insert_grid,
-                                 x->rollback_grid, st);
+                                 x->rollback_grid, st, x->ev_k[1]);
+        CK(cudaEventRecord(x->ev_k[2], st));
         x->tr.mark("insert_kernel", st);
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(x->h_state, x->ins_state, 8 * sizeof(u32), cudaMemcpyDeviceToHost, st));
@@ -878,6 +908,18 @@ void insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, u32 C, u32 ncav, u32
             continue;
         }
         if (x->h_state[0] == 2u) throw Fail{GDP2D_EMESH, "insertion exceeded its step bound"};
+        {
+            // roofline instrumentation of the two persistent kernels
+            const Counters& h = *x->h_ctr;
+            const u64 ins = h.ins_mid + h.ins_cc;
+            const u64 f_split = x->h_state[7];
+            const u64 f_rb = h.flips >= f_split ? h.flips - f_split : 0;
+            x->k_split_s += ev_ms(x->ev_k[0], x->ev_k[1]) * 1e-3;
+            x->k_split_b += 32ull * C + 128ull * ins + 128ull * f_split;
+            x->k_rb_s += ev_ms(x->ev_k[1], x->ev_k[2]) * 1e-3;
+            x->k_rb_b += 64ull * nv + 128ull * f_rb + 128ull * h.rm_done;
+            x->k_launches += 1;
+        }
         x->round += x->h_state[1] + 1;
         flip_rounds = x->h_state[2];
         rm_rounds = x->h_state[3];
@@ -887,6 +929,14 @@ void insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, u32 C, u32 ncav, u32
         return;
     }
 }
+
+// Algorithmic bytes of one Line-3 scan launch (k_collect_flags): every
+// element reads its 1 B cached verdict and writes its 1 B flag, every
+// subsegment reads alive + the sticky encroached flag (5 B); a re-evaluated
+// (dirty) element moves its 16 B record + three 16 B corner gathers (64 B,
+// SURVEY 8(d)'s per-triangle figure; the subsegment record + apex gathers
+// are taken as the same 64 B).
+u64 scan_alg_bytes(u64 nT, u64 nS, u64 dirty) { return 2 * (nT + nS) + 5 * nS + 64 * dirty; }
 
 // The refinement loop (refine.hpp:651-713) on the working mesh.
 void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
@@ -900,6 +950,8 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
     std::memset(r, 0, sizeof *r);
     r->batches = keep.batches;
     r->batches_capacity = keep.batches_capacity;
+    x->k_split_s = x->k_rb_s = 0;
+    x->k_split_b = x->k_rb_b = x->k_launches = 0;
     CK(cudaEventRecord(x->ev[GDP2D_NPHASES + 1], st));  // loop start
     for (u64 iter = 0;; ++iter) {
         if (iter >= p->iteration_cap) {
@@ -918,34 +970,25 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
         CK(cudaEventRecord(x->ev[0], st));
         x->tr.mark("start", st);
         CollectCache cache;
-        cache.stamp = x->aux.stamp;
-        cache.tbad = x->aux.tbad;
-        cache.last_round = x->collect_round;
-        cache.nT_last = x->collect_nT;
         cache.full = (x->full_scan || x->full_collect) ? 1 : 0;
         bool tris_scanned = false;
         const u32 C = launch_collect(m, q, p->rule4_unified_collection != 0, x->flags, x->c,
                                      x->ccap, x->scan, x->d_ctr, st, cache, &tris_scanned,
                                      x->d_C, x->ev[GDP2D_NPHASES + 2], x->ev[GDP2D_NPHASES + 3]);
-        if (tris_scanned) {
-            // the cached triangle flags are current as of this round
-            x->full_scan = false;
-            x->collect_round = x->round;
-            x->collect_nT = m.nT;
-        }
+        // a full scan has refreshed every cached verdict it covered; with
+        // rule 4 off and subsegment candidates, triangles were not scanned
+        if (tris_scanned) x->full_scan = false;
         CK(cudaGetLastError());
         // launch_collect synchronised: the scan events are complete
         r->scan_seconds += ev_ms(x->ev[GDP2D_NPHASES + 2], x->ev[GDP2D_NPHASES + 3]) * 1e-3;
-        // bytes the scan must move: 5 B per clean triangle (stamp + cached
-        // flag), 16 B record + 3 x 16 B corners + 5 B per re-evaluated one,
-        // 48 B per subsegment (SURVEY 8(d) per-unit figure); the dirty count
-        // arrives with the end-of-batch counters
+        // scan bytes (scan_alg_bytes); the dirty count arrives with the
+        // end-of-batch counters
         const u64 scan_nT = m.nT, scan_nS = m.nS;
         r->scan_launches += 1;
         x->tr.mark("collect", st);
         if (C == 0) {
             check_dev_err(x);
-            r->scan_bytes += 5ull * scan_nT + 64ull * x->h_ctr->scan_dirty + 48ull * scan_nS;
+            r->scan_bytes += scan_alg_bytes(scan_nT, scan_nS, x->h_ctr->scan_dirty);
             break;
         }
         CK(cudaEventRecord(x->ev[1], st));   // split points are fused into collect
@@ -998,7 +1041,7 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
         else
             raise_dev_err(x);   // counters came back with the insertion's status
         const Counters& h = *x->h_ctr;
-        r->scan_bytes += 5ull * scan_nT + 64ull * h.scan_dirty + 48ull * scan_nS;
+        r->scan_bytes += scan_alg_bytes(scan_nT, scan_nS, h.scan_dirty);
         const u32 inserted = h.ins_mid + h.ins_cc;
         const u32 retained = inserted - std::min(inserted, h.rm_done);
         x->alive_v += inserted;
@@ -1059,6 +1102,12 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
     }
     r->device_seconds = ev_ms(x->ev[GDP2D_NPHASES + 1], x->ev[GDP2D_NPHASES]) * 1e-3;
     r->kernel_launches = gdp2d::launch_counter() - launches0;
+    r->split_seconds = x->k_split_s;
+    r->split_bytes = x->k_split_b;
+    r->split_launches = x->k_launches;
+    r->rollback_seconds = x->k_rb_s;
+    r->rollback_bytes = x->k_rb_b;
+    r->rollback_launches = x->k_launches;
     r->wall_seconds =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
 }
@@ -1342,8 +1391,6 @@ int gdp2d_collect(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_candidate* out, uin
         ensure_cands(x, m.nS + m.nT);
         CK(cudaMemsetAsync(x->d_ctr, 0, sizeof(Counters), x->st));
         CollectCache cache;
-        cache.stamp = x->aux.stamp;
-        cache.tbad = x->aux.tbad;
         cache.full = 1;
         bool tris_scanned = false;
         const u32 C = launch_collect(m, make_quality(p), p->rule4_unified_collection != 0,

@@ -39,7 +39,6 @@ struct TriAux {
     u32* owner = nullptr;    // flip / removal claim
     u32* stamp = nullptr;    // round in which the triangle was rewritten
     u32* emap = nullptr;     // 3 per triangle: old edge slot -> new (tri<<2|edge)
-    uint8_t* tbad = nullptr; // cached is_bad && resolvable per triangle (incremental collect)
 };
 
 struct CollectBufs {
@@ -53,13 +52,10 @@ struct CollectBufs {
 // candidate count (synchronises).  If rule4 == false and subsegment
 // candidates exist, triangles are skipped (refine.hpp:239); *tris_scanned
 // then stays false and the caller must not advance the incremental cache
-// (the cached per-triangle flags were not refreshed).
+// (the cached per-triangle flags were not refreshed; with the dirty-bit
+// cache this only matters for the full flag).
 struct CollectCache {
-    const u32* stamp = nullptr;   // TriAux::stamp
-    uint8_t* tbad = nullptr;      // cached per-triangle flag
-    u32 last_round = 0;           // round id at the previous collect
-    u32 nT_last = 0;              // triangle count at the previous collect
-    int full = 1;                 // 1 = recompute every triangle
+    int full = 1;                 // 1 = recompute every element (ignore the dirty bits)
 };
 u32 launch_collect(const DevMesh& m, const Quality& q, bool rule4, uint8_t* flags, DevCands c,
                    u32 ccap, ScanScratch& s, Counters* d_ctr, cudaStream_t st,
@@ -94,6 +90,7 @@ struct FreshInfo {
     uint8_t* cc = nullptr;
     uint8_t* removed = nullptr;
     uint8_t* mark = nullptr;
+    uint8_t* dirty = nullptr;   // star rewritten since the last detection pass
     u32 cap = 0;
 };
 
@@ -110,6 +107,10 @@ struct WorkLists {
     u32 rm_cap = 0;
     RoundCtr* rc = nullptr;           // device round counters
     double* dbg = nullptr;            // debug dump: [0]=flag, [1]=k, [2..3]=v, then link xy
+    // fresh-vertex dirty marking by fixup (persistent insertion kernel only):
+    // a rewritten triangle flags its corners in [fresh_v0, fresh_v0 + fresh_n)
+    uint8_t* vdirty = nullptr;
+    u32 fresh_v0 = 0, fresh_n = 0;
 };
 
 void launch_plan_ops(const DevMesh& m, DevCands c, u32 n, u64 depth_cap, InsertBufs b,
@@ -145,7 +146,7 @@ struct InsertLaunch {
     TriAux x;
     FreshInfo f;
     WorkLists w;
-    RoundCtr* ring;       // [4] zeroed before the launch
+    RoundCtr* ring;       // [5] zeroed before the launch
     u32* state;           // [8] status / steps / flip rounds / removal rounds / handoff
     Counters* ctr;
     const u32* d_C;
@@ -161,6 +162,7 @@ struct InsertLaunch {
     int resume = 0;
     int filter = 1;
     unsigned long long* trace = nullptr;   // device step trace (GDP2D_TRACE=1)
+    u32* trace_val = nullptr;
     u32* trace_n = nullptr;
     u32 trace_cap = 0;
 };
@@ -169,7 +171,7 @@ int rollback_persistent_grid(int device);
 // Kernel 1 (plan + splits + Lawson, with Lines 5-7 when L.filter) then
 // kernel 2 (detect + rollback loop), both cooperative, no host sync between.
 void launch_insert_persistent(const InsertLaunch& L, int mode, int grid, int grid2,
-                              cudaStream_t st);
+                              cudaStream_t st, cudaEvent_t between = nullptr);
 
 // Redundancy detection (refine.hpp:551-608): fills w.rm[0], count in w.rc->detect.
 void launch_detect(const DevMesh& m, const Quality& q, u64 depth_cap, u32 V0, u32 F,

@@ -58,6 +58,12 @@ struct DevMesh {
     uint8_t* salive;
     u32* stri;
     u32* sdepth;
+    // collect cache: bit0 = cached verdict (is_bad_triangle && resolvable /
+    // geometric encroachment), bit1 = dirty.  Every triangle rewrite
+    // (write_tri) and kill sets 2 on the triangle and on its subsegments, so
+    // the Line-3 scan re-evaluates exactly the elements whose inputs changed.
+    uint8_t* tflag;
+    uint8_t* sflag;
     u32 nV, nT, nS;
 };
 

@@ -17,18 +17,16 @@ struct CollectRange {
     u32 tilesS, tilesT;  // tile counts
 };
 
-// Incremental mode (full == 0): a triangle untouched since the previous
-// collect (stamp <= last_round, id < nT_last) keeps its cached quality flag
-// tbad[t] -- its corners and hence is_bad_triangle are unchanged -- so the
-// scan reads 5 B instead of 16 B + three vertex gathers.  The candidate list is
-// identical to a full scan (same flags, same stable compaction).
+// Incremental mode (full == 0): an element whose dirty bit is clear keeps its
+// cached verdict -- its corners (and, for a subsegment, both adjacent
+// triangles and hence its apexes) are unchanged since the last scan -- so the
+// scan reads one byte instead of the 64 B record + corner gathers.  The
+// candidate list is bit-identical to a full scan (same flags, same stable
+// compaction); only the sticky encroached flag is read for every subsegment.
 template <int MODE>
 __global__ void __launch_bounds__(SCAN_BLOCK) k_collect_flags(DevMesh m, Quality q, CollectRange r,
                                                            uint8_t* __restrict__ flags,
-                                                           u32* __restrict__ partial,
-                                                           const u32* __restrict__ stamp,
-                                                           uint8_t* __restrict__ tbad,
-                                                           u32 last_round, u32 nT_last, int full,
+                                                           u32* __restrict__ partial, int full,
                                                            Counters* ctr) {
     __shared__ u32 sh[SCAN_BLOCK / 32 + 1];
     const bool is_sub = blockIdx.x < r.tilesS;
@@ -42,17 +40,31 @@ __global__ void __launch_bounds__(SCAN_BLOCK) k_collect_flags(DevMesh m, Quality
         uint8_t f = 0;
         if (i < n) {
             if (is_sub) {
-                if (m.salive[i] && (m.senc[i] || is_encroached<MODE>(m, i))) f = 1;
-            } else if (!full && i < nT_last && stamp[i] <= last_round) {
-                f = tbad[i];
-            } else {
-                const uint4 tv = m.tv[i];
-                if (tv.w) {
-                    const double2 a = m.xy[tv.x], b = m.xy[tv.y], c = m.xy[tv.z];
-                    if (is_bad_pts(a, b, c, q) && resolvable_pts(a, b, c)) f = 1;
+                if (m.salive[i]) {
+                    const uint8_t sf = full ? 2 : m.sflag[i];
+                    bool enc;
+                    if (sf & 2) {
+                        enc = is_encroached<MODE>(m, i);
+                        m.sflag[i] = enc ? 1 : 0;
+                        ++dirty;
+                    } else {
+                        enc = sf & 1;
+                    }
+                    f = (m.senc[i] || enc) ? 1 : 0;
                 }
-                tbad[i] = f;
-                ++dirty;
+            } else {
+                const uint8_t tf = full ? 2 : m.tflag[i];
+                if (tf & 2) {
+                    const uint4 tv = m.tv[i];
+                    if (tv.w) {
+                        const double2 a = m.xy[tv.x], b = m.xy[tv.y], c = m.xy[tv.z];
+                        if (is_bad_pts(a, b, c, q) && resolvable_pts(a, b, c)) f = 1;
+                    }
+                    m.tflag[i] = f;
+                    ++dirty;
+                } else {
+                    f = tf & 1;
+                }
             }
         }
         flags[(size_t)blockIdx.x * SCAN_TILE + (u32)k * SCAN_BLOCK + threadIdx.x] = f;
@@ -161,9 +173,9 @@ u32 launch_collect(const DevMesh& m, const Quality& q, bool rule4, uint8_t* flag
         }
         if (ev_scan0 && sub) cudaEventRecord(ev_scan0, st);
         if (q.mode == 0)
-            note_launch(), k_collect_flags<0><<<tiles, SCAN_BLOCK, 0, st>>>(m, q, r, flags, s.partial, cache.stamp, cache.tbad, cache.last_round, cache.nT_last, cache.full, d_ctr);
+            note_launch(), k_collect_flags<0><<<tiles, SCAN_BLOCK, 0, st>>>(m, q, r, flags, s.partial, cache.full, d_ctr);
         else
-            note_launch(), k_collect_flags<1><<<tiles, SCAN_BLOCK, 0, st>>>(m, q, r, flags, s.partial, cache.stamp, cache.tbad, cache.last_round, cache.nT_last, cache.full, d_ctr);
+            note_launch(), k_collect_flags<1><<<tiles, SCAN_BLOCK, 0, st>>>(m, q, r, flags, s.partial, cache.full, d_ctr);
         if (ev_scan1 && (tri || !rule4)) cudaEventRecord(ev_scan1, st);
         scan_partials(s.partial, tiles, d_count, st);
         u32 total = 0;

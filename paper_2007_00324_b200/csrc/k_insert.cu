@@ -40,12 +40,13 @@ __device__ __forceinline__ void write_tri(const DevMesh& m, u32 t, u32 a, u32 b,
     m.tv[t] = make_uint4(a, b, c, 1u);
     m.tn[t] = make_uint4(n0, n1, n2, pend);
     m.ts[t] = make_uint4(s0, s1, s2, 0u);
+    m.tflag[t] = 2;
     m.vtri[a] = NONE;
     m.vtri[b] = NONE;
     m.vtri[c] = NONE;
-    if (s0 != NONE) m.stri[s0] = NONE;
-    if (s1 != NONE) m.stri[s1] = NONE;
-    if (s2 != NONE) m.stri[s2] = NONE;
+    if (s0 != NONE) m.stri[s0] = NONE, m.sflag[s0] = 2;
+    if (s1 != NONE) m.stri[s1] = NONE, m.sflag[s1] = 2;
+    if (s2 != NONE) m.stri[s2] = NONE, m.sflag[s2] = 2;
 }
 
 __device__ __forceinline__ void push_touched(const WorkLists& w, const u32* ts, int k,
@@ -189,6 +190,7 @@ __device__ __forceinline__ int apply_one(const DevMesh& m, const DevCands& c, u3
     f.cc[fi] = c.kind[i] == 1;
     f.removed[fi] = 0;
     f.mark[fi] = 0;
+    f.dirty[fi] = 1;
     const u32 t = c.loc[i];
     if (c.kind[i] == 0) {
         const u32 s = c.id[i];
@@ -274,6 +276,11 @@ __device__ __forceinline__ void fixup_one(const DevMesh& m, u32 round, const Tri
     atomicMin(&m.vtri[tv.x], t);
     atomicMin(&m.vtri[tv.y], t);
     atomicMin(&m.vtri[tv.z], t);
+    if (w.vdirty) {
+        if (tv.x - w.fresh_v0 < w.fresh_n) w.vdirty[tv.x - w.fresh_v0] = 1;
+        if (tv.y - w.fresh_v0 < w.fresh_n) w.vdirty[tv.y - w.fresh_v0] = 1;
+        if (tv.z - w.fresh_v0 < w.fresh_n) w.vdirty[tv.z - w.fresh_v0] = 1;
+    }
     const uint4 ts = m.ts[t];
 #pragma unroll
     for (int e = 0; e < 3; ++e) {
@@ -648,10 +655,12 @@ __global__ void k_rm_claim(DevMesh m, const u32* __restrict__ list, u32 n, TriAu
 // flip of remove_free_vertex (both orient tests of mesh.hpp:223-225), the
 // last three link vertices are the flop.  The k star triangles become k-2
 // (ids reused in star order), the last two die.
+// Lawson seeds of the rebuilt star go to seed_rc->wl_next (so successive
+// removal rounds can accumulate one list for a single Lawson pass).
 __device__ __noinline__ u32 rm_apply_one(const DevMesh& m, const u32* __restrict__ list, u32 i,
                                          u32 round, u32 V0, u32 widx, u32 next_list,
                                          const TriAux& x, const FreshInfo& f, const WorkLists& w,
-                                         RoundCtr* rc, Counters* ctr) {
+                                         RoundCtr* rc, Counters* ctr, RoundCtr* seed_rc) {
     u32 done = 0;
     {
         const u32 v = list[i];
@@ -787,6 +796,7 @@ __device__ __noinline__ u32 rm_apply_one(const DevMesh& m, const u32* __restrict
                     uint4 tv = m.tv[st[q]];
                     tv.w = 0;
                     m.tv[st[q]] = tv;
+                    m.tflag[st[q]] = 2;
                 }
                 m.valive[v] = 0;
                 m.vtri[v] = NONE;
@@ -794,7 +804,7 @@ __device__ __noinline__ u32 rm_apply_one(const DevMesh& m, const u32* __restrict
                 push_touched(w, st, created, rc);
                 for (int ci = 0; ci < created; ++ci) {
                     const u32 codes[3] = {enc(st[ci], 0), enc(st[ci], 1), enc(st[ci], 2)};
-                    push_work(w, widx, codes, 3, ctr, rc);
+                    push_work(w, widx, codes, 3, ctr, seed_rc);
                 }
                 done = 1;
             }
@@ -809,7 +819,7 @@ __global__ void __launch_bounds__(64) k_rm_apply(DevMesh m, const u32* __restric
                                                  Counters* ctr) {
     const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
     u32 done = 0;
-    if (i < n) done = rm_apply_one(m, list, i, round, V0, widx, next_list, x, f, w, w.rc, ctr);
+    if (i < n) done = rm_apply_one(m, list, i, round, V0, widx, next_list, x, f, w, w.rc, ctr, w.rc);
     warp_add_u32(&ctr->rm_done, done);
 }
 
@@ -882,7 +892,7 @@ struct InsertArgs {
     TriAux x;
     FreshInfo f;
     WorkLists w;
-    RoundCtr* ring;       // [4], zeroed by the host before the launch
+    RoundCtr* ring;       // [5]: 4-slot step ring + removal-seed accumulator, zeroed by the host
     u32* state;           // [0] status, [1] steps, [2] flip rounds, [3] removal rounds, [4..7] handoff
     Counters* ctr;
     const u32* d_C;       // candidate count (collect)
@@ -902,6 +912,7 @@ struct InsertArgs {
     int resume;           // 1: candidates are planned, start at the capacity check
     int filter;           // 1: run Lines 5-7 in kernel 1 (tiny batches)
     unsigned long long* trace;   // GDP2D_TRACE: (globaltimer << 8 | tag) per step, or null
+    u32* trace_val;              // a work count per trace entry
     u32* trace_n;
     u32 trace_cap;
 };
@@ -917,10 +928,13 @@ enum : u32 { TR_START = 1, TR_APPLY, TR_FIXUP, TR_FTEST, TR_FAPPLY, TR_FPOST, TR
              TR_DET_C, TR_RM_CLAIM, TR_RM_APPLY, TR_RM_POST, TR_BLOCK_IN, TR_BLOCK_OUT, TR_END,
              TR_LOCATE, TR_CLAIM, TR_CAVITY, TR_PLAN };
 
-__device__ __forceinline__ void trace(const InsertArgs& a, bool leader, u32 tag) {
+__device__ __forceinline__ void trace(const InsertArgs& a, bool leader, u32 tag, u32 value = 0) {
     if (a.trace && leader) {
         const u32 i = atomicAdd(a.trace_n, 1u);
-        if (i < a.trace_cap) a.trace[i] = (globaltimer() << 8) | tag;
+        if (i < a.trace_cap) {
+            a.trace[i] = (globaltimer() << 8) | tag;
+            a.trace_val[i] = value;
+        }
     }
 }
 
@@ -948,19 +962,19 @@ __device__ void lawson_rounds(const InsertArgs& a, const Exec& ex, const DevMesh
         const u32* wl = w.w[cur];
         for (u32 i = ex.tid; i < n; i += ex.nthr) flip_test_one(m, wl[i], a.x, w, rc, a.ctr);
         ex.sync();
-        trace(a, ex.leader(), TR_FTEST);
+        trace(a, ex.leader(), TR_FTEST, n);
         const u32 nc = min(vload(&rc->cand), w.cap);
         for (u32 i = ex.tid; i < nc; i += ex.nthr)
             flipped += flip_apply_one(m, i, round, cur ^ 1u, a.x, w, rc, a.ctr);
         ex.sync();
-        trace(a, ex.leader(), TR_FAPPLY);
+        trace(a, ex.leader(), TR_FAPPLY, nc);
         for (u32 i = ex.tid; i < nc; i += ex.nthr)
             flip_post_one(i, round, cur ^ 1u, a.x, w, rc, a.ctr);
         const u32 nt = min(vload(&rc->touched), w.cap);
         for (u32 i = ex.tid; i < nt; i += ex.nthr)
             fixup_one(m, round, a.x, w, w.touched[i], 0, 0, rc, a.ctr);
         ex.sync();
-        trace(a, ex.leader(), TR_FPOST);
+        trace(a, ex.leader(), TR_FPOST, nt);
         n = vload(&rc->wl_next);
         if (n > w.cap) {
             raise_err(a.ctr, DERR_WORKLIST_OVERFLOW, n);
@@ -1007,19 +1021,19 @@ __device__ void lawson_fixpoint_dev(const InsertArgs& a, const Exec& ex, const D
         const u32* wl = a.w.w[cur];
         for (u32 i = ex.tid; i < n; i += ex.nthr) flip_test_one(m, wl[i], a.x, a.w, rc, a.ctr);
         ex.sync();
-        trace(a, ex.leader(), TR_FTEST);
+        trace(a, ex.leader(), TR_FTEST, n);
         const u32 nc = min(vload(&rc->cand), a.w.cap);
         for (u32 i = ex.tid; i < nc; i += ex.nthr)
             flipped += flip_apply_one(m, i, round, cur ^ 1u, a.x, a.w, rc, a.ctr);
         ex.sync();
-        trace(a, ex.leader(), TR_FAPPLY);
+        trace(a, ex.leader(), TR_FAPPLY, nc);
         for (u32 i = ex.tid; i < nc; i += ex.nthr)
             flip_post_one(i, round, cur ^ 1u, a.x, a.w, rc, a.ctr);
         const u32 nt = min(vload(&rc->touched), a.w.cap);
         for (u32 i = ex.tid; i < nt; i += ex.nthr)
             fixup_one(m, round, a.x, a.w, a.w.touched[i], 0, 0, rc, a.ctr);
         ex.sync();
-        trace(a, ex.leader(), TR_FPOST);
+        trace(a, ex.leader(), TR_FPOST, nt);
         n = vload(&rc->wl_next);
         if (n > a.w.cap) {
             raise_err(a.ctr, DERR_WORKLIST_OVERFLOW, n);
@@ -1183,6 +1197,12 @@ __device__ void split_and_flip(const InsertArgs& a, const Exec& ex, u32 nv, u32 
     warp_add_u32(&a.ctr->ins_mid, mid);
     warp_add_u32(&a.ctr->ins_cc, cc);
     warp_add_ull(&a.ctr->flips, flipped);
+    {
+        // flips of this kernel alone (roofline split of the two launches)
+        u32 f32 = (u32)flipped;
+        f32 = __reduce_add_sync(0xFFFFFFFFu, f32);
+        if ((threadIdx.x & 31) == 0 && f32) atomicAdd(&a.state[7], f32);
+    }
     if (ex.leader()) {
         a.state[0] = step >= a.max_steps ? INS_STEPS : INS_OK;
         a.state[1] = step;
@@ -1205,13 +1225,29 @@ __device__ void rollback_loop(const InsertArgs& a, const Exec& ex, u32 nv, u32 n
     u32 marked = 0, red = 0, dep = 0, done = 0;
     const u32 V0 = a.m.nV, F = nv;
     ex.sync();   // every thread has read state[1] before the leader rewrites it
-    while (step < a.max_steps) {
+    // Detection passes.  Pass 0 evaluates every fresh vertex; later passes
+    // only those whose star was rewritten since (f.dirty, set by fixup_one):
+    // a clean star keeps its neighbours and subsegments, so its verdict
+    // cannot change (a neighbour turning redundant only removes a reason to
+    // be dependent, and redundant neighbours were removed, dirtying it).
+    // dirty: 1 = rewritten, 2 = evaluated in this pass, 0 = clean.
+    RoundCtr* seed_rc = a.ring + 4;   // Lawson seeds of all removal rounds of a pass
+    for (u32 pass = 0; step < a.max_steps; ++pass) {
         RoundCtr* rc = ring_at(a, step);
         ring_advance(a, ex, step);
-        for (u32 j = ex.tid; j < F; j += ex.nthr) marked += detect_a_one<MODE>(m, a.depth_cap, V0, j, a.f, a.ctr);
+        if (ex.leader()) seed_rc->wl_next = 0;   // visible after the barriers below
+        for (u32 j = ex.tid; j < F; j += ex.nthr) {
+            if (pass > 0 && a.f.dirty[j] == 0) continue;
+            a.f.dirty[j] = 2;
+            marked += detect_a_one<MODE>(m, a.depth_cap, V0, j, a.f, a.ctr);
+        }
         ex.sync();
         trace(a, ex.leader(), TR_DET_A);
-        for (u32 j = ex.tid; j < F; j += ex.nthr) detect_b_one(m, V0, F, j, a.f);
+        for (u32 j = ex.tid; j < F; j += ex.nthr) {
+            if (a.f.dirty[j] != 2) continue;
+            a.f.dirty[j] = 0;
+            detect_b_one(m, V0, F, j, a.f);
+        }
         ex.sync();
         trace(a, ex.leader(), TR_DET_B);
         for (u32 j = ex.tid; j < F; j += ex.nthr) {
@@ -1225,6 +1261,11 @@ __device__ void rollback_loop(const InsertArgs& a, const Exec& ex, u32 nv, u32 n
         u32 nrm = min(vload(&rc->detect), w.rm_cap);
         ++step;
         if (nrm == 0) break;
+        // Removal rounds until every listed vertex is gone (or kept): each
+        // round removes the vertices whose stars it owns; the rebuilt stars'
+        // edges accumulate in ONE Lawson list (seed_rc), flipped once after
+        // the last round -- a removal only needs a valid triangulation, not
+        // a Delaunay one, so intermediate Lawson passes are unnecessary.
         u32 rcur = 0;
         while (nrm > 0 && step < a.max_steps) {
             rc = ring_at(a, step);
@@ -1233,9 +1274,10 @@ __device__ void rollback_loop(const InsertArgs& a, const Exec& ex, u32 nv, u32 n
             const u32* list = w.rm[rcur];
             for (u32 i = ex.tid; i < nrm; i += ex.nthr) rm_claim_one(m, list, i, a.x, w, a.ctr);
             ex.sync();
-            trace(a, ex.leader(), TR_RM_CLAIM);
+            trace(a, ex.leader(), TR_RM_CLAIM, nrm);
             for (u32 i = ex.tid; i < nrm; i += ex.nthr)
-                done += rm_apply_one(m, list, i, round, V0, 0, rcur ^ 1u, a.x, a.f, w, rc, a.ctr);
+                done += rm_apply_one(m, list, i, round, V0, 0, rcur ^ 1u, a.x, a.f, w, rc, a.ctr,
+                                     seed_rc);
             ex.sync();
             trace(a, ex.leader(), TR_RM_APPLY);
             for (u32 i = ex.tid; i < nrm; i += ex.nthr) rm_post_one(i, a.x, w);
@@ -1244,15 +1286,15 @@ __device__ void rollback_loop(const InsertArgs& a, const Exec& ex, u32 nv, u32 n
                 fixup_one(m, round, a.x, w, w.touched[i], 0, 0, rc, a.ctr);
             ex.sync();
             trace(a, ex.leader(), TR_RM_POST);
-            const u32 nl = vload(&rc->wl_next);
-            const u32 nnext = min(vload(&rc->rm_next), w.rm_cap);
+            nrm = min(vload(&rc->rm_next), w.rm_cap);
             ++step;
             ++rm_rounds;
-            cur = 0;
-            lawson_fixpoint_dev(a, ex, m, step, cur, nl, flipped, flip_rounds);
-            nrm = nnext;
             rcur ^= 1u;
         }
+        const u32 nl = min(vload(&seed_rc->wl_next), w.cap);
+        ex.sync();   // everyone has read the seed count before the next pass resets it
+        cur = 0;
+        lawson_fixpoint_dev(a, ex, m, step, cur, nl, flipped, flip_rounds);
     }
     warp_add_u32(&a.ctr->marked, marked);
     warp_add_u32(&a.ctr->rm_red, red);
@@ -1328,7 +1370,8 @@ int rollback_persistent_grid(int device) {
     return coop_grid(k_batch_rollback<0>, k_batch_rollback<1>, device);
 }
 
-void launch_insert_persistent(const InsertLaunch& L, int mode, int grid, int grid2, cudaStream_t st) {
+void launch_insert_persistent(const InsertLaunch& L, int mode, int grid, int grid2, cudaStream_t st,
+                              cudaEvent_t between) {
     InsertArgs a;
     a.m = L.m;
     a.c = L.c;
@@ -1358,12 +1401,14 @@ void launch_insert_persistent(const InsertLaunch& L, int mode, int grid, int gri
     a.resume = L.resume;
     a.filter = L.filter;
     a.trace = L.trace;
+    a.trace_val = L.trace_val;
     a.trace_n = L.trace_n;
     a.trace_cap = L.trace_cap;
     void* args[] = {&a};
     note_launch();
     cudaLaunchCooperativeKernel(mode ? (void*)k_batch_split<1> : (void*)k_batch_split<0>, dim3(grid),
                                 dim3(INSERT_BLOCK), args, 0, st);
+    if (between) cudaEventRecord(between, st);
     note_launch();
     cudaLaunchCooperativeKernel(mode ? (void*)k_batch_rollback<1> : (void*)k_batch_rollback<0>,
                                 dim3(grid2), dim3(INSERT_BLOCK), args, 0, st);

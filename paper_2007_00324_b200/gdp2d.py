@@ -129,6 +129,12 @@ class RunReport:
     scan_seconds: float = 0.0
     scan_bytes: int = 0
     scan_launches: int = 0
+    split_seconds: float = 0.0
+    split_bytes: int = 0
+    split_launches: int = 0
+    rollback_seconds: float = 0.0
+    rollback_bytes: int = 0
+    rollback_launches: int = 0
     kernel_launches: int = 0
 
     def algorithmic_bytes(self) -> int:
@@ -165,6 +171,9 @@ def _report(r: A.Report, arr) -> RunReport:
                      iteration_cap_hit=bool(r.iteration_cap_hit), device_seconds=r.device_seconds,
                      totals={k: getattr(r, k) for k in _TOTALS}, scan_seconds=r.scan_seconds,
                      scan_bytes=r.scan_bytes, scan_launches=r.scan_launches,
+                     split_seconds=r.split_seconds, split_bytes=r.split_bytes,
+                     split_launches=r.split_launches, rollback_seconds=r.rollback_seconds,
+                     rollback_bytes=r.rollback_bytes, rollback_launches=r.rollback_launches,
                      kernel_launches=r.kernel_launches)
 
 
