@@ -249,8 +249,23 @@ def main():
     last = reps[-1]
     eng = engines[0]
 
-    # ---- e2e: the public C ABI with host buffers ----
+    # ---- e2e: the public API with HOST buffers (page-locked) ----
+    # Every step: H2D of the input mesh from pinned host memory (Engine.upload
+    # -> gdp2d_ctx_upload), the refinement, and D2H of the whole refined mesh
+    # into pinned host buffers (Engine.download_to -> gdp2d_ctx_download_to).
+    # The pinned pools are filled / allocated once, outside the timed region.
+    from paper_2007_00324_b200 import PinnedPool
     e2e_steps = a.e2e_steps or a.steps
+    e2e_eng = Engine(device)
+    pins = []
+    for mm in meshes:
+        pin_in = PinnedPool(mm.n_vertices, mm.n_triangles, mm.n_subsegments)
+        pin_out = PinnedPool(3 * mm.n_vertices, 3 * mm.n_triangles, 3 * mm.n_subsegments)
+        pins.append((pin_in.load(mm), pin_in, pin_out))
+    for m_in, _, pin_out in pins:        # warm the e2e context (growth, caches)
+        e2e_eng.upload(m_in)
+        e2e_eng.refine(q)
+        e2e_eng.download_to(pin_out)
     e2e_s = []
     e2e_st = 0
     h2d = sum(mesh_bytes(mm) for mm in meshes)
@@ -259,16 +274,18 @@ def main():
     for _ in range(e2e_steps):
         d2h = 0
         t_step = 0.0
-        for mm in meshes:
-            m = mm.copy()
+        for m_in, _, pin_out in pins:
             t = time.perf_counter()
-            r = refine(m, q)          # upload (H2D) + refine + download (D2H)
+            e2e_eng.upload(m_in)                  # H2D
+            r = e2e_eng.refine(q)
+            out = e2e_eng.download_to(pin_out)    # D2H
             t_step += time.perf_counter() - t
             e2e_st += r.steiner_points
-            d2h += mesh_bytes(m)
+            d2h += mesh_bytes(out)
         e2e_s.append(t_step)
     e2e_total = dist.max(sum(e2e_s))
     e2e_value = dist.sum(e2e_st) / e2e_total
+    e2e_eng.close()
 
     # ---- roofline: the dominant engine kernel (largest share of the step) ----
     peak, peak_kind = load_peaks()

@@ -704,10 +704,13 @@ void upload(gdp2d_ctx* x, const gdp2d_mesh_view* v) {
 
 void reset_work(gdp2d_ctx* x) {
     const DevMesh& p = x->pristine.m;
-    // headroom: 2.5x the input (amortised growth handles the rest)
+    // headroom: 2.5x the input (amortised growth handles the rest);
+    // GDP2D_HEADROOM overrides the factor (tests use 1.0 to force growth)
+    double hr = 2.5;
+    if (const char* e = std::getenv("GDP2D_HEADROOM")) hr = std::max(1.0, std::atof(e));
     x->work.m.nV = x->work.m.nT = x->work.m.nS = 0;
-    mesh_reserve(x->work, std::max<u32>(p.nV * 5 / 2, 1024), std::max<u32>(p.nT * 5 / 2, 2048),
-                 std::max<u32>(p.nS * 5 / 2, 1024), x->st);
+    mesh_reserve(x->work, std::max<u32>((u32)(p.nV * hr), 64), std::max<u32>((u32)(p.nT * hr), 128),
+                 std::max<u32>((u32)(p.nS * hr), 64), x->st);
     mesh_copy(x->work, x->pristine, x->st);
     // subsegment depth restarts at 0 for every refine call (refine.hpp:655)
     if (x->work.m.nS) CK(cudaMemsetAsync(x->work.m.sdepth, 0, 4ull * x->work.m.nS, x->st));
@@ -1348,6 +1351,19 @@ int gdp2d_refine(const gdp2d_mesh_view* in, gdp2d_mesh_buf* out, const gdp2d_par
         fill_summary(x, p, r);
         r->wall_seconds = wall;
     });
+}
+
+void* gdp2d_host_alloc(size_t bytes) {
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, bytes ? bytes : 1, cudaHostAllocPortable) != cudaSuccess) {
+        g_err = "cudaHostAlloc failed";
+        return nullptr;
+    }
+    return p;
+}
+
+void gdp2d_host_free(void* p) {
+    if (p) cudaFreeHost(p);
 }
 
 void gdp2d_release_cached(void) {

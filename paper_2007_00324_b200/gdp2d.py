@@ -274,6 +274,69 @@ class Mesh:
         return np.take_along_axis(t, idx, axis=1)
 
 
+class PinnedPool:
+    """Page-locked host buffers (gdp2d_host_alloc) for meshes of up to
+    (nv, nt, ns) elements: uploads / downloads from here run at full link rate.
+    ``mesh(...)`` returns a Mesh whose arrays are views into the pool (no copy)."""
+
+    def __init__(self, nv: int, nt: int, ns: int):
+        self.lib = A.engine()
+        self._ptrs = []
+        self._bufs = {}
+        self._alloc(nv, nt, ns)
+
+    def reserve(self, nv: int, nt: int, ns: int) -> None:
+        """Grow (reallocate) so a mesh of (nv, nt, ns) fits; contents are not kept."""
+        if nv > self.caps["v"] or nt > self.caps["t"] or ns > self.caps["s"]:
+            self.close()
+            self._alloc(max(nv, self.caps["v"]) * 5 // 4, max(nt, self.caps["t"]) * 5 // 4,
+                        max(ns, self.caps["s"]) * 5 // 4)
+
+    def _alloc(self, nv: int, nt: int, ns: int) -> None:
+        self.caps = {"v": max(1, nv), "t": max(1, nt), "s": max(1, ns)}
+        for name, dt, w in _FIELDS:
+            n = self.caps["v" if name in _VERT else "t" if name in _TRI else "s"] * w
+            nbytes = n * np.dtype(dt).itemsize
+            ptr = self.lib.gdp2d_host_alloc(nbytes)
+            if not ptr:
+                raise MemoryError(f"gdp2d_host_alloc({nbytes}) failed")
+            self._ptrs.append(ptr)
+            buf = (C.c_uint8 * nbytes).from_address(ptr)
+            self._bufs[name] = np.frombuffer(buf, dtype=dt, count=n)
+
+    def close(self) -> None:
+        for p in self._ptrs:
+            self.lib.gdp2d_host_free(p)
+        self._ptrs = []
+        self._bufs = {}
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def mesh(self, nv: int, nt: int, ns: int, batch_epoch: int = 0) -> "Mesh":
+        counts = {"v": nv, "t": nt, "s": ns}
+        if any(counts[k] > self.caps[k] for k in counts):
+            raise ValueError(f"mesh {counts} exceeds pinned capacity {self.caps}")
+        arrays = {}
+        for name, dt, w in _FIELDS:
+            n = counts["v" if name in _VERT else "t" if name in _TRI else "s"]
+            a = self._bufs[name][: n * w]
+            arrays[name] = a.reshape(-1, w) if w > 1 else a
+        m = Mesh(batch_epoch=batch_epoch, **arrays)
+        m._pool = self   # keep the pinned memory alive with the views
+        return m
+
+    def load(self, src: "Mesh") -> "Mesh":
+        """Copy a mesh into the pool (outside any timed region)."""
+        m = self.mesh(src.n_vertices, src.n_triangles, src.n_subsegments, src.batch_epoch)
+        for name, _, _ in _FIELDS:
+            getattr(m, name)[...] = getattr(src, name)
+        return m
+
+
 # ---- whole-run entry point ---------------------------------------------------------
 
 
@@ -380,6 +443,21 @@ class Engine:
         v = mesh.view()
         for fname, _ in A.MeshView._fields_[4:]:
             setattr(b, fname, getattr(v, fname))
+        _raise(self.lib.gdp2d_ctx_download_to(self.ctx, C.byref(b)), "gdp2d_ctx_download_to")
+        mesh.batch_epoch = b.batch_epoch
+        return mesh
+
+    def download_to(self, pool: "PinnedPool") -> Mesh:
+        """D2H of the working mesh into page-locked pool buffers (allocation only
+        when the pool is too small)."""
+        nv, nt, ns = self.sizes()
+        pool.reserve(nv, nt, ns)
+        mesh = pool.mesh(nv, nt, ns)
+        b = A.MeshBuf()
+        b.n_vertices, b.n_triangles, b.n_subsegments = nv, nt, ns
+        for name, dt, _ in _FIELDS:
+            ct = {np.float64: C.c_double, np.uint8: C.c_uint8, np.uint32: C.c_uint32}[dt]
+            setattr(b, name, getattr(mesh, name).ctypes.data_as(C.POINTER(ct)))
         _raise(self.lib.gdp2d_ctx_download_to(self.ctx, C.byref(b)), "gdp2d_ctx_download_to")
         mesh.batch_epoch = b.batch_epoch
         return mesh

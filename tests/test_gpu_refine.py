@@ -133,3 +133,61 @@ def test_chew_mode(built):
     q = QualityCriteria(20.0, math.inf, CHEW)
     out, closed, rep, _ = _run(pts, segs, q)
     check_invariants(out, pts, closed, q)
+
+
+def test_growth_paths_identical(built, monkeypatch):
+    """Headroom 1.0 forces device-side INS_GROW + host growth + relaunch on
+    almost every batch; the result must be bit-identical to the default run."""
+    from paper_2007_00324_b200 import QualityCriteria, host, refine
+    pts, segs = host.generate_pslg(30_000, 3_000, "uniform", 11)
+    m, closed = host.build_cdt(pts, segs)
+    q = QualityCriteria(B_SQRT2_THETA)
+    a = m.copy()
+    refine(a, q)
+    monkeypatch.setenv("GDP2D_HEADROOM", "1.0")
+    b = m.copy()
+    rep = refine(b, q)
+    assert rep.bad_triangles == 0
+    for name in ("xy", "tri_v", "tri_n", "tri_seg", "tri_alive", "seg_v", "seg_alive"):
+        assert np.array_equal(getattr(a, name), getattr(b, name)), name
+    check_invariants(b, pts, closed, q, cdt_check=False)
+
+
+def test_pinned_round_trip(built):
+    """Engine.upload from / download_to page-locked pools (the bench e2e path)."""
+    from paper_2007_00324_b200 import Engine, PinnedPool, QualityCriteria, host
+    pts, segs = host.generate_pslg(20_000, 2_000, "uniform", 12)
+    m, closed = host.build_cdt(pts, segs)
+    q = QualityCriteria(B_SQRT2_THETA)
+    pin_in = PinnedPool(m.n_vertices, m.n_triangles, m.n_subsegments)
+    pin_out = PinnedPool(3 * m.n_vertices, 3 * m.n_triangles, 3 * m.n_subsegments)
+    src = pin_in.load(m)
+    with Engine(0) as eng:
+        eng.upload(src)
+        rep = eng.refine(q)
+        out = eng.download_to(pin_out)
+        ref = eng.download()
+    for name in ("xy", "tri_v", "tri_n", "seg_v", "vert_kind"):
+        assert np.array_equal(getattr(out, name), getattr(ref, name)), name
+    assert rep.bad_triangles == 0
+    check_invariants(out, pts, closed, q, cdt_check=False)
+
+
+@pytest.mark.parametrize("small_c", ["0", "100000000"])
+def test_block_and_grid_modes_agree(built, monkeypatch, small_c):
+    """Block mode (whole batch in one CTA) and grid mode give the same mesh."""
+    from paper_2007_00324_b200 import Engine, QualityCriteria, host
+    pts, segs = host.generate_pslg(10_000, 1_000, "gaussian", 13)
+    m, _ = host.build_cdt(pts, segs)
+    q = QualityCriteria(B_SQRT2_THETA)
+    with Engine(0) as eng:
+        eng.upload(m)
+        eng.refine(q)
+        base = eng.download()
+    monkeypatch.setenv("GDP2D_SMALL_C", small_c)
+    with Engine(0) as eng:
+        eng.upload(m)
+        eng.refine(q)
+        other = eng.download()
+    assert np.array_equal(base.tri_v, other.tri_v)
+    assert np.array_equal(base.xy, other.xy)
