@@ -117,10 +117,29 @@ typedef struct gdp2d_params {
     uint32_t rule2_filtering_enabled;    /* cavity filter on/off               */
     uint32_t rule4_unified_collection;   /* subsegs + triangles in one batch   */
     uint32_t little_batch_sizing;    /* GPU: Little's-law batch cap (0 = off)   */
+    uint32_t insert_mode;            /* GDP2D_INSERT_* (see below)               */
+    uint32_t reserved0;
     uint64_t iteration_cap;          /* 10000                                   */
     uint64_t split_depth_cap;        /* 64                                      */
     uint64_t batch_size_cap;         /* 0 = unlimited; keep highest priorities  */
 } gdp2d_params;
+
+/* Insertion policy of a batch (gdp2d_params.insert_mode).
+ * ROLLBACK: the reference's insert_batch (refine.hpp:464-610): every cavity
+ *   survivor is inserted, then redundant (encroaching) and dependent
+ *   same-batch circumcenters are rolled back by vertex removal.
+ * ISOLATED: a survivor also owns the one-ring of its cavity (both sides of a
+ *   split subsegment), so inserted points cannot interact: no dependent pair
+ *   can form and no rollback is needed.  A circumcenter that would encroach a
+ *   splittable subsegment on its cavity boundary is not inserted and the
+ *   subsegment is marked instead (encroachment precedence, the classic rule of
+ *   refine.hpp:786-804).  Cavities that hit the cavity_n cap fall back to the
+ *   rollback detection for that batch. */
+/* PRECEDENCE: the reference's claim sets and rollback, plus the encroachment
+ *   precedence test on each survivor's cavity boundary (an encroaching
+ *   circumcenter marks its subsegment instead of being inserted and rolled
+ *   back). */
+enum { GDP2D_INSERT_ISOLATED = 0, GDP2D_INSERT_ROLLBACK = 1, GDP2D_INSERT_PRECEDENCE = 2 };
 
 /* Phase order of the per-batch timers (refine.hpp:671-701). */
 enum { GDP2D_PH_COLLECT = 0, GDP2D_PH_SPLIT_POINTS = 1, GDP2D_PH_LOCATE = 2,

@@ -42,6 +42,7 @@ class Params(C.Structure):
                 ("rule1_compaction_threshold", C.c_uint32),
                 ("rule2_filtering_enabled", C.c_uint32),
                 ("rule4_unified_collection", C.c_uint32), ("little_batch_sizing", C.c_uint32),
+                ("insert_mode", C.c_uint32), ("reserved0", C.c_uint32),
                 ("iteration_cap", C.c_uint64), ("split_depth_cap", C.c_uint64),
                 ("batch_size_cap", C.c_uint64)]
 

@@ -322,7 +322,7 @@ struct gdp2d_ctx {
     int rollback_grid = 0;        // persistent rollback kernel grid
     bool legacy_insert = false;   // GDP2D_INSERT=legacy: host-driven insertion rounds
     RoundCtr* ring = nullptr;     // [4] step counters of the persistent insertion kernel
-    u32* ins_state = nullptr;     // [8] its status words
+    u32* ins_state = nullptr;     // [16] status words (see k_insert.cu; [8] = unsafe flag)
     u32* h_state = nullptr;       // pinned copy
     cudaEvent_t ev_k[3] = {};     // around the split and rollback kernels
     double k_split_s = 0, k_rb_s = 0;   // per refine call: roofline accumulators
@@ -331,6 +331,7 @@ struct gdp2d_ctx {
     u32 small_nv = 256;           // GDP2D_SMALL_NV: block-mode insertion at or below
     u32 small_wl = 256;           // GDP2D_SMALL_WL: block-mode Lawson below this list size
     u32 small_c = 256;            // GDP2D_SMALL_C: whole batch in one CTA at or below
+    bool dep_mis = false;         // GDP2D_DEP=mis: dependent pairs by the priority-MIS rule
     u32* scan_part = nullptr;     // [3 * insert_grid] plan chunk sums
     RoundCtr* rcs = nullptr;      // per-round counters of the persistent kernel
     u32* d_res = nullptr;
@@ -348,6 +349,7 @@ namespace {
 void cands_free(DevCands& c) {
     dfree(c.pt); dfree(c.key); dfree(c.id); dfree(c.tie); dfree(c.loc);
     dfree(c.kind); dfree(c.alive); dfree(c.lkind); dfree(c.ledge); dfree(c.fb);
+    dfree(c.red); dfree(c.unsafe);
 }
 
 void ensure_cands(gdp2d_ctx* x, u32 n) {
@@ -357,6 +359,7 @@ void ensure_cands(gdp2d_ctx* x, u32 n) {
     dalloc(x->c.pt, cap); dalloc(x->c.key, cap); dalloc(x->c.id, cap); dalloc(x->c.tie, cap);
     dalloc(x->c.loc, cap); dalloc(x->c.kind, cap); dalloc(x->c.alive, cap);
     dalloc(x->c.lkind, cap); dalloc(x->c.ledge, cap); dalloc(x->c.fb, cap);
+    dalloc(x->c.red, cap); dalloc(x->c.unsafe, cap);
     x->ccap = cap;
     // per-candidate insertion buffers
     dfree(x->ib.nv); dfree(x->ib.nt); dfree(x->ib.ns); dfree(x->ib.ov); dfree(x->ib.ot);
@@ -367,8 +370,8 @@ void ensure_cands(gdp2d_ctx* x, u32 n) {
     x->ib.cap = cap;
 }
 
-void ensure_regions(gdp2d_ctx* x, u32 n, u32 ncav) {
-    const size_t rs = ncav + 1 + MAX_CLAIM_EXTRA;
+void ensure_regions(gdp2d_ctx* x, u32 n, u32 ncav, u32 stride = 0) {
+    const size_t rs = stride ? stride : ncav + 1 + MAX_CLAIM_EXTRA;
     if ((size_t)n * rs > x->reg_cap) {
         dfree(x->regions);
         x->reg_cap = std::max<size_t>((size_t)n * rs * 3 / 2, 4096);
@@ -431,9 +434,11 @@ void ensure_fresh(gdp2d_ctx* x, u32 n) {
     if (n <= x->fresh.cap) return;
     FreshInfo& f = x->fresh;
     dfree(f.key); dfree(f.tie); dfree(f.cc); dfree(f.removed); dfree(f.mark); dfree(f.dirty);
+    dfree(f.dstat); dfree(f.hcnt); dfree(f.hlist);
     const u32 cap = std::max<u32>(n + n / 2, 1024);
     dalloc(f.key, cap); dalloc(f.tie, cap); dalloc(f.cc, cap); dalloc(f.removed, cap);
     dalloc(f.mark, cap); dalloc(f.dirty, cap);
+    dalloc(f.dstat, cap); dalloc(f.hcnt, cap); dalloc(f.hlist, (size_t)cap * DEP_HMAX);
     f.cap = cap;
     dfree(x->wl.rm[0]); dfree(x->wl.rm[1]); dfree(x->wl.star); dfree(x->wl.star_len);
     dalloc(x->wl.rm[0], cap); dalloc(x->wl.rm[1], cap);
@@ -581,9 +586,10 @@ void ctx_init(gdp2d_ctx* x, int device) {
     if (const char* e = std::getenv("GDP2D_SMALL_NV")) x->small_nv = (u32)std::strtoul(e, nullptr, 10);
     if (const char* e = std::getenv("GDP2D_SMALL_WL")) x->small_wl = (u32)std::strtoul(e, nullptr, 10);
     if (const char* e = std::getenv("GDP2D_SMALL_C")) x->small_c = (u32)std::strtoul(e, nullptr, 10);
+    if (const char* e = std::getenv("GDP2D_DEP")) x->dep_mis = std::string(e) == "mis";
     dalloc(x->scan_part, 3ull * x->insert_grid + 3);
-    dalloc(x->ins_state, 8);
-    CK(cudaMallocHost(&x->h_state, 8 * sizeof(u32)));
+    dalloc(x->ins_state, 16);
+    CK(cudaMallocHost(&x->h_state, 16 * sizeof(u32)));
     const char* fc = std::getenv("GDP2D_COLLECT");
     x->full_collect = fc && std::string(fc) == "full";
     dalloc(x->rcs, 1024);
@@ -604,6 +610,7 @@ void ctx_release(gdp2d_ctx* x) {
     dfree(x->ib.os); dfree(x->ib.totals);
     dfree(x->fresh.key); dfree(x->fresh.tie); dfree(x->fresh.cc); dfree(x->fresh.removed);
     dfree(x->fresh.mark); dfree(x->fresh.dirty);
+    dfree(x->fresh.dstat); dfree(x->fresh.hcnt); dfree(x->fresh.hlist);
     dfree(x->wl.w[0]); dfree(x->wl.w[1]); dfree(x->wl.fc); dfree(x->wl.fu);
     dfree(x->wl.touched); dfree(x->wl.fwin); dfree(x->wl.rm[0]); dfree(x->wl.rm[1]);
     dfree(x->wl.star); dfree(x->wl.star_len); dfree(x->wl.rc);
@@ -844,8 +851,9 @@ void insert_legacy(gdp2d_ctx* x, const gdp2d_params* p, const Quality& q, u32 C,
 // round trip inside; the capacity check runs on the device and a batch that
 // does not fit is re-launched after growing the buffers (the mesh is not
 // touched by a launch that reports INS_GROW).
-void insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, u32 C, u32 ncav, u32 batch, u32& nv,
-                       u32& nt, u32& ns, u32& flip_rounds, u32& rm_rounds) {
+void insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, u32 C, u32 ncav, u32 rs,
+                       int isolate, u32 batch, u32& nv, u32& nt, u32& ns, u32& flip_rounds,
+                       u32& rm_rounds) {
     (void)C;
     cudaStream_t st = x->st;
     for (int attempt = 0;; ++attempt) {
@@ -874,7 +882,9 @@ void insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, u32 C, u32 ncav, u32
         L.small_wl = x->small_wl;
         L.max_steps = 1u << 20;
         L.ncav = ncav;
-        L.rs = ncav + 1 + MAX_CLAIM_EXTRA;
+        L.rs = rs;
+        L.isolate = isolate;
+        L.dep_mis = x->dep_mis ? 1 : 0;
         L.regions = x->regions;
         L.region_len = x->region_len;
         L.scan_part = x->scan_part;
@@ -889,14 +899,14 @@ void insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, u32 C, u32 ncav, u32
             CK(cudaMemsetAsync(x->tr.d_trace_n, 0, sizeof(u32), st));
         }
         x->tr.mark("pre_ins", st);
-        CK(cudaMemsetAsync(x->ins_state, 0, 8 * sizeof(u32), st));
+        CK(cudaMemsetAsync(x->ins_state, 0, 8 * sizeof(u32), st));   // word 8 = unsafe flag stays
         CK(cudaEventRecord(x->ev_k[0], st));
         launch_insert_persistent(L, p->mode == GDP2D_CHEW ? 1 : 0, x->insert_grid,
                                  x->rollback_grid, st, x->ev_k[1]);
         CK(cudaEventRecord(x->ev_k[2], st));
         x->tr.mark("insert_kernel", st);
         CK(cudaGetLastError());
-        CK(cudaMemcpyAsync(x->h_state, x->ins_state, 8 * sizeof(u32), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(x->h_state, x->ins_state, 16 * sizeof(u32), cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(x->h_tot, x->ib.totals, 3 * sizeof(u32), cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(x->h_ctr, x->d_ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
@@ -996,7 +1006,14 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
         }
         CK(cudaEventRecord(x->ev[1], st));   // split points are fused into collect
         CK(cudaEventRecord(x->ev[2], st));
-        ensure_regions(x, C, ncav);
+        // isolated insertion needs the cavity filter (rule 2)
+        const int isolate = (ncav == 0 || x->legacy_insert) ? 0
+                            : p->insert_mode == GDP2D_INSERT_ISOLATED   ? 1
+                            : p->insert_mode == GDP2D_INSERT_PRECEDENCE ? 2
+                                                                        : 0;
+        const u32 rs = isolate ? isolated_stride(ncav) : ncav + 1 + MAX_CLAIM_EXTRA;
+        ensure_regions(x, C, ncav, rs);
+        CK(cudaMemsetAsync(x->ins_state + 8, 0, sizeof(u32), st));   // unsafe flag
         const u32 batch = ++x->epoch;
         u32 flip_rounds = 0, rm_rounds = 0;
         u32 nv = 0, nt = 0, ns = 0;
@@ -1024,8 +1041,13 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
                 CK(cudaEventRecord(x->ev[3], st));
                 launch_claim(m, x->c, C, x->aux, x->d_ctr, st);
                 CK(cudaEventRecord(x->ev[4], st));
-                launch_cavity(m, x->c, C, ncav, true, x->aux, x->regions, x->region_len,
-                              nullptr, x->d_ctr, st);
+                if (isolate)
+                    launch_cavity_isolated(m, x->c, C, ncav, rs, p->mode == GDP2D_CHEW ? 1 : 0,
+                                           p->split_depth_cap, isolate == 1, x->aux, x->regions,
+                                           x->region_len, x->ins_state + 8, x->d_ctr, st);
+                else
+                    launch_cavity(m, x->c, C, ncav, true, x->aux, x->regions, x->region_len,
+                                  nullptr, x->d_ctr, st);
                 CK(cudaEventRecord(x->ev[5], st));
             } else {
                 // tail batch: everything runs inside the block-mode kernels
@@ -1033,7 +1055,8 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
                 CK(cudaEventRecord(x->ev[4], st));
                 CK(cudaEventRecord(x->ev[5], st));
             }
-            insert_persistent(x, p, C, ncav, batch, nv, nt, ns, flip_rounds, rm_rounds);
+            insert_persistent(x, p, C, ncav, rs, isolate, batch, nv, nt, ns, flip_rounds,
+                              rm_rounds);
         }
         CK(cudaEventRecord(x->ev[6], st));
         x->tr.mark("sync", st);
@@ -1261,6 +1284,8 @@ void gdp2d_params_init(gdp2d_params* p, double theta_deg, double ell, uint32_t m
     p->rule2_filtering_enabled = 1;
     p->rule4_unified_collection = 1;
     p->little_batch_sizing = 0;
+    p->insert_mode = GDP2D_INSERT_ROLLBACK;
+    p->reserved0 = 0;
     p->iteration_cap = 10000;
     p->split_depth_cap = 64;
     p->batch_size_cap = 0;

@@ -71,6 +71,14 @@ void launch_cavity(const DevMesh& m, DevCands c, u32 n, u32 ncav, bool extras, T
                    u32* regions, u32* region_len, u32* bfs_len, Counters* d_ctr,
                    cudaStream_t st);
 
+// Isolated-insertion claims (cavity + one-ring + encroachment precedence);
+// regions stride rs = isolated_stride(ncav); *unsafe_flag |= 1 when a survivor
+// inserts from a capped claim set.
+inline u32 isolated_stride(u32 ncav) { return 4 * (ncav + 1) + 8; }
+void launch_cavity_isolated(const DevMesh& m, DevCands c, u32 n, u32 ncav, u32 rs, int mode,
+                            u64 depth_cap, bool ring, TriAux a, u32* regions, u32* region_len,
+                            u32* unsafe_flag, Counters* d_ctr, cudaStream_t st);
+
 // ---- insertion ---------------------------------------------------------------------
 
 struct InsertBufs {
@@ -91,8 +99,13 @@ struct FreshInfo {
     uint8_t* removed = nullptr;
     uint8_t* mark = nullptr;
     uint8_t* dirty = nullptr;   // star rewritten since the last detection pass
+    // dependent-pair resolution by priority (MIS rule, see k_insert.cu)
+    uint8_t* dstat = nullptr;   // 0 undecided, 1 kept, 2 removed
+    uint8_t* hcnt = nullptr;    // higher-priority same-batch circumcenter neighbours
+    u32* hlist = nullptr;       // [cap * DEP_HMAX]
     u32 cap = 0;
 };
+constexpr int DEP_HMAX = 16;
 
 struct WorkLists {
     u32* w[2] = {nullptr, nullptr};   // Lawson edge codes
@@ -161,6 +174,8 @@ struct InsertLaunch {
     u32 small_c = 0;
     int resume = 0;
     int filter = 1;
+    int isolate = 1;            // claims: 0 reference cavity, 1 isolated (ring), 2 precedence
+    int dep_mis = 0;            // dependent pairs by the priority-MIS rule
     unsigned long long* trace = nullptr;   // device step trace (GDP2D_TRACE=1)
     u32* trace_val = nullptr;
     u32* trace_n = nullptr;

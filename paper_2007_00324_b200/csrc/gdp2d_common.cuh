@@ -79,6 +79,8 @@ struct DevCands {
     uint8_t* lkind; // Location kind found by the walk (GDP2D_LOC_*)
     int8_t* ledge;  // edge for OnEdge
     uint8_t* fb;    // circumcenter fallback used
+    u32* red;       // isolated insertion: lowest splittable subsegment the point would encroach
+    uint8_t* unsafe;// isolated insertion: cavity hit the cap (not provably isolated)
 };
 
 // Per-batch device counters (zeroed at the start of each batch).

@@ -224,6 +224,189 @@ __device__ __forceinline__ void cavity_reset_one(u32 i, u32 rs, const u32* regio
     }
 }
 
+// ---- isolated insertion claims (GDP2D_INSERT_ISOLATED) ------------------------
+//
+// Claim set = the constrained Delaunay cavity of p (BFS of triangles whose
+// circumcircle strictly contains p, never crossing a subsegment, as above;
+// for a subsegment midpoint also the cavity on the far side of the
+// subsegment) + its one-ring (the triangles across every non-subsegment
+// boundary edge).  If two survivors own disjoint claim sets, Lawson after
+// their splits reaches exactly the Bowyer-Watson result of each point on its
+// own cavity: every boundary edge separates p's fan from an untouched ring
+// triangle whose circumcircle excludes p, so it is locally Delaunay, and no
+// edge can ever join two fresh points (no dependent pair, refine.hpp:589-607).
+// While scanning the boundary, a circumcenter that encroaches a splittable
+// subsegment on it records the lowest such subsegment (red): the point would
+// be redundant after insertion (refine.hpp:555-588), so a surviving
+// candidate marks the subsegment instead of inserting (encroachment
+// precedence, refine.hpp:786-804).  A cavity that reaches the cap, or a ring
+// larger than the region buffer, is flagged unsafe (the batch then runs the
+// rollback detection as a fallback).
+
+__device__ __forceinline__ bool in_list(const u32* reg, u32 len, u32 t) {
+    bool in = false;
+    for (u32 k = 0; k < len; ++k) in |= reg[k] == t;
+    return in;
+}
+
+// BFS cavity from `seed` appended to reg[len..]; returns false if capped.
+// `located` always belongs (as in cavity_filter).
+__device__ __forceinline__ bool cavity_bfs_into(const DevMesh& m, u32 seed, bool seed_always,
+                                                double2 p, u32 ncav, u32* reg, u32& len, u32 rs) {
+    u32 queue[1 + 3 * (MAX_CAVITY_N + 1)];
+    u32 head = 0, tail = 0;
+    const u32 start = len;
+    queue[tail++] = seed;
+    while (head < tail) {
+        if (len - start > ncav) return false;   // cap reached with work left
+        const u32 t = queue[head++];
+        const uint4 tv = m.tv[t];
+        bool pred = seed_always && t == seed;
+        if (!pred && tv.w) pred = incircle(m.xy[tv.x], m.xy[tv.y], m.xy[tv.z], p) > 0;
+        if (!pred) continue;
+        if (in_list(reg, len, t)) continue;
+        if (len >= rs) return false;
+        reg[len++] = t;
+        const uint4 tn = m.tn[t];
+        const uint4 ts = m.ts[t];
+        for (int e = 0; e < 3; ++e) {
+            if (comp(ts, e) != NONE) continue;
+            const u32 cc = comp(tn, e);
+            if (cc == NONE) continue;
+            const u32 nb = etri(cc);
+            if (in_list(reg, len, nb)) continue;
+            if (tail >= 1 + 3 * (MAX_CAVITY_N + 1)) return false;
+            queue[tail++] = nb;
+        }
+    }
+    return true;
+}
+
+// ring == false (GDP2D_INSERT_PRECEDENCE): the claim set is the reference's
+// (cavity_bfs_one with extras); only the encroachment precedence is added and
+// the rollback detection still runs for dependent pairs.
+template <int MODE>
+__device__ __forceinline__ u32 cavity_claims_one(const DevMesh& m, const DevCands& c, u32 i,
+                                                 u32 ncav, u32 rs, u32* regions,
+                                                 u32* region_len, u64* ckey, u64 depth_cap,
+                                                 bool ring = true) {
+    u32 len = 0, blen = 0;
+    c.red[i] = NONE;
+    c.unsafe[i] = 0;
+    if (c.alive[i]) {
+        u32* reg = regions + (size_t)i * rs;
+        const u32 located = c.loc[i];
+        const double2 p = c.pt[i];
+        bool ok = cavity_bfs_into(m, located, true, p, ncav, reg, len, rs);
+        if (!ring) {
+            // reference claim set: the (possibly capped) BFS region + the far
+            // side of a split edge; the precedence test reads the region's
+            // subsegment edges
+            blen = len;
+            u32 red = NONE;
+            if (c.kind[i] == 1) {
+                for (u32 k = 0; k < blen; ++k) {
+                    const uint4 ts = m.ts[reg[k]];
+                    for (int e = 0; e < 3; ++e) {
+                        const u32 s = comp(ts, e);
+                        if (s == NONE || s >= red) continue;
+                        const uint2 sv = m.sv[s];
+                        if (encroaches<MODE>(m.xy[sv.x], m.xy[sv.y], p) &&
+                            (u64)m.sdepth[s] < depth_cap && subseg_split_ok(m, s, subseg_mid(m, s)))
+                            red = s;
+                    }
+                }
+            }
+            c.red[i] = red;
+            ok = false;   // take the reference fallback below (extras), no unsafe flag
+        }
+        if (ok && c.kind[i] == 0) {
+            // subsegment midpoint: the cavity on the far side of s as well
+            const u32 s = c.id[i];
+            const int e = seg_slot(m.ts[located], s);
+            if (e >= 0) {
+                const u32 cc = comp(m.tn[located], e);
+                if (cc != NONE) ok = cavity_bfs_into(m, etri(cc), true, p, ncav, reg, len, rs);
+            }
+        }
+        blen = len;
+        // one-ring across non-subsegment boundary edges; encroachment precedence
+        u32 red = NONE;
+        const bool is_cc = c.kind[i] == 1;
+        for (u32 k = 0; k < blen && ok; ++k) {
+            const u32 t = reg[k];
+            const uint4 tn = m.tn[t];
+            const uint4 ts = m.ts[t];
+            for (int e = 0; e < 3; ++e) {
+                const u32 s = comp(ts, e);
+                if (s != NONE) {
+                    if (is_cc && s < red) {
+                        const uint2 sv = m.sv[s];
+                        if (encroaches<MODE>(m.xy[sv.x], m.xy[sv.y], p) &&
+                            (u64)m.sdepth[s] < depth_cap && subseg_split_ok(m, s, subseg_mid(m, s)))
+                            red = s;
+                    }
+                    continue;
+                }
+                const u32 cc = comp(tn, e);
+                if (cc == NONE) continue;
+                const u32 nb = etri(cc);
+                if (in_list(reg, len, nb)) continue;
+                if (len >= rs) {
+                    ok = false;
+                    break;
+                }
+                reg[len++] = nb;
+            }
+        }
+        if (ring) {
+            c.red[i] = red;
+            c.unsafe[i] = ok ? 0 : 1;
+        }
+        if (!ok) {
+            // fall back to the reference claim set: the capped region (first
+            // ncav + 1 triangles of the BFS) + the far side of a split edge
+            len = min(len, ncav + 1);
+            u32 far = NONE;
+            if (c.kind[i] == 0) {
+                const int e = seg_slot(m.ts[located], c.id[i]);
+                if (e >= 0) {
+                    const u32 cc = comp(m.tn[located], e);
+                    if (cc != NONE) far = etri(cc);
+                }
+            } else if (c.lkind[i] == 1) {
+                const u32 cc = comp(m.tn[located], c.ledge[i]);
+                if (cc != NONE) far = etri(cc);
+            }
+            if (far != NONE && !in_list(reg, len, far) && len < rs) reg[len++] = far;
+            blen = len;
+        }
+        const u64 key = c.key[i];
+        for (u32 k = 0; k < len; ++k) atomicMax((ull*)&ckey[reg[k]], (ull)key);
+    }
+    region_len[i] = len;
+    return blen;
+}
+
+// Survivor of an isolated claim set: inserts, unless encroachment precedence
+// turns it into a subsegment mark.  Returns 1 = inserts, 0 = not; *marked set
+// when this candidate newly marked a subsegment; *unsafe when it inserts from
+// a capped (non-isolated) claim set.
+__device__ __forceinline__ u32 isolated_check_one(const DevMesh& m, const DevCands& c, u32 i,
+                                                  u32 rs, const u32* regions,
+                                                  const u32* region_len, const u64* ckey,
+                                                  const u64* ctie, u32& marked, u32& unsafe) {
+    if (!cavity_check_one(c, i, rs, regions, region_len, ckey, ctie)) return 0;
+    const u32 red = c.red[i];
+    if (red != NONE) {
+        c.alive[i] = 0;
+        if (atomicExch(&m.senc[red], 1u) == 0u) marked = 1;
+        return 0;
+    }
+    if (c.unsafe[i]) unsafe = 1;
+    return 1;
+}
+
 // Needs of one surviving candidate (refine.hpp:493-539): subsegments that hit
 // the depth cap or fail subsegment_split_ok are abandoned (:501-506).
 // Returns 1 if the candidate was dropped.

@@ -79,6 +79,48 @@ __global__ void k_cavity_reset(u32 n, u32 rs, const u32* __restrict__ regions,
     if (i < n) cavity_reset_one(i, rs, regions, region_len, ckey, ctie);
 }
 
+// ---- isolated claims (GDP2D_INSERT_ISOLATED, gdp2d_phases.cuh) ----
+
+template <int MODE>
+__global__ void __launch_bounds__(128) k_cavity_claims(DevMesh m, DevCands c, u32 n, u32 ncav,
+                                                       u32 rs, u32* __restrict__ regions,
+                                                       u32* __restrict__ region_len,
+                                                       u64* __restrict__ ckey, u64 depth_cap,
+                                                       int ring, Counters* ctr) {
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    ull visits = 0;
+    if (i < n)
+        visits = cavity_claims_one<MODE>(m, c, i, ncav, rs, regions, region_len, ckey, depth_cap,
+                                         ring != 0);
+    block_add<ull>(&ctr->cavity_visits, visits);
+}
+
+__global__ void k_isolated_check(DevMesh m, DevCands c, u32 n, u32 rs,
+                                 const u32* __restrict__ regions,
+                                 const u32* __restrict__ region_len, const u64* __restrict__ ckey,
+                                 const u64* __restrict__ ctie, u32* unsafe_flag, Counters* ctr) {
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    u32 surv = 0, marked = 0, unsafe = 0;
+    if (i < n) surv = isolated_check_one(m, c, i, rs, regions, region_len, ckey, ctie, marked, unsafe);
+    if (unsafe) atomicOr(unsafe_flag, 1u);
+    block_add<u32>(&ctr->surv_cavity, surv);
+    block_add<u32>(&ctr->marked, marked);
+}
+
+void launch_cavity_isolated(const DevMesh& m, DevCands c, u32 n, u32 ncav, u32 rs, int mode,
+                            u64 depth_cap, bool ring, TriAux a, u32* regions, u32* region_len,
+                            u32* unsafe_flag, Counters* d_ctr, cudaStream_t st) {
+    if (!n) return;
+    if (mode == 0)
+        note_launch(), k_cavity_claims<0><<<(n + 127) / 128, 128, 0, st>>>(m, c, n, ncav, rs, regions, region_len, a.ckey, depth_cap, ring ? 1 : 0, d_ctr);
+    else
+        note_launch(), k_cavity_claims<1><<<(n + 127) / 128, 128, 0, st>>>(m, c, n, ncav, rs, regions, region_len, a.ckey, depth_cap, ring ? 1 : 0, d_ctr);
+    const u32 g = (n + 255) / 256;
+    note_launch(), k_cavity_tie<<<g, 256, 0, st>>>(c, n, rs, regions, region_len, a.ckey, a.ctie);
+    note_launch(), k_isolated_check<<<g, 256, 0, st>>>(m, c, n, rs, regions, region_len, a.ckey, a.ctie, unsafe_flag, d_ctr);
+    note_launch(), k_cavity_reset<<<g, 256, 0, st>>>(n, rs, regions, region_len, a.ckey, a.ctie);
+}
+
 void launch_cavity(const DevMesh& m, DevCands c, u32 n, u32 ncav, bool extras, TriAux a,
                    u32* regions, u32* region_len, u32* bfs_len, Counters* d_ctr,
                    cudaStream_t st) {

@@ -591,6 +591,68 @@ __device__ __noinline__ void detect_b_one(const DevMesh& m, u32 V0, u32 F, u32 j
     }
 }
 
+// (b) with the priority-MIS rule: a same-batch circumcenter is rolled back
+// iff a higher-priority neighbour that STAYS exists.  This is the smallest
+// removal set leaving no two adjacent same-batch circumcenters; the
+// reference's sequential sweep (refine.hpp:589-607) removes a set between it
+// and the "any higher neighbour" rule of detect_b_one (a chain a > b > c loses
+// b only, or b and c, depending on the triangle order of the sweep).
+// Pass 1 (this function): collect the higher-priority eligible neighbours;
+// no neighbour -> kept, else undecided (returned true).
+__device__ __noinline__ bool detect_b_mis_one(const DevMesh& m, u32 V0, u32 F, u32 j,
+                                              const FreshInfo& f) {
+    if (!f.cc[j] || f.removed[j] || f.mark[j] == 1) {
+        f.dstat[j] = 2;   // not a live circumcenter of this batch
+        return false;
+    }
+    const u32 v = V0 + j;
+    u32 st[MAX_STAR];
+    int si[MAX_STAR];
+    const int k = walk_star(m, v, st, si, MAX_STAR);
+    u32 cnt = 0;
+    bool overflow = false;
+    for (int q = 0; q < k; ++q) {
+        const u32 x = comp(m.tv[st[q]], nxt(si[q]));
+        if (x < V0 || x >= V0 + F) continue;
+        const u32 jx = x - V0;
+        if (!f.cc[jx] || f.removed[jx] == 1 || f.mark[jx] == 1) continue;
+        if (prio_gt(f, jx, j)) {
+            if (cnt < (u32)DEP_HMAX)
+                f.hlist[(size_t)j * DEP_HMAX + cnt++] = jx;
+            else
+                overflow = true;
+        }
+    }
+    f.hcnt[j] = (uint8_t)cnt;
+    if (overflow) {       // cannot track them all: the conservative rule
+        f.dstat[j] = 2;
+        f.mark[j] = 2;
+        return false;
+    }
+    f.dstat[j] = cnt == 0 ? 1 : 0;
+    return cnt != 0;
+}
+
+// One MIS round for an undecided vertex; returns true if still undecided.
+__device__ __forceinline__ bool mis_round_one(u32 j, const FreshInfo& f) {
+    const u32 cnt = f.hcnt[j];
+    bool all_removed = true;
+    for (u32 q = 0; q < cnt; ++q) {
+        const uint8_t s = f.dstat[f.hlist[(size_t)j * DEP_HMAX + q]];
+        if (s == 1) {
+            f.dstat[j] = 2;
+            f.mark[j] = 2;
+            return false;
+        }
+        all_removed &= s == 2;
+    }
+    if (all_removed) {
+        f.dstat[j] = 1;
+        return false;
+    }
+    return true;
+}
+
 __global__ void k_detect_b(DevMesh m, u32 V0, u32 F, FreshInfo f, Counters* ctr) {
     const u32 j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j < F) detect_b_one(m, V0, F, j, f);
@@ -911,6 +973,8 @@ struct InsertArgs {
     u32 small_c;          // block mode for the whole batch when C <= small_c
     int resume;           // 1: candidates are planned, start at the capacity check
     int filter;           // 1: run Lines 5-7 in kernel 1 (tiny batches)
+    int isolate;          // claims: 0 reference, 1 isolated (rollback only if state[8]), 2 precedence
+    int dep_mis;          // dependent pairs: 1 = priority-MIS rule, 0 = any-higher-neighbour rule
     unsigned long long* trace;   // GDP2D_TRACE: (globaltimer << 8 | tag) per step, or null
     u32* trace_val;              // a work count per trace entry
     u32* trace_n;
@@ -1066,15 +1130,24 @@ __device__ void filter(const InsertArgs& a, const Exec& ex, u32 C) {
     for (u32 i = ex.tid; i < C; i += ex.nthr) claim_reset_one(a.c, i, m.nT, a.x.ckey, a.x.ctie);
     ex.sync();
     trace(a, ex.leader(), TR_CLAIM);
+    u32 marked = 0, unsafe = 0;
     for (u32 i = ex.tid; i < C; i += ex.nthr)
-        visits += cavity_bfs_one(m, a.c, i, a.ncav, 1, a.rs, a.regions, a.region_len, nullptr,
-                                 a.x.ckey);
+        visits += a.isolate
+                      ? cavity_claims_one<MODE>(m, a.c, i, a.ncav, a.rs, a.regions, a.region_len,
+                                                a.x.ckey, a.depth_cap, a.isolate == 1)
+                      : cavity_bfs_one(m, a.c, i, a.ncav, 1, a.rs, a.regions, a.region_len,
+                                       nullptr, a.x.ckey);
     ex.sync();
     for (u32 i = ex.tid; i < C; i += ex.nthr)
         cavity_tie_one(a.c, i, a.rs, a.regions, a.region_len, a.x.ckey, a.x.ctie);
     ex.sync();
     for (u32 i = ex.tid; i < C; i += ex.nthr)
-        surv2 += cavity_check_one(a.c, i, a.rs, a.regions, a.region_len, a.x.ckey, a.x.ctie);
+        surv2 += a.isolate ? isolated_check_one(m, a.c, i, a.rs, a.regions, a.region_len,
+                                                a.x.ckey, a.x.ctie, marked, unsafe)
+                           : cavity_check_one(a.c, i, a.rs, a.regions, a.region_len, a.x.ckey,
+                                              a.x.ctie);
+    if (unsafe) atomicOr(&a.state[8], 1u);
+    warp_add_u32(&a.ctr->marked, marked);
     ex.sync();
     for (u32 i = ex.tid; i < C; i += ex.nthr)
         cavity_reset_one(i, a.rs, a.regions, a.region_len, a.x.ckey, a.x.ctie);
@@ -1243,12 +1316,61 @@ __device__ void rollback_loop(const InsertArgs& a, const Exec& ex, u32 nv, u32 n
         }
         ex.sync();
         trace(a, ex.leader(), TR_DET_A);
-        for (u32 j = ex.tid; j < F; j += ex.nthr) {
-            if (a.f.dirty[j] != 2) continue;
-            a.f.dirty[j] = 0;
-            detect_b_one(m, V0, F, j, a.f);
+        if (!a.dep_mis) {
+            for (u32 j = ex.tid; j < F; j += ex.nthr) {
+                if (a.f.dirty[j] != 2) continue;
+                a.f.dirty[j] = 0;
+                detect_b_one(m, V0, F, j, a.f);
+            }
+            ex.sync();
+        } else {
+            // undecided vertices go to w.rm[1] (free until the removal rounds)
+            for (u32 j = ex.tid; j < F; j += ex.nthr) {
+                if (a.f.dirty[j] != 2) continue;
+                a.f.dirty[j] = 0;
+                if (detect_b_mis_one(m, V0, F, j, a.f)) {
+                    const u32 o = agg_reserve(&rc->cand, 1u);
+                    if (o < w.rm_cap) w.rm[1][o] = j;
+                }
+            }
+            ex.sync();
+            u32 nu = min(vload(&rc->cand), w.rm_cap);
+            ++step;   // the detect slot is used up: MIS rounds take fresh ring slots
+            // rounds alternate between rm[1] and w.touched (both >= F entries)
+            u32* lists[2] = {w.rm[1], w.touched};
+            u32 lc = 0;
+            for (u32 r = 0; nu > 0 && r < 4096; ++r) {
+                RoundCtr* rr = ring_at(a, step);
+                ring_advance(a, ex, step);
+                ++step;
+                for (u32 i = ex.tid; i < nu; i += ex.nthr) {
+                    const u32 j = lists[lc][i];
+                    if (mis_round_one(j, a.f)) {
+                        const u32 o = agg_reserve(&rr->cand, 1u);
+                        lists[lc ^ 1u][o] = j;
+                    }
+                }
+                ex.sync();
+                const u32 nn = vload(&rr->cand);
+                if (nn == nu) {
+                    // no progress (cannot happen for a strict priority order):
+                    // fall back to removing the rest
+                    for (u32 i = ex.tid; i < nn; i += ex.nthr) {
+                        const u32 j = lists[lc ^ 1u][i];
+                        a.f.dstat[j] = 2;
+                        a.f.mark[j] = 2;
+                    }
+                    ex.sync();
+                    break;
+                }
+                nu = nn;
+                lc ^= 1u;
+            }
+            rc = ring_at(a, step);
+            ring_advance(a, ex, step);
+            if (ex.leader()) seed_rc->wl_next = 0;
+            ex.sync();
         }
-        ex.sync();
         trace(a, ex.leader(), TR_DET_B);
         for (u32 j = ex.tid; j < F; j += ex.nthr) {
             u32 r1 = 0, r2 = 0;
@@ -1346,6 +1468,9 @@ __global__ void __launch_bounds__(INSERT_BLOCK, GDP2D_SPLIT_MINB) k_batch_split(
 template <int MODE>
 __global__ void __launch_bounds__(INSERT_BLOCK) k_batch_rollback(InsertArgs a) {
     if (vload(&a.state[0]) != INS_OK) return;
+    // isolated insertions cannot create redundant or dependent points: the
+    // detection runs only when some survivor came from a capped claim set
+    if (a.isolate == 1 && vload(&a.state[8]) == 0) return;
     const u32 nv = vload(&a.b.totals[0]), nt = vload(&a.b.totals[1]), ns = vload(&a.b.totals[2]);
     if (nv == 0) return;
     const bool block = nv <= a.small_c;
@@ -1400,6 +1525,8 @@ void launch_insert_persistent(const InsertLaunch& L, int mode, int grid, int gri
     a.small_c = L.small_c;
     a.resume = L.resume;
     a.filter = L.filter;
+    a.isolate = L.isolate;
+    a.dep_mis = L.dep_mis;
     a.trace = L.trace;
     a.trace_val = L.trace_val;
     a.trace_n = L.trace_n;

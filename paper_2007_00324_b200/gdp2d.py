@@ -75,6 +75,7 @@ class EngineConfig:
     batch_size_cap: int = 0
     seed: int = 0
     little_batch_sizing: bool = False
+    insert_mode: int = 1          # 1 = rollback (reference, default), 0 = isolated, 2 = precedence
     device: int = 0
 
 
@@ -92,6 +93,7 @@ def make_params(q: QualityCriteria, cfg: Optional[EngineConfig] = None) -> A.Par
     p.rule2_filtering_enabled = int(bool(cfg.rules.rule2_filtering_enabled))
     p.rule4_unified_collection = int(bool(cfg.rules.rule4_unified_collection))
     p.little_batch_sizing = int(bool(cfg.little_batch_sizing))
+    p.insert_mode = int(cfg.insert_mode)
     p.iteration_cap = cfg.iteration_cap
     p.split_depth_cap = cfg.split_depth_cap
     p.batch_size_cap = cfg.batch_size_cap

@@ -84,12 +84,13 @@ def test_corpus(built):
                                                                      rref.steiner_points)
 
 
+@pytest.mark.parametrize("insert_mode", [0, 1, 2])
 @pytest.mark.parametrize("theta", [B_SQRT2_THETA, 30.0])
-def test_uniform_50k(built, theta):
-    from paper_2007_00324_b200 import QualityCriteria, host
+def test_uniform_50k(built, theta, insert_mode):
+    from paper_2007_00324_b200 import EngineConfig, QualityCriteria, host
     q = QualityCriteria(theta)
     pts, segs = host.generate_pslg(50_000, 5_000, "uniform", 3)
-    out, closed, rep, rref = _run(pts, segs, q)
+    out, closed, rep, rref = _run(pts, segs, q, EngineConfig(insert_mode=insert_mode))
     check_invariants(out, pts, closed, q, cdt_check=True)
     assert abs(rep.steiner_points - rref.steiner_points) <= 0.10 * rref.steiner_points, \
         (rep.steiner_points, rref.steiner_points)

@@ -9,7 +9,8 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 
 import numpy as np  # noqa: E402
 
-from paper_2007_00324_b200 import Engine, QualityCriteria, host  # noqa: E402
+from paper_2007_00324_b200 import Engine, EngineConfig, QualityCriteria, host  # noqa: E402
+import os  # noqa: E402
 
 
 def main():
@@ -35,7 +36,7 @@ def main():
         for r in range(a.reps):
             eng.reset()
             t = time.time()
-            rep = eng.refine(q)
+            rep = eng.refine(q, EngineConfig(insert_mode=int(os.environ.get('GDP2D_MODE', '1'))))
             dt = time.time() - t
             print(f"rep {r}: wall {rep.wall_seconds*1e3:.1f} ms device {rep.device_seconds*1e3:.1f} ms "
                   f"py {dt*1e3:.1f} ms steiner {rep.steiner_points} batches {len(rep.batches)} "
