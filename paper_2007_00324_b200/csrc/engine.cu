@@ -332,6 +332,7 @@ struct gdp2d_ctx {
     u32 small_wl = 256;           // GDP2D_SMALL_WL: block-mode Lawson below this list size
     u32 small_c = 256;            // GDP2D_SMALL_C: whole batch in one CTA at or below
     bool dep_mis = false;         // GDP2D_DEP=mis: dependent pairs by the priority-MIS rule
+    bool check = false;           // GDP2D_CHECK=1: validate after each insertion kernel
     u32* scan_part = nullptr;     // [3 * insert_grid] plan chunk sums
     RoundCtr* rcs = nullptr;      // per-round counters of the persistent kernel
     u32* d_res = nullptr;
@@ -587,6 +588,7 @@ void ctx_init(gdp2d_ctx* x, int device) {
     if (const char* e = std::getenv("GDP2D_SMALL_WL")) x->small_wl = (u32)std::strtoul(e, nullptr, 10);
     if (const char* e = std::getenv("GDP2D_SMALL_C")) x->small_c = (u32)std::strtoul(e, nullptr, 10);
     if (const char* e = std::getenv("GDP2D_DEP")) x->dep_mis = std::string(e) == "mis";
+    if (const char* e = std::getenv("GDP2D_CHECK")) x->check = e[0] == '1';
     dalloc(x->scan_part, 3ull * x->insert_grid + 3);
     dalloc(x->ins_state, 16);
     CK(cudaMallocHost(&x->h_state, 16 * sizeof(u32)));
@@ -847,6 +849,30 @@ void insert_legacy(gdp2d_ctx* x, const gdp2d_params* p, const Quality& q, u32 C,
     }
 }
 
+// GDP2D_CHECK=1: device structural validation of the working mesh grown by
+// this batch's reserved ids (totals read back first).
+void check_structure_now(gdp2d_ctx* x, u32 nV, u32 nT, u32 nS, const char* where) {
+    CK(cudaMemcpyAsync(x->h_tot, x->ib.totals, 3 * sizeof(u32), cudaMemcpyDeviceToHost, x->st));
+    CK(cudaMemcpyAsync(x->h_state, x->ins_state, 16 * sizeof(u32), cudaMemcpyDeviceToHost, x->st));
+    CK(cudaStreamSynchronize(x->st));
+    if (x->h_state[0] != 0u) return;   // growth request: nothing was written
+    DevMesh m = x->work.m;
+    m.nV = nV + x->h_tot[0];
+    m.nT = nT + x->h_tot[1];
+    m.nS = nS + x->h_tot[2];
+    launch_validate(m, x->d_val, x->st);
+    u32 h[4];
+    CK(cudaMemcpyAsync(h, x->d_val, sizeof h, cudaMemcpyDeviceToHost, x->st));
+    CK(cudaStreamSynchronize(x->st));
+    check_dev_err(x);
+    if (h[0]) {
+        char buf[200];
+        snprintf(buf, sizeof buf, "check after %s (batch %u): failure %u at triangle %u edge %d",
+                 where, x->epoch, h[0], h[1], (int)h[2]);
+        throw Fail{GDP2D_EMESH, buf};
+    }
+}
+
 // Insertion phase as one persistent cooperative launch (k_insert.cu): no host
 // round trip inside; the capacity check runs on the device and a batch that
 // does not fit is re-launched after growing the buffers (the mesh is not
@@ -901,8 +927,18 @@ void insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, u32 C, u32 ncav, u32
         x->tr.mark("pre_ins", st);
         CK(cudaMemsetAsync(x->ins_state, 0, 8 * sizeof(u32), st));   // word 8 = unsafe flag stays
         CK(cudaEventRecord(x->ev_k[0], st));
-        launch_insert_persistent(L, p->mode == GDP2D_CHEW ? 1 : 0, x->insert_grid,
-                                 x->rollback_grid, st, x->ev_k[1]);
+        if (!x->check) {
+            launch_insert_persistent(L, p->mode == GDP2D_CHEW ? 1 : 0, x->insert_grid,
+                                     x->rollback_grid, st, x->ev_k[1]);
+        } else {
+            // GDP2D_CHECK=1: structural validation after each kernel
+            launch_insert_persistent(L, p->mode == GDP2D_CHEW ? 1 : 0, x->insert_grid,
+                                     x->rollback_grid, st, x->ev_k[1], 1);
+            check_structure_now(x, x->work.m.nV, x->work.m.nT, x->work.m.nS, "split kernel");
+            launch_insert_persistent(L, p->mode == GDP2D_CHEW ? 1 : 0, x->insert_grid,
+                                     x->rollback_grid, st, nullptr, 2);
+            check_structure_now(x, x->work.m.nV, x->work.m.nT, x->work.m.nS, "rollback kernel");
+        }
         CK(cudaEventRecord(x->ev_k[2], st));
         x->tr.mark("insert_kernel", st);
         CK(cudaGetLastError());

@@ -185,8 +185,9 @@ int insert_persistent_grid(int device);
 int rollback_persistent_grid(int device);
 // Kernel 1 (plan + splits + Lawson, with Lines 5-7 when L.filter) then
 // kernel 2 (detect + rollback loop), both cooperative, no host sync between.
+// which: 1 = kernel 1 only, 2 = kernel 2 only, 3 = both back to back.
 void launch_insert_persistent(const InsertLaunch& L, int mode, int grid, int grid2,
-                              cudaStream_t st, cudaEvent_t between = nullptr);
+                              cudaStream_t st, cudaEvent_t between = nullptr, int which = 3);
 
 // Redundancy detection (refine.hpp:551-608): fills w.rm[0], count in w.rc->detect.
 void launch_detect(const DevMesh& m, const Quality& q, u64 depth_cap, u32 V0, u32 F,

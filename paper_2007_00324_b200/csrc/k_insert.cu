@@ -541,7 +541,30 @@ __device__ __noinline__ u32 detect_a_one(const DevMesh& m, u64 depth_cap, u32 V0
         u32 st[MAX_STAR];
         int si[MAX_STAR];
         const int k = walk_star(m, v, st, si, MAX_STAR);
-        if (k == 0) raise_err(ctr, DERR_OPEN_STAR, v);
+        if (k == 0 && atomicCAS(&ctr->err_code, 0u, (u32)DERR_OPEN_STAR) == 0u) {
+            // dbg: vtri, alive, fresh index, xy, walk steps, reason
+            // (1 vertex missing from a fan triangle, 2 star > MAX_STAR, 3 open fan)
+            ctr->err_info = v;
+            const u32 t0 = m.vtri[v];
+            ctr->dbg[0] = (double)t0;
+            ctr->dbg[1] = (double)m.valive[v];
+            ctr->dbg[2] = (double)j;
+            ctr->dbg[3] = m.xy[v].x;
+            ctr->dbg[4] = m.xy[v].y;
+            u32 cur = t0;
+            int kk = 0, why = 0;
+            for (; t0 != NONE && kk < 256; ++kk) {
+                const uint4 tv = m.tv[cur];
+                const int ii = tv.x == v ? 0 : (tv.y == v ? 1 : (tv.z == v ? 2 : -1));
+                if (ii < 0) { why = 1; break; }
+                const u32 cn = comp(m.tn[cur], nxt(ii));
+                if (cn == NONE) { why = 3; break; }
+                cur = etri(cn);
+                if (cur == t0) { why = 2; break; }
+            }
+            ctr->dbg[5] = (double)kk;
+            ctr->dbg[6] = (double)why;
+        }
         const double2 pv = m.xy[v];
         u32 best = NONE;
         for (int q = 0; q < k; ++q) {
@@ -1496,7 +1519,7 @@ int rollback_persistent_grid(int device) {
 }
 
 void launch_insert_persistent(const InsertLaunch& L, int mode, int grid, int grid2, cudaStream_t st,
-                              cudaEvent_t between) {
+                              cudaEvent_t between, int which) {
     InsertArgs a;
     a.m = L.m;
     a.c = L.c;
@@ -1532,13 +1555,17 @@ void launch_insert_persistent(const InsertLaunch& L, int mode, int grid, int gri
     a.trace_n = L.trace_n;
     a.trace_cap = L.trace_cap;
     void* args[] = {&a};
-    note_launch();
-    cudaLaunchCooperativeKernel(mode ? (void*)k_batch_split<1> : (void*)k_batch_split<0>, dim3(grid),
-                                dim3(INSERT_BLOCK), args, 0, st);
+    if (which & 1) {
+        note_launch();
+        cudaLaunchCooperativeKernel(mode ? (void*)k_batch_split<1> : (void*)k_batch_split<0>,
+                                    dim3(grid), dim3(INSERT_BLOCK), args, 0, st);
+    }
     if (between) cudaEventRecord(between, st);
-    note_launch();
-    cudaLaunchCooperativeKernel(mode ? (void*)k_batch_rollback<1> : (void*)k_batch_rollback<0>,
-                                dim3(grid2), dim3(INSERT_BLOCK), args, 0, st);
+    if (which & 2) {
+        note_launch();
+        cudaLaunchCooperativeKernel(mode ? (void*)k_batch_rollback<1> : (void*)k_batch_rollback<0>,
+                                    dim3(grid2), dim3(INSERT_BLOCK), args, 0, st);
+    }
 }
 
 }  // namespace gdp2d
