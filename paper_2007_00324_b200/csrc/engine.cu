@@ -333,6 +333,7 @@ struct gdp2d_ctx {
     u32 small_c = 256;            // GDP2D_SMALL_C: whole batch in one CTA at or below
     bool dep_mis = false;         // GDP2D_DEP=mis: dependent pairs by the priority-MIS rule
     bool check = false;           // GDP2D_CHECK=1: validate after each insertion kernel
+    int extras = 2;               // GDP2D_EXTRAS: 2 rewrite table (default), 1 far side in main claims
     u32* scan_part = nullptr;     // [3 * insert_grid] plan chunk sums
     RoundCtr* rcs = nullptr;      // per-round counters of the persistent kernel
     u32* d_res = nullptr;
@@ -350,7 +351,7 @@ namespace {
 void cands_free(DevCands& c) {
     dfree(c.pt); dfree(c.key); dfree(c.id); dfree(c.tie); dfree(c.loc);
     dfree(c.kind); dfree(c.alive); dfree(c.lkind); dfree(c.ledge); dfree(c.fb);
-    dfree(c.red); dfree(c.unsafe);
+    dfree(c.red); dfree(c.unsafe); dfree(c.far);
 }
 
 void ensure_cands(gdp2d_ctx* x, u32 n) {
@@ -360,7 +361,7 @@ void ensure_cands(gdp2d_ctx* x, u32 n) {
     dalloc(x->c.pt, cap); dalloc(x->c.key, cap); dalloc(x->c.id, cap); dalloc(x->c.tie, cap);
     dalloc(x->c.loc, cap); dalloc(x->c.kind, cap); dalloc(x->c.alive, cap);
     dalloc(x->c.lkind, cap); dalloc(x->c.ledge, cap); dalloc(x->c.fb, cap);
-    dalloc(x->c.red, cap); dalloc(x->c.unsafe, cap);
+    dalloc(x->c.red, cap); dalloc(x->c.unsafe, cap); dalloc(x->c.far, cap);
     x->ccap = cap;
     // per-candidate insertion buffers
     dfree(x->ib.nv); dfree(x->ib.nt); dfree(x->ib.ns); dfree(x->ib.ov); dfree(x->ib.ot);
@@ -391,11 +392,14 @@ void ensure_aux(gdp2d_ctx* x) {
     const u32 T = x->work.tcap;
     if (T > x->aux_cap) {
         dfree(x->aux.ckey); dfree(x->aux.ctie); dfree(x->aux.owner); dfree(x->aux.stamp);
-        dfree(x->aux.emap);
+        dfree(x->aux.emap); dfree(x->aux.fkey); dfree(x->aux.ftie);
         dalloc(x->aux.ckey, T); dalloc(x->aux.ctie, T); dalloc(x->aux.owner, T);
         dalloc(x->aux.stamp, T); dalloc(x->aux.emap, 3ull * T);
+        dalloc(x->aux.fkey, T); dalloc(x->aux.ftie, T);
         CK(cudaMemsetAsync(x->aux.ckey, 0, sizeof(u64) * T, x->st));
         CK(cudaMemsetAsync(x->aux.ctie, 0xFF, sizeof(u64) * T, x->st));
+        CK(cudaMemsetAsync(x->aux.fkey, 0, sizeof(u64) * T, x->st));
+        CK(cudaMemsetAsync(x->aux.ftie, 0xFF, sizeof(u64) * T, x->st));
         CK(cudaMemsetAsync(x->aux.owner, 0xFF, sizeof(u32) * T, x->st));
         CK(cudaMemsetAsync(x->aux.stamp, 0, sizeof(u32) * T, x->st));
         x->aux_cap = T;
@@ -589,6 +593,7 @@ void ctx_init(gdp2d_ctx* x, int device) {
     if (const char* e = std::getenv("GDP2D_SMALL_C")) x->small_c = (u32)std::strtoul(e, nullptr, 10);
     if (const char* e = std::getenv("GDP2D_DEP")) x->dep_mis = std::string(e) == "mis";
     if (const char* e = std::getenv("GDP2D_CHECK")) x->check = e[0] == '1';
+    if (const char* e = std::getenv("GDP2D_EXTRAS")) x->extras = std::atoi(e);
     dalloc(x->scan_part, 3ull * x->insert_grid + 3);
     dalloc(x->ins_state, 16);
     CK(cudaMallocHost(&x->h_state, 16 * sizeof(u32)));
@@ -605,7 +610,7 @@ void ctx_release(gdp2d_ctx* x) {
     mesh_free(x->work);
     mesh_free(x->pristine);
     dfree(x->aux.ckey); dfree(x->aux.ctie); dfree(x->aux.owner); dfree(x->aux.stamp);
-    dfree(x->aux.emap); dfree(x->flags);
+    dfree(x->aux.emap); dfree(x->aux.fkey); dfree(x->aux.ftie); dfree(x->flags);
     cands_free(x->c);
     dfree(x->regions); dfree(x->region_len); dfree(x->bfs_len);
     dfree(x->ib.nv); dfree(x->ib.nt); dfree(x->ib.ns); dfree(x->ib.ov); dfree(x->ib.ot);
@@ -911,6 +916,7 @@ void insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, u32 C, u32 ncav, u32
         L.rs = rs;
         L.isolate = isolate;
         L.dep_mis = x->dep_mis ? 1 : 0;
+        L.extras = x->extras;
         L.regions = x->regions;
         L.region_len = x->region_len;
         L.scan_part = x->scan_part;
@@ -1060,7 +1066,7 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
             launch_claim(m, x->c, C, x->aux, x->d_ctr, st);
             x->tr.mark("claim", st);
             CK(cudaEventRecord(x->ev[4], st));
-            launch_cavity(m, x->c, C, ncav, true, x->aux, x->regions, x->region_len, nullptr,
+            launch_cavity(m, x->c, C, ncav, 1, x->aux, x->regions, x->region_len, nullptr,
                           x->d_ctr, st);
             x->tr.mark("cavity", st);
             CK(cudaEventRecord(x->ev[5], st));
@@ -1082,8 +1088,8 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
                                            p->split_depth_cap, isolate == 1, x->aux, x->regions,
                                            x->region_len, x->ins_state + 8, x->d_ctr, st);
                 else
-                    launch_cavity(m, x->c, C, ncav, true, x->aux, x->regions, x->region_len,
-                                  nullptr, x->d_ctr, st);
+                    launch_cavity(m, x->c, C, ncav, x->extras, x->aux, x->regions,
+                                  x->region_len, nullptr, x->d_ctr, st);
                 CK(cudaEventRecord(x->ev[5], st));
             } else {
                 // tail batch: everything runs inside the block-mode kernels
@@ -1532,7 +1538,7 @@ int gdp2d_cavity(gdp2d_ctx* x, gdp2d_candidate* c, uint32_t n, uint32_t n_cav,
         upload_cands(x, c, n);
         ensure_regions(x, n, n_cav);
         CK(cudaMemsetAsync(x->d_ctr, 0, sizeof(Counters), x->st));
-        launch_cavity(x->work.m, x->c, n, n_cav, false, x->aux, x->regions, x->region_len,
+        launch_cavity(x->work.m, x->c, n, n_cav, 0, x->aux, x->regions, x->region_len,
                       x->bfs_len, x->d_ctr, x->st);
         CK(cudaGetLastError());
         download_cands(x, c, n);

@@ -39,6 +39,10 @@ struct TriAux {
     u32* owner = nullptr;    // flip / removal claim
     u32* stamp = nullptr;    // round in which the triangle was rewritten
     u32* emap = nullptr;     // 3 per triangle: old edge slot -> new (tri<<2|edge)
+    // rewrite table: every candidate claims the triangles its split REWRITES
+    // (located, + the far side of a split edge); see gdp2d_phases.cuh
+    u64* fkey = nullptr;
+    u64* ftie = nullptr;
 };
 
 struct CollectBufs {
@@ -67,7 +71,10 @@ void launch_locate(const DevMesh& m, DevCands c, u32 n, Counters* d_ctr, cudaStr
 void launch_claim(const DevMesh& m, DevCands c, u32 n, TriAux a, Counters* d_ctr,
                   cudaStream_t st);
 // Cavity filter; extras = refine-mode extra claims (far side of a split edge).
-void launch_cavity(const DevMesh& m, DevCands c, u32 n, u32 ncav, bool extras, TriAux a,
+// extras: 0 parity (reference claims only), 1 refine with the far side of a
+// split edge added to the main claims, 2 refine with the rewrite table
+// (gdp2d_phases.cuh).
+void launch_cavity(const DevMesh& m, DevCands c, u32 n, u32 ncav, int extras, TriAux a,
                    u32* regions, u32* region_len, u32* bfs_len, Counters* d_ctr,
                    cudaStream_t st);
 
@@ -176,6 +183,7 @@ struct InsertLaunch {
     int filter = 1;
     int isolate = 1;            // claims: 0 reference cavity, 1 isolated (ring), 2 precedence
     int dep_mis = 0;            // dependent pairs by the priority-MIS rule
+    int extras = 2;             // cavity extras mode (see launch_cavity)
     unsigned long long* trace = nullptr;   // device step trace (GDP2D_TRACE=1)
     u32* trace_val = nullptr;
     u32* trace_n = nullptr;

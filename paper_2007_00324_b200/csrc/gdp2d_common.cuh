@@ -81,6 +81,7 @@ struct DevCands {
     uint8_t* fb;    // circumcenter fallback used
     u32* red;       // isolated insertion: lowest splittable subsegment the point would encroach
     uint8_t* unsafe;// isolated insertion: cavity hit the cap (not provably isolated)
+    u32* far;       // far side of this candidate's split edge (rewrite table), or NONE
 };
 
 // Per-batch device counters (zeroed at the start of each batch).

@@ -115,8 +115,10 @@ __device__ __forceinline__ void claim_reset_one(const DevCands& c, u32 i, u32 nT
 // with emissions appended in (source, slot) order visits triangles in exactly
 // the window order of expand() (expandlist.hpp:98-152), so the region -- and
 // hence the claim set -- is the reference's, including when the cap binds.
-// extras (refine mode): the triangle across a split edge is claimed too
-// (SURVEY §7 hard part (i)).  Returns the BFS region size (cavity visits).
+// extras == 1: the triangle across a split edge is added to the claims
+// (SURVEY §7 hard part (i)).  extras == 2 leaves the region exactly the
+// reference's and the rewrite table (rw_*_one) guards the split instead.
+// Returns the BFS region size (cavity visits).
 __device__ __forceinline__ u32 cavity_bfs_one(const DevMesh& m, const DevCands& c, u32 i,
                                               u32 ncav, int extras, u32 rs, u32* regions,
                                               u32* region_len, u32* bfs_len, u64* ckey) {
@@ -154,7 +156,7 @@ __device__ __forceinline__ u32 cavity_bfs_one(const DevMesh& m, const DevCands& 
             }
         }
         blen = len;
-        if (extras) {
+        if (extras == 1) {
             u32 far = NONE;
             if (c.kind[i] == 0) {
                 const u32 s = c.id[i];
@@ -365,20 +367,9 @@ __device__ __forceinline__ u32 cavity_claims_one(const DevMesh& m, const DevCand
         }
         if (!ok) {
             // fall back to the reference claim set: the capped region (first
-            // ncav + 1 triangles of the BFS) + the far side of a split edge
+            // ncav + 1 triangles of the BFS); the rewrite table guards the
+            // far side of a split edge
             len = min(len, ncav + 1);
-            u32 far = NONE;
-            if (c.kind[i] == 0) {
-                const int e = seg_slot(m.ts[located], c.id[i]);
-                if (e >= 0) {
-                    const u32 cc = comp(m.tn[located], e);
-                    if (cc != NONE) far = etri(cc);
-                }
-            } else if (c.lkind[i] == 1) {
-                const u32 cc = comp(m.tn[located], c.ledge[i]);
-                if (cc != NONE) far = etri(cc);
-            }
-            if (far != NONE && !in_list(reg, len, far) && len < rs) reg[len++] = far;
             blen = len;
         }
         const u64 key = c.key[i];
@@ -405,6 +396,73 @@ __device__ __forceinline__ u32 isolated_check_one(const DevMesh& m, const DevCan
     }
     if (c.unsafe[i]) unsafe = 1;
     return 1;
+}
+
+// ---- rewrite table -------------------------------------------------------------
+//
+// Two splits must never rewrite the same triangle: a circumcenter rewrites its
+// located triangle (and the far side when it lies on an edge), a subsegment
+// midpoint its located triangle and the triangle across the subsegment.  The
+// cavity claims (the reference's, main table) do not cover the far sides, so
+// every candidate also claims its rewritten triangles, with its priority, in a
+// second table; a survivor must own both.  Unlike adding the far side to the
+// cavity claim, this only blocks a circumcenter whose own split would touch a
+// midpoint's far triangle, not one whose cavity merely reaches it (the
+// reference inserts both, serially, refine.hpp:492-539).
+
+__device__ __forceinline__ void rw_set(const DevMesh& m, const DevCands& c, u32 i, u32& t,
+                                       u32& far) {
+    t = c.loc[i];
+    far = NONE;
+    int e = -1;
+    if (c.kind[i] == 0) e = seg_slot(m.ts[t], c.id[i]);
+    else if (c.lkind[i] == 1) e = c.ledge[i];
+    if (e >= 0) {
+        const u32 cc = comp(m.tn[t], e);
+        if (cc != NONE) far = etri(cc);
+    }
+}
+
+__device__ __forceinline__ void rw_claim_one(const DevMesh& m, const DevCands& c, u32 i,
+                                             u64* fkey) {
+    u32 far = NONE;
+    if (c.alive[i]) {
+        u32 t;
+        rw_set(m, c, i, t, far);
+        atomicMax((ull*)&fkey[t], (ull)c.key[i]);
+        if (far != NONE) atomicMax((ull*)&fkey[far], (ull)c.key[i]);
+    }
+    c.far[i] = far;
+}
+
+__device__ __forceinline__ void rw_tie_one(const DevCands& c, u32 i, const u64* fkey, u64* ftie) {
+    if (!c.alive[i]) return;
+    const u64 key = c.key[i], tie = tie_of(c, i);
+    const u32 t = c.loc[i], far = c.far[i];
+    if (fkey[t] == key) atomicMin((ull*)&ftie[t], (ull)tie);
+    if (far != NONE && fkey[far] == key) atomicMin((ull*)&ftie[far], (ull)tie);
+}
+
+__device__ __forceinline__ bool rw_owns(const DevCands& c, u32 i, const u64* fkey,
+                                        const u64* ftie) {
+    const u64 key = c.key[i], tie = tie_of(c, i);
+    const u32 t = c.loc[i], far = c.far[i];
+    if (fkey[t] != key || ftie[t] != tie) return false;
+    if (far != NONE && (fkey[far] != key || ftie[far] != tie)) return false;
+    return true;
+}
+
+__device__ __forceinline__ void rw_reset_one(const DevCands& c, u32 i, u32 nT, u64* fkey,
+                                             u64* ftie) {
+    const u32 t = c.loc[i], far = c.far[i];
+    if (t < nT) {
+        fkey[t] = 0;
+        ftie[t] = ~0ull;
+    }
+    if (far != NONE && far < nT) {
+        fkey[far] = 0;
+        ftie[far] = ~0ull;
+    }
 }
 
 // Needs of one surviving candidate (refine.hpp:493-539): subsegments that hit

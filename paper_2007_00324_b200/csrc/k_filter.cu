@@ -56,6 +56,16 @@ __global__ void __launch_bounds__(128) k_cavity_bfs(DevMesh m, DevCands c, u32 n
     block_add<ull>(&ctr->cavity_visits, visits);
 }
 
+// rewrite table (gdp2d_phases.cuh)
+__global__ void k_rw_claim(DevMesh m, DevCands c, u32 n, u64* __restrict__ fkey) {
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) rw_claim_one(m, c, i, fkey);
+}
+__global__ void k_rw_tie(DevCands c, u32 n, const u64* __restrict__ fkey, u64* __restrict__ ftie) {
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) rw_tie_one(c, i, fkey, ftie);
+}
+
 __global__ void k_cavity_tie(DevCands c, u32 n, u32 rs, const u32* __restrict__ regions,
                              const u32* __restrict__ region_len, const u64* __restrict__ ckey,
                              u64* __restrict__ ctie) {
@@ -63,20 +73,34 @@ __global__ void k_cavity_tie(DevCands c, u32 n, u32 rs, const u32* __restrict__ 
     if (i < n) cavity_tie_one(c, i, rs, regions, region_len, ckey, ctie);
 }
 
+// fkey != null: a survivor must also own its rewritten triangles
 __global__ void k_cavity_check(DevCands c, u32 n, u32 rs, const u32* __restrict__ regions,
                                const u32* __restrict__ region_len, const u64* __restrict__ ckey,
-                               const u64* __restrict__ ctie, Counters* ctr) {
+                               const u64* __restrict__ ctie, const u64* __restrict__ fkey,
+                               const u64* __restrict__ ftie, Counters* ctr) {
     const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
     u32 surv = 0;
-    if (i < n) surv = cavity_check_one(c, i, rs, regions, region_len, ckey, ctie);
+    if (i < n) {
+        const bool rw_ok = !fkey || !c.alive[i] || rw_owns(c, i, fkey, ftie);
+        surv = cavity_check_one(c, i, rs, regions, region_len, ckey, ctie);
+        if (surv && !rw_ok) {
+            c.alive[i] = 0;
+            surv = 0;
+        }
+    }
     block_add<u32>(&ctr->surv_cavity, surv);
 }
 
-__global__ void k_cavity_reset(u32 n, u32 rs, const u32* __restrict__ regions,
+__global__ void k_cavity_reset(DevCands c, u32 n, u32 nT, u32 rs,
+                               const u32* __restrict__ regions,
                                const u32* __restrict__ region_len, u64* __restrict__ ckey,
-                               u64* __restrict__ ctie) {
+                               u64* __restrict__ ctie, u64* __restrict__ fkey,
+                               u64* __restrict__ ftie) {
     const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) cavity_reset_one(i, rs, regions, region_len, ckey, ctie);
+    if (i < n) {
+        cavity_reset_one(i, rs, regions, region_len, ckey, ctie);
+        if (fkey) rw_reset_one(c, i, nT, fkey, ftie);
+    }
 }
 
 // ---- isolated claims (GDP2D_INSERT_ISOLATED, gdp2d_phases.cuh) ----
@@ -98,10 +122,14 @@ __global__ void __launch_bounds__(128) k_cavity_claims(DevMesh m, DevCands c, u3
 __global__ void k_isolated_check(DevMesh m, DevCands c, u32 n, u32 rs,
                                  const u32* __restrict__ regions,
                                  const u32* __restrict__ region_len, const u64* __restrict__ ckey,
-                                 const u64* __restrict__ ctie, u32* unsafe_flag, Counters* ctr) {
+                                 const u64* __restrict__ ctie, const u64* __restrict__ fkey,
+                                 const u64* __restrict__ ftie, u32* unsafe_flag, Counters* ctr) {
     const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
     u32 surv = 0, marked = 0, unsafe = 0;
-    if (i < n) surv = isolated_check_one(m, c, i, rs, regions, region_len, ckey, ctie, marked, unsafe);
+    if (i < n) {
+        if (c.alive[i] && !rw_owns(c, i, fkey, ftie)) c.alive[i] = 0;
+        else surv = isolated_check_one(m, c, i, rs, regions, region_len, ckey, ctie, marked, unsafe);
+    }
     if (unsafe) atomicOr(unsafe_flag, 1u);
     block_add<u32>(&ctr->surv_cavity, surv);
     block_add<u32>(&ctr->marked, marked);
@@ -116,22 +144,31 @@ void launch_cavity_isolated(const DevMesh& m, DevCands c, u32 n, u32 ncav, u32 r
     else
         note_launch(), k_cavity_claims<1><<<(n + 127) / 128, 128, 0, st>>>(m, c, n, ncav, rs, regions, region_len, a.ckey, depth_cap, ring ? 1 : 0, d_ctr);
     const u32 g = (n + 255) / 256;
+    note_launch(), k_rw_claim<<<g, 256, 0, st>>>(m, c, n, a.fkey);
     note_launch(), k_cavity_tie<<<g, 256, 0, st>>>(c, n, rs, regions, region_len, a.ckey, a.ctie);
-    note_launch(), k_isolated_check<<<g, 256, 0, st>>>(m, c, n, rs, regions, region_len, a.ckey, a.ctie, unsafe_flag, d_ctr);
-    note_launch(), k_cavity_reset<<<g, 256, 0, st>>>(n, rs, regions, region_len, a.ckey, a.ctie);
+    note_launch(), k_rw_tie<<<g, 256, 0, st>>>(c, n, a.fkey, a.ftie);
+    note_launch(), k_isolated_check<<<g, 256, 0, st>>>(m, c, n, rs, regions, region_len, a.ckey, a.ctie, a.fkey, a.ftie, unsafe_flag, d_ctr);
+    note_launch(), k_cavity_reset<<<g, 256, 0, st>>>(c, n, m.nT, rs, regions, region_len, a.ckey, a.ctie, a.fkey, a.ftie);
 }
 
-void launch_cavity(const DevMesh& m, DevCands c, u32 n, u32 ncav, bool extras, TriAux a,
+void launch_cavity(const DevMesh& m, DevCands c, u32 n, u32 ncav, int extras, TriAux a,
                    u32* regions, u32* region_len, u32* bfs_len, Counters* d_ctr,
                    cudaStream_t st) {
     if (!n) return;
     const u32 rs = ncav + 1 + MAX_CLAIM_EXTRA;
-    note_launch(), k_cavity_bfs<<<(n + 127) / 128, 128, 0, st>>>(m, c, n, ncav, extras ? 1 : 0, rs, regions,
+    const bool rw = extras == 2;
+    note_launch(), k_cavity_bfs<<<(n + 127) / 128, 128, 0, st>>>(m, c, n, ncav, extras, rs, regions,
                                                    region_len, bfs_len, a.ckey, d_ctr);
     const u32 g = (n + 255) / 256;
+    if (rw) note_launch(), k_rw_claim<<<g, 256, 0, st>>>(m, c, n, a.fkey);
     note_launch(), k_cavity_tie<<<g, 256, 0, st>>>(c, n, rs, regions, region_len, a.ckey, a.ctie);
-    note_launch(), k_cavity_check<<<g, 256, 0, st>>>(c, n, rs, regions, region_len, a.ckey, a.ctie, d_ctr);
-    note_launch(), k_cavity_reset<<<g, 256, 0, st>>>(n, rs, regions, region_len, a.ckey, a.ctie);
+    if (rw) note_launch(), k_rw_tie<<<g, 256, 0, st>>>(c, n, a.fkey, a.ftie);
+    note_launch(), k_cavity_check<<<g, 256, 0, st>>>(c, n, rs, regions, region_len, a.ckey, a.ctie,
+                                                     rw ? a.fkey : nullptr, rw ? a.ftie : nullptr,
+                                                     d_ctr);
+    note_launch(), k_cavity_reset<<<g, 256, 0, st>>>(c, n, m.nT, rs, regions, region_len, a.ckey,
+                                                     a.ctie, rw ? a.fkey : nullptr,
+                                                     rw ? a.ftie : nullptr);
 }
 
 }  // namespace gdp2d

@@ -998,6 +998,7 @@ struct InsertArgs {
     int filter;           // 1: run Lines 5-7 in kernel 1 (tiny batches)
     int isolate;          // claims: 0 reference, 1 isolated (rollback only if state[8]), 2 precedence
     int dep_mis;          // dependent pairs: 1 = priority-MIS rule, 0 = any-higher-neighbour rule
+    int extras;           // refine cavity claims: 1 far side in the main claims, 2 rewrite table
     unsigned long long* trace;   // GDP2D_TRACE: (globaltimer << 8 | tag) per step, or null
     u32* trace_val;              // a work count per trace entry
     u32* trace_n;
@@ -1154,26 +1155,38 @@ __device__ void filter(const InsertArgs& a, const Exec& ex, u32 C) {
     ex.sync();
     trace(a, ex.leader(), TR_CLAIM);
     u32 marked = 0, unsafe = 0;
-    for (u32 i = ex.tid; i < C; i += ex.nthr)
+    const bool rw = a.isolate || a.extras == 2;
+    for (u32 i = ex.tid; i < C; i += ex.nthr) {
         visits += a.isolate
                       ? cavity_claims_one<MODE>(m, a.c, i, a.ncav, a.rs, a.regions, a.region_len,
                                                 a.x.ckey, a.depth_cap, a.isolate == 1)
-                      : cavity_bfs_one(m, a.c, i, a.ncav, 1, a.rs, a.regions, a.region_len,
+                      : cavity_bfs_one(m, a.c, i, a.ncav, a.extras, a.rs, a.regions, a.region_len,
                                        nullptr, a.x.ckey);
+        if (rw) rw_claim_one(m, a.c, i, a.x.fkey);
+    }
     ex.sync();
-    for (u32 i = ex.tid; i < C; i += ex.nthr)
+    for (u32 i = ex.tid; i < C; i += ex.nthr) {
         cavity_tie_one(a.c, i, a.rs, a.regions, a.region_len, a.x.ckey, a.x.ctie);
+        if (rw) rw_tie_one(a.c, i, a.x.fkey, a.x.ftie);
+    }
     ex.sync();
-    for (u32 i = ex.tid; i < C; i += ex.nthr)
+    for (u32 i = ex.tid; i < C; i += ex.nthr) {
+        if (rw && a.c.alive[i] && !rw_owns(a.c, i, a.x.fkey, a.x.ftie)) {
+            a.c.alive[i] = 0;
+            continue;
+        }
         surv2 += a.isolate ? isolated_check_one(m, a.c, i, a.rs, a.regions, a.region_len,
                                                 a.x.ckey, a.x.ctie, marked, unsafe)
                            : cavity_check_one(a.c, i, a.rs, a.regions, a.region_len, a.x.ckey,
                                               a.x.ctie);
+    }
     if (unsafe) atomicOr(&a.state[8], 1u);
     warp_add_u32(&a.ctr->marked, marked);
     ex.sync();
-    for (u32 i = ex.tid; i < C; i += ex.nthr)
+    for (u32 i = ex.tid; i < C; i += ex.nthr) {
         cavity_reset_one(i, a.rs, a.regions, a.region_len, a.x.ckey, a.x.ctie);
+        if (rw) rw_reset_one(a.c, i, m.nT, a.x.fkey, a.x.ftie);
+    }
     trace(a, ex.leader(), TR_CAVITY);
     warp_add_ull(&a.ctr->walk_steps, steps);
     warp_add_ull(&a.ctr->cavity_visits, visits);
@@ -1550,6 +1563,7 @@ void launch_insert_persistent(const InsertLaunch& L, int mode, int grid, int gri
     a.filter = L.filter;
     a.isolate = L.isolate;
     a.dep_mis = L.dep_mis;
+    a.extras = L.extras;
     a.trace = L.trace;
     a.trace_val = L.trace_val;
     a.trace_n = L.trace_n;
