@@ -896,7 +896,8 @@ void insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, u32 C, u32 ncav, u32
         L.x = x->aux;
         L.f = x->fresh;
         L.w = x->wl;
-        L.w.vdirty = x->fresh.dirty;          // fixup flags rewritten fresh stars
+        L.w.vdirty = x->fresh.dirty;          // fixup flags detection suspects
+        L.w.fresh_cc = x->fresh.cc;
         L.w.fresh_v0 = x->work.m.nV;          // fresh ids start here ...
         L.w.fresh_n = x->fresh.cap;           // ... and never exceed the buffer
         L.ring = x->ring;
@@ -1103,6 +1104,12 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
         CK(cudaEventRecord(x->ev[6], st));
         x->tr.mark("sync", st);
         x->tr.flush(bm.batch_index, st);
+        if (x->tr.on)
+            fprintf(stderr, "[trace] batch %u counters: C=%u surv=%u/%u mid=%u cc=%u red=%u dep=%u "
+                            "marked=%u flips=%llu rm=%u\n",
+                    bm.batch_index, C, x->h_ctr->surv_claim, x->h_ctr->surv_cavity,
+                    x->h_ctr->ins_mid, x->h_ctr->ins_cc, x->h_ctr->rm_red, x->h_ctr->rm_dep,
+                    x->h_ctr->marked, (unsigned long long)x->h_ctr->flips, x->h_ctr->rm_done);
         CK(cudaGetLastError());
         if (x->legacy_insert)
             check_dev_err(x);

@@ -130,6 +130,7 @@ struct WorkLists {
     // fresh-vertex dirty marking by fixup (persistent insertion kernel only):
     // a rewritten triangle flags its corners in [fresh_v0, fresh_v0 + fresh_n)
     uint8_t* vdirty = nullptr;
+    const uint8_t* fresh_cc = nullptr;   // FreshInfo::cc
     u32 fresh_v0 = 0, fresh_n = 0;
 };
 

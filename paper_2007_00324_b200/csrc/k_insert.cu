@@ -190,7 +190,7 @@ __device__ __forceinline__ int apply_one(const DevMesh& m, const DevCands& c, u3
     f.cc[fi] = c.kind[i] == 1;
     f.removed[fi] = 0;
     f.mark[fi] = 0;
-    f.dirty[fi] = 1;
+    f.dirty[fi] = 0;   // becomes a detection suspect through fixup_one
     const u32 t = c.loc[i];
     if (c.kind[i] == 0) {
         const u32 s = c.id[i];
@@ -276,12 +276,22 @@ __device__ __forceinline__ void fixup_one(const DevMesh& m, u32 round, const Tri
     atomicMin(&m.vtri[tv.x], t);
     atomicMin(&m.vtri[tv.y], t);
     atomicMin(&m.vtri[tv.z], t);
-    if (w.vdirty) {
-        if (tv.x - w.fresh_v0 < w.fresh_n) w.vdirty[tv.x - w.fresh_v0] = 1;
-        if (tv.y - w.fresh_v0 < w.fresh_n) w.vdirty[tv.y - w.fresh_v0] = 1;
-        if (tv.z - w.fresh_v0 < w.fresh_n) w.vdirty[tv.z - w.fresh_v0] = 1;
-    }
     const uint4 ts = m.ts[t];
+    if (w.vdirty) {
+        // Suspects for the redundancy detection (refine.hpp:551-608): a
+        // same-batch circumcenter can only be redundant as the apex of a
+        // subsegment, or dependent next to another same-batch circumcenter --
+        // both visible on one triangle, and every triangle around a fresh
+        // vertex passes through a fixup.  Only suspects are evaluated.
+        const u32 j0 = tv.x - w.fresh_v0, j1 = tv.y - w.fresh_v0, j2 = tv.z - w.fresh_v0;
+        const bool c0 = j0 < w.fresh_n && w.fresh_cc[j0];
+        const bool c1 = j1 < w.fresh_n && w.fresh_cc[j1];
+        const bool c2 = j2 < w.fresh_n && w.fresh_cc[j2];
+        const bool pair = (int)c0 + (int)c1 + (int)c2 >= 2;
+        if (c0 && (pair || ts.x != NONE)) w.vdirty[j0] = 1;
+        if (c1 && (pair || ts.y != NONE)) w.vdirty[j1] = 1;
+        if (c2 && (pair || ts.z != NONE)) w.vdirty[j2] = 1;
+    }
 #pragma unroll
     for (int e = 0; e < 3; ++e) {
         const u32 s = comp(ts, e);
@@ -1334,19 +1344,20 @@ __device__ void rollback_loop(const InsertArgs& a, const Exec& ex, u32 nv, u32 n
     u32 marked = 0, red = 0, dep = 0, done = 0;
     const u32 V0 = a.m.nV, F = nv;
     ex.sync();   // every thread has read state[1] before the leader rewrites it
-    // Detection passes.  Pass 0 evaluates every fresh vertex; later passes
-    // only those whose star was rewritten since (f.dirty, set by fixup_one):
-    // a clean star keeps its neighbours and subsegments, so its verdict
-    // cannot change (a neighbour turning redundant only removes a reason to
-    // be dependent, and redundant neighbours were removed, dirtying it).
-    // dirty: 1 = rewritten, 2 = evaluated in this pass, 0 = clean.
+    // Detection passes evaluate only suspects (f.dirty, set by fixup_one when
+    // a rewritten triangle makes a fresh circumcenter the apex of a
+    // subsegment or puts two of them on one triangle).  A vertex that is not
+    // re-suspected keeps its verdict: its star did not change in a way that
+    // could make it redundant or dependent (a neighbour turning redundant only
+    // removes a reason to be dependent, and removed neighbours rewrite it).
+    // dirty: 1 = suspect, 2 = evaluated in this pass, 0 = clean.
     RoundCtr* seed_rc = a.ring + 4;   // Lawson seeds of all removal rounds of a pass
     for (u32 pass = 0; step < a.max_steps; ++pass) {
         RoundCtr* rc = ring_at(a, step);
         ring_advance(a, ex, step);
         if (ex.leader()) seed_rc->wl_next = 0;   // visible after the barriers below
         for (u32 j = ex.tid; j < F; j += ex.nthr) {
-            if (pass > 0 && a.f.dirty[j] == 0) continue;
+            if (a.f.dirty[j] == 0) continue;   // not a suspect since the last pass
             a.f.dirty[j] = 2;
             marked += detect_a_one<MODE>(m, a.depth_cap, V0, j, a.f, a.ctr);
         }
