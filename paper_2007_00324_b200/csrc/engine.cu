@@ -320,6 +320,8 @@ struct gdp2d_ctx {
     int lawson_grid = 0;          // persistent Lawson kernel grid (co-resident blocks)
     int insert_grid = 0;          // persistent insertion kernel grid
     int rollback_grid = 0;        // persistent rollback kernel grid
+    int lawson_grid2 = 0;         // separate batch Lawson kernel grid
+    bool lawson_kernel = false;   // GDP2D_LAWSON_KERNEL=1: separate Lawson launch (measured slower)
     bool legacy_insert = false;   // GDP2D_INSERT=legacy: host-driven insertion rounds
     RoundCtr* ring = nullptr;     // [4] step counters of the persistent insertion kernel
     u32* ins_state = nullptr;     // [16] status words (see k_insert.cu; [8] = unsafe flag)
@@ -579,6 +581,8 @@ void ctx_init(gdp2d_ctx* x, int device) {
     x->lawson_grid = lawson_persistent_grid(device);
     x->insert_grid = insert_persistent_grid(device);
     x->rollback_grid = rollback_persistent_grid(device);
+    x->lawson_grid2 = lawson_batch_grid(device);
+    if (const char* e = std::getenv("GDP2D_LAWSON_KERNEL")) x->lawson_kernel = e[0] == '1';
     const char* li = std::getenv("GDP2D_INSERT");
     x->legacy_insert = (li && std::string(li) == "legacy") || x->validate || x->lawson_rounds;
     dalloc(x->ring, 5);   // 4-slot step ring + the removal-seed accumulator
@@ -918,6 +922,7 @@ void insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, u32 C, u32 ncav, u32
         L.isolate = isolate;
         L.dep_mis = x->dep_mis ? 1 : 0;
         L.extras = x->extras;
+        L.lawson_kernel = x->lawson_kernel ? 1 : 0;
         L.regions = x->regions;
         L.region_len = x->region_len;
         L.scan_part = x->scan_part;
@@ -934,16 +939,17 @@ void insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, u32 C, u32 ncav, u32
         x->tr.mark("pre_ins", st);
         CK(cudaMemsetAsync(x->ins_state, 0, 8 * sizeof(u32), st));   // word 8 = unsafe flag stays
         CK(cudaEventRecord(x->ev_k[0], st));
+        const int mode = p->mode == GDP2D_CHEW ? 1 : 0;
+        const int k1 = x->lawson_kernel ? (1 | 4) : 1;
         if (!x->check) {
-            launch_insert_persistent(L, p->mode == GDP2D_CHEW ? 1 : 0, x->insert_grid,
-                                     x->rollback_grid, st, x->ev_k[1]);
+            launch_insert_persistent(L, mode, x->insert_grid, x->rollback_grid, st, x->ev_k[1],
+                                     k1 | 2, x->lawson_grid2);
         } else {
             // GDP2D_CHECK=1: structural validation after each kernel
-            launch_insert_persistent(L, p->mode == GDP2D_CHEW ? 1 : 0, x->insert_grid,
-                                     x->rollback_grid, st, x->ev_k[1], 1);
+            launch_insert_persistent(L, mode, x->insert_grid, x->rollback_grid, st, x->ev_k[1],
+                                     k1, x->lawson_grid2);
             check_structure_now(x, x->work.m.nV, x->work.m.nT, x->work.m.nS, "split kernel");
-            launch_insert_persistent(L, p->mode == GDP2D_CHEW ? 1 : 0, x->insert_grid,
-                                     x->rollback_grid, st, nullptr, 2);
+            launch_insert_persistent(L, mode, x->insert_grid, x->rollback_grid, st, nullptr, 2);
             check_structure_now(x, x->work.m.nV, x->work.m.nT, x->work.m.nS, "rollback kernel");
         }
         CK(cudaEventRecord(x->ev_k[2], st));

@@ -185,6 +185,7 @@ struct InsertLaunch {
     int isolate = 1;            // claims: 0 reference cavity, 1 isolated (ring), 2 precedence
     int dep_mis = 0;            // dependent pairs by the priority-MIS rule
     int extras = 2;             // cavity extras mode (see launch_cavity)
+    int lawson_kernel = 1;      // separate Lawson launch after the splits
     unsigned long long* trace = nullptr;   // device step trace (GDP2D_TRACE=1)
     u32* trace_val = nullptr;
     u32* trace_n = nullptr;
@@ -194,9 +195,12 @@ int insert_persistent_grid(int device);
 int rollback_persistent_grid(int device);
 // Kernel 1 (plan + splits + Lawson, with Lines 5-7 when L.filter) then
 // kernel 2 (detect + rollback loop), both cooperative, no host sync between.
-// which: 1 = kernel 1 only, 2 = kernel 2 only, 3 = both back to back.
+// which: bit 0 = kernel 1 (splits [+ Lawson]), bit 2 = the separate Lawson
+// kernel, bit 1 = kernel 2 (rollback), launched in that order.
+int lawson_batch_grid(int device);
 void launch_insert_persistent(const InsertLaunch& L, int mode, int grid, int grid2,
-                              cudaStream_t st, cudaEvent_t between = nullptr, int which = 3);
+                              cudaStream_t st, cudaEvent_t between = nullptr, int which = 3,
+                              int grid3 = 0);
 
 // Redundancy detection (refine.hpp:551-608): fills w.rm[0], count in w.rc->detect.
 void launch_detect(const DevMesh& m, const Quality& q, u64 depth_cap, u32 V0, u32 F,

@@ -30,6 +30,9 @@ namespace cg = cooperative_groups;
 #ifndef GDP2D_SPLIT_MINB
 #define GDP2D_SPLIT_MINB 2
 #endif
+#ifndef GDP2D_LAWSON_MINB
+#define GDP2D_LAWSON_MINB 4
+#endif
 
 namespace gdp2d {
 
@@ -1009,6 +1012,7 @@ struct InsertArgs {
     int isolate;          // claims: 0 reference, 1 isolated (rollback only if state[8]), 2 precedence
     int dep_mis;          // dependent pairs: 1 = priority-MIS rule, 0 = any-higher-neighbour rule
     int extras;           // refine cavity claims: 1 far side in the main claims, 2 rewrite table
+    int lawson_kernel;    // 1: kernel 1 stops after the splits, k_batch_lawson flips
     unsigned long long* trace;   // GDP2D_TRACE: (globaltimer << 8 | tag) per step, or null
     u32* trace_val;              // a work count per trace entry
     u32* trace_n;
@@ -1312,6 +1316,19 @@ __device__ void split_and_flip(const InsertArgs& a, const Exec& ex, u32 nv, u32 
     }
     const u32 n = vload(&rc->wl_next);
     ++step;
+    if (a.lawson_kernel) {
+        // the Lawson fixpoint runs in its own lean launch (k_batch_lawson)
+        warp_add_u32(&a.ctr->ins_mid, mid);
+        warp_add_u32(&a.ctr->ins_cc, cc);
+        if (ex.leader()) {
+            a.state[0] = INS_OK;
+            a.state[1] = step;
+            a.state[2] = 0;
+            a.state[3] = 0;
+            a.state[9] = n;
+        }
+        return;
+    }
     lawson_fixpoint_dev(a, ex, m, step, cur, n, flipped, flip_rounds);
     warp_add_u32(&a.ctr->ins_mid, mid);
     warp_add_u32(&a.ctr->ins_cc, cc);
@@ -1511,6 +1528,40 @@ __global__ void __launch_bounds__(INSERT_BLOCK, GDP2D_SPLIT_MINB) k_batch_split(
     split_and_flip(a, ex, nv, nt, ns);
 }
 
+// Kernel 1b (a.lawson_kernel): the Lawson fixpoint after the splits in its
+// own launch, compiled for GDP2D_LAWSON_MINB CTAs per SM (the split kernel's
+// register budget would hold it at two).
+template <int MODE>
+__global__ void __launch_bounds__(INSERT_BLOCK, GDP2D_LAWSON_MINB) k_batch_lawson(InsertArgs a) {
+    if (vload(&a.state[0]) != INS_OK) return;
+    const u32 nv = vload(&a.b.totals[0]), nt = vload(&a.b.totals[1]), ns = vload(&a.b.totals[2]);
+    if (nv == 0) return;
+    const u32 C = vload(a.d_C);
+    const bool block = C <= a.small_c;
+    if (block && blockIdx.x != 0) return;
+    const Exec ex = block ? block_exec() : grid_exec();
+    DevMesh m = a.m;
+    m.nV += nv;
+    m.nT += nt;
+    m.nS += ns;
+    u32 step = vload(&a.state[1]), cur = 0, flip_rounds = 0;
+    const u32 n = vload(&a.state[9]);
+    ull flipped = 0;
+    ex.sync();   // every thread has read state[] before the leader rewrites it
+    lawson_fixpoint_dev(a, ex, m, step, cur, n, flipped, flip_rounds);
+    warp_add_ull(&a.ctr->flips, flipped);
+    {
+        u32 f32 = (u32)flipped;
+        f32 = __reduce_add_sync(0xFFFFFFFFu, f32);
+        if ((threadIdx.x & 31) == 0 && f32) atomicAdd(&a.state[7], f32);
+    }
+    if (ex.leader()) {
+        a.state[0] = step >= a.max_steps ? INS_STEPS : INS_OK;
+        a.state[1] = step;
+        a.state[2] = flip_rounds;
+    }
+}
+
 // Kernel 2: phase 3 rollback (skipped when kernel 1 asked for growth).
 template <int MODE>
 __global__ void __launch_bounds__(INSERT_BLOCK) k_batch_rollback(InsertArgs a) {
@@ -1538,12 +1589,15 @@ static int coop_grid(K0 k0, K1 k1, int device) {
 int insert_persistent_grid(int device) {
     return coop_grid(k_batch_split<0>, k_batch_split<1>, device);
 }
+int lawson_batch_grid(int device) {
+    return coop_grid(k_batch_lawson<0>, k_batch_lawson<1>, device);
+}
 int rollback_persistent_grid(int device) {
     return coop_grid(k_batch_rollback<0>, k_batch_rollback<1>, device);
 }
 
 void launch_insert_persistent(const InsertLaunch& L, int mode, int grid, int grid2, cudaStream_t st,
-                              cudaEvent_t between, int which) {
+                              cudaEvent_t between, int which, int grid3) {
     InsertArgs a;
     a.m = L.m;
     a.c = L.c;
@@ -1575,6 +1629,7 @@ void launch_insert_persistent(const InsertLaunch& L, int mode, int grid, int gri
     a.isolate = L.isolate;
     a.dep_mis = L.dep_mis;
     a.extras = L.extras;
+    a.lawson_kernel = L.lawson_kernel;
     a.trace = L.trace;
     a.trace_val = L.trace_val;
     a.trace_n = L.trace_n;
@@ -1584,6 +1639,11 @@ void launch_insert_persistent(const InsertLaunch& L, int mode, int grid, int gri
         note_launch();
         cudaLaunchCooperativeKernel(mode ? (void*)k_batch_split<1> : (void*)k_batch_split<0>,
                                     dim3(grid), dim3(INSERT_BLOCK), args, 0, st);
+    }
+    if (which & 4) {
+        note_launch();
+        cudaLaunchCooperativeKernel(mode ? (void*)k_batch_lawson<1> : (void*)k_batch_lawson<0>,
+                                    dim3(grid3), dim3(INSERT_BLOCK), args, 0, st);
     }
     if (between) cudaEventRecord(between, st);
     if (which & 2) {
