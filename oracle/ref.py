@@ -227,6 +227,11 @@ class RefMesh:
     def locate(self, cands):
         return self._inplace(ref_lib().ref_locate, cands)
 
+    def split_points(self, cands):
+        """compute_splitting_points (refine.hpp:267) on a candidate list."""
+        fb = C.c_uint32()
+        return self._inplace(ref_lib().ref_split_points, cands, C.byref(fb))
+
     def claim_filter(self, cands):
         return self._inplace(ref_lib().ref_claim, cands)
 

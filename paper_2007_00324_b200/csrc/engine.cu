@@ -321,6 +321,8 @@ struct gdp2d_ctx {
     int insert_grid = 0;          // persistent insertion kernel grid
     int rollback_grid = 0;        // persistent rollback kernel grid
     int lawson_grid2 = 0;         // separate batch Lawson kernel grid
+    void* sel_state = nullptr;    // batch_size_cap radix-select state
+    u32 little_cap = 0;           // Little's-law batch cap (resident cavity-filter candidates)
     bool lawson_kernel = false;   // GDP2D_LAWSON_KERNEL=1: separate Lawson launch (measured slower)
     bool legacy_insert = false;   // GDP2D_INSERT=legacy: host-driven insertion rounds
     RoundCtr* ring = nullptr;     // [4] step counters of the persistent insertion kernel
@@ -582,6 +584,8 @@ void ctx_init(gdp2d_ctx* x, int device) {
     x->insert_grid = insert_persistent_grid(device);
     x->rollback_grid = rollback_persistent_grid(device);
     x->lawson_grid2 = lawson_batch_grid(device);
+    CK(cudaMalloc(&x->sel_state, select_state_bytes()));
+    x->little_cap = cavity_resident_candidates(device);
     if (const char* e = std::getenv("GDP2D_LAWSON_KERNEL")) x->lawson_kernel = e[0] == '1';
     const char* li = std::getenv("GDP2D_INSERT");
     x->legacy_insert = (li && std::string(li) == "legacy") || x->validate || x->lawson_rounds;
@@ -640,6 +644,7 @@ void ctx_release(gdp2d_ctx* x) {
     dfree(x->ring);
     dfree(x->d_C);
     dfree(x->scan_part);
+    if (x->sel_state) cudaFree(x->sel_state);
     x->tr.release();
     dfree(x->ins_state);
     if (x->h_state) cudaFreeHost(x->h_state);
@@ -1053,6 +1058,12 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
             r->scan_bytes += scan_alg_bytes(scan_nT, scan_nS, x->h_ctr->scan_dirty);
             break;
         }
+        // Batch sizing (refine.hpp:252-261 + the Little's-law cap): keep the
+        // highest priorities; the list keeps its order, the rest is dead
+        u64 cap = p->batch_size_cap;
+        if (p->little_batch_sizing && (cap == 0 || x->little_cap < cap)) cap = x->little_cap;
+        const u32 attempted = (cap > 0 && C > cap) ? (u32)cap : C;
+        if (attempted < C) launch_select_topk(x->c, C, attempted, x->sel_state, st);
         CK(cudaEventRecord(x->ev[1], st));   // split points are fused into collect
         CK(cudaEventRecord(x->ev[2], st));
         // isolated insertion needs the cavity filter (rule 2)
@@ -1131,7 +1142,7 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
         x->alive_t -= std::min<ull>(x->alive_t, 2ull * h.rm_done);
         x->alive_s += h.ins_mid;
         // metrics (record_batch, ruleskit.hpp:128-142)
-        bm.attempted = C;
+        bm.attempted = attempted;
         bm.concurrency = retained;
         bm.phase_seconds[GDP2D_PH_COLLECT] = ev_ms(x->ev[0], x->ev[1]) * 1e-3;
         bm.phase_seconds[GDP2D_PH_SPLIT_POINTS] = ev_ms(x->ev[1], x->ev[2]) * 1e-3;
@@ -1141,7 +1152,7 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
         bm.phase_seconds[GDP2D_PH_INSERT] = ev_ms(x->ev[5], x->ev[6]) * 1e-3;
         for (double s : bm.phase_seconds) bm.latency += s;
         bm.throughput = bm.latency > 0 ? retained / bm.latency : 0.0;
-        bm.waste_fraction = C ? double(C - retained) / C : 0.0;
+        bm.waste_fraction = attempted ? double(attempted - retained) / attempted : 0.0;
         bm.walk_steps = h.walk_steps;
         bm.cavity_visits = h.cavity_visits;
         bm.survivors_claim = h.surv_claim;
@@ -1158,7 +1169,7 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
         bm.removals_kept = h.rm_kept;
         if (r->batches && r->n_batches < r->batches_capacity) r->batches[r->n_batches] = bm;
         r->n_batches++;
-        r->total_candidates += C;
+        r->total_candidates += attempted;
         r->total_walk_steps += h.walk_steps;
         r->total_cavity_visits += h.cavity_visits;
         r->total_inserted += inserted;
@@ -1489,27 +1500,45 @@ int gdp2d_collect(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_candidate* out, uin
         CollectCache cache;
         cache.full = 1;
         bool tris_scanned = false;
-        const u32 C = launch_collect(m, make_quality(p), p->rule4_unified_collection != 0,
-                                     x->flags, x->c, x->ccap, x->scan, x->d_ctr, x->st, cache,
-                                     &tris_scanned, x->d_C);
+        u32 C = launch_collect(m, make_quality(p), p->rule4_unified_collection != 0,
+                               x->flags, x->c, x->ccap, x->scan, x->d_ctr, x->st, cache,
+                               &tris_scanned, x->d_C);
+        std::vector<gdp2d_candidate> tmp(C);
+        if (C) {
+            // batch_size_cap (refine.hpp:252-261): the kept candidates in list
+            // order, with their original tiebreaks
+            const bool capped = p->batch_size_cap > 0 && C > p->batch_size_cap;
+            if (capped) launch_select_topk(x->c, C, (u32)p->batch_size_cap, x->sel_state, x->st);
+            download_cands(x, tmp.data(), C);
+            if (capped) {
+                u32 k = 0;
+                for (u32 i = 0; i < C; ++i)
+                    if (tmp[i].alive) tmp[k++] = tmp[i];
+                tmp.resize(k);
+                C = k;
+            }
+        }
         *n = C;
         if (C > cap) {
             status = GDP2D_ECAPACITY;
             g_err = "candidate buffer too small";
         }
-        if (out && C) {
-            std::vector<gdp2d_candidate> tmp(C);
-            download_cands(x, tmp.data(), C);
-            std::memcpy(out, tmp.data(), sizeof(gdp2d_candidate) * std::min(C, cap));
-        }
+        if (out && C) std::memcpy(out, tmp.data(), sizeof(gdp2d_candidate) * std::min(C, cap));
     });
     return rc ? rc : status;
 }
 
 int gdp2d_split_points(gdp2d_ctx* x, gdp2d_candidate* c, uint32_t n) {
-    (void)x; (void)c; (void)n;
-    g_err = "split points are fused into gdp2d_collect";
-    return GDP2D_EINVAL;
+    if (!x || (!c && n)) return GDP2D_EINVAL;
+    DeviceGuard g(x->device);
+    return run_guarded([&] {
+        if (!n) return;
+        upload_cands(x, c, n);
+        CK(cudaMemsetAsync(x->d_ctr, 0, sizeof(Counters), x->st));
+        launch_split_points(x->work.m, x->c, n, x->d_ctr, x->st);
+        CK(cudaGetLastError());
+        download_cands(x, c, n);
+    });
 }
 
 int gdp2d_locate(gdp2d_ctx* x, gdp2d_candidate* c, uint32_t n) {

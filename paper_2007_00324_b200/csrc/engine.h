@@ -67,6 +67,11 @@ u32 launch_collect(const DevMesh& m, const Quality& q, bool rule4, uint8_t* flag
                    cudaEvent_t ev_scan0 = nullptr,
                    cudaEvent_t ev_scan1 = nullptr);
 void launch_split_points(const DevMesh& m, DevCands c, u32 n, Counters* d_ctr, cudaStream_t st);
+// batch_size_cap (refine.hpp:252-261): keep the k highest-priority alive
+// candidates of the list (others marked dead), device-side radix select.
+size_t select_state_bytes();
+u32 cavity_resident_candidates(int device);
+void launch_select_topk(DevCands c, u32 n, u32 k, void* state, cudaStream_t st);
 void launch_locate(const DevMesh& m, DevCands c, u32 n, Counters* d_ctr, cudaStream_t st);
 void launch_claim(const DevMesh& m, DevCands c, u32 n, TriAux a, Counters* d_ctr,
                   cudaStream_t st);

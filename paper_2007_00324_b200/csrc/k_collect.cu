@@ -7,6 +7,8 @@
 // order is the reference's (subsegments by id, then triangles by id) thanks to
 // a stable three-kernel compaction (flag+tile count, tile-sum scan, tile-local
 // shuffle scan + scatter).  Tiebreak = list index (refine.hpp:236,248).
+#include <algorithm>
+
 #include "engine.h"
 #include "scan.cuh"
 
@@ -189,6 +191,115 @@ u32 launch_collect(const DevMesh& m, const Quality& q, bool rule4, uint8_t* flag
     const u32 ns = run(true, false);
     if (ns > 0) return ns;
     return run(false, true);
+}
+
+// ---- batch_size_cap: keep the k highest priorities (refine.hpp:252-261) -------------
+//
+// The reference sorts the list by priority, keeps the first k and restores
+// list order.  Here the list stays in place and the others are marked dead:
+// an MSD radix select (8-bit digits, 12 passes) finds the k-th largest
+// 96-bit rank (key, ~tiebreak) -- unique, since the tiebreak is the list
+// index -- and a last pass keeps every candidate whose rank is at least it.
+// No host round trip: the selection state lives in device memory.
+
+struct SelState {
+    unsigned long long key;   // prefix of the k-th largest rank: key part
+    u32 tie;                  // ... and ~tiebreak part
+    u32 k;                    // rank still to find inside the current bucket
+    u32 hist[256];
+};
+
+__device__ __forceinline__ u32 sel_digit(u64 key, u32 ntie, int d) {
+    return d < 8 ? (u32)(key >> (56 - 8 * d)) & 0xFFu : (ntie >> (24 - 8 * (d - 8))) & 0xFFu;
+}
+
+// true if (key, ntie) matches the selected prefix on the digits before d
+__device__ __forceinline__ bool sel_match(u64 key, u32 ntie, const SelState& s, int d) {
+    if (d == 0) return true;
+    if (d <= 8) {
+        const u64 mask = ~0ull << (64 - 8 * d);
+        return (key & mask) == (s.key & mask);
+    }
+    if (key != s.key) return false;
+    const u32 mask = ~0u << (32 - 8 * (d - 8));
+    return (ntie & mask) == (s.tie & mask);
+}
+
+__global__ void __launch_bounds__(256) k_sel_hist(DevCands c, u32 n, SelState* st, int d) {
+    __shared__ u32 h[256];
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    const SelState s = *st;
+    for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        if (!c.alive[i]) continue;
+        const u64 key = c.key[i];
+        const u32 ntie = ~c.tie[i];
+        if (!sel_match(key, ntie, s, d)) continue;
+        atomicAdd(&h[sel_digit(key, ntie, d)], 1u);
+    }
+    __syncthreads();
+    if (h[threadIdx.x]) atomicAdd(&st->hist[threadIdx.x], h[threadIdx.x]);
+}
+
+// one thread: pick the bucket holding the k-th largest, extend the prefix
+__global__ void k_sel_pick(SelState* st, int d) {
+    u32 k = st->k, above = 0;
+    int b = 255;
+    for (; b > 0; --b) {
+        const u32 cnt = st->hist[b];
+        if (above + cnt >= k) break;
+        above += cnt;
+    }
+    st->k = k - above;
+    if (d < 8)
+        st->key |= (unsigned long long)b << (56 - 8 * d);
+    else
+        st->tie |= (u32)b << (24 - 8 * (d - 8));
+    for (int i = 0; i < 256; ++i) st->hist[i] = 0;
+}
+
+__global__ void k_sel_apply(DevCands c, u32 n, const SelState* st) {
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n || !c.alive[i]) return;
+    const u64 key = c.key[i];
+    const u32 ntie = ~c.tie[i];
+    const bool keep = key > st->key || (key == st->key && ntie >= st->tie);
+    if (!keep) c.alive[i] = 0;
+}
+
+size_t select_state_bytes() { return sizeof(SelState); }
+
+void launch_select_topk(DevCands c, u32 n, u32 k, void* state, cudaStream_t st) {
+    if (k == 0 || k >= n) return;
+    SelState init{};
+    init.k = k;
+    SelState* s = reinterpret_cast<SelState*>(state);
+    cudaMemcpyAsync(s, &init, sizeof init, cudaMemcpyHostToDevice, st);
+    const u32 grid = std::min<u32>((n + 255) / 256, 148 * 8);
+    for (int d = 0; d < 12; ++d) {
+        note_launch(), k_sel_hist<<<grid, 256, 0, st>>>(c, n, s, d);
+        note_launch(), k_sel_pick<<<1, 1, 0, st>>>(s, d);
+    }
+    note_launch(), k_sel_apply<<<(n + 255) / 256, 256, 0, st>>>(c, n, s);
+}
+
+// compute_splitting_points on a caller list (refine.hpp:267-296): the gdp2d_split_points
+// parity entry point; the refinement fuses it into k_collect_scatter.
+__global__ void k_split_points(DevMesh m, DevCands c, u32 n, Counters* ctr) {
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    u32 fb_count = 0;
+    if (i < n) {
+        uint8_t fb;
+        c.pt[i] = split_point(m, c.kind[i], c.id[i], fb);
+        c.fb[i] = fb;
+        fb_count = fb;
+    }
+    warp_add_u32(&ctr->fallbacks, fb_count);
+}
+
+void launch_split_points(const DevMesh& m, DevCands c, u32 n, Counters* d_ctr, cudaStream_t st) {
+    if (!n) return;
+    note_launch(), k_split_points<<<(n + 255) / 256, 256, 0, st>>>(m, c, n, d_ctr);
 }
 
 }  // namespace gdp2d

@@ -4,6 +4,8 @@
 // (cavity_filter, refine.hpp:382-429 -> expand, expandlist.hpp:93-157).  The
 // per-candidate bodies live in gdp2d_phases.cuh and are the ones the
 // persistent batch kernel runs.
+#include <algorithm>
+
 #include "gdp2d_phases.cuh"
 #include "scan.cuh"
 
@@ -169,6 +171,17 @@ void launch_cavity(const DevMesh& m, DevCands c, u32 n, u32 ncav, int extras, Tr
     note_launch(), k_cavity_reset<<<g, 256, 0, st>>>(c, n, m.nT, rs, regions, region_len, a.ckey,
                                                      a.ctie, rw ? a.fkey : nullptr,
                                                      rw ? a.ftie : nullptr);
+}
+
+// Little's law against measured occupancy: the number of candidates the
+// cavity filter (the heaviest per-candidate kernel) keeps in flight at once
+// on this device -- SMs x resident CTAs x threads.  A batch larger than this
+// only queues (latency grows linearly) while its waste (conflicts) grows.
+u32 cavity_resident_candidates(int device) {
+    int sms = 0, per_sm = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cavity_bfs, 128, 0);
+    return (u32)std::max(1, sms * std::max(1, per_sm) * 128);
 }
 
 }  // namespace gdp2d

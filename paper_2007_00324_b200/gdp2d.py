@@ -483,6 +483,12 @@ class Engine:
             _raise(rc, "gdp2d_collect")
             return out[: n.value].copy()
 
+    def split_points(self, cands: np.ndarray) -> np.ndarray:
+        """compute_splitting_points (refine.hpp:267-296) on a caller list."""
+        c = np.ascontiguousarray(cands, dtype=A.candidate_dtype()).copy()
+        _raise(self.lib.gdp2d_split_points(self.ctx, c.ctypes.data, len(c)), "gdp2d_split_points")
+        return c
+
     def locate(self, cands: np.ndarray) -> np.ndarray:
         c = np.ascontiguousarray(cands, dtype=A.candidate_dtype()).copy()
         _raise(self.lib.gdp2d_locate(self.ctx, c.ctypes.data, len(c)), "gdp2d_locate")

@@ -118,3 +118,40 @@ def test_flip_fixpoint_matches_reference(meshes):
         assert flips > 0
         assert a.shape == b.shape and np.array_equal(a, b), name
         RefMesh.from_mesh(out).check_structure()
+
+
+def test_split_points_bit_exact(meshes):
+    """gdp2d_split_points == compute_splitting_points (refine.hpp:267-296) on the
+    reference's own candidate list with the points wiped."""
+    from paper_2007_00324_b200 import Engine, QualityCriteria
+    from oracle.ref import RefMesh
+    q = QualityCriteria(theta=B_SQRT2_THETA)
+    with Engine() as eng:
+        for name, (m, _) in meshes.items():
+            rm = RefMesh.from_mesh(m)
+            eng.upload(m)
+            c = rm.collect(q)
+            c["x"] = 0.0
+            c["y"] = 0.0
+            _same(eng.split_points(c), rm.split_points(c), f"{name} split points")
+
+
+@pytest.mark.parametrize("cap_frac", [0.0, 0.01, 0.33, 0.999])
+def test_batch_size_cap_bit_exact(meshes, cap_frac):
+    """batch_size_cap keeps the highest priorities in list order with the
+    original tiebreaks (refine.hpp:252-261); device radix select vs the
+    reference's sort."""
+    from paper_2007_00324_b200 import Engine, EngineConfig, QualityCriteria
+    from oracle.ref import RefMesh
+    q = QualityCriteria(theta=B_SQRT2_THETA)
+    with Engine() as eng:
+        for name, (m, _) in meshes.items():
+            rm = RefMesh.from_mesh(m)
+            eng.upload(m)
+            full = rm.collect(q)
+            cap = max(1, int(len(full) * cap_frac))
+            cfg = EngineConfig(batch_size_cap=cap)
+            g = eng.collect(q, cfg)
+            r = rm.collect(q, cfg)
+            assert len(r) == min(cap, len(full))
+            _same(g, r, f"{name} collect cap={cap}")

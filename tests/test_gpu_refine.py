@@ -192,3 +192,17 @@ def test_block_and_grid_modes_agree(built, monkeypatch, small_c):
         other = eng.download()
     assert np.array_equal(base.tri_v, other.tri_v)
     assert np.array_equal(base.xy, other.xy)
+
+
+@pytest.mark.parametrize("cfgkw", [dict(batch_size_cap=500), dict(little_batch_sizing=True)])
+def test_batch_sizing(built, cfgkw):
+    """Capped batches (refine.hpp:252-261) and the Little's-law cap refine to
+    quality with every batch at most the cap."""
+    from paper_2007_00324_b200 import EngineConfig, QualityCriteria, host
+    q = QualityCriteria(B_SQRT2_THETA)
+    pts, segs = host.generate_pslg(20_000, 2_000, "uniform", 21)
+    out, closed, rep, rref = _run(pts, segs, q, EngineConfig(**cfgkw))
+    check_invariants(out, pts, closed, q, cdt_check=True)
+    if "batch_size_cap" in cfgkw:
+        assert max(b.attempted for b in rep.batches) <= cfgkw["batch_size_cap"]
+    assert abs(rep.steiner_points - rref.steiner_points) <= 0.10 * rref.steiner_points
