@@ -117,7 +117,10 @@ __device__ void split_edge_A(const DevMesh& m, const TriAux& x, const WorkLists&
         m.vtri[wv] = NONE;
         const u32 tl[2] = {t, t2};
         push_touched(w, tl, 2, rc);
-        if (seed) {
+        if (seed && s_bw != NONE) {
+            const u32 codes[2] = {enc(t, 2), enc(t2, 1)};
+            push_work(w, 0, codes, 2, ctr, rc);
+        } else if (seed) {
             const u32 codes[6] = {enc(t, 0), enc(t, 1), enc(t, 2), enc(t2, 0), enc(t2, 1),
                                   enc(t2, 2)};
             push_work(w, 0, codes, 6, ctr, rc);
@@ -148,7 +151,13 @@ __device__ void split_edge_A(const DevMesh& m, const TriAux& x, const WorkLists&
     m.vtri[wv] = NONE;
     const u32 tl[4] = {t, t2, u, u2};
     push_touched(w, tl, 4, rc);
-    if (seed) {
+    if (seed && s_bw != NONE) {
+        // subsegment midpoint: the halves are constrained and the spokes
+        // (w,a), (w,d) are constrained-Delaunay (a circle through a and w
+        // inside the empty circumcircle of (a,b,c)); only the link edges
+        const u32 codes[4] = {enc(t, 2), enc(t2, 1), enc(u, 2), enc(u2, 1)};
+        push_work(w, 0, codes, 4, ctr, rc);
+    } else if (seed) {
         const u32 codes[12] = {enc(t, 0), enc(t, 1), enc(t, 2), enc(t2, 0), enc(t2, 1),
                                enc(t2, 2), enc(u, 0), enc(u, 1), enc(u, 2), enc(u2, 0),
                                enc(u2, 1), enc(u2, 2)};
