@@ -25,6 +25,35 @@ struct CollectRange {
 // scan reads one byte instead of the 64 B record + corner gathers.  The
 // candidate list is bit-identical to a full scan (same flags, same stable
 // compaction); only the sticky encroached flag is read for every subsegment.
+// Each thread owns SCAN_ITEMS (= 8) consecutive elements: one 8-byte load of
+// the cached verdicts, one 8-byte store of the flags.  Order inside a tile is
+// element order, so the scatter needs a single block scan per tile.
+template <int MODE>
+__device__ __forceinline__ uint8_t eval_sub(const DevMesh& m, u32 i, int full, u32& dirty) {
+    if (!m.salive[i]) return 0;
+    const uint8_t sf = full ? 2 : m.sflag[i];
+    bool enc;
+    if (sf & 2) {
+        enc = is_encroached<MODE>(m, i);
+        m.sflag[i] = enc ? 1 : 0;
+        ++dirty;
+    } else {
+        enc = sf & 1;
+    }
+    return (m.senc[i] || enc) ? 1 : 0;
+}
+
+__device__ __forceinline__ uint8_t eval_tri(const DevMesh& m, const Quality& q, u32 i) {
+    uint8_t f = 0;
+    const uint4 tv = m.tv[i];
+    if (tv.w) {
+        const double2 a = m.xy[tv.x], b = m.xy[tv.y], c = m.xy[tv.z];
+        if (is_bad_pts(a, b, c, q) && resolvable_pts(a, b, c)) f = 1;
+    }
+    m.tflag[i] = f;
+    return f;
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(SCAN_BLOCK) k_collect_flags(DevMesh m, Quality q, CollectRange r,
                                                            uint8_t* __restrict__ flags,
@@ -34,44 +63,47 @@ __global__ void __launch_bounds__(SCAN_BLOCK) k_collect_flags(DevMesh m, Quality
     const bool is_sub = blockIdx.x < r.tilesS;
     const u32 tile = is_sub ? blockIdx.x : blockIdx.x - r.tilesS;
     const u32 n = is_sub ? r.nS : r.nT;
-    const u32 base = tile * (u32)SCAN_TILE;
+    const u32 i0 = tile * (u32)SCAN_TILE + threadIdx.x * (u32)SCAN_ITEMS;
     u32 cnt = 0, dirty = 0;
-#pragma unroll 4
-    for (int k = 0; k < SCAN_ITEMS; ++k) {
-        const u32 i = base + (u32)k * SCAN_BLOCK + threadIdx.x;
-        uint8_t f = 0;
-        if (i < n) {
-            if (is_sub) {
-                if (m.salive[i]) {
-                    const uint8_t sf = full ? 2 : m.sflag[i];
-                    bool enc;
-                    if (sf & 2) {
-                        enc = is_encroached<MODE>(m, i);
-                        m.sflag[i] = enc ? 1 : 0;
-                        ++dirty;
-                    } else {
-                        enc = sf & 1;
-                    }
-                    f = (m.senc[i] || enc) ? 1 : 0;
+    unsigned long long out = 0;
+    if (!is_sub && !full && i0 + SCAN_ITEMS <= n) {
+        // common case: eight cached verdicts in one load; dirty ones re-evaluated
+        unsigned long long v = *reinterpret_cast<const unsigned long long*>(m.tflag + i0);
+        if (v & 0x0202020202020202ull) {
+#pragma unroll
+            for (int j = 0; j < SCAN_ITEMS; ++j) {
+                const uint8_t tf = (uint8_t)(v >> (8 * j));
+                if (tf & 2) {
+                    const uint8_t f = eval_tri(m, q, i0 + j);
+                    ++dirty;
+                    v = (v & ~(0xFFull << (8 * j))) | ((unsigned long long)f << (8 * j));
                 }
+            }
+        }
+        out = v & 0x0101010101010101ull;
+    } else {
+#pragma unroll 2
+        for (int j = 0; j < SCAN_ITEMS; ++j) {
+            const u32 i = i0 + j;
+            if (i >= n) break;
+            uint8_t f;
+            if (is_sub) {
+                f = eval_sub<MODE>(m, i, full, dirty);
             } else {
                 const uint8_t tf = full ? 2 : m.tflag[i];
                 if (tf & 2) {
-                    const uint4 tv = m.tv[i];
-                    if (tv.w) {
-                        const double2 a = m.xy[tv.x], b = m.xy[tv.y], c = m.xy[tv.z];
-                        if (is_bad_pts(a, b, c, q) && resolvable_pts(a, b, c)) f = 1;
-                    }
-                    m.tflag[i] = f;
+                    f = eval_tri(m, q, i);
                     ++dirty;
                 } else {
                     f = tf & 1;
                 }
             }
+            out |= (unsigned long long)f << (8 * j);
         }
-        flags[(size_t)blockIdx.x * SCAN_TILE + (u32)k * SCAN_BLOCK + threadIdx.x] = f;
-        cnt += f;
     }
+    *reinterpret_cast<unsigned long long*>(flags + (size_t)blockIdx.x * SCAN_TILE +
+                                           threadIdx.x * SCAN_ITEMS) = out;
+    cnt = __popcll(out);
     // one reduction for both: count and dirty are <= SCAN_TILE < 2^16
     const u32 t = block_sum<SCAN_BLOCK>(cnt | (dirty << 16), sh);
     if (threadIdx.x == 0) {
@@ -111,42 +143,41 @@ __global__ void __launch_bounds__(SCAN_BLOCK) k_collect_scatter(DevMesh m, Colle
     __shared__ u32 sh[SCAN_BLOCK / 32 + 1];
     const bool is_sub = blockIdx.x < r.tilesS;
     const u32 tile = is_sub ? blockIdx.x : blockIdx.x - r.tilesS;
-    const u32 base = tile * (u32)SCAN_TILE;
-    u32 carry = partial[blockIdx.x];
+    const u32 carry = partial[blockIdx.x];
     const u32 end = blockIdx.x + 1 < r.tilesS + r.tilesT ? partial[blockIdx.x + 1] : *d_total;
     if (end == carry) return;   // no candidate in this tile (the common case in the tail)
+    const u32 i0 = tile * (u32)SCAN_TILE + threadIdx.x * (u32)SCAN_ITEMS;
+    const unsigned long long f8 = *reinterpret_cast<const unsigned long long*>(
+        flags + (size_t)blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_ITEMS);
+    u32 tot;
+    u32 o = carry + block_exclusive<SCAN_BLOCK>((u32)__popcll(f8), sh, &tot);
     u32 nfb = 0;
-    for (int k = 0; k < SCAN_ITEMS; ++k) {
-        const u32 i = base + (u32)k * SCAN_BLOCK + threadIdx.x;
-        const uint8_t f = flags[(size_t)blockIdx.x * SCAN_TILE + (u32)k * SCAN_BLOCK + threadIdx.x];
-        u32 tot;
-        const u32 ex = block_exclusive<SCAN_BLOCK>(f, sh, &tot);
-        if (f) {
-            const u32 o = carry + ex;
-            if (o < ccap) {
-                uint8_t fb;
-                const int kind = is_sub ? 0 : 1;
-                c.pt[o] = split_point(m, kind, i, fb);
-                nfb += fb;
-                double measure;
-                if (is_sub) {
-                    measure = subseg_len(m, i);
-                } else {
-                    const uint4 tv = m.tv[i];
-                    measure = area_pts(m.xy[tv.x], m.xy[tv.y], m.xy[tv.z]);
-                }
-                c.key[o] = make_key(is_sub ? 1 : 0, measure);
-                c.id[o] = i;
-                c.tie[o] = o;
-                c.loc[o] = PENDING;
-                c.kind[o] = (uint8_t)kind;
-                c.alive[o] = 1;
-                c.lkind[o] = 0;
-                c.ledge[o] = -1;
-                c.fb[o] = fb;
+    const int kind = is_sub ? 0 : 1;
+    for (int j = 0; j < SCAN_ITEMS; ++j) {
+        if (!((f8 >> (8 * j)) & 1ull)) continue;
+        const u32 i = i0 + j;
+        if (o < ccap) {
+            uint8_t fb;
+            c.pt[o] = split_point(m, kind, i, fb);
+            nfb += fb;
+            double measure;
+            if (is_sub) {
+                measure = subseg_len(m, i);
+            } else {
+                const uint4 tv = m.tv[i];
+                measure = area_pts(m.xy[tv.x], m.xy[tv.y], m.xy[tv.z]);
             }
+            c.key[o] = make_key(is_sub ? 1 : 0, measure);
+            c.id[o] = i;
+            c.tie[o] = o;
+            c.loc[o] = PENDING;
+            c.kind[o] = (uint8_t)kind;
+            c.alive[o] = 1;
+            c.lkind[o] = 0;
+            c.ledge[o] = -1;
+            c.fb[o] = fb;
         }
-        carry += tot;
+        ++o;
     }
     warp_add_u32(&ctr->fallbacks, nfb);
 }
