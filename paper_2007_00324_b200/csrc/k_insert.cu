@@ -821,19 +821,33 @@ __device__ __noinline__ u32 rm_apply_one(const DevMesh& m, const u32* __restrict
             while (cnt > 3 && ok) {
                 int j = head;
                 bool found = false;
+                // Pass -1: a strict ear whose circumcircle holds no other
+                // vertex of the remaining link polygon -- an edge of the
+                // polygon's Delaunay triangulation.  Clipping only such ears
+                // rebuilds the hole exactly as remove_free_vertex + Lawson on
+                // the ring would (refine.hpp:442-456: the CDT around a removed
+                // vertex is the polygon's), so the Lawson pass after the
+                // removal round finds nothing left to flip.
                 // Pass 0: a strict ear = one valid flip of remove_free_vertex.
                 // Pass 1 (degenerate stars only, e.g. a point that was inserted
                 // exactly on an edge): v may lie ON the new diagonal -- the
                 // final hole triangulation is still valid because v leaves.
-                for (int pass = 0; pass < 2 && !found; ++pass) {
+                for (int pass = -1; pass < 2 && !found; ++pass) {
                     j = head;
                     for (int it = 0; it < cnt; ++it) {
                         const int a = PV[j], c = NX[j];
                         const double2 pa = m.xy[L[a]], pj = m.xy[L[j]], pc = m.xy[L[c]];
                         const int side = orient2d(pa, pc, pv);
                         if (orient2d(pa, pj, pc) > 0 && (side > 0 || (pass == 1 && side == 0))) {
-                            found = true;
-                            break;
+                            bool delaunay = true;
+                            if (pass < 0) {
+                                for (int q = NX[c]; q != a && delaunay; q = NX[q])
+                                    delaunay = incircle(pa, pj, pc, m.xy[L[q]]) <= 0;
+                            }
+                            if (delaunay) {
+                                found = true;
+                                break;
+                            }
                         }
                         j = NX[j];
                     }
