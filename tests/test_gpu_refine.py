@@ -206,3 +206,77 @@ def test_batch_sizing(built, cfgkw):
     if "batch_size_cap" in cfgkw:
         assert max(b.attempted for b in rep.batches) <= cfgkw["batch_size_cap"]
     assert abs(rep.steiner_points - rref.steiner_points) <= 0.10 * rref.steiner_points
+
+
+def test_edge_length_bound(built):
+    """test_refine.cpp:392-401: quality + ell bound on every triangle."""
+    from paper_2007_00324_b200 import QualityCriteria
+    pts, segs = unit_square()
+    q = QualityCriteria(20.0, 0.2)
+    out, closed, rep, _ = _run(pts, segs, q)
+    assert rep.bad_triangles == 0 and rep.max_edge <= 0.2
+    check_invariants(out, pts, closed, q)
+
+
+def test_small_input_angle_stays_local(built):
+    """test_refine.cpp:403-425: a 10-degree wedge; any triangle left bad hugs the
+    small-angle apex, and the mesh is a conforming CDT."""
+    from paper_2007_00324_b200 import QualityCriteria
+    from oracle.ref import RefMesh
+    r = math.radians(10.0)
+    pts = np.array([[0, 0], [4, 0], [4 * math.cos(r), 4 * math.sin(r)], [4, 4], [0, 4]], float)
+    segs = np.array([[0, 1], [0, 2], [1, 3], [3, 4], [4, 0]], np.uint32)
+    q = QualityCriteria(20.0, 1e9)
+    out, closed, rep, _ = _run(pts, segs, q)
+    rm = RefMesh.from_mesh(out)
+    rm.check_structure()
+    assert rm.conformity_ok(pts, closed)
+    assert rm.cdt_violations() == 0
+    # bad triangles (if any) near the apex only
+    alive = out.tri_alive.astype(bool)
+    t = out.tri_v[alive]
+    xy = out.xy
+    a, b, c = xy[t[:, 0]], xy[t[:, 1]], xy[t[:, 2]]
+
+    def ang(p, u, v):
+        e1, e2 = u - p, v - p
+        return np.degrees(np.arctan2(np.abs(e1[:, 0] * e2[:, 1] - e1[:, 1] * e2[:, 0]),
+                                     (e1 * e2).sum(1)))
+    mins = np.minimum(np.minimum(ang(a, b, c), ang(b, c, a)), ang(c, a, b))
+    bad = mins < 20.0 - 1e-9
+    if bad.any():
+        far = np.linalg.norm(np.concatenate([a[bad], b[bad], c[bad]]), axis=1)
+        assert far.max() < 0.1
+
+
+def test_iteration_cap_and_batch_prefixes(built):
+    """refine.hpp:659-662 (iteration_cap_hit) and acceptance C3: after every
+    batch prefix the mesh is a valid conforming CDT."""
+    from paper_2007_00324_b200 import EngineConfig, QualityCriteria, host
+    from oracle.ref import RefMesh
+    pts, segs = host.generate_pslg(5_000, 500, "uniform", 31)
+    q = QualityCriteria(B_SQRT2_THETA)
+    for k in (0, 1, 2, 5):
+        out, closed, rep, _ = _run(pts, segs, q, EngineConfig(iteration_cap=k))
+        assert rep.iteration_cap_hit and len(rep.batches) == k
+        rm = RefMesh.from_mesh(out)
+        rm.check_structure()
+        assert rm.euler_holds() and rm.conformity_ok(pts, closed)
+        assert rm.cdt_violations() == 0
+
+
+def test_quality_report_fractions(built):
+    """test_refine.cpp:454-489 analogues through the GPU quality summary
+    (refine.hpp:614-645), reached with iteration_cap = 0."""
+    from paper_2007_00324_b200 import EngineConfig, QualityCriteria, host, refine
+    s = math.sqrt(3.0) / 2.0
+    m, _ = host.build_cdt(np.array([[0, 0], [1, 0], [0.5, s]], float),
+                          np.array([[0, 1], [1, 2], [2, 0]], np.uint32))
+    rep = refine(m.copy(), QualityCriteria(20.0, 1e9), EngineConfig(iteration_cap=0))
+    assert rep.bad_triangles == 0 and rep.bad_area_percent == 0.0
+    rep = refine(m.copy(), QualityCriteria(20.0, 0.9), EngineConfig(iteration_cap=0))
+    assert rep.bad_triangles == 1 and rep.bad_area_percent == 100.0
+    m, _ = host.build_cdt(np.array([[0, 0], [10, 0], [5, 0.01]], float),
+                          np.array([[0, 1], [1, 2], [2, 0]], np.uint32))
+    rep = refine(m.copy(), QualityCriteria(0.0, math.inf), EngineConfig(iteration_cap=0))
+    assert rep.bad_triangles == 0 and rep.bad_area_percent == 0.0
