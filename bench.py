@@ -315,6 +315,9 @@ def main():
                             "traffic": traffic_db.get(name)}
     dom = max(per_kernel, key=lambda k: per_kernel[k]["share_of_step"] or 0.0)
     refine_gbs = last.algorithmic_bytes() / last.device_seconds / 1e9
+    # device validators on the last timed output (outside the timed region):
+    # structure, local CDT, quality and conformity (k_verify.cu)
+    validation = engines[-1].validate(q)
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
@@ -328,6 +331,7 @@ def main():
         "steiner_points": last.steiner_points,
         "batches": len(last.batches),
         "quality": {"bad_triangles": last.bad_triangles, "min_angle_deg": last.min_angle_deg},
+        "validation": validation,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "wall_s_per_step": e2e_total / e2e_steps},
         "roofline": {"kernel": dom, "bound": "hbm", "achieved": per_kernel[dom]["achieved"],

@@ -238,7 +238,8 @@ void gdp2d_free(gdp2d_mesh_buf* out);
 const char* gdp2d_last_error(void);
 const char* gdp2d_version(void);
 /* sizeof() of the exchange structs, for binding-layout checks:
- * 0 mesh_view, 1 mesh_buf, 2 params, 3 batch_metrics, 4 report, 5 candidate */
+ * 0 mesh_view, 1 mesh_buf, 2 params, 3 batch_metrics, 4 report, 5 candidate,
+ * 6 validation */
 size_t gdp2d_struct_size(int which);
 /* Process-wide count of engine kernel launches so far (all devices). */
 uint64_t gdp2d_kernel_launches(void);
@@ -270,6 +271,24 @@ void  gdp2d_host_free(void* p);
 void gdp2d_release_cached(void);
 /* Bytes of device memory held by the context. */
 uint64_t gdp2d_ctx_device_bytes(gdp2d_ctx* ctx);
+
+/* ---- device validators (k_verify.cu) ------------------- */
+
+/* What the reference validates on the host (mesh.hpp:505-557,
+ * verify.hpp:92-200) computed on the device for the working mesh: */
+typedef struct gdp2d_validation {
+    uint32_t structure_failure;    /* 0 = check_structure passes, else a code  */
+    uint32_t structure_tri;        /* first failing triangle                   */
+    uint64_t cdt_violations;       /* interior non-subsegment edges failing the
+                                      exact local Delaunay test                 */
+    uint64_t bad_triangles;        /* is_bad_triangle && triangle_resolvable    */
+    uint64_t conformity_failures;  /* 0 = every input segment exactly covered   */
+    double   min_angle_deg;
+} gdp2d_validation;
+
+/* Validate the working mesh against p's quality criteria and the uploaded
+ * input's segments (the pristine mesh's subsegments). */
+int gdp2d_ctx_validate(gdp2d_ctx* ctx, const gdp2d_params* p, gdp2d_validation* out);
 
 /* ---- per-phase parity entry points (operate on the working mesh) ----------- */
 

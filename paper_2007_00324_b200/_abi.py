@@ -81,6 +81,12 @@ class Report(C.Structure):
                 ("rollback_bytes", C.c_uint64), ("rollback_launches", C.c_uint64)]
 
 
+class Validation(C.Structure):
+    _fields_ = [("structure_failure", C.c_uint32), ("structure_tri", C.c_uint32),
+                ("cdt_violations", C.c_uint64), ("bad_triangles", C.c_uint64),
+                ("conformity_failures", C.c_uint64), ("min_angle_deg", C.c_double)]
+
+
 class Candidate(C.Structure):
     _fields_ = [("x", C.c_double), ("y", C.c_double), ("measure", C.c_double),
                 ("id", C.c_uint32), ("tiebreak", C.c_uint32), ("located", C.c_uint32),
@@ -96,7 +102,7 @@ def candidate_dtype():
                      ("alive", "u1"), ("fallback", "u1")])
 
 
-STRUCTS = [MeshView, MeshBuf, Params, BatchMetrics, Report, Candidate]
+STRUCTS = [MeshView, MeshBuf, Params, BatchMetrics, Report, Candidate, Validation]
 
 # Every entry point of include/gdp2d.h: name -> (restype, argtypes)
 ctx_p = C.c_void_p
@@ -106,6 +112,7 @@ SIGNATURES = {
                                C.POINTER(Report), C.c_int]),
     "gdp2d_free": (None, [C.POINTER(MeshBuf)]),
     "gdp2d_host_alloc": (C.c_void_p, [C.c_size_t]),
+    "gdp2d_ctx_validate": (C.c_int, [ctx_p, C.POINTER(Params), C.POINTER(Validation)]),
     "gdp2d_host_free": (None, [C.c_void_p]),
     "gdp2d_last_error": (C.c_char_p, []),
     "gdp2d_version": (C.c_char_p, []),

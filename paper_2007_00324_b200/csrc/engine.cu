@@ -322,6 +322,10 @@ struct gdp2d_ctx {
     int rollback_grid = 0;        // persistent rollback kernel grid
     int lawson_grid2 = 0;         // separate batch Lawson kernel grid
     void* sel_state = nullptr;    // batch_size_cap radix-select state
+    uint2* in_sv = nullptr;       // input segments by parent index (validators)
+    u32 n_in = 0;
+    void* vscratch = nullptr;     // validator scratch
+    size_t vscratch_bytes = 0;
     u32 little_cap = 0;           // Little's-law batch cap (resident cavity-filter candidates)
     bool lawson_kernel = false;   // GDP2D_LAWSON_KERNEL=1: separate Lawson launch (measured slower)
     bool legacy_insert = false;   // GDP2D_INSERT=legacy: host-driven insertion rounds
@@ -645,6 +649,8 @@ void ctx_release(gdp2d_ctx* x) {
     dfree(x->d_C);
     dfree(x->scan_part);
     if (x->sel_state) cudaFree(x->sel_state);
+    dfree(x->in_sv);
+    if (x->vscratch) cudaFree(x->vscratch);
     x->tr.release();
     dfree(x->ins_state);
     if (x->h_state) cudaFreeHost(x->h_state);
@@ -716,6 +722,33 @@ void upload(gdp2d_ctx* x, const gdp2d_mesh_view* v) {
     }
     CK(cudaGetLastError());
     x->pristine_epoch = v->batch_epoch;
+    {
+        // input segments by parent index: the chain endpoints of each
+        // parent's subsegments (vertices of odd degree within the parent)
+        u32 np = 0;
+        for (u32 i = 0; i < S; ++i)
+            if (v->seg_alive[i] && v->seg_parent[i] != GDP2D_NONE)
+                np = std::max(np, v->seg_parent[i] + 1);
+        std::vector<std::vector<u32>> ends(np);
+        for (u32 i = 0; i < S; ++i) {
+            if (!v->seg_alive[i] || v->seg_parent[i] == GDP2D_NONE) continue;
+            auto& e = ends[v->seg_parent[i]];
+            for (int k = 0; k < 2; ++k) {
+                const u32 w = v->seg_v[2 * i + k];
+                auto it = std::find(e.begin(), e.end(), w);
+                if (it == e.end()) e.push_back(w);
+                else e.erase(it);
+            }
+        }
+        std::vector<uint2> in(np, make_uint2(0, 0));
+        for (u32 p = 0; p < np; ++p)
+            if (ends[p].size() == 2) in[p] = make_uint2(ends[p][0], ends[p][1]);
+        dfree(x->in_sv);
+        dalloc(x->in_sv, std::max<u32>(np, 1));
+        if (np) CK(cudaMemcpyAsync(x->in_sv, in.data(), sizeof(uint2) * np, cudaMemcpyHostToDevice, st));
+        CK(cudaStreamSynchronize(st));
+        x->n_in = np;
+    }
     ull av = 0, at = 0, as = 0;
     for (u32 i = 0; i < V; ++i) av += v->vert_alive[i] != 0;
     for (u32 i = 0; i < T; ++i) at += v->tri_alive[i] != 0;
@@ -1333,6 +1366,7 @@ size_t gdp2d_struct_size(int which) {
         case 3: return sizeof(gdp2d_batch_metrics);
         case 4: return sizeof(gdp2d_report);
         case 5: return sizeof(gdp2d_candidate);
+        case 6: return sizeof(gdp2d_validation);
         default: return 0;
     }
 }
@@ -1526,6 +1560,29 @@ int gdp2d_collect(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_candidate* out, uin
         if (out && C) std::memcpy(out, tmp.data(), sizeof(gdp2d_candidate) * std::min(C, cap));
     });
     return rc ? rc : status;
+}
+
+int gdp2d_ctx_validate(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_validation* out) {
+    if (!x || !p || !out) return GDP2D_EINVAL;
+    DeviceGuard g(x->device);
+    return run_guarded([&] {
+        VerifySummary v = launch_verify(x->work.m, make_quality(p), x->in_sv, x->n_in,
+                                        x->vscratch, x->vscratch_bytes, x->d_val, x->st);
+        if (v.scratch_needed) {
+            if (x->vscratch) cudaFree(x->vscratch);
+            x->vscratch_bytes = v.scratch_needed;
+            CK(cudaMalloc(&x->vscratch, x->vscratch_bytes));
+            v = launch_verify(x->work.m, make_quality(p), x->in_sv, x->n_in, x->vscratch,
+                              x->vscratch_bytes, x->d_val, x->st);
+        }
+        CK(cudaGetLastError());
+        out->structure_failure = v.structure_failure;
+        out->structure_tri = v.structure_tri;
+        out->cdt_violations = v.cdt_violations;
+        out->bad_triangles = v.bad_triangles;
+        out->conformity_failures = v.conformity_failures;
+        out->min_angle_deg = v.min_angle_deg;
+    });
 }
 
 int gdp2d_split_points(gdp2d_ctx* x, gdp2d_candidate* c, uint32_t n) {

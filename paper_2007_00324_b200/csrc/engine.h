@@ -224,6 +224,17 @@ struct QualitySummary {
 QualitySummary launch_quality(const DevMesh& m, const Quality& q, void* scratch,
                               cudaStream_t st);
 
+// Device validators (k_verify.cu): structure, local CDT, quality, conformity
+// against the input segments (in_sv = the pristine mesh's subsegments).
+struct VerifySummary {
+    u32 structure_failure, structure_tri;
+    ull cdt_violations, bad_triangles, conformity_failures;
+    double min_angle_deg;
+    size_t scratch_needed;   // nonzero: scratch too small, nothing run
+};
+VerifySummary launch_verify(const DevMesh& m, const Quality& q, const uint2* in_sv, u32 nIn,
+                            void* scratch, size_t scratch_bytes, u32* d_val, cudaStream_t st);
+
 // Debug structural validator (out: 4 u32 device words).
 void launch_validate(const DevMesh& m, u32* out, cudaStream_t st);
 

@@ -464,6 +464,14 @@ class Engine:
         mesh.batch_epoch = b.batch_epoch
         return mesh
 
+    def validate(self, q: QualityCriteria) -> dict:
+        """Device validators (k_verify.cu) on the working mesh: structure, local
+        CDT, quality and conformity to the uploaded input segments."""
+        p = make_params(q)
+        v = A.Validation()
+        _raise(self.lib.gdp2d_ctx_validate(self.ctx, C.byref(p), C.byref(v)), "gdp2d_ctx_validate")
+        return {f: getattr(v, f) for f, _ in A.Validation._fields_}
+
     def device_bytes(self) -> int:
         return int(self.lib.gdp2d_ctx_device_bytes(self.ctx))
 
