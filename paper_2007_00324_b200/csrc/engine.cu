@@ -17,6 +17,7 @@
 
 #include "engine.h"
 #include "gdp2d.h"
+#include "scan.cuh"
 
 using namespace gdp2d;
 
@@ -177,6 +178,16 @@ __global__ void k_fill_u64(u64* p, u64 v, size_t n) {
 
 u32 grid(size_t n, u32 b = 256) { return (u32)((n + b - 1) / b); }
 
+__global__ void k_count_alive(DevMesh m, ull* cnt) {
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    const ull v = i < m.nV && m.valive[i];
+    const ull t = i < m.nT && m.tv[i].w;
+    const ull s = i < m.nS && m.salive[i];
+    block_add<ull>(&cnt[0], v);
+    block_add<ull>(&cnt[1], t);
+    block_add<ull>(&cnt[2], s);
+}
+
 Quality make_quality(const gdp2d_params* p) {
     Quality q;
     q.cos2 = p->cos2_theta;
@@ -324,6 +335,7 @@ struct gdp2d_ctx {
     void* sel_state = nullptr;    // batch_size_cap radix-select state
     uint2* in_sv = nullptr;       // input segments by parent index (validators)
     u32 n_in = 0;
+    bool in_valid = false;        // in_sv derived from the current pristine mesh
     void* vscratch = nullptr;     // validator scratch
     size_t vscratch_bytes = 0;
     u32 little_cap = 0;           // Little's-law batch cap (resident cavity-filter candidates)
@@ -722,40 +734,18 @@ void upload(gdp2d_ctx* x, const gdp2d_mesh_view* v) {
     }
     CK(cudaGetLastError());
     x->pristine_epoch = v->batch_epoch;
-    {
-        // input segments by parent index: the chain endpoints of each
-        // parent's subsegments (vertices of odd degree within the parent)
-        u32 np = 0;
-        for (u32 i = 0; i < S; ++i)
-            if (v->seg_alive[i] && v->seg_parent[i] != GDP2D_NONE)
-                np = std::max(np, v->seg_parent[i] + 1);
-        std::vector<std::vector<u32>> ends(np);
-        for (u32 i = 0; i < S; ++i) {
-            if (!v->seg_alive[i] || v->seg_parent[i] == GDP2D_NONE) continue;
-            auto& e = ends[v->seg_parent[i]];
-            for (int k = 0; k < 2; ++k) {
-                const u32 w = v->seg_v[2 * i + k];
-                auto it = std::find(e.begin(), e.end(), w);
-                if (it == e.end()) e.push_back(w);
-                else e.erase(it);
-            }
-        }
-        std::vector<uint2> in(np, make_uint2(0, 0));
-        for (u32 p = 0; p < np; ++p)
-            if (ends[p].size() == 2) in[p] = make_uint2(ends[p][0], ends[p][1]);
-        dfree(x->in_sv);
-        dalloc(x->in_sv, std::max<u32>(np, 1));
-        if (np) CK(cudaMemcpyAsync(x->in_sv, in.data(), sizeof(uint2) * np, cudaMemcpyHostToDevice, st));
-        CK(cudaStreamSynchronize(st));
-        x->n_in = np;
-    }
-    ull av = 0, at = 0, as = 0;
-    for (u32 i = 0; i < V; ++i) av += v->vert_alive[i] != 0;
-    for (u32 i = 0; i < T; ++i) at += v->tri_alive[i] != 0;
-    for (u32 i = 0; i < S; ++i) as += v->seg_alive[i] != 0;
-    x->p_alive_v = av;
-    x->p_alive_t = at;
-    x->p_alive_s = as;
+    x->n_in = 0;   // input segments are derived lazily by gdp2d_ctx_validate
+    x->in_valid = false;
+    // alive counts (batch metrics) on the device, read back with the upload
+    ull* cnt = reinterpret_cast<ull*>(x->qscratch);
+    CK(cudaMemsetAsync(cnt, 0, 3 * sizeof(ull), st));
+    note_launch(), k_count_alive<<<grid(std::max(V, std::max(T, S))), 256, 0, st>>>(m, cnt);
+    ull h[3];
+    CK(cudaMemcpyAsync(h, cnt, sizeof h, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    x->p_alive_v = h[0];
+    x->p_alive_t = h[1];
+    x->p_alive_s = h[2];
 }
 
 void reset_work(gdp2d_ctx* x) {
@@ -1562,10 +1552,51 @@ int gdp2d_collect(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_candidate* out, uin
     return rc ? rc : status;
 }
 
+namespace {
+// Input segments by parent index from the pristine mesh: the chain endpoints
+// of each parent's subsegments (vertices of odd degree within the parent).
+void derive_input_segments(gdp2d_ctx* x) {
+    const DevMesh& pm = x->pristine.m;
+    const u32 S = pm.nS;
+    std::vector<uint2> sv(S);
+    std::vector<u32> par(S);
+    std::vector<uint8_t> al(S);
+    if (S) {
+        CK(cudaMemcpyAsync(sv.data(), pm.sv, sizeof(uint2) * S, cudaMemcpyDeviceToHost, x->st));
+        CK(cudaMemcpyAsync(par.data(), pm.sparent, 4ull * S, cudaMemcpyDeviceToHost, x->st));
+        CK(cudaMemcpyAsync(al.data(), pm.salive, S, cudaMemcpyDeviceToHost, x->st));
+        CK(cudaStreamSynchronize(x->st));
+    }
+    u32 np = 0;
+    for (u32 i = 0; i < S; ++i)
+        if (al[i] && par[i] != GDP2D_NONE) np = std::max(np, par[i] + 1);
+    std::vector<std::vector<u32>> ends(np);
+    for (u32 i = 0; i < S; ++i) {
+        if (!al[i] || par[i] == GDP2D_NONE) continue;
+        auto& e = ends[par[i]];
+        for (const u32 w : {sv[i].x, sv[i].y}) {
+            auto it = std::find(e.begin(), e.end(), w);
+            if (it == e.end()) e.push_back(w);
+            else e.erase(it);
+        }
+    }
+    std::vector<uint2> in(np, make_uint2(0, 0));
+    for (u32 q = 0; q < np; ++q)
+        if (ends[q].size() == 2) in[q] = make_uint2(ends[q][0], ends[q][1]);
+    dfree(x->in_sv);
+    dalloc(x->in_sv, std::max<u32>(np, 1));
+    if (np) CK(cudaMemcpyAsync(x->in_sv, in.data(), sizeof(uint2) * np, cudaMemcpyHostToDevice, x->st));
+    CK(cudaStreamSynchronize(x->st));
+    x->n_in = np;
+    x->in_valid = true;
+}
+}  // namespace
+
 int gdp2d_ctx_validate(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_validation* out) {
     if (!x || !p || !out) return GDP2D_EINVAL;
     DeviceGuard g(x->device);
     return run_guarded([&] {
+        if (!x->in_valid) derive_input_segments(x);
         VerifySummary v = launch_verify(x->work.m, make_quality(p), x->in_sv, x->n_in,
                                         x->vscratch, x->vscratch_bytes, x->d_val, x->st);
         if (v.scratch_needed) {
