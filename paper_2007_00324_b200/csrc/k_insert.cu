@@ -783,11 +783,13 @@ __device__ __noinline__ u32 rm_apply_one(const DevMesh& m, const u32* __restrict
             u32 L[MAX_STAR], R[MAX_STAR], SG[MAX_STAR], ORG[MAX_STAR];
             uint8_t PK[MAX_STAR];  // 1 = old outer ref, 2 = local (idx<<2|slot), 0 = none
             int NX[MAX_STAR], PV[MAX_STAR];
+            double2 XY[MAX_STAR];  // link vertex coordinates, gathered once
             for (int q = 0; q < k; ++q) {
                 const u32 t = st[q];
                 const uint4 tv = m.tv[t], tn = m.tn[t], ts = m.ts[t];
                 const int iv = tv.x == v ? 0 : (tv.y == v ? 1 : 2);
                 L[q] = comp(tv, nxt(iv));
+                XY[q] = m.xy[L[q]];
                 R[q] = comp(tn, iv);
                 PK[q] = R[q] == NONE ? 0 : 1;
                 SG[q] = comp(ts, iv);
@@ -836,13 +838,13 @@ __device__ __noinline__ u32 rm_apply_one(const DevMesh& m, const u32* __restrict
                     j = head;
                     for (int it = 0; it < cnt; ++it) {
                         const int a = PV[j], c = NX[j];
-                        const double2 pa = m.xy[L[a]], pj = m.xy[L[j]], pc = m.xy[L[c]];
+                        const double2 pa = XY[a], pj = XY[j], pc = XY[c];
                         const int side = orient2d(pa, pc, pv);
                         if (orient2d(pa, pj, pc) > 0 && (side > 0 || (pass == 1 && side == 0))) {
                             bool delaunay = true;
                             if (pass < 0) {
                                 for (int q = NX[c]; q != a && delaunay; q = NX[q])
-                                    delaunay = incircle(pa, pj, pc, m.xy[L[q]]) <= 0;
+                                    delaunay = incircle(pa, pj, pc, XY[q]) <= 0;
                             }
                             if (delaunay) {
                                 found = true;
@@ -885,7 +887,7 @@ __device__ __noinline__ u32 rm_apply_one(const DevMesh& m, const u32* __restrict
                 bind(ci, 0, b);
                 bind(ci, 1, c);
                 bind(ci, 2, a);
-                ok = orient2d(m.xy[L[a]], m.xy[L[b]], m.xy[L[c]]) > 0;
+                ok = orient2d(XY[a], XY[b], XY[c]) > 0;
             }
             if (!ok) {
                 // No flippable incident edge (degenerate star): like
