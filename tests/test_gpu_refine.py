@@ -280,3 +280,30 @@ def test_quality_report_fractions(built):
                           np.array([[0, 1], [1, 2], [2, 0]], np.uint32))
     rep = refine(m.copy(), QualityCriteria(0.0, math.inf), EngineConfig(iteration_cap=0))
     assert rep.bad_triangles == 0 and rep.bad_area_percent == 0.0
+
+
+@pytest.mark.parametrize("mode,ell", [(1, math.inf), (0, 0.01), (1, 0.01)])
+def test_chew_and_edge_bound_at_scale(built, mode, ell):
+    """Chew's lens rule (predicates.hpp:126-162) and the
+    edge-length bound (refine.hpp:192-206) on a 50K-point PSLG: quality,
+    conforming CDT (device validators + reference validators) and Steiner
+    count within 10% of the reference."""
+    from paper_2007_00324_b200 import Engine, QualityCriteria, host
+    from oracle.ref import RefMesh
+    q = QualityCriteria(B_SQRT2_THETA, ell, mode)
+    pts, segs = host.generate_pslg(50_000, 5_000, "uniform", 51)
+    m, closed = host.build_cdt(pts, segs)
+    with Engine(0) as eng:
+        eng.upload(m)
+        rep = eng.refine(q)
+        val = eng.validate(q)
+        out = eng.download()
+    rref = RefMesh.from_mesh(m).refine(q)
+    assert val["structure_failure"] == 0 and val["cdt_violations"] == 0
+    assert val["conformity_failures"] == 0 and val["bad_triangles"] == 0
+    rm = RefMesh.from_mesh(out)
+    assert rm.conformity_ok(pts, closed) and len(rm.collect(q)) == 0
+    if math.isfinite(ell):
+        assert rep.max_edge <= ell
+    assert abs(rep.steiner_points - rref.steiner_points) <= 0.10 * rref.steiner_points, \
+        (rep.steiner_points, rref.steiner_points)
