@@ -265,8 +265,8 @@ int  gdp2d_ctx_sizes(gdp2d_ctx* ctx, uint32_t* n_vertices, uint32_t* n_triangles
 int  gdp2d_ctx_download_to(gdp2d_ctx* ctx, gdp2d_mesh_buf* dst);
 /* Page-locked host memory (cudaHostAlloc, portable) for meshes that are
  * uploaded / downloaded repeatedly: H2D/D2H at full PCIe/C2C rate. */
-void* gdp2d_host_alloc(size_t bytes);
-void  gdp2d_host_free(void* p);
+void* gdp2d_pinned_alloc(size_t bytes);
+void  gdp2d_pinned_free(void* p);
 /* Release the per-device contexts that gdp2d_refine() keeps cached. */
 void gdp2d_release_cached(void);
 /* Bytes of device memory held by the context. */

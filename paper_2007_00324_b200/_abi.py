@@ -111,9 +111,9 @@ SIGNATURES = {
     "gdp2d_refine": (C.c_int, [C.POINTER(MeshView), C.POINTER(MeshBuf), C.POINTER(Params),
                                C.POINTER(Report), C.c_int]),
     "gdp2d_free": (None, [C.POINTER(MeshBuf)]),
-    "gdp2d_host_alloc": (C.c_void_p, [C.c_size_t]),
+    "gdp2d_pinned_alloc": (C.c_void_p, [C.c_size_t]),
+    "gdp2d_pinned_free": (None, [C.c_void_p]),
     "gdp2d_ctx_validate": (C.c_int, [ctx_p, C.POINTER(Params), C.POINTER(Validation)]),
-    "gdp2d_host_free": (None, [C.c_void_p]),
     "gdp2d_last_error": (C.c_char_p, []),
     "gdp2d_version": (C.c_char_p, []),
     "gdp2d_struct_size": (C.c_size_t, [C.c_int]),

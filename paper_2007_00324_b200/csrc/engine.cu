@@ -1468,7 +1468,7 @@ int gdp2d_refine(const gdp2d_mesh_view* in, gdp2d_mesh_buf* out, const gdp2d_par
     });
 }
 
-void* gdp2d_host_alloc(size_t bytes) {
+void* gdp2d_pinned_alloc(size_t bytes) {
     void* p = nullptr;
     if (cudaHostAlloc(&p, bytes ? bytes : 1, cudaHostAllocPortable) != cudaSuccess) {
         g_err = "cudaHostAlloc failed";
@@ -1477,7 +1477,7 @@ void* gdp2d_host_alloc(size_t bytes) {
     return p;
 }
 
-void gdp2d_host_free(void* p) {
+void gdp2d_pinned_free(void* p) {
     if (p) cudaFreeHost(p);
 }
 

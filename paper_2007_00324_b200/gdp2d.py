@@ -277,7 +277,7 @@ class Mesh:
 
 
 class PinnedPool:
-    """Page-locked host buffers (gdp2d_host_alloc) for meshes of up to
+    """Page-locked host buffers (gdp2d_pinned_alloc) for meshes of up to
     (nv, nt, ns) elements: uploads / downloads from here run at full link rate.
     ``mesh(...)`` returns a Mesh whose arrays are views into the pool (no copy)."""
 
@@ -299,16 +299,16 @@ class PinnedPool:
         for name, dt, w in _FIELDS:
             n = self.caps["v" if name in _VERT else "t" if name in _TRI else "s"] * w
             nbytes = n * np.dtype(dt).itemsize
-            ptr = self.lib.gdp2d_host_alloc(nbytes)
+            ptr = self.lib.gdp2d_pinned_alloc(nbytes)
             if not ptr:
-                raise MemoryError(f"gdp2d_host_alloc({nbytes}) failed")
+                raise MemoryError(f"gdp2d_pinned_alloc({nbytes}) failed")
             self._ptrs.append(ptr)
             buf = (C.c_uint8 * nbytes).from_address(ptr)
             self._bufs[name] = np.frombuffer(buf, dtype=dt, count=n)
 
     def close(self) -> None:
         for p in self._ptrs:
-            self.lib.gdp2d_host_free(p)
+            self.lib.gdp2d_pinned_free(p)
         self._ptrs = []
         self._bufs = {}
 
