@@ -239,7 +239,7 @@ const char* gdp2d_last_error(void);
 const char* gdp2d_version(void);
 /* sizeof() of the exchange structs, for binding-layout checks:
  * 0 mesh_view, 1 mesh_buf, 2 params, 3 batch_metrics, 4 report, 5 candidate,
- * 6 validation */
+ * 6 validation, 7 node_ele */
 size_t gdp2d_struct_size(int which);
 /* Process-wide count of engine kernel launches so far (all devices). */
 uint64_t gdp2d_kernel_launches(void);
@@ -289,6 +289,23 @@ typedef struct gdp2d_validation {
 /* Validate the working mesh against p's quality criteria and the uploaded
  * input's segments (the pristine mesh's subsegments). */
 int gdp2d_ctx_validate(gdp2d_ctx* ctx, const gdp2d_params* p, gdp2d_validation* out);
+
+/* ---- compacted export ----------------------------------- */
+
+/* write_node_ele (pslg_io.hpp:294-319) data, compacted on the device: alive
+ * vertices renumbered densely in id order (xy + marker 1 = input, 0 =
+ * Steiner), alive triangles in id order as dense vertex triples.  Caller
+ * allocates xy[2V], marker[V], tri[3T] with V, T from gdp2d_ctx_sizes (upper
+ * bounds); n_nodes / n_tris return the counts.  Moves ~17 B per alive vertex
+ * + 12 B per alive triangle instead of the whole slot-preserving mesh. */
+typedef struct gdp2d_node_ele {
+    uint32_t n_nodes, n_tris;
+    double*  xy;
+    uint8_t* marker;
+    uint32_t* tri;
+} gdp2d_node_ele;
+
+int gdp2d_ctx_export(gdp2d_ctx* ctx, gdp2d_node_ele* out);
 
 /* ---- per-phase parity entry points (operate on the working mesh) ----------- */
 

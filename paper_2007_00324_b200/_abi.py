@@ -87,6 +87,12 @@ class Validation(C.Structure):
                 ("conformity_failures", C.c_uint64), ("min_angle_deg", C.c_double)]
 
 
+class NodeEle(C.Structure):
+    _fields_ = [("n_nodes", C.c_uint32), ("n_tris", C.c_uint32),
+                ("xy", C.POINTER(C.c_double)), ("marker", C.POINTER(C.c_uint8)),
+                ("tri", C.POINTER(C.c_uint32))]
+
+
 class Candidate(C.Structure):
     _fields_ = [("x", C.c_double), ("y", C.c_double), ("measure", C.c_double),
                 ("id", C.c_uint32), ("tiebreak", C.c_uint32), ("located", C.c_uint32),
@@ -102,7 +108,7 @@ def candidate_dtype():
                      ("alive", "u1"), ("fallback", "u1")])
 
 
-STRUCTS = [MeshView, MeshBuf, Params, BatchMetrics, Report, Candidate, Validation]
+STRUCTS = [MeshView, MeshBuf, Params, BatchMetrics, Report, Candidate, Validation, NodeEle]
 
 # Every entry point of include/gdp2d.h: name -> (restype, argtypes)
 ctx_p = C.c_void_p
@@ -114,6 +120,7 @@ SIGNATURES = {
     "gdp2d_pinned_alloc": (C.c_void_p, [C.c_size_t]),
     "gdp2d_pinned_free": (None, [C.c_void_p]),
     "gdp2d_ctx_validate": (C.c_int, [ctx_p, C.POINTER(Params), C.POINTER(Validation)]),
+    "gdp2d_ctx_export": (C.c_int, [ctx_p, C.POINTER(NodeEle)]),
     "gdp2d_last_error": (C.c_char_p, []),
     "gdp2d_version": (C.c_char_p, []),
     "gdp2d_struct_size": (C.c_size_t, [C.c_int]),
@@ -155,6 +162,9 @@ HOST_SIGNATURES = {
                                        C.POINTER(u32p), C.POINTER(C.c_uint32)]),
     "gdp2d_host_write_node_ele": (C.c_int, [C.POINTER(MeshView), C.POINTER(C.c_char_p),
                                             C.POINTER(C.c_char_p)]),
+    "gdp2d_host_format_node_ele": (C.c_int, [C.c_uint32, C.c_void_p, C.c_void_p, C.c_uint32,
+                                             C.c_void_p, C.POINTER(C.c_char_p),
+                                             C.POINTER(C.c_char_p)]),
     "gdp2d_host_free_buf": (None, [C.POINTER(MeshBuf)]),
     "gdp2d_host_last_error": (C.c_char_p, []),
 }

@@ -1357,6 +1357,7 @@ size_t gdp2d_struct_size(int which) {
         case 4: return sizeof(gdp2d_report);
         case 5: return sizeof(gdp2d_candidate);
         case 6: return sizeof(gdp2d_validation);
+        case 7: return sizeof(gdp2d_node_ele);
         default: return 0;
     }
 }
@@ -1613,6 +1614,46 @@ int gdp2d_ctx_validate(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_validation* ou
         out->bad_triangles = v.bad_triangles;
         out->conformity_failures = v.conformity_failures;
         out->min_angle_deg = v.min_angle_deg;
+    });
+}
+
+int gdp2d_ctx_export(gdp2d_ctx* x, gdp2d_node_ele* out) {
+    if (!x || !out || !out->xy || !out->marker || !out->tri) return GDP2D_EINVAL;
+    DeviceGuard g(x->device);
+    return run_guarded([&] {
+        const DevMesh& m = x->work.m;
+        const u32 V = m.nV, T = m.nT;
+        cudaStream_t st = x->st;
+        // device scratch: flags + offsets + compacted outputs
+        const size_t need = 8ull * V + 8ull * T + 16ull * V + V + 12ull * T + 64;
+        if (need > x->vscratch_bytes) {
+            if (x->vscratch) cudaFree(x->vscratch);
+            x->vscratch_bytes = need;
+            CK(cudaMalloc(&x->vscratch, need));
+        }
+        char* b = static_cast<char*>(x->vscratch);
+        double2* xy = reinterpret_cast<double2*>(b);
+        b += 16ull * V;
+        u32* fv = reinterpret_cast<u32*>(b);
+        u32* ov = fv + V;
+        u32* ft = ov + V;
+        u32* ot = ft + T;
+        u32* tri = ot + T;
+        u32* totals = tri + 3ull * T;
+        uint8_t* marker = reinterpret_cast<uint8_t*>(totals + 4);
+        launch_export(m, fv, ov, ft, ot, xy, marker, tri, totals, x->scan, st);
+        CK(cudaGetLastError());
+        u32 h[2];
+        CK(cudaMemcpyAsync(h, totals, sizeof h, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        out->n_nodes = h[0];
+        out->n_tris = h[1];
+        if (h[0]) {
+            CK(cudaMemcpyAsync(out->xy, xy, 16ull * h[0], cudaMemcpyDeviceToHost, st));
+            CK(cudaMemcpyAsync(out->marker, marker, h[0], cudaMemcpyDeviceToHost, st));
+        }
+        if (h[1]) CK(cudaMemcpyAsync(out->tri, tri, 12ull * h[1], cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
     });
 }
 

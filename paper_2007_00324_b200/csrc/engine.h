@@ -235,6 +235,10 @@ struct VerifySummary {
 VerifySummary launch_verify(const DevMesh& m, const Quality& q, const uint2* in_sv, u32 nIn,
                             void* scratch, size_t scratch_bytes, u32* d_val, cudaStream_t st);
 
+// Compacted node/ele export (k_verify.cu).
+void launch_export(const DevMesh& m, u32* fv, u32* ov, u32* ft, u32* ot, double2* xy,
+                   uint8_t* marker, u32* tri, u32* totals, ScanScratch& s, cudaStream_t st);
+
 // Debug structural validator (out: 4 u32 device words).
 void launch_validate(const DevMesh& m, u32* out, cudaStream_t st);
 

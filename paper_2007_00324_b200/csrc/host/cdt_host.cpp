@@ -187,6 +187,43 @@ int gdp2d_host_write_node_ele(const gdp2d_mesh_view* v, char** node, char** ele)
     }
 }
 
+// write_node_ele's text (pslg_io.hpp:294-319) from an already compacted mesh
+// (gdp2d_ctx_export): same header lines, same shortest round-trip doubles
+// (detail::shortest -> std::to_chars), same row numbering.
+int gdp2d_host_format_node_ele(uint32_t n_nodes, const double* xy, const uint8_t* marker,
+                               uint32_t n_tris, const uint32_t* tri, char** node, char** ele) {
+    try {
+        std::string nd = std::to_string(n_nodes) + " 2 0 1\n";
+        nd.reserve(nd.size() + 48ull * n_nodes);
+        for (uint32_t i = 0; i < n_nodes; ++i) {
+            nd += std::to_string(i);
+            nd += ' ';
+            nd += cdtref::detail::shortest(xy[2 * i]);
+            nd += ' ';
+            nd += cdtref::detail::shortest(xy[2 * i + 1]);
+            nd += marker[i] ? " 1\n" : " 0\n";
+        }
+        std::string el = std::to_string(n_tris) + " 3 0\n";
+        el.reserve(el.size() + 32ull * n_tris);
+        for (uint32_t t = 0; t < n_tris; ++t) {
+            el += std::to_string(t);
+            for (int k = 0; k < 3; ++k) {
+                el += ' ';
+                el += std::to_string(tri[3ull * t + k]);
+            }
+            el += '\n';
+        }
+        *node = static_cast<char*>(std::malloc(nd.size() + 1));
+        *ele = static_cast<char*>(std::malloc(el.size() + 1));
+        std::memcpy(*node, nd.c_str(), nd.size() + 1);
+        std::memcpy(*ele, el.c_str(), el.size() + 1);
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
 void gdp2d_host_free_buf(gdp2d_mesh_buf* b) {
     void* ptrs[] = {b->xy,      b->vert_kind, b->vert_birth, b->vert_alive, b->vert_tri,
                     b->tri_v,   b->tri_n,     b->tri_seg,    b->tri_alive,  b->seg_v,

@@ -168,4 +168,44 @@ VerifySummary launch_verify(const DevMesh& m, const Quality& q, const uint2* in_
     return out;
 }
 
+// ---- compacted export (write_node_ele, pslg_io.hpp:294-319) ---------------------
+
+__global__ void k_alive_flags(DevMesh m, u32* __restrict__ fv, u32* __restrict__ ft) {
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m.nV) fv[i] = m.valive[i] ? 1u : 0u;
+    if (i < m.nT) ft[i] = m.tv[i].w ? 1u : 0u;
+}
+
+__global__ void k_emit_nodes(DevMesh m, const u32* __restrict__ ov, double2* __restrict__ xy,
+                             uint8_t* __restrict__ marker) {
+    const u32 v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= m.nV || !m.valive[v]) return;
+    const u32 o = ov[v];
+    xy[o] = m.xy[v];
+    marker[o] = m.vkind[v] == 0 ? 1 : 0;
+}
+
+__global__ void k_emit_tris(DevMesh m, const u32* __restrict__ ov, const u32* __restrict__ ot,
+                            u32* __restrict__ tri) {
+    const u32 t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= m.nT) return;
+    const uint4 tv = m.tv[t];
+    if (!tv.w) return;
+    const u32 o = ot[t];
+    tri[3 * (size_t)o] = ov[tv.x];
+    tri[3 * (size_t)o + 1] = ov[tv.y];
+    tri[3 * (size_t)o + 2] = ov[tv.z];
+}
+
+// scratch: fv[V] ov[V] ft[T] ot[T] | out xy[2V] marker[V] tri[3T] | totals
+void launch_export(const DevMesh& m, u32* fv, u32* ov, u32* ft, u32* ot, double2* xy,
+                   uint8_t* marker, u32* tri, u32* totals, ScanScratch& s, cudaStream_t st) {
+    const u32 n = m.nV > m.nT ? m.nV : m.nT;
+    if (n) note_launch(), k_alive_flags<<<(n + 255) / 256, 256, 0, st>>>(m, fv, ft);
+    scan_exclusive(fv, ov, m.nV, totals + 0, s, st);
+    scan_exclusive(ft, ot, m.nT, totals + 1, s, st);
+    if (m.nV) note_launch(), k_emit_nodes<<<(m.nV + 255) / 256, 256, 0, st>>>(m, ov, xy, marker);
+    if (m.nT) note_launch(), k_emit_tris<<<(m.nT + 255) / 256, 256, 0, st>>>(m, ov, ot, tri);
+}
+
 }  // namespace gdp2d

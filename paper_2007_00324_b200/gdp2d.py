@@ -464,6 +464,20 @@ class Engine:
         mesh.batch_epoch = b.batch_epoch
         return mesh
 
+    def export_node_ele(self):
+        """Compacted write_node_ele data (gdp2d_ctx_export): (xy[n,2], marker[n],
+        tri[m,3]) with dense vertex numbering, alive elements in id order."""
+        nv, nt, _ = self.sizes()
+        xy = np.empty((max(nv, 1), 2), np.float64)
+        marker = np.empty(max(nv, 1), np.uint8)
+        tri = np.empty((max(nt, 1), 3), np.uint32)
+        o = A.NodeEle()
+        o.xy = xy.ctypes.data_as(C.POINTER(C.c_double))
+        o.marker = marker.ctypes.data_as(C.POINTER(C.c_uint8))
+        o.tri = tri.ctypes.data_as(C.POINTER(C.c_uint32))
+        _raise(self.lib.gdp2d_ctx_export(self.ctx, C.byref(o)), "gdp2d_ctx_export")
+        return xy[: o.n_nodes], marker[: o.n_nodes], tri[: o.n_tris]
+
     def validate(self, q: QualityCriteria) -> dict:
         """Device validators (k_verify.cu) on the working mesh: structure, local
         CDT, quality and conformity to the uploaded input segments."""

@@ -82,6 +82,22 @@ def write_node_ele(mesh: Mesh):
     return out
 
 
+def format_node_ele(xy: np.ndarray, marker: np.ndarray, tri: np.ndarray):
+    """.node/.ele text of a compacted export (Engine.export_node_ele), byte-
+    identical to write_node_ele (pslg_io.hpp:294) of the same mesh."""
+    lib = A.host()
+    node = C.c_char_p()
+    ele = C.c_char_p()
+    xy = np.ascontiguousarray(xy, np.float64)
+    marker = np.ascontiguousarray(marker, np.uint8)
+    tri = np.ascontiguousarray(tri, np.uint32)
+    rc = lib.gdp2d_host_format_node_ele(len(xy), xy.ctypes.data, marker.ctypes.data, len(tri),
+                                        tri.ctypes.data, C.byref(node), C.byref(ele))
+    if rc:
+        raise RuntimeError(lib.gdp2d_host_last_error().decode())
+    return node.value.decode(), ele.value.decode()
+
+
 def workload(config: int, seed: int = SEED):
     """BASELINE.json configs -> (points, segments, theta).  Theta in degrees."""
     import math

@@ -85,3 +85,21 @@ def test_baseline_size_validation(built):
     assert res["bad_triangles"] == 0 and res["conformity_failures"] == 0
     assert res["min_angle_deg"] >= q.theta - 1e-9
     assert dt < 5.0
+
+
+def test_compacted_export_matches_write_node_ele(built):
+    """the device-compacted export formats to exactly the
+    reference's write_node_ele text (pslg_io.hpp:294-319) of the same mesh,
+    while moving only the alive elements."""
+    from paper_2007_00324_b200 import Engine, host
+    mesh, pts, closed, q = _refined(20_000, 2_000, "gaussian", 43)
+    with Engine(0) as eng:
+        eng.upload(mesh)
+        eng.refine(q)
+        xy, marker, tri = eng.export_node_ele()
+        full = eng.download()
+    node, ele = host.format_node_ele(xy, marker, tri)
+    rnode, rele = host.write_node_ele(full)
+    assert node == rnode
+    assert ele == rele
+    assert len(xy) == full.alive_vertex_count() and len(tri) == full.alive_triangle_count()
