@@ -125,6 +125,10 @@ __device__ __forceinline__ u32 cavity_bfs_one(const DevMesh& m, const DevCands& 
     u32 len = 0, blen = 0;
     if (c.alive[i]) {
         u32* reg = regions + (size_t)i * rs;
+        // the region is built in a thread-local array (L1) and written out
+        // once: membership tests against global memory would cost an L2
+        // round trip each
+        u32 lreg[MAX_CAVITY_N + 1 + MAX_CLAIM_EXTRA];
         u32 queue[1 + 3 * (MAX_CAVITY_N + 1)];
         u32 head = 0, tail = 0;
         const u32 located = c.loc[i];
@@ -133,28 +137,30 @@ __device__ __forceinline__ u32 cavity_bfs_one(const DevMesh& m, const DevCands& 
         queue[tail++] = located;
         while (head < tail && len <= ncav) {
             const u32 t = queue[head++];
+            // issue the three record loads together (one dependent level)
             const uint4 tv = m.tv[t];
+            const uint4 tn = m.tn[t];
+            const uint4 ts = m.ts[t];
             bool pred = t == located;
             if (!pred && tv.w) pred = incircle(m.xy[tv.x], m.xy[tv.y], m.xy[tv.z], p) > 0;
             if (!pred) continue;
             bool in = false;
-            for (u32 k = 0; k < len; ++k) in |= reg[k] == t;
+            for (u32 k = 0; k < len; ++k) in |= lreg[k] == t;
             if (in) continue;
-            reg[len++] = t;
+            lreg[len++] = t;
             atomicMax((ull*)&ckey[t], (ull)key);
-            const uint4 tn = m.tn[t];
-            const uint4 ts = m.ts[t];
             for (int e = 0; e < 3; ++e) {
                 if (comp(ts, e) != NONE) continue;
                 const u32 cc = comp(tn, e);
                 if (cc == NONE) continue;
                 const u32 nb = etri(cc);
                 bool seen = false;
-                for (u32 k = 0; k < len; ++k) seen |= reg[k] == nb;
+                for (u32 k = 0; k < len; ++k) seen |= lreg[k] == nb;
                 if (seen) continue;
                 queue[tail++] = nb;
             }
         }
+        for (u32 k = 0; k < len; ++k) reg[k] = lreg[k];
         blen = len;
         if (extras == 1) {
             u32 far = NONE;

@@ -268,6 +268,7 @@ __device__ __forceinline__ void fixup_one(const DevMesh& m, u32 round, const Tri
                                           RoundCtr* rc, Counters* ctr) {
     uint4 tn = m.tn[t];
     const uint4 tv = m.tv[t];
+    const uint4 ts = m.ts[t];
     if (!tv.w) return;
     const u32 pend = tn.w;
     u32* tn_words = reinterpret_cast<u32*>(m.tn);
@@ -288,7 +289,6 @@ __device__ __forceinline__ void fixup_one(const DevMesh& m, u32 round, const Tri
     atomicMin(&m.vtri[tv.x], t);
     atomicMin(&m.vtri[tv.y], t);
     atomicMin(&m.vtri[tv.z], t);
-    const uint4 ts = m.ts[t];
     if (w.vdirty) {
         // Suspects for the redundancy detection (refine.hpp:551-608): a
         // same-batch circumcenter can only be redundant as the apex of a
@@ -343,14 +343,20 @@ __device__ __forceinline__ void flip_test_one(const DevMesh& m, u32 code, const 
     u32 t = etri(code);
     int e = eidx(code);
     if (t >= m.nT) return;
-    const uint4 tv0 = m.tv[t];
+    // record loads issued together: the dependent chain is t's record ->
+    // the neighbour's corners -> the four coordinates
+    const uint4 tv0 = m.tv[t], tn0 = m.tn[t], ts0 = m.ts[t];
     if (!tv0.w) return;
-    const u32 c = comp(m.tn[t], e);
-    if (c == NONE) return;
-    if (comp(m.ts[t], e) != NONE) return;
+    const u32 c = comp(tn0, e);
+    if (c == NONE || comp(ts0, e) != NONE) return;
     u32 u = etri(c);
     int f = eidx(c);
-    if (u < t) {
+    const uint4 tvu = m.tv[u];
+    uint4 tv = tv0;
+    u32 d = comp(tvu, f);
+    if (u < t) {   // test on the canonical (lower id) side
+        d = comp(tv0, e);
+        tv = tvu;
         const u32 tt = t;
         const int ee = e;
         t = u;
@@ -358,8 +364,6 @@ __device__ __forceinline__ void flip_test_one(const DevMesh& m, u32 code, const 
         u = tt;
         f = ee;
     }
-    const uint4 tv = m.tv[t];
-    const u32 d = comp(m.tv[u], f);
     if (incircle(m.xy[tv.x], m.xy[tv.y], m.xy[tv.z], m.xy[d]) <= 0) return;
     const u32 key = enc(t, e);
     atomicMin(&x.owner[t], key);
@@ -380,14 +384,16 @@ __device__ __forceinline__ u32 flip_apply_one(const DevMesh& m, u32 i, u32 round
     const u32 key = w.fc[i], uc = w.fu[i];
     const u32 t = etri(key), u = etri(uc);
     const int e = eidx(key), f = eidx(uc);
-    const bool won = x.owner[t] == key && x.owner[u] == key;
-    w.fwin[i] = won;
-    // Duplicate work items carry the same key and all "win"; exactly one
-    // performs the flip -- the stamp exchange comes BEFORE any read, so a
-    // duplicate never sees the half-rewritten pair.
-    if (!won || atomicExch(&x.stamp[t], round) == round) return 0;
+    // the pair's records are loaded together with the claims; a duplicate
+    // work item (same key, all "win") that loses the stamp exchange below
+    // discards them, and the winner's reads precede any write to the pair
+    const u32 ot = x.owner[t], ou = x.owner[u];
     const uint4 tv = m.tv[t], tn = m.tn[t], ts = m.ts[t];
     const uint4 uv = m.tv[u], un = m.tn[u], us = m.ts[u];
+    const bool won = ot == key && ou == key;
+    w.fwin[i] = won;
+    // exactly one duplicate performs the flip
+    if (!won || atomicExch(&x.stamp[t], round) == round) return 0;
     const u32 a = comp(tv, e), b = comp(tv, nxt(e)), c = comp(tv, prv(e));
     const u32 d = comp(uv, f);
     const double2 pa = m.xy[a], pb = m.xy[b], pc = m.xy[c], pd = m.xy[d];
