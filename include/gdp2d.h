@@ -49,7 +49,10 @@ enum {
     GDP2D_ENODEVICE = 3,  /* no usable sm_100 device                       */
     GDP2D_ECAPACITY = 4,  /* device work-list / stack capacity exceeded    */
     GDP2D_EMESH = 5,      /* structural failure inside a mesh mutation     */
-    GDP2D_EINTERNAL = 6
+    GDP2D_EINTERNAL = 6,
+    GDP2D_ECDT = 7        /* PSLG cannot be triangulated (CdtError, cdt.hpp:20):
+                             duplicate points, all collinear, crossing segments,
+                             non-finite coordinates                        */
 };
 
 /* VertexKind (mesh.hpp:26) */
@@ -239,7 +242,7 @@ const char* gdp2d_last_error(void);
 const char* gdp2d_version(void);
 /* sizeof() of the exchange structs, for binding-layout checks:
  * 0 mesh_view, 1 mesh_buf, 2 params, 3 batch_metrics, 4 report, 5 candidate,
- * 6 validation, 7 node_ele */
+ * 6 validation, 7 node_ele, 8 cdt_report */
 size_t gdp2d_struct_size(int which);
 /* Process-wide count of engine kernel launches so far (all devices). */
 uint64_t gdp2d_kernel_launches(void);
@@ -306,6 +309,43 @@ typedef struct gdp2d_node_ele {
 } gdp2d_node_ele;
 
 int gdp2d_ctx_export(gdp2d_ctx* ctx, gdp2d_node_ele* out);
+
+/* ---- Line 1 on the device: initial constrained Delaunay triangulation ----
+ * Replaces build_cdt(const Pslg&) (cdt.hpp:483 = build_delaunay :198 +
+ * recover_segments :437 + lawson_fixpoint_all).  Input: the PSLG after
+ * close_hull (cdt.hpp:447; read_poly/to_pslg already apply it): n points
+ * xy[2n] and m segments seg[2m] (vertex indices).  The result becomes the
+ * context's input mesh (as gdp2d_ctx_upload would), so gdp2d_ctx_refine /
+ * gdp2d_ctx_download follow directly.  Vertex i = points[i]; subsegment s
+ * belongs to segment sparent[s] (s = segment index unless a segment passes
+ * through a vertex, which splits it exactly as recover_chain does).  Triangle
+ * ids differ from the reference's; the triangle SET equals it for PSLGs in
+ * general position (the CDT is unique).  Errors: GDP2D_ECDT. */
+typedef struct gdp2d_cdt_report {
+    uint32_t struct_size;
+    uint32_t n_triangles;        /* alive triangles of the CDT            */
+    uint32_t n_subsegments;
+    uint32_t insert_rounds;      /* parallel insertion rounds             */
+    uint32_t flip_rounds;        /* Lawson rounds during insertion        */
+    uint32_t recover_rounds;     /* segment recovery rounds               */
+    uint32_t segments_present;   /* pieces already edges of the DT        */
+    uint32_t pipes_recovered;    /* pieces recovered by pipe flips        */
+    uint32_t collinear_splits;   /* pieces split at a vertex on them      */
+    uint32_t max_pipe;           /* longest pipe (triangles)              */
+    uint32_t final_flip_rounds;  /* constrained Lawson after recovery     */
+    uint32_t reserved;
+    uint64_t flips;              /* all Lawson flips                      */
+    double seconds;              /* device time, upload to compacted mesh */
+    double delaunay_seconds, recover_seconds, finish_seconds;
+} gdp2d_cdt_report;
+
+int gdp2d_ctx_build_cdt(gdp2d_ctx* ctx, const double* xy, uint32_t n_points,
+                        const uint32_t* seg, uint32_t n_segments, gdp2d_cdt_report* rep);
+/* One-shot form: build on `device` and download into *out (free with
+ * gdp2d_free). */
+int gdp2d_build_cdt(const double* xy, uint32_t n_points, const uint32_t* seg,
+                    uint32_t n_segments, gdp2d_mesh_buf* out, gdp2d_cdt_report* rep,
+                    int device);
 
 /* ---- per-phase parity entry points (operate on the working mesh) ----------- */
 

@@ -10,9 +10,9 @@ NONE = 0xFFFFFFFF
 PENDING = 0xFFFFFFFE
 
 # status codes
-OK, EINVAL, ECUDA, ENODEVICE, ECAPACITY, EMESH, EINTERNAL = range(7)
+OK, EINVAL, ECUDA, ENODEVICE, ECAPACITY, EMESH, EINTERNAL, ECDT = range(8)
 STATUS_NAMES = {0: "OK", 1: "EINVAL", 2: "ECUDA", 3: "ENODEVICE", 4: "ECAPACITY", 5: "EMESH",
-                6: "EINTERNAL"}
+                6: "EINTERNAL", 7: "ECDT"}
 RUPPERT, CHEW = 0, 1
 CAND_SUBSEG, CAND_TRI = 0, 1
 BAND_CIRCUMCENTER, BAND_MIDPOINT = 0, 1
@@ -93,6 +93,18 @@ class NodeEle(C.Structure):
                 ("tri", C.POINTER(C.c_uint32))]
 
 
+class CdtReport(C.Structure):
+    _fields_ = [("struct_size", C.c_uint32), ("n_triangles", C.c_uint32),
+                ("n_subsegments", C.c_uint32), ("insert_rounds", C.c_uint32),
+                ("flip_rounds", C.c_uint32), ("recover_rounds", C.c_uint32),
+                ("segments_present", C.c_uint32), ("pipes_recovered", C.c_uint32),
+                ("collinear_splits", C.c_uint32), ("max_pipe", C.c_uint32),
+                ("final_flip_rounds", C.c_uint32), ("reserved", C.c_uint32),
+                ("flips", C.c_uint64), ("seconds", C.c_double),
+                ("delaunay_seconds", C.c_double), ("recover_seconds", C.c_double),
+                ("finish_seconds", C.c_double)]
+
+
 class Candidate(C.Structure):
     _fields_ = [("x", C.c_double), ("y", C.c_double), ("measure", C.c_double),
                 ("id", C.c_uint32), ("tiebreak", C.c_uint32), ("located", C.c_uint32),
@@ -108,7 +120,8 @@ def candidate_dtype():
                      ("alive", "u1"), ("fallback", "u1")])
 
 
-STRUCTS = [MeshView, MeshBuf, Params, BatchMetrics, Report, Candidate, Validation, NodeEle]
+STRUCTS = [MeshView, MeshBuf, Params, BatchMetrics, Report, Candidate, Validation, NodeEle,
+           CdtReport]
 
 # Every entry point of include/gdp2d.h: name -> (restype, argtypes)
 ctx_p = C.c_void_p
@@ -121,6 +134,10 @@ SIGNATURES = {
     "gdp2d_pinned_free": (None, [C.c_void_p]),
     "gdp2d_ctx_validate": (C.c_int, [ctx_p, C.POINTER(Params), C.POINTER(Validation)]),
     "gdp2d_ctx_export": (C.c_int, [ctx_p, C.POINTER(NodeEle)]),
+    "gdp2d_ctx_build_cdt": (C.c_int, [ctx_p, C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint32,
+                                      C.POINTER(CdtReport)]),
+    "gdp2d_build_cdt": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint32,
+                                  C.POINTER(MeshBuf), C.POINTER(CdtReport), C.c_int]),
     "gdp2d_last_error": (C.c_char_p, []),
     "gdp2d_version": (C.c_char_p, []),
     "gdp2d_struct_size": (C.c_size_t, [C.c_int]),
@@ -158,6 +175,8 @@ HOST_SIGNATURES = {
     "gdp2d_host_build_cdt": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint32, C.c_int,
                                        C.POINTER(MeshBuf), C.POINTER(u32p),
                                        C.POINTER(C.c_uint32)]),
+    "gdp2d_host_close_hull": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint32, C.c_int,
+                                        C.POINTER(u32p), C.POINTER(C.c_uint32)]),
     "gdp2d_host_read_poly": (C.c_int, [C.c_char_p, C.POINTER(f64p), C.POINTER(C.c_uint32),
                                        C.POINTER(u32p), C.POINTER(C.c_uint32)]),
     "gdp2d_host_write_node_ele": (C.c_int, [C.POINTER(MeshView), C.POINTER(C.c_char_p),

@@ -205,6 +205,11 @@ const char* dev_err_name(u32 c) {
         case DERR_OPEN_STAR: return "open star around a free vertex";
         case DERR_STALE: return "stale handle";
         case DERR_WALK: return "walk failure";
+        case DERR_DUPLICATE: return "duplicate point";
+        case DERR_SEG_CROSS: return "input segments cross";
+        case DERR_CDT: return "CDT construction did not converge";
+        case DERR_NONFINITE: return "non-finite coordinate";
+        case DERR_SEG_VERTEX: return "degenerate pipe vertex";
         default: return "unknown device error";
     }
 }
@@ -360,6 +365,20 @@ struct gdp2d_ctx {
     u32* d_val = nullptr;
     const char* phase = "";
     cudaEvent_t ev[GDP2D_NPHASES + 4];   // phases, loop start/end, scan start/end
+    // device CDT builder (k_cdt.cu) scratch
+    struct {
+        u32* ptri = nullptr; int8_t* pedge = nullptr; u32* pother = nullptr; u64* pkey = nullptr;
+        uint8_t* pwin = nullptr; u32 ncap = 0;
+        u64* tkey = nullptr; u32* newid = nullptr; u32 tcap = 0;
+        uint2* pc = nullptr; u32* ppar = nullptr; u32* plist[2] = {nullptr, nullptr};
+        u32* poff = nullptr; u32* plen = nullptr; u32* plive = nullptr; u32* pmap = nullptr;
+        u32 pcap = 0;
+        u32* claims = nullptr; u32 claim_cap = 0;
+        u32* seeds = nullptr; u32 seed_cap = 0;
+        CdtLocal* pool = nullptr; uint2* queue = nullptr; u32 pool_cap = 0;
+        u32* part = nullptr; u32 part_cap = 0;
+        RoundCtr* ring = nullptr; u32* state = nullptr; ull* bbox = nullptr;
+    } cdt;
     // upload / download staging
     u32* stage_u32[3] = {nullptr, nullptr, nullptr};
     uint8_t* stage_u8 = nullptr;
@@ -508,7 +527,10 @@ void raise_dev_err(gdp2d_ctx* x) {
                  "device error %u (%s), info %u, dbg [%.17g %.17g %.17g %.17g %.17g %.17g %.17g %.17g]",
                  x->h_ctr->err_code, dev_err_name(x->h_ctr->err_code), x->h_ctr->err_info, d[0],
                  d[1], d[2], d[3], d[4], d[5], d[6], d[7]);
-        throw Fail{x->h_ctr->err_code == DERR_WORKLIST_OVERFLOW ? GDP2D_ECAPACITY : GDP2D_EMESH,
+        const u32 ec = x->h_ctr->err_code;
+        throw Fail{ec == DERR_WORKLIST_OVERFLOW ? GDP2D_ECAPACITY
+                   : ec >= DERR_DUPLICATE       ? GDP2D_ECDT
+                                                : GDP2D_EMESH,
                    buf};
     }
 }
@@ -660,6 +682,14 @@ void ctx_release(gdp2d_ctx* x) {
     dfree(x->ring);
     dfree(x->d_C);
     dfree(x->scan_part);
+    {
+        auto& c = x->cdt;
+        dfree(c.ptri); dfree(c.pedge); dfree(c.pother); dfree(c.pkey); dfree(c.pwin);
+        dfree(c.tkey); dfree(c.newid); dfree(c.pc); dfree(c.ppar); dfree(c.plist[0]);
+        dfree(c.plist[1]); dfree(c.poff); dfree(c.plen); dfree(c.plive); dfree(c.pmap);
+        dfree(c.claims); dfree(c.seeds); dfree(c.pool); dfree(c.queue); dfree(c.part);
+        dfree(c.ring); dfree(c.state); dfree(c.bbox);
+    }
     if (x->sel_state) cudaFree(x->sel_state);
     dfree(x->in_sv);
     if (x->vscratch) cudaFree(x->vscratch);
@@ -1239,6 +1269,299 @@ void fill_summary(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
 
 }  // namespace
 
+
+// ---- Line 1 on the device (k_cdt.cu) ------------------------------------------------
+
+namespace {
+
+template <class T>
+void cdt_grow(T*& p, u32& cap, size_t n) {
+    (void)cap;
+    dfree(p);
+    dalloc(p, n);
+}
+
+void build_cdt(gdp2d_ctx* x, const double* xy, u32 N, const u32* seg, u32 M,
+               gdp2d_cdt_report* rep) {
+    if (N < 3) throw Fail{GDP2D_ECDT, "need at least 3 points"};
+    if (!xy || (M && !seg)) throw Fail{GDP2D_EINVAL, "missing point / segment arrays"};
+    if (N >= (1u << 29) - 8) throw Fail{GDP2D_EINVAL, "too many points"};
+    for (u32 i = 0; i < M; ++i) {
+        const u32 a = seg[2 * i], b = seg[2 * i + 1];
+        if (a >= N || b >= N) throw Fail{GDP2D_EINVAL, "segment endpoint out of range"};
+        if (a == b) throw Fail{GDP2D_ECDT, "degenerate segment"};
+    }
+    cudaStream_t st = x->st;
+    auto& c = x->cdt;
+    const u32 T = 2 * N + 1;          // triangles of the DT of N points inside the super triangle
+    const u32 pcap = 2 * M + 1024;    // pieces (segments + collinear splits)
+    cudaEvent_t e0, e1, e2, e3;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventCreate(&e2));
+    CK(cudaEventCreate(&e3));
+    struct EvFree {
+        cudaEvent_t* e;
+        ~EvFree() { for (int i = 0; i < 4; ++i) cudaEventDestroy(e[i]); }
+    };
+    cudaEvent_t evs[4] = {e0, e1, e2, e3};
+    EvFree evfree{evs};
+    CK(cudaEventRecord(e0, st));
+
+    // working mesh: the DT of the points + super triangle
+    MeshStore& w = x->work;
+    w.m.nV = w.m.nT = w.m.nS = 0;
+    mesh_reserve(w, N + 3, T, pcap, st);
+    ensure_aux(x);
+    ensure_worklists(x, 3ull * T + (1u << 20));
+    DevMesh& m = w.m;
+    CK(cudaMemcpyAsync(m.xy, xy, 16ull * N, cudaMemcpyHostToDevice, st));
+    if (c.bbox == nullptr) {
+        dalloc(c.bbox, 4);
+        dalloc(c.ring, 4);
+        dalloc(c.state, 16);
+    }
+    CK(cudaMemsetAsync(x->d_ctr, 0, sizeof(Counters), st));
+    launch_cdt_bbox(m.xy, N, c.bbox, x->d_ctr, st);
+    ull hb[4];
+    CK(cudaMemcpyAsync(hb, c.bbox, sizeof hb, cudaMemcpyDeviceToHost, st));
+    check_dev_err(x);   // synchronises
+    const auto unkey = [](ull k) {
+        const ull b = (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
+        double d;
+        std::memcpy(&d, &b, 8);
+        return d;
+    };
+    const double x0 = unkey(hb[0]), y0 = unkey(hb[1]), x1 = unkey(hb[2]), y1 = unkey(hb[3]);
+    const double R = std::max(x1 - x0, y1 - y0);
+    if (!(R > 0)) throw Fail{GDP2D_ECDT, "duplicate point"};
+    const double cx = 0.5 * (x0 + x1), cy = 0.5 * (y0 + y1), K = 32.0 * R;
+    const double2 sup[3] = {make_double2(cx - K, cy - K), make_double2(cx + K, cy - K),
+                            make_double2(cx, cy + K)};
+    CK(cudaMemcpyAsync(m.xy + N, sup, sizeof sup, cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(m.vkind, 0, N + 3, st));
+    CK(cudaMemsetAsync(m.vbirth, 0, 4ull * (N + 3), st));
+    CK(cudaMemsetAsync(m.valive, 1, N + 3, st));
+    CK(cudaMemsetAsync(m.vtri, 0xFF, 4ull * (N + 3), st));
+    const uint4 t0v[3] = {make_uint4(N, N + 1, N + 2, 1u), make_uint4(NONE, NONE, NONE, 0u),
+                          make_uint4(NONE, NONE, NONE, 0u)};
+    CK(cudaMemcpyAsync(m.tv, &t0v[0], 16, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(m.tn, &t0v[1], 16, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(m.ts, &t0v[2], 16, cudaMemcpyHostToDevice, st));
+    m.nV = N + 3;
+    m.nT = T;
+    m.nS = 0;
+
+    // builder scratch
+    if (N > c.ncap) {
+        const u32 n2 = N + N / 4 + 1024;
+        cdt_grow(c.ptri, c.ncap, n2);
+        cdt_grow(c.pedge, c.ncap, n2);
+        cdt_grow(c.pother, c.ncap, n2);
+        cdt_grow(c.pkey, c.ncap, n2);
+        cdt_grow(c.pwin, c.ncap, n2);
+        c.ncap = n2;
+    }
+    if (T > c.tcap) {
+        const u32 t2 = T + T / 4 + 1024;
+        cdt_grow(c.tkey, c.tcap, t2);
+        cdt_grow(c.newid, c.tcap, t2);
+        cdt_grow(c.pool, c.tcap, t2);
+        cdt_grow(c.queue, c.tcap, t2);
+        c.pool_cap = t2;
+        const u32 cc2 = 2 * t2 + (1u << 20);
+        cdt_grow(c.claims, c.claim_cap, cc2);
+        c.claim_cap = cc2;
+        const u32 sc2 = 3 * t2 + (1u << 20);
+        cdt_grow(c.seeds, c.seed_cap, sc2);
+        c.seed_cap = sc2;
+        c.tcap = t2;
+    }
+    if (pcap > c.pcap) {
+        cdt_grow(c.pc, c.pcap, pcap);
+        cdt_grow(c.ppar, c.pcap, pcap);
+        cdt_grow(c.plist[0], c.pcap, pcap);
+        cdt_grow(c.plist[1], c.pcap, pcap);
+        cdt_grow(c.poff, c.pcap, pcap);
+        cdt_grow(c.plen, c.pcap, pcap);
+        cdt_grow(c.plive, c.pcap, pcap);
+        cdt_grow(c.pmap, c.pcap, pcap);
+        c.pcap = pcap;
+    }
+    const int g1 = cdt_grid(x->device, 0), g2 = cdt_grid(x->device, 1);
+    if ((u32)std::max(g1, g2) > c.part_cap) {
+        c.part_cap = (u32)std::max(g1, g2);
+        dfree(c.part);
+        dalloc(c.part, c.part_cap);
+    }
+    CK(cudaMemsetAsync(c.tkey, 0xFF, 8ull * T, st));
+    CK(cudaMemsetAsync(c.ring, 0, 4 * sizeof(RoundCtr), st));
+    CK(cudaMemsetAsync(c.state, 0, 16 * sizeof(u32), st));
+
+    CdtArgs a{};
+    a.m = m;
+    a.N = N;
+    a.x = x->aux;
+    a.w = x->wl;
+    a.w.vdirty = nullptr;
+    a.w.fresh_n = 0;
+    a.ring = c.ring;
+    a.state = c.state;
+    a.ctr = x->d_ctr;
+    a.round0 = x->round + 1;
+    a.ptri = c.ptri;
+    a.pedge = c.pedge;
+    a.pother = c.pother;
+    a.pkey = c.pkey;
+    a.pwin = c.pwin;
+    a.tkey = c.tkey;
+    a.part = c.part;
+    a.pc = c.pc;
+    a.ppar = c.ppar;
+    a.plist[0] = c.plist[0];
+    a.plist[1] = c.plist[1];
+    a.poff = c.poff;
+    a.plen = c.plen;
+    a.claims = c.claims;
+    a.seeds = c.seeds;
+    a.pool = c.pool;
+    a.queue = c.queue;
+    a.pcap = c.pcap;
+    a.claim_cap = c.claim_cap;
+    a.seed_cap = c.seed_cap;
+    a.pool_cap = c.pool_cap;
+
+    // 1. Delaunay triangulation (one persistent launch)
+    launch_cdt_delaunay(a, g1, st);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(e1, st));
+    u32 hs[16];
+    CK(cudaMemcpyAsync(hs, c.state, sizeof hs, cudaMemcpyDeviceToHost, st));
+    check_dev_err(x);
+    if (hs[0] != T) throw Fail{GDP2D_ECDT, "CDT insertion rounds stopped early"};
+    const u32 ins_rounds = hs[CDT_ST_ROUNDS], ins_flip_rounds = hs[CDT_ST_FLIP_ROUNDS];
+    x->round += hs[CDT_ST_STEPS] + 8;
+
+    // 2. segment recovery
+    u32 np = M, found = 0, pipes = 0, splits = 0, rec_rounds = 0, pmax = 0, nseeds = 0;
+    if (M) {
+        std::vector<u32> iota(M);
+        for (u32 i = 0; i < M; ++i) iota[i] = i;
+        CK(cudaMemcpyAsync(c.pc, seg, 8ull * M, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(c.ppar, iota.data(), 4ull * M, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(c.plist[0], iota.data(), 4ull * M, cudaMemcpyHostToDevice, st));
+        CK(cudaMemsetAsync(c.ring, 0, 4 * sizeof(RoundCtr), st));
+        CK(cudaMemsetAsync(c.state, 0, 16 * sizeof(u32), st));
+        CK(cudaMemcpyAsync(c.state + CDT_ST_NPIECES, &M, 4, cudaMemcpyHostToDevice, st));
+        a.round0 = x->round + 1;
+        launch_cdt_recover(a, M, g2, st);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(hs, c.state, sizeof hs, cudaMemcpyDeviceToHost, st));
+        check_dev_err(x);   // synchronises (iota stays alive until here)
+        np = hs[CDT_ST_NPIECES];
+        found = hs[CDT_ST_FOUND];
+        pipes = hs[CDT_ST_PIPES];
+        splits = hs[CDT_ST_SPLITS];
+        rec_rounds = hs[CDT_ST_RECOVER_ROUNDS];
+        pmax = hs[CDT_ST_PIPE_MAX];
+        nseeds = std::min(hs[CDT_ST_SEEDS], c.seed_cap);
+        x->round += hs[12] + 8;
+    }
+    CK(cudaEventRecord(e2, st));
+
+    // 3. cut away the super triangle's fan; constrained Lawson from the pipes
+    launch_cdt_strip(m, N, st);
+    u32 fin_rounds = 0;
+    if (nseeds) {
+        CK(cudaMemcpyAsync(x->wl.w[0], c.seeds, 4ull * nseeds, cudaMemcpyDeviceToDevice, st));
+        lawson_from(x, 0, nseeds, &fin_rounds);
+        check_dev_err(x);
+    }
+    // subsegment ids: live pieces in (segment, position along it) order
+    u32 nS = 0;
+    CK(cudaMemsetAsync(c.plive, 0, 4ull * np, st));
+    launch_cdt_piece_live(m, c.plive, st);
+    if (splits == 0) {
+        u32* d_tot = x->d_res;
+        scan_exclusive(c.plive, c.newid, np, d_tot, x->scan, st);
+        launch_cdt_pmap(c.plive, c.newid, c.pmap, np, st);
+        CK(cudaMemcpyAsync(&nS, d_tot, 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    } else {
+        std::vector<uint2> hpc(np);
+        std::vector<u32> hpar(np), hlive(np), hmap(np, NONE);
+        CK(cudaMemcpyAsync(hpc.data(), c.pc, 8ull * np, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(hpar.data(), c.ppar, 4ull * np, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(hlive.data(), c.plive, 4ull * np, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        std::vector<std::pair<std::pair<u32, double>, u32>> order;
+        for (u32 p = 0; p < np; ++p) {
+            if (!hlive[p]) continue;
+            const u32 par = hpar[p];
+            const u32 sa = seg[2 * par], sb = seg[2 * par + 1], u = hpc[p].x;
+            const double dx = xy[2 * sb] - xy[2 * sa], dy = xy[2 * sb + 1] - xy[2 * sa + 1];
+            const double t = (xy[2 * u] - xy[2 * sa]) * dx + (xy[2 * u + 1] - xy[2 * sa + 1]) * dy;
+            order.push_back({{par, t}, p});
+        }
+        std::sort(order.begin(), order.end());
+        for (const auto& o : order) hmap[o.second] = nS++;
+        CK(cudaMemcpyAsync(c.pmap, hmap.data(), 4ull * np, cudaMemcpyHostToDevice, st));
+        CK(cudaStreamSynchronize(st));
+    }
+    // compaction into the context's input mesh
+    launch_alive_flags(m, c.newid, st);
+    // newid doubles as the flag array: scan in place is not supported, use the pool
+    u32* flags = reinterpret_cast<u32*>(c.pool);
+    CK(cudaMemcpyAsync(flags, c.newid, 4ull * T, cudaMemcpyDeviceToDevice, st));
+    scan_exclusive(flags, c.newid, T, x->d_res, x->scan, st);
+    u32 nTf = 0;
+    CK(cudaMemcpyAsync(&nTf, x->d_res, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (nTf == 0) throw Fail{GDP2D_ECDT, "all points collinear"};
+    MeshStore& pr = x->pristine;
+    pr.m.nV = pr.m.nT = pr.m.nS = 0;
+    mesh_reserve(pr, N, nTf, std::max<u32>(nS, 1), st);
+    pr.m.nV = N;
+    pr.m.nT = nTf;
+    pr.m.nS = nS;
+    launch_cdt_compact(m, pr.m, N, c.newid, c.pc, c.ppar, c.pmap, np, st);
+    CK(cudaGetLastError());
+    x->pristine_epoch = 0;
+    x->p_alive_v = N;
+    x->p_alive_t = nTf;
+    x->p_alive_s = nS;
+    x->n_in = 0;
+    x->in_valid = false;
+    reset_work(x);
+    CK(cudaEventRecord(e3, st));
+    CK(cudaStreamSynchronize(st));
+    float ms01 = 0, ms12 = 0, ms23 = 0;
+    cudaEventElapsedTime(&ms01, e0, e1);
+    cudaEventElapsedTime(&ms12, e1, e2);
+    cudaEventElapsedTime(&ms23, e2, e3);
+    if (rep) {
+        rep->struct_size = sizeof(gdp2d_cdt_report);
+        rep->n_triangles = nTf;
+        rep->n_subsegments = nS;
+        rep->insert_rounds = ins_rounds;
+        rep->flip_rounds = ins_flip_rounds;
+        rep->recover_rounds = rec_rounds;
+        rep->segments_present = found;
+        rep->pipes_recovered = pipes;
+        rep->collinear_splits = splits;
+        rep->max_pipe = pmax;
+        rep->final_flip_rounds = fin_rounds;
+        rep->reserved = 0;
+        rep->flips = x->h_ctr->flips;
+        rep->delaunay_seconds = ms01 * 1e-3;
+        rep->recover_seconds = ms12 * 1e-3;
+        rep->finish_seconds = ms23 * 1e-3;
+        rep->seconds = (ms01 + ms12 + ms23) * 1e-3;
+    }
+}
+
+}  // namespace
+
 // ---------------------------------------------------------------------------
 // C ABI
 // ---------------------------------------------------------------------------
@@ -1358,6 +1681,7 @@ size_t gdp2d_struct_size(int which) {
         case 5: return sizeof(gdp2d_candidate);
         case 6: return sizeof(gdp2d_validation);
         case 7: return sizeof(gdp2d_node_ele);
+        case 8: return sizeof(gdp2d_cdt_report);
         default: return 0;
     }
 }
@@ -1614,6 +1938,31 @@ int gdp2d_ctx_validate(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_validation* ou
         out->bad_triangles = v.bad_triangles;
         out->conformity_failures = v.conformity_failures;
         out->min_angle_deg = v.min_angle_deg;
+    });
+}
+
+int gdp2d_ctx_build_cdt(gdp2d_ctx* x, const double* xy, uint32_t n_points, const uint32_t* seg,
+                        uint32_t n_segments, gdp2d_cdt_report* rep) {
+    if (!x) return GDP2D_EINVAL;
+    DeviceGuard g(x->device);
+    return run_guarded([&] { build_cdt(x, xy, n_points, seg, n_segments, rep); });
+}
+
+int gdp2d_build_cdt(const double* xy, uint32_t n_points, const uint32_t* seg,
+                    uint32_t n_segments, gdp2d_mesh_buf* out, gdp2d_cdt_report* rep,
+                    int device) {
+    if (!out) return GDP2D_EINVAL;
+    if (device < 0 || device >= kMaxDevices) return GDP2D_ENODEVICE;
+    std::lock_guard<std::mutex> lock(g_cache_mu[device]);
+    if (!g_cache[device]) {
+        const int rc = gdp2d_ctx_create(&g_cache[device], device);
+        if (rc) return rc;
+    }
+    gdp2d_ctx* x = g_cache[device];
+    return run_guarded([&] {
+        DeviceGuard g(x->device);
+        build_cdt(x, xy, n_points, seg, n_segments, rep);
+        download(x, out);
     });
 }
 

@@ -242,6 +242,63 @@ void launch_export(const DevMesh& m, u32* fv, u32* ov, u32* ft, u32* ot, double2
 // Debug structural validator (out: 4 u32 device words).
 void launch_validate(const DevMesh& m, u32* out, cudaStream_t st);
 
+// Line 1 on the device (k_cdt.cu): Delaunay triangulation of the input
+// points inside a super triangle (vertices N..N+2), then segment recovery by
+// pipe flips, removal of the super triangle and a constrained Lawson pass.
+struct CdtLocal {          // one triangle of a pipe being re-triangulated
+    uint4 v;               // corners (w unused)
+    uint4 n;               // neighbours: local (j<<2|e) where bit e of n.w is set, else global code
+    uint4 s;               // subsegment (piece id) per edge
+    uint4 o;               // original (tri<<2|edge) of an outer edge (emap key)
+};
+struct CdtArgs {
+    DevMesh m;             // work mesh; nT = triangle capacity (2N+1)
+    u32 N;                 // input points (vertices 0..N-1)
+    TriAux x;
+    WorkLists w;           // vdirty = null
+    RoundCtr* ring;        // [4]
+    u32* state;            // [16], see k_cdt.cu
+    Counters* ctr;
+    u32 round0;
+    // points
+    u32* ptri;             // containing triangle, NONE once inserted
+    int8_t* pedge;         // -1 inside, else the edge the point lies on
+    u32* pother;           // far triangle claimed by an on-edge point
+    u64* pkey;             // pick key (distance to the circumcircle centre, index)
+    uint8_t* pwin;
+    u64* tkey;             // per-triangle pick slot (~0 when free)
+    u32* part;             // [grid] chunk sums
+    // segment recovery: pieces are (sub)segments still to be recovered
+    uint2* pc;             // piece endpoints
+    u32* ppar;             // input segment the piece belongs to
+    u32* plist[2];         // active piece lists
+    u32* poff;             // claim-log offset of the piece's pipe
+    u32* plen;             // pipe length (triangles)
+    u32* claims;           // claim log (pipe triangles)
+    u32* seeds;            // Lawson seeds (edge codes) of re-triangulated pipes
+    CdtLocal* pool;        // per-pipe scratch (pipes of a round are disjoint)
+    uint2* queue;          // per-pipe crossing-edge ring
+    u32 pcap, claim_cap, seed_cap, pool_cap;
+};
+constexpr int CDT_BLOCK = 256;
+enum : u32 { CDT_ST_ROUNDS = 1, CDT_ST_FLIP_ROUNDS = 2, CDT_ST_STEPS = 3, CDT_ST_RECOVER_ROUNDS = 4,
+             CDT_ST_NPIECES = 5, CDT_ST_FOUND = 6, CDT_ST_PIPES = 7, CDT_ST_SPLITS = 8,
+             CDT_ST_SEEDS = 9, CDT_ST_POOL = 10, CDT_ST_PIPE_MAX = 11 };
+int cdt_grid(int device, int which);
+void launch_cdt_delaunay(const CdtArgs& a, int grid, cudaStream_t st);
+void launch_cdt_recover(const CdtArgs& a, u32 n_pieces, int grid, cudaStream_t st);
+// super-triangle removal: unlink (pass 0) then kill (pass 1)
+void launch_cdt_strip(const DevMesh& m, u32 N, cudaStream_t st);
+void launch_cdt_bbox(const double2* xy, u32 n, ull* out4, Counters* ctr, cudaStream_t st);
+// compaction of the work mesh into dst (alive triangles renumbered, pieces
+// mapped through pmap), vertex/subsegment records rebuilt
+void launch_cdt_piece_live(const DevMesh& m, u32* plive, cudaStream_t st);
+void launch_cdt_compact(const DevMesh& src, DevMesh dst, u32 N, const u32* newid,
+                        const uint2* pc, const u32* ppar, const u32* pmap, u32 npieces,
+                        cudaStream_t st);
+void launch_alive_flags(const DevMesh& m, u32* flags, cudaStream_t st);
+void launch_cdt_pmap(const u32* plive, const u32* pre, u32* pmap, u32 n, cudaStream_t st);
+
 // Upload helpers.
 void launch_encode_neighbors(DevMesh m, const u32* plain_n, cudaStream_t st);
 void launch_decode_neighbors(const DevMesh& m, u32* plain_n, cudaStream_t st);

@@ -128,6 +128,11 @@ enum DevErr : u32 {
     DERR_OPEN_STAR = 5,
     DERR_STALE = 6,
     DERR_WALK = 7,
+    DERR_DUPLICATE = 8,     // CDT: two input points coincide
+    DERR_SEG_CROSS = 9,     // CDT: input segments cross
+    DERR_CDT = 10,          // CDT: walk / recovery did not converge
+    DERR_NONFINITE = 11,    // CDT: non-finite coordinate
+    DERR_SEG_VERTEX = 12,   // CDT: a segment passes through a vertex at its end (degenerate pipe)
 };
 
 __device__ __forceinline__ void raise_err(Counters* c, u32 code, u32 info) {

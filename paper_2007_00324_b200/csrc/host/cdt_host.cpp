@@ -147,6 +147,30 @@ int gdp2d_host_build_cdt(const double* xy, uint32_t n, const uint32_t* segs, uin
     }
 }
 
+// close_hull (cdt.hpp:447) [+ check_crossings]: the segment list the device
+// CDT builder (gdp2d_ctx_build_cdt) takes.
+int gdp2d_host_close_hull(const double* xy, uint32_t n, const uint32_t* segs, uint32_t m,
+                          int check, uint32_t** segs_out, uint32_t* m_out) {
+    try {
+        Pslg g;
+        g.points.resize(n);
+        for (uint32_t i = 0; i < n; ++i) g.points[i] = {xy[2 * i], xy[2 * i + 1]};
+        for (uint32_t i = 0; i < m; ++i) g.segments.emplace_back(segs[2 * i], segs[2 * i + 1]);
+        g = close_hull(std::move(g));
+        if (check) detail::check_crossings(g);
+        *m_out = (uint32_t)g.segments.size();
+        *segs_out = static_cast<uint32_t*>(std::malloc(8 * (g.segments.size() + 1)));
+        for (size_t i = 0; i < g.segments.size(); ++i) {
+            (*segs_out)[2 * i] = g.segments[i].first;
+            (*segs_out)[2 * i + 1] = g.segments[i].second;
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
 // read_poly (pslg_io.hpp:272): text -> closed PSLG.
 int gdp2d_host_read_poly(const char* text, double** xy, uint32_t* n, uint32_t** segs,
                          uint32_t* m) {

@@ -21,6 +21,7 @@
 #include <algorithm>
 
 #include "gdp2d_phases.cuh"
+#include "gdp2d_rewrite.cuh"
 #include "scan.cuh"
 
 namespace cg = cooperative_groups;
@@ -35,135 +36,6 @@ namespace cg = cooperative_groups;
 #endif
 
 namespace gdp2d {
-
-// ---- shared phase-A helpers ----------------------------------------------------
-
-__device__ __forceinline__ void write_tri(const DevMesh& m, u32 t, u32 a, u32 b, u32 c, u32 n0,
-                                          u32 n1, u32 n2, u32 pend, u32 s0, u32 s1, u32 s2) {
-    m.tv[t] = make_uint4(a, b, c, 1u);
-    m.tn[t] = make_uint4(n0, n1, n2, pend);
-    m.ts[t] = make_uint4(s0, s1, s2, 0u);
-    m.tflag[t] = 2;
-    m.vtri[a] = NONE;
-    m.vtri[b] = NONE;
-    m.vtri[c] = NONE;
-    if (s0 != NONE) m.stri[s0] = NONE, m.sflag[s0] = 2;
-    if (s1 != NONE) m.stri[s1] = NONE, m.sflag[s1] = 2;
-    if (s2 != NONE) m.stri[s2] = NONE, m.sflag[s2] = 2;
-}
-
-__device__ __forceinline__ void push_touched(const WorkLists& w, const u32* ts, int k,
-                                             RoundCtr* rc = nullptr) {
-    const u32 o = agg_reserve(&(rc ? rc : w.rc)->touched, (u32)k);
-    for (int j = 0; j < k; ++j)
-        if (o + j < w.cap) w.touched[o + j] = ts[j];
-}
-
-__device__ __forceinline__ void push_work(const WorkLists& w, u32 widx, const u32* codes, int k,
-                                          Counters* ctr, RoundCtr* rc = nullptr) {
-    const u32 o = agg_reserve(&(rc ? rc : w.rc)->wl_next, (u32)k);
-    if (o + k > w.cap) {
-        raise_err(ctr, DERR_WORKLIST_OVERFLOW, o);
-        return;
-    }
-    for (int j = 0; j < k; ++j) w.w[widx][o + j] = codes[j];
-}
-
-// split_triangle_with (mesh.hpp:323-346): t := (a,b,w), t1 := (b,c,w), t2 := (c,a,w).
-// seed != 0: push the three link edges (opposite wv) as Lawson seeds.  The
-// spokes (wv, a) need no test: an empty circle through wv and a exists inside
-// the old circumcircle, so they are Delaunay edges (Lawson insertion); the
-// flips that later change a spoke's quad push it again (flip_apply_one).
-__device__ void split_triangle_A(const DevMesh& m, const TriAux& x, const WorkLists& w, u32 t,
-                                 u32 wv, u32 t1, u32 t2, u32 round, RoundCtr* rc = nullptr,
-                                 int seed = 0, Counters* ctr = nullptr) {
-    const uint4 ov = m.tv[t], on = m.tn[t], os = m.ts[t];
-    x.stamp[t] = round;
-    write_tri(m, t, ov.x, ov.y, wv, enc(t1, 1), enc(t2, 0), on.z, 4u, NONE, NONE, os.z);
-    write_tri(m, t1, ov.y, ov.z, wv, enc(t2, 1), enc(t, 0), on.x, 4u, NONE, NONE, os.x);
-    write_tri(m, t2, ov.z, ov.x, wv, enc(t, 1), enc(t1, 0), on.y, 4u, NONE, NONE, os.y);
-    x.emap[3 * t + 0] = enc(t1, 2);
-    x.emap[3 * t + 1] = enc(t2, 2);
-    x.emap[3 * t + 2] = enc(t, 2);
-    m.vtri[wv] = NONE;
-    const u32 tl[3] = {t, t1, t2};
-    push_touched(w, tl, 3, rc);
-    if (seed) {
-        const u32 codes[3] = {enc(t, 2), enc(t1, 2), enc(t2, 2)};
-        push_work(w, 0, codes, 3, ctr, rc);
-    }
-}
-
-// split_edge_with (mesh.hpp:358-401) on edge e of t; new t2 (and u2 when the
-// edge has a far side).  s_bw / s_wc are the child subsegments or NONE.
-// seed != 0: push every edge of the new triangles (a point on an edge gets no
-// empty-circle guarantee for the edge halves).
-__device__ void split_edge_A(const DevMesh& m, const TriAux& x, const WorkLists& w, u32 t, int e,
-                             u32 wv, u32 t2, u32 u2, u32 s_bw, u32 s_wc, u32 round,
-                             RoundCtr* rc = nullptr, int seed = 0, Counters* ctr = nullptr) {
-    const uint4 ov = m.tv[t], on = m.tn[t], os = m.ts[t];
-    const u32 a = comp(ov, e), b = comp(ov, nxt(e)), c = comp(ov, prv(e));
-    const u32 uc = comp(on, e);
-    x.stamp[t] = round;
-    if (uc == NONE) {
-        // t := (a,b,w) {-, t2, n_prev}, t2 := (a,w,c) {-, n_next, t}
-        write_tri(m, t, a, b, wv, NONE, enc(t2, 2), comp(on, prv(e)), 4u, s_bw, NONE,
-                  comp(os, prv(e)));
-        write_tri(m, t2, a, wv, c, NONE, comp(on, nxt(e)), enc(t, 1), 2u, s_wc,
-                  comp(os, nxt(e)), NONE);
-        x.emap[3 * t + nxt(e)] = enc(t2, 1);
-        x.emap[3 * t + prv(e)] = enc(t, 2);
-        x.emap[3 * t + e] = NONE;
-        m.vtri[wv] = NONE;
-        const u32 tl[2] = {t, t2};
-        push_touched(w, tl, 2, rc);
-        if (seed && s_bw != NONE) {
-            const u32 codes[2] = {enc(t, 2), enc(t2, 1)};
-            push_work(w, 0, codes, 2, ctr, rc);
-        } else if (seed) {
-            const u32 codes[6] = {enc(t, 0), enc(t, 1), enc(t, 2), enc(t2, 0), enc(t2, 1),
-                                  enc(t2, 2)};
-            push_work(w, 0, codes, 6, ctr, rc);
-        }
-        return;
-    }
-    const u32 u = etri(uc);
-    const int f = eidx(uc);
-    const uint4 uv = m.tv[u], un = m.tn[u], us = m.ts[u];
-    const u32 d = comp(uv, f);
-    x.stamp[u] = round;
-    // t := (a,b,w) {u2, t2, n_ab}; t2 := (a,w,c) {u, n_ca, t}
-    write_tri(m, t, a, b, wv, enc(u2, 0), enc(t2, 2), comp(on, prv(e)), 4u, s_bw, NONE,
-              comp(os, prv(e)));
-    write_tri(m, t2, a, wv, c, enc(u, 0), comp(on, nxt(e)), enc(t, 1), 2u, s_wc,
-              comp(os, nxt(e)), NONE);
-    // u := (d,c,w) {t2, u2, n_dc}; u2 := (d,w,b) {t, n_bd, u}
-    write_tri(m, u, d, c, wv, enc(t2, 0), enc(u2, 2), comp(un, prv(f)), 4u, s_wc, NONE,
-              comp(us, prv(f)));
-    write_tri(m, u2, d, wv, b, enc(t, 0), comp(un, nxt(f)), enc(u, 1), 2u, s_bw,
-              comp(us, nxt(f)), NONE);
-    x.emap[3 * t + nxt(e)] = enc(t2, 1);
-    x.emap[3 * t + prv(e)] = enc(t, 2);
-    x.emap[3 * t + e] = NONE;
-    x.emap[3 * u + prv(f)] = enc(u, 2);
-    x.emap[3 * u + nxt(f)] = enc(u2, 1);
-    x.emap[3 * u + f] = NONE;
-    m.vtri[wv] = NONE;
-    const u32 tl[4] = {t, t2, u, u2};
-    push_touched(w, tl, 4, rc);
-    if (seed && s_bw != NONE) {
-        // subsegment midpoint: the halves are constrained and the spokes
-        // (w,a), (w,d) are constrained-Delaunay (a circle through a and w
-        // inside the empty circumcircle of (a,b,c)); only the link edges
-        const u32 codes[4] = {enc(t, 2), enc(t2, 1), enc(u, 2), enc(u2, 1)};
-        push_work(w, 0, codes, 4, ctr, rc);
-    } else if (seed) {
-        const u32 codes[12] = {enc(t, 0), enc(t, 1), enc(t, 2), enc(t2, 0), enc(t2, 1),
-                               enc(t2, 2), enc(u, 0), enc(u, 1), enc(u, 2), enc(u2, 0),
-                               enc(u2, 1), enc(u2, 2)};
-        push_work(w, 0, codes, 12, ctr, rc);
-    }
-}
 
 // ---- planning + phase-1 splits ----------------------------------------------------
 
@@ -261,63 +133,6 @@ void launch_apply_splits(const DevMesh& m, DevCands c, u32 n, u32 batch, u32 rou
     note_launch(), k_apply_splits<<<(n + 255) / 256, 256, 0, st>>>(m, c, n, batch, round, b, a, f, w, d_ctr);
 }
 
-// ---- phase B ------------------------------------------------------------------------
-
-__device__ __forceinline__ void fixup_one(const DevMesh& m, u32 round, const TriAux& x,
-                                          const WorkLists& w, u32 t, int seed, u32 widx,
-                                          RoundCtr* rc, Counters* ctr) {
-    uint4 tn = m.tn[t];
-    const uint4 tv = m.tv[t];
-    const uint4 ts = m.ts[t];
-    if (!tv.w) return;
-    const u32 pend = tn.w;
-    u32* tn_words = reinterpret_cast<u32*>(m.tn);
-#pragma unroll
-    for (int e = 0; e < 3; ++e) {
-        if (!((pend >> e) & 1u)) continue;
-        const u32 r = comp(tn, e);
-        if (r == NONE) continue;
-        const u32 X = etri(r);
-        if (x.stamp[X] == round) {
-            set_comp(tn, e, x.emap[3 * X + eidx(r)]);
-        } else {
-            tn_words[4 * (size_t)X + eidx(r)] = enc(t, e);
-        }
-    }
-    tn.w = 0;
-    m.tn[t] = tn;
-    atomicMin(&m.vtri[tv.x], t);
-    atomicMin(&m.vtri[tv.y], t);
-    atomicMin(&m.vtri[tv.z], t);
-    if (w.vdirty) {
-        // Suspects for the redundancy detection (refine.hpp:551-608): a
-        // same-batch circumcenter can only be redundant as the apex of a
-        // subsegment, or dependent next to another same-batch circumcenter --
-        // both visible on one triangle, and every triangle around a fresh
-        // vertex passes through a fixup.  Only suspects are evaluated.
-        const u32 j0 = tv.x - w.fresh_v0, j1 = tv.y - w.fresh_v0, j2 = tv.z - w.fresh_v0;
-        const bool c0 = j0 < w.fresh_n && w.fresh_cc[j0];
-        const bool c1 = j1 < w.fresh_n && w.fresh_cc[j1];
-        const bool c2 = j2 < w.fresh_n && w.fresh_cc[j2];
-        const bool pair = (int)c0 + (int)c1 + (int)c2 >= 2;
-        if (c0 && (pair || ts.x != NONE)) w.vdirty[j0] = 1;
-        if (c1 && (pair || ts.y != NONE)) w.vdirty[j1] = 1;
-        if (c2 && (pair || ts.z != NONE)) w.vdirty[j2] = 1;
-    }
-#pragma unroll
-    for (int e = 0; e < 3; ++e) {
-        const u32 s = comp(ts, e);
-        if (s == NONE) continue;
-        const u32 r = comp(tn, e);
-        const u32 other = r == NONE ? NONE : etri(r);
-        atomicMin(&m.stri[s], min(t, other));
-    }
-    if (seed) {
-        const u32 codes[3] = {enc(t, 0), enc(t, 1), enc(t, 2)};
-        push_work(w, widx, codes, 3, ctr, rc);
-    }
-}
-
 __global__ void k_fixup(DevMesh m, u32 round, TriAux x, WorkLists w, u32 n_bound, int seed,
                         u32 widx, Counters* ctr) {
     const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -331,109 +146,6 @@ void launch_fixup(const DevMesh& m, u32 round, TriAux a, WorkLists w, u32 n_boun
     if (!n_bound) return;
     note_launch(), k_fixup<<<(n_bound + 255) / 256, 256, 0, st>>>(m, round, a, w, n_bound,
                                                    seed_all_edges ? 1 : 0, widx, d_ctr);
-}
-
-// ---- Lawson flip rounds (lawson_fixpoint cdt.hpp:111-123) -----------------------------
-
-// Test one work item (is_non_delaunay_edge mesh.hpp:430-437) on its canonical
-// side (lower triangle id) and claim both triangles with the edge code as key:
-// the minimum key wins, so a round's flip set is deterministic.
-__device__ __forceinline__ void flip_test_one(const DevMesh& m, u32 code, const TriAux& x,
-                                              const WorkLists& w, RoundCtr* rc, Counters* ctr) {
-    u32 t = etri(code);
-    int e = eidx(code);
-    if (t >= m.nT) return;
-    // record loads issued together: the dependent chain is t's record ->
-    // the neighbour's corners -> the four coordinates
-    const uint4 tv0 = m.tv[t], tn0 = m.tn[t], ts0 = m.ts[t];
-    if (!tv0.w) return;
-    const u32 c = comp(tn0, e);
-    if (c == NONE || comp(ts0, e) != NONE) return;
-    u32 u = etri(c);
-    int f = eidx(c);
-    const uint4 tvu = m.tv[u];
-    uint4 tv = tv0;
-    u32 d = comp(tvu, f);
-    if (u < t) {   // test on the canonical (lower id) side
-        d = comp(tv0, e);
-        tv = tvu;
-        const u32 tt = t;
-        const int ee = e;
-        t = u;
-        e = f;
-        u = tt;
-        f = ee;
-    }
-    if (incircle(m.xy[tv.x], m.xy[tv.y], m.xy[tv.z], m.xy[d]) <= 0) return;
-    const u32 key = enc(t, e);
-    atomicMin(&x.owner[t], key);
-    atomicMin(&x.owner[u], key);
-    const u32 o = agg_reserve(&rc->cand, 1u);
-    if (o < w.cap) {
-        w.fc[o] = key;
-        w.fu[o] = enc(u, f);
-    } else {
-        raise_err(ctr, DERR_WORKLIST_OVERFLOW, o);
-    }
-}
-
-// flip (mesh.hpp:210-258) as a phase-A rewrite: t := (a,b,d), u := (a,d,c).
-__device__ __forceinline__ u32 flip_apply_one(const DevMesh& m, u32 i, u32 round, u32 widx,
-                                              const TriAux& x, const WorkLists& w, RoundCtr* rc,
-                                              Counters* ctr) {
-    const u32 key = w.fc[i], uc = w.fu[i];
-    const u32 t = etri(key), u = etri(uc);
-    const int e = eidx(key), f = eidx(uc);
-    // the pair's records are loaded together with the claims; a duplicate
-    // work item (same key, all "win") that loses the stamp exchange below
-    // discards them, and the winner's reads precede any write to the pair
-    const u32 ot = x.owner[t], ou = x.owner[u];
-    const uint4 tv = m.tv[t], tn = m.tn[t], ts = m.ts[t];
-    const uint4 uv = m.tv[u], un = m.tn[u], us = m.ts[u];
-    const bool won = ot == key && ou == key;
-    w.fwin[i] = won;
-    // exactly one duplicate performs the flip
-    if (!won || atomicExch(&x.stamp[t], round) == round) return 0;
-    const u32 a = comp(tv, e), b = comp(tv, nxt(e)), c = comp(tv, prv(e));
-    const u32 d = comp(uv, f);
-    const double2 pa = m.xy[a], pb = m.xy[b], pc = m.xy[c], pd = m.xy[d];
-    x.stamp[u] = round;
-    if (orient2d(pa, pb, pd) <= 0 || orient2d(pa, pd, pc) <= 0) {
-        if (atomicCAS(&ctr->err_code, 0u, (u32)DERR_NONCONVEX_FLIP) == 0u) {
-            ctr->err_info = t;
-            ctr->dbg[0] = pa.x; ctr->dbg[1] = pa.y; ctr->dbg[2] = pb.x; ctr->dbg[3] = pb.y;
-            ctr->dbg[4] = pc.x; ctr->dbg[5] = pc.y; ctr->dbg[6] = pd.x; ctr->dbg[7] = pd.y;
-        }
-        return 0;
-    }
-    write_tri(m, t, a, b, d, comp(un, nxt(f)), enc(u, 2), comp(tn, prv(e)), 5u,
-              comp(us, nxt(f)), NONE, comp(ts, prv(e)));
-    write_tri(m, u, a, d, c, comp(un, prv(f)), comp(tn, nxt(e)), enc(t, 1), 3u,
-              comp(us, prv(f)), comp(ts, nxt(e)), NONE);
-    x.emap[3 * t + nxt(e)] = enc(u, 1);
-    x.emap[3 * t + prv(e)] = enc(t, 2);
-    x.emap[3 * t + e] = NONE;
-    x.emap[3 * u + nxt(f)] = enc(t, 0);
-    x.emap[3 * u + prv(f)] = enc(u, 0);
-    x.emap[3 * u + f] = NONE;
-    const u32 tl[2] = {t, u};
-    push_touched(w, tl, 2, rc);
-    const u32 codes[4] = {enc(t, 0), enc(t, 2), enc(u, 0), enc(u, 1)};
-    push_work(w, widx, codes, 4, ctr, rc);
-    return 1;
-}
-
-// Release claims; a loser whose triangles were both left untouched retries.
-__device__ __forceinline__ void flip_post_one(u32 i, u32 round, u32 widx, const TriAux& x,
-                                              const WorkLists& w, RoundCtr* rc, Counters* ctr) {
-    const u32 key = w.fc[i], uc = w.fu[i];
-    const u32 t = etri(key), u = etri(uc);
-    x.owner[t] = NONE;
-    x.owner[u] = NONE;
-    if (!w.fwin[i] && x.stamp[t] != round && x.stamp[u] != round) {
-        const u32 codes[1] = {key};
-        push_work(w, widx, codes, 1, ctr, rc);
-    }
 }
 
 __global__ void k_flip_test(DevMesh m, const u32* __restrict__ wl, u32 n, TriAux x, WorkLists w,

@@ -35,6 +35,11 @@ class CapacityExceeded(RuntimeError):
     """Device work-list capacity exceeded (cdtref::CapacityExceeded, expandlist.hpp:21)."""
 
 
+class CdtError(RuntimeError):
+    """The PSLG cannot be triangulated (cdtref::CdtError, cdt.hpp:20): duplicate
+    points, all points collinear, crossing segments, non-finite coordinates."""
+
+
 def _raise(rc: int, what: str = "") -> None:
     if rc == A.OK:
         return
@@ -44,6 +49,8 @@ def _raise(rc: int, what: str = "") -> None:
         raise MeshError(text)
     if rc == A.ECAPACITY:
         raise CapacityExceeded(text)
+    if rc == A.ECDT:
+        raise CdtError(text)
     raise RuntimeError(text)
 
 
@@ -388,6 +395,21 @@ def refine_c(m: Mesh, q: QualityCriteria, cfg: Optional[EngineConfig] = None) ->
 # ---- device-resident engine ---------------------------------------------------------
 
 
+def build_cdt(points: np.ndarray, segments: np.ndarray, device: int = 0):
+    """build_cdt (cdt.hpp:483) on the GPU: (Mesh, report).  ``segments`` must
+    already include the hull edges (host.close_hull / read_poly).  Raises
+    CdtError where the reference throws CdtError."""
+    lib = A.engine()
+    pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 2)
+    seg = np.ascontiguousarray(segments, dtype=np.uint32).reshape(-1, 2)
+    out = A.MeshBuf()
+    r = A.CdtReport()
+    _raise(lib.gdp2d_build_cdt(pts.ctypes.data, len(pts), seg.ctypes.data, len(seg),
+                               C.byref(out), C.byref(r), device), "gdp2d_build_cdt")
+    return (Mesh.from_buf(out, lib.gdp2d_free),
+            {name: getattr(r, name) for name, _ in A.CdtReport._fields_})
+
+
 class Engine:
     """One device context: a pristine copy of the input mesh and a working mesh in HBM."""
 
@@ -420,6 +442,17 @@ class Engine:
 
     def reset(self) -> None:
         _raise(self.lib.gdp2d_ctx_reset(self.ctx), "gdp2d_ctx_reset")
+
+    def build_cdt(self, points: np.ndarray, segments: np.ndarray) -> dict:
+        """Line 1 on the device (build_cdt, cdt.hpp:483): the CDT of the PSLG
+        (segments already hull-closed, host.close_hull) becomes this context's
+        input mesh, as upload() would make it.  Returns the build report."""
+        pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 2)
+        seg = np.ascontiguousarray(segments, dtype=np.uint32).reshape(-1, 2)
+        r = A.CdtReport()
+        _raise(self.lib.gdp2d_ctx_build_cdt(self.ctx, pts.ctypes.data, len(pts), seg.ctypes.data,
+                                            len(seg), C.byref(r)), "gdp2d_ctx_build_cdt")
+        return {name: getattr(r, name) for name, _ in A.CdtReport._fields_}
 
     def refine(self, q: QualityCriteria, cfg: Optional[EngineConfig] = None) -> RunReport:
         p = make_params(q, cfg)

@@ -50,6 +50,23 @@ def build_cdt(points: np.ndarray, segments: np.ndarray, close_hull: bool = True)
     return Mesh.from_buf(out, lib.gdp2d_host_free_buf), closed
 
 
+def close_hull(points: np.ndarray, segments: np.ndarray, check: bool = True) -> np.ndarray:
+    """close_hull (cdt.hpp:447) [+ check_crossings]: the closed segment list."""
+    lib = A.host()
+    pts = np.ascontiguousarray(points, dtype=np.float64)
+    seg = np.ascontiguousarray(segments, dtype=np.uint32).reshape(-1, 2)
+    so = C.POINTER(C.c_uint32)()
+    mo = C.c_uint32(0)
+    rc = lib.gdp2d_host_close_hull(pts.ctypes.data, len(pts), seg.ctypes.data, len(seg),
+                                   1 if check else 0, C.byref(so), C.byref(mo))
+    if rc:
+        raise RuntimeError("close_hull: " + lib.gdp2d_host_last_error().decode())
+    closed = np.ctypeslib.as_array(so, shape=(2 * mo.value,)).reshape(-1, 2).copy() \
+        if mo.value else np.zeros((0, 2), np.uint32)
+    lib.gdp2d_host_free(C.cast(so, C.c_void_p))
+    return closed
+
+
 def read_poly(text: str):
     """read_poly (pslg_io.hpp:272): parsed, de-duplicated, crossing-checked, hull closed."""
     lib = A.host()
