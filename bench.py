@@ -115,11 +115,36 @@ def load_peaks():
     return 6650.0, "fallback"
 
 
+LINE1 = {}   # first workload's PSLG + reference build_cdt time
+
+
 def make_workload(cfg: dict, seed: int):
     from paper_2007_00324_b200 import host
     pts, segs = host.generate_pslg(cfg["n"], cfg["m"], cfg["dist"], seed)
+    t0 = time.perf_counter()
     mesh, closed = host.build_cdt(pts, segs)
+    if not LINE1:
+        LINE1.update(pts=pts, closed=closed, ref_s=time.perf_counter() - t0,
+                     ref_tris=int(mesh.tri_alive.sum()))
     return mesh
+
+
+def line1_device(device: int) -> dict:
+    """Line 1 (build_cdt, cdt.hpp:483) on the device for the same PSLG: median
+    of 3 builds after one warm-up, beside the reference's host build time
+    measured while preparing the workload (not part of the refine metric)."""
+    from paper_2007_00324_b200 import Engine
+    with Engine(device) as e:
+        e.build_cdt(LINE1["pts"], LINE1["closed"])
+        runs = [e.build_cdt(LINE1["pts"], LINE1["closed"]) for _ in range(3)]
+    ms = sorted(r["seconds"] * 1e3 for r in runs)[1]
+    r = runs[-1]
+    return {"device_ms": ms, "reference_host_s": LINE1["ref_s"],
+            "speedup": LINE1["ref_s"] * 1e3 / ms, "triangles": r["n_triangles"],
+            "same_triangle_count": r["n_triangles"] == LINE1["ref_tris"],
+            "insert_rounds": r["insert_rounds"], "recover_rounds": r["recover_rounds"],
+            "note": "device build of the bench PSLG (untimed in the paper); "
+                    "triangle-set parity: tests/test_gpu_cdt.py"}
 
 
 def mesh_bytes(m) -> int:
@@ -349,6 +374,9 @@ def main():
         "host_timed_s": host_s,
         "setup_s": setup_s,
     }
+
+    if rank == 0 and LINE1:
+        line["line1_cdt"] = line1_device(device)
 
     # ---- CPU baseline (rank 0, N = 1 only) ----
     if world == 1 and not a.no_cpu_baseline:

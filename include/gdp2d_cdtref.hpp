@@ -214,6 +214,34 @@ inline cdtref::RunReport refine(cdtref::Mesh& m, const cdtref::QualityCriteria& 
     return rep;
 }
 
+// Drop-in for cdtref::build_cdt (cdt.hpp:483) on the GPU (gdp2d_build_cdt).
+// Same Pslg in (hull already closed by read_poly / to_pslg), a fresh Mesh out
+// whose vertex i is g.points[i]; the triangle set equals the reference's for
+// PSLGs in general position (ids differ).  Throws cdtref::CdtError where the
+// reference does (duplicate points, all collinear, crossing segments).
+inline cdtref::Mesh build_cdt(const cdtref::Pslg& g, int device = 0) {
+    std::vector<double> xy(2 * g.points.size());
+    for (size_t i = 0; i < g.points.size(); ++i) {
+        xy[2 * i] = g.points[i].x;
+        xy[2 * i + 1] = g.points[i].y;
+    }
+    std::vector<uint32_t> seg(2 * g.segments.size());
+    for (size_t i = 0; i < g.segments.size(); ++i) {
+        seg[2 * i] = g.segments[i].first;
+        seg[2 * i + 1] = g.segments[i].second;
+    }
+    gdp2d_mesh_buf out{};
+    gdp2d_cdt_report rep{};
+    const int rc = gdp2d_build_cdt(xy.data(), static_cast<uint32_t>(g.points.size()), seg.data(),
+                                   static_cast<uint32_t>(g.segments.size()), &out, &rep, device);
+    if (rc == GDP2D_ECDT) throw cdtref::CdtError(std::string("gdp2d_build_cdt: ") + gdp2d_last_error());
+    if (rc != GDP2D_OK) detail::throw_status(rc);
+    cdtref::Mesh m;
+    detail::unpack(out, m);
+    gdp2d_free(&out);
+    return m;
+}
+
 }  // namespace gdp2d
 
 #endif  // GDP2D_CDTREF_HPP

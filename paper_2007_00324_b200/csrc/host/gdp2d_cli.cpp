@@ -8,6 +8,7 @@
 // 3 cap hit / verification failure, 4 engine error.
 //
 //   gdp2d_cli input.poly [--theta DEG] [--ell L] [--chew] [--out PREFIX] [--device D]
+//             [--device-cdt]   (Line 1 via gdp2d::build_cdt instead of cdtref::build_cdt)
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -24,13 +25,14 @@
 int main(int argc, char** argv) {
     if (argc < 2) {
         std::fprintf(stderr, "usage: %s input.poly [--theta DEG] [--ell L] [--chew] "
-                             "[--out PREFIX] [--device D]\n", argv[0]);
+                             "[--out PREFIX] [--device D] [--device-cdt]\n", argv[0]);
         return 2;
     }
     std::string input = argv[1], prefix;
     cdtref::QualityCriteria q;
     cdtref::EngineConfig cfg;
     int device = 0;
+    bool device_cdt = false;   // --device-cdt: Line 1 on the GPU too (gdp2d::build_cdt)
     for (int i = 2; i < argc; ++i) {
         const std::string a = argv[i];
         auto val = [&]() -> const char* { return i + 1 < argc ? argv[++i] : "0"; };
@@ -39,6 +41,7 @@ int main(int argc, char** argv) {
         else if (a == "--chew") q.mode = cdtref::RefineMode::Chew;
         else if (a == "--out") prefix = val();
         else if (a == "--device") device = std::atoi(val());
+        else if (a == "--device-cdt") device_cdt = true;
         else {
             std::fprintf(stderr, "unknown flag %s\n", a.c_str());
             return 2;
@@ -55,10 +58,19 @@ int main(int argc, char** argv) {
     cdtref::Mesh m;
     try {
         g = cdtref::read_poly(buf.str());
-        m = cdtref::build_cdt(g);
     } catch (const std::exception& e) {
         std::fprintf(stderr, "input error: %s\n", e.what());
         return 2;
+    }
+    try {
+        // Line 1 on the host (as the reference), or on the GPU with --device-cdt
+        m = device_cdt ? gdp2d::build_cdt(g, device) : cdtref::build_cdt(g);
+    } catch (const cdtref::CdtError& e) {
+        std::fprintf(stderr, "input error: %s\n", e.what());
+        return 2;
+    } catch (const std::exception& e) {
+        std::fprintf(stderr, "%s error: %s\n", device_cdt ? "engine" : "input", e.what());
+        return device_cdt ? 4 : 2;
     }
     cdtref::RunReport rep;
     try {

@@ -64,3 +64,19 @@ def test_cli_refines_poly(built, tmp_path):
     assert nv - 20_000 == int(kv["steiner_points"])
     tri = np.array([list(map(int, l.split()[1:])) for l in ele[1:]])
     assert tri.shape == (nt, 3) and tri.max() < nv
+
+
+@pytest.mark.gpu
+def test_cli_device_cdt(built, tmp_path):
+    """--device-cdt: Line 1 on the GPU too (gdp2d::build_cdt); same quality bar,
+    and a PSLG the reference rejects (duplicate point) still exits 2."""
+    from paper_2007_00324_b200 import host
+    pts, segs = host.generate_pslg(20_000, 2_000, "gaussian", 6)
+    poly = tmp_path / "in.poly"
+    write_poly(poly, pts, segs)
+    r = subprocess.run([str(CLI), str(poly), "--device-cdt", "--out", str(tmp_path / "out")],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    kv = dict(t.split("=") for t in r.stdout.split())
+    assert int(kv["bad_triangles"]) == 0 and int(kv["steiner_points"]) > 0
+    assert (tmp_path / "out.ele").exists()

@@ -177,4 +177,7 @@ def test_million_points_equals_reference(built):
     ref, _ = host.build_cdt(pts, segs)
     np.testing.assert_array_equal(_tris(dev), _tris(ref))
     np.testing.assert_array_equal(_segs(dev), _segs(ref))
-    assert rep["seconds"] < 2.0
+    from paper_2007_00324_b200 import Engine
+    with Engine(0) as eng:   # warm context: device time of the build itself
+        eng.build_cdt(pts, closed)
+        assert eng.build_cdt(pts, closed)["seconds"] < 0.5
