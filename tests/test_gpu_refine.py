@@ -307,3 +307,24 @@ def test_chew_and_edge_bound_at_scale(built, mode, ell):
         assert rep.max_edge <= ell
     assert abs(rep.steiner_points - rref.steiner_points) <= 0.10 * rref.steiner_points, \
         (rep.steiner_points, rref.steiner_points)
+
+
+@pytest.mark.parametrize("mode,ell", [(1, math.inf), (1, 0.002)])
+def test_chew_and_edge_bound_at_million_points(built, mode, ell):
+    """SURVEY 8(f) row 3 at BASELINE size: Lines 1-9 on the device (device CDT,
+    Chew lens rule, edge-length bound) on config 2's 1M-point PSLG, checked by
+    the device validators (structure, exact local CDT, quality, conformity)."""
+    from paper_2007_00324_b200 import Engine, QualityCriteria, host
+    q = QualityCriteria(B_SQRT2_THETA, ell, mode)
+    pts, segs = host.generate_pslg(1_000_000, 100_000, "uniform", 20261017)
+    closed = host.close_hull(pts, segs, check=False)
+    with Engine(0) as eng:
+        eng.build_cdt(pts, closed)
+        rep = eng.refine(q)
+        val = eng.validate(q)
+    assert val["structure_failure"] == 0 and val["cdt_violations"] == 0
+    assert val["conformity_failures"] == 0 and val["bad_triangles"] == 0
+    assert rep.bad_triangles == 0 and rep.steiner_points > 500_000
+    assert val["min_angle_deg"] >= B_SQRT2_THETA - 1e-9 or mode == 1
+    if math.isfinite(ell):
+        assert rep.max_edge <= ell
