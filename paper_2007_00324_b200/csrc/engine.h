@@ -254,6 +254,7 @@ struct CdtLocal {          // one triangle of a pipe being re-triangulated
 struct CdtArgs {
     DevMesh m;             // work mesh; nT = triangle capacity (2N+1)
     u32 N;                 // input points (vertices 0..N-1)
+    u32 stride0;           // first insertion level: points i % stride0 == 0
     TriAux x;
     WorkLists w;           // vdirty = null
     RoundCtr* ring;        // [4]

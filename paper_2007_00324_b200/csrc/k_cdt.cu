@@ -59,6 +59,8 @@ __device__ __forceinline__ void ring_next(const CdtArgs& a, u32 step, bool leade
     }
 }
 
+static constexpr u32 PT_DEFER = 0xFFFFFFFDu;   // point of a later insertion level
+
 __device__ __forceinline__ bool has_super(const uint4& tv, u32 N) {
     return tv.x >= N || tv.y >= N || tv.z >= N;
 }
@@ -146,12 +148,22 @@ __global__ void __launch_bounds__(CDT_BLOCK) k_cdt_delaunay(CdtArgs a) {
     __shared__ u32 sh[CDT_BLOCK / 32 + 1];
     __shared__ u32 bc[2];
 
-    // every point starts in the super triangle (slot 0)
-    for (u32 i = tid; i < N; i += nthr) relocate(a, i, 0);
+    // Insertion levels (biased randomised insertion order): the points with
+    // i % stride == 0 first, then stride / 32, ... 1.  A level's points start
+    // their walk at the triangle of the previous level's point (i / stride) *
+    // stride -- a neighbour for spatially sorted input -- so the early rounds,
+    // where every point would re-walk after every round, run on a sample.
+    u32 stride = a.stride0;
+    for (u32 i = tid; i < N; i += nthr) {
+        if (i % stride == 0)
+            relocate(a, i, 0);   // the super triangle
+        else
+            a.ptri[i] = PT_DEFER;
+    }
     const u32 nblk = gridDim.x, b = blockIdx.x;
     const u32 chunk = ((N + nblk - 1) / nblk + CDT_BLOCK - 1) / CDT_BLOCK * CDT_BLOCK;
     const u32 lo = min(N, b * chunk), hi = min(N, lo + chunk);
-    u32 step = 0, nT = 1, remaining = N, rounds = 0, flip_rounds = 0;
+    u32 step = 0, nT = 1, remaining = (N + stride - 1) / stride, rounds = 0, flip_rounds = 0;
     ull flipped = 0;
     ring_next(a, step + 3u, leader);   // slot of step 0
     g.sync();
@@ -166,7 +178,10 @@ __global__ void __launch_bounds__(CDT_BLOCK) k_cdt_delaunay(CdtArgs a) {
             u64 key = ~0ull;
             if (i < N) {
                 t = a.ptri[i];
-                if (t != NONE) key = a.pkey[i];
+                if (t < PT_DEFER)
+                    key = a.pkey[i];
+                else
+                    t = NONE;
             }
             const u32 grp = __match_any_sync(0xFFFFFFFFu, t);
             const u32 khi = (u32)(key >> 32);
@@ -185,7 +200,7 @@ __global__ void __launch_bounds__(CDT_BLOCK) k_cdt_delaunay(CdtArgs a) {
         for (u32 i = lo + threadIdx.x; i < hi; i += CDT_BLOCK) {
             const u32 t = a.ptri[i];
             uint8_t win = 0;
-            if (t != NONE) {
+            if (t < PT_DEFER) {
                 const u64 key = a.pkey[i];
                 const u32 u = a.pother[i];
                 win = a.tkey[t] == key && (u == NONE || a.tkey[u] == key);
@@ -221,7 +236,7 @@ __global__ void __launch_bounds__(CDT_BLOCK) k_cdt_delaunay(CdtArgs a) {
             const u32 ex = block_exclusive<CDT_BLOCK>(wv, sh, &bsum);
             if (i < hi) {
                 const u32 t = a.ptri[i];
-                if (t != NONE) {
+                if (t < PT_DEFER) {
                     const u32 u = a.pother[i];
                     if (wv) {
                         const u32 t1 = nT + 2u * (c0 + ex);
@@ -283,7 +298,7 @@ __global__ void __launch_bounds__(CDT_BLOCK) k_cdt_delaunay(CdtArgs a) {
         u32 left = 0;
         for (u32 i = tid; i < N; i += nthr) {
             const u32 t = a.ptri[i];
-            if (t == NONE) continue;
+            if (t >= PT_DEFER) continue;
             ++left;
             if (a.x.stamp[t] >= R) relocate(a, i, t);
         }
@@ -292,6 +307,24 @@ __global__ void __launch_bounds__(CDT_BLOCK) k_cdt_delaunay(CdtArgs a) {
         remaining = vld(&lr->detect);
         ++step;
         ++rounds;
+        if (remaining == 0 && stride > 1) {
+            // next level: walk from the previous level's anchor point
+            const u32 s2 = stride > 32 ? stride / 32 : 1;
+            RoundCtr* ar = ring_slot(a, step);
+            ring_next(a, step, leader);
+            u32 act = 0;
+            for (u32 i = tid; i < N; i += nthr) {
+                if (i % s2 != 0 || a.ptri[i] != PT_DEFER) continue;
+                const u32 t0 = m.vtri[(i / stride) * stride];
+                relocate(a, i, t0 == NONE ? 0u : t0);
+                ++act;
+            }
+            block_add(&ar->detect, act);
+            g.sync();
+            remaining = vld(&ar->detect);
+            ++step;
+            stride = s2;
+        }
     }
     warp_add_ull(&a.ctr->flips, flipped);
     if (leader) {
