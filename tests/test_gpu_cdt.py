@@ -181,3 +181,25 @@ def test_million_points_equals_reference(built):
     with Engine(0) as eng:   # warm context: device time of the build itself
         eng.build_cdt(pts, closed)
         assert eng.build_cdt(pts, closed)["seconds"] < 0.5
+
+
+def test_cocircular_grid_is_a_valid_cdt(built):
+    """A lattice is maximally cocircular: the CDT is not unique, so the device
+    result is checked by the reference's validators (structure, local CDT with
+    ties allowed, conformity) and by the triangle count every triangulation of
+    the same points and hull shares."""
+    from paper_2007_00324_b200 import build_cdt, host
+    from oracle.ref import RefMesh
+    k = 60
+    g = np.linspace(0.0, 1.0, k)
+    pts = np.array([(x, y) for y in g for x in g], np.float64)
+    segs = np.array([[k * 10 + 10, k * 10 + 40], [k * 30 + 5, k * 50 + 5]], np.uint32)
+    closed = host.close_hull(pts, segs)
+    dev, rep = build_cdt(pts, closed)
+    ref, _ = host.build_cdt(pts, segs)
+    assert rep["n_triangles"] == int(ref.tri_alive.sum())
+    assert rep["collinear_splits"] >= 2          # both segments pass through lattice points
+    np.testing.assert_array_equal(_segs(dev), _segs(ref))
+    rm = RefMesh.from_mesh(dev)
+    rm.check_structure()
+    assert rm.euler_holds() and rm.cdt_violations() == 0 and rm.conformity_ok(pts, closed)

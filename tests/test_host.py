@@ -58,3 +58,15 @@ def test_reference_refine_small(built):
     rm.check_structure()
     assert rep.bad_triangles == 0 and rep.max_edge <= 0.2
     assert rm.cdt_violations() == 0
+
+
+def test_close_hull_matches_build_cdt_segments():
+    """host.close_hull (the device CDT builder's input) returns exactly the
+    segment list the reference's build path closes (cdt.hpp:447)."""
+    import numpy as np
+    from paper_2007_00324_b200 import host
+    pts, segs = host.generate_pslg(3000, 300, "gaussian", 2)
+    closed = host.close_hull(pts, segs)
+    _, closed_ref = host.build_cdt(pts, segs)
+    np.testing.assert_array_equal(closed, closed_ref)
+    assert len(closed) > len(segs)
