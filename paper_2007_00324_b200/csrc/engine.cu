@@ -353,6 +353,9 @@ struct gdp2d_ctx {
     double k_split_s = 0, k_rb_s = 0;   // per refine call: roofline accumulators
     u64 k_split_b = 0, k_rb_b = 0, k_launches = 0;
     u32* d_C = nullptr;           // candidate count written by collect (device)
+    u32 c_prev = 0;               // previous batch's candidate count (host, after its sync)
+    bool have_c_prev = false;
+    bool sync_collect = false;    // GDP2D_SYNC_COLLECT=1: host round trip after every collect
     u32 small_nv = 256;           // GDP2D_SMALL_NV: block-mode insertion at or below
     u32 small_wl = 256;           // GDP2D_SMALL_WL: block-mode Lawson below this list size
     u32 small_c = 256;            // GDP2D_SMALL_C: whole batch in one CTA at or below
@@ -618,6 +621,7 @@ void ctx_init(gdp2d_ctx* x, int device) {
     x->validate = ev && ev[0] == '1';
     const char* lr = std::getenv("GDP2D_LAWSON");
     x->lawson_rounds = lr && std::string(lr) == "rounds";
+    if (const char* e = std::getenv("GDP2D_SYNC_COLLECT")) x->sync_collect = e[0] == '1';
     x->lawson_grid = lawson_persistent_grid(device);
     x->insert_grid = insert_persistent_grid(device);
     x->rollback_grid = rollback_persistent_grid(device);
@@ -944,10 +948,11 @@ void check_structure_now(gdp2d_ctx* x, u32 nV, u32 nT, u32 nS, const char* where
 // round trip inside; the capacity check runs on the device and a batch that
 // does not fit is re-launched after growing the buffers (the mesh is not
 // touched by a launch that reports INS_GROW).
-void insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, u32 C, u32 ncav, u32 rs,
-                       int isolate, u32 batch, u32& nv, u32& nt, u32& ns, u32& flip_rounds,
-                       u32& rm_rounds) {
-    (void)C;
+// Returns false when the candidate list outgrew the region buffers (the batch
+// did nothing; the caller grows them and redoes it).  x->h_tot[3] = C.
+bool insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, int prefiltered, u32 reg_cap,
+                       u32 ncav, u32 rs, int isolate, u32 batch, u32& nv, u32& nt, u32& ns,
+                       u32& flip_rounds, u32& rm_rounds) {
     cudaStream_t st = x->st;
     for (int attempt = 0;; ++attempt) {
         CK(cudaMemsetAsync(x->ring, 0, 5 * sizeof(RoundCtr), st));
@@ -986,7 +991,8 @@ void insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, u32 C, u32 ncav, u32
         L.scan_part = x->scan_part;
         L.small_c = x->small_c;
         L.resume = attempt > 0 ? 1 : 0;
-        L.filter = C <= x->small_c ? 1 : 0;
+        L.prefiltered = prefiltered;
+        L.reg_cap = reg_cap;
         if (x->tr.on) {
             L.trace = x->tr.d_trace;
             L.trace_val = x->tr.d_trace_val;
@@ -1015,8 +1021,11 @@ void insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, u32 C, u32 ncav, u32
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(x->h_state, x->ins_state, 16 * sizeof(u32), cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(x->h_tot, x->ib.totals, 3 * sizeof(u32), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(x->h_tot + 3, x->d_C, sizeof(u32), cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(x->h_ctr, x->d_ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
+        const u32 C = x->h_tot[3];
+        if (x->h_state[0] == 3u) return false;   // INS_REGIONS
         nv = x->h_tot[0];
         nt = x->h_tot[1];
         ns = x->h_tot[2];
@@ -1046,7 +1055,7 @@ void insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, u32 C, u32 ncav, u32
         x->work.m.nV += nv;
         x->work.m.nT += nt;
         x->work.m.nS += ns;
-        return;
+        return true;
     }
 }
 
@@ -1072,6 +1081,7 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
     r->batches_capacity = keep.batches_capacity;
     x->k_split_s = x->k_rb_s = 0;
     x->k_split_b = x->k_rb_b = x->k_launches = 0;
+    x->have_c_prev = false;
     CK(cudaEventRecord(x->ev[GDP2D_NPHASES + 1], st));  // loop start
     for (u64 iter = 0;; ++iter) {
         if (iter >= p->iteration_cap) {
@@ -1092,22 +1102,28 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
         CollectCache cache;
         cache.full = (x->full_scan || x->full_collect) ? 1 : 0;
         bool tris_scanned = false;
-        const u32 C = launch_collect(m, q, p->rule4_unified_collection != 0, x->flags, x->c,
-                                     x->ccap, x->scan, x->d_ctr, st, cache, &tris_scanned,
-                                     x->d_C, x->ev[GDP2D_NPHASES + 2], x->ev[GDP2D_NPHASES + 3]);
+        // No host round trip after collect (ncs): the count stays on the
+        // device; the filter kernels read it, the loop learns it with the
+        // batch's end-of-batch readback.  The first batch of a call, the
+        // batch caps and rule 4 off take the synchronous path.
+        const bool ncs = !x->sync_collect && !x->legacy_insert && x->have_c_prev &&
+                         p->rule4_unified_collection != 0 && p->batch_size_cap == 0 &&
+                         !p->little_batch_sizing;
+        u32 C = launch_collect(m, q, p->rule4_unified_collection != 0, x->flags, x->c, x->ccap,
+                               x->scan, x->d_ctr, st, cache, &tris_scanned, x->d_C,
+                               x->ev[GDP2D_NPHASES + 2], x->ev[GDP2D_NPHASES + 3], !ncs);
         // a full scan has refreshed every cached verdict it covered; with
         // rule 4 off and subsegment candidates, triangles were not scanned
         if (tris_scanned) x->full_scan = false;
         CK(cudaGetLastError());
-        // launch_collect synchronised: the scan events are complete
-        r->scan_seconds += ev_ms(x->ev[GDP2D_NPHASES + 2], x->ev[GDP2D_NPHASES + 3]) * 1e-3;
         // scan bytes (scan_alg_bytes); the dirty count arrives with the
         // end-of-batch counters
         const u64 scan_nT = m.nT, scan_nS = m.nS;
         r->scan_launches += 1;
         x->tr.mark("collect", st);
-        if (C == 0) {
+        if (!ncs && C == 0) {
             check_dev_err(x);
+            r->scan_seconds += ev_ms(x->ev[GDP2D_NPHASES + 2], x->ev[GDP2D_NPHASES + 3]) * 1e-3;
             r->scan_bytes += scan_alg_bytes(scan_nT, scan_nS, x->h_ctr->scan_dirty);
             break;
         }
@@ -1115,8 +1131,8 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
         // highest priorities; the list keeps its order, the rest is dead
         u64 cap = p->batch_size_cap;
         if (p->little_batch_sizing && (cap == 0 || x->little_cap < cap)) cap = x->little_cap;
-        const u32 attempted = (cap > 0 && C > cap) ? (u32)cap : C;
-        if (attempted < C) launch_select_topk(x->c, C, attempted, x->sel_state, st);
+        u32 attempted = (!ncs && cap > 0 && C > cap) ? (u32)cap : C;
+        if (!ncs && attempted < C) launch_select_topk(x->c, C, attempted, x->sel_state, st);
         CK(cudaEventRecord(x->ev[1], st));   // split points are fused into collect
         CK(cudaEventRecord(x->ev[2], st));
         // isolated insertion needs the cavity filter (rule 2)
@@ -1125,7 +1141,8 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
                             : p->insert_mode == GDP2D_INSERT_PRECEDENCE ? 2
                                                                         : 0;
         const u32 rs = isolate ? isolated_stride(ncav) : ncav + 1 + MAX_CLAIM_EXTRA;
-        ensure_regions(x, C, ncav, rs);
+        if (!ncs) ensure_regions(x, C, ncav, rs);
+        const u32 reg_cap = (u32)std::min<size_t>(x->reg_cap / rs, x->rl_cap);
         CK(cudaMemsetAsync(x->ins_state + 8, 0, sizeof(u32), st));   // unsafe flag
         const u32 batch = ++x->epoch;
         u32 flip_rounds = 0, rm_rounds = 0;
@@ -1148,18 +1165,29 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
             x->tr.mark("plan+scans", st);
             insert_legacy(x, p, q, C, batch, nv, nt, ns, flip_rounds, rm_rounds);
         } else {
-            if (C > x->small_c) {
-                // big batch: Lines 5-7 as high-occupancy standalone kernels
-                launch_locate(m, x->c, C, x->d_ctr, st);
+            // Lines 5-7 as high-occupancy standalone kernels for big batches
+            // (they skip C <= small_c: the batch kernel filters in one CTA)
+            NArg na = NArg::host(C);
+            bool standalone = C > x->small_c;
+            if (ncs) {
+                standalone = x->c_prev > x->small_c;   // predicted from the last batch
+                na.d_n = x->d_C;
+                na.skip_le = x->small_c;
+                na.cap = reg_cap;
+                na.grid_n = (u32)std::min<u64>((u64)m.nS + m.nT,
+                                               std::max<u64>(x->c_prev + x->c_prev / 2, 4096));
+            }
+            if (standalone) {
+                launch_locate(m, x->c, na, x->d_ctr, st);
                 CK(cudaEventRecord(x->ev[3], st));
-                launch_claim(m, x->c, C, x->aux, x->d_ctr, st);
+                launch_claim(m, x->c, na, x->aux, x->d_ctr, st);
                 CK(cudaEventRecord(x->ev[4], st));
                 if (isolate)
-                    launch_cavity_isolated(m, x->c, C, ncav, rs, p->mode == GDP2D_CHEW ? 1 : 0,
+                    launch_cavity_isolated(m, x->c, na, ncav, rs, p->mode == GDP2D_CHEW ? 1 : 0,
                                            p->split_depth_cap, isolate == 1, x->aux, x->regions,
                                            x->region_len, x->ins_state + 8, x->d_ctr, st);
                 else
-                    launch_cavity(m, x->c, C, ncav, x->extras, x->aux, x->regions,
+                    launch_cavity(m, x->c, na, ncav, x->extras, x->aux, x->regions,
                                   x->region_len, nullptr, x->d_ctr, st);
                 CK(cudaEventRecord(x->ev[5], st));
             } else {
@@ -1168,8 +1196,29 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
                 CK(cudaEventRecord(x->ev[4], st));
                 CK(cudaEventRecord(x->ev[5], st));
             }
-            insert_persistent(x, p, C, ncav, rs, isolate, batch, nv, nt, ns, flip_rounds,
-                              rm_rounds);
+            if (!insert_persistent(x, p, standalone ? 1 : 0, reg_cap, ncav, rs, isolate, batch,
+                                   nv, nt, ns, flip_rounds, rm_rounds)) {
+                // the list outgrew the region buffers: grow them, redo the batch
+                // (collect recomputes the same list from its cached verdicts)
+                ensure_regions(x, x->h_tot[3], ncav, rs);
+                --x->epoch;
+                x->c_prev = x->h_tot[3];
+                --iter;
+                continue;
+            }
+            if (ncs) {
+                C = x->h_tot[3];
+                attempted = C;
+            }
+        }
+        r->scan_seconds += ev_ms(x->ev[GDP2D_NPHASES + 2], x->ev[GDP2D_NPHASES + 3]) * 1e-3;
+        x->c_prev = C;
+        x->have_c_prev = true;
+        if (C == 0) {   // ncs: the batch found no candidates (its kernels did nothing)
+            raise_dev_err(x);
+            r->scan_bytes += scan_alg_bytes(scan_nT, scan_nS, x->h_ctr->scan_dirty);
+            --x->epoch;
+            break;
         }
         CK(cudaEventRecord(x->ev[6], st));
         x->tr.mark("sync", st);

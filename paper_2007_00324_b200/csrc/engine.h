@@ -65,29 +65,52 @@ u32 launch_collect(const DevMesh& m, const Quality& q, bool rule4, uint8_t* flag
                    u32 ccap, ScanScratch& s, Counters* d_ctr, cudaStream_t st,
                    const CollectCache& cache, bool* tris_scanned, u32* d_count,
                    cudaEvent_t ev_scan0 = nullptr,
-                   cudaEvent_t ev_scan1 = nullptr);
+                   cudaEvent_t ev_scan1 = nullptr, bool sync = true);
 void launch_split_points(const DevMesh& m, DevCands c, u32 n, Counters* d_ctr, cudaStream_t st);
 // batch_size_cap (refine.hpp:252-261): keep the k highest-priority alive
 // candidates of the list (others marked dead), device-side radix select.
 size_t select_state_bytes();
 u32 cavity_resident_candidates(int device);
 void launch_select_topk(DevCands c, u32 n, u32 k, void* state, cudaStream_t st);
-void launch_locate(const DevMesh& m, DevCands c, u32 n, Counters* d_ctr, cudaStream_t st);
-void launch_claim(const DevMesh& m, DevCands c, u32 n, TriAux a, Counters* d_ctr,
+// Item count of a standalone filter kernel: a host value, or the device count
+// written by collect (no host round trip).  Kernels loop grid-stride over
+// [0, n) and do nothing when n <= skip_le or n > cap (region capacity).
+struct NArg {
+    u32 n = 0;
+    const u32* d_n = nullptr;
+    u32 skip_le = 0;
+    u32 cap = 0xFFFFFFFFu;
+    u32 grid_n = 0;   // items the launch grid is sized for (grid-stride covers the rest)
+    static NArg host(u32 n) { NArg a; a.n = n; a.grid_n = n; return a; }
+};
+void launch_locate(const DevMesh& m, DevCands c, NArg n, Counters* d_ctr, cudaStream_t st);
+inline void launch_locate(const DevMesh& m, DevCands c, u32 n, Counters* d_ctr, cudaStream_t st) {
+    launch_locate(m, c, NArg::host(n), d_ctr, st);
+}
+void launch_claim(const DevMesh& m, DevCands c, NArg n, TriAux a, Counters* d_ctr,
                   cudaStream_t st);
+inline void launch_claim(const DevMesh& m, DevCands c, u32 n, TriAux a, Counters* d_ctr,
+                         cudaStream_t st) {
+    launch_claim(m, c, NArg::host(n), a, d_ctr, st);
+}
 // Cavity filter; extras = refine-mode extra claims (far side of a split edge).
 // extras: 0 parity (reference claims only), 1 refine with the far side of a
 // split edge added to the main claims, 2 refine with the rewrite table
 // (gdp2d_phases.cuh).
-void launch_cavity(const DevMesh& m, DevCands c, u32 n, u32 ncav, int extras, TriAux a,
+void launch_cavity(const DevMesh& m, DevCands c, NArg n, u32 ncav, int extras, TriAux a,
                    u32* regions, u32* region_len, u32* bfs_len, Counters* d_ctr,
                    cudaStream_t st);
+inline void launch_cavity(const DevMesh& m, DevCands c, u32 n, u32 ncav, int extras, TriAux a,
+                          u32* regions, u32* region_len, u32* bfs_len, Counters* d_ctr,
+                          cudaStream_t st) {
+    launch_cavity(m, c, NArg::host(n), ncav, extras, a, regions, region_len, bfs_len, d_ctr, st);
+}
 
 // Isolated-insertion claims (cavity + one-ring + encroachment precedence);
 // regions stride rs = isolated_stride(ncav); *unsafe_flag |= 1 when a survivor
 // inserts from a capped claim set.
 inline u32 isolated_stride(u32 ncav) { return 4 * (ncav + 1) + 8; }
-void launch_cavity_isolated(const DevMesh& m, DevCands c, u32 n, u32 ncav, u32 rs, int mode,
+void launch_cavity_isolated(const DevMesh& m, DevCands c, NArg n, u32 ncav, u32 rs, int mode,
                             u64 depth_cap, bool ring, TriAux a, u32* regions, u32* region_len,
                             u32* unsafe_flag, Counters* d_ctr, cudaStream_t st);
 
@@ -186,7 +209,8 @@ struct InsertLaunch {
     u32* scan_part = nullptr;   // [3 * grid]
     u32 small_c = 0;
     int resume = 0;
-    int filter = 1;
+    int prefiltered = 0;        // standalone Lines 5-7 kernels ran (they skip C <= small_c)
+    u32 reg_cap = 0xFFFFFFFFu;  // candidates the region buffers hold (INS_REGIONS beyond)
     int isolate = 1;            // claims: 0 reference cavity, 1 isolated (ring), 2 precedence
     int dep_mis = 0;            // dependent pairs by the priority-MIS rule
     int extras = 2;             // cavity extras mode (see launch_cavity)
@@ -198,7 +222,7 @@ struct InsertLaunch {
 };
 int insert_persistent_grid(int device);
 int rollback_persistent_grid(int device);
-// Kernel 1 (plan + splits + Lawson, with Lines 5-7 when L.filter) then
+// Kernel 1 (plan + splits + Lawson, with Lines 5-7 unless L.prefiltered) then
 // kernel 2 (detect + rollback loop), both cooperative, no host sync between.
 // which: bit 0 = kernel 1 (splits [+ Lawson]), bit 2 = the separate Lawson
 // kernel, bit 1 = kernel 2 (rollback), launched in that order.

@@ -21,6 +21,14 @@
 
 namespace gdp2d {
 
+// Count of a standalone filter kernel (NArg, engine.h) and its grid-stride loop.
+__device__ __forceinline__ u32 narg(const NArg& a) {
+    const u32 n = a.d_n ? *a.d_n : a.n;
+    return (n <= a.skip_le || n > a.cap) ? 0u : n;
+}
+#define GRID_STRIDE(i, n) \
+    for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < (n); i += gridDim.x * blockDim.x)
+
 // Returns the walk steps.
 __device__ __forceinline__ u32 locate_one(const DevMesh& m, const DevCands& c, u32 i) {
     if (!c.alive[i]) return 0;

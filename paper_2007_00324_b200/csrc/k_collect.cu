@@ -185,8 +185,11 @@ __global__ void __launch_bounds__(SCAN_BLOCK) k_collect_scatter(DevMesh m, Colle
 u32 launch_collect(const DevMesh& m, const Quality& q, bool rule4, uint8_t* flags, DevCands c,
                    u32 ccap, ScanScratch& s, Counters* d_ctr, cudaStream_t st,
                    const CollectCache& cache, bool* tris_scanned, u32* d_count,
-                   cudaEvent_t ev_scan0, cudaEvent_t ev_scan1) {
+                   cudaEvent_t ev_scan0, cudaEvent_t ev_scan1, bool sync) {
     *tris_scanned = false;
+    // sync == false (rule 4 only): no host round trip -- the scatter runs
+    // unconditionally and the count stays on the device (*d_count)
+    if (!sync && !rule4) sync = true;
     auto run = [&](bool sub, bool tri) -> u32 {
         if (tri) *tris_scanned = true;
         CollectRange r;
@@ -211,6 +214,10 @@ u32 launch_collect(const DevMesh& m, const Quality& q, bool rule4, uint8_t* flag
             note_launch(), k_collect_flags<1><<<tiles, SCAN_BLOCK, 0, st>>>(m, q, r, flags, s.partial, cache.full, d_ctr);
         if (ev_scan1 && (tri || !rule4)) cudaEventRecord(ev_scan1, st);
         scan_partials(s.partial, tiles, d_count, st);
+        if (!sync) {
+            note_launch(), k_collect_scatter<<<tiles, SCAN_BLOCK, 0, st>>>(m, r, flags, s.partial, c, ccap, d_count, d_ctr);
+            return NONE;
+        }
         u32 total = 0;
         cudaMemcpyAsync(&total, d_count, sizeof(u32), cudaMemcpyDeviceToHost, st);
         cudaStreamSynchronize(st);

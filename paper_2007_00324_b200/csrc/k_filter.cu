@@ -11,95 +11,96 @@
 
 namespace gdp2d {
 
-__global__ void k_claim_max(DevCands c, u32 n, u64* __restrict__ ckey) {
-    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) claim_max_one(c, i, ckey);
+__global__ void k_claim_max(DevCands c, NArg na, u64* __restrict__ ckey) {
+    const u32 n = narg(na);
+    GRID_STRIDE(i, n) claim_max_one(c, i, ckey);
 }
 
-__global__ void k_claim_tie(DevCands c, u32 n, const u64* __restrict__ ckey,
+__global__ void k_claim_tie(DevCands c, NArg na, const u64* __restrict__ ckey,
                             u64* __restrict__ ctie) {
-    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) claim_tie_one(c, i, ckey, ctie);
+    const u32 n = narg(na);
+    GRID_STRIDE(i, n) claim_tie_one(c, i, ckey, ctie);
 }
 
-__global__ void k_claim_check(DevCands c, u32 n, const u64* __restrict__ ckey,
+__global__ void k_claim_check(DevCands c, NArg na, const u64* __restrict__ ckey,
                               const u64* __restrict__ ctie, Counters* ctr) {
-    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    const u32 n = narg(na);
     u32 surv = 0;
-    if (i < n) surv = claim_check_one(c, i, ckey, ctie);
+    GRID_STRIDE(i, n) surv += claim_check_one(c, i, ckey, ctie);
     block_add<u32>(&ctr->surv_claim, surv);
 }
 
-__global__ void k_claim_reset(DevCands c, u32 n, u32 nT, u64* __restrict__ ckey,
+__global__ void k_claim_reset(DevCands c, NArg na, u32 nT, u64* __restrict__ ckey,
                               u64* __restrict__ ctie) {
-    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) claim_reset_one(c, i, nT, ckey, ctie);
+    const u32 n = narg(na);
+    GRID_STRIDE(i, n) claim_reset_one(c, i, nT, ckey, ctie);
 }
 
-void launch_claim(const DevMesh& m, DevCands c, u32 n, TriAux a, Counters* d_ctr,
+void launch_claim(const DevMesh& m, DevCands c, NArg n, TriAux a, Counters* d_ctr,
                   cudaStream_t st) {
-    if (!n) return;
-    const u32 g = (n + 255) / 256;
+    if (!n.grid_n) return;
+    const u32 g = (n.grid_n + 255) / 256;
     note_launch(), k_claim_max<<<g, 256, 0, st>>>(c, n, a.ckey);
     note_launch(), k_claim_tie<<<g, 256, 0, st>>>(c, n, a.ckey, a.ctie);
     note_launch(), k_claim_check<<<g, 256, 0, st>>>(c, n, a.ckey, a.ctie, d_ctr);
     note_launch(), k_claim_reset<<<g, 256, 0, st>>>(c, n, m.nT, a.ckey, a.ctie);
 }
 
-__global__ void __launch_bounds__(128) k_cavity_bfs(DevMesh m, DevCands c, u32 n, u32 ncav,
+__global__ void __launch_bounds__(128) k_cavity_bfs(DevMesh m, DevCands c, NArg na, u32 ncav,
                                                     int extras, u32 rs,
                                                     u32* __restrict__ regions,
                                                     u32* __restrict__ region_len,
                                                     u32* __restrict__ bfs_len,
                                                     u64* __restrict__ ckey, Counters* ctr) {
-    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    const u32 n = narg(na);
     ull visits = 0;
-    if (i < n) visits = cavity_bfs_one(m, c, i, ncav, extras, rs, regions, region_len, bfs_len, ckey);
+    GRID_STRIDE(i, n) visits += cavity_bfs_one(m, c, i, ncav, extras, rs, regions, region_len, bfs_len, ckey);
     block_add<ull>(&ctr->cavity_visits, visits);
 }
 
 // rewrite table (gdp2d_phases.cuh)
-__global__ void k_rw_claim(DevMesh m, DevCands c, u32 n, u64* __restrict__ fkey) {
-    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) rw_claim_one(m, c, i, fkey);
+__global__ void k_rw_claim(DevMesh m, DevCands c, NArg na, u64* __restrict__ fkey) {
+    const u32 n = narg(na);
+    GRID_STRIDE(i, n) rw_claim_one(m, c, i, fkey);
 }
-__global__ void k_rw_tie(DevCands c, u32 n, const u64* __restrict__ fkey, u64* __restrict__ ftie) {
-    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) rw_tie_one(c, i, fkey, ftie);
+__global__ void k_rw_tie(DevCands c, NArg na, const u64* __restrict__ fkey, u64* __restrict__ ftie) {
+    const u32 n = narg(na);
+    GRID_STRIDE(i, n) rw_tie_one(c, i, fkey, ftie);
 }
 
-__global__ void k_cavity_tie(DevCands c, u32 n, u32 rs, const u32* __restrict__ regions,
+__global__ void k_cavity_tie(DevCands c, NArg na, u32 rs, const u32* __restrict__ regions,
                              const u32* __restrict__ region_len, const u64* __restrict__ ckey,
                              u64* __restrict__ ctie) {
-    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) cavity_tie_one(c, i, rs, regions, region_len, ckey, ctie);
+    const u32 n = narg(na);
+    GRID_STRIDE(i, n) cavity_tie_one(c, i, rs, regions, region_len, ckey, ctie);
 }
 
 // fkey != null: a survivor must also own its rewritten triangles
-__global__ void k_cavity_check(DevCands c, u32 n, u32 rs, const u32* __restrict__ regions,
+__global__ void k_cavity_check(DevCands c, NArg na, u32 rs, const u32* __restrict__ regions,
                                const u32* __restrict__ region_len, const u64* __restrict__ ckey,
                                const u64* __restrict__ ctie, const u64* __restrict__ fkey,
                                const u64* __restrict__ ftie, Counters* ctr) {
-    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    const u32 n = narg(na);
     u32 surv = 0;
-    if (i < n) {
+    GRID_STRIDE(i, n) {
         const bool rw_ok = !fkey || !c.alive[i] || rw_owns(c, i, fkey, ftie);
-        surv = cavity_check_one(c, i, rs, regions, region_len, ckey, ctie);
-        if (surv && !rw_ok) {
+        u32 sv = cavity_check_one(c, i, rs, regions, region_len, ckey, ctie);
+        if (sv && !rw_ok) {
             c.alive[i] = 0;
-            surv = 0;
+            sv = 0;
         }
+        surv += sv;
     }
     block_add<u32>(&ctr->surv_cavity, surv);
 }
 
-__global__ void k_cavity_reset(DevCands c, u32 n, u32 nT, u32 rs,
+__global__ void k_cavity_reset(DevCands c, NArg na, u32 nT, u32 rs,
                                const u32* __restrict__ regions,
                                const u32* __restrict__ region_len, u64* __restrict__ ckey,
                                u64* __restrict__ ctie, u64* __restrict__ fkey,
                                u64* __restrict__ ftie) {
-    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) {
+    const u32 n = narg(na);
+    GRID_STRIDE(i, n) {
         cavity_reset_one(i, rs, regions, region_len, ckey, ctie);
         if (fkey) rw_reset_one(c, i, nT, fkey, ftie);
     }
@@ -108,44 +109,50 @@ __global__ void k_cavity_reset(DevCands c, u32 n, u32 nT, u32 rs,
 // ---- isolated claims (GDP2D_INSERT_ISOLATED, gdp2d_phases.cuh) ----
 
 template <int MODE>
-__global__ void __launch_bounds__(128) k_cavity_claims(DevMesh m, DevCands c, u32 n, u32 ncav,
+__global__ void __launch_bounds__(128) k_cavity_claims(DevMesh m, DevCands c, NArg na, u32 ncav,
                                                        u32 rs, u32* __restrict__ regions,
                                                        u32* __restrict__ region_len,
                                                        u64* __restrict__ ckey, u64 depth_cap,
                                                        int ring, Counters* ctr) {
-    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    const u32 n = narg(na);
     ull visits = 0;
-    if (i < n)
-        visits = cavity_claims_one<MODE>(m, c, i, ncav, rs, regions, region_len, ckey, depth_cap,
-                                         ring != 0);
+    GRID_STRIDE(i, n)
+        visits += cavity_claims_one<MODE>(m, c, i, ncav, rs, regions, region_len, ckey, depth_cap,
+                                          ring != 0);
     block_add<ull>(&ctr->cavity_visits, visits);
 }
 
-__global__ void k_isolated_check(DevMesh m, DevCands c, u32 n, u32 rs,
+__global__ void k_isolated_check(DevMesh m, DevCands c, NArg na, u32 rs,
                                  const u32* __restrict__ regions,
                                  const u32* __restrict__ region_len, const u64* __restrict__ ckey,
                                  const u64* __restrict__ ctie, const u64* __restrict__ fkey,
                                  const u64* __restrict__ ftie, u32* unsafe_flag, Counters* ctr) {
-    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    const u32 n = narg(na);
     u32 surv = 0, marked = 0, unsafe = 0;
-    if (i < n) {
-        if (c.alive[i] && !rw_owns(c, i, fkey, ftie)) c.alive[i] = 0;
-        else surv = isolated_check_one(m, c, i, rs, regions, region_len, ckey, ctie, marked, unsafe);
+    GRID_STRIDE(i, n) {
+        if (c.alive[i] && !rw_owns(c, i, fkey, ftie)) {
+            c.alive[i] = 0;
+        } else {
+            u32 mk = 0, us = 0;
+            surv += isolated_check_one(m, c, i, rs, regions, region_len, ckey, ctie, mk, us);
+            marked += mk;
+            unsafe |= us;
+        }
     }
     if (unsafe) atomicOr(unsafe_flag, 1u);
     block_add<u32>(&ctr->surv_cavity, surv);
     block_add<u32>(&ctr->marked, marked);
 }
 
-void launch_cavity_isolated(const DevMesh& m, DevCands c, u32 n, u32 ncav, u32 rs, int mode,
+void launch_cavity_isolated(const DevMesh& m, DevCands c, NArg n, u32 ncav, u32 rs, int mode,
                             u64 depth_cap, bool ring, TriAux a, u32* regions, u32* region_len,
                             u32* unsafe_flag, Counters* d_ctr, cudaStream_t st) {
-    if (!n) return;
+    if (!n.grid_n) return;
     if (mode == 0)
-        note_launch(), k_cavity_claims<0><<<(n + 127) / 128, 128, 0, st>>>(m, c, n, ncav, rs, regions, region_len, a.ckey, depth_cap, ring ? 1 : 0, d_ctr);
+        note_launch(), k_cavity_claims<0><<<(n.grid_n + 127) / 128, 128, 0, st>>>(m, c, n, ncav, rs, regions, region_len, a.ckey, depth_cap, ring ? 1 : 0, d_ctr);
     else
-        note_launch(), k_cavity_claims<1><<<(n + 127) / 128, 128, 0, st>>>(m, c, n, ncav, rs, regions, region_len, a.ckey, depth_cap, ring ? 1 : 0, d_ctr);
-    const u32 g = (n + 255) / 256;
+        note_launch(), k_cavity_claims<1><<<(n.grid_n + 127) / 128, 128, 0, st>>>(m, c, n, ncav, rs, regions, region_len, a.ckey, depth_cap, ring ? 1 : 0, d_ctr);
+    const u32 g = (n.grid_n + 255) / 256;
     note_launch(), k_rw_claim<<<g, 256, 0, st>>>(m, c, n, a.fkey);
     note_launch(), k_cavity_tie<<<g, 256, 0, st>>>(c, n, rs, regions, region_len, a.ckey, a.ctie);
     note_launch(), k_rw_tie<<<g, 256, 0, st>>>(c, n, a.fkey, a.ftie);
@@ -153,15 +160,15 @@ void launch_cavity_isolated(const DevMesh& m, DevCands c, u32 n, u32 ncav, u32 r
     note_launch(), k_cavity_reset<<<g, 256, 0, st>>>(c, n, m.nT, rs, regions, region_len, a.ckey, a.ctie, a.fkey, a.ftie);
 }
 
-void launch_cavity(const DevMesh& m, DevCands c, u32 n, u32 ncav, int extras, TriAux a,
+void launch_cavity(const DevMesh& m, DevCands c, NArg n, u32 ncav, int extras, TriAux a,
                    u32* regions, u32* region_len, u32* bfs_len, Counters* d_ctr,
                    cudaStream_t st) {
-    if (!n) return;
+    if (!n.grid_n) return;
     const u32 rs = ncav + 1 + MAX_CLAIM_EXTRA;
     const bool rw = extras == 2;
-    note_launch(), k_cavity_bfs<<<(n + 127) / 128, 128, 0, st>>>(m, c, n, ncav, extras, rs, regions,
+    note_launch(), k_cavity_bfs<<<(n.grid_n + 127) / 128, 128, 0, st>>>(m, c, n, ncav, extras, rs, regions,
                                                    region_len, bfs_len, a.ckey, d_ctr);
-    const u32 g = (n + 255) / 256;
+    const u32 g = (n.grid_n + 255) / 256;
     if (rw) note_launch(), k_rw_claim<<<g, 256, 0, st>>>(m, c, n, a.fkey);
     note_launch(), k_cavity_tie<<<g, 256, 0, st>>>(c, n, rs, regions, region_len, a.ckey, a.ctie);
     if (rw) note_launch(), k_rw_tie<<<g, 256, 0, st>>>(c, n, a.fkey, a.ftie);

@@ -751,7 +751,8 @@ struct InsertArgs {
     u32* scan_part;       // [3 * grid] per-CTA chunk sums of the insertion plan
     u32 small_c;          // block mode for the whole batch when C <= small_c
     int resume;           // 1: candidates are planned, start at the capacity check
-    int filter;           // 1: run Lines 5-7 in kernel 1 (tiny batches)
+    int prefiltered;      // standalone Lines 5-7 ran (for C > small_c)
+    u32 reg_cap;          // candidates the region buffers hold
     int isolate;          // claims: 0 reference, 1 isolated (rollback only if state[8]), 2 precedence
     int dep_mis;          // dependent pairs: 1 = priority-MIS rule, 0 = any-higher-neighbour rule
     int extras;           // refine cavity claims: 1 far side in the main claims, 2 rewrite table
@@ -783,7 +784,7 @@ __device__ __forceinline__ void trace(const InsertArgs& a, bool leader, u32 tag,
     }
 }
 
-enum : u32 { INS_OK = 0, INS_GROW = 1, INS_STEPS = 2 };
+enum : u32 { INS_OK = 0, INS_GROW = 1, INS_STEPS = 2, INS_REGIONS = 3 };
 
 __device__ __forceinline__ RoundCtr* ring_at(const InsertArgs& a, u32 step) {
     return a.ring + (step & 3u);
@@ -1258,12 +1259,16 @@ __device__ __forceinline__ bool fits_and_status(const InsertArgs& a, u32 nv, u32
 template <int MODE>
 __global__ void __launch_bounds__(INSERT_BLOCK, GDP2D_SPLIT_MINB) k_batch_split(InsertArgs a) {
     const u32 C = vload(a.d_C);
+    if (C > a.reg_cap) {   // uniform: the host grows the regions and redoes the batch
+        if (blockIdx.x == 0 && threadIdx.x == 0) a.state[0] = INS_REGIONS;
+        return;
+    }
     const bool block = C <= a.small_c;
     if (block && blockIdx.x != 0) return;
     const Exec ex = block ? block_exec() : grid_exec();
     if (!a.resume) {
         trace(a, ex.leader(), TR_START);
-        if (a.filter) filter<MODE>(a, ex, C);
+        if (block || !a.prefiltered) filter<MODE>(a, ex, C);
         plan_and_scan(a, ex, C);
     }
     const u32 nv = vload(&a.b.totals[0]), nt = vload(&a.b.totals[1]), ns = vload(&a.b.totals[2]);
@@ -1368,7 +1373,8 @@ void launch_insert_persistent(const InsertLaunch& L, int mode, int grid, int gri
     a.scan_part = L.scan_part;
     a.small_c = L.small_c;
     a.resume = L.resume;
-    a.filter = L.filter;
+    a.prefiltered = L.prefiltered;
+    a.reg_cap = L.reg_cap;
     a.isolate = L.isolate;
     a.dep_mis = L.dep_mis;
     a.extras = L.extras;

@@ -10,16 +10,17 @@
 
 namespace gdp2d {
 
-__global__ void __launch_bounds__(256) k_locate(DevMesh m, DevCands c, u32 n, Counters* ctr) {
-    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(256) k_locate(DevMesh m, DevCands c, NArg na, Counters* ctr) {
+    const u32 n = narg(na);
     ull steps = 0;
-    if (i < n) steps = locate_one(m, c, i);
+    for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        steps += locate_one(m, c, i);
     block_add<ull>(&ctr->walk_steps, steps);
 }
 
-void launch_locate(const DevMesh& m, DevCands c, u32 n, Counters* d_ctr, cudaStream_t st) {
-    if (!n) return;
-    note_launch(), k_locate<<<(n + 255) / 256, 256, 0, st>>>(m, c, n, d_ctr);
+void launch_locate(const DevMesh& m, DevCands c, NArg n, Counters* d_ctr, cudaStream_t st) {
+    if (!n.grid_n) return;
+    note_launch(), k_locate<<<(n.grid_n + 255) / 256, 256, 0, st>>>(m, c, n, d_ctr);
 }
 
 }  // namespace gdp2d
