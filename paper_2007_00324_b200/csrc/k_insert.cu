@@ -708,7 +708,9 @@ void launch_removal_round(const DevMesh& m, u32 round, u32 V0, TriAux a, FreshIn
 
 struct Exec {
     u32 tid, nthr;
-    bool block;  // block mode: CTA 0 only
+    bool block;      // block mode: CTA 0 only
+    RoundCtr* ring;  // step counters: global ring (grid mode) or shared memory (block mode,
+                     // so the work-list atomics and the post-barrier count reads stay on-SM)
     __device__ __forceinline__ void sync() const {
         if (block)
             __syncthreads();
@@ -718,11 +720,20 @@ struct Exec {
     __device__ __forceinline__ bool leader() const { return tid == 0; }
 };
 
-__device__ __forceinline__ Exec grid_exec() {
+__device__ __forceinline__ Exec grid_exec(RoundCtr* ring) {
     cg::grid_group g = cg::this_grid();
-    return Exec{(u32)g.thread_rank(), (u32)g.size(), false};
+    return Exec{(u32)g.thread_rank(), (u32)g.size(), false, ring};
 }
-__device__ __forceinline__ Exec block_exec() { return Exec{threadIdx.x, blockDim.x, true}; }
+// Block mode with its counters in shared memory: sring[5] is zeroed here
+// (every thread of the CTA must call it).
+__device__ __forceinline__ Exec block_exec(RoundCtr* sring) {
+    if (threadIdx.x < 5) {
+        RoundCtr z = {};
+        sring[threadIdx.x] = z;
+    }
+    __syncthreads();
+    return Exec{threadIdx.x, blockDim.x, true, sring};
+}
 
 __device__ __forceinline__ u32 vload(const u32* p) { return *(const volatile u32*)p; }
 
@@ -786,12 +797,13 @@ __device__ __forceinline__ void trace(const InsertArgs& a, bool leader, u32 tag,
 
 enum : u32 { INS_OK = 0, INS_GROW = 1, INS_STEPS = 2, INS_REGIONS = 3 };
 
-__device__ __forceinline__ RoundCtr* ring_at(const InsertArgs& a, u32 step) {
-    return a.ring + (step & 3u);
+__device__ __forceinline__ RoundCtr* ring_at(const Exec& ex, u32 step) {
+    return ex.ring + (step & 3u);
 }
 __device__ __forceinline__ void ring_advance(const InsertArgs& a, const Exec& ex, u32 step) {
+    (void)a;
     if (ex.leader()) {
-        RoundCtr* z = a.ring + ((step + 1u) & 3u);
+        RoundCtr* z = ex.ring + ((step + 1u) & 3u);
         z->wl_next = z->cand = z->touched = z->rm_next = z->detect = 0;
     }
 }
@@ -802,7 +814,7 @@ __device__ void lawson_rounds(const InsertArgs& a, const Exec& ex, const DevMesh
                               u32& cur, u32 n, ull& flipped, u32& rounds) {
     const WorkLists& w = a.w;
     while (n > 0 && step < a.max_steps) {
-        RoundCtr* rc = ring_at(a, step);
+        RoundCtr* rc = ring_at(ex, step);
         ring_advance(a, ex, step);
         const u32 round = a.round0 + step;
         const u32* wl = w.w[cur];
@@ -842,7 +854,8 @@ __device__ void lawson_fixpoint_dev(const InsertArgs& a, const Exec& ex, const D
     while (n > 0 && step < a.max_steps) {
         if (n <= a.small_wl) {
             if (blockIdx.x == 0) {
-                const Exec bx = block_exec();
+                __shared__ RoundCtr hring[5];
+                const Exec bx = block_exec(hring);
                 trace(a, bx.leader(), TR_BLOCK_IN);
                 u32 s2 = step, c2 = cur, r2 = 0;
                 lawson_rounds(a, bx, m, s2, c2, n, flipped, r2);
@@ -851,6 +864,9 @@ __device__ void lawson_fixpoint_dev(const InsertArgs& a, const Exec& ex, const D
                     a.state[4] = s2;
                     a.state[5] = c2;
                     a.state[6] = r2;
+                    // the grid resumes at step s2 on the global ring
+                    RoundCtr z = {};
+                    a.ring[s2 & 3u] = z;
                 }
             }
             ex.sync();
@@ -861,7 +877,7 @@ __device__ void lawson_fixpoint_dev(const InsertArgs& a, const Exec& ex, const D
             return;
         }
         // one grid-wide round, then re-evaluate the list size
-        RoundCtr* rc = ring_at(a, step);
+        RoundCtr* rc = ring_at(ex, step);
         ring_advance(a, ex, step);
         const u32 round = a.round0 + step;
         const u32* wl = a.w.w[cur];
@@ -1038,7 +1054,7 @@ __device__ void split_and_flip(const InsertArgs& a, const Exec& ex, u32 nv, u32 
     u32 step = 0, cur = 0, flip_rounds = 0;
     ull flipped = 0;
     u32 mid = 0, cc = 0;
-    RoundCtr* rc = ring_at(a, step);
+    RoundCtr* rc = ring_at(ex, step);
     ring_advance(a, ex, step);
     {
         const u32 round = a.round0 + step;
@@ -1104,6 +1120,10 @@ __device__ void rollback_loop(const InsertArgs& a, const Exec& ex, u32 nv, u32 n
     ull flipped = 0;
     u32 marked = 0, red = 0, dep = 0, done = 0;
     const u32 V0 = a.m.nV, F = nv;
+    if (ex.leader()) {   // the split kernel may have run on a different ring
+        RoundCtr z = {};
+        ex.ring[step & 3u] = z;
+    }
     ex.sync();   // every thread has read state[1] before the leader rewrites it
     // Detection passes evaluate only suspects (f.dirty, set by fixup_one when
     // a rewritten triangle makes a fresh circumcenter the apex of a
@@ -1112,9 +1132,9 @@ __device__ void rollback_loop(const InsertArgs& a, const Exec& ex, u32 nv, u32 n
     // could make it redundant or dependent (a neighbour turning redundant only
     // removes a reason to be dependent, and removed neighbours rewrite it).
     // dirty: 1 = suspect, 2 = evaluated in this pass, 0 = clean.
-    RoundCtr* seed_rc = a.ring + 4;   // Lawson seeds of all removal rounds of a pass
+    RoundCtr* seed_rc = ex.ring + 4;   // Lawson seeds of all removal rounds of a pass
     for (u32 pass = 0; step < a.max_steps; ++pass) {
-        RoundCtr* rc = ring_at(a, step);
+        RoundCtr* rc = ring_at(ex, step);
         ring_advance(a, ex, step);
         if (ex.leader()) seed_rc->wl_next = 0;   // visible after the barriers below
         for (u32 j = ex.tid; j < F; j += ex.nthr) {
@@ -1148,7 +1168,7 @@ __device__ void rollback_loop(const InsertArgs& a, const Exec& ex, u32 nv, u32 n
             u32* lists[2] = {w.rm[1], w.touched};
             u32 lc = 0;
             for (u32 r = 0; nu > 0 && r < 4096; ++r) {
-                RoundCtr* rr = ring_at(a, step);
+                RoundCtr* rr = ring_at(ex, step);
                 ring_advance(a, ex, step);
                 ++step;
                 for (u32 i = ex.tid; i < nu; i += ex.nthr) {
@@ -1174,7 +1194,7 @@ __device__ void rollback_loop(const InsertArgs& a, const Exec& ex, u32 nv, u32 n
                 nu = nn;
                 lc ^= 1u;
             }
-            rc = ring_at(a, step);
+            rc = ring_at(ex, step);
             ring_advance(a, ex, step);
             if (ex.leader()) seed_rc->wl_next = 0;
             ex.sync();
@@ -1198,7 +1218,7 @@ __device__ void rollback_loop(const InsertArgs& a, const Exec& ex, u32 nv, u32 n
         // a Delaunay one, so intermediate Lawson passes are unnecessary.
         u32 rcur = 0;
         while (nrm > 0 && step < a.max_steps) {
-            rc = ring_at(a, step);
+            rc = ring_at(ex, step);
             ring_advance(a, ex, step);
             const u32 round = a.round0 + step;
             const u32* list = w.rm[rcur];
@@ -1265,7 +1285,8 @@ __global__ void __launch_bounds__(INSERT_BLOCK, GDP2D_SPLIT_MINB) k_batch_split(
     }
     const bool block = C <= a.small_c;
     if (block && blockIdx.x != 0) return;
-    const Exec ex = block ? block_exec() : grid_exec();
+    __shared__ RoundCtr sring[5];
+    const Exec ex = block ? block_exec(sring) : grid_exec(a.ring);
     if (!a.resume) {
         trace(a, ex.leader(), TR_START);
         if (block || !a.prefiltered) filter<MODE>(a, ex, C);
@@ -1287,7 +1308,8 @@ __global__ void __launch_bounds__(INSERT_BLOCK, GDP2D_LAWSON_MINB) k_batch_lawso
     const u32 C = vload(a.d_C);
     const bool block = C <= a.small_c;
     if (block && blockIdx.x != 0) return;
-    const Exec ex = block ? block_exec() : grid_exec();
+    __shared__ RoundCtr sring[5];
+    const Exec ex = block ? block_exec(sring) : grid_exec(a.ring);
     DevMesh m = a.m;
     m.nV += nv;
     m.nT += nt;
@@ -1295,6 +1317,10 @@ __global__ void __launch_bounds__(INSERT_BLOCK, GDP2D_LAWSON_MINB) k_batch_lawso
     u32 step = vload(&a.state[1]), cur = 0, flip_rounds = 0;
     const u32 n = vload(&a.state[9]);
     ull flipped = 0;
+    if (ex.leader()) {
+        RoundCtr z = {};
+        ex.ring[step & 3u] = z;
+    }
     ex.sync();   // every thread has read state[] before the leader rewrites it
     lawson_fixpoint_dev(a, ex, m, step, cur, n, flipped, flip_rounds);
     warp_add_ull(&a.ctr->flips, flipped);
@@ -1321,7 +1347,8 @@ __global__ void __launch_bounds__(INSERT_BLOCK) k_batch_rollback(InsertArgs a) {
     if (nv == 0) return;
     const bool block = nv <= a.small_c;
     if (block && blockIdx.x != 0) return;
-    const Exec ex = block ? block_exec() : grid_exec();
+    __shared__ RoundCtr sring[5];
+    const Exec ex = block ? block_exec(sring) : grid_exec(a.ring);
     rollback_loop<MODE>(a, ex, nv, nt, ns);
 }
 

@@ -58,6 +58,7 @@ def main():
                 tot[k] = tot.get(k, 0.0) + v
         print("phase totals (ms): " + " ".join(f"{k}={v*1e3:.2f}" for k, v in tot.items()),
               f"sum={sum(tot.values())*1e3:.2f}", flush=True)
+        print("totals: " + " ".join(f"{k}={v}" for k, v in rep.totals.items()), flush=True)
         out = eng.download()
     if a.check or a.ref:
         from oracle.ref import RefMesh
