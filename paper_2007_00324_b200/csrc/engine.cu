@@ -393,7 +393,7 @@ namespace {
 void cands_free(DevCands& c) {
     dfree(c.pt); dfree(c.key); dfree(c.id); dfree(c.tie); dfree(c.loc);
     dfree(c.kind); dfree(c.alive); dfree(c.lkind); dfree(c.ledge); dfree(c.fb);
-    dfree(c.red); dfree(c.unsafe); dfree(c.far);
+    dfree(c.red); dfree(c.unsafe); dfree(c.far); dfree(c.bw);
 }
 
 void ensure_cands(gdp2d_ctx* x, u32 n) {
@@ -404,6 +404,8 @@ void ensure_cands(gdp2d_ctx* x, u32 n) {
     dalloc(x->c.loc, cap); dalloc(x->c.kind, cap); dalloc(x->c.alive, cap);
     dalloc(x->c.lkind, cap); dalloc(x->c.ledge, cap); dalloc(x->c.fb, cap);
     dalloc(x->c.red, cap); dalloc(x->c.unsafe, cap); dalloc(x->c.far, cap);
+    dalloc(x->c.bw, cap);
+    CK(cudaMemsetAsync(x->c.bw, 0, cap, x->st));
     x->ccap = cap;
     // per-candidate insertion buffers
     dfree(x->ib.nv); dfree(x->ib.nt); dfree(x->ib.ns); dfree(x->ib.ov); dfree(x->ib.ot);

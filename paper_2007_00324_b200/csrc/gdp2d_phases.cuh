@@ -479,6 +479,27 @@ __device__ __forceinline__ void rw_reset_one(const DevCands& c, u32 i, u32 nT, u
     }
 }
 
+// Bowyer-Watson eligibility of a surviving candidate (extras == 3): a
+// circumcenter strictly inside its located triangle whose cavity was not
+// capped and holds no triangle that another candidate's split rewrites (a
+// midpoint's far side, claimed in the rewrite table only).  Such a survivor
+// owns its whole cavity, so it can rewrite it as the star of p.
+static __device__ __noinline__ uint8_t bw_eligible(const DevCands& c, u32 i, u32 ncav, u32 rs,
+                                               const u32* regions, const u32* region_len,
+                                               const u64* fkey, const u64* ftie) {
+    if (!c.alive[i] || c.kind[i] != 1 || c.lkind[i] != 0) return 0;
+    const u32 len = region_len[i];
+    if (len == 0 || len > ncav) return 0;
+    const u64 key = c.key[i], tie = tie_of(c, i);
+    const u32* reg = regions + (size_t)i * rs;
+    for (u32 k = 0; k < len; ++k) {
+        const u32 t = reg[k];
+        const u64 fk = fkey[t];
+        if (fk != 0 && !(fk == key && ftie[t] == tie)) return 0;
+    }
+    return 1;
+}
+
 // Needs of one surviving candidate (refine.hpp:493-539): subsegments that hit
 // the depth cap or fail subsegment_split_ok are abandoned (:501-506).
 // Returns 1 if the candidate was dropped.

@@ -56,10 +56,22 @@ __global__ void k_plan_ops(DevMesh m, DevCands c, u32 n, u64 depth_cap, InsertBu
 
 // One surviving candidate's phase-1 insertion (refine.hpp:492-539).
 // Returns 1 = midpoint, 2 = circumcenter, 0 = nothing.
-__device__ __forceinline__ int apply_one(const DevMesh& m, const DevCands& c, u32 i, u32 batch,
+// GDP2D_BW=1 builds the Bowyer-Watson insertion option (GDP2D_EXTRAS=3/4);
+// apply_one is then kept out of line (inlined, the extra path makes the
+// 128-register split kernel spill).
+#ifndef GDP2D_BW
+#define GDP2D_BW 0
+#endif
+#if GDP2D_BW
+#define APPLY_INLINE __noinline__
+#else
+#define APPLY_INLINE __forceinline__
+#endif
+__device__ APPLY_INLINE int apply_one(const DevMesh& m, const DevCands& c, u32 i, u32 batch,
                                          u32 round, const InsertBufs& b, const TriAux& x,
                                          const FreshInfo& f, const WorkLists& w, RoundCtr* rc,
-                                         int seed, Counters* ctr) {
+                                         int seed, Counters* ctr, const u32* regions = nullptr,
+                                         const u32* region_len = nullptr, u32 rs = 0) {
     if (!b.nv[i]) return 0;
     const u32 wv = m.nV + b.ov[i];
     const u32 nt0 = m.nT + b.ot[i];
@@ -100,10 +112,21 @@ __device__ __forceinline__ int apply_one(const DevMesh& m, const DevCands& c, u3
         split_edge_A(m, x, w, t, e, wv, nt0, nt0 + 1, s_bw, s_wc, round, rc, seed, ctr);
         return 1;
     }
-    if (c.lkind[i] == 0)
+    if (c.lkind[i] == 0) {
+#if GDP2D_BW
+        if (regions && c.bw[i] &&
+            bw_insert(m, x, w, regions + (size_t)i * rs, region_len[i], wv, p, nt0, round, rc, seed,
+                      ctr))
+            return 2;
+#else
+        (void)regions;
+        (void)region_len;
+        (void)rs;
+#endif
         split_triangle_A(m, x, w, t, wv, nt0, nt0 + 1, round, rc, seed, ctr);
-    else
+    } else {
         split_edge_A(m, x, w, t, c.ledge[i], wv, nt0, nt0 + 1, NONE, NONE, round, rc, seed, ctr);
+    }
     return 2;
 }
 
@@ -929,7 +952,8 @@ __device__ void filter(const InsertArgs& a, const Exec& ex, u32 C) {
     ex.sync();
     trace(a, ex.leader(), TR_CLAIM);
     u32 marked = 0, unsafe = 0;
-    const bool rw = a.isolate || a.extras == 2;
+    const bool rw = a.isolate || a.extras >= 2;
+    const bool bw = GDP2D_BW && !a.isolate && a.extras >= 3;
     for (u32 i = ex.tid; i < C; i += ex.nthr) {
         visits += a.isolate
                       ? cavity_claims_one<MODE>(m, a.c, i, a.ncav, a.rs, a.regions, a.region_len,
@@ -957,6 +981,13 @@ __device__ void filter(const InsertArgs& a, const Exec& ex, u32 C) {
     if (unsafe) atomicOr(&a.state[8], 1u);
     warp_add_u32(&a.ctr->marked, marked);
     ex.sync();
+    if (bw) {
+        // survivors are final (alive); the rewrite table is still set
+        for (u32 i = ex.tid; i < C; i += ex.nthr)
+            a.c.bw[i] = bw_eligible(a.c, i, a.ncav, a.rs, a.regions, a.region_len, a.x.fkey,
+                                    a.x.ftie);
+        ex.sync();
+    }
     for (u32 i = ex.tid; i < C; i += ex.nthr) {
         cavity_reset_one(i, a.rs, a.regions, a.region_len, a.x.ckey, a.x.ctie);
         if (rw) rw_reset_one(a.c, i, m.nT, a.x.fkey, a.x.ftie);
@@ -1059,7 +1090,11 @@ __device__ void split_and_flip(const InsertArgs& a, const Exec& ex, u32 nv, u32 
     {
         const u32 round = a.round0 + step;
         for (u32 i = ex.tid; i < C; i += ex.nthr) {
-            const int r = apply_one(m, a.c, i, a.batch, round, a.b, a.x, a.f, w, rc, 1, a.ctr);
+            const int r = apply_one(m, a.c, i, a.batch, round, a.b, a.x, a.f, w, rc, 1, a.ctr,
+                                    !a.isolate && (a.extras == 3 || (a.extras == 4 && !ex.block))
+                                        ? a.regions
+                                        : nullptr,
+                                    a.region_len, a.rs);
             mid += r == 1;
             cc += r == 2;
         }
@@ -1277,7 +1312,7 @@ __device__ __forceinline__ bool fits_and_status(const InsertArgs& a, u32 nv, u32
 // the phase-1 plan + splits + Lawson.  Block mode (CTA 0 alone) when the
 // candidate list is small -- the long tail of the refinement (Rule 1).
 template <int MODE>
-__global__ void __launch_bounds__(INSERT_BLOCK, GDP2D_SPLIT_MINB) k_batch_split(InsertArgs a) {
+__global__ void __launch_bounds__(INSERT_BLOCK, GDP2D_SPLIT_MINB) k_batch_split(const __grid_constant__ InsertArgs a) {
     const u32 C = vload(a.d_C);
     if (C > a.reg_cap) {   // uniform: the host grows the regions and redoes the batch
         if (blockIdx.x == 0 && threadIdx.x == 0) a.state[0] = INS_REGIONS;
