@@ -108,13 +108,14 @@ def build_cli(force: bool = False) -> Path | None:
         if target.exists():
             return target
         raise RuntimeError(f"{REF_INCLUDE} missing and no prebuilt {target}")
-    deps = [src, INCLUDE / "gdp2d.h", INCLUDE / "gdp2d_cdtref.hpp", Path(__file__)]
+    deps = [src, INCLUDE / "gdp2d.h", INCLUDE / "gdp2d_cdtref.hpp", Path(__file__),
+            LIB / "libgdp2d_host.so"]
     if not force and _newer(target, deps):
         return target
     tmp = target.with_name(target.name + ".tmp")
     _run(["g++", "-std=c++20", "-O3", "-DNDEBUG", "-ffp-contract=off", "-pthread",
           "-I", str(INCLUDE), "-I", str(REF_INCLUDE), str(src), "-o", str(tmp),
-          "-L", str(LIB), "-lgdp2d", "-Wl,-rpath,$ORIGIN"])
+          "-L", str(LIB), "-lgdp2d", "-lgdp2d_host", "-Wl,-rpath,$ORIGIN"])
     os.replace(tmp, target)
     return target
 

@@ -11,6 +11,8 @@
 #include <exception>
 #include <string>
 #include <vector>
+#include <thread>
+#include <algorithm>
 
 #include "cdtref/cdt.hpp"
 #include "cdtref/mesh.hpp"
@@ -217,30 +219,59 @@ int gdp2d_host_write_node_ele(const gdp2d_mesh_view* v, char** node, char** ele)
 int gdp2d_host_format_node_ele(uint32_t n_nodes, const double* xy, const uint8_t* marker,
                                uint32_t n_tris, const uint32_t* tri, char** node, char** ele) {
     try {
-        std::string nd = std::to_string(n_nodes) + " 2 0 1\n";
-        nd.reserve(nd.size() + 48ull * n_nodes);
-        for (uint32_t i = 0; i < n_nodes; ++i) {
-            nd += std::to_string(i);
-            nd += ' ';
-            nd += cdtref::detail::shortest(xy[2 * i]);
-            nd += ' ';
-            nd += cdtref::detail::shortest(xy[2 * i + 1]);
-            nd += marker[i] ? " 1\n" : " 0\n";
-        }
-        std::string el = std::to_string(n_tris) + " 3 0\n";
-        el.reserve(el.size() + 32ull * n_tris);
-        for (uint32_t t = 0; t < n_tris; ++t) {
-            el += std::to_string(t);
-            for (int k = 0; k < 3; ++k) {
-                el += ' ';
-                el += std::to_string(tri[3ull * t + k]);
+        // Text of write_node_ele (pslg_io.hpp:294-319), formatted in parallel:
+        // each thread renders a contiguous block of lines, the blocks are
+        // concatenated in order (byte-identical to the serial loop).
+        unsigned nthr = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+        if (const char* e = std::getenv("GDP2D_IO_THREADS")) nthr = std::max(1, std::atoi(e));
+        auto render = [&](uint32_t n, size_t per_line, auto&& line) {
+            const uint32_t parts = (uint32_t)std::min<uint64_t>(nthr, std::max<uint32_t>(1, n / 4096));
+            std::vector<std::string> blk(parts);
+            std::vector<std::thread> th;
+            for (uint32_t p = 0; p < parts; ++p) {
+                th.emplace_back([&, p] {
+                    const uint32_t lo = (uint32_t)((uint64_t)n * p / parts);
+                    const uint32_t hi = (uint32_t)((uint64_t)n * (p + 1) / parts);
+                    std::string& out = blk[p];
+                    out.reserve(per_line * (hi - lo));
+                    for (uint32_t i = lo; i < hi; ++i) line(out, i);
+                });
             }
-            el += '\n';
-        }
-        *node = static_cast<char*>(std::malloc(nd.size() + 1));
-        *ele = static_cast<char*>(std::malloc(el.size() + 1));
-        std::memcpy(*node, nd.c_str(), nd.size() + 1);
-        std::memcpy(*ele, el.c_str(), el.size() + 1);
+            for (auto& t : th) t.join();
+            return blk;
+        };
+        const auto node_blocks = render(n_nodes, 48, [&](std::string& o, uint32_t i) {
+            o += std::to_string(i);
+            o += ' ';
+            o += cdtref::detail::shortest(xy[2 * i]);
+            o += ' ';
+            o += cdtref::detail::shortest(xy[2 * i + 1]);
+            o += marker[i] ? " 1\n" : " 0\n";
+        });
+        const auto ele_blocks = render(n_tris, 32, [&](std::string& o, uint32_t t) {
+            o += std::to_string(t);
+            for (int k = 0; k < 3; ++k) {
+                o += ' ';
+                o += std::to_string(tri[3ull * t + k]);
+            }
+            o += '\n';
+        });
+        auto join = [](const std::string& head, const std::vector<std::string>& blocks) {
+            size_t len = head.size();
+            for (const auto& b : blocks) len += b.size();
+            char* out = static_cast<char*>(std::malloc(len + 1));
+            size_t o = 0;
+            std::memcpy(out, head.data(), head.size());
+            o += head.size();
+            for (const auto& b : blocks) {
+                std::memcpy(out + o, b.data(), b.size());
+                o += b.size();
+            }
+            out[o] = 0;
+            return out;
+        };
+        *node = join(std::to_string(n_nodes) + " 2 0 1\n", node_blocks);
+        *ele = join(std::to_string(n_tris) + " 3 0\n", ele_blocks);
         return 0;
     } catch (const std::exception& e) {
         g_err = e.what();

@@ -80,3 +80,24 @@ def test_cli_device_cdt(built, tmp_path):
     kv = dict(t.split("=") for t in r.stdout.split())
     assert int(kv["bad_triangles"]) == 0 and int(kv["steiner_points"]) > 0
     assert (tmp_path / "out.ele").exists()
+
+
+@pytest.mark.gpu
+def test_cli_device_io_same_bytes(built, tmp_path):
+    """--device-io (device validators, device compaction, parallel text) writes
+    the same .node/.ele bytes as the host path (write_node_ele) for the same
+    refinement, with and without the device CDT."""
+    from paper_2007_00324_b200 import host
+    pts, segs = host.generate_pslg(30_000, 3_000, "uniform", 8)
+    poly = tmp_path / "in.poly"
+    write_poly(poly, pts, segs)
+    outs = {}
+    for tag, flags in {"host": [], "dio": ["--device-io"], "dcdt": ["--device-cdt"],
+                       "dcdt_dio": ["--device-cdt", "--device-io"]}.items():
+        r = subprocess.run([str(CLI), str(poly), "--out", str(tmp_path / tag)] + flags,
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, (tag, r.stdout + r.stderr)
+        outs[tag] = ((tmp_path / f"{tag}.node").read_bytes(), (tmp_path / f"{tag}.ele").read_bytes(),
+                     r.stdout.split("wall_seconds")[0])
+    assert outs["host"][:2] == outs["dio"][:2] and outs["host"][2] == outs["dio"][2]
+    assert outs["dcdt"][:2] == outs["dcdt_dio"][:2]

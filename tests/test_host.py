@@ -70,3 +70,24 @@ def test_close_hull_matches_build_cdt_segments():
     _, closed_ref = host.build_cdt(pts, segs)
     np.testing.assert_array_equal(closed, closed_ref)
     assert len(closed) > len(segs)
+
+
+def test_parallel_node_ele_formatting_is_byte_identical(monkeypatch):
+    """format_node_ele renders blocks of lines on several threads and joins
+    them in order: the text must not depend on the thread count."""
+    import numpy as np
+    from paper_2007_00324_b200 import host
+    rng = np.random.default_rng(3)
+    n, m = 50_000, 90_000
+    xy = rng.uniform(-1e3, 1e3, size=(n, 2))
+    xy[::7] = np.round(xy[::7], 2)
+    marker = (rng.random(n) < 0.1).astype(np.uint8)
+    tri = rng.integers(0, n, size=(m, 3)).astype(np.uint32)
+    monkeypatch.setenv("GDP2D_IO_THREADS", "1")
+    a = host.format_node_ele(xy, marker, tri)
+    monkeypatch.setenv("GDP2D_IO_THREADS", "7")
+    b = host.format_node_ele(xy, marker, tri)
+    assert a == b
+    node, ele = a
+    assert node.startswith(f"{n} 2 0 1\n") and ele.startswith(f"{m} 3 0\n")
+    assert node.count("\n") == n + 1 and ele.count("\n") == m + 1
