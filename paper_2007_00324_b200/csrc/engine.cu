@@ -356,6 +356,8 @@ struct gdp2d_ctx {
     u32 c_prev = 0;               // previous batch's candidate count (host, after its sync)
     bool have_c_prev = false;
     bool sync_collect = false;    // GDP2D_SYNC_COLLECT=1: host round trip after every collect
+    bool regions_tight = false;   // GDP2D_REGIONS_TIGHT=1 (tests): advertise half the region
+                                  // capacity to no-round-trip batches, forcing the redo path
     u32 small_nv = 256;           // GDP2D_SMALL_NV: block-mode insertion at or below
     u32 small_wl = 256;           // GDP2D_SMALL_WL: block-mode Lawson below this list size
     u32 small_c = 256;            // GDP2D_SMALL_C: whole batch in one CTA at or below
@@ -624,6 +626,7 @@ void ctx_init(gdp2d_ctx* x, int device) {
     const char* lr = std::getenv("GDP2D_LAWSON");
     x->lawson_rounds = lr && std::string(lr) == "rounds";
     if (const char* e = std::getenv("GDP2D_SYNC_COLLECT")) x->sync_collect = e[0] == '1';
+    if (const char* e = std::getenv("GDP2D_REGIONS_TIGHT")) x->regions_tight = e[0] == '1';
     x->lawson_grid = lawson_persistent_grid(device);
     x->insert_grid = insert_persistent_grid(device);
     x->rollback_grid = rollback_persistent_grid(device);
@@ -1144,7 +1147,8 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
                                                                         : 0;
         const u32 rs = isolate ? isolated_stride(ncav) : ncav + 1 + MAX_CLAIM_EXTRA;
         if (!ncs) ensure_regions(x, C, ncav, rs);
-        const u32 reg_cap = (u32)std::min<size_t>(x->reg_cap / rs, x->rl_cap);
+        u32 reg_cap = (u32)std::min<size_t>(x->reg_cap / rs, x->rl_cap);
+        if (ncs && x->regions_tight) reg_cap = std::min(reg_cap, x->c_prev / 2);
         CK(cudaMemsetAsync(x->ins_state + 8, 0, sizeof(u32), st));   // unsafe flag
         const u32 batch = ++x->epoch;
         u32 flip_rounds = 0, rm_rounds = 0;
@@ -1202,9 +1206,11 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
                                    nv, nt, ns, flip_rounds, rm_rounds)) {
                 // the list outgrew the region buffers: grow them, redo the batch
                 // (collect recomputes the same list from its cached verdicts)
+                // (the redo takes the synchronous path: it knows C exactly)
                 ensure_regions(x, x->h_tot[3], ncav, rs);
                 --x->epoch;
                 x->c_prev = x->h_tot[3];
+                x->have_c_prev = false;
                 --iter;
                 continue;
             }

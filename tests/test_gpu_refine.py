@@ -154,6 +154,32 @@ def test_growth_paths_identical(built, monkeypatch):
     check_invariants(b, pts, closed, q, cdt_check=False)
 
 
+def test_collect_round_trip_paths_identical(built, monkeypatch):
+    """The candidate count stays on the device between collect and insertion;
+    the synchronous path (GDP2D_SYNC_COLLECT=1) and the region-overflow redo
+    (GDP2D_REGIONS_TIGHT=1 makes every no-round-trip batch overflow and redo)
+    must give bit-identical meshes."""
+    from paper_2007_00324_b200 import Engine, QualityCriteria, host
+    pts, segs = host.generate_pslg(40_000, 4_000, "gaussian", 13)
+    m, closed = host.build_cdt(pts, segs)
+    q = QualityCriteria(B_SQRT2_THETA)
+    outs = []
+    for env in ({}, {"GDP2D_SYNC_COLLECT": "1"}, {"GDP2D_REGIONS_TIGHT": "1"}):
+        for k in ("GDP2D_SYNC_COLLECT", "GDP2D_REGIONS_TIGHT"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        with Engine(0) as eng:
+            eng.upload(m)
+            rep = eng.refine(q)
+            outs.append((rep, eng.download()))
+    base = outs[0][1]
+    for rep, out in outs[1:]:
+        assert rep.bad_triangles == 0 and len(rep.batches) == len(outs[0][0].batches)
+        for name in ("xy", "tri_v", "tri_n", "tri_seg", "tri_alive", "seg_v", "seg_alive"):
+            assert np.array_equal(getattr(base, name), getattr(out, name)), name
+
+
 def test_pinned_round_trip(built):
     """Engine.upload from / download_to page-locked pools (the bench e2e path)."""
     from paper_2007_00324_b200 import Engine, PinnedPool, QualityCriteria, host
