@@ -356,6 +356,9 @@ struct gdp2d_ctx {
     u32 c_prev = 0;               // previous batch's candidate count (host, after its sync)
     bool have_c_prev = false;
     bool sync_collect = false;    // GDP2D_SYNC_COLLECT=1: host round trip after every collect
+    u32 half_grid_c = 100000;     // GDP2D_HALF_GRID_C: batches below this many candidates run the
+                                  // persistent kernels on one CTA per SM (cheaper grid barriers)
+    u32 quarter_grid_c = 10000;   // GDP2D_QUARTER_GRID_C: ... below this on half the SMs
     bool regions_tight = false;   // GDP2D_REGIONS_TIGHT=1 (tests): advertise half the region
                                   // capacity to no-round-trip batches, forcing the redo path
     u32 small_nv = 256;           // GDP2D_SMALL_NV: block-mode insertion at or below
@@ -627,10 +630,19 @@ void ctx_init(gdp2d_ctx* x, int device) {
     x->lawson_rounds = lr && std::string(lr) == "rounds";
     if (const char* e = std::getenv("GDP2D_SYNC_COLLECT")) x->sync_collect = e[0] == '1';
     if (const char* e = std::getenv("GDP2D_REGIONS_TIGHT")) x->regions_tight = e[0] == '1';
+    if (const char* e = std::getenv("GDP2D_HALF_GRID_C")) x->half_grid_c = (u32)std::atoll(e);
+    if (const char* e = std::getenv("GDP2D_QUARTER_GRID_C")) x->quarter_grid_c = (u32)std::atoll(e);
     x->lawson_grid = lawson_persistent_grid(device);
     x->insert_grid = insert_persistent_grid(device);
     x->rollback_grid = rollback_persistent_grid(device);
     x->lawson_grid2 = lawson_batch_grid(device);
+    if (const char* e = std::getenv("GDP2D_GRID")) {   // experiments: fewer co-resident CTAs
+        const int g = std::atoi(e);
+        if (g > 0) {
+            x->insert_grid = std::min(x->insert_grid, g);
+            x->rollback_grid = std::min(x->rollback_grid, g);
+        }
+    }
     CK(cudaMalloc(&x->sel_state, select_state_bytes()));
     x->little_cap = cavity_resident_candidates(device);
     if (const char* e = std::getenv("GDP2D_LAWSON_KERNEL")) x->lawson_kernel = e[0] == '1';
@@ -956,9 +968,16 @@ void check_structure_now(gdp2d_ctx* x, u32 nV, u32 nT, u32 nS, const char* where
 // Returns false when the candidate list outgrew the region buffers (the batch
 // did nothing; the caller grows them and redoes it).  x->h_tot[3] = C.
 bool insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, int prefiltered, u32 reg_cap,
-                       u32 ncav, u32 rs, int isolate, u32 batch, u32& nv, u32& nt, u32& ns,
-                       u32& flip_rounds, u32& rm_rounds) {
+                       u32 c_est, u32 ncav, u32 rs, int isolate, u32 batch, u32& nv, u32& nt,
+                       u32& ns, u32& flip_rounds, u32& rm_rounds) {
     cudaStream_t st = x->st;
+    // Smaller batches run the persistent kernels on fewer co-resident CTAs:
+    // their phases have little parallel work and a grid barrier's cost grows
+    // with the CTA count (measured: cfg 2 42.6 -> 40.5 ms with the half grid
+    // below 100K candidates; identical output for any grid size).
+    const int div = c_est < x->quarter_grid_c ? 4 : c_est < x->half_grid_c ? 2 : 1;
+    const int g_ins = std::max(1, x->insert_grid / div);
+    const int g_rb = std::max(1, x->rollback_grid / div);
     for (int attempt = 0;; ++attempt) {
         CK(cudaMemsetAsync(x->ring, 0, 5 * sizeof(RoundCtr), st));
         InsertLaunch L;
@@ -1011,14 +1030,12 @@ bool insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, int prefiltered, u32
         const int mode = p->mode == GDP2D_CHEW ? 1 : 0;
         const int k1 = x->lawson_kernel ? (1 | 4) : 1;
         if (!x->check) {
-            launch_insert_persistent(L, mode, x->insert_grid, x->rollback_grid, st, x->ev_k[1],
-                                     k1 | 2, x->lawson_grid2);
+            launch_insert_persistent(L, mode, g_ins, g_rb, st, x->ev_k[1], k1 | 2, x->lawson_grid2);
         } else {
             // GDP2D_CHECK=1: structural validation after each kernel
-            launch_insert_persistent(L, mode, x->insert_grid, x->rollback_grid, st, x->ev_k[1],
-                                     k1, x->lawson_grid2);
+            launch_insert_persistent(L, mode, g_ins, g_rb, st, x->ev_k[1], k1, x->lawson_grid2);
             check_structure_now(x, x->work.m.nV, x->work.m.nT, x->work.m.nS, "split kernel");
-            launch_insert_persistent(L, mode, x->insert_grid, x->rollback_grid, st, nullptr, 2);
+            launch_insert_persistent(L, mode, g_ins, g_rb, st, nullptr, 2);
             check_structure_now(x, x->work.m.nV, x->work.m.nT, x->work.m.nS, "rollback kernel");
         }
         CK(cudaEventRecord(x->ev_k[2], st));
@@ -1202,8 +1219,8 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
                 CK(cudaEventRecord(x->ev[4], st));
                 CK(cudaEventRecord(x->ev[5], st));
             }
-            if (!insert_persistent(x, p, standalone ? 1 : 0, reg_cap, ncav, rs, isolate, batch,
-                                   nv, nt, ns, flip_rounds, rm_rounds)) {
+            if (!insert_persistent(x, p, standalone ? 1 : 0, reg_cap, ncs ? x->c_prev : C, ncav,
+                                   rs, isolate, batch, nv, nt, ns, flip_rounds, rm_rounds)) {
                 // the list outgrew the region buffers: grow them, redo the batch
                 // (collect recomputes the same list from its cached verdicts)
                 // (the redo takes the synchronous path: it knows C exactly)
