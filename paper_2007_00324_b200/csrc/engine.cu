@@ -359,6 +359,7 @@ struct gdp2d_ctx {
     u32 half_grid_c = 100000;     // GDP2D_HALF_GRID_C: batches below this many candidates run the
                                   // persistent kernels on one CTA per SM (cheaper grid barriers)
     u32 quarter_grid_c = 10000;   // GDP2D_QUARTER_GRID_C: ... below this on half the SMs
+    u32 eighth_grid_c = 0;        // GDP2D_EIGHTH_GRID_C: ... below this on a quarter of the SMs
     bool regions_tight = false;   // GDP2D_REGIONS_TIGHT=1 (tests): advertise half the region
                                   // capacity to no-round-trip batches, forcing the redo path
     u32 small_nv = 256;           // GDP2D_SMALL_NV: block-mode insertion at or below
@@ -632,6 +633,7 @@ void ctx_init(gdp2d_ctx* x, int device) {
     if (const char* e = std::getenv("GDP2D_REGIONS_TIGHT")) x->regions_tight = e[0] == '1';
     if (const char* e = std::getenv("GDP2D_HALF_GRID_C")) x->half_grid_c = (u32)std::atoll(e);
     if (const char* e = std::getenv("GDP2D_QUARTER_GRID_C")) x->quarter_grid_c = (u32)std::atoll(e);
+    if (const char* e = std::getenv("GDP2D_EIGHTH_GRID_C")) x->eighth_grid_c = (u32)std::atoll(e);
     x->lawson_grid = lawson_persistent_grid(device);
     x->insert_grid = insert_persistent_grid(device);
     x->rollback_grid = rollback_persistent_grid(device);
@@ -975,7 +977,10 @@ bool insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, int prefiltered, u32
     // their phases have little parallel work and a grid barrier's cost grows
     // with the CTA count (measured: cfg 2 42.6 -> 40.5 ms with the half grid
     // below 100K candidates; identical output for any grid size).
-    const int div = c_est < x->quarter_grid_c ? 4 : c_est < x->half_grid_c ? 2 : 1;
+    const int div = c_est < x->eighth_grid_c     ? 8
+                    : c_est < x->quarter_grid_c ? 4
+                    : c_est < x->half_grid_c    ? 2
+                                                : 1;
     const int g_ins = std::max(1, x->insert_grid / div);
     const int g_rb = std::max(1, x->rollback_grid / div);
     for (int attempt = 0;; ++attempt) {
@@ -1462,7 +1467,14 @@ void build_cdt(gdp2d_ctx* x, const double* xy, u32 N, const u32* seg, u32 M,
         cdt_grow(c.pmap, c.pcap, pcap);
         c.pcap = pcap;
     }
-    const int g1 = cdt_grid(x->device, 0), g2 = cdt_grid(x->device, 1);
+    int g1 = cdt_grid(x->device, 0), g2 = cdt_grid(x->device, 1);
+    if (const char* e = std::getenv("GDP2D_CDT_GRID")) {   // experiments
+        const int g = std::atoi(e);
+        if (g > 0) {
+            g1 = std::min(g1, g);
+            g2 = std::min(g2, g);
+        }
+    }
     if ((u32)std::max(g1, g2) > c.part_cap) {
         c.part_cap = (u32)std::max(g1, g2);
         dfree(c.part);

@@ -41,6 +41,10 @@
 
 namespace cg = cooperative_groups;
 
+#ifndef GDP2D_CDT_MINB
+#define GDP2D_CDT_MINB 2   // CTAs per SM the Delaunay kernel is compiled for
+#endif
+
 namespace gdp2d {
 
 namespace {
@@ -138,7 +142,7 @@ __device__ __forceinline__ void relocate(const CdtArgs& a, u32 i, u32 t) {
 
 // state[]: CDT_ST_ROUNDS insertion rounds, CDT_ST_FLIP_ROUNDS, CDT_ST_STEPS,
 // [0] = triangles in use at the end.
-__global__ void __launch_bounds__(CDT_BLOCK) k_cdt_delaunay(CdtArgs a) {
+__global__ void __launch_bounds__(CDT_BLOCK, GDP2D_CDT_MINB) k_cdt_delaunay(CdtArgs a) {
     cg::grid_group g = cg::this_grid();
     const u32 tid = (u32)g.thread_rank(), nthr = (u32)g.size();
     const u32 lane = threadIdx.x & 31u;
