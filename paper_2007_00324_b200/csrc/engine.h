@@ -187,7 +187,11 @@ void launch_lawson_persistent(const DevMesh& m, u32 round0, u32 cur0, u32 n0, u3
                               int grid, cudaStream_t st);
 // The whole insertion phase of a batch (phase 1 splits, Lawson, detect +
 // rollback loops) as one persistent cooperative launch (k_insert.cu).
-constexpr int INSERT_BLOCK = 256;
+#ifndef GDP2D_INSERT_BLOCK
+#define GDP2D_INSERT_BLOCK 256
+#endif
+constexpr int INSERT_BLOCK = GDP2D_INSERT_BLOCK;
+constexpr int ROLLBACK_BLOCK = 256;   // the rollback kernel's frame needs the 255-register budget
 struct InsertLaunch {
     DevMesh m;            // counts before the batch
     DevCands c;

@@ -1373,7 +1373,7 @@ __global__ void __launch_bounds__(INSERT_BLOCK, GDP2D_LAWSON_MINB) k_batch_lawso
 
 // Kernel 2: phase 3 rollback (skipped when kernel 1 asked for growth).
 template <int MODE>
-__global__ void __launch_bounds__(INSERT_BLOCK) k_batch_rollback(InsertArgs a) {
+__global__ void __launch_bounds__(ROLLBACK_BLOCK) k_batch_rollback(InsertArgs a) {
     if (vload(&a.state[0]) != INS_OK) return;
     // isolated insertions cannot create redundant or dependent points: the
     // detection runs only when some survivor came from a capped claim set
@@ -1388,11 +1388,11 @@ __global__ void __launch_bounds__(INSERT_BLOCK) k_batch_rollback(InsertArgs a) {
 }
 
 template <class K0, class K1>
-static int coop_grid(K0 k0, K1 k1, int device) {
+static int coop_grid(K0 k0, K1 k1, int device, int block = INSERT_BLOCK) {
     int sms = 0, per0 = 0, per1 = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per0, k0, INSERT_BLOCK, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per1, k1, INSERT_BLOCK, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per0, k0, block, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per1, k1, block, 0);
     return std::max(1, sms * std::max(1, std::min(per0, per1)));
 }
 
@@ -1403,7 +1403,7 @@ int lawson_batch_grid(int device) {
     return coop_grid(k_batch_lawson<0>, k_batch_lawson<1>, device);
 }
 int rollback_persistent_grid(int device) {
-    return coop_grid(k_batch_rollback<0>, k_batch_rollback<1>, device);
+    return coop_grid(k_batch_rollback<0>, k_batch_rollback<1>, device, ROLLBACK_BLOCK);
 }
 
 void launch_insert_persistent(const InsertLaunch& L, int mode, int grid, int grid2, cudaStream_t st,
@@ -1460,7 +1460,7 @@ void launch_insert_persistent(const InsertLaunch& L, int mode, int grid, int gri
     if (which & 2) {
         note_launch();
         cudaLaunchCooperativeKernel(mode ? (void*)k_batch_rollback<1> : (void*)k_batch_rollback<0>,
-                                    dim3(grid2), dim3(INSERT_BLOCK), args, 0, st);
+                                    dim3(grid2), dim3(ROLLBACK_BLOCK), args, 0, st);
     }
 }
 
