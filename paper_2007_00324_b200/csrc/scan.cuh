@@ -72,6 +72,7 @@ __device__ __forceinline__ void block_add(T* ctr, T v) {
     if ((threadIdx.x & 31) == 0 && v) atomicAdd(&acc, v);
     __syncthreads();
     if (threadIdx.x == 0 && acc) atomicAdd(ctr, acc);
+    __syncthreads();   // the next call's reset must not overtake this read
 }
 
 }  // namespace gdp2d
