@@ -268,7 +268,8 @@ void launch_lawson_persistent(const DevMesh& m, u32 round0, u32 cur0, u32 n0, u3
 
 // Star of v in rotation order (incident_triangles, mesh.hpp:145-171, interior
 // case).  Returns the size, or 0 if the fan is open / too large.
-__device__ __forceinline__ int walk_star(const DevMesh& m, u32 v, u32* st, int* si, int cap) {
+__device__ __forceinline__ int walk_star(const DevMesh& m, u32 v, u32* st, int* si, int cap,
+                                         u32* nb = nullptr) {
     const u32 t0 = m.vtri[v];
     if (t0 == NONE) return 0;
     u32 cur = t0;
@@ -279,6 +280,7 @@ __device__ __forceinline__ int walk_star(const DevMesh& m, u32 v, u32* st, int* 
         if (i < 0 || k >= cap) return 0;
         st[k] = cur;
         si[k] = i;
+        if (nb) nb[k] = comp(tv, nxt(i));   // the star's next link vertex
         ++k;
         const u32 c = comp(m.tn[cur], nxt(i));
         if (c == NONE) return 0;
@@ -294,16 +296,35 @@ __device__ __forceinline__ bool prio_gt(const FreshInfo& f, u32 a, u32 b) {
 
 // (a) a same-batch circumcenter that encroaches a splittable subsegment of
 // its star is redundant; the lowest-id such subsegment is marked.
+// collect_dep != 0 (the any-higher-neighbour rule): the same star walk also
+// lists the higher-priority same-batch circumcenters around v (hlist/hcnt,
+// 255 = too many), so detect_b_fast needs no second walk.
 template <int MODE>
-__device__ __noinline__ u32 detect_a_one(const DevMesh& m, u64 depth_cap, u32 V0, u32 j,
-                                         const FreshInfo& f, Counters* ctr) {
+__device__ __noinline__ u32 detect_a_one(const DevMesh& m, u64 depth_cap, u32 V0, u32 F, u32 j,
+                                         const FreshInfo& f, Counters* ctr, int collect_dep) {
     u32 marked = 0;
     uint8_t mark = 0;
     const u32 v = V0 + j;
+    if (collect_dep) f.hcnt[j] = 0;
     if (f.cc[j] && !f.removed[j]) {
-        u32 st[MAX_STAR];
+        u32 st[MAX_STAR], nb[MAX_STAR];
         int si[MAX_STAR];
-        const int k = walk_star(m, v, st, si, MAX_STAR);
+        const int k = walk_star(m, v, st, si, MAX_STAR, nb);
+        if (collect_dep) {
+            u32 cnt = 0;
+            for (int q = 0; q < k; ++q) {
+                const u32 x = nb[q];
+                if (x < V0 || x >= V0 + F) continue;
+                const u32 jx = x - V0;
+                if (!f.cc[jx] || f.removed[jx] == 1 || !prio_gt(f, jx, j)) continue;
+                if (cnt == (u32)DEP_HMAX) {
+                    cnt = 255;
+                    break;
+                }
+                f.hlist[(size_t)j * DEP_HMAX + cnt++] = jx;
+            }
+            f.hcnt[j] = (uint8_t)cnt;
+        }
         if (k == 0 && atomicCAS(&ctr->err_code, 0u, (u32)DERR_OPEN_STAR) == 0u) {
             // dbg: vtri, alive, fresh index, xy, walk steps, reason
             // (1 vertex missing from a fan triangle, 2 star > MAX_STAR, 3 open fan)
@@ -352,7 +373,7 @@ template <int MODE>
 __global__ void k_detect_a(DevMesh m, u64 depth_cap, u32 V0, u32 F, FreshInfo f, Counters* ctr) {
     const u32 j = blockIdx.x * blockDim.x + threadIdx.x;
     u32 marked = 0;
-    if (j < F) marked = detect_a_one<MODE>(m, depth_cap, V0, j, f, ctr);
+    if (j < F) marked = detect_a_one<MODE>(m, depth_cap, V0, F, j, f, ctr, 0);
     warp_add_u32(&ctr->marked, marked);
 }
 
@@ -373,6 +394,24 @@ __device__ __noinline__ void detect_b_one(const DevMesh& m, u32 V0, u32 F, u32 j
         if (prio_gt(f, jx, j)) {
             f.mark[j] = 2;
             break;
+        }
+    }
+}
+
+// (b) from the list detect_a_one collected: the first higher-priority
+// neighbour that is not itself redundant makes v dependent.
+__device__ __forceinline__ void detect_b_fast(const DevMesh& m, u32 V0, u32 F, u32 j,
+                                              const FreshInfo& f) {
+    if (!f.cc[j] || f.removed[j] || f.mark[j] == 1) return;
+    const u32 cnt = f.hcnt[j];
+    if (cnt == 255) {
+        detect_b_one(m, V0, F, j, f);
+        return;
+    }
+    for (u32 q = 0; q < cnt; ++q) {
+        if (f.mark[f.hlist[(size_t)j * DEP_HMAX + q]] != 1) {
+            f.mark[j] = 2;
+            return;
         }
     }
 }
@@ -1175,7 +1214,7 @@ __device__ void rollback_loop(const InsertArgs& a, const Exec& ex, u32 nv, u32 n
         for (u32 j = ex.tid; j < F; j += ex.nthr) {
             if (a.f.dirty[j] == 0) continue;   // not a suspect since the last pass
             a.f.dirty[j] = 2;
-            marked += detect_a_one<MODE>(m, a.depth_cap, V0, j, a.f, a.ctr);
+            marked += detect_a_one<MODE>(m, a.depth_cap, V0, F, j, a.f, a.ctr, !a.dep_mis);
         }
         ex.sync();
         trace(a, ex.leader(), TR_DET_A);
@@ -1183,7 +1222,7 @@ __device__ void rollback_loop(const InsertArgs& a, const Exec& ex, u32 nv, u32 n
             for (u32 j = ex.tid; j < F; j += ex.nthr) {
                 if (a.f.dirty[j] != 2) continue;
                 a.f.dirty[j] = 0;
-                detect_b_one(m, V0, F, j, a.f);
+                detect_b_fast(m, V0, F, j, a.f);
             }
             ex.sync();
         } else {
