@@ -554,7 +554,9 @@ __device__ __noinline__ u32 rm_apply_one(const DevMesh& m, const u32* __restrict
         const u32* st = w.star + (size_t)i * MAX_STAR;
         const int k = (int)w.star_len[i];
         bool own = k >= 3;
-        for (int q = 0; q < k && own; ++q) own = x.owner[st[q]] == v;
+        // independent loads, no early exit: the claims arrive together
+#pragma unroll 8
+        for (int q = 0; q < k; ++q) own &= x.owner[st[q]] == v;
         if (k >= 3 && !own) {
             const u32 o = agg_reserve(&rc->rm_next, 1u);
             if (o < w.rm_cap) w.rm[next_list][o] = v;
@@ -564,12 +566,14 @@ __device__ __noinline__ u32 rm_apply_one(const DevMesh& m, const u32* __restrict
             uint8_t PK[MAX_STAR];  // 1 = old outer ref, 2 = local (idx<<2|slot), 0 = none
             int NX[MAX_STAR], PV[MAX_STAR];
             double2 XY[MAX_STAR];  // link vertex coordinates, gathered once
+            // records of the whole star first (independent loads), then the
+            // link coordinates: two dependent levels instead of 2k
+#pragma unroll 4
             for (int q = 0; q < k; ++q) {
                 const u32 t = st[q];
                 const uint4 tv = m.tv[t], tn = m.tn[t], ts = m.ts[t];
                 const int iv = tv.x == v ? 0 : (tv.y == v ? 1 : 2);
                 L[q] = comp(tv, nxt(iv));
-                XY[q] = m.xy[L[q]];
                 R[q] = comp(tn, iv);
                 PK[q] = R[q] == NONE ? 0 : 1;
                 SG[q] = comp(ts, iv);
@@ -577,6 +581,8 @@ __device__ __noinline__ u32 rm_apply_one(const DevMesh& m, const u32* __restrict
                 NX[q] = q + 1 == k ? 0 : q + 1;
                 PV[q] = q == 0 ? k - 1 : q - 1;
             }
+#pragma unroll 4
+            for (int q = 0; q < k; ++q) XY[q] = m.xy[L[q]];
             // created triangles (local): vertices, refs, kinds, segs
             u32 CV[MAX_STAR][3];
             u32 CN[MAX_STAR][3];
@@ -695,19 +701,26 @@ __device__ __noinline__ u32 rm_apply_one(const DevMesh& m, const u32* __restrict
                     write_tri(m, st[ci], CV[ci][0], CV[ci][1], CV[ci][2], CN[ci][0], CN[ci][1],
                               CN[ci][2], pend, CS[ci][0], CS[ci][1], CS[ci][2]);
                 }
+                u32* tv_words = reinterpret_cast<u32*>(m.tv);
                 for (int q = created; q < k; ++q) {
-                    uint4 tv = m.tv[st[q]];
-                    tv.w = 0;
-                    m.tv[st[q]] = tv;
+                    tv_words[4 * (size_t)st[q] + 3] = 0;   // dead (no read-modify-write)
                     m.tflag[st[q]] = 2;
                 }
                 m.valive[v] = 0;
                 m.vtri[v] = NONE;
                 f.removed[v - V0] = 1;
                 push_touched(w, st, created, rc);
-                for (int ci = 0; ci < created; ++ci) {
-                    const u32 codes[3] = {enc(st[ci], 0), enc(st[ci], 1), enc(st[ci], 2)};
-                    push_work(w, widx, codes, 3, ctr, seed_rc);
+                {
+                    // every edge of the rebuilt hole seeds the Lawson pass: one
+                    // reservation for all of them
+                    const u32 ns = 3u * (u32)created;
+                    const u32 o = agg_reserve(&seed_rc->wl_next, ns);
+                    if (o + ns > w.cap) {
+                        raise_err(ctr, DERR_WORKLIST_OVERFLOW, o);
+                    } else {
+                        for (int ci = 0; ci < created; ++ci)
+                            for (int e = 0; e < 3; ++e) w.w[widx][o + 3 * ci + e] = enc(st[ci], e);
+                    }
                 }
                 done = 1;
             }
