@@ -984,7 +984,7 @@ bool insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, int prefiltered, u32
     const int g_ins = std::max(1, x->insert_grid / div);
     const int g_rb = std::max(1, x->rollback_grid / div);
     for (int attempt = 0;; ++attempt) {
-        CK(cudaMemsetAsync(x->ring, 0, 5 * sizeof(RoundCtr), st));
+        if (attempt > 0) CK(cudaMemsetAsync(x->ring, 0, 5 * sizeof(RoundCtr), st));
         InsertLaunch L;
         L.m = x->work.m;
         L.c = x->c;
@@ -1030,7 +1030,8 @@ bool insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, int prefiltered, u32
             CK(cudaMemsetAsync(x->tr.d_trace_n, 0, sizeof(u32), st));
         }
         x->tr.mark("pre_ins", st);
-        CK(cudaMemsetAsync(x->ins_state, 0, 8 * sizeof(u32), st));   // word 8 = unsafe flag stays
+        // word 8 = unsafe flag stays; attempt 0's words were zeroed by the scan
+        if (attempt > 0) CK(cudaMemsetAsync(x->ins_state, 0, 8 * sizeof(u32), st));
         CK(cudaEventRecord(x->ev_k[0], st));
         const int mode = p->mode == GDP2D_CHEW ? 1 : 0;
         const int k1 = x->lawson_kernel ? (1 | 4) : 1;
@@ -1128,6 +1129,10 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
         x->tr.mark("start", st);
         CollectCache cache;
         cache.full = (x->full_scan || x->full_collect) ? 1 : 0;
+        cache.zero[0] = reinterpret_cast<u32*>(x->ring);
+        cache.zero_n[0] = (u32)(5 * sizeof(RoundCtr) / 4);
+        cache.zero[1] = x->ins_state;
+        cache.zero_n[1] = 9;   // status words + the unsafe flag
         bool tris_scanned = false;
         // No host round trip after collect (ncs): the count stays on the
         // device; the filter kernels read it, the loop learns it with the
@@ -1171,7 +1176,7 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
         if (!ncs) ensure_regions(x, C, ncav, rs);
         u32 reg_cap = (u32)std::min<size_t>(x->reg_cap / rs, x->rl_cap);
         if (ncs && x->regions_tight) reg_cap = std::min(reg_cap, x->c_prev / 2);
-        CK(cudaMemsetAsync(x->ins_state + 8, 0, sizeof(u32), st));   // unsafe flag
+        // (the scan zeroed the step ring, the status words and the unsafe flag)
         const u32 batch = ++x->epoch;
         u32 flip_rounds = 0, rm_rounds = 0;
         u32 nv = 0, nt = 0, ns = 0;

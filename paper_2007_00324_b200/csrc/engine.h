@@ -60,6 +60,10 @@ struct CollectBufs {
 // cache this only matters for the full flag).
 struct CollectCache {
     int full = 1;                 // 1 = recompute every element (ignore the dirty bits)
+    // words the first CTA of the scan zeroes for the insertion kernels that
+    // follow (step ring + status words): saves the per-batch memsets
+    u32* zero[2] = {nullptr, nullptr};
+    u32 zero_n[2] = {0, 0};
 };
 u32 launch_collect(const DevMesh& m, const Quality& q, bool rule4, uint8_t* flags, DevCands c,
                    u32 ccap, ScanScratch& s, Counters* d_ctr, cudaStream_t st,

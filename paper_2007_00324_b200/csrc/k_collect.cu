@@ -58,8 +58,13 @@ template <int MODE>
 __global__ void __launch_bounds__(SCAN_BLOCK) k_collect_flags(DevMesh m, Quality q, CollectRange r,
                                                            uint8_t* __restrict__ flags,
                                                            u32* __restrict__ partial, int full,
-                                                           Counters* ctr) {
+                                                           Counters* ctr, u32* z0, u32 n0, u32* z1,
+                                                           u32 n1) {
     __shared__ u32 sh[SCAN_BLOCK / 32 + 1];
+    if (blockIdx.x == 0) {
+        for (u32 k = threadIdx.x; k < n0; k += blockDim.x) z0[k] = 0;
+        for (u32 k = threadIdx.x; k < n1; k += blockDim.x) z1[k] = 0;
+    }
     const bool is_sub = blockIdx.x < r.tilesS;
     const u32 tile = is_sub ? blockIdx.x : blockIdx.x - r.tilesS;
     const u32 n = is_sub ? r.nS : r.nT;
@@ -187,6 +192,8 @@ u32 launch_collect(const DevMesh& m, const Quality& q, bool rule4, uint8_t* flag
                    const CollectCache& cache, bool* tris_scanned, u32* d_count,
                    cudaEvent_t ev_scan0, cudaEvent_t ev_scan1, bool sync) {
     *tris_scanned = false;
+    u32 *zp0 = cache.zero[0], *zp1 = cache.zero[1];
+    u32 zn0 = cache.zero_n[0], zn1 = cache.zero_n[1];
     // sync == false (rule 4 only): no host round trip -- the scatter runs
     // unconditionally and the count stays on the device (*d_count)
     if (!sync && !rule4) sync = true;
@@ -199,6 +206,9 @@ u32 launch_collect(const DevMesh& m, const Quality& q, bool rule4, uint8_t* flag
         r.tilesT = (r.nT + SCAN_TILE - 1) / SCAN_TILE;
         const u32 tiles = r.tilesS + r.tilesT;
         if (tiles == 0) {
+            if (zn0) cudaMemsetAsync(zp0, 0, 4ull * zn0, st);
+            if (zn1) cudaMemsetAsync(zp1, 0, 4ull * zn1, st);
+            zn0 = zn1 = 0;
             cudaMemsetAsync(d_count, 0, sizeof(u32), st);
             return 0;
         }
@@ -209,9 +219,10 @@ u32 launch_collect(const DevMesh& m, const Quality& q, bool rule4, uint8_t* flag
         }
         if (ev_scan0 && sub) cudaEventRecord(ev_scan0, st);
         if (q.mode == 0)
-            note_launch(), k_collect_flags<0><<<tiles, SCAN_BLOCK, 0, st>>>(m, q, r, flags, s.partial, cache.full, d_ctr);
+            note_launch(), k_collect_flags<0><<<tiles, SCAN_BLOCK, 0, st>>>(m, q, r, flags, s.partial, cache.full, d_ctr, zp0, zn0, zp1, zn1);
         else
-            note_launch(), k_collect_flags<1><<<tiles, SCAN_BLOCK, 0, st>>>(m, q, r, flags, s.partial, cache.full, d_ctr);
+            note_launch(), k_collect_flags<1><<<tiles, SCAN_BLOCK, 0, st>>>(m, q, r, flags, s.partial, cache.full, d_ctr, zp0, zn0, zp1, zn1);
+        zn0 = zn1 = 0;   // zeroed once
         if (ev_scan1 && (tri || !rule4)) cudaEventRecord(ev_scan1, st);
         scan_partials(s.partial, tiles, d_count, st);
         if (!sync) {
