@@ -46,7 +46,10 @@ void launch_claim(const DevMesh& m, DevCands c, NArg n, TriAux a, Counters* d_ct
     note_launch(), k_claim_reset<<<g, 256, 0, st>>>(c, n, m.nT, a.ckey, a.ctie);
 }
 
-__global__ void __launch_bounds__(128) k_cavity_bfs(DevMesh m, DevCands c, NArg na, u32 ncav,
+#ifndef GDP2D_CAVITY_MINB
+#define GDP2D_CAVITY_MINB 1
+#endif
+__global__ void __launch_bounds__(128, GDP2D_CAVITY_MINB) k_cavity_bfs(DevMesh m, DevCands c, NArg na, u32 ncav,
                                                     int extras, u32 rs,
                                                     u32* __restrict__ regions,
                                                     u32* __restrict__ region_len,
