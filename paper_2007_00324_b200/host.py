@@ -95,8 +95,16 @@ def write_node_ele(mesh: Mesh):
     rc = lib.gdp2d_host_write_node_ele(C.byref(v), C.byref(node), C.byref(ele))
     if rc:
         raise RuntimeError(lib.gdp2d_host_last_error().decode())
-    out = node.value.decode(), ele.value.decode()
-    return out
+    return _take_texts(lib, node, ele)
+
+
+def _take_texts(lib, node, ele):
+    """Decode two malloc'ed C strings from the host library and free them."""
+    try:
+        return node.value.decode(), ele.value.decode()
+    finally:
+        lib.gdp2d_host_free(C.cast(node, C.c_void_p))
+        lib.gdp2d_host_free(C.cast(ele, C.c_void_p))
 
 
 def format_node_ele(xy: np.ndarray, marker: np.ndarray, tri: np.ndarray):
@@ -112,7 +120,7 @@ def format_node_ele(xy: np.ndarray, marker: np.ndarray, tri: np.ndarray):
                                         tri.ctypes.data, C.byref(node), C.byref(ele))
     if rc:
         raise RuntimeError(lib.gdp2d_host_last_error().decode())
-    return node.value.decode(), ele.value.decode()
+    return _take_texts(lib, node, ele)
 
 
 def workload(config: int, seed: int = SEED):
