@@ -365,6 +365,8 @@ struct gdp2d_ctx {
     u32 small_nv = 256;           // GDP2D_SMALL_NV: block-mode insertion at or below
     u32 small_wl = 256;           // GDP2D_SMALL_WL: block-mode Lawson below this list size
     u32 small_c = 256;            // GDP2D_SMALL_C: whole batch in one CTA at or below
+    u32 standalone_c = 30000;     // GDP2D_STANDALONE_C: Lines 5-7 as standalone kernels only above this
+                                  // (smaller batches filter inside the grid-mode batch kernel)
     bool dep_mis = false;         // GDP2D_DEP=mis: dependent pairs by the priority-MIS rule
     bool check = false;           // GDP2D_CHECK=1: validate after each insertion kernel
     int extras = 2;               // GDP2D_EXTRAS: 2 rewrite table (default), 1 far side in main claims
@@ -630,6 +632,7 @@ void ctx_init(gdp2d_ctx* x, int device) {
     const char* lr = std::getenv("GDP2D_LAWSON");
     x->lawson_rounds = lr && std::string(lr) == "rounds";
     if (const char* e = std::getenv("GDP2D_SYNC_COLLECT")) x->sync_collect = e[0] == '1';
+    if (const char* e = std::getenv("GDP2D_STANDALONE_C")) x->standalone_c = (u32)std::atoll(e);
     if (const char* e = std::getenv("GDP2D_REGIONS_TIGHT")) x->regions_tight = e[0] == '1';
     if (const char* e = std::getenv("GDP2D_HALF_GRID_C")) x->half_grid_c = (u32)std::atoll(e);
     if (const char* e = std::getenv("GDP2D_QUARTER_GRID_C")) x->quarter_grid_c = (u32)std::atoll(e);
@@ -1201,9 +1204,9 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
             // Lines 5-7 as high-occupancy standalone kernels for big batches
             // (they skip C <= small_c: the batch kernel filters in one CTA)
             NArg na = NArg::host(C);
-            bool standalone = C > x->small_c;
+            bool standalone = C > std::max(x->small_c, x->standalone_c);
             if (ncs) {
-                standalone = x->c_prev > x->small_c;   // predicted from the last batch
+                standalone = x->c_prev > std::max(x->small_c, x->standalone_c);   // predicted
                 na.d_n = x->d_C;
                 na.skip_le = x->small_c;
                 na.cap = reg_cap;
