@@ -985,7 +985,11 @@ bool insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, int prefiltered, u32
                     : c_est < x->half_grid_c    ? 2
                                                 : 1;
     const int g_ins = std::max(1, x->insert_grid / div);
-    const int g_rb = std::max(1, x->rollback_grid / div);
+    static const int rb_div = [] {
+        const char* e = std::getenv("GDP2D_RB_DIV");   // experiments: extra divisor, rollback kernel
+        return e ? std::max(1, std::atoi(e)) : 1;
+    }();
+    const int g_rb = std::max(1, x->rollback_grid / (div * rb_div));
     for (int attempt = 0;; ++attempt) {
         if (attempt > 0) CK(cudaMemsetAsync(x->ring, 0, 5 * sizeof(RoundCtr), st));
         InsertLaunch L;
