@@ -32,12 +32,14 @@
 #ifndef GDP2D_CDTREF_HPP
 #define GDP2D_CDTREF_HPP
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
 #include <map>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "gdp2d.h"
@@ -45,6 +47,26 @@
 namespace gdp2d {
 
 namespace detail {
+
+// The AoS <-> SoA conversion of a multi-million-element mesh is host work on
+// the drop-in path: split it over the host cores (contiguous blocks, so the
+// result is identical to a serial loop).
+template <class F>
+inline void parallel_for(size_t n, F&& f) {
+    const unsigned hw = std::thread::hardware_concurrency();
+    const size_t parts = std::min<size_t>(hw ? hw : 1, std::max<size_t>(1, n / 65536));
+    if (parts <= 1) {
+        for (size_t i = 0; i < n; ++i) f(i);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (size_t p = 0; p < parts; ++p)
+        th.emplace_back([&, p] {
+            const size_t lo = n * p / parts, hi = n * (p + 1) / parts;
+            for (size_t i = lo; i < hi; ++i) f(i);
+        });
+    for (auto& t : th) t.join();
+}
 
 inline const char* const kPhaseNames[GDP2D_NPHASES] = {"collect", "split_points", "locate",
                                                        "claim", "cavity", "insert"};
@@ -78,19 +100,19 @@ struct Packed {
         vkind.resize(V);
         valive.resize(V);
         vbirth.resize(V);
-        for (size_t i = 0; i < V; ++i) {
+        parallel_for(V, [&](size_t i) {
             const cdtref::Vertex& v = m.vertices[i];
             xy[2 * i] = v.pos.x;
             xy[2 * i + 1] = v.pos.y;
             vkind[i] = static_cast<uint8_t>(v.kind);
             vbirth[i] = v.birth_batch;
             valive[i] = v.alive ? 1 : 0;
-        }
+        });
         tv.resize(3 * T);
         tn.resize(3 * T);
         ts.resize(3 * T);
         talive.resize(T);
-        for (size_t t = 0; t < T; ++t) {
+        parallel_for(T, [&](size_t t) {
             const cdtref::Triangle& tr = m.triangles[t];
             for (int i = 0; i < 3; ++i) {
                 tv[3 * t + i] = tr.v[i];
@@ -98,7 +120,7 @@ struct Packed {
                 ts[3 * t + i] = tr.seg[i];
             }
             talive[t] = tr.alive ? 1 : 0;
-        }
+        });
         sv.resize(2 * S);
         sparent.resize(S);
         senc.resize(S);
@@ -137,15 +159,15 @@ inline void unpack(const gdp2d_mesh_buf& b, cdtref::Mesh& m) {
     const size_t V = b.n_vertices, T = b.n_triangles, S = b.n_subsegments;
     m.vertices.resize(V);
     m.vert_tri.assign(b.vert_tri, b.vert_tri + V);
-    for (size_t i = 0; i < V; ++i) {
+    parallel_for(V, [&](size_t i) {
         cdtref::Vertex& v = m.vertices[i];
         v.pos = cdtref::Point2{b.xy[2 * i], b.xy[2 * i + 1]};
         v.kind = static_cast<cdtref::VertexKind>(b.vert_kind[i]);
         v.birth_batch = b.vert_birth[i];
         v.alive = b.vert_alive[i] != 0;
-    }
+    });
     m.triangles.resize(T);
-    for (size_t t = 0; t < T; ++t) {
+    parallel_for(T, [&](size_t t) {
         cdtref::Triangle& tr = m.triangles[t];
         for (int i = 0; i < 3; ++i) {
             tr.v[i] = b.tri_v[3 * t + i];
@@ -153,7 +175,7 @@ inline void unpack(const gdp2d_mesh_buf& b, cdtref::Mesh& m) {
             tr.seg[i] = b.tri_seg[3 * t + i];
         }
         tr.alive = b.tri_alive[t] != 0;
-    }
+    });
     m.subsegments.resize(S);
     m.seg_tri.assign(b.seg_tri, b.seg_tri + S);
     for (size_t s = 0; s < S; ++s) {
