@@ -804,11 +804,15 @@ void upload(gdp2d_ctx* x, const gdp2d_mesh_view* v) {
     x->p_alive_s = h[2];
 }
 
-void reset_work(gdp2d_ctx* x) {
+// theta_hint (degrees, 0 = unknown): the one-shot gdp2d_refine sizes the
+// working mesh for the growth the quality bound implies (the mesh grows about
+// 2.1x at B = sqrt(2) and 5.4x at 30 degrees on the BASELINE PSLGs), so a single
+// call does not pay reallocations mid-refinement.
+void reset_work(gdp2d_ctx* x, double theta_hint = 0.0) {
     const DevMesh& p = x->pristine.m;
     // headroom: 2.5x the input (amortised growth handles the rest);
     // GDP2D_HEADROOM overrides the factor (tests use 1.0 to force growth)
-    double hr = 2.5;
+    double hr = theta_hint >= 28.0 ? 6.0 : theta_hint >= 24.0 ? 4.0 : 2.5;
     if (const char* e = std::getenv("GDP2D_HEADROOM")) hr = std::max(1.0, std::atof(e));
     x->work.m.nV = x->work.m.nT = x->work.m.nS = 0;
     mesh_reserve(x->work, std::max<u32>((u32)(p.nV * hr), 64), std::max<u32>((u32)(p.nT * hr), 128),
@@ -1893,7 +1897,7 @@ int gdp2d_refine(const gdp2d_mesh_view* in, gdp2d_mesh_buf* out, const gdp2d_par
     return run_guarded([&] {
         DeviceGuard g(x->device);
         upload(x, in);
-        reset_work(x);
+        reset_work(x, p->theta_deg);
         refine_loop(x, p, r);
         download(x, out);
         const double wall =
