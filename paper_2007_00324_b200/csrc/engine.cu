@@ -14,6 +14,7 @@
 #include <mutex>
 #include <string>
 #include <vector>
+#include <thread>
 
 #include "engine.h"
 #include "gdp2d.h"
@@ -390,6 +391,9 @@ struct gdp2d_ctx {
         u32* part = nullptr; u32 part_cap = 0;
         RoundCtr* ring = nullptr; u32* state = nullptr; ull* bbox = nullptr;
     } cdt;
+    // pageable host <-> device copies go through two pinned chunks (see xfer)
+    void* pin_chunk[2] = {nullptr, nullptr};
+    cudaEvent_t pin_ev[2] = {nullptr, nullptr};
     // upload / download staging
     u32* stage_u32[3] = {nullptr, nullptr, nullptr};
     uint8_t* stage_u8 = nullptr;
@@ -726,6 +730,10 @@ void ctx_release(gdp2d_ctx* x) {
         if (e) cudaEventDestroy(e);
     for (auto& e : x->ev_k)
         if (e) cudaEventDestroy(e);
+    for (int i = 0; i < 2; ++i) {
+        if (x->pin_chunk[i]) cudaFreeHost(x->pin_chunk[i]);
+        if (x->pin_ev[i]) cudaEventDestroy(x->pin_ev[i]);
+    }
     if (x->st) cudaStreamDestroy(x->st);
 }
 
@@ -753,6 +761,92 @@ void validate_view(const gdp2d_mesh_view* v) {
     if (v->n_triangles >= (1u << 30)) throw Fail{GDP2D_EINVAL, "too many triangles"};
 }
 
+// ---- host <-> device copies -----------------------------------------------------
+// Pinned caller memory is copied directly.  Pageable memory (malloc'ed output
+// of gdp2d_refine, the C++ shim's vectors) goes through two 32 MB pinned
+// chunks: the DMA of one chunk overlaps the multi-threaded host copy of the
+// other, instead of the driver's single-threaded pageable path.
+constexpr size_t kPinChunk = 32u << 20;
+
+bool host_pinned(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+void ensure_pin_chunks(gdp2d_ctx* x) {
+    for (int i = 0; i < 2; ++i) {
+        if (!x->pin_chunk[i]) CK(cudaMallocHost(&x->pin_chunk[i], kPinChunk));
+        if (!x->pin_ev[i]) CK(cudaEventCreateWithFlags(&x->pin_ev[i], cudaEventDisableTiming));
+    }
+}
+
+void par_memcpy(void* dst, const void* src, size_t n) {
+    const unsigned hw = std::thread::hardware_concurrency();
+    const size_t parts = std::min<size_t>(std::min(8u, hw ? hw : 1u), std::max<size_t>(1, n >> 22));
+    if (parts <= 1) {
+        std::memcpy(dst, src, n);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (size_t p = 0; p < parts; ++p)
+        th.emplace_back([=] {
+            const size_t lo = n * p / parts, hi = n * (p + 1) / parts;
+            std::memcpy(static_cast<char*>(dst) + lo, static_cast<const char*>(src) + lo, hi - lo);
+        });
+    for (auto& t : th) t.join();
+}
+
+void d2h(gdp2d_ctx* x, void* dst, const void* src, size_t bytes) {
+    if (!bytes) return;
+    cudaStream_t st = x->st;
+    if (bytes < (4u << 20) || host_pinned(dst)) {
+        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+        return;
+    }
+    ensure_pin_chunks(x);
+    size_t prev_off = 0, prev_n = 0;
+    int k = 0;
+    for (size_t off = 0; off < bytes; off += kPinChunk, ++k) {
+        const size_t n = std::min(kPinChunk, bytes - off);
+        CK(cudaMemcpyAsync(x->pin_chunk[k & 1], static_cast<const char*>(src) + off, n,
+                           cudaMemcpyDeviceToHost, st));
+        CK(cudaEventRecord(x->pin_ev[k & 1], st));
+        if (k > 0) {
+            CK(cudaEventSynchronize(x->pin_ev[(k - 1) & 1]));
+            par_memcpy(static_cast<char*>(dst) + prev_off, x->pin_chunk[(k - 1) & 1], prev_n);
+        }
+        prev_off = off;
+        prev_n = n;
+    }
+    CK(cudaEventSynchronize(x->pin_ev[(k - 1) & 1]));
+    par_memcpy(static_cast<char*>(dst) + prev_off, x->pin_chunk[(k - 1) & 1], prev_n);
+}
+
+void h2d(gdp2d_ctx* x, void* dst, const void* src, size_t bytes) {
+    if (!bytes) return;
+    cudaStream_t st = x->st;
+    if (bytes < (4u << 20) || host_pinned(src)) {
+        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+        return;
+    }
+    ensure_pin_chunks(x);
+    int k = 0;
+    for (size_t off = 0; off < bytes; off += kPinChunk, ++k) {
+        const size_t n = std::min(kPinChunk, bytes - off);
+        CK(cudaEventSynchronize(x->pin_ev[k & 1]));   // the chunk's previous DMA is done
+        par_memcpy(x->pin_chunk[k & 1], static_cast<const char*>(src) + off, n);
+        CK(cudaMemcpyAsync(static_cast<char*>(dst) + off, x->pin_chunk[k & 1], n,
+                           cudaMemcpyHostToDevice, st));
+        CK(cudaEventRecord(x->pin_ev[k & 1], st));
+    }
+    // the last chunks stay in flight; any later reuse of a chunk waits on its
+    // event (or follows it in stream order)
+}
+
 void upload(gdp2d_ctx* x, const gdp2d_mesh_view* v) {
     validate_view(v);
     const u32 V = v->n_vertices, T = v->n_triangles, S = v->n_subsegments;
@@ -764,25 +858,25 @@ void upload(gdp2d_ctx* x, const gdp2d_mesh_view* v) {
     m.nT = T;
     m.nS = S;
     cudaStream_t st = x->st;
-    CK(cudaMemcpyAsync(m.xy, v->xy, 16ull * V, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(m.vkind, v->vert_kind, V, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(m.vbirth, v->vert_birth, 4ull * V, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(m.valive, v->vert_alive, V, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(m.vtri, v->vert_tri, 4ull * V, cudaMemcpyHostToDevice, st));
+    h2d(x, m.xy, v->xy, 16ull * V);
+    h2d(x, m.vkind, v->vert_kind, V);
+    h2d(x, m.vbirth, v->vert_birth, 4ull * V);
+    h2d(x, m.valive, v->vert_alive, V);
+    h2d(x, m.vtri, v->vert_tri, 4ull * V);
     ensure_stage(x, std::max<size_t>(3ull * T, 2ull * S) + T + S + 16);
     if (T) {
-        CK(cudaMemcpyAsync(x->stage_u32[0], v->tri_v, 12ull * T, cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(x->stage_u32[1], v->tri_seg, 12ull * T, cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(x->stage_u32[2], v->tri_n, 12ull * T, cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(x->stage_u8, v->tri_alive, T, cudaMemcpyHostToDevice, st));
+        h2d(x, x->stage_u32[0], v->tri_v, 12ull * T);
+        h2d(x, x->stage_u32[1], v->tri_seg, 12ull * T);
+        h2d(x, x->stage_u32[2], v->tri_n, 12ull * T);
+        h2d(x, x->stage_u8, v->tri_alive, T);
         note_launch(), k_pack_tris<<<grid(T), 256, 0, st>>>(m, x->stage_u32[0], x->stage_u32[1], x->stage_u8);
         launch_encode_neighbors(m, x->stage_u32[2], st);
     }
     if (S) {
-        CK(cudaMemcpyAsync(m.sv, v->seg_v, 8ull * S, cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(m.sparent, v->seg_parent, 4ull * S, cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(m.salive, v->seg_alive, S, cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(m.stri, v->seg_tri, 4ull * S, cudaMemcpyHostToDevice, st));
+        h2d(x, m.sv, v->seg_v, 8ull * S);
+        h2d(x, m.sparent, v->seg_parent, 4ull * S);
+        h2d(x, m.salive, v->seg_alive, S);
+        h2d(x, m.stri, v->seg_tri, 4ull * S);
         CK(cudaMemcpyAsync(x->stage_u8 + T + 8, v->seg_encroached, S, cudaMemcpyHostToDevice,
                            st));
         note_launch(), k_u8_to_u32<<<grid(S), 256, 0, st>>>(x->stage_u8 + T + 8, m.senc, S);
@@ -839,27 +933,27 @@ void download_into(gdp2d_ctx* x, gdp2d_mesh_buf* b) {
     b->batch_epoch = x->epoch;
     ensure_stage(x, std::max<size_t>(3ull * T, 2ull * S) + T + S + 16);
     if (V) {
-        CK(cudaMemcpyAsync(b->xy, m.xy, 16ull * V, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(b->vert_kind, m.vkind, V, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(b->vert_birth, m.vbirth, 4ull * V, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(b->vert_alive, m.valive, V, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(b->vert_tri, m.vtri, 4ull * V, cudaMemcpyDeviceToHost, st));
+        d2h(x, b->xy, m.xy, 16ull * V);
+        d2h(x, b->vert_kind, m.vkind, V);
+        d2h(x, b->vert_birth, m.vbirth, 4ull * V);
+        d2h(x, b->vert_alive, m.valive, V);
+        d2h(x, b->vert_tri, m.vtri, 4ull * V);
     }
     if (T) {
         note_launch(), k_unpack_tris<<<grid(T), 256, 0, st>>>(m, x->stage_u32[0], x->stage_u32[1], x->stage_u8);
         launch_decode_neighbors(m, x->stage_u32[2], st);
-        CK(cudaMemcpyAsync(b->tri_v, x->stage_u32[0], 12ull * T, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(b->tri_seg, x->stage_u32[1], 12ull * T, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(b->tri_n, x->stage_u32[2], 12ull * T, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(b->tri_alive, x->stage_u8, T, cudaMemcpyDeviceToHost, st));
+        d2h(x, b->tri_v, x->stage_u32[0], 12ull * T);
+        d2h(x, b->tri_seg, x->stage_u32[1], 12ull * T);
+        d2h(x, b->tri_n, x->stage_u32[2], 12ull * T);
+        d2h(x, b->tri_alive, x->stage_u8, T);
     }
     if (S) {
-        CK(cudaMemcpyAsync(b->seg_v, m.sv, 8ull * S, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(b->seg_parent, m.sparent, 4ull * S, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(b->seg_alive, m.salive, S, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(b->seg_tri, m.stri, 4ull * S, cudaMemcpyDeviceToHost, st));
+        d2h(x, b->seg_v, m.sv, 8ull * S);
+        d2h(x, b->seg_parent, m.sparent, 4ull * S);
+        d2h(x, b->seg_alive, m.salive, S);
+        d2h(x, b->seg_tri, m.stri, 4ull * S);
         note_launch(), k_u32_to_u8<<<grid(S), 256, 0, st>>>(m.senc, x->stage_u8 + T + 8, S);
-        CK(cudaMemcpyAsync(b->seg_encroached, x->stage_u8 + T + 8, S, cudaMemcpyDeviceToHost, st));
+        d2h(x, b->seg_encroached, x->stage_u8 + T + 8, S);
     }
     CK(cudaStreamSynchronize(st));
     CK(cudaGetLastError());
