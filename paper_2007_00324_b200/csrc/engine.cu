@@ -299,6 +299,9 @@ struct Tracer {
     }
 };
 
+constexpr size_t kStatusWords = 20 + (sizeof(Counters) + 3) / 4;
+static_assert(sizeof(Counters) % 8 == 0, "Counters follows word 20 (8-byte aligned)");
+
 struct gdp2d_ctx {
     int device = 0;
     Tracer tr;
@@ -354,6 +357,12 @@ struct gdp2d_ctx {
     double k_split_s = 0, k_rb_s = 0;   // per refine call: roofline accumulators
     u64 k_split_b = 0, k_rb_b = 0, k_launches = 0;
     u32* d_C = nullptr;           // candidate count written by collect (device)
+    // One device block holds everything the host reads after a batch, so the
+    // end-of-batch readback is a single copy: ins_state [0,16), insertion
+    // totals [16,19), the candidate count [19], the Counters from word 20.
+    // h_status is its pinned mirror; the pointers above alias into both.
+    u32* status = nullptr;
+    u32* h_status = nullptr;
     u32 c_prev = 0;               // previous batch's candidate count (host, after its sync)
     bool have_c_prev = false;
     bool sync_collect = false;    // GDP2D_SYNC_COLLECT=1: host round trip after every collect
@@ -424,7 +433,6 @@ void ensure_cands(gdp2d_ctx* x, u32 n) {
     dfree(x->ib.os);
     dalloc(x->ib.nv, cap); dalloc(x->ib.nt, cap); dalloc(x->ib.ns, cap);
     dalloc(x->ib.ov, cap); dalloc(x->ib.ot, cap); dalloc(x->ib.os, cap);
-    if (!x->ib.totals) dalloc(x->ib.totals, 4);
     x->ib.cap = cap;
 }
 
@@ -622,11 +630,17 @@ void ctx_init(gdp2d_ctx* x, int device) {
         throw Fail{GDP2D_ENODEVICE, std::string("sm_100a required, found ") + prop.name};
     x->device = device;
     CK(cudaStreamCreateWithFlags(&x->st, cudaStreamNonBlocking));
-    dalloc(x->d_ctr, 1);
+    dalloc(x->status, kStatusWords);
+    CK(cudaMallocHost(&x->h_status, kStatusWords * sizeof(u32)));
+    x->ins_state = x->status;
+    x->ib.totals = x->status + 16;
+    x->d_C = x->status + 19;
+    x->d_ctr = reinterpret_cast<Counters*>(x->status + 20);
+    x->h_state = x->h_status;
+    x->h_tot = x->h_status + 16;
+    x->h_ctr = reinterpret_cast<Counters*>(x->h_status + 20);
     dalloc(x->wl.rc, 1);
-    CK(cudaMallocHost(&x->h_ctr, sizeof(Counters)));
     CK(cudaMallocHost(&x->h_rc, sizeof(RoundCtr)));
-    CK(cudaMallocHost(&x->h_tot, 4 * sizeof(u32)));
     CK(cudaMalloc(&x->qscratch, 256));
     dalloc(x->d_val, 4);
     dalloc(x->wl.dbg, 4 + 2 * MAX_STAR);
@@ -658,7 +672,6 @@ void ctx_init(gdp2d_ctx* x, int device) {
     const char* li = std::getenv("GDP2D_INSERT");
     x->legacy_insert = (li && std::string(li) == "legacy") || x->validate || x->lawson_rounds;
     dalloc(x->ring, 5);   // 4-slot step ring + the removal-seed accumulator
-    dalloc(x->d_C, 1);
     if (const char* e = std::getenv("GDP2D_TRACE"); e && (e[0] == '1' || e[0] == '2')) {
         x->tr.on = true;
         x->tr.rounds = e[0] == '2';
@@ -671,8 +684,6 @@ void ctx_init(gdp2d_ctx* x, int device) {
     if (const char* e = std::getenv("GDP2D_CHECK")) x->check = e[0] == '1';
     if (const char* e = std::getenv("GDP2D_EXTRAS")) x->extras = std::atoi(e);
     dalloc(x->scan_part, 3ull * x->insert_grid + 3);
-    dalloc(x->ins_state, 16);
-    CK(cudaMallocHost(&x->h_state, 16 * sizeof(u32)));
     const char* fc = std::getenv("GDP2D_COLLECT");
     x->full_collect = fc && std::string(fc) == "full";
     dalloc(x->rcs, 1024);
@@ -690,7 +701,7 @@ void ctx_release(gdp2d_ctx* x) {
     cands_free(x->c);
     dfree(x->regions); dfree(x->region_len); dfree(x->bfs_len);
     dfree(x->ib.nv); dfree(x->ib.nt); dfree(x->ib.ns); dfree(x->ib.ov); dfree(x->ib.ot);
-    dfree(x->ib.os); dfree(x->ib.totals);
+    dfree(x->ib.os);
     dfree(x->fresh.key); dfree(x->fresh.tie); dfree(x->fresh.cc); dfree(x->fresh.removed);
     dfree(x->fresh.mark); dfree(x->fresh.dirty);
     dfree(x->fresh.dstat); dfree(x->fresh.hcnt); dfree(x->fresh.hlist);
@@ -698,19 +709,21 @@ void ctx_release(gdp2d_ctx* x) {
     dfree(x->wl.touched); dfree(x->wl.fwin); dfree(x->wl.rm[0]); dfree(x->wl.rm[1]);
     dfree(x->wl.star); dfree(x->wl.star_len); dfree(x->wl.rc);
     dfree(x->scan.partial);
-    dfree(x->d_ctr);
+    x->ins_state = x->ib.totals = x->d_C = nullptr;
+    x->d_ctr = nullptr;
+    dfree(x->status);
+    if (x->h_status) cudaFreeHost(x->h_status);
+    x->h_status = x->h_state = x->h_tot = nullptr;
+    x->h_ctr = nullptr;
     for (auto& s : x->stage_u32) dfree(s);
     dfree(x->stage_u8);
-    if (x->h_ctr) cudaFreeHost(x->h_ctr);
     if (x->h_rc) cudaFreeHost(x->h_rc);
-    if (x->h_tot) cudaFreeHost(x->h_tot);
     if (x->qscratch) cudaFree(x->qscratch);
     dfree(x->d_val);
     dfree(x->wl.dbg);
     dfree(x->rcs);
     dfree(x->d_res);
     dfree(x->ring);
-    dfree(x->d_C);
     dfree(x->scan_part);
     {
         auto& c = x->cdt;
@@ -724,8 +737,6 @@ void ctx_release(gdp2d_ctx* x) {
     dfree(x->in_sv);
     if (x->vscratch) cudaFree(x->vscratch);
     x->tr.release();
-    dfree(x->ins_state);
-    if (x->h_state) cudaFreeHost(x->h_state);
     for (auto& e : x->ev)
         if (e) cudaEventDestroy(e);
     for (auto& e : x->ev_k)
@@ -1152,10 +1163,9 @@ bool insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, int prefiltered, u32
         CK(cudaEventRecord(x->ev_k[2], st));
         x->tr.mark("insert_kernel", st);
         CK(cudaGetLastError());
-        CK(cudaMemcpyAsync(x->h_state, x->ins_state, 16 * sizeof(u32), cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(x->h_tot, x->ib.totals, 3 * sizeof(u32), cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(x->h_tot + 3, x->d_C, sizeof(u32), cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(x->h_ctr, x->d_ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+        // status words, totals, C and the counters in one copy
+        CK(cudaMemcpyAsync(x->h_status, x->status, kStatusWords * sizeof(u32),
+                           cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         const u32 C = x->h_tot[3];
         if (x->h_state[0] == 3u) return false;   // INS_REGIONS
