@@ -1083,7 +1083,7 @@ void check_structure_now(gdp2d_ctx* x, u32 nV, u32 nT, u32 nS, const char* where
 // did nothing; the caller grows them and redoes it).  x->h_tot[3] = C.
 bool insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, int prefiltered, u32 reg_cap,
                        u32 c_est, u32 ncav, u32 rs, int isolate, u32 batch, u32& nv, u32& nt,
-                       u32& ns, u32& flip_rounds, u32& rm_rounds) {
+                       u32& ns, u32& flip_rounds, u32& rm_rounds, cudaEvent_t start_ev) {
     cudaStream_t st = x->st;
     // Smaller batches run the persistent kernels on fewer co-resident CTAs:
     // their phases have little parallel work and a grid barrier's cost grows
@@ -1148,7 +1148,13 @@ bool insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, int prefiltered, u32
         x->tr.mark("pre_ins", st);
         // word 8 = unsafe flag stays; attempt 0's words were zeroed by the scan
         if (attempt > 0) CK(cudaMemsetAsync(x->ins_state, 0, 8 * sizeof(u32), st));
-        CK(cudaEventRecord(x->ev_k[0], st));
+        // the caller's last phase event marks the kernel start when nothing
+        // was queued since (each event record costs ~3 us of stream time)
+        cudaEvent_t k_start = start_ev;
+        if (attempt > 0 || x->tr.on || !start_ev) {
+            CK(cudaEventRecord(x->ev_k[0], st));
+            k_start = x->ev_k[0];
+        }
         const int mode = p->mode == GDP2D_CHEW ? 1 : 0;
         const int k1 = x->lawson_kernel ? (1 | 4) : 1;
         if (!x->check) {
@@ -1186,7 +1192,7 @@ bool insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, int prefiltered, u32
             const u64 ins = h.ins_mid + h.ins_cc;
             const u64 f_split = x->h_state[7];
             const u64 f_rb = h.flips >= f_split ? h.flips - f_split : 0;
-            x->k_split_s += ev_ms(x->ev_k[0], x->ev_k[1]) * 1e-3;
+            x->k_split_s += ev_ms(k_start, x->ev_k[1]) * 1e-3;
             x->k_split_b += 32ull * C + 128ull * ins + 128ull * f_split;
             x->k_rb_s += ev_ms(x->ev_k[1], x->ev_k[2]) * 1e-3;
             x->k_rb_b += 64ull * nv + 128ull * f_rb + 128ull * h.rm_done;
@@ -1258,7 +1264,7 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
                          !p->little_batch_sizing;
         u32 C = launch_collect(m, q, p->rule4_unified_collection != 0, x->flags, x->c, x->ccap,
                                x->scan, x->d_ctr, st, cache, &tris_scanned, x->d_C,
-                               x->ev[GDP2D_NPHASES + 2], x->ev[GDP2D_NPHASES + 3], !ncs);
+                               nullptr, x->ev[GDP2D_NPHASES + 3], !ncs);
         // a full scan has refreshed every cached verdict it covered; with
         // rule 4 off and subsegment candidates, triangles were not scanned
         if (tris_scanned) x->full_scan = false;
@@ -1270,7 +1276,7 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
         x->tr.mark("collect", st);
         if (!ncs && C == 0) {
             check_dev_err(x);
-            r->scan_seconds += ev_ms(x->ev[GDP2D_NPHASES + 2], x->ev[GDP2D_NPHASES + 3]) * 1e-3;
+            r->scan_seconds += ev_ms(x->ev[0], x->ev[GDP2D_NPHASES + 3]) * 1e-3;
             r->scan_bytes += scan_alg_bytes(scan_nT, scan_nS, x->h_ctr->scan_dirty);
             break;
         }
@@ -1280,8 +1286,9 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
         if (p->little_batch_sizing && (cap == 0 || x->little_cap < cap)) cap = x->little_cap;
         u32 attempted = (!ncs && cap > 0 && C > cap) ? (u32)cap : C;
         if (!ncs && attempted < C) launch_select_topk(x->c, C, attempted, x->sel_state, st);
-        CK(cudaEventRecord(x->ev[1], st));   // split points are fused into collect
-        CK(cudaEventRecord(x->ev[2], st));
+        // split points are fused into collect: one event ends both phases
+        CK(cudaEventRecord(x->ev[1], st));
+        bool filtered_events = false;   // ev[3..5] recorded (standalone filters)
         // isolated insertion needs the cavity filter (rule 2)
         const int isolate = (ncav == 0 || x->legacy_insert) ? 0
                             : p->insert_mode == GDP2D_INSERT_ISOLATED   ? 1
@@ -1306,6 +1313,7 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
                           x->d_ctr, st);
             x->tr.mark("cavity", st);
             CK(cudaEventRecord(x->ev[5], st));
+            filtered_events = true;
             launch_plan_ops(m, x->c, C, p->split_depth_cap, x->ib, x->d_ctr, st);
             scan_exclusive(x->ib.nv, x->ib.ov, C, x->ib.totals + 0, x->scan, st);
             scan_exclusive(x->ib.nt, x->ib.ot, C, x->ib.totals + 1, x->scan, st);
@@ -1338,14 +1346,13 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
                     launch_cavity(m, x->c, na, ncav, x->extras, x->aux, x->regions,
                                   x->region_len, nullptr, x->d_ctr, st);
                 CK(cudaEventRecord(x->ev[5], st));
-            } else {
-                // tail batch: everything runs inside the block-mode kernels
-                CK(cudaEventRecord(x->ev[3], st));
-                CK(cudaEventRecord(x->ev[4], st));
-                CK(cudaEventRecord(x->ev[5], st));
+                filtered_events = true;
             }
+            // (tail batch: everything runs inside the block-mode kernels; the
+            // filter phases get no events of their own)
             if (!insert_persistent(x, p, standalone ? 1 : 0, reg_cap, ncs ? x->c_prev : C, ncav,
-                                   rs, isolate, batch, nv, nt, ns, flip_rounds, rm_rounds)) {
+                                   rs, isolate, batch, nv, nt, ns, flip_rounds, rm_rounds,
+                                   standalone ? x->ev[5] : x->ev[1])) {
                 // the list outgrew the region buffers: grow them, redo the batch
                 // (collect recomputes the same list from its cached verdicts)
                 // (the redo takes the synchronous path: it knows C exactly)
@@ -1361,7 +1368,7 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
                 attempted = C;
             }
         }
-        r->scan_seconds += ev_ms(x->ev[GDP2D_NPHASES + 2], x->ev[GDP2D_NPHASES + 3]) * 1e-3;
+        r->scan_seconds += ev_ms(x->ev[0], x->ev[GDP2D_NPHASES + 3]) * 1e-3;
         x->c_prev = C;
         x->have_c_prev = true;
         if (C == 0) {   // ncs: the batch found no candidates (its kernels did nothing)
@@ -1370,7 +1377,13 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
             --x->epoch;
             break;
         }
-        CK(cudaEventRecord(x->ev[6], st));
+        // end of the insertion phase: the rollback kernel's end event (the
+        // legacy path records its own)
+        cudaEvent_t ins_end = x->ev_k[2];
+        if (x->legacy_insert) {
+            CK(cudaEventRecord(x->ev[6], st));
+            ins_end = x->ev[6];
+        }
         x->tr.mark("sync", st);
         x->tr.flush(bm.batch_index, st);
         if (x->tr.on)
@@ -1397,11 +1410,15 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
         bm.attempted = attempted;
         bm.concurrency = retained;
         bm.phase_seconds[GDP2D_PH_COLLECT] = ev_ms(x->ev[0], x->ev[1]) * 1e-3;
-        bm.phase_seconds[GDP2D_PH_SPLIT_POINTS] = ev_ms(x->ev[1], x->ev[2]) * 1e-3;
-        bm.phase_seconds[GDP2D_PH_LOCATE] = ev_ms(x->ev[2], x->ev[3]) * 1e-3;
-        bm.phase_seconds[GDP2D_PH_CLAIM] = ev_ms(x->ev[3], x->ev[4]) * 1e-3;
-        bm.phase_seconds[GDP2D_PH_CAVITY] = ev_ms(x->ev[4], x->ev[5]) * 1e-3;
-        bm.phase_seconds[GDP2D_PH_INSERT] = ev_ms(x->ev[5], x->ev[6]) * 1e-3;
+        bm.phase_seconds[GDP2D_PH_SPLIT_POINTS] = 0.0;   // fused into collect
+        if (filtered_events) {
+            bm.phase_seconds[GDP2D_PH_LOCATE] = ev_ms(x->ev[1], x->ev[3]) * 1e-3;
+            bm.phase_seconds[GDP2D_PH_CLAIM] = ev_ms(x->ev[3], x->ev[4]) * 1e-3;
+            bm.phase_seconds[GDP2D_PH_CAVITY] = ev_ms(x->ev[4], x->ev[5]) * 1e-3;
+            bm.phase_seconds[GDP2D_PH_INSERT] = ev_ms(x->ev[5], ins_end) * 1e-3;
+        } else {   // filtered inside the batch kernel
+            bm.phase_seconds[GDP2D_PH_INSERT] = ev_ms(x->ev[1], ins_end) * 1e-3;
+        }
         for (double s : bm.phase_seconds) bm.latency += s;
         bm.throughput = bm.latency > 0 ? retained / bm.latency : 0.0;
         bm.waste_fraction = attempted ? double(attempted - retained) / attempted : 0.0;
