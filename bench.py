@@ -315,7 +315,7 @@ def main():
     # ---- roofline: the dominant engine kernel (largest share of the step) ----
     peak, peak_kind = load_peaks()
     kernels = {
-        "k_collect_flags": ("Line-3 scan (incremental bad/encroached flags)",
+        "k_collect_flags": ("Line-3 collect (incremental flags + compaction + candidate scatter)",
                             sum(r.scan_seconds for r in reps), sum(r.scan_bytes for r in reps),
                             sum(r.scan_launches for r in reps)),
         "k_batch_split": ("Lines 5-8a: plan + splits + Lawson flips (persistent)",

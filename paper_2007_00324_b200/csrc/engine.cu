@@ -1208,13 +1208,17 @@ bool insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, int prefiltered, u32
     }
 }
 
-// Algorithmic bytes of one Line-3 scan launch (k_collect_flags): every
-// element reads its 1 B cached verdict and writes its 1 B flag, every
-// subsegment reads alive + the sticky encroached flag (5 B); a re-evaluated
-// (dirty) element moves its 16 B record + three 16 B corner gathers (64 B,
-// SURVEY 8(d)'s per-triangle figure; the subsegment record + apex gathers
-// are taken as the same 64 B).
-u64 scan_alg_bytes(u64 nT, u64 nS, u64 dirty) { return 2 * (nT + nS) + 5 * nS + 64 * dirty; }
+// Algorithmic bytes of one Line-3 scan: every element reads its 1 B cached
+// verdict, every subsegment reads alive + the sticky encroached flag (5 B); a
+// re-evaluated (dirty) element moves its 16 B record + three 16 B corner
+// gathers (64 B, SURVEY 8(d)'s per-triangle figure; the subsegment record +
+// apex gathers are taken as the same 64 B) and every element writes its 1 B
+// flag (k_collect_flags).  When the timed region includes the scatter (the
+// no-round-trip path), each candidate adds its element's record + corners
+// (64 B) and its 41 B candidate record.
+u64 scan_alg_bytes(u64 nT, u64 nS, u64 dirty, u64 cands, bool scatter) {
+    return 2 * (nT + nS) + 5 * nS + 64 * dirty + (scatter ? 105 * cands : 0);
+}
 
 // The refinement loop (refine.hpp:651-713) on the working mesh.
 void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
@@ -1264,7 +1268,10 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
                          !p->little_batch_sizing;
         u32 C = launch_collect(m, q, p->rule4_unified_collection != 0, x->flags, x->c, x->ccap,
                                x->scan, x->d_ctr, st, cache, &tris_scanned, x->d_C,
-                               nullptr, x->ev[GDP2D_NPHASES + 3], !ncs);
+                               nullptr, ncs ? nullptr : x->ev[GDP2D_NPHASES + 3], !ncs);
+        // the no-round-trip collect is timed to ev[1], scatter included (one
+        // event record less per batch)
+        const cudaEvent_t scan_end = ncs ? x->ev[1] : x->ev[GDP2D_NPHASES + 3];
         // a full scan has refreshed every cached verdict it covered; with
         // rule 4 off and subsegment candidates, triangles were not scanned
         if (tris_scanned) x->full_scan = false;
@@ -1277,7 +1284,7 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
         if (!ncs && C == 0) {
             check_dev_err(x);
             r->scan_seconds += ev_ms(x->ev[0], x->ev[GDP2D_NPHASES + 3]) * 1e-3;
-            r->scan_bytes += scan_alg_bytes(scan_nT, scan_nS, x->h_ctr->scan_dirty);
+            r->scan_bytes += scan_alg_bytes(scan_nT, scan_nS, x->h_ctr->scan_dirty, 0, false);
             break;
         }
         // Batch sizing (refine.hpp:252-261 + the Little's-law cap): keep the
@@ -1368,12 +1375,12 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
                 attempted = C;
             }
         }
-        r->scan_seconds += ev_ms(x->ev[0], x->ev[GDP2D_NPHASES + 3]) * 1e-3;
+        r->scan_seconds += ev_ms(x->ev[0], scan_end) * 1e-3;
         x->c_prev = C;
         x->have_c_prev = true;
         if (C == 0) {   // ncs: the batch found no candidates (its kernels did nothing)
             raise_dev_err(x);
-            r->scan_bytes += scan_alg_bytes(scan_nT, scan_nS, x->h_ctr->scan_dirty);
+            r->scan_bytes += scan_alg_bytes(scan_nT, scan_nS, x->h_ctr->scan_dirty, 0, true);
             --x->epoch;
             break;
         }
@@ -1398,7 +1405,7 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
         else
             raise_dev_err(x);   // counters came back with the insertion's status
         const Counters& h = *x->h_ctr;
-        r->scan_bytes += scan_alg_bytes(scan_nT, scan_nS, h.scan_dirty);
+        r->scan_bytes += scan_alg_bytes(scan_nT, scan_nS, h.scan_dirty, C, ncs);
         const u32 inserted = h.ins_mid + h.ins_cc;
         const u32 retained = inserted - std::min(inserted, h.rm_done);
         x->alive_v += inserted;
