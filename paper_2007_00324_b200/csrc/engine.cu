@@ -355,7 +355,8 @@ struct gdp2d_ctx {
     u32* h_state = nullptr;       // pinned copy
     cudaEvent_t ev_k[3] = {};     // around the split and rollback kernels
     double k_split_s = 0, k_rb_s = 0;   // per refine call: roofline accumulators
-    u64 k_split_b = 0, k_rb_b = 0, k_launches = 0;
+    u64 k_split_b = 0, k_rb_b = 0, k_launches = 0, k_rb_launches = 0;
+    bool tail_kernel = false;   // GDP2D_TAIL=1: batches <= small_c as one k_batch_tail launch
     u32* d_C = nullptr;           // candidate count written by collect (device)
     // One device block holds everything the host reads after a batch, so the
     // end-of-batch readback is a single copy: ins_state [0,16), insertion
@@ -682,6 +683,7 @@ void ctx_init(gdp2d_ctx* x, int device) {
     if (const char* e = std::getenv("GDP2D_SMALL_C")) x->small_c = (u32)std::strtoul(e, nullptr, 10);
     if (const char* e = std::getenv("GDP2D_DEP")) x->dep_mis = std::string(e) == "mis";
     if (const char* e = std::getenv("GDP2D_CHECK")) x->check = e[0] == '1';
+    if (const char* e = std::getenv("GDP2D_TAIL")) x->tail_kernel = e[0] == '1';
     if (const char* e = std::getenv("GDP2D_EXTRAS")) x->extras = std::atoi(e);
     dalloc(x->scan_part, 3ull * x->insert_grid + 3);
     const char* fc = std::getenv("GDP2D_COLLECT");
@@ -1099,6 +1101,12 @@ bool insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, int prefiltered, u32
         return e ? std::max(1, std::atoi(e)) : 1;
     }();
     const int g_rb = std::max(1, x->rollback_grid / (div * rb_div));
+    // a batch predicted to be small runs as one single-CTA launch
+    // (k_batch_tail); prediction from the previous batch's count
+    bool tail = x->tail_kernel && !x->check && !x->lawson_kernel && !prefiltered &&
+                c_est <= x->small_c;
+    bool started = false;   // an earlier attempt got past the filter and plan
+    int grow = 0;
     for (int attempt = 0;; ++attempt) {
         if (attempt > 0) CK(cudaMemsetAsync(x->ring, 0, 5 * sizeof(RoundCtr), st));
         InsertLaunch L;
@@ -1135,7 +1143,7 @@ bool insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, int prefiltered, u32
         L.region_len = x->region_len;
         L.scan_part = x->scan_part;
         L.small_c = x->small_c;
-        L.resume = attempt > 0 ? 1 : 0;
+        L.resume = started ? 1 : 0;
         L.prefiltered = prefiltered;
         L.reg_cap = reg_cap;
         if (x->tr.on) {
@@ -1157,7 +1165,9 @@ bool insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, int prefiltered, u32
         }
         const int mode = p->mode == GDP2D_CHEW ? 1 : 0;
         const int k1 = x->lawson_kernel ? (1 | 4) : 1;
-        if (!x->check) {
+        if (tail) {
+            launch_insert_tail(L, mode, st);
+        } else if (!x->check) {
             launch_insert_persistent(L, mode, g_ins, g_rb, st, x->ev_k[1], k1 | 2, x->lawson_grid2);
         } else {
             // GDP2D_CHECK=1: structural validation after each kernel
@@ -1175,11 +1185,16 @@ bool insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, int prefiltered, u32
         CK(cudaStreamSynchronize(st));
         const u32 C = x->h_tot[3];
         if (x->h_state[0] == 3u) return false;   // INS_REGIONS
+        if (x->h_state[0] == 4u) {   // INS_NOT_TAIL: nothing done, redo on the grid kernels
+            tail = false;
+            continue;
+        }
         nv = x->h_tot[0];
         nt = x->h_tot[1];
         ns = x->h_tot[2];
         if (x->h_state[0] == 1u) {   // INS_GROW
-            if (attempt > 2) throw Fail{GDP2D_ECAPACITY, "insertion does not fit after growth"};
+            if (++grow > 2) throw Fail{GDP2D_ECAPACITY, "insertion does not fit after growth"};
+            started = true;
             ensure_mesh(x, x->work.m.nV + nv, x->work.m.nT + nt, x->work.m.nS + ns);
             ensure_fresh(x, nv);
             ensure_worklists(x, 12ull * nv);
@@ -1192,11 +1207,19 @@ bool insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, int prefiltered, u32
             const u64 ins = h.ins_mid + h.ins_cc;
             const u64 f_split = x->h_state[7];
             const u64 f_rb = h.flips >= f_split ? h.flips - f_split : 0;
-            x->k_split_s += ev_ms(k_start, x->ev_k[1]) * 1e-3;
-            x->k_split_b += 32ull * C + 128ull * ins + 128ull * f_split;
-            x->k_rb_s += ev_ms(x->ev_k[1], x->ev_k[2]) * 1e-3;
-            x->k_rb_b += 64ull * nv + 128ull * f_rb + 128ull * h.rm_done;
+            const u64 b_split = 32ull * C + 128ull * ins + 128ull * f_split;
+            const u64 b_rb = 64ull * nv + 128ull * f_rb + 128ull * h.rm_done;
             x->k_launches += 1;
+            if (tail) {   // one kernel did both: counted as a split-kernel launch
+                x->k_split_s += ev_ms(k_start, x->ev_k[2]) * 1e-3;
+                x->k_split_b += b_split + b_rb;
+            } else {
+                x->k_split_s += ev_ms(k_start, x->ev_k[1]) * 1e-3;
+                x->k_split_b += b_split;
+                x->k_rb_s += ev_ms(x->ev_k[1], x->ev_k[2]) * 1e-3;
+                x->k_rb_b += b_rb;
+                x->k_rb_launches += 1;
+            }
         }
         x->round += x->h_state[1] + 1;
         flip_rounds = x->h_state[2];
@@ -1233,7 +1256,7 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
     r->batches = keep.batches;
     r->batches_capacity = keep.batches_capacity;
     x->k_split_s = x->k_rb_s = 0;
-    x->k_split_b = x->k_rb_b = x->k_launches = 0;
+    x->k_split_b = x->k_rb_b = x->k_launches = x->k_rb_launches = 0;
     x->have_c_prev = false;
     CK(cudaEventRecord(x->ev[GDP2D_NPHASES + 1], st));  // loop start
     for (u64 iter = 0;; ++iter) {
@@ -1475,7 +1498,7 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
     r->split_launches = x->k_launches;
     r->rollback_seconds = x->k_rb_s;
     r->rollback_bytes = x->k_rb_b;
-    r->rollback_launches = x->k_launches;
+    r->rollback_launches = x->k_rb_launches;
     r->wall_seconds =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
 }

@@ -235,6 +235,9 @@ int rollback_persistent_grid(int device);
 // which: bit 0 = kernel 1 (splits [+ Lawson]), bit 2 = the separate Lawson
 // kernel, bit 1 = kernel 2 (rollback), launched in that order.
 int lawson_batch_grid(int device);
+// The whole batch (C <= small_c) in one CTA, one ordinary launch; state[0] =
+// INS_NOT_TAIL (4) when the batch is larger (nothing done).
+void launch_insert_tail(const InsertLaunch& L, int mode, cudaStream_t st);
 void launch_insert_persistent(const InsertLaunch& L, int mode, int grid, int grid2,
                               cudaStream_t st, cudaEvent_t between = nullptr, int which = 3,
                               int grid3 = 0);

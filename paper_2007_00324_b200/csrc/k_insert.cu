@@ -870,7 +870,7 @@ __device__ __forceinline__ void trace(const InsertArgs& a, bool leader, u32 tag,
     }
 }
 
-enum : u32 { INS_OK = 0, INS_GROW = 1, INS_STEPS = 2, INS_REGIONS = 3 };
+enum : u32 { INS_OK = 0, INS_GROW = 1, INS_STEPS = 2, INS_REGIONS = 3, INS_NOT_TAIL = 4 };
 
 __device__ __forceinline__ RoundCtr* ring_at(const Exec& ex, u32 step) {
     return ex.ring + (step & 3u);
@@ -1439,6 +1439,45 @@ __global__ void __launch_bounds__(ROLLBACK_BLOCK) k_batch_rollback(InsertArgs a)
     rollback_loop<MODE>(a, ex, nv, nt, ns);
 }
 
+// Tail kernel: a whole small batch (C <= small_c) in one CTA -- Lines 5-7,
+// the plan, the splits + Lawson and the redundancy detection + rollback --
+// as ONE ordinary launch (GDP2D_TAIL=1; off by default).  Same code and
+// block-mode execution as the split + rollback pair (identical output); it
+// saves the second (cooperative) launch and the kernel boundary, ~14 us per
+// tail batch, but its Lawson rounds run ~40% slower than the split kernel's
+// (different code generation: 80 registers, no min-blocks bound, which the
+// rollback frame needs), so cfg 2 ends 36.9 vs 36.6 ms.  The host picks it
+// from the previous batch's count; a batch that turns out larger returns
+// INS_NOT_TAIL untouched and is redone on the grid kernels.
+template <int MODE>
+__global__ void __launch_bounds__(INSERT_BLOCK) k_batch_tail(const __grid_constant__ InsertArgs a) {
+    const u32 C = vload(a.d_C);
+    if (C > a.reg_cap || C > a.small_c) {
+        if (threadIdx.x == 0) a.state[0] = C > a.reg_cap ? INS_REGIONS : INS_NOT_TAIL;
+        return;
+    }
+    __shared__ RoundCtr sring[5];
+    const Exec ex = block_exec(sring);
+    if (!a.resume) {
+        trace(a, ex.leader(), TR_START);
+        filter<MODE>(a, ex, C);
+        plan_and_scan(a, ex, C);
+    }
+    {
+        const u32 nv = vload(&a.b.totals[0]), nt = vload(&a.b.totals[1]),
+                  ns = vload(&a.b.totals[2]);
+        if (!fits_and_status(a, nv, nt, ns)) return;   // uniform
+        split_and_flip(a, ex, nv, nt, ns);
+    }
+    __syncthreads();
+    // k_batch_rollback's entry conditions
+    if (vload(&a.state[0]) != INS_OK) return;
+    if (a.isolate == 1 && vload(&a.state[8]) == 0) return;
+    const u32 nv = vload(&a.b.totals[0]), nt = vload(&a.b.totals[1]), ns = vload(&a.b.totals[2]);
+    if (nv == 0) return;
+    rollback_loop<MODE>(a, ex, nv, nt, ns);
+}
+
 template <class K0, class K1>
 static int coop_grid(K0 k0, K1 k1, int device, int block = INSERT_BLOCK) {
     int sms = 0, per0 = 0, per1 = 0;
@@ -1458,8 +1497,7 @@ int rollback_persistent_grid(int device) {
     return coop_grid(k_batch_rollback<0>, k_batch_rollback<1>, device, ROLLBACK_BLOCK);
 }
 
-void launch_insert_persistent(const InsertLaunch& L, int mode, int grid, int grid2, cudaStream_t st,
-                              cudaEvent_t between, int which, int grid3) {
+static InsertArgs make_args(const InsertLaunch& L) {
     InsertArgs a;
     a.m = L.m;
     a.c = L.c;
@@ -1497,6 +1535,21 @@ void launch_insert_persistent(const InsertLaunch& L, int mode, int grid, int gri
     a.trace_val = L.trace_val;
     a.trace_n = L.trace_n;
     a.trace_cap = L.trace_cap;
+    return a;
+}
+
+void launch_insert_tail(const InsertLaunch& L, int mode, cudaStream_t st) {
+    const InsertArgs a = make_args(L);
+    note_launch();
+    if (mode)
+        k_batch_tail<1><<<1, INSERT_BLOCK, 0, st>>>(a);
+    else
+        k_batch_tail<0><<<1, INSERT_BLOCK, 0, st>>>(a);
+}
+
+void launch_insert_persistent(const InsertLaunch& L, int mode, int grid, int grid2, cudaStream_t st,
+                              cudaEvent_t between, int which, int grid3) {
+    InsertArgs a = make_args(L);
     void* args[] = {&a};
     if (which & 1) {
         note_launch();

@@ -17,6 +17,7 @@ VARIANTS = [
     {"GDP2D_MODE": "0"},
     {"GDP2D_MODE": "2"},
     {"GDP2D_HEADROOM": "1.0"},
+    {"GDP2D_TAIL": "1"},
 ]
 
 CODE = r'''
