@@ -237,6 +237,14 @@ void gdp2d_params_init(gdp2d_params* p, double theta_deg, double ell, uint32_t m
 int gdp2d_refine(const gdp2d_mesh_view* in, gdp2d_mesh_buf* out, const gdp2d_params* p,
                  gdp2d_report* r, int device);
 
+/* Create the cached context of `device` and run one tiny CDT build +
+ * refinement on it, so CUDA context creation and kernel loading (~1-2 s in a
+ * fresh process) are paid here.  Meant to run on a helper thread while the
+ * caller reads its input; later gdp2d_refine / gdp2d_build_cdt calls on the
+ * device wait for it (they share the context's lock).  No reference
+ * counterpart (the CPU reference has no device to prepare). */
+int gdp2d_warmup(int device);
+
 void gdp2d_free(gdp2d_mesh_buf* out);
 const char* gdp2d_last_error(void);
 const char* gdp2d_version(void);

@@ -153,6 +153,7 @@ SIGNATURES = {
                                   C.POINTER(C.c_uint32)]),
     "gdp2d_ctx_download_to": (C.c_int, [ctx_p, C.POINTER(MeshBuf)]),
     "gdp2d_release_cached": (None, []),
+    "gdp2d_warmup": (C.c_int, [C.c_int]),
     "gdp2d_collect": (C.c_int, [ctx_p, C.POINTER(Params), C.c_void_p, C.c_uint32,
                                 C.POINTER(C.c_uint32)]),
     "gdp2d_split_points": (C.c_int, [ctx_p, C.c_void_p, C.c_uint32]),

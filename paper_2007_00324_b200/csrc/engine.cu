@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <limits>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -2055,6 +2056,30 @@ int gdp2d_refine(const gdp2d_mesh_view* in, gdp2d_mesh_buf* out, const gdp2d_par
             std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         fill_summary(x, p, r);
         r->wall_seconds = wall;
+    });
+}
+
+int gdp2d_warmup(int device) {
+    if (device < 0 || device >= kMaxDevices) return GDP2D_ENODEVICE;
+    std::lock_guard<std::mutex> lock(g_cache_mu[device]);
+    if (!g_cache[device]) {
+        const int rc = gdp2d_ctx_create(&g_cache[device], device);
+        if (rc) return rc;
+    }
+    gdp2d_ctx* x = g_cache[device];
+    return run_guarded([&] {
+        DeviceGuard g(x->device);
+        // unit square + five interior points: every Line-1 and refinement
+        // kernel launches at least once
+        static const double xy[] = {0.0,  0.0,  1.0,  0.0,  1.0,  1.0,  0.0,  1.0,  0.31,
+                                    0.27, 0.72, 0.33, 0.45, 0.71, 0.18, 0.62, 0.83, 0.79};
+        static const uint32_t seg[] = {0, 1, 1, 2, 2, 3, 3, 0};
+        build_cdt(x, xy, 9, seg, 4, nullptr);
+        gdp2d_params p;
+        gdp2d_params_init(&p, 30.0, std::numeric_limits<double>::infinity(), GDP2D_RUPPERT);
+        gdp2d_report r;
+        std::memset(&r, 0, sizeof r);
+        refine_loop(x, &p, &r);
     });
 }
 

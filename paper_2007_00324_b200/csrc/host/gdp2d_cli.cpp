@@ -17,6 +17,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
+#include <thread>
 #include <sstream>
 #include <string>
 
@@ -160,6 +161,13 @@ int main(int argc, char** argv) {
             return 2;
         }
     }
+    // CUDA context creation and kernel loading overlap the input parsing and
+    // the host CDT (gdp2d_refine / build_cdt wait on the context's lock)
+    std::thread warm([device] { gdp2d_warmup(device); });
+    struct Join {
+        std::thread& t;
+        ~Join() { t.join(); }
+    } join{warm};
     std::ifstream in(input);
     if (!in) {
         std::fprintf(stderr, "cannot open %s\n", input.c_str());

@@ -359,6 +359,12 @@ def _engine_for(device: int) -> "Engine":
     return eng
 
 
+def warmup(device: int = 0) -> None:
+    """gdp2d_warmup: create the cached device context and load the kernels
+    (one tiny build + refinement), e.g. on a thread while inputs are read."""
+    _raise(A.engine().gdp2d_warmup(int(device)), "gdp2d_warmup")
+
+
 def refine(m: Mesh, q: QualityCriteria, cfg: Optional[EngineConfig] = None) -> RunReport:
     """cdtref::refine (refine.hpp:651) on the GPU; `m` is replaced by the refined mesh.
 

@@ -354,3 +354,21 @@ def test_chew_and_edge_bound_at_million_points(built, mode, ell):
     assert val["min_angle_deg"] >= B_SQRT2_THETA - 1e-9 or mode == 1
     if math.isfinite(ell):
         assert rep.max_edge <= ell
+
+
+def test_warmup_then_one_shot_refine(built):
+    """gdp2d_warmup prepares the cached context (tiny build + refinement); a
+    one-shot refine afterwards gives the same result as without it."""
+    from paper_2007_00324_b200 import QualityCriteria, host
+    from paper_2007_00324_b200.gdp2d import refine, warmup
+    pts, segs = host.generate_pslg(20_000, 2_000, "uniform", 5)
+    m0, _ = host.build_cdt(pts, segs)
+    a = m0.copy()
+    ra = refine(a, QualityCriteria(30.0))
+    warmup(0)
+    b = m0.copy()
+    rb = refine(b, QualityCriteria(30.0))
+    assert ra.steiner_points == rb.steiner_points and rb.bad_triangles == 0
+    np.testing.assert_array_equal(a.tri_v, b.tri_v)
+    with pytest.raises(Exception):
+        warmup(999)
