@@ -1169,7 +1169,8 @@ bool insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, int prefiltered, u32
         if (tail) {
             launch_insert_tail(L, mode, st);
         } else if (!x->check) {
-            launch_insert_persistent(L, mode, g_ins, g_rb, st, x->ev_k[1], k1 | 2, x->lawson_grid2);
+            // (the split/rollback boundary comes from the kernels' start stamps)
+            launch_insert_persistent(L, mode, g_ins, g_rb, st, nullptr, k1 | 2, x->lawson_grid2);
         } else {
             // GDP2D_CHECK=1: structural validation after each kernel
             launch_insert_persistent(L, mode, g_ins, g_rb, st, x->ev_k[1], k1, x->lawson_grid2);
@@ -1215,9 +1216,22 @@ bool insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, int prefiltered, u32
                 x->k_split_s += ev_ms(k_start, x->ev_k[2]) * 1e-3;
                 x->k_split_b += b_split + b_rb;
             } else {
-                x->k_split_s += ev_ms(k_start, x->ev_k[1]) * 1e-3;
+                // the pair's span by events, split at the rollback kernel's
+                // start (globaltimer stamps in state words 10-13; GDP2D_CHECK
+                // records an event between the launches instead)
+                const double pair = ev_ms(k_start, x->ev_k[2]) * 1e-3;
+                double s_split;
+                if (x->check) {
+                    s_split = ev_ms(k_start, x->ev_k[1]) * 1e-3;
+                } else {
+                    u64 t0, t1;
+                    std::memcpy(&t0, x->h_state + 10, sizeof t0);
+                    std::memcpy(&t1, x->h_state + 12, sizeof t1);
+                    s_split = t1 > t0 ? std::min(pair, double(t1 - t0) * 1e-9) : 0.0;
+                }
+                x->k_split_s += s_split;
                 x->k_split_b += b_split;
-                x->k_rb_s += ev_ms(x->ev_k[1], x->ev_k[2]) * 1e-3;
+                x->k_rb_s += pair - s_split;
                 x->k_rb_b += b_rb;
                 x->k_rb_launches += 1;
             }

@@ -1365,6 +1365,11 @@ __device__ __forceinline__ bool fits_and_status(const InsertArgs& a, u32 nv, u32
 // candidate list is small -- the long tail of the refinement (Rule 1).
 template <int MODE>
 __global__ void __launch_bounds__(INSERT_BLOCK, GDP2D_SPLIT_MINB) k_batch_split(const __grid_constant__ InsertArgs a) {
+    // start stamp (state words 10-11): the host splits the kernel pair's
+    // event-timed span at the rollback kernel's stamp, so no event record sits
+    // between the two launches
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        *reinterpret_cast<unsigned long long*>(a.state + 10) = globaltimer();
     const u32 C = vload(a.d_C);
     if (C > a.reg_cap) {   // uniform: the host grows the regions and redoes the batch
         if (blockIdx.x == 0 && threadIdx.x == 0) a.state[0] = INS_REGIONS;
@@ -1426,6 +1431,8 @@ __global__ void __launch_bounds__(INSERT_BLOCK, GDP2D_LAWSON_MINB) k_batch_lawso
 // Kernel 2: phase 3 rollback (skipped when kernel 1 asked for growth).
 template <int MODE>
 __global__ void __launch_bounds__(ROLLBACK_BLOCK) k_batch_rollback(InsertArgs a) {
+    if (blockIdx.x == 0 && threadIdx.x == 0)   // start stamp (state words 12-13)
+        *reinterpret_cast<unsigned long long*>(a.state + 12) = globaltimer();
     if (vload(&a.state[0]) != INS_OK) return;
     // isolated insertions cannot create redundant or dependent points: the
     // detection runs only when some survivor came from a capped claim set
