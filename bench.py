@@ -2,33 +2,52 @@
 """gDP2d refinement benchmark (BASELINE.json metric: refine wall time and
 Steiner points/s on one B200, against the CPU reference on the host cores).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl gdp2d|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--impl gdp2d|reference]
 
+The default workload is the north-star config 3: 5M Gaussian-clustered points
++ 500K segments (SURVEY 8(d) generator, seed 20261017), radius-edge <= sqrt(2).
 A *step* is one complete refinement (Algorithm 1, lines 2-9) of the workload
-PSLG's initial CDT to radius-edge <= sqrt(2): the device-resident working mesh
-is restored from the pristine copy in HBM, then refined to quality.  Line 1
-(build_cdt, untimed in the paper) runs once on the host before
-timing.  Under torchrun every rank refines its own independent PSLG (seed +
-rank): replicas, no data-path collective ("scaling": "weak").
+PSLG's initial CDT: the device-resident working mesh is restored from the
+pristine copy in HBM, then refined to quality.  Line 1 (build_cdt, untimed in
+the paper) runs once on the host before timing.  Under torchrun
+every rank refines its own independent PSLG (seed + rank): replicas, no
+data-path collective ("scaling": "weak"); the max/sum over ranks goes over gloo.
 
 Keys beyond the base contract:
-  e2e          the same metric through the C ABI entry point gdp2d_refine with
-               HOST buffers (H2D of the input mesh + D2H of the refined mesh
-               inside the timed region)
+  e2e          the same metric through the C ABI context calls with HOST
+               buffers: gdp2d_ctx_upload from page-locked memory (H2D), the
+               refinement, gdp2d_ctx_download_to into page-locked memory (D2H),
+               all inside the timed region
+  e2e_dropin   the drop-in caller's path: gdp2d::refine(cdtref::Mesh&, q, cfg)
+               (include/gdp2d_cdtref.hpp) on the reference's own AoS Mesh in
+               pageable memory -- AoS->SoA pack, gdp2d_refine, unpack in place
   roofline     the engine kernel with the largest share of the step (CUDA events
                on the engine stream, every launch in the timed region): its
                algorithmic bytes per launch over its average
                launch time, against MEASURED_PEAKS.json hbm_gbs; traffic = ncu
                dram bytes per launch from profiles/traffic.json when present
-  cpu_baseline the reference (oracle/_ref, unmodified cdtref headers) timed on a
-               bounded sample of the same workload on this box's host cores
+  parity       the refined mesh against the reference's own refinement of the
+               identical PSLG (tests/golden/refine_cfg.json, made by
+               tests/golden/make_refine_golden.py from oracle/_ref): Steiner
+               ratio, min-angle histogram total-variation distance, mean min angle
+  cpu_baseline the reference (oracle/_ref, unmodified cdtref headers) on the
+               IDENTICAL PSLG, host cores of this box, bounded to its first
+               batches so the default run stays within minutes (the full
+               reference refinement is the --impl reference arm)
+
+--impl reference (the driver's reference arm) builds the same PSLG entirely
+inside oracle/_ref (generator + close_hull + build_cdt; no product library is
+loaded) and times cdtref::refine on it with all host threads.  For configs of
+>= 1M points it refines ONCE, and says so.
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import math
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -42,6 +61,7 @@ from paper_2007_00324_b200.replicas import Dist, assign, dist_env, replica_seed 
 
 METRIC = "Refine wall-time (s) & Steiner pts/sec on 1 B200 vs CPU ref on host cores"
 UNIT = "Steiner pts/s"
+SEED = 20261017
 B_THETA = math.degrees(math.asin(1.0 / (2.0 * math.sqrt(2.0))))
 CONFIGS = {
     1: dict(n=100_000, m=1_000, dist="uniform", theta=B_THETA,
@@ -55,7 +75,44 @@ CONFIGS = {
     5: dict(n=2_000_000, m=200_000, dist="uniform", theta=B_THETA,
             name="cfg5: 2M uniform pts + 10% segs per GPU (replicas), radius-edge<=sqrt2"),
 }
-CPU_SAMPLE = dict(n=250_000, m=25_000)   # bounded CPU-reference sample (~5-10 s)
+DEFAULT_CONFIG = 3
+# cpu_baseline leg: the reference's first batches on the identical PSLG
+# (about 15-30 s of one core at config 3); the full run is the reference arm
+CPU_BASELINE_BATCHES = {1: 10000, 2: 6, 3: 1, 4: 4, 5: 4}
+GOLDEN = ROOT / "tests" / "golden" / "refine_cfg.json"
+
+
+def pslg_sha(pts, segs) -> str:
+    """Digest of the closed PSLG (points f64 + segments u32), as in
+    tests/golden/make_refine_golden.py: equal digests = identical input."""
+    import numpy as np
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(pts, np.float64).tobytes())
+    h.update(np.ascontiguousarray(segs, np.uint32).tobytes())
+    return h.hexdigest()[:32]
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor() or platform.machine()
+
+
+def loaded_repo_libs() -> list[str]:
+    """In-repo shared objects mapped into this process (evidence of what ran)."""
+    out = set()
+    try:
+        for line in open("/proc/self/maps"):
+            p = line.split()[-1] if line.strip() else ""
+            if p.endswith(".so") and p.startswith(str(ROOT)):
+                out.add(os.path.relpath(p, ROOT))
+    except OSError:
+        pass
+    return sorted(out)
 
 
 class ClockSampler:
@@ -115,6 +172,85 @@ def load_peaks():
     return 6650.0, "fallback"
 
 
+def golden_record(config: int):
+    if not GOLDEN.exists():
+        return None
+    return json.loads(GOLDEN.read_text()).get(f"cfg{config}")
+
+
+def hist_tv(a, b) -> float:
+    """Total-variation distance between two histograms (normalised)."""
+    sa, sb = float(sum(a)), float(sum(b))
+    if not sa or not sb:
+        return 1.0
+    return 0.5 * sum(abs(x / sa - y / sb) for x, y in zip(a, b))
+
+
+def config_block(cfg: dict, world: int, sha: str, seed: int) -> dict:
+    return {"workload": cfg["name"], "points_per_gpu": cfg["n"], "segments_per_gpu": cfg["m"],
+            "distribution": cfg["dist"], "theta_deg": cfg["theta"], "seed": seed,
+            "pslg_sha": sha, "parallelism": f"replicas{world}" if world > 1 else "single",
+            "l2": "512 MB flush before every step; mesh > L2"}
+
+
+# ---------------------------------------------------------------------------------------
+# reference arm: the unmodified cdtref headers (oracle/_ref) only
+# ---------------------------------------------------------------------------------------
+
+def run_reference_arm(a, world, rank):
+    if rank != 0:
+        return 0
+    from oracle.ref import ref_workload
+    from paper_2007_00324_b200.gdp2d import QualityCriteria   # pure Python (no library)
+    cfg = CONFIGS[a.config]
+    seed = replica_seed(SEED, 0)
+    t0 = time.perf_counter()
+    pts, closed, base = ref_workload(cfg["n"], cfg["m"], cfg["dist"], seed)
+    setup_s = time.perf_counter() - t0
+    sha = pslg_sha(pts, closed)
+    q = QualityCriteria(cfg["theta"])
+    cores = os.cpu_count() or 1
+    big = cfg["n"] >= 1_000_000
+    runs = 1 if big else max(1, a.steps)
+    warm = 0 if big else max(0, a.warmup)
+    for _ in range(warm):
+        base.clone().refine(q, executors=cores)
+    st, secs, batches = [], [], []
+    for _ in range(runs):
+        m = base.clone()
+        rep = m.refine(q, executors=cores)
+        st.append(rep.steiner_points)
+        secs.append(rep.wall_seconds)
+        batches.append(len(rep.batches))
+    total = sum(secs)
+    value = sum(st) / total
+    sample = (f"cdtref::refine (oracle/_ref: the unmodified reference headers, g++ -O3) on the "
+              f"identical {cfg['name'].split(':')[0]} PSLG (pslg_sha {sha}), "
+              f"ExecutionMode::Parallel with {cores} executors, {runs} full run(s)"
+              + (" -- one run for configs >= 1M points (BASELINE.md section 2), "
+                 f"{a.steps} requested" if big else ""))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": runs, "requested_steps": a.steps, "warmup": warm, "requested_warmup": a.warmup,
+        "ms_per_step": total / runs * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_block(cfg, world, sha, seed),
+        "same_config": True,
+        "refine_wall_s": total / runs, "steiner_points": st[-1], "batches": batches[-1],
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": sample, "cpu_model": cpu_model()},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "setup_s": setup_s,
+        "native_so_loaded": loaded_repo_libs(),
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------------------
+
 LINE1 = {}   # first workload's PSLG + reference build_cdt time (SURVEY 8(f) rank 1)
 
 
@@ -126,7 +262,7 @@ def make_workload(cfg: dict, seed: int):
     if not LINE1:
         LINE1.update(pts=pts, closed=closed, ref_s=time.perf_counter() - t0,
                      ref_tris=int(mesh.tri_alive.sum()))
-    return mesh
+    return mesh, pslg_sha(pts, closed)
 
 
 def line1_device(device: int) -> dict:
@@ -154,48 +290,25 @@ def mesh_bytes(m) -> int:
                                               "seg_tri"))
 
 
-def cpu_reference_steps(cfg, steps, seed, executors):
-    """Time the reference refine (oracle/_ref) on a bounded sample; returns
-    (steiner per step list, seconds per step list, sample description)."""
-    from paper_2007_00324_b200 import QualityCriteria
+def cpu_baseline_leg(cfg: dict, config: int, mesh, sha: str) -> dict:
+    """The reference (oracle/_ref) on the identical initial CDT, bounded to its
+    first CPU_BASELINE_BATCHES batches, one core (EngineConfig{} is sequential)."""
     from oracle.ref import RefMesh
-    sample = dict(cfg, **CPU_SAMPLE)
-    mesh = make_workload(sample, seed)
-    base = RefMesh.from_mesh(mesh)
-    q = QualityCriteria(cfg["theta"])
-    st, secs = [], []
-    for _ in range(steps):
-        m = base.clone()
-        rep = m.refine(q, executors=executors)
-        st.append(rep.steiner_points)
-        secs.append(rep.wall_seconds)
-    desc = (f"reference cdtref::refine (oracle/_ref, g++ -O3) on a {sample['n']}-point "
-            f"{sample['dist']} PSLG + {sample['m']} segs (same generator and quality bound as "
-            f"the workload), executors={executors}")
-    return st, secs, desc
-
-
-def run_reference_arm(a, world, rank):
-    cfg = CONFIGS[a.config]
-    if rank != 0:
-        return 0
-    cores = os.cpu_count() or 1
-    warm_st, warm_s, _ = cpu_reference_steps(cfg, a.warmup, 1234, cores) if a.warmup else ([], [], "")
-    st, secs, desc = cpu_reference_steps(cfg, a.steps, 1234, cores)
-    total = sum(secs)
-    value = sum(st) / total
-    line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-        "steps": a.steps, "warmup": a.warmup, "ms_per_step": total / a.steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": cfg["name"], "cpu_sample": CPU_SAMPLE},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
-                         "sample": desc},
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "refine_wall_s": total / a.steps,
-    }
-    print(json.dumps(line), flush=True)
-    return 0
+    from paper_2007_00324_b200 import EngineConfig, QualityCriteria
+    cap = CPU_BASELINE_BATCHES[config]
+    rm = RefMesh.from_mesh(mesh)
+    rep = rm.refine(QualityCriteria(cfg["theta"]), EngineConfig(iteration_cap=cap))
+    full = not rep.iteration_cap_hit
+    return {"value": rep.steiner_points / rep.wall_seconds, "unit": UNIT, "cores": 1,
+            "kind": "reference", "cpu_model": cpu_model(),
+            "sample": (f"cdtref::refine (oracle/_ref, g++ -O3, EngineConfig{{}} sequential) on the "
+                       f"identical PSLG (pslg_sha {sha}), "
+                       + ("the full refinement" if full else
+                          f"its first {len(rep.batches)} batches (iteration_cap={cap}); "
+                          "the tail batches are slower per point, so this overstates the "
+                          "reference's full-run rate. The full run is --impl reference")),
+            "seconds": rep.wall_seconds, "steiner": rep.steiner_points,
+            "batches": len(rep.batches)}
 
 
 def main():
@@ -203,20 +316,21 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="gdp2d", choices=["gdp2d", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps")
+    ap.add_argument("--dropin-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     a = ap.parse_args()
     world, rank, local = dist_env()
     if a.impl == "reference":
         return run_reference_arm(a, world, rank)
 
-    import numpy as np
     import torch
 
-    from paper_2007_00324_b200 import Engine, QualityCriteria, refine
+    from paper_2007_00324_b200 import Engine, QualityCriteria
     from paper_2007_00324_b200 import _abi as A
+    from paper_2007_00324_b200 import host
 
     dist = Dist(world, rank, local)
     device = local
@@ -226,11 +340,12 @@ def main():
     # config 5: a batch of 8 independent PSLGs spread round-robin over the
     # ranks; otherwise one PSLG per rank (weak scaling)
     items = assign(8, world, rank) if a.config == 5 else [0]
+    seeds = [replica_seed(SEED, rank if a.config != 5 else 0, it) for it in items]
     t0 = time.time()
-    meshes = [make_workload(cfg, replica_seed(20261017, rank if a.config != 5 else 0, it))
-              for it in items]
+    work = [make_workload(cfg, s) for s in seeds]
+    meshes = [w[0] for w in work]
+    sha = work[0][1]
     setup_s = time.time() - t0
-    mesh = meshes[0]
     lib = A.engine()
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{device}")  # > 126 MB L2
 
@@ -272,9 +387,8 @@ def main():
     steiner_all = dist.sum(steiner_local)
     value = steiner_all / dev_s_max
     last = reps[-1]
-    eng = engines[0]
 
-    # ---- e2e: the public API with HOST buffers (page-locked) ----
+    # ---- e2e: the C ABI context calls with HOST buffers (page-locked) ----
     # Every step: H2D of the input mesh from pinned host memory (Engine.upload
     # -> gdp2d_ctx_upload), the refinement, and D2H of the whole refined mesh
     # into pinned host buffers (Engine.download_to -> gdp2d_ctx_download_to).
@@ -311,6 +425,19 @@ def main():
     e2e_total = dist.max(sum(e2e_s))
     e2e_value = dist.sum(e2e_st) / e2e_total
     e2e_eng.close()
+    del pins
+
+    # ---- e2e through the drop-in C++ shim (reference AoS Mesh, pageable) ----
+    dropin = None
+    if a.dropin_steps > 0:
+        host.time_dropin(meshes[0], cfg["theta"], 1, device)          # warm the cached context
+        ds, dst = host.time_dropin(meshes[0], cfg["theta"], a.dropin_steps, device)
+        dropin = {"value": dst * a.dropin_steps / ds, "unit": UNIT,
+                  "wall_s_per_step": ds / a.dropin_steps, "steps": a.dropin_steps,
+                  "path": "gdp2d::refine(cdtref::Mesh&, q, EngineConfig{}) from "
+                          "include/gdp2d_cdtref.hpp: AoS->SoA pack, gdp2d_refine with pageable "
+                          "host buffers (H2D + loop + D2H), unpack in place",
+                  "h2d_bytes_per_step": mesh_bytes(meshes[0]), "steiner": dst}
 
     # ---- roofline: the dominant engine kernel (largest share of the step) ----
     peak, peak_kind = load_peaks()
@@ -341,24 +468,43 @@ def main():
     dom = max(per_kernel, key=lambda k: per_kernel[k]["share_of_step"] or 0.0)
     refine_gbs = last.algorithmic_bytes() / last.device_seconds / 1e9
     # device validators on the last timed output (outside the timed region):
-    # structure, local CDT, quality and conformity (k_verify.cu)
+    # structure, local CDT, quality, conformity and the min-angle histogram
     validation = engines[-1].validate(q)
+
+    parity = None
+    gold = golden_record(a.config) if rank == 0 and a.config != 5 else None
+    if gold:
+        parity = {
+            "reference": "tests/golden/refine_cfg.json (oracle/_ref cdtref::refine, sequential)",
+            "same_pslg": gold["pslg_sha"] == sha,
+            "reference_steiner": gold["steiner_points"],
+            "steiner_ratio": last.steiner_points / gold["steiner_points"],
+            "reference_batches": gold["batches"],
+            "hist_bin_deg": gold["hist_bin_deg"],
+            "min_angle_hist_tv": hist_tv(validation["min_angle_hist"], gold["min_angle_hist"]),
+            "mean_min_angle_deg": validation["mean_min_angle_deg"],
+            "reference_mean_min_angle_deg": gold["mean_min_angle_deg"],
+            "reference_wall_s_in_container": gold["wall_seconds"],
+        }
+    hist_full = validation.pop("min_angle_hist")
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": dev_s_max / a.steps * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg["name"], "points_per_gpu": cfg["n"],
-                   "segments_per_gpu": cfg["m"], "theta_deg": cfg["theta"],
-                   "parallelism": f"replicas{world}" if world > 1 else "single",
-                   "l2": "512 MB flush before every step; mesh > L2"},
+        "config": config_block(cfg, world, sha, seeds[0]),
         "refine_wall_s": dev_s_max / a.steps,
         "steiner_points": last.steiner_points,
         "batches": len(last.batches),
         "quality": {"bad_triangles": last.bad_triangles, "min_angle_deg": last.min_angle_deg},
         "validation": validation,
+        "min_angle_hist": {"bin_deg": 0.5, "counts": hist_full},
+        "parity": parity,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "wall_s_per_step": e2e_total / e2e_steps},
+                "d2h_bytes_per_step": d2h, "wall_s_per_step": e2e_total / e2e_steps,
+                "path": "C ABI: gdp2d_ctx_upload (pinned) + gdp2d_ctx_refine + "
+                        "gdp2d_ctx_download_to (pinned)"},
+        "e2e_dropin": dropin,
         "roofline": {"kernel": dom, "bound": "hbm", "achieved": per_kernel[dom]["achieved"],
                      "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": per_kernel[dom]["frac"], "traffic": per_kernel[dom]["traffic"],
@@ -378,12 +524,10 @@ def main():
     if rank == 0 and LINE1:
         line["line1_cdt"] = line1_device(device)
 
-    # ---- CPU baseline (rank 0, N = 1 only) ----
+    # ---- CPU baseline (rank 0, N = 1 only): the identical PSLG ----
     if world == 1 and not a.no_cpu_baseline:
-        st, secs, desc = cpu_reference_steps(cfg, 1, 1234, 1)
-        line["cpu_baseline"] = {"value": st[0] / secs[0], "unit": UNIT, "cores": 1,
-                                "kind": "reference", "sample": desc,
-                                "seconds": secs[0], "steiner": st[0]}
+        line["cpu_baseline"] = cpu_baseline_leg(cfg, a.config, meshes[0], sha)
+    line["native_so_loaded"] = loaded_repo_libs()
     if rank == 0:
         print(json.dumps(line), flush=True)
     for e in engines:

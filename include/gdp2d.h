@@ -208,6 +208,9 @@ typedef struct gdp2d_report {
     double   rollback_seconds;
     uint64_t rollback_bytes;
     uint64_t rollback_launches;
+    /* gdp2d_refine only: H2D of the input + refine loop + D2H of the output,
+     * timed once the device context exists (0 from gdp2d_ctx_refine). */
+    double   e2e_seconds;
 } gdp2d_report;
 
 /* SplitCandidate (refine.hpp:71) in exchange form. */
@@ -285,6 +288,12 @@ uint64_t gdp2d_ctx_device_bytes(gdp2d_ctx* ctx);
 
 /* ---- device validators (k_verify.cu) ------------------- */
 
+/* Histogram of per-triangle minimum angles: bin k counts alive triangles whose
+ * smallest corner angle (min_angle_degrees' formula, verify.hpp:186-200) lies
+ * in [k, k+1) * GDP2D_HIST_BIN_DEG degrees; the last bin takes the rest. */
+#define GDP2D_HIST_BINS 120
+#define GDP2D_HIST_BIN_DEG 0.5
+
 /* What the reference validates on the host (mesh.hpp:505-557,
  * verify.hpp:92-200) computed on the device for the working mesh: */
 typedef struct gdp2d_validation {
@@ -295,6 +304,8 @@ typedef struct gdp2d_validation {
     uint64_t bad_triangles;        /* is_bad_triangle && triangle_resolvable    */
     uint64_t conformity_failures;  /* 0 = every input segment exactly covered   */
     double   min_angle_deg;
+    double   mean_min_angle_deg;   /* mean over alive triangles of their min angle */
+    uint64_t min_angle_hist[GDP2D_HIST_BINS];
 } gdp2d_validation;
 
 /* Validate the working mesh against p's quality criteria and the uploaded

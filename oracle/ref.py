@@ -74,6 +74,13 @@ def ref_lib() -> C.CDLL:
             "ref_predicates_batch": (None, [C.c_int, C.c_void_p, C.c_uint32, C.POINTER(A.Params),
                                             C.c_void_p]),
             "ref_circumcenter_batch": (None, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p]),
+            "ref_min_angle_hist": (C.c_uint64, [mp, C.c_double, C.c_uint32, C.c_void_p,
+                                                C.POINTER(C.c_double)]),
+            "gdp2d_host_generate": (C.c_int, [C.c_uint64, C.c_uint32, C.c_int, C.c_uint64,
+                                               C.POINTER(C.POINTER(C.c_double)),
+                                               C.POINTER(C.POINTER(C.c_uint32)),
+                                               C.POINTER(C.c_uint32)]),
+            "gdp2d_host_free": (None, [C.c_void_p]),
         }
         for k, (res, args) in sig.items():
             f = getattr(lib, k)
@@ -126,6 +133,47 @@ def params(q: QualityCriteria, cfg: EngineConfig | None = None) -> A.Params:
     p.split_depth_cap = cfg.split_depth_cap
     p.batch_size_cap = cfg.batch_size_cap
     return p
+
+
+HIST_BIN_DEG = 0.5   # min-angle histogram: 120 bins of 0.5 degrees over [0, 60]
+HIST_BINS = 120
+
+
+def ref_generate_pslg(n: int, m: int, dist: str = "uniform", seed: int = 20261017):
+    """The SURVEY 8(d) generator (pslg_gen.cpp) as compiled into the oracle
+    library: (points (n,2) f64, segments (m',2) u32), hull not yet closed.
+    Bit-identical to paper_2007_00324_b200.host.generate_pslg (same source)."""
+    lib = ref_lib()
+    xy = C.POINTER(C.c_double)()
+    segs = C.POINTER(C.c_uint32)()
+    mout = C.c_uint32(0)
+    if lib.gdp2d_host_generate(n, m, 1 if dist == "gaussian" else 0, seed, C.byref(xy),
+                               C.byref(segs), C.byref(mout)):
+        raise RuntimeError("generator failed")
+    pts = np.ctypeslib.as_array(xy, shape=(2 * n,)).reshape(n, 2).copy()
+    s = (np.ctypeslib.as_array(segs, shape=(2 * mout.value,)).reshape(-1, 2).copy()
+         if mout.value else np.zeros((0, 2), np.uint32))
+    lib.gdp2d_host_free(C.cast(xy, C.c_void_p))
+    lib.gdp2d_host_free(C.cast(segs, C.c_void_p))
+    return pts, s
+
+
+def ref_close_hull(pts, segs) -> np.ndarray:
+    """close_hull (cdt.hpp:447) through the reference library."""
+    pts = np.ascontiguousarray(pts, np.float64)
+    segs = np.ascontiguousarray(segs, np.uint32).reshape(-1, 2)
+    out = np.zeros((len(segs) + len(pts), 2), np.uint32)
+    k = ref_lib().ref_close_hull(pts.ctypes.data, len(pts), segs.ctypes.data, len(segs),
+                                 out.ctypes.data)
+    return out[:k].copy()
+
+
+def ref_workload(n: int, m: int, dist: str, seed: int):
+    """Generator + close_hull + build_cdt entirely inside oracle/_ref:
+    (points, closed segments, RefMesh of the initial CDT)."""
+    pts, segs = ref_generate_pslg(n, m, dist, seed)
+    closed = ref_close_hull(pts, segs)
+    return pts, closed, RefMesh.build_cdt(pts, closed)
 
 
 def _err() -> str:
@@ -290,6 +338,14 @@ class RefMesh:
     def count_bad(self, q: QualityCriteria) -> int:
         p = params(q)
         return int(ref_lib().ref_count_bad(self.h, C.byref(p)))
+
+    def min_angle_hist(self, bin_deg: float = HIST_BIN_DEG, nbins: int = HIST_BINS):
+        """(histogram of per-triangle min angles, mean min angle) with the
+        corner-angle formula of min_angle_degrees (verify.hpp:186-200)."""
+        h = np.zeros(nbins, np.uint64)
+        s = C.c_double()
+        n = ref_lib().ref_min_angle_hist(self.h, bin_deg, nbins, h.ctypes.data, C.byref(s))
+        return h, (s.value / n if n else 0.0)
 
     def canonical_triangles(self) -> np.ndarray:
         _, t, _ = self.sizes()

@@ -15,9 +15,15 @@
 //   build_cdt / close_hull    cdt.hpp:483 / cdt.hpp:447
 //   validators                mesh.hpp:505-557, verify.hpp:92-200
 //   predicates                predicates.hpp:63-185, refine.hpp:192
+//   min-angle histogram       verify.hpp:186-200 / refine.hpp:625-632 (per triangle)
+// The SURVEY 8(d) synthetic PSLG generator (paper_2007_00324_b200/csrc/host/
+// pslg_gen.cpp, plain host code) is compiled into this library as well, so the
+// CPU reference legs build their input without loading any product library.
 // Mesh exchange uses the gdp2d_mesh_view SoA layout of include/gdp2d.h.
 // Build: oracle/Makefile (g++ -std=c++20 -O3 -DNDEBUG -ffp-contract=off).
 
+#include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <exception>
 #include <string>
@@ -333,6 +339,36 @@ int ref_refine_sequential(ref_mesh* h, const gdp2d_params* p, gdp2d_report* r) {
     } catch (const std::exception& e) {
         return fail(e);
     }
+}
+
+// Histogram of per-triangle minimum angles, in degrees, with the corner angle
+// formula of min_angle_degrees (verify.hpp:186-200): bin k counts alive
+// triangles whose min angle lies in [k*bin_deg, (k+1)*bin_deg); the last bin
+// also takes everything above.  *sum gets the sum of the min angles.
+uint64_t ref_min_angle_hist(const ref_mesh* h, double bin_deg, uint32_t nbins, uint64_t* hist,
+                            double* sum) {
+    const Mesh& m = *reinterpret_cast<const Mesh*>(h);
+    std::memset(hist, 0, sizeof(uint64_t) * nbins);
+    double s = 0.0;
+    uint64_t n = 0;
+    for (const Triangle& t : m.triangles) {
+        if (!t.alive) continue;
+        double best = 180.0;
+        for (int i = 0; i < 3; ++i) {
+            const Point2& p = m.pos(t.v[i]);
+            const Point2 u = m.pos(t.v[Mesh::next(i)]) - p;
+            const Point2 v = m.pos(t.v[Mesh::prev(i)]) - p;
+            best = std::min(best, std::atan2(std::abs(cross(u, v)), dot(u, v)) * 180.0 /
+                                      3.14159265358979323846);
+        }
+        uint32_t k = static_cast<uint32_t>(best / bin_deg);
+        if (k >= nbins) k = nbins - 1;
+        ++hist[k];
+        s += best;
+        ++n;
+    }
+    *sum = s;
+    return n;
 }
 
 // quality_report (refine.hpp:716)

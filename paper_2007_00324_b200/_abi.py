@@ -78,13 +78,15 @@ class Report(C.Structure):
                 ("scan_launches", C.c_uint64), ("kernel_launches", C.c_uint64),
                 ("split_seconds", C.c_double), ("split_bytes", C.c_uint64),
                 ("split_launches", C.c_uint64), ("rollback_seconds", C.c_double),
-                ("rollback_bytes", C.c_uint64), ("rollback_launches", C.c_uint64)]
+                ("rollback_bytes", C.c_uint64), ("rollback_launches", C.c_uint64),
+                ("e2e_seconds", C.c_double)]
 
 
 class Validation(C.Structure):
     _fields_ = [("structure_failure", C.c_uint32), ("structure_tri", C.c_uint32),
                 ("cdt_violations", C.c_uint64), ("bad_triangles", C.c_uint64),
-                ("conformity_failures", C.c_uint64), ("min_angle_deg", C.c_double)]
+                ("conformity_failures", C.c_uint64), ("min_angle_deg", C.c_double),
+                ("mean_min_angle_deg", C.c_double), ("min_angle_hist", C.c_uint64 * 120)]
 
 
 class NodeEle(C.Structure):
@@ -187,6 +189,8 @@ HOST_SIGNATURES = {
                                              C.POINTER(C.c_char_p)]),
     "gdp2d_host_free_buf": (None, [C.POINTER(MeshBuf)]),
     "gdp2d_host_last_error": (C.c_char_p, []),
+    "gdp2d_host_time_dropin": (C.c_int, [C.POINTER(MeshView), C.c_double, C.c_int, C.c_int,
+                                         C.POINTER(C.c_double), C.POINTER(C.c_uint64)]),
 }
 
 _LIBS: dict[str, C.CDLL] = {}

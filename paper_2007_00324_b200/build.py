@@ -2,8 +2,9 @@
 
   lib/libgdp2d.so       CUDA engine (sm_100a only), C ABI of include/gdp2d.h
   lib/libgdp2d_host.so  host side kept from the reference (PSLG/mesh I/O, Line-1
-                        build_cdt) + the synthetic PSLG generator; compiled against
-                        /root/reference/proj/include when that tree is present
+                        build_cdt, the drop-in shim's timing entry) + the synthetic
+                        PSLG generator; compiled against /root/reference/proj/include
+                        when that tree is present; links libgdp2d.so
   oracle/_ref/*.so      test-infrastructure checkers (oracle/Makefile)
 
 Run ``python -m paper_2007_00324_b200.build`` or ``__graft_entry__.build()``.
@@ -90,11 +91,15 @@ def build_host(force: bool = False) -> Path | None:
         if target.exists():
             return target  # prebuilt (GPU box: /root/reference is absent)
         raise RuntimeError(f"{REF_INCLUDE} missing and no prebuilt {target}")
-    if not force and _newer(target, srcs + [INCLUDE / "gdp2d.h", Path(__file__)]):
+    deps = srcs + [INCLUDE / "gdp2d.h", INCLUDE / "gdp2d_cdtref.hpp", Path(__file__),
+                   LIB / "libgdp2d.so"]
+    if not force and _newer(target, deps):
         return target
     tmp = target.with_suffix(".so.tmp")
+    # links libgdp2d.so for the drop-in timing entry (gdp2d_host_time_dropin)
     _run(["g++", "-std=c++20", "-O3", "-DNDEBUG", "-ffp-contract=off", "-fPIC", "-shared",
-          "-pthread", "-I", str(INCLUDE), "-I", str(REF_INCLUDE), *map(str, srcs), "-o", str(tmp)])
+          "-pthread", "-I", str(INCLUDE), "-I", str(REF_INCLUDE), *map(str, srcs), "-o", str(tmp),
+          "-L", str(LIB), "-lgdp2d", "-Wl,-rpath,$ORIGIN"])
     os.replace(tmp, target)
     return target
 

@@ -2053,7 +2053,6 @@ int gdp2d_refine(const gdp2d_mesh_view* in, gdp2d_mesh_buf* out, const gdp2d_par
                  gdp2d_report* r, int device) {
     if (!in || !out || !p || !r) return GDP2D_EINVAL;
     if (device < 0 || device >= kMaxDevices) return GDP2D_ENODEVICE;
-    const auto t0 = std::chrono::steady_clock::now();
     std::lock_guard<std::mutex> lock(g_cache_mu[device]);
     if (!g_cache[device]) {
         const int rc = gdp2d_ctx_create(&g_cache[device], device);
@@ -2062,14 +2061,16 @@ int gdp2d_refine(const gdp2d_mesh_view* in, gdp2d_mesh_buf* out, const gdp2d_par
     gdp2d_ctx* x = g_cache[device];
     return run_guarded([&] {
         DeviceGuard g(x->device);
+        // e2e clock: from the held lock and a live context to the refined
+        // mesh in host memory; refine_loop sets wall_seconds (loop only)
+        const auto t0 = std::chrono::steady_clock::now();
         upload(x, in);
         reset_work(x, p->theta_deg);
         refine_loop(x, p, r);
         download(x, out);
-        const double wall =
+        r->e2e_seconds =
             std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         fill_summary(x, p, r);
-        r->wall_seconds = wall;
     });
 }
 
@@ -2242,6 +2243,8 @@ int gdp2d_ctx_validate(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_validation* ou
         out->bad_triangles = v.bad_triangles;
         out->conformity_failures = v.conformity_failures;
         out->min_angle_deg = v.min_angle_deg;
+        out->mean_min_angle_deg = v.mean_min_angle_deg;
+        for (int i = 0; i < GDP2D_HIST_BINS; ++i) out->min_angle_hist[i] = v.min_angle_hist[i];
     });
 }
 

@@ -6,6 +6,7 @@
 #include <string>
 #include <vector>
 
+#include "gdp2d.h"
 #include "gdp2d_common.cuh"
 #include "gdp2d_geom.cuh"
 
@@ -265,6 +266,8 @@ struct VerifySummary {
     u32 structure_failure, structure_tri;
     ull cdt_violations, bad_triangles, conformity_failures;
     double min_angle_deg;
+    double mean_min_angle_deg;
+    ull min_angle_hist[GDP2D_HIST_BINS];
     size_t scratch_needed;   // nonzero: scratch too small, nothing run
 };
 VerifySummary launch_verify(const DevMesh& m, const Quality& q, const uint2* in_sv, u32 nIn,

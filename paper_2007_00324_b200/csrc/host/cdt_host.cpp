@@ -5,7 +5,9 @@
 //   close_hull            cdt.hpp:447
 //   build_cdt             cdt.hpp:483 (Line 1; PAPER.md:508 excludes it from timing)
 //   write_node_ele        pslg_io.hpp:294
-// The refinement itself (Lines 2-9) never runs here: it is libgdp2d.so.
+// The refinement itself (Lines 2-9) never runs here: it is libgdp2d.so, reached
+// through the drop-in shim (include/gdp2d_cdtref.hpp) by gdp2d_host_time_dropin.
+#include <chrono>
 #include <cstdlib>
 #include <cstring>
 #include <exception>
@@ -17,7 +19,9 @@
 #include "cdtref/cdt.hpp"
 #include "cdtref/mesh.hpp"
 #include "cdtref/pslg_io.hpp"
+#include "cdtref/refine.hpp"
 #include "gdp2d.h"
+#include "gdp2d_cdtref.hpp"
 
 using namespace cdtref;
 
@@ -285,6 +289,36 @@ void gdp2d_host_free_buf(gdp2d_mesh_buf* b) {
                     b->seg_parent, b->seg_encroached, b->seg_alive, b->seg_tri};
     for (void* p : ptrs) std::free(p);
     std::memset(b, 0, sizeof *b);
+}
+
+// The drop-in caller's path, timed: gdp2d::refine(cdtref::Mesh&, q, cfg)
+// (include/gdp2d_cdtref.hpp) on the reference's own AoS Mesh in pageable
+// memory -- pack to SoA, gdp2d_refine (H2D, device loop, D2H), unpack in
+// place -- exactly what a cdtref caller gets after swapping the namespace.
+// The reference Mesh is built from *in once; each of `steps` calls refines a
+// fresh copy of it (the copy is untimed).  Writes the summed call time and
+// the last call's Steiner count.
+int gdp2d_host_time_dropin(const gdp2d_mesh_view* in, double theta_deg, int steps, int device,
+                           double* seconds, uint64_t* steiner) {
+    try {
+        const Mesh base = view_to_mesh(in);
+        QualityCriteria q;
+        q.theta = theta_deg;
+        const EngineConfig cfg{};
+        double total = 0.0;
+        for (int i = 0; i < steps; ++i) {
+            Mesh m = base;
+            const auto t0 = std::chrono::steady_clock::now();
+            const RunReport rep = gdp2d::refine(m, q, cfg, device);
+            total += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            *steiner = rep.steiner_points;
+        }
+        *seconds = total;
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
 }
 
 }  // extern "C"

@@ -19,6 +19,8 @@
 #include <fstream>
 #include <thread>
 #include <sstream>
+#include <limits>
+#include <stdexcept>
 #include <string>
 
 #include "cdtref/cdt.hpp"
@@ -148,9 +150,17 @@ int main(int argc, char** argv) {
     bool device_io = false;    // --device-io: validate + compact on the device
     for (int i = 2; i < argc; ++i) {
         const std::string a = argv[i];
-        auto val = [&]() -> const char* { return i + 1 < argc ? argv[++i] : "0"; };
+        auto val = [&]() -> const char* {
+            if (i + 1 >= argc) throw std::invalid_argument("flag " + a + " needs a value");
+            return argv[++i];
+        };
+        try {
         if (a == "--theta") q.theta = std::atof(val());
-        else if (a == "--ell") q.ell = std::atof(val());
+        else if (a == "--ell") {
+            // 0 (or negative) = unbounded, as the reference CLI (tools/cdtref.cpp:85)
+            const double v = std::atof(val());
+            q.ell = v > 0.0 ? v : std::numeric_limits<double>::infinity();
+        }
         else if (a == "--chew") q.mode = cdtref::RefineMode::Chew;
         else if (a == "--out") prefix = val();
         else if (a == "--device") device = std::atoi(val());
@@ -158,6 +168,10 @@ int main(int argc, char** argv) {
         else if (a == "--device-io") device_io = true;
         else {
             std::fprintf(stderr, "unknown flag %s\n", a.c_str());
+            return 2;
+        }
+        } catch (const std::invalid_argument& e) {
+            std::fprintf(stderr, "%s\n", e.what());
             return 2;
         }
     }

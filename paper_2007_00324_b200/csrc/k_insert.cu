@@ -267,9 +267,9 @@ void launch_lawson_persistent(const DevMesh& m, u32 round0, u32 cur0, u32 n0, u3
 // ---- redundancy detection (refine.hpp:551-608) ----------------------------------------
 
 // Star of v in rotation order (incident_triangles, mesh.hpp:145-171, interior
-// case).  Returns the size, or 0 if the fan is open / too large.
-__device__ __forceinline__ int walk_star(const DevMesh& m, u32 v, u32* st, int* si, int cap,
-                                         u32* nb = nullptr) {
+// case).  Returns the size, 0 if the fan is open or broken, or -1 if it has
+// more than cap triangles (st/si are then incomplete).
+__device__ __forceinline__ int walk_star(const DevMesh& m, u32 v, u32* st, int* si, int cap) {
     const u32 t0 = m.vtri[v];
     if (t0 == NONE) return 0;
     u32 cur = t0;
@@ -277,10 +277,34 @@ __device__ __forceinline__ int walk_star(const DevMesh& m, u32 v, u32* st, int* 
     do {
         const uint4 tv = m.tv[cur];
         const int i = tv.x == v ? 0 : (tv.y == v ? 1 : (tv.z == v ? 2 : -1));
-        if (i < 0 || k >= cap) return 0;
+        if (i < 0) return 0;
+        if (k >= cap) return -1;
         st[k] = cur;
         si[k] = i;
-        if (nb) nb[k] = comp(tv, nxt(i));   // the star's next link vertex
+        ++k;
+        const u32 c = comp(m.tn[cur], nxt(i));
+        if (c == NONE) return 0;
+        cur = etri(c);
+    } while (cur != t0);
+    return k;
+}
+
+// The same rotation as a stream: fn(t, i, tv) for every star triangle (i =
+// v's slot in t), nothing stored, so a vertex of any degree is handled (a
+// disc bounded by an N-gon gives its centre degree N).  Returns the size, or
+// 0 if the fan is open or broken (fn may have seen part of it).
+static constexpr int STAR_WALK_LIMIT = 1 << 20;
+template <class Fn>
+__device__ __forceinline__ int stream_star(const DevMesh& m, u32 v, Fn&& fn) {
+    const u32 t0 = m.vtri[v];
+    if (t0 == NONE) return 0;
+    u32 cur = t0;
+    int k = 0;
+    do {
+        const uint4 tv = m.tv[cur];
+        const int i = tv.x == v ? 0 : (tv.y == v ? 1 : (tv.z == v ? 2 : -1));
+        if (i < 0 || k >= STAR_WALK_LIMIT) return 0;
+        fn(cur, i, tv);
         ++k;
         const u32 c = comp(m.tn[cur], nxt(i));
         if (c == NONE) return 0;
@@ -307,58 +331,40 @@ __device__ __noinline__ u32 detect_a_one(const DevMesh& m, u64 depth_cap, u32 V0
     const u32 v = V0 + j;
     if (collect_dep) f.hcnt[j] = 0;
     if (f.cc[j] && !f.removed[j]) {
-        u32 st[MAX_STAR], nb[MAX_STAR];
-        int si[MAX_STAR];
-        const int k = walk_star(m, v, st, si, MAX_STAR, nb);
-        if (collect_dep) {
-            u32 cnt = 0;
-            for (int q = 0; q < k; ++q) {
-                const u32 x = nb[q];
-                if (x < V0 || x >= V0 + F) continue;
-                const u32 jx = x - V0;
-                if (!f.cc[jx] || f.removed[jx] == 1 || !prio_gt(f, jx, j)) continue;
-                if (cnt == (u32)DEP_HMAX) {
-                    cnt = 255;
-                    break;
+        // one streamed walk: the lowest-id splittable subsegment on an edge
+        // opposite v that v encroaches, and (collect_dep) the higher-priority
+        // same-batch circumcenters among the link vertices
+        const double2 pv = m.xy[v];
+        u32 best = NONE, cnt = 0;
+        const int k = stream_star(m, v, [&](u32 t, int i, const uint4& tv) {
+            if (collect_dep && cnt != 255u) {
+                const u32 x = comp(tv, nxt(i));   // the star's next link vertex
+                if (x >= V0 && x < V0 + F) {
+                    const u32 jx = x - V0;
+                    if (f.cc[jx] && f.removed[jx] != 1 && prio_gt(f, jx, j)) {
+                        if (cnt == (u32)DEP_HMAX)
+                            cnt = 255u;
+                        else
+                            f.hlist[(size_t)j * DEP_HMAX + cnt++] = jx;
+                    }
                 }
-                f.hlist[(size_t)j * DEP_HMAX + cnt++] = jx;
             }
-            f.hcnt[j] = (uint8_t)cnt;
-        }
+            const u32 s = comp(m.ts[t], i);
+            if (s == NONE || s >= best) return;
+            const uint2 sv = m.sv[s];
+            if (!encroaches<MODE>(m.xy[sv.x], m.xy[sv.y], pv)) return;
+            if ((u64)m.sdepth[s] >= depth_cap) return;
+            if (!subseg_split_ok(m, s, subseg_mid(m, s))) return;
+            best = s;
+        });
+        if (collect_dep) f.hcnt[j] = (uint8_t)cnt;
         if (k == 0 && atomicCAS(&ctr->err_code, 0u, (u32)DERR_OPEN_STAR) == 0u) {
-            // dbg: vtri, alive, fresh index, xy, walk steps, reason
-            // (1 vertex missing from a fan triangle, 2 star > MAX_STAR, 3 open fan)
             ctr->err_info = v;
-            const u32 t0 = m.vtri[v];
-            ctr->dbg[0] = (double)t0;
+            ctr->dbg[0] = (double)m.vtri[v];
             ctr->dbg[1] = (double)m.valive[v];
             ctr->dbg[2] = (double)j;
-            ctr->dbg[3] = m.xy[v].x;
-            ctr->dbg[4] = m.xy[v].y;
-            u32 cur = t0;
-            int kk = 0, why = 0;
-            for (; t0 != NONE && kk < 256; ++kk) {
-                const uint4 tv = m.tv[cur];
-                const int ii = tv.x == v ? 0 : (tv.y == v ? 1 : (tv.z == v ? 2 : -1));
-                if (ii < 0) { why = 1; break; }
-                const u32 cn = comp(m.tn[cur], nxt(ii));
-                if (cn == NONE) { why = 3; break; }
-                cur = etri(cn);
-                if (cur == t0) { why = 2; break; }
-            }
-            ctr->dbg[5] = (double)kk;
-            ctr->dbg[6] = (double)why;
-        }
-        const double2 pv = m.xy[v];
-        u32 best = NONE;
-        for (int q = 0; q < k; ++q) {
-            const u32 s = comp(m.ts[st[q]], si[q]);
-            if (s == NONE || s >= best) continue;
-            const uint2 sv = m.sv[s];
-            if (!encroaches<MODE>(m.xy[sv.x], m.xy[sv.y], pv)) continue;
-            if ((u64)m.sdepth[s] >= depth_cap) continue;
-            if (!subseg_split_ok(m, s, subseg_mid(m, s))) continue;
-            best = s;
+            ctr->dbg[3] = pv.x;
+            ctr->dbg[4] = pv.y;
         }
         if (best != NONE) {
             mark = 1;
@@ -383,19 +389,15 @@ __device__ __noinline__ void detect_b_one(const DevMesh& m, u32 V0, u32 F, u32 j
                                           const FreshInfo& f) {
     if (!f.cc[j] || f.removed[j] || f.mark[j] == 1) return;
     const u32 v = V0 + j;
-    u32 st[MAX_STAR];
-    int si[MAX_STAR];
-    const int k = walk_star(m, v, st, si, MAX_STAR);
-    for (int q = 0; q < k; ++q) {
-        const u32 x = comp(m.tv[st[q]], nxt(si[q]));
-        if (x < V0 || x >= V0 + F) continue;
+    bool dep = false;
+    stream_star(m, v, [&](u32, int i, const uint4& tv) {
+        const u32 x = comp(tv, nxt(i));
+        if (dep || x < V0 || x >= V0 + F) return;
         const u32 jx = x - V0;
-        if (!f.cc[jx] || f.removed[jx] == 1 || f.mark[jx] == 1) continue;
-        if (prio_gt(f, jx, j)) {
-            f.mark[j] = 2;
-            break;
-        }
-    }
+        if (!f.cc[jx] || f.removed[jx] == 1 || f.mark[jx] == 1) return;
+        if (prio_gt(f, jx, j)) dep = true;
+    });
+    if (dep) f.mark[j] = 2;
 }
 
 // (b) from the list detect_a_one collected: the first higher-priority
@@ -431,23 +433,20 @@ __device__ __noinline__ bool detect_b_mis_one(const DevMesh& m, u32 V0, u32 F, u
         return false;
     }
     const u32 v = V0 + j;
-    u32 st[MAX_STAR];
-    int si[MAX_STAR];
-    const int k = walk_star(m, v, st, si, MAX_STAR);
     u32 cnt = 0;
     bool overflow = false;
-    for (int q = 0; q < k; ++q) {
-        const u32 x = comp(m.tv[st[q]], nxt(si[q]));
-        if (x < V0 || x >= V0 + F) continue;
+    stream_star(m, v, [&](u32, int i, const uint4& tv) {
+        const u32 x = comp(tv, nxt(i));
+        if (x < V0 || x >= V0 + F) return;
         const u32 jx = x - V0;
-        if (!f.cc[jx] || f.removed[jx] == 1 || f.mark[jx] == 1) continue;
+        if (!f.cc[jx] || f.removed[jx] == 1 || f.mark[jx] == 1) return;
         if (prio_gt(f, jx, j)) {
             if (cnt < (u32)DEP_HMAX)
                 f.hlist[(size_t)j * DEP_HMAX + cnt++] = jx;
             else
                 overflow = true;
         }
-    }
+    });
     f.hcnt[j] = (uint8_t)cnt;
     if (overflow) {       // cannot track them all: the conservative rule
         f.dstat[j] = 2;
@@ -518,24 +517,33 @@ void launch_detect(const DevMesh& m, const Quality& q, u64 depth_cap, u32 V0, u3
 // ---- parallel vertex removal (remove_free_vertex + flop, mesh.hpp:261-304,442-466) ----
 
 __device__ __forceinline__ void rm_claim_one(const DevMesh& m, const u32* __restrict__ list, u32 i,
-                                             const TriAux& x, const WorkLists& w, Counters* ctr) {
+                                             u32 V0, const TriAux& x, const FreshInfo& f,
+                                             const WorkLists& w, Counters* ctr) {
     const u32 v = list[i];
     u32* st = w.star + (size_t)i * MAX_STAR;
     int si[MAX_STAR];
     const int k = walk_star(m, v, st, si, MAX_STAR);
-    w.star_len[i] = (u32)k;
+    w.star_len[i] = k > 0 ? (u32)k : 0u;
+    if (k < 0) {
+        // Star larger than the ear-clipping buffers: keep the vertex, as the
+        // reference does when remove_free_vertex returns false (mesh.hpp:462,
+        // refine.hpp:580/601); it is never selected again.
+        f.removed[v - V0] = 2;
+        atomicAdd(&ctr->rm_kept, 1u);
+        return;
+    }
     if (k < 3) {
-        raise_err(ctr, k == 0 ? DERR_STAR_TOO_LARGE : DERR_OPEN_STAR, v);
+        raise_err(ctr, DERR_OPEN_STAR, v);
         w.star_len[i] = 0;
         return;
     }
     for (int q = 0; q < k; ++q) atomicMin(&x.owner[st[q]], v);
 }
 
-__global__ void k_rm_claim(DevMesh m, const u32* __restrict__ list, u32 n, TriAux x,
-                           WorkLists w, Counters* ctr) {
+__global__ void k_rm_claim(DevMesh m, const u32* __restrict__ list, u32 n, u32 V0, TriAux x,
+                           FreshInfo f, WorkLists w, Counters* ctr) {
     const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) rm_claim_one(m, list, i, x, w, ctr);
+    if (i < n) rm_claim_one(m, list, i, V0, x, f, w, ctr);
 }
 
 // Remove v by ear-clipping its link polygon: each ear is one degree-reducing
@@ -754,7 +762,7 @@ void launch_removal_round(const DevMesh& m, u32 round, u32 V0, TriAux a, FreshIn
                           WorkLists w, u32 cur, u32 n, u32 widx, Counters* d_ctr,
                           cudaStream_t st) {
     if (!n) return;
-    note_launch(), k_rm_claim<<<(n + 127) / 128, 128, 0, st>>>(m, w.rm[cur], n, a, w, d_ctr);
+    note_launch(), k_rm_claim<<<(n + 127) / 128, 128, 0, st>>>(m, w.rm[cur], n, V0, a, f, w, d_ctr);
     note_launch(), k_rm_apply<<<(n + 63) / 64, 64, 0, st>>>(m, w.rm[cur], n, round, V0, widx, cur ^ 1u, a, f, w,
                                             d_ctr);
     note_launch(), k_rm_post<<<(n + 255) / 256, 256, 0, st>>>(n, a, w);
@@ -1309,7 +1317,7 @@ __device__ void rollback_loop(const InsertArgs& a, const Exec& ex, u32 nv, u32 n
             ring_advance(a, ex, step);
             const u32 round = a.round0 + step;
             const u32* list = w.rm[rcur];
-            for (u32 i = ex.tid; i < nrm; i += ex.nthr) rm_claim_one(m, list, i, a.x, w, a.ctr);
+            for (u32 i = ex.tid; i < nrm; i += ex.nthr) rm_claim_one(m, list, i, V0, a.x, a.f, w, a.ctr);
             ex.sync();
             trace(a, ex.leader(), TR_RM_CLAIM, nrm);
             for (u32 i = ex.tid; i < nrm; i += ex.nthr)

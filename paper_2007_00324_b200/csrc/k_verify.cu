@@ -9,7 +9,10 @@
 //                 (exact) -- for a valid triangulation equivalent to the
 //                 global constrained-Delaunay property
 //   quality       is_bad_triangle && triangle_resolvable (refine.hpp:169-206)
-//                 count + min angle
+//                 count + min angle + the histogram of per-triangle minimum
+//                 angles (GDP2D_HIST_BINS bins of GDP2D_HIST_BIN_DEG degrees,
+//                 corner formula of min_angle_degrees, verify.hpp:186-200)
+//                 and their mean (fixed-point sum, so it is deterministic)
 //   conformity    conformity_ok (verify.hpp:147-183): every alive subsegment
 //                 is a mesh edge carrying it (structure), its parent is an
 //                 input segment, its interior endpoints lie on the parent
@@ -28,11 +31,18 @@ struct VerifyAcc {
     unsigned long long bad;
     unsigned long long conformity_failures;
     unsigned long long min_angle_bits;   // double bits, atomicMin on non-negative values
+    unsigned long long angle_sum_fx;     // sum of per-triangle min angles * 2^kAngleFx
+    unsigned long long hist[GDP2D_HIST_BINS];
 };
 
+constexpr int kAngleFx = 30;
+
 __global__ void k_verify_tris(DevMesh m, Quality q, VerifyAcc* acc) {
+    __shared__ u32 hist[GDP2D_HIST_BINS];
+    for (u32 i = threadIdx.x; i < GDP2D_HIST_BINS; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
     const u32 t = blockIdx.x * blockDim.x + threadIdx.x;
-    ull viol = 0, bad = 0;
+    ull viol = 0, bad = 0, angle_fx = 0;
     double min_ang = 180.0;
     if (t < m.nT) {
         const uint4 tv = m.tv[t];
@@ -45,6 +55,10 @@ __global__ void k_verify_tris(DevMesh m, Quality q, VerifyAcc* acc) {
                 min_ang = fmin(min_ang, atan2(fabs(cross2(u, v)), dot2(u, v)) * 180.0 /
                                             3.14159265358979323846);
             }
+            u32 bin = (u32)(min_ang / GDP2D_HIST_BIN_DEG);
+            if (bin >= GDP2D_HIST_BINS) bin = GDP2D_HIST_BINS - 1;
+            atomicAdd(&hist[bin], 1u);
+            angle_fx = (ull)__double2ll_rn(ldexp(min_ang, kAngleFx));
             const uint4 tn = m.tn[t], ts = m.ts[t];
             for (int e = 0; e < 3; ++e) {
                 const u32 c = comp(tn, e);
@@ -58,6 +72,9 @@ __global__ void k_verify_tris(DevMesh m, Quality q, VerifyAcc* acc) {
     }
     block_add<ull>(&acc->cdt_violations, viol);
     block_add<ull>(&acc->bad, bad);
+    block_add<ull>(&acc->angle_sum_fx, angle_fx);
+    for (u32 i = threadIdx.x; i < GDP2D_HIST_BINS; i += blockDim.x)
+        if (hist[i]) atomicAdd(&acc->hist[i], (ull)hist[i]);
     for (int o = 16; o > 0; o >>= 1) min_ang = fmin(min_ang, __shfl_down_sync(0xFFFFFFFFu, min_ang, o));
     if ((threadIdx.x & 31) == 0 && min_ang < 180.0)
         atomicMin(&acc->min_angle_bits, (ull)__double_as_longlong(min_ang));
@@ -130,14 +147,14 @@ VerifySummary launch_verify(const DevMesh& m, const Quality& q, const uint2* in_
                             cudaStream_t st) {
     VerifySummary out{};
     // scratch: acc | deg[V] | in_deg[V] | len_sum[nIn]
-    const size_t need = 64 + 8ull * m.nV + 8ull * nIn + 16;
+    const size_t need = sizeof(VerifyAcc) + 8ull * m.nV + 8ull * nIn + 16;
     if (scratch_bytes < need) {
         out.scratch_needed = need;
         return out;
     }
     char* base = static_cast<char*>(scratch);
     VerifyAcc* acc = reinterpret_cast<VerifyAcc*>(base);
-    u32* deg = reinterpret_cast<u32*>(base + 64);
+    u32* deg = reinterpret_cast<u32*>(base + sizeof(VerifyAcc));
     u32* in_deg = deg + m.nV;
     double* len_sum = reinterpret_cast<double*>(
         (reinterpret_cast<uintptr_t>(in_deg + m.nV) + 15) & ~uintptr_t(15));
@@ -165,6 +182,12 @@ VerifySummary launch_verify(const DevMesh& m, const Quality& q, const uint2* in_
     double ma;
     memcpy(&ma, &h.min_angle_bits, sizeof ma);
     out.min_angle_deg = ma;
+    ull n_alive = 0;
+    for (int i = 0; i < GDP2D_HIST_BINS; ++i) {
+        out.min_angle_hist[i] = h.hist[i];
+        n_alive += h.hist[i];
+    }
+    out.mean_min_angle_deg = n_alive ? ldexp((double)h.angle_sum_fx, -kAngleFx) / n_alive : 0.0;
     return out;
 }
 

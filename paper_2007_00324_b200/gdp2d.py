@@ -145,6 +145,7 @@ class RunReport:
     rollback_bytes: int = 0
     rollback_launches: int = 0
     kernel_launches: int = 0
+    e2e_seconds: float = 0.0
 
     def algorithmic_bytes(self) -> int:
         """SURVEY §8(d) bytes_alg from the per-batch counters."""
@@ -183,6 +184,7 @@ def _report(r: A.Report, arr) -> RunReport:
                      split_seconds=r.split_seconds, split_bytes=r.split_bytes,
                      split_launches=r.split_launches, rollback_seconds=r.rollback_seconds,
                      rollback_bytes=r.rollback_bytes, rollback_launches=r.rollback_launches,
+                     e2e_seconds=r.e2e_seconds,
                      kernel_launches=r.kernel_launches)
 
 
@@ -283,14 +285,34 @@ class Mesh:
         return np.take_along_axis(t, idx, axis=1)
 
 
+class _PinnedBlock:
+    """One gdp2d_pinned_alloc allocation, freed when the last numpy view of it
+    is gone (the views reference it through their ctypes base buffer)."""
+
+    def __init__(self, lib, nbytes: int):
+        self.lib = lib
+        self.ptr = lib.gdp2d_pinned_alloc(nbytes)
+        if not self.ptr:
+            raise MemoryError(f"gdp2d_pinned_alloc({nbytes}) failed")
+
+    def __del__(self):
+        try:
+            if self.ptr:
+                self.lib.gdp2d_pinned_free(self.ptr)
+                self.ptr = None
+        except Exception:
+            pass
+
+
 class PinnedPool:
     """Page-locked host buffers (gdp2d_pinned_alloc) for meshes of up to
     (nv, nt, ns) elements: uploads / downloads from here run at full link rate.
-    ``mesh(...)`` returns a Mesh whose arrays are views into the pool (no copy)."""
+    ``mesh(...)`` returns a Mesh whose arrays are views into the pool (no copy).
+    Each allocation lives as long as any view of it, so growing or closing the
+    pool never frees memory a returned mesh still uses."""
 
     def __init__(self, nv: int, nt: int, ns: int):
         self.lib = A.engine()
-        self._ptrs = []
         self._bufs = {}
         self._alloc(nv, nt, ns)
 
@@ -306,24 +328,14 @@ class PinnedPool:
         for name, dt, w in _FIELDS:
             n = self.caps["v" if name in _VERT else "t" if name in _TRI else "s"] * w
             nbytes = n * np.dtype(dt).itemsize
-            ptr = self.lib.gdp2d_pinned_alloc(nbytes)
-            if not ptr:
-                raise MemoryError(f"gdp2d_pinned_alloc({nbytes}) failed")
-            self._ptrs.append(ptr)
-            buf = (C.c_uint8 * nbytes).from_address(ptr)
+            block = _PinnedBlock(self.lib, nbytes)
+            buf = (C.c_uint8 * nbytes).from_address(block.ptr)
+            buf._owner = block          # views -> buf -> block: freed with the last view
             self._bufs[name] = np.frombuffer(buf, dtype=dt, count=n)
 
     def close(self) -> None:
-        for p in self._ptrs:
-            self.lib.gdp2d_pinned_free(p)
-        self._ptrs = []
+        """Drop the pool's references (memory still viewed elsewhere stays valid)."""
         self._bufs = {}
-
-    def __del__(self):
-        try:
-            self.close()
-        except Exception:
-            pass
 
     def mesh(self, nv: int, nt: int, ns: int, batch_epoch: int = 0) -> "Mesh":
         counts = {"v": nv, "t": nt, "s": ns}
@@ -334,9 +346,7 @@ class PinnedPool:
             n = counts["v" if name in _VERT else "t" if name in _TRI else "s"]
             a = self._bufs[name][: n * w]
             arrays[name] = a.reshape(-1, w) if w > 1 else a
-        m = Mesh(batch_epoch=batch_epoch, **arrays)
-        m._pool = self   # keep the pinned memory alive with the views
-        return m
+        return Mesh(batch_epoch=batch_epoch, **arrays)
 
     def load(self, src: "Mesh") -> "Mesh":
         """Copy a mesh into the pool (outside any timed region)."""
@@ -519,11 +529,15 @@ class Engine:
 
     def validate(self, q: QualityCriteria) -> dict:
         """Device validators (k_verify.cu) on the working mesh: structure, local
-        CDT, quality and conformity to the uploaded input segments."""
+        CDT, quality, conformity to the uploaded input segments, and the
+        histogram of per-triangle min angles (GDP2D_HIST_BINS bins of
+        GDP2D_HIST_BIN_DEG degrees) with their mean."""
         p = make_params(q)
         v = A.Validation()
         _raise(self.lib.gdp2d_ctx_validate(self.ctx, C.byref(p), C.byref(v)), "gdp2d_ctx_validate")
-        return {f: getattr(v, f) for f, _ in A.Validation._fields_}
+        out = {f: getattr(v, f) for f, _ in A.Validation._fields_}
+        out["min_angle_hist"] = [int(x) for x in v.min_angle_hist]
+        return out
 
     def device_bytes(self) -> int:
         return int(self.lib.gdp2d_ctx_device_bytes(self.ctx))

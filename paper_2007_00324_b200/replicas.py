@@ -1,7 +1,7 @@
 """Multi-GPU = independent replicas: one process per GPU, one
-mesh per process, no data-path collective.  torch.distributed is used only
-for the barrier and the max/sum of per-rank timings (NCCL on GPUs, gloo in
-the CPU tests)."""
+mesh per process, no data-path collective.  torch.distributed (gloo, host
+side: north_star says no NCCL) is used only for the barrier and the max/sum
+of per-rank timings, which are taken on each device with CUDA events."""
 from __future__ import annotations
 
 import os
@@ -27,7 +27,7 @@ def replica_seed(base: int, rank: int, item: int = 0) -> int:
 class Dist:
     """Barrier + max/sum of host floats over ranks; a no-op for world == 1."""
 
-    def __init__(self, world: int, rank: int, local: int, backend: str = "nccl"):
+    def __init__(self, world: int, rank: int, local: int, backend: str = "gloo"):
         self.world, self.rank, self.local, self.backend = world, rank, local, backend
         if world > 1:
             import torch

@@ -374,3 +374,23 @@ def test_warmup_then_one_shot_refine(built):
     np.testing.assert_array_equal(a.tri_v, b.tri_v)
     with pytest.raises(Exception):
         warmup(999)
+
+
+@pytest.mark.parametrize("n_sides", [97, 128, 400])
+def test_high_degree_ngon(built, n_sides):
+    """A disc bounded by a regular N-gon with no interior points: after batch 1
+    the inserted centre has degree N, and every fan triangle has a subsegment
+    opposite it, so redundancy detection walks a star of N triangles
+    (walk_star capped stars at MAX_STAR = 96 and failed the
+    refine).  The reference finishes this input; so must the device."""
+    from gdp2d_testlib import regular_polygon
+    from paper_2007_00324_b200 import QualityCriteria
+    b = np.array(regular_polygon(n_sides, 1.0), np.float64)
+    segs = np.array([(i, (i + 1) % n_sides) for i in range(n_sides)], np.uint32)
+    q = QualityCriteria(B_SQRT2_THETA)
+    out, closed, rep, rref = _run(b, segs, q)
+    assert not rep.iteration_cap_hit
+    check_invariants(out, b, closed, q)
+    assert rep.bad_triangles == 0
+    assert abs(rep.steiner_points - rref.steiner_points) <= 0.10 * rref.steiner_points + 8, \
+        (rep.steiner_points, rref.steiner_points)

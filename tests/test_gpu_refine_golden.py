@@ -1,0 +1,128 @@
+"""Full-refinement parity at the BASELINE sizes (north_star):
+the device refines the identical PSLGs the reference refined in
+tests/golden/refine_cfg.json (tests/golden/make_refine_golden.py, oracle/_ref
+cdtref::refine, refine.hpp:651-713) and the result is compared with the
+reference's own:
+
+  * the input is identical: the PSLG digest equals the golden record's;
+  * device validators clean: check_structure (mesh.hpp:505-551), exact local
+    CDT, no bad triangle (refine.hpp:192-206), conformity (verify.hpp:147-183);
+  * Steiner count within 10% of the reference's (acceptance.cpp:290-307 uses
+    1.3x + 8 against the sequential yardstick; north_star asks 10%);
+  * min-angle distribution comparable (north_star; verify.hpp:186-200): the
+    total-variation distance between the two 0.5-degree histograms of
+    per-triangle min angles is below HIST_TV_MAX, and the mean per-triangle
+    min angle is within MEAN_ANGLE_TOL degrees of the reference's.
+
+Also the bit-exact phase comparison (collect / locate / claim / cavity) on
+the 1M-point config-2 initial CDT, where ties and exact-predicate paths are
+far more frequent than on the 20K meshes of test_gpu_phases.py.
+"""
+import json
+import math
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from test_gpu_phases import _same
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = Path(__file__).resolve().parent / "golden" / "refine_cfg.json"
+STEINER_BAND = 0.10       # north_star: within 10% of the reference
+HIST_TV_MAX = 0.05        # total-variation distance of the min-angle histograms
+MEAN_ANGLE_TOL = 0.5      # degrees, mean per-triangle min angle
+B_THETA = math.degrees(math.asin(1.0 / (2.0 * math.sqrt(2.0))))
+
+
+def hist_tv(a, b) -> float:
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return 0.5 * float(np.abs(a / a.sum() - b / b.sum()).sum())
+
+
+def _pslg_sha(pts, segs) -> str:
+    import hashlib
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(pts, np.float64).tobytes())
+    h.update(np.ascontiguousarray(segs, np.uint32).tobytes())
+    return h.hexdigest()[:32]
+
+
+@pytest.mark.parametrize("config", ["cfg1", "cfg2", "cfg3", "cfg4"])
+def test_refine_matches_reference_at_baseline_size(built, config):
+    from paper_2007_00324_b200 import Engine, QualityCriteria, host
+    gold = json.loads(GOLDEN.read_text())[config]
+    pts, segs = host.generate_pslg(gold["n"], gold["m"], gold["dist"], gold["seed"])
+    mesh, closed = host.build_cdt(pts, segs)
+    assert _pslg_sha(pts, closed) == gold["pslg_sha"], "not the PSLG the reference refined"
+    assert (mesh.n_vertices, mesh.n_triangles, mesh.n_subsegments) == \
+        (gold["initial"]["vertices"], gold["initial"]["triangles"], gold["initial"]["subsegments"])
+    q = QualityCriteria(gold["theta"])
+    with Engine() as eng:
+        eng.upload(mesh)
+        rep = eng.refine(q)
+        v = eng.validate(q)
+    assert not rep.iteration_cap_hit
+    assert v["structure_failure"] == 0, v
+    assert v["cdt_violations"] == 0, v
+    assert v["bad_triangles"] == 0 and rep.bad_triangles == 0, v
+    assert v["conformity_failures"] == 0, v
+    assert v["min_angle_deg"] >= gold["theta"] - 1e-9 or gold["theta"] > 30.0
+    ratio = rep.steiner_points / gold["steiner_points"]
+    assert abs(ratio - 1.0) <= STEINER_BAND, (rep.steiner_points, gold["steiner_points"])
+    tv = hist_tv(v["min_angle_hist"], gold["min_angle_hist"])
+    assert tv <= HIST_TV_MAX, tv
+    assert abs(v["mean_min_angle_deg"] - gold["mean_min_angle_deg"]) <= MEAN_ANGLE_TOL, \
+        (v["mean_min_angle_deg"], gold["mean_min_angle_deg"])
+    print(f"{config}: steiner {rep.steiner_points} vs {gold['steiner_points']} ({ratio:.4f}), "
+          f"hist TV {tv:.4f}, mean min angle {v['mean_min_angle_deg']:.3f} vs "
+          f"{gold['mean_min_angle_deg']:.3f}, {len(rep.batches)} vs {gold['batches']} batches")
+
+
+def test_device_histogram_matches_reference_formula(built):
+    """The device min-angle histogram of a mesh equals the reference's
+    (verify.hpp:186-200 corner formula) on the same mesh, bin for bin."""
+    from paper_2007_00324_b200 import Engine, QualityCriteria, host
+    from oracle.ref import RefMesh
+    pts, segs = host.generate_pslg(200_000, 20_000, "gaussian", 5)
+    mesh, _ = host.build_cdt(pts, segs)
+    q = QualityCriteria(B_THETA)
+    with Engine() as eng:
+        eng.upload(mesh)
+        eng.refine(q)
+        v = eng.validate(q)
+        out = eng.download()
+    h, mean = RefMesh.from_mesh(out).min_angle_hist()
+    assert sum(v["min_angle_hist"]) == int(h.sum())
+    # libdevice atan2 and glibc atan2 may differ by an ulp right at a bin edge
+    assert int(np.abs(np.asarray(v["min_angle_hist"], np.int64) - h.astype(np.int64)).sum()) <= 4
+    assert abs(v["mean_min_angle_deg"] - mean) < 1e-9
+
+
+@pytest.mark.parametrize("theta", [B_THETA, 30.0])
+def test_phases_bit_exact_cfg2_initial_cdt(built, theta):
+    """collect / locate / claim / cavity on the 1M-point config-2 initial CDT,
+    GPU vs the reference on the same uploaded mesh, record for record."""
+    from paper_2007_00324_b200 import Engine, QualityCriteria, host
+    from oracle.ref import RefMesh
+    pts, segs = host.generate_pslg(1_000_000, 100_000, "uniform", 20261017)
+    m, _ = host.build_cdt(pts, segs)
+    q = QualityCriteria(theta=theta)
+    rm = RefMesh.from_mesh(m)
+    with Engine() as eng:
+        eng.upload(m)
+        g = eng.collect(q)
+        r = rm.collect(q)
+        _same(g, r, "cfg2 collect")
+        g = eng.locate(r)
+        r = rm.locate(r)
+        _same(g, r, "cfg2 locate")
+        g = eng.claim_filter(r)
+        r = rm.claim_filter(r)
+        _same(g, r, "cfg2 claim")
+        g = eng.cavity_filter(r, 32)
+        rr = rm.cavity_filter(r, 32)
+        _same(g, rr, "cfg2 cavity")
+    assert len(r) > 100_000
