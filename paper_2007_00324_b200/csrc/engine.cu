@@ -303,6 +303,48 @@ struct Tracer {
 constexpr size_t kStatusWords = 20 + (sizeof(Counters) + 3) / 4;
 static_assert(sizeof(Counters) % 8 == 0, "Counters follows word 20 (8-byte aligned)");
 
+// Little's-law batch sizing (PAPER.md:94 and Rules 1-2, :104-137; the
+// throughput of ruleskit.hpp:55-58 little_throughput as record_batch
+// :128-142 measures it per batch; the cap policy of refine.hpp:252-261).
+// Every finished batch is one measurement: attempted A, concurrency U (the
+// retained insertions -- the useful work) and latency L (its device time),
+// throughput T = U / L.  The size of the next batch follows from them:
+//   * low workload -- C at most the measured occupancy of the filter kernels
+//     (`resident` candidates in flight, cudaOccupancy*): never capped (Rule 1);
+//   * high workload: A* = the attempted size of the best measured throughput.
+//     If a batch that attempted MORE than A* achieved LESS throughput, the
+//     measurements say oversubscription costs more than it yields (Rule 2):
+//     a larger batch is cut to A* (highest priorities kept, as the reference's
+//     batch_size_cap).  Without that evidence the batch runs whole.
+struct LittleSizer {
+    struct Rec {
+        double a, u, l;
+    };
+    std::vector<Rec> h;
+    u64 resident = 0;
+    void reset() { h.clear(); }
+    void record(u64 attempted, u64 useful, double latency) {
+        if (attempted && latency > 0) h.push_back({(double)attempted, (double)useful, latency});
+    }
+    // the cap level A* (0: no measured evidence for a cap)
+    u64 level() const {
+        if (h.empty()) return 0;
+        size_t b = 0;
+        for (size_t i = 1; i < h.size(); ++i)
+            if (h[i].u / h[i].l > h[b].u / h[b].l) b = i;
+        const double tb = h[b].u / h[b].l;
+        for (const Rec& r : h)
+            if (r.a > 1.05 * h[b].a && r.u / r.l < tb)
+                return std::max<u64>(resident, (u64)h[b].a);
+        return 0;
+    }
+    u64 cap(u64 C) const {
+        if (C <= resident) return 0;
+        const u64 lv = level();
+        return lv && C > lv ? lv : 0;
+    }
+};
+
 struct gdp2d_ctx {
     int device = 0;
     Tracer tr;
@@ -348,7 +390,7 @@ struct gdp2d_ctx {
     bool in_valid = false;        // in_sv derived from the current pristine mesh
     void* vscratch = nullptr;     // validator scratch
     size_t vscratch_bytes = 0;
-    u32 little_cap = 0;           // Little's-law batch cap (resident cavity-filter candidates)
+    LittleSizer little;           // Little's-law batch sizing (measured C / L per batch)
     bool lawson_kernel = false;   // GDP2D_LAWSON_KERNEL=1: separate Lawson launch (measured slower)
     bool legacy_insert = false;   // GDP2D_INSERT=legacy: host-driven insertion rounds
     RoundCtr* ring = nullptr;     // [4] step counters of the persistent insertion kernel
@@ -669,7 +711,7 @@ void ctx_init(gdp2d_ctx* x, int device) {
         }
     }
     CK(cudaMalloc(&x->sel_state, select_state_bytes()));
-    x->little_cap = cavity_resident_candidates(device);
+    x->little.resident = cavity_resident_candidates(device);
     if (const char* e = std::getenv("GDP2D_LAWSON_KERNEL")) x->lawson_kernel = e[0] == '1';
     const char* li = std::getenv("GDP2D_INSERT");
     x->legacy_insert = (li && std::string(li) == "legacy") || x->validate || x->lawson_rounds;
@@ -1273,6 +1315,7 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
     x->k_split_s = x->k_rb_s = 0;
     x->k_split_b = x->k_rb_b = x->k_launches = x->k_rb_launches = 0;
     x->have_c_prev = false;
+    x->little.reset();
     CK(cudaEventRecord(x->ev[GDP2D_NPHASES + 1], st));  // loop start
     for (u64 iter = 0;; ++iter) {
         if (iter >= p->iteration_cap) {
@@ -1301,9 +1344,14 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
         // device; the filter kernels read it, the loop learns it with the
         // batch's end-of-batch readback.  The first batch of a call, the
         // batch caps and rule 4 off take the synchronous path.
+        // Little's-law sizing needs C on the host only where a cap can
+        // apply: a measured cap level exists and the previous batch came
+        // within half of it (batches shrink over a refinement)
+        const u64 little_lv = p->little_batch_sizing ? x->little.level() : 0;
+        const bool little_sync = little_lv && (u64)x->c_prev * 2 > little_lv;
         const bool ncs = !x->sync_collect && !x->legacy_insert && x->have_c_prev &&
                          p->rule4_unified_collection != 0 && p->batch_size_cap == 0 &&
-                         !p->little_batch_sizing;
+                         !little_sync;
         u32 C = launch_collect(m, q, p->rule4_unified_collection != 0, x->flags, x->c, x->ccap,
                                x->scan, x->d_ctr, st, cache, &tris_scanned, x->d_C,
                                nullptr, ncs ? nullptr : x->ev[GDP2D_NPHASES + 3], !ncs);
@@ -1328,7 +1376,10 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
         // Batch sizing (refine.hpp:252-261 + the Little's-law cap): keep the
         // highest priorities; the list keeps its order, the rest is dead
         u64 cap = p->batch_size_cap;
-        if (p->little_batch_sizing && (cap == 0 || x->little_cap < cap)) cap = x->little_cap;
+        if (p->little_batch_sizing && !ncs) {
+            const u64 lc = x->little.cap(C);
+            if (lc && (cap == 0 || lc < cap)) cap = lc;
+        }
         u32 attempted = (!ncs && cap > 0 && C > cap) ? (u32)cap : C;
         if (!ncs && attempted < C) launch_select_topk(x->c, C, attempted, x->sel_state, st);
         // split points are fused into collect: one event ends both phases
@@ -1466,6 +1517,7 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
         }
         for (double s : bm.phase_seconds) bm.latency += s;
         bm.throughput = bm.latency > 0 ? retained / bm.latency : 0.0;
+        x->little.record(attempted, retained, bm.latency);
         bm.waste_fraction = attempted ? double(attempted - retained) / attempted : 0.0;
         bm.walk_steps = h.walk_steps;
         bm.cavity_visits = h.cavity_visits;
