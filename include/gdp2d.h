@@ -119,7 +119,9 @@ typedef struct gdp2d_params {
     uint32_t rule1_compaction_threshold; /* 1024: below it work lists are not compacted */
     uint32_t rule2_filtering_enabled;    /* cavity filter on/off               */
     uint32_t rule4_unified_collection;   /* subsegs + triangles in one batch   */
-    uint32_t little_batch_sizing;    /* GPU: Little's-law batch cap (0 = off)   */
+    uint32_t little_batch_sizing;    /* GPU: Little's-law batch sizing from the
+                                        measured concurrency / latency of the
+                                        previous batches (1 = on, the default)  */
     uint32_t insert_mode;            /* GDP2D_INSERT_* (see below)               */
     uint32_t reserved0;
     uint64_t iteration_cap;          /* 10000                                   */

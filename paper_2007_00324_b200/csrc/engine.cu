@@ -377,13 +377,10 @@ struct gdp2d_ctx {
     void* qscratch = nullptr;
     u32 round = 0;
     bool full_scan = true;        // next collect recomputes every triangle
-    bool validate = false;        // GDP2D_VALIDATE=1: check structure after every round
-    bool lawson_rounds = false;   // GDP2D_LAWSON=rounds: per-round launches
     bool full_collect = false;    // GDP2D_COLLECT=full: never reuse cached flags
     int lawson_grid = 0;          // persistent Lawson kernel grid (co-resident blocks)
     int insert_grid = 0;          // persistent insertion kernel grid
     int rollback_grid = 0;        // persistent rollback kernel grid
-    int lawson_grid2 = 0;         // separate batch Lawson kernel grid
     void* sel_state = nullptr;    // batch_size_cap radix-select state
     uint2* in_sv = nullptr;       // input segments by parent index (validators)
     u32 n_in = 0;
@@ -391,15 +388,12 @@ struct gdp2d_ctx {
     void* vscratch = nullptr;     // validator scratch
     size_t vscratch_bytes = 0;
     LittleSizer little;           // Little's-law batch sizing (measured C / L per batch)
-    bool lawson_kernel = false;   // GDP2D_LAWSON_KERNEL=1: separate Lawson launch (measured slower)
-    bool legacy_insert = false;   // GDP2D_INSERT=legacy: host-driven insertion rounds
     RoundCtr* ring = nullptr;     // [4] step counters of the persistent insertion kernel
     u32* ins_state = nullptr;     // [16] status words (see k_insert.cu; [8] = unsafe flag)
     u32* h_state = nullptr;       // pinned copy
     cudaEvent_t ev_k[3] = {};     // around the split and rollback kernels
     double k_split_s = 0, k_rb_s = 0;   // per refine call: roofline accumulators
     u64 k_split_b = 0, k_rb_b = 0, k_launches = 0, k_rb_launches = 0;
-    bool tail_kernel = false;   // GDP2D_TAIL=1: batches <= small_c as one k_batch_tail launch
     u32* d_C = nullptr;           // candidate count written by collect (device)
     // One device block holds everything the host reads after a batch, so the
     // end-of-batch readback is a single copy: ins_state [0,16), insertion
@@ -423,7 +417,6 @@ struct gdp2d_ctx {
                                   // (smaller batches filter inside the grid-mode batch kernel)
     bool dep_mis = false;         // GDP2D_DEP=mis: dependent pairs by the priority-MIS rule
     bool check = false;           // GDP2D_CHECK=1: validate after each insertion kernel
-    int extras = 2;               // GDP2D_EXTRAS: 2 rewrite table (default), 1 far side in main claims
     u32* scan_part = nullptr;     // [3 * insert_grid] plan chunk sums
     RoundCtr* rcs = nullptr;      // per-round counters of the persistent kernel
     u32* d_res = nullptr;
@@ -458,7 +451,7 @@ namespace {
 void cands_free(DevCands& c) {
     dfree(c.pt); dfree(c.key); dfree(c.id); dfree(c.tie); dfree(c.loc);
     dfree(c.kind); dfree(c.alive); dfree(c.lkind); dfree(c.ledge); dfree(c.fb);
-    dfree(c.red); dfree(c.unsafe); dfree(c.far); dfree(c.bw);
+    dfree(c.red); dfree(c.unsafe); dfree(c.far);
 }
 
 void ensure_cands(gdp2d_ctx* x, u32 n) {
@@ -469,8 +462,6 @@ void ensure_cands(gdp2d_ctx* x, u32 n) {
     dalloc(x->c.loc, cap); dalloc(x->c.kind, cap); dalloc(x->c.alive, cap);
     dalloc(x->c.lkind, cap); dalloc(x->c.ledge, cap); dalloc(x->c.fb, cap);
     dalloc(x->c.red, cap); dalloc(x->c.unsafe, cap); dalloc(x->c.far, cap);
-    dalloc(x->c.bw, cap);
-    CK(cudaMemsetAsync(x->c.bw, 0, cap, x->st));
     x->ccap = cap;
     // per-candidate insertion buffers
     dfree(x->ib.nv); dfree(x->ib.nt); dfree(x->ib.ns); dfree(x->ib.ov); dfree(x->ib.ot);
@@ -604,59 +595,28 @@ void raise_dev_err(gdp2d_ctx* x) {
     }
 }
 
-void validate_now(gdp2d_ctx* x, const char* where) {
-    if (!x->validate) return;
-    launch_validate(x->work.m, x->d_val, x->st);
-    u32 h[4];
-    CK(cudaMemcpyAsync(h, x->d_val, sizeof h, cudaMemcpyDeviceToHost, x->st));
-    CK(cudaStreamSynchronize(x->st));
-    check_dev_err(x);
-    if (h[0]) {
-        char buf[200];
-        snprintf(buf, sizeof buf, "validate after %s (round %u): failure %u at triangle %u edge %d",
-                 where, x->round, h[0], h[1], (int)h[2]);
-        throw Fail{GDP2D_EMESH, buf};
-    }
-}
-
 }  // namespace
 
-// Lawson driver: the persistent cooperative kernel runs every round of the
-// fixpoint in one launch; GDP2D_VALIDATE=1 (or GDP2D_LAWSON=rounds) uses one
-// launch sequence per round so the structure can be checked in between.
+// Lawson driver (cdt.hpp:111-123): the persistent cooperative kernel runs
+// every round of the fixpoint in one launch; the host continues only when a
+// launch used up its round budget.
 static void lawson_from(gdp2d_ctx* x, u32 start_buf, u32 n, u32* rounds) {
     u32 cur = start_buf;
     u32 guard = 0;
-    if (!x->validate && !x->lawson_rounds) {
-        constexpr u32 kMax = 1024;
-        while (n > 0) {
-            if (n > x->wl.cap) throw Fail{GDP2D_ECAPACITY, "Lawson work list overflow"};
-            if (++guard > 1000) throw Fail{GDP2D_EMESH, "Lawson flip rounds did not converge"};
-            CK(cudaMemsetAsync(x->rcs, 0, sizeof(RoundCtr) * kMax, x->st));
-            launch_lawson_persistent(x->work.m, x->round + 1, cur, n, kMax, x->aux, x->wl, x->rcs,
-                                     x->d_res, x->d_ctr, x->lawson_grid, x->st);
-            CK(cudaGetLastError());
-            CK(cudaMemcpyAsync(x->h_tot, x->d_res, 3 * sizeof(u32), cudaMemcpyDeviceToHost, x->st));
-            CK(cudaStreamSynchronize(x->st));
-            x->round += x->h_tot[0];
-            if (rounds) *rounds += x->h_tot[0];
-            cur = x->h_tot[1];
-            n = x->h_tot[2];
-        }
-        return;
-    }
+    constexpr u32 kMax = 1024;
     while (n > 0) {
         if (n > x->wl.cap) throw Fail{GDP2D_ECAPACITY, "Lawson work list overflow"};
-        if (++guard > 200000) throw Fail{GDP2D_EMESH, "Lawson flip rounds did not converge"};
-        ++x->round;
-        zero_rc(x);
-        launch_flip_round(x->work.m, x->round, x->aux, x->wl, cur, n, x->d_ctr, x->st);
-        const RoundCtr rc = read_rc(x);
-        if (rc.wl_next > x->wl.cap) throw Fail{GDP2D_ECAPACITY, "Lawson work list overflow"};
-        n = rc.wl_next;
-        cur ^= 1u;
-        if (rounds) ++*rounds;
-        validate_now(x, "flip round");
+        if (++guard > 1000) throw Fail{GDP2D_EMESH, "Lawson flip rounds did not converge"};
+        CK(cudaMemsetAsync(x->rcs, 0, sizeof(RoundCtr) * kMax, x->st));
+        launch_lawson_persistent(x->work.m, x->round + 1, cur, n, kMax, x->aux, x->wl, x->rcs,
+                                 x->d_res, x->d_ctr, x->lawson_grid, x->st);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(x->h_tot, x->d_res, 3 * sizeof(u32), cudaMemcpyDeviceToHost, x->st));
+        CK(cudaStreamSynchronize(x->st));
+        x->round += x->h_tot[0];
+        if (rounds) *rounds += x->h_tot[0];
+        cur = x->h_tot[1];
+        n = x->h_tot[2];
     }
 }
 
@@ -689,10 +649,6 @@ void ctx_init(gdp2d_ctx* x, int device) {
     dalloc(x->d_val, 4);
     dalloc(x->wl.dbg, 4 + 2 * MAX_STAR);
     CK(cudaMemsetAsync(x->wl.dbg, 0, sizeof(double) * (4 + 2 * MAX_STAR), x->st));
-    const char* ev = std::getenv("GDP2D_VALIDATE");
-    x->validate = ev && ev[0] == '1';
-    const char* lr = std::getenv("GDP2D_LAWSON");
-    x->lawson_rounds = lr && std::string(lr) == "rounds";
     if (const char* e = std::getenv("GDP2D_SYNC_COLLECT")) x->sync_collect = e[0] == '1';
     if (const char* e = std::getenv("GDP2D_STANDALONE_C")) x->standalone_c = (u32)std::atoll(e);
     if (const char* e = std::getenv("GDP2D_REGIONS_TIGHT")) x->regions_tight = e[0] == '1';
@@ -702,7 +658,6 @@ void ctx_init(gdp2d_ctx* x, int device) {
     x->lawson_grid = lawson_persistent_grid(device);
     x->insert_grid = insert_persistent_grid(device);
     x->rollback_grid = rollback_persistent_grid(device);
-    x->lawson_grid2 = lawson_batch_grid(device);
     if (const char* e = std::getenv("GDP2D_GRID")) {   // experiments: fewer co-resident CTAs
         const int g = std::atoi(e);
         if (g > 0) {
@@ -712,9 +667,6 @@ void ctx_init(gdp2d_ctx* x, int device) {
     }
     CK(cudaMalloc(&x->sel_state, select_state_bytes()));
     x->little.resident = cavity_resident_candidates(device);
-    if (const char* e = std::getenv("GDP2D_LAWSON_KERNEL")) x->lawson_kernel = e[0] == '1';
-    const char* li = std::getenv("GDP2D_INSERT");
-    x->legacy_insert = (li && std::string(li) == "legacy") || x->validate || x->lawson_rounds;
     dalloc(x->ring, 5);   // 4-slot step ring + the removal-seed accumulator
     if (const char* e = std::getenv("GDP2D_TRACE"); e && (e[0] == '1' || e[0] == '2')) {
         x->tr.on = true;
@@ -726,8 +678,6 @@ void ctx_init(gdp2d_ctx* x, int device) {
     if (const char* e = std::getenv("GDP2D_SMALL_C")) x->small_c = (u32)std::strtoul(e, nullptr, 10);
     if (const char* e = std::getenv("GDP2D_DEP")) x->dep_mis = std::string(e) == "mis";
     if (const char* e = std::getenv("GDP2D_CHECK")) x->check = e[0] == '1';
-    if (const char* e = std::getenv("GDP2D_TAIL")) x->tail_kernel = e[0] == '1';
-    if (const char* e = std::getenv("GDP2D_EXTRAS")) x->extras = std::atoi(e);
     dalloc(x->scan_part, 3ull * x->insert_grid + 3);
     const char* fc = std::getenv("GDP2D_COLLECT");
     x->full_collect = fc && std::string(fc) == "full";
@@ -1043,59 +993,6 @@ double ev_ms(cudaEvent_t a, cudaEvent_t b) {
     return (double)ms;
 }
 
-// Insertion phase, host-driven (one launch sequence per flip / removal round,
-// a host round trip after each): kept for GDP2D_VALIDATE=1 (structure checked
-// after every round) and GDP2D_INSERT=legacy.
-void insert_legacy(gdp2d_ctx* x, const gdp2d_params* p, const Quality& q, u32 C, u32 batch,
-                   u32& nv, u32& nt, u32& ns, u32& flip_rounds, u32& rm_rounds) {
-    cudaStream_t st = x->st;
-    CK(cudaMemcpyAsync(x->h_tot, x->ib.totals, 3 * sizeof(u32), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    nv = x->h_tot[0];
-    nt = x->h_tot[1];
-    ns = x->h_tot[2];
-    const u32 V0 = x->work.m.nV;
-    ensure_mesh(x, x->work.m.nV + nv, x->work.m.nT + nt, x->work.m.nS + ns);
-    ensure_fresh(x, nv);
-    if (!nv) return;
-    DevMesh& mm = x->work.m;
-    ++x->round;
-    zero_rc(x);
-    launch_apply_splits(mm, x->c, C, batch, x->round, x->ib, x->aux, x->fresh, x->wl, x->d_ctr,
-                        st);
-    mm.nV += nv;
-    mm.nT += nt;
-    mm.nS += ns;
-    launch_fixup(mm, x->round, x->aux, x->wl, 4 * nv, true, 0, x->d_ctr, st);
-    RoundCtr rc = read_rc(x);
-    validate_now(x, "splits");
-    lawson_from(x, 0, rc.wl_next, &flip_rounds);
-    // Phase 3: redundant-point removal to fixpoint (refine.hpp:551-608).
-    for (;;) {
-        zero_rc(x);
-        launch_detect(mm, q, p->split_depth_cap, V0, nv, x->fresh, x->wl, x->d_ctr, st);
-        rc = read_rc(x);
-        u32 nrm = std::min(rc.detect, x->wl.rm_cap);
-        if (nrm == 0) break;
-        u32 cur = 0;
-        u32 guard = 0;
-        while (nrm > 0) {
-            if (++guard > 100000) throw Fail{GDP2D_EMESH, "vertex removal did not converge"};
-            ++x->round;
-            zero_rc(x);
-            launch_removal_round(mm, x->round, V0, x->aux, x->fresh, x->wl, cur, nrm, 0,
-                                 x->d_ctr, st);
-            rc = read_rc(x);
-            ++rm_rounds;
-            check_dev_err(x);
-            validate_now(x, "removal round");
-            lawson_from(x, 0, rc.wl_next, &flip_rounds);
-            nrm = rc.rm_next;
-            cur ^= 1u;
-        }
-    }
-}
-
 // GDP2D_CHECK=1: device structural validation of the working mesh grown by
 // this batch's reserved ids (totals read back first).
 void check_structure_now(gdp2d_ctx* x, u32 nV, u32 nT, u32 nS, const char* where) {
@@ -1144,10 +1041,6 @@ bool insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, int prefiltered, u32
         return e ? std::max(1, std::atoi(e)) : 1;
     }();
     const int g_rb = std::max(1, x->rollback_grid / (div * rb_div));
-    // a batch predicted to be small runs as one single-CTA launch
-    // (k_batch_tail); prediction from the previous batch's count
-    bool tail = x->tail_kernel && !x->check && !x->lawson_kernel && !prefiltered &&
-                c_est <= x->small_c;
     bool started = false;   // an earlier attempt got past the filter and plan
     int grow = 0;
     for (int attempt = 0;; ++attempt) {
@@ -1180,8 +1073,7 @@ bool insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, int prefiltered, u32
         L.rs = rs;
         L.isolate = isolate;
         L.dep_mis = x->dep_mis ? 1 : 0;
-        L.extras = x->extras;
-        L.lawson_kernel = x->lawson_kernel ? 1 : 0;
+        L.extras = 2;   // refinement claims: the rewrite table (launch_cavity)
         L.regions = x->regions;
         L.region_len = x->region_len;
         L.scan_part = x->scan_part;
@@ -1207,15 +1099,12 @@ bool insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, int prefiltered, u32
             k_start = x->ev_k[0];
         }
         const int mode = p->mode == GDP2D_CHEW ? 1 : 0;
-        const int k1 = x->lawson_kernel ? (1 | 4) : 1;
-        if (tail) {
-            launch_insert_tail(L, mode, st);
-        } else if (!x->check) {
+        if (!x->check) {
             // (the split/rollback boundary comes from the kernels' start stamps)
-            launch_insert_persistent(L, mode, g_ins, g_rb, st, nullptr, k1 | 2, x->lawson_grid2);
+            launch_insert_persistent(L, mode, g_ins, g_rb, st, nullptr, 1 | 2);
         } else {
             // GDP2D_CHECK=1: structural validation after each kernel
-            launch_insert_persistent(L, mode, g_ins, g_rb, st, x->ev_k[1], k1, x->lawson_grid2);
+            launch_insert_persistent(L, mode, g_ins, g_rb, st, x->ev_k[1], 1);
             check_structure_now(x, x->work.m.nV, x->work.m.nT, x->work.m.nS, "split kernel");
             launch_insert_persistent(L, mode, g_ins, g_rb, st, nullptr, 2);
             check_structure_now(x, x->work.m.nV, x->work.m.nT, x->work.m.nS, "rollback kernel");
@@ -1229,10 +1118,6 @@ bool insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, int prefiltered, u32
         CK(cudaStreamSynchronize(st));
         const u32 C = x->h_tot[3];
         if (x->h_state[0] == 3u) return false;   // INS_REGIONS
-        if (x->h_state[0] == 4u) {   // INS_NOT_TAIL: nothing done, redo on the grid kernels
-            tail = false;
-            continue;
-        }
         nv = x->h_tot[0];
         nt = x->h_tot[1];
         ns = x->h_tot[2];
@@ -1254,29 +1139,24 @@ bool insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, int prefiltered, u32
             const u64 b_split = 32ull * C + 128ull * ins + 128ull * f_split;
             const u64 b_rb = 64ull * nv + 128ull * f_rb + 128ull * h.rm_done;
             x->k_launches += 1;
-            if (tail) {   // one kernel did both: counted as a split-kernel launch
-                x->k_split_s += ev_ms(k_start, x->ev_k[2]) * 1e-3;
-                x->k_split_b += b_split + b_rb;
+            // the pair's span by events, split at the rollback kernel's
+            // start (globaltimer stamps in state words 10-13; GDP2D_CHECK
+            // records an event between the launches instead)
+            const double pair = ev_ms(k_start, x->ev_k[2]) * 1e-3;
+            double s_split;
+            if (x->check) {
+                s_split = ev_ms(k_start, x->ev_k[1]) * 1e-3;
             } else {
-                // the pair's span by events, split at the rollback kernel's
-                // start (globaltimer stamps in state words 10-13; GDP2D_CHECK
-                // records an event between the launches instead)
-                const double pair = ev_ms(k_start, x->ev_k[2]) * 1e-3;
-                double s_split;
-                if (x->check) {
-                    s_split = ev_ms(k_start, x->ev_k[1]) * 1e-3;
-                } else {
-                    u64 t0, t1;
-                    std::memcpy(&t0, x->h_state + 10, sizeof t0);
-                    std::memcpy(&t1, x->h_state + 12, sizeof t1);
-                    s_split = t1 > t0 ? std::min(pair, double(t1 - t0) * 1e-9) : 0.0;
-                }
-                x->k_split_s += s_split;
-                x->k_split_b += b_split;
-                x->k_rb_s += pair - s_split;
-                x->k_rb_b += b_rb;
-                x->k_rb_launches += 1;
+                u64 t0, t1;
+                std::memcpy(&t0, x->h_state + 10, sizeof t0);
+                std::memcpy(&t1, x->h_state + 12, sizeof t1);
+                s_split = t1 > t0 ? std::min(pair, double(t1 - t0) * 1e-9) : 0.0;
             }
+            x->k_split_s += s_split;
+            x->k_split_b += b_split;
+            x->k_rb_s += pair - s_split;
+            x->k_rb_b += b_rb;
+            x->k_rb_launches += 1;
         }
         x->round += x->h_state[1] + 1;
         flip_rounds = x->h_state[2];
@@ -1349,7 +1229,7 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
         // within half of it (batches shrink over a refinement)
         const u64 little_lv = p->little_batch_sizing ? x->little.level() : 0;
         const bool little_sync = little_lv && (u64)x->c_prev * 2 > little_lv;
-        const bool ncs = !x->sync_collect && !x->legacy_insert && x->have_c_prev &&
+        const bool ncs = !x->sync_collect && x->have_c_prev &&
                          p->rule4_unified_collection != 0 && p->batch_size_cap == 0 &&
                          !little_sync;
         u32 C = launch_collect(m, q, p->rule4_unified_collection != 0, x->flags, x->c, x->ccap,
@@ -1386,7 +1266,7 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
         CK(cudaEventRecord(x->ev[1], st));
         bool filtered_events = false;   // ev[3..5] recorded (standalone filters)
         // isolated insertion needs the cavity filter (rule 2)
-        const int isolate = (ncav == 0 || x->legacy_insert) ? 0
+        const int isolate = ncav == 0 ? 0
                             : p->insert_mode == GDP2D_INSERT_ISOLATED   ? 1
                             : p->insert_mode == GDP2D_INSERT_PRECEDENCE ? 2
                                                                         : 0;
@@ -1398,25 +1278,7 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
         const u32 batch = ++x->epoch;
         u32 flip_rounds = 0, rm_rounds = 0;
         u32 nv = 0, nt = 0, ns = 0;
-        if (x->legacy_insert) {
-            launch_locate(m, x->c, C, x->d_ctr, st);
-            x->tr.mark("locate", st);
-            CK(cudaEventRecord(x->ev[3], st));
-            launch_claim(m, x->c, C, x->aux, x->d_ctr, st);
-            x->tr.mark("claim", st);
-            CK(cudaEventRecord(x->ev[4], st));
-            launch_cavity(m, x->c, C, ncav, 1, x->aux, x->regions, x->region_len, nullptr,
-                          x->d_ctr, st);
-            x->tr.mark("cavity", st);
-            CK(cudaEventRecord(x->ev[5], st));
-            filtered_events = true;
-            launch_plan_ops(m, x->c, C, p->split_depth_cap, x->ib, x->d_ctr, st);
-            scan_exclusive(x->ib.nv, x->ib.ov, C, x->ib.totals + 0, x->scan, st);
-            scan_exclusive(x->ib.nt, x->ib.ot, C, x->ib.totals + 1, x->scan, st);
-            scan_exclusive(x->ib.ns, x->ib.os, C, x->ib.totals + 2, x->scan, st);
-            x->tr.mark("plan+scans", st);
-            insert_legacy(x, p, q, C, batch, nv, nt, ns, flip_rounds, rm_rounds);
-        } else {
+        {
             // Lines 5-7 as high-occupancy standalone kernels for big batches
             // (they skip C <= small_c: the batch kernel filters in one CTA)
             NArg na = NArg::host(C);
@@ -1439,7 +1301,7 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
                                            p->split_depth_cap, isolate == 1, x->aux, x->regions,
                                            x->region_len, x->ins_state + 8, x->d_ctr, st);
                 else
-                    launch_cavity(m, x->c, na, ncav, x->extras, x->aux, x->regions,
+                    launch_cavity(m, x->c, na, ncav, 2, x->aux, x->regions,
                                   x->region_len, nullptr, x->d_ctr, st);
                 CK(cudaEventRecord(x->ev[5], st));
                 filtered_events = true;
@@ -1473,13 +1335,8 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
             --x->epoch;
             break;
         }
-        // end of the insertion phase: the rollback kernel's end event (the
-        // legacy path records its own)
-        cudaEvent_t ins_end = x->ev_k[2];
-        if (x->legacy_insert) {
-            CK(cudaEventRecord(x->ev[6], st));
-            ins_end = x->ev[6];
-        }
+        // end of the insertion phase: the rollback kernel's end event
+        const cudaEvent_t ins_end = x->ev_k[2];
         x->tr.mark("sync", st);
         x->tr.flush(bm.batch_index, st);
         if (x->tr.on)
@@ -1489,10 +1346,7 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
                     x->h_ctr->ins_mid, x->h_ctr->ins_cc, x->h_ctr->rm_red, x->h_ctr->rm_dep,
                     x->h_ctr->marked, (unsigned long long)x->h_ctr->flips, x->h_ctr->rm_done);
         CK(cudaGetLastError());
-        if (x->legacy_insert)
-            check_dev_err(x);
-        else
-            raise_dev_err(x);   // counters came back with the insertion's status
+        raise_dev_err(x);   // counters came back with the insertion's status
         const Counters& h = *x->h_ctr;
         r->scan_bytes += scan_alg_bytes(scan_nT, scan_nS, h.scan_dirty, C, ncs);
         const u32 inserted = h.ins_mid + h.ins_cc;
@@ -2030,7 +1884,7 @@ void gdp2d_params_init(gdp2d_params* p, double theta_deg, double ell, uint32_t m
     p->rule1_compaction_threshold = 1024;
     p->rule2_filtering_enabled = 1;
     p->rule4_unified_collection = 1;
-    p->little_batch_sizing = 0;
+    p->little_batch_sizing = 1;   // measured-C/L sizing (LittleSizer), on by default
     p->insert_mode = GDP2D_INSERT_ROLLBACK;
     p->reserved0 = 0;
     p->iteration_cap = 10000;

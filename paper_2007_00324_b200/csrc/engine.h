@@ -98,10 +98,9 @@ inline void launch_claim(const DevMesh& m, DevCands c, u32 n, TriAux a, Counters
                          cudaStream_t st) {
     launch_claim(m, c, NArg::host(n), a, d_ctr, st);
 }
-// Cavity filter; extras = refine-mode extra claims (far side of a split edge).
-// extras: 0 parity (reference claims only), 1 refine with the far side of a
-// split edge added to the main claims, 2 refine with the rewrite table
-// (gdp2d_phases.cuh).
+// Cavity filter (refine.hpp:382-429).  extras: 0 parity (the reference's
+// claims only), 2 refinement: the rewrite table also guards each split
+// (rw_*_one, gdp2d_phases.cuh).
 void launch_cavity(const DevMesh& m, DevCands c, NArg n, u32 ncav, int extras, TriAux a,
                    u32* regions, u32* region_len, u32* bfs_len, Counters* d_ctr,
                    cudaStream_t st);
@@ -167,21 +166,6 @@ struct WorkLists {
     u32 fresh_v0 = 0, fresh_n = 0;
 };
 
-void launch_plan_ops(const DevMesh& m, DevCands c, u32 n, u64 depth_cap, InsertBufs b,
-                     Counters* d_ctr, cudaStream_t st);
-void launch_apply_splits(const DevMesh& m, DevCands c, u32 n, u32 batch, u32 round,
-                         InsertBufs b, TriAux a, FreshInfo f, WorkLists w, Counters* d_ctr,
-                         cudaStream_t st);
-// Phase B of every local rewrite: resolve pending outer references through
-// the edge maps, write back-pointers, refresh vert_tri / seg_tri.  Touched
-// triangles come from w.touched (count in w.rc->touched, bound n_bound).
-// seed_all_edges pushes every edge of every touched triangle onto w.w[widx].
-void launch_fixup(const DevMesh& m, u32 round, TriAux a, WorkLists w, u32 n_bound,
-                  bool seed_all_edges, u32 widx, Counters* d_ctr, cudaStream_t st);
-// One Lawson round over w.w[cur] (n items); next list in w.w[cur^1].  The
-// caller zeroes w.rc before the round.
-void launch_flip_round(const DevMesh& m, u32 round, TriAux a, WorkLists w, u32 cur, u32 n,
-                       Counters* d_ctr, cudaStream_t st);
 // The whole Lawson fixpoint as one persistent cooperative kernel (see
 // k_insert.cu).  result[0..2] = rounds run, list buffer holding the remaining
 // work, remaining work count.
@@ -223,7 +207,6 @@ struct InsertLaunch {
     int isolate = 1;            // claims: 0 reference cavity, 1 isolated (ring), 2 precedence
     int dep_mis = 0;            // dependent pairs by the priority-MIS rule
     int extras = 2;             // cavity extras mode (see launch_cavity)
-    int lawson_kernel = 1;      // separate Lawson launch after the splits
     unsigned long long* trace = nullptr;   // device step trace (GDP2D_TRACE=1)
     u32* trace_val = nullptr;
     u32* trace_n = nullptr;
@@ -233,24 +216,9 @@ int insert_persistent_grid(int device);
 int rollback_persistent_grid(int device);
 // Kernel 1 (plan + splits + Lawson, with Lines 5-7 unless L.prefiltered) then
 // kernel 2 (detect + rollback loop), both cooperative, no host sync between.
-// which: bit 0 = kernel 1 (splits [+ Lawson]), bit 2 = the separate Lawson
-// kernel, bit 1 = kernel 2 (rollback), launched in that order.
-int lawson_batch_grid(int device);
-// The whole batch (C <= small_c) in one CTA, one ordinary launch; state[0] =
-// INS_NOT_TAIL (4) when the batch is larger (nothing done).
-void launch_insert_tail(const InsertLaunch& L, int mode, cudaStream_t st);
+// which: bit 0 = kernel 1, bit 1 = kernel 2, launched in that order.
 void launch_insert_persistent(const InsertLaunch& L, int mode, int grid, int grid2,
-                              cudaStream_t st, cudaEvent_t between = nullptr, int which = 3,
-                              int grid3 = 0);
-
-// Redundancy detection (refine.hpp:551-608): fills w.rm[0], count in w.rc->detect.
-void launch_detect(const DevMesh& m, const Quality& q, u64 depth_cap, u32 V0, u32 F,
-                   FreshInfo f, WorkLists w, Counters* d_ctr, cudaStream_t st);
-// One parallel vertex-removal round over w.rm[cur] (n); deferred ones go to
-// w.rm[cur^1]; Lawson seeds to w.w[widx].
-void launch_removal_round(const DevMesh& m, u32 round, u32 V0, TriAux a, FreshInfo f,
-                          WorkLists w, u32 cur, u32 n, u32 widx, Counters* d_ctr,
-                          cudaStream_t st);
+                              cudaStream_t st, cudaEvent_t between = nullptr, int which = 3);
 
 // Quality summary (refine.hpp:614-645).
 struct QualitySummary {

@@ -82,7 +82,6 @@ struct DevCands {
     u32* red;       // isolated insertion: lowest splittable subsegment the point would encroach
     uint8_t* unsafe;// isolated insertion: cavity hit the cap (not provably isolated)
     u32* far;       // far side of this candidate's split edge (rewrite table), or NONE
-    uint8_t* bw;    // survivor inserts by Bowyer-Watson (cavity rewrite) instead of a split
 };
 
 // Per-batch device counters (zeroed at the start of each batch).

@@ -123,9 +123,8 @@ __device__ __forceinline__ void claim_reset_one(const DevCands& c, u32 i, u32 nT
 // with emissions appended in (source, slot) order visits triangles in exactly
 // the window order of expand() (expandlist.hpp:98-152), so the region -- and
 // hence the claim set -- is the reference's, including when the cap binds.
-// extras == 1: the triangle across a split edge is added to the claims
-// (SURVEY §7 hard part (i)).  extras == 2 leaves the region exactly the
-// reference's and the rewrite table (rw_*_one) guards the split instead.
+// The region is exactly the reference's in both uses (extras 0: the parity
+// hooks; 2: refinement, where the rewrite table rw_*_one guards the split).
 // Returns the BFS region size (cavity visits).
 __device__ __forceinline__ u32 cavity_bfs_one(const DevMesh& m, const DevCands& c, u32 i,
                                               u32 ncav, int extras, u32 rs, u32* regions,
@@ -170,28 +169,6 @@ __device__ __forceinline__ u32 cavity_bfs_one(const DevMesh& m, const DevCands& 
         }
         for (u32 k = 0; k < len; ++k) reg[k] = lreg[k];
         blen = len;
-        if (extras == 1) {
-            u32 far = NONE;
-            if (c.kind[i] == 0) {
-                const u32 s = c.id[i];
-                const int e = seg_slot(m.ts[located], s);
-                if (e >= 0) {
-                    const u32 cc = comp(m.tn[located], e);
-                    if (cc != NONE) far = etri(cc);
-                }
-            } else if (c.lkind[i] == 1) {
-                const u32 cc = comp(m.tn[located], c.ledge[i]);
-                if (cc != NONE) far = etri(cc);
-            }
-            if (far != NONE) {
-                bool in = false;
-                for (u32 k = 0; k < len; ++k) in |= reg[k] == far;
-                if (!in) {
-                    reg[len++] = far;
-                    atomicMax((ull*)&ckey[far], (ull)key);
-                }
-            }
-        }
     }
     region_len[i] = len;
     if (bfs_len) bfs_len[i] = blen;
@@ -477,27 +454,6 @@ __device__ __forceinline__ void rw_reset_one(const DevCands& c, u32 i, u32 nT, u
         fkey[far] = 0;
         ftie[far] = ~0ull;
     }
-}
-
-// Bowyer-Watson eligibility of a surviving candidate (extras == 3): a
-// circumcenter strictly inside its located triangle whose cavity was not
-// capped and holds no triangle that another candidate's split rewrites (a
-// midpoint's far side, claimed in the rewrite table only).  Such a survivor
-// owns its whole cavity, so it can rewrite it as the star of p.
-static __device__ __noinline__ uint8_t bw_eligible(const DevCands& c, u32 i, u32 ncav, u32 rs,
-                                               const u32* regions, const u32* region_len,
-                                               const u64* fkey, const u64* ftie) {
-    if (!c.alive[i] || c.kind[i] != 1 || c.lkind[i] != 0) return 0;
-    const u32 len = region_len[i];
-    if (len == 0 || len > ncav) return 0;
-    const u64 key = c.key[i], tie = tie_of(c, i);
-    const u32* reg = regions + (size_t)i * rs;
-    for (u32 k = 0; k < len; ++k) {
-        const u32 t = reg[k];
-        const u64 fk = fkey[t];
-        if (fk != 0 && !(fk == key && ftie[t] == tie)) return 0;
-    }
-    return 1;
 }
 
 // Needs of one surviving candidate (refine.hpp:493-539): subsegments that hit

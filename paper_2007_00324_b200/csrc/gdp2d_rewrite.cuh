@@ -145,95 +145,6 @@ static __device__ void split_edge_A(const DevMesh& m, const TriAux& x, const Wor
     }
 }
 
-// Bowyer-Watson insertion of circumcenter wv at p into its cavity reg[0..k)
-// (the filter's BFS region, owned exclusively): the cavity's boundary cycle
-// becomes the star of wv -- k old slots + the two new ones t_new0, t_new0+1,
-// the same +2 triangles as a 1->3 split.  The result is the CDT a split +
-// Lawson would reach (the insertion's conflict region, bounded by
-// constraints), so the Lawson pass only has to look at the boundary edges
-// (seeds), where the cavities of concurrent insertions touch.  Boundary
-// edges keep their outer references pending (phase B) and their old slot
-// maps through emap.  Returns false -- nothing written -- unless the cavity is
-// a disk (k + 2 boundary edges in one simple cycle, no subsegment inside)
-// that p sees edge by edge; the caller then splits the located triangle.
-static __device__ __noinline__ bool bw_insert(const DevMesh& m, const TriAux& x, const WorkLists& w,
-                                       const u32* reg, u32 k, u32 wv, double2 p, u32 t_new0,
-                                       u32 round, RoundCtr* rc, int seed, Counters* ctr) {
-    constexpr int MB = MAX_CAVITY_N + 3;
-    if (k == 0 || k + 2 > (u32)MB) return false;
-    u32 bs[MB], be[MB], bo[MB], bg[MB], borg[MB], ord[MB];
-    u32 B = 0;
-    for (u32 j = 0; j < k; ++j) {
-        const u32 T = reg[j];
-        const uint4 tv = m.tv[T], tn = m.tn[T], ts = m.ts[T];
-#pragma unroll
-        for (int e = 0; e < 3; ++e) {
-            const u32 r = comp(tn, e);
-            bool inside = false;
-            if (r != NONE) {
-                const u32 X = etri(r);
-                for (u32 q = 0; q < k; ++q) inside |= reg[q] == X;
-            }
-            if (inside) {
-                if (comp(ts, e) != NONE) return false;   // a constraint inside the cavity
-                continue;
-            }
-            if (B >= k + 2) return false;
-            bs[B] = comp(tv, nxt(e));
-            be[B] = comp(tv, prv(e));
-            bo[B] = r;
-            bg[B] = comp(ts, e);
-            borg[B] = enc(T, e);
-            ++B;
-        }
-    }
-    if (B != k + 2) return false;
-    // the boundary as one simple cycle: successor = the edge starting where
-    // this one ends (a vertex met twice would have two candidates)
-    ord[0] = 0;
-    for (u32 i = 1; i < B; ++i) {
-        const u32 want = be[ord[i - 1]];
-        u32 nx = NONE;
-        for (u32 q = 0; q < B; ++q) {
-            if (bs[q] != want) continue;
-            if (nx != NONE) return false;
-            nx = q;
-        }
-        if (nx == NONE || nx == 0) return false;
-        ord[i] = nx;
-    }
-    if (be[ord[B - 1]] != bs[0]) return false;
-    for (u32 i = 0; i < B; ++i)
-        if (orient2d(m.xy[bs[ord[i]]], m.xy[be[ord[i]]], p) <= 0) return false;
-    for (u32 j = 0; j < k; ++j) x.stamp[reg[j]] = round;
-    const auto slot = [&](u32 i) { return i < k ? reg[i] : t_new0 + (i - k); };
-    for (u32 i = 0; i < B; ++i) {
-        const u32 o = ord[i];
-        const u32 sl = slot(i);
-        const u32 sn = slot(i + 1 == B ? 0 : i + 1), sp = slot(i == 0 ? B - 1 : i - 1);
-        // (a, b, wv): edge 0 = (b, wv) -> next star triangle's edge 1,
-        // edge 1 = (wv, a) -> previous one's edge 0, edge 2 = the boundary edge
-        write_tri(m, sl, bs[o], be[o], wv, enc(sn, 1), enc(sp, 0), bo[o],
-                  bo[o] != NONE ? 4u : 0u, NONE, NONE, bg[o]);
-        x.emap[3 * etri(borg[o]) + eidx(borg[o])] = enc(sl, 2);
-    }
-    m.vtri[wv] = NONE;
-    {
-        const u32 o = agg_reserve(&rc->touched, B);
-        for (u32 i = 0; i < B; ++i)
-            if (o + i < w.cap) w.touched[o + i] = slot(i);
-    }
-    if (seed) {
-        const u32 o = agg_reserve(&rc->wl_next, B);
-        if (o + B > w.cap) {
-            raise_err(ctr, DERR_WORKLIST_OVERFLOW, o);
-        } else {
-            for (u32 i = 0; i < B; ++i) w.w[0][o + i] = enc(slot(i), 2);
-        }
-    }
-    return true;
-}
-
 // ---- phase B ------------------------------------------------------------------------
 
 __device__ __forceinline__ void fixup_one(const DevMesh& m, u32 round, const TriAux& x,

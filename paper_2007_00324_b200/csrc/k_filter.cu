@@ -82,7 +82,7 @@ __global__ void k_cavity_tie(DevCands c, NArg na, u32 rs, const u32* __restrict_
 __global__ void k_cavity_check(DevCands c, NArg na, u32 rs, const u32* __restrict__ regions,
                                const u32* __restrict__ region_len, const u64* __restrict__ ckey,
                                const u64* __restrict__ ctie, const u64* __restrict__ fkey,
-                               const u64* __restrict__ ftie, u32 bw_ncav, Counters* ctr) {
+                               const u64* __restrict__ ftie, Counters* ctr) {
     const u32 n = narg(na);
     u32 surv = 0;
     GRID_STRIDE(i, n) {
@@ -92,8 +92,6 @@ __global__ void k_cavity_check(DevCands c, NArg na, u32 rs, const u32* __restric
             c.alive[i] = 0;
             sv = 0;
         }
-        if (bw_ncav)
-            c.bw[i] = sv ? bw_eligible(c, i, bw_ncav, rs, regions, region_len, fkey, ftie) : 0;
         surv += sv;
     }
     block_add<u32>(&ctr->surv_cavity, surv);
@@ -170,7 +168,7 @@ void launch_cavity(const DevMesh& m, DevCands c, NArg n, u32 ncav, int extras, T
                    cudaStream_t st) {
     if (!n.grid_n) return;
     const u32 rs = ncav + 1 + MAX_CLAIM_EXTRA;
-    const bool rw = extras >= 2;   // 3: + Bowyer-Watson eligibility
+    const bool rw = extras >= 2;   // refinement: the rewrite table
     note_launch(), k_cavity_bfs<<<(n.grid_n + 127) / 128, 128, 0, st>>>(m, c, n, ncav, extras, rs, regions,
                                                    region_len, bfs_len, a.ckey, d_ctr);
     const u32 g = (n.grid_n + 255) / 256;
@@ -179,7 +177,7 @@ void launch_cavity(const DevMesh& m, DevCands c, NArg n, u32 ncav, int extras, T
     if (rw) note_launch(), k_rw_tie<<<g, 256, 0, st>>>(c, n, a.fkey, a.ftie);
     note_launch(), k_cavity_check<<<g, 256, 0, st>>>(c, n, rs, regions, region_len, a.ckey, a.ctie,
                                                      rw ? a.fkey : nullptr, rw ? a.ftie : nullptr,
-                                                     extras >= 3 ? ncav : 0u, d_ctr);
+                                                     d_ctr);
     note_launch(), k_cavity_reset<<<g, 256, 0, st>>>(c, n, m.nT, rs, regions, region_len, a.ckey,
                                                      a.ctie, rw ? a.fkey : nullptr,
                                                      rw ? a.ftie : nullptr);

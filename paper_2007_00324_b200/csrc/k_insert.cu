@@ -31,47 +31,17 @@ namespace cg = cooperative_groups;
 #ifndef GDP2D_SPLIT_MINB
 #define GDP2D_SPLIT_MINB 2
 #endif
-#ifndef GDP2D_LAWSON_MINB
-#define GDP2D_LAWSON_MINB 4
-#endif
 
 namespace gdp2d {
 
 // ---- planning + phase-1 splits ----------------------------------------------------
 
-// Needs of each surviving candidate (plan_one, gdp2d_phases.cuh).
-__global__ void k_plan_ops(DevMesh m, DevCands c, u32 n, u64 depth_cap, InsertBufs b,
-                           Counters* ctr) {
-    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
-    u32 dropped = 0;
-    if (i < n) {
-        u32 nv, nt, ns;
-        dropped = plan_one(m, c, i, depth_cap, nv, nt, ns);
-        b.nv[i] = nv;
-        b.nt[i] = nt;
-        b.ns[i] = ns;
-    }
-    warp_add_u32(&ctr->dropped, dropped);
-}
-
 // One surviving candidate's phase-1 insertion (refine.hpp:492-539).
 // Returns 1 = midpoint, 2 = circumcenter, 0 = nothing.
-// GDP2D_BW=1 builds the Bowyer-Watson insertion option (GDP2D_EXTRAS=3/4);
-// apply_one is then kept out of line (inlined, the extra path makes the
-// 128-register split kernel spill).
-#ifndef GDP2D_BW
-#define GDP2D_BW 0
-#endif
-#if GDP2D_BW
-#define APPLY_INLINE __noinline__
-#else
-#define APPLY_INLINE __forceinline__
-#endif
-__device__ APPLY_INLINE int apply_one(const DevMesh& m, const DevCands& c, u32 i, u32 batch,
+__device__ __forceinline__ int apply_one(const DevMesh& m, const DevCands& c, u32 i, u32 batch,
                                          u32 round, const InsertBufs& b, const TriAux& x,
                                          const FreshInfo& f, const WorkLists& w, RoundCtr* rc,
-                                         int seed, Counters* ctr, const u32* regions = nullptr,
-                                         const u32* region_len = nullptr, u32 rs = 0) {
+                                         int seed, Counters* ctr) {
     if (!b.nv[i]) return 0;
     const u32 wv = m.nV + b.ov[i];
     const u32 nt0 = m.nT + b.ot[i];
@@ -113,95 +83,11 @@ __device__ APPLY_INLINE int apply_one(const DevMesh& m, const DevCands& c, u32 i
         return 1;
     }
     if (c.lkind[i] == 0) {
-#if GDP2D_BW
-        if (regions && c.bw[i] &&
-            bw_insert(m, x, w, regions + (size_t)i * rs, region_len[i], wv, p, nt0, round, rc, seed,
-                      ctr))
-            return 2;
-#else
-        (void)regions;
-        (void)region_len;
-        (void)rs;
-#endif
         split_triangle_A(m, x, w, t, wv, nt0, nt0 + 1, round, rc, seed, ctr);
     } else {
         split_edge_A(m, x, w, t, c.ledge[i], wv, nt0, nt0 + 1, NONE, NONE, round, rc, seed, ctr);
     }
     return 2;
-}
-
-__global__ void k_apply_splits(DevMesh m, DevCands c, u32 n, u32 batch, u32 round, InsertBufs b,
-                               TriAux x, FreshInfo f, WorkLists w, Counters* ctr) {
-    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
-    u32 mid = 0, cc = 0;
-    if (i < n) {
-        const int r = apply_one(m, c, i, batch, round, b, x, f, w, w.rc, 0, ctr);
-        mid = r == 1;
-        cc = r == 2;
-    }
-    warp_add_u32(&ctr->ins_mid, mid);
-    warp_add_u32(&ctr->ins_cc, cc);
-}
-
-void launch_plan_ops(const DevMesh& m, DevCands c, u32 n, u64 depth_cap, InsertBufs b,
-                     Counters* d_ctr, cudaStream_t st) {
-    if (!n) return;
-    note_launch(), k_plan_ops<<<(n + 255) / 256, 256, 0, st>>>(m, c, n, depth_cap, b, d_ctr);
-}
-
-void launch_apply_splits(const DevMesh& m, DevCands c, u32 n, u32 batch, u32 round,
-                         InsertBufs b, TriAux a, FreshInfo f, WorkLists w, Counters* d_ctr,
-                         cudaStream_t st) {
-    if (!n) return;
-    note_launch(), k_apply_splits<<<(n + 255) / 256, 256, 0, st>>>(m, c, n, batch, round, b, a, f, w, d_ctr);
-}
-
-__global__ void k_fixup(DevMesh m, u32 round, TriAux x, WorkLists w, u32 n_bound, int seed,
-                        u32 widx, Counters* ctr) {
-    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
-    const u32 n = min(w.rc->touched, w.cap);
-    if (i >= n || i >= n_bound) return;
-    fixup_one(m, round, x, w, w.touched[i], seed, widx, w.rc, ctr);
-}
-
-void launch_fixup(const DevMesh& m, u32 round, TriAux a, WorkLists w, u32 n_bound,
-                  bool seed_all_edges, u32 widx, Counters* d_ctr, cudaStream_t st) {
-    if (!n_bound) return;
-    note_launch(), k_fixup<<<(n_bound + 255) / 256, 256, 0, st>>>(m, round, a, w, n_bound,
-                                                   seed_all_edges ? 1 : 0, widx, d_ctr);
-}
-
-__global__ void k_flip_test(DevMesh m, const u32* __restrict__ wl, u32 n, TriAux x, WorkLists w,
-                            Counters* ctr) {
-    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) flip_test_one(m, wl[i], x, w, w.rc, ctr);
-}
-
-__global__ void k_flip_apply(DevMesh m, u32 n_bound, u32 round, u32 widx, TriAux x,
-                             WorkLists w, Counters* ctr) {
-    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
-    const u32 n = min(w.rc->cand, w.cap);
-    u32 flipped = 0;
-    if (i < n && i < n_bound) flipped = flip_apply_one(m, i, round, widx, x, w, w.rc, ctr);
-    warp_add_ull(&ctr->flips, flipped);
-}
-
-__global__ void k_flip_post(u32 n_bound, u32 round, u32 widx, TriAux x, WorkLists w,
-                            Counters* ctr) {
-    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
-    const u32 n = min(w.rc->cand, w.cap);
-    if (i < n && i < n_bound) flip_post_one(i, round, widx, x, w, w.rc, ctr);
-}
-
-void launch_flip_round(const DevMesh& m, u32 round, TriAux a, WorkLists w, u32 cur, u32 n,
-                       Counters* d_ctr, cudaStream_t st) {
-    if (!n) return;
-    const u32 g = (n + 255) / 256;
-    note_launch(), k_flip_test<<<g, 256, 0, st>>>(m, w.w[cur], n, a, w, d_ctr);
-    note_launch(), k_flip_apply<<<g, 256, 0, st>>>(m, n, round, cur ^ 1u, a, w, d_ctr);
-    note_launch(), k_flip_post<<<g, 256, 0, st>>>(n, round, cur ^ 1u, a, w, d_ctr);
-    const u32 nt = 2 * n;
-    note_launch(), k_fixup<<<(nt + 255) / 256, 256, 0, st>>>(m, round, a, w, nt, 0, 0, d_ctr);
 }
 
 // Whole Lawson fixpoint in ONE persistent cooperative launch: each round is
@@ -375,14 +261,6 @@ __device__ __noinline__ u32 detect_a_one(const DevMesh& m, u64 depth_cap, u32 V0
     return marked;
 }
 
-template <int MODE>
-__global__ void k_detect_a(DevMesh m, u64 depth_cap, u32 V0, u32 F, FreshInfo f, Counters* ctr) {
-    const u32 j = blockIdx.x * blockDim.x + threadIdx.x;
-    u32 marked = 0;
-    if (j < F) marked = detect_a_one<MODE>(m, depth_cap, V0, F, j, f, ctr, 0);
-    warp_add_u32(&ctr->marked, marked);
-}
-
 // (b) Delaunay-dependent pairs: a same-batch circumcenter adjacent to a
 // higher-priority one (not itself redundant) is removed.
 __device__ __noinline__ void detect_b_one(const DevMesh& m, u32 V0, u32 F, u32 j,
@@ -477,11 +355,6 @@ __device__ __forceinline__ bool mis_round_one(u32 j, const FreshInfo& f) {
     return true;
 }
 
-__global__ void k_detect_b(DevMesh m, u32 V0, u32 F, FreshInfo f, Counters* ctr) {
-    const u32 j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j < F) detect_b_one(m, V0, F, j, f);
-}
-
 // Removal list of a detection pass; returns (redundant, dependent) flags.
 __device__ __forceinline__ void detect_collect_one(u32 V0, u32 j, const FreshInfo& f,
                                                    const WorkLists& w, RoundCtr* rc, u32& red,
@@ -492,26 +365,6 @@ __device__ __forceinline__ void detect_collect_one(u32 V0, u32 j, const FreshInf
         red = f.mark[j] == 1;
         dep = f.mark[j] == 2;
     }
-}
-
-__global__ void k_detect_collect(u32 V0, u32 F, FreshInfo f, WorkLists w, Counters* ctr) {
-    const u32 j = blockIdx.x * blockDim.x + threadIdx.x;
-    u32 red = 0, dep = 0;
-    if (j < F) detect_collect_one(V0, j, f, w, w.rc, red, dep);
-    warp_add_u32(&ctr->rm_red, red);
-    warp_add_u32(&ctr->rm_dep, dep);
-}
-
-void launch_detect(const DevMesh& m, const Quality& q, u64 depth_cap, u32 V0, u32 F,
-                   FreshInfo f, WorkLists w, Counters* d_ctr, cudaStream_t st) {
-    if (!F) return;
-    const u32 g = (F + 127) / 128;
-    if (q.mode == 0)
-        note_launch(), k_detect_a<0><<<g, 128, 0, st>>>(m, depth_cap, V0, F, f, d_ctr);
-    else
-        note_launch(), k_detect_a<1><<<g, 128, 0, st>>>(m, depth_cap, V0, F, f, d_ctr);
-    note_launch(), k_detect_b<<<g, 128, 0, st>>>(m, V0, F, f, d_ctr);
-    note_launch(), k_detect_collect<<<g, 128, 0, st>>>(V0, F, f, w, d_ctr);
 }
 
 // ---- parallel vertex removal (remove_free_vertex + flop, mesh.hpp:261-304,442-466) ----
@@ -538,12 +391,6 @@ __device__ __forceinline__ void rm_claim_one(const DevMesh& m, const u32* __rest
         return;
     }
     for (int q = 0; q < k; ++q) atomicMin(&x.owner[st[q]], v);
-}
-
-__global__ void k_rm_claim(DevMesh m, const u32* __restrict__ list, u32 n, u32 V0, TriAux x,
-                           FreshInfo f, WorkLists w, Counters* ctr) {
-    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) rm_claim_one(m, list, i, V0, x, f, w, ctr);
 }
 
 // Remove v by ear-clipping its link polygon: each ear is one degree-reducing
@@ -737,37 +584,10 @@ __device__ __noinline__ u32 rm_apply_one(const DevMesh& m, const u32* __restrict
     return done;
 }
 
-__global__ void __launch_bounds__(64) k_rm_apply(DevMesh m, const u32* __restrict__ list, u32 n,
-                                                 u32 round, u32 V0, u32 widx, u32 next_list,
-                                                 TriAux x, FreshInfo f, WorkLists w,
-                                                 Counters* ctr) {
-    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
-    u32 done = 0;
-    if (i < n) done = rm_apply_one(m, list, i, round, V0, widx, next_list, x, f, w, w.rc, ctr, w.rc);
-    warp_add_u32(&ctr->rm_done, done);
-}
-
 __device__ __forceinline__ void rm_post_one(u32 i, const TriAux& x, const WorkLists& w) {
     const u32* st = w.star + (size_t)i * MAX_STAR;
     const u32 k = w.star_len[i];
     for (u32 q = 0; q < k; ++q) x.owner[st[q]] = NONE;
-}
-
-__global__ void k_rm_post(u32 n, TriAux x, WorkLists w) {
-    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) rm_post_one(i, x, w);
-}
-
-void launch_removal_round(const DevMesh& m, u32 round, u32 V0, TriAux a, FreshInfo f,
-                          WorkLists w, u32 cur, u32 n, u32 widx, Counters* d_ctr,
-                          cudaStream_t st) {
-    if (!n) return;
-    note_launch(), k_rm_claim<<<(n + 127) / 128, 128, 0, st>>>(m, w.rm[cur], n, V0, a, f, w, d_ctr);
-    note_launch(), k_rm_apply<<<(n + 63) / 64, 64, 0, st>>>(m, w.rm[cur], n, round, V0, widx, cur ^ 1u, a, f, w,
-                                            d_ctr);
-    note_launch(), k_rm_post<<<(n + 255) / 256, 256, 0, st>>>(n, a, w);
-    const u32 nt = n * (MAX_STAR - 2);
-    note_launch(), k_fixup<<<(nt + 255) / 256, 256, 0, st>>>(m, round, a, w, nt, 0, 0, d_ctr);
 }
 
 // =====================================================================================
@@ -849,8 +669,7 @@ struct InsertArgs {
     u32 reg_cap;          // candidates the region buffers hold
     int isolate;          // claims: 0 reference, 1 isolated (rollback only if state[8]), 2 precedence
     int dep_mis;          // dependent pairs: 1 = priority-MIS rule, 0 = any-higher-neighbour rule
-    int extras;           // refine cavity claims: 1 far side in the main claims, 2 rewrite table
-    int lawson_kernel;    // 1: kernel 1 stops after the splits, k_batch_lawson flips
+    int extras;           // refine cavity claims: 2 = the rewrite table (launch_cavity)
     unsigned long long* trace;   // GDP2D_TRACE: (globaltimer << 8 | tag) per step, or null
     u32* trace_val;              // a work count per trace entry
     u32* trace_n;
@@ -878,7 +697,7 @@ __device__ __forceinline__ void trace(const InsertArgs& a, bool leader, u32 tag,
     }
 }
 
-enum : u32 { INS_OK = 0, INS_GROW = 1, INS_STEPS = 2, INS_REGIONS = 3, INS_NOT_TAIL = 4 };
+enum : u32 { INS_OK = 0, INS_GROW = 1, INS_STEPS = 2, INS_REGIONS = 3 };
 
 __device__ __forceinline__ RoundCtr* ring_at(const Exec& ex, u32 step) {
     return ex.ring + (step & 3u);
@@ -1013,7 +832,6 @@ __device__ void filter(const InsertArgs& a, const Exec& ex, u32 C) {
     trace(a, ex.leader(), TR_CLAIM);
     u32 marked = 0, unsafe = 0;
     const bool rw = a.isolate || a.extras >= 2;
-    const bool bw = GDP2D_BW && !a.isolate && a.extras >= 3;
     for (u32 i = ex.tid; i < C; i += ex.nthr) {
         visits += a.isolate
                       ? cavity_claims_one<MODE>(m, a.c, i, a.ncav, a.rs, a.regions, a.region_len,
@@ -1041,13 +859,6 @@ __device__ void filter(const InsertArgs& a, const Exec& ex, u32 C) {
     if (unsafe) atomicOr(&a.state[8], 1u);
     warp_add_u32(&a.ctr->marked, marked);
     ex.sync();
-    if (bw) {
-        // survivors are final (alive); the rewrite table is still set
-        for (u32 i = ex.tid; i < C; i += ex.nthr)
-            a.c.bw[i] = bw_eligible(a.c, i, a.ncav, a.rs, a.regions, a.region_len, a.x.fkey,
-                                    a.x.ftie);
-        ex.sync();
-    }
     for (u32 i = ex.tid; i < C; i += ex.nthr) {
         cavity_reset_one(i, a.rs, a.regions, a.region_len, a.x.ckey, a.x.ctie);
         if (rw) rw_reset_one(a.c, i, m.nT, a.x.fkey, a.x.ftie);
@@ -1150,11 +961,7 @@ __device__ void split_and_flip(const InsertArgs& a, const Exec& ex, u32 nv, u32 
     {
         const u32 round = a.round0 + step;
         for (u32 i = ex.tid; i < C; i += ex.nthr) {
-            const int r = apply_one(m, a.c, i, a.batch, round, a.b, a.x, a.f, w, rc, 1, a.ctr,
-                                    !a.isolate && (a.extras == 3 || (a.extras == 4 && !ex.block))
-                                        ? a.regions
-                                        : nullptr,
-                                    a.region_len, a.rs);
+            const int r = apply_one(m, a.c, i, a.batch, round, a.b, a.x, a.f, w, rc, 1, a.ctr);
             mid += r == 1;
             cc += r == 2;
         }
@@ -1171,19 +978,6 @@ __device__ void split_and_flip(const InsertArgs& a, const Exec& ex, u32 nv, u32 
     }
     const u32 n = vload(&rc->wl_next);
     ++step;
-    if (a.lawson_kernel) {
-        // the Lawson fixpoint runs in its own lean launch (k_batch_lawson)
-        warp_add_u32(&a.ctr->ins_mid, mid);
-        warp_add_u32(&a.ctr->ins_cc, cc);
-        if (ex.leader()) {
-            a.state[0] = INS_OK;
-            a.state[1] = step;
-            a.state[2] = 0;
-            a.state[3] = 0;
-            a.state[9] = n;
-        }
-        return;
-    }
     lawson_fixpoint_dev(a, ex, m, step, cur, n, flipped, flip_rounds);
     warp_add_u32(&a.ctr->ins_mid, mid);
     warp_add_u32(&a.ctr->ins_cc, cc);
@@ -1397,45 +1191,6 @@ __global__ void __launch_bounds__(INSERT_BLOCK, GDP2D_SPLIT_MINB) k_batch_split(
     split_and_flip(a, ex, nv, nt, ns);
 }
 
-// Kernel 1b (a.lawson_kernel): the Lawson fixpoint after the splits in its
-// own launch, compiled for GDP2D_LAWSON_MINB CTAs per SM (the split kernel's
-// register budget would hold it at two).
-template <int MODE>
-__global__ void __launch_bounds__(INSERT_BLOCK, GDP2D_LAWSON_MINB) k_batch_lawson(InsertArgs a) {
-    if (vload(&a.state[0]) != INS_OK) return;
-    const u32 nv = vload(&a.b.totals[0]), nt = vload(&a.b.totals[1]), ns = vload(&a.b.totals[2]);
-    if (nv == 0) return;
-    const u32 C = vload(a.d_C);
-    const bool block = C <= a.small_c;
-    if (block && blockIdx.x != 0) return;
-    __shared__ RoundCtr sring[5];
-    const Exec ex = block ? block_exec(sring) : grid_exec(a.ring);
-    DevMesh m = a.m;
-    m.nV += nv;
-    m.nT += nt;
-    m.nS += ns;
-    u32 step = vload(&a.state[1]), cur = 0, flip_rounds = 0;
-    const u32 n = vload(&a.state[9]);
-    ull flipped = 0;
-    if (ex.leader()) {
-        RoundCtr z = {};
-        ex.ring[step & 3u] = z;
-    }
-    ex.sync();   // every thread has read state[] before the leader rewrites it
-    lawson_fixpoint_dev(a, ex, m, step, cur, n, flipped, flip_rounds);
-    warp_add_ull(&a.ctr->flips, flipped);
-    {
-        u32 f32 = (u32)flipped;
-        f32 = __reduce_add_sync(0xFFFFFFFFu, f32);
-        if ((threadIdx.x & 31) == 0 && f32) atomicAdd(&a.state[7], f32);
-    }
-    if (ex.leader()) {
-        a.state[0] = step >= a.max_steps ? INS_STEPS : INS_OK;
-        a.state[1] = step;
-        a.state[2] = flip_rounds;
-    }
-}
-
 // Kernel 2: phase 3 rollback (skipped when kernel 1 asked for growth).
 template <int MODE>
 __global__ void __launch_bounds__(ROLLBACK_BLOCK) k_batch_rollback(InsertArgs a) {
@@ -1454,45 +1209,6 @@ __global__ void __launch_bounds__(ROLLBACK_BLOCK) k_batch_rollback(InsertArgs a)
     rollback_loop<MODE>(a, ex, nv, nt, ns);
 }
 
-// Tail kernel: a whole small batch (C <= small_c) in one CTA -- Lines 5-7,
-// the plan, the splits + Lawson and the redundancy detection + rollback --
-// as ONE ordinary launch (GDP2D_TAIL=1; off by default).  Same code and
-// block-mode execution as the split + rollback pair (identical output); it
-// saves the second (cooperative) launch and the kernel boundary, ~14 us per
-// tail batch, but its Lawson rounds run ~40% slower than the split kernel's
-// (different code generation: 80 registers, no min-blocks bound, which the
-// rollback frame needs), so cfg 2 ends 36.9 vs 36.6 ms.  The host picks it
-// from the previous batch's count; a batch that turns out larger returns
-// INS_NOT_TAIL untouched and is redone on the grid kernels.
-template <int MODE>
-__global__ void __launch_bounds__(INSERT_BLOCK) k_batch_tail(const __grid_constant__ InsertArgs a) {
-    const u32 C = vload(a.d_C);
-    if (C > a.reg_cap || C > a.small_c) {
-        if (threadIdx.x == 0) a.state[0] = C > a.reg_cap ? INS_REGIONS : INS_NOT_TAIL;
-        return;
-    }
-    __shared__ RoundCtr sring[5];
-    const Exec ex = block_exec(sring);
-    if (!a.resume) {
-        trace(a, ex.leader(), TR_START);
-        filter<MODE>(a, ex, C);
-        plan_and_scan(a, ex, C);
-    }
-    {
-        const u32 nv = vload(&a.b.totals[0]), nt = vload(&a.b.totals[1]),
-                  ns = vload(&a.b.totals[2]);
-        if (!fits_and_status(a, nv, nt, ns)) return;   // uniform
-        split_and_flip(a, ex, nv, nt, ns);
-    }
-    __syncthreads();
-    // k_batch_rollback's entry conditions
-    if (vload(&a.state[0]) != INS_OK) return;
-    if (a.isolate == 1 && vload(&a.state[8]) == 0) return;
-    const u32 nv = vload(&a.b.totals[0]), nt = vload(&a.b.totals[1]), ns = vload(&a.b.totals[2]);
-    if (nv == 0) return;
-    rollback_loop<MODE>(a, ex, nv, nt, ns);
-}
-
 template <class K0, class K1>
 static int coop_grid(K0 k0, K1 k1, int device, int block = INSERT_BLOCK) {
     int sms = 0, per0 = 0, per1 = 0;
@@ -1504,9 +1220,6 @@ static int coop_grid(K0 k0, K1 k1, int device, int block = INSERT_BLOCK) {
 
 int insert_persistent_grid(int device) {
     return coop_grid(k_batch_split<0>, k_batch_split<1>, device);
-}
-int lawson_batch_grid(int device) {
-    return coop_grid(k_batch_lawson<0>, k_batch_lawson<1>, device);
 }
 int rollback_persistent_grid(int device) {
     return coop_grid(k_batch_rollback<0>, k_batch_rollback<1>, device, ROLLBACK_BLOCK);
@@ -1545,7 +1258,6 @@ static InsertArgs make_args(const InsertLaunch& L) {
     a.isolate = L.isolate;
     a.dep_mis = L.dep_mis;
     a.extras = L.extras;
-    a.lawson_kernel = L.lawson_kernel;
     a.trace = L.trace;
     a.trace_val = L.trace_val;
     a.trace_n = L.trace_n;
@@ -1553,28 +1265,14 @@ static InsertArgs make_args(const InsertLaunch& L) {
     return a;
 }
 
-void launch_insert_tail(const InsertLaunch& L, int mode, cudaStream_t st) {
-    const InsertArgs a = make_args(L);
-    note_launch();
-    if (mode)
-        k_batch_tail<1><<<1, INSERT_BLOCK, 0, st>>>(a);
-    else
-        k_batch_tail<0><<<1, INSERT_BLOCK, 0, st>>>(a);
-}
-
 void launch_insert_persistent(const InsertLaunch& L, int mode, int grid, int grid2, cudaStream_t st,
-                              cudaEvent_t between, int which, int grid3) {
+                              cudaEvent_t between, int which) {
     InsertArgs a = make_args(L);
     void* args[] = {&a};
     if (which & 1) {
         note_launch();
         cudaLaunchCooperativeKernel(mode ? (void*)k_batch_split<1> : (void*)k_batch_split<0>,
                                     dim3(grid), dim3(INSERT_BLOCK), args, 0, st);
-    }
-    if (which & 4) {
-        note_launch();
-        cudaLaunchCooperativeKernel(mode ? (void*)k_batch_lawson<1> : (void*)k_batch_lawson<0>,
-                                    dim3(grid3), dim3(INSERT_BLOCK), args, 0, st);
     }
     if (between) cudaEventRecord(between, st);
     if (which & 2) {

@@ -199,7 +199,7 @@ QualitySummary launch_quality(const DevMesh& m, const Quality& q, void* scratch,
 
 namespace gdp2d {
 
-// Debug validator (GDP2D_VALIDATE=1): the structural checks of
+// Debug validator (GDP2D_CHECK=1, gdp2d_ctx_validate): the structural checks of
 // Mesh::check_structure (mesh.hpp:505-551) on the device.  out[0] = first
 // failure code, out[1] = triangle, out[2] = edge.
 __global__ void k_validate(DevMesh m, u32* out) {

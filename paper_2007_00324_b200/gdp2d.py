@@ -81,7 +81,7 @@ class EngineConfig:
     split_depth_cap: int = 64
     batch_size_cap: int = 0
     seed: int = 0
-    little_batch_sizing: bool = False
+    little_batch_sizing: bool = True   # Little's-law sizing from measured C / L (engine.cu)
     insert_mode: int = 1          # 1 = rollback (reference, default), 0 = isolated, 2 = precedence
     device: int = 0
 

@@ -7,17 +7,13 @@ import sys
 
 VARIANTS = [
     {},
-    {"GDP2D_INSERT": "legacy"},
     {"GDP2D_STANDALONE_C": "0"},
     {"GDP2D_SYNC_COLLECT": "1"},
     {"GDP2D_HALF_GRID_C": "0", "GDP2D_QUARTER_GRID_C": "0"},
     {"GDP2D_DEP": "mis"},
-    {"GDP2D_EXTRAS": "1"},
-    {"GDP2D_LAWSON_KERNEL": "1"},
     {"GDP2D_MODE": "0"},
     {"GDP2D_MODE": "2"},
     {"GDP2D_HEADROOM": "1.0"},
-    {"GDP2D_TAIL": "1"},
 ]
 
 CODE = r'''
