@@ -270,7 +270,7 @@ struct Tracer {
             static const char* tags[] = {"?", "start", "apply", "fixup", "ftest", "fapply", "fpost",
                                          "detA", "detB", "detC", "rmclaim", "rmapply", "rmpost",
                                          "blkin", "blkout", "end", "locate", "claim", "cavity",
-                                         "plan"};
+                                         "plan", "splitend", "rbstart"};
             constexpr u32 NT = sizeof(tags) / sizeof(tags[0]);
             double sum[NT] = {0};
             int cntt[NT] = {0};

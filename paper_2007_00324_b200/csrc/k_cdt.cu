@@ -142,7 +142,7 @@ __device__ __forceinline__ void relocate(const CdtArgs& a, u32 i, u32 t) {
 
 // state[]: CDT_ST_ROUNDS insertion rounds, CDT_ST_FLIP_ROUNDS, CDT_ST_STEPS,
 // [0] = triangles in use at the end.
-__global__ void __launch_bounds__(CDT_BLOCK, GDP2D_CDT_MINB) k_cdt_delaunay(CdtArgs a) {
+__global__ void __launch_bounds__(CDT_BLOCK, GDP2D_CDT_MINB) k_cdt_delaunay(const __grid_constant__ CdtArgs a) {
     cg::grid_group g = cg::this_grid();
     const u32 tid = (u32)g.thread_rank(), nthr = (u32)g.size();
     const u32 lane = threadIdx.x & 31u;
@@ -669,7 +669,7 @@ __device__ bool recover_pipe(const CdtArgs& a, u32 p, const u32* gid, u32 len, u
 }  // namespace
 
 // Pieces of plist[0][0..n0).  state[CDT_ST_NPIECES] = pieces allocated.
-__global__ void __launch_bounds__(CDT_BLOCK) k_cdt_recover(CdtArgs a, u32 n0) {
+__global__ void __launch_bounds__(CDT_BLOCK) k_cdt_recover(const __grid_constant__ CdtArgs a, u32 n0) {
     cg::grid_group g = cg::this_grid();
     const u32 tid = (u32)g.thread_rank(), nthr = (u32)g.size();
     const bool leader = tid == 0;

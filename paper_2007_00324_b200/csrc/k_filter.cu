@@ -49,7 +49,7 @@ void launch_claim(const DevMesh& m, DevCands c, NArg n, TriAux a, Counters* d_ct
 #ifndef GDP2D_CAVITY_MINB
 #define GDP2D_CAVITY_MINB 1
 #endif
-__global__ void __launch_bounds__(128, GDP2D_CAVITY_MINB) k_cavity_bfs(DevMesh m, DevCands c, NArg na, u32 ncav,
+__global__ void __launch_bounds__(128, GDP2D_CAVITY_MINB) k_cavity_bfs(const __grid_constant__ DevMesh m, const __grid_constant__ DevCands c, NArg na, u32 ncav,
                                                     int extras, u32 rs,
                                                     u32* __restrict__ regions,
                                                     u32* __restrict__ region_len,
@@ -112,7 +112,7 @@ __global__ void k_cavity_reset(DevCands c, NArg na, u32 nT, u32 rs,
 // ---- isolated claims (GDP2D_INSERT_ISOLATED, gdp2d_phases.cuh) ----
 
 template <int MODE>
-__global__ void __launch_bounds__(128) k_cavity_claims(DevMesh m, DevCands c, NArg na, u32 ncav,
+__global__ void __launch_bounds__(128) k_cavity_claims(const __grid_constant__ DevMesh m, const __grid_constant__ DevCands c, NArg na, u32 ncav,
                                                        u32 rs, u32* __restrict__ regions,
                                                        u32* __restrict__ region_len,
                                                        u64* __restrict__ ckey, u64 depth_cap,

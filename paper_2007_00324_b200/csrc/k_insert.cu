@@ -96,8 +96,9 @@ __device__ __forceinline__ int apply_one(const DevMesh& m, const DevCands& c, u3
 // trips.  Per-round counters live in rcs[r] (zeroed by the host).  Stops when
 // the next work list is empty or after max_rounds (the host then continues).
 __global__ void __launch_bounds__(LAWSON_BLOCK) k_lawson_persistent(
-    DevMesh m, u32 round0, u32 cur0, u32 n0, u32 max_rounds, TriAux x, WorkLists w,
-    RoundCtr* rcs, u32* result, Counters* ctr) {
+    const __grid_constant__ DevMesh m, u32 round0, u32 cur0, u32 n0, u32 max_rounds,
+    const __grid_constant__ TriAux x, const __grid_constant__ WorkLists w, RoundCtr* rcs,
+    u32* result, Counters* ctr) {
     cg::grid_group g = cg::this_grid();
     const u32 tid = (u32)g.thread_rank(), nthr = (u32)g.size();
     u32 n = n0, cur = cur0, r = 0;
@@ -685,7 +686,7 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 // Step tags of the device trace (printed by the host under GDP2D_TRACE=1).
 enum : u32 { TR_START = 1, TR_APPLY, TR_FIXUP, TR_FTEST, TR_FAPPLY, TR_FPOST, TR_DET_A, TR_DET_B,
              TR_DET_C, TR_RM_CLAIM, TR_RM_APPLY, TR_RM_POST, TR_BLOCK_IN, TR_BLOCK_OUT, TR_END,
-             TR_LOCATE, TR_CLAIM, TR_CAVITY, TR_PLAN };
+             TR_LOCATE, TR_CLAIM, TR_CAVITY, TR_PLAN, TR_SPLIT_END, TR_RB_START };
 
 __device__ __forceinline__ void trace(const InsertArgs& a, bool leader, u32 tag, u32 value = 0) {
     if (a.trace && leader) {
@@ -994,6 +995,7 @@ __device__ void split_and_flip(const InsertArgs& a, const Exec& ex, u32 nv, u32 
         a.state[2] = flip_rounds;
         a.state[3] = 0;
     }
+    trace(a, ex.leader(), TR_SPLIT_END);
 }
 
 // Phase 3 (refine.hpp:551-608): detection + parallel rollback to fixpoint,
@@ -1193,7 +1195,7 @@ __global__ void __launch_bounds__(INSERT_BLOCK, GDP2D_SPLIT_MINB) k_batch_split(
 
 // Kernel 2: phase 3 rollback (skipped when kernel 1 asked for growth).
 template <int MODE>
-__global__ void __launch_bounds__(ROLLBACK_BLOCK) k_batch_rollback(InsertArgs a) {
+__global__ void __launch_bounds__(ROLLBACK_BLOCK) k_batch_rollback(const __grid_constant__ InsertArgs a) {
     if (blockIdx.x == 0 && threadIdx.x == 0)   // start stamp (state words 12-13)
         *reinterpret_cast<unsigned long long*>(a.state + 12) = globaltimer();
     if (vload(&a.state[0]) != INS_OK) return;
@@ -1206,6 +1208,7 @@ __global__ void __launch_bounds__(ROLLBACK_BLOCK) k_batch_rollback(InsertArgs a)
     if (block && blockIdx.x != 0) return;
     __shared__ RoundCtr sring[5];
     const Exec ex = block ? block_exec(sring) : grid_exec(a.ring);
+    trace(a, ex.leader(), TR_RB_START);
     rollback_loop<MODE>(a, ex, nv, nt, ns);
 }
 

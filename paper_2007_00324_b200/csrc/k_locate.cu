@@ -10,7 +10,9 @@
 
 namespace gdp2d {
 
-__global__ void __launch_bounds__(256) k_locate(DevMesh m, DevCands c, NArg na, Counters* ctr) {
+__global__ void __launch_bounds__(256) k_locate(const __grid_constant__ DevMesh m,
+                                                const __grid_constant__ DevCands c, NArg na,
+                                                Counters* ctr) {
     const u32 n = narg(na);
     ull steps = 0;
     for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
