@@ -146,7 +146,8 @@ __global__ void k_pack_tris(DevMesh m, const u32* __restrict__ tv3, const u32* _
                             const uint8_t* __restrict__ alive) {
     const u32 t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= m.nT) return;
-    m.tv[t] = make_uint4(tv3[3 * t], tv3[3 * t + 1], tv3[3 * t + 2], alive[t] ? 1u : 0u);
+    m.tv[t] = make_uint4(tv3[3 * t], tv3[3 * t + 1], tv3[3 * t + 2],
+                         alive[t] ? tri_flags(ts3[3 * t], ts3[3 * t + 1], ts3[3 * t + 2]) : 0u);
     m.ts[t] = make_uint4(ts3[3 * t], ts3[3 * t + 1], ts3[3 * t + 2], 0u);
 }
 

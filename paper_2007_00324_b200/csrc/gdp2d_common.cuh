@@ -4,7 +4,11 @@
 // HBM layout (structure of arrays, one mesh per GPU, pre-allocated with
 // headroom and grown by the host between batches):
 //   double2 xy[V]                       vertex coordinates (16 B, one LDG.128)
-//   uint4   tv[T] = {v0, v1, v2, alive} triangle corners   (reference Triangle::v)
+//   uint4   tv[T] = {v0, v1, v2, flags} triangle corners   (reference Triangle::v);
+//                                       flags = 0 dead, else bit 0 (alive) | bit 1+e
+//                                       when edge e carries a subsegment, so the hot
+//                                       paths read ts only for the few triangles
+//                                       that have one
 //   uint4   tn[T] = {n0, n1, n2, pend}  neighbours encoded (tri << 2) | edge so the
 //                                       far side's edge slot is known without the
 //                                       index_of_neighbor scan of mesh.hpp:107
@@ -43,6 +47,14 @@ __device__ __forceinline__ void set_comp(uint4& q, int i, u32 v) {
     if (i == 0) q.x = v; else if (i == 1) q.y = v; else q.z = v;
 }
 
+// tv.w of an alive triangle whose edges carry subsegments s0, s1, s2 (or NONE)
+__host__ __device__ __forceinline__ u32 tri_flags(u32 s0, u32 s1, u32 s2) {
+    return 1u | (s0 != NONE ? 2u : 0u) | (s1 != NONE ? 4u : 0u) | (s2 != NONE ? 8u : 0u);
+}
+// edge e of the triangle whose corners record is tv carries a subsegment
+__device__ __forceinline__ bool has_seg(const uint4& tv, int e) { return (tv.w >> (1 + e)) & 1u; }
+__device__ __forceinline__ bool any_seg(const uint4& tv) { return (tv.w & 14u) != 0u; }
+
 struct DevMesh {
     double2* xy;
     uint8_t* vkind;
@@ -66,6 +78,12 @@ struct DevMesh {
     uint8_t* sflag;
     u32 nV, nT, nS;
 };
+
+// ts[t] for a triangle whose corners record tv is already loaded: the load is
+// skipped (all NONE) when no edge carries a subsegment -- most triangles.
+__device__ __forceinline__ uint4 load_ts(const DevMesh& m, u32 t, const uint4& tv) {
+    return any_seg(tv) ? m.ts[t] : make_uint4(NONE, NONE, NONE, 0u);
+}
 
 // Candidate list (SplitCandidate, refine.hpp:71) as structure of arrays.
 struct DevCands {

@@ -175,9 +175,8 @@ __device__ __forceinline__ Loc locate_point(const DevMesh& m, u32 start, double2
             if (loc.kind != 3) return loc;
             exit_edge = loc.edge;
         }
-        const uint4 ts = m.ts[cur];
-        if (intercept && comp(ts, exit_edge) != NONE)
-            return Loc{4 /*Intercepted*/, cur, exit_edge, comp(ts, exit_edge), (u32)step};
+        if (intercept && has_seg(tv, exit_edge))
+            return Loc{4 /*Intercepted*/, cur, exit_edge, comp(m.ts[cur], exit_edge), (u32)step};
         const u32 c = comp(tn, exit_edge);
         if (c == NONE) return Loc{3, cur, exit_edge, NONE, (u32)step};
         prev = cur;

@@ -144,10 +144,10 @@ __device__ __forceinline__ u32 cavity_bfs_one(const DevMesh& m, const DevCands& 
         queue[tail++] = located;
         while (head < tail && len <= ncav) {
             const u32 t = queue[head++];
-            // issue the three record loads together (one dependent level)
+            // issue the record loads together (one dependent level); the
+            // subsegment bits of tv.w stand in for the ts record
             const uint4 tv = m.tv[t];
             const uint4 tn = m.tn[t];
-            const uint4 ts = m.ts[t];
             bool pred = t == located;
             if (!pred && tv.w) pred = incircle(m.xy[tv.x], m.xy[tv.y], m.xy[tv.z], p) > 0;
             if (!pred) continue;
@@ -157,7 +157,7 @@ __device__ __forceinline__ u32 cavity_bfs_one(const DevMesh& m, const DevCands& 
             lreg[len++] = t;
             atomicMax((ull*)&ckey[t], (ull)key);
             for (int e = 0; e < 3; ++e) {
-                if (comp(ts, e) != NONE) continue;
+                if (has_seg(tv, e)) continue;
                 const u32 cc = comp(tn, e);
                 if (cc == NONE) continue;
                 const u32 nb = etri(cc);

@@ -20,7 +20,7 @@ namespace gdp2d {
 
 __device__ __forceinline__ void write_tri(const DevMesh& m, u32 t, u32 a, u32 b, u32 c, u32 n0,
                                           u32 n1, u32 n2, u32 pend, u32 s0, u32 s1, u32 s2) {
-    m.tv[t] = make_uint4(a, b, c, 1u);
+    m.tv[t] = make_uint4(a, b, c, tri_flags(s0, s1, s2));
     m.tn[t] = make_uint4(n0, n1, n2, pend);
     m.ts[t] = make_uint4(s0, s1, s2, 0u);
     m.tflag[t] = 2;
@@ -57,7 +57,7 @@ __device__ __forceinline__ void push_work(const WorkLists& w, u32 widx, const u3
 static __device__ void split_triangle_A(const DevMesh& m, const TriAux& x, const WorkLists& w, u32 t,
                                  u32 wv, u32 t1, u32 t2, u32 round, RoundCtr* rc = nullptr,
                                  int seed = 0, Counters* ctr = nullptr) {
-    const uint4 ov = m.tv[t], on = m.tn[t], os = m.ts[t];
+    const uint4 ov = m.tv[t], on = m.tn[t], os = load_ts(m, t, ov);
     x.stamp[t] = round;
     write_tri(m, t, ov.x, ov.y, wv, enc(t1, 1), enc(t2, 0), on.z, 4u, NONE, NONE, os.z);
     write_tri(m, t1, ov.y, ov.z, wv, enc(t2, 1), enc(t, 0), on.x, 4u, NONE, NONE, os.x);
@@ -81,7 +81,7 @@ static __device__ void split_triangle_A(const DevMesh& m, const TriAux& x, const
 static __device__ void split_edge_A(const DevMesh& m, const TriAux& x, const WorkLists& w, u32 t, int e,
                              u32 wv, u32 t2, u32 u2, u32 s_bw, u32 s_wc, u32 round,
                              RoundCtr* rc = nullptr, int seed = 0, Counters* ctr = nullptr) {
-    const uint4 ov = m.tv[t], on = m.tn[t], os = m.ts[t];
+    const uint4 ov = m.tv[t], on = m.tn[t], os = load_ts(m, t, ov);
     const u32 a = comp(ov, e), b = comp(ov, nxt(e)), c = comp(ov, prv(e));
     const u32 uc = comp(on, e);
     x.stamp[t] = round;
@@ -109,7 +109,7 @@ static __device__ void split_edge_A(const DevMesh& m, const TriAux& x, const Wor
     }
     const u32 u = etri(uc);
     const int f = eidx(uc);
-    const uint4 uv = m.tv[u], un = m.tn[u], us = m.ts[u];
+    const uint4 uv = m.tv[u], un = m.tn[u], us = load_ts(m, u, uv);
     const u32 d = comp(uv, f);
     x.stamp[u] = round;
     // t := (a,b,w) {u2, t2, n_ab}; t2 := (a,w,c) {u, n_ca, t}
@@ -152,8 +152,8 @@ __device__ __forceinline__ void fixup_one(const DevMesh& m, u32 round, const Tri
                                           RoundCtr* rc, Counters* ctr) {
     uint4 tn = m.tn[t];
     const uint4 tv = m.tv[t];
-    const uint4 ts = m.ts[t];
     if (!tv.w) return;
+    const uint4 ts = load_ts(m, t, tv);
     const u32 pend = tn.w;
     u32* tn_words = reinterpret_cast<u32*>(m.tn);
 #pragma unroll
@@ -214,10 +214,10 @@ __device__ __forceinline__ void flip_test_one(const DevMesh& m, u32 code, const 
     if (t >= m.nT) return;
     // record loads issued together: the dependent chain is t's record ->
     // the neighbour's corners -> the four coordinates
-    const uint4 tv0 = m.tv[t], tn0 = m.tn[t], ts0 = m.ts[t];
+    const uint4 tv0 = m.tv[t], tn0 = m.tn[t];
     if (!tv0.w) return;
     const u32 c = comp(tn0, e);
-    if (c == NONE || comp(ts0, e) != NONE) return;
+    if (c == NONE || has_seg(tv0, e)) return;
     u32 u = etri(c);
     int f = eidx(c);
     const uint4 tvu = m.tv[u];
@@ -257,8 +257,8 @@ __device__ __forceinline__ u32 flip_apply_one(const DevMesh& m, u32 i, u32 round
     // work item (same key, all "win") that loses the stamp exchange below
     // discards them, and the winner's reads precede any write to the pair
     const u32 ot = x.owner[t], ou = x.owner[u];
-    const uint4 tv = m.tv[t], tn = m.tn[t], ts = m.ts[t];
-    const uint4 uv = m.tv[u], un = m.tn[u], us = m.ts[u];
+    const uint4 tv = m.tv[t], tn = m.tn[t];
+    const uint4 uv = m.tv[u], un = m.tn[u];
     const bool won = ot == key && ou == key;
     w.fwin[i] = won;
     // exactly one duplicate performs the flip
@@ -266,6 +266,7 @@ __device__ __forceinline__ u32 flip_apply_one(const DevMesh& m, u32 i, u32 round
     const u32 a = comp(tv, e), b = comp(tv, nxt(e)), c = comp(tv, prv(e));
     const u32 d = comp(uv, f);
     const double2 pa = m.xy[a], pb = m.xy[b], pc = m.xy[c], pd = m.xy[d];
+    const uint4 ts = load_ts(m, t, tv), us = load_ts(m, u, uv);
     x.stamp[u] = round;
     if (orient2d(pa, pb, pd) <= 0 || orient2d(pa, pd, pc) <= 0) {
         if (atomicCAS(&ctr->err_code, 0u, (u32)DERR_NONCONVEX_FLIP) == 0u) {

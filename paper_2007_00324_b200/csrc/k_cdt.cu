@@ -866,9 +866,9 @@ __global__ void k_cdt_compact_tris(DevMesh s, DevMesh d, const u32* __restrict__
     const uint4 tn = s.tn[t], ts = s.ts[t];
     const auto mapn = [&](u32 r) { return r == NONE ? NONE : enc(newid[etri(r)], eidx(r)); };
     const auto maps = [&](u32 p) { return p == NONE ? NONE : pmap[p]; };
-    d.tv[nt] = make_uint4(tv.x, tv.y, tv.z, 1u);
-    d.tn[nt] = make_uint4(mapn(tn.x), mapn(tn.y), mapn(tn.z), 0u);
     const uint4 sn = make_uint4(maps(ts.x), maps(ts.y), maps(ts.z), 0u);
+    d.tv[nt] = make_uint4(tv.x, tv.y, tv.z, tri_flags(sn.x, sn.y, sn.z));
+    d.tn[nt] = make_uint4(mapn(tn.x), mapn(tn.y), mapn(tn.z), 0u);
     d.ts[nt] = sn;
     d.tflag[nt] = 2;
     atomicMin(&d.vtri[tv.x], nt);

@@ -236,8 +236,9 @@ __device__ __noinline__ u32 detect_a_one(const DevMesh& m, u64 depth_cap, u32 V0
                     }
                 }
             }
+            if (!has_seg(tv, i)) return;
             const u32 s = comp(m.ts[t], i);
-            if (s == NONE || s >= best) return;
+            if (s >= best) return;
             const uint2 sv = m.sv[s];
             if (!encroaches<MODE>(m.xy[sv.x], m.xy[sv.y], pv)) return;
             if ((u64)m.sdepth[s] >= depth_cap) return;
@@ -427,7 +428,7 @@ __device__ __noinline__ u32 rm_apply_one(const DevMesh& m, const u32* __restrict
 #pragma unroll 4
             for (int q = 0; q < k; ++q) {
                 const u32 t = st[q];
-                const uint4 tv = m.tv[t], tn = m.tn[t], ts = m.ts[t];
+                const uint4 tv = m.tv[t], tn = m.tn[t], ts = load_ts(m, t, tv);
                 const int iv = tv.x == v ? 0 : (tv.y == v ? 1 : 2);
                 L[q] = comp(tv, nxt(iv));
                 R[q] = comp(tn, iv);
