@@ -155,7 +155,7 @@ __global__ void k_unpack_tris(DevMesh m, u32* __restrict__ tv3, u32* __restrict_
                               uint8_t* __restrict__ alive) {
     const u32 t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= m.nT) return;
-    const uint4 tv = m.tv[t], ts = m.ts[t];
+    const uint4 tv = m.tv[t], ts = load_ts(m, t, tv);
     tv3[3 * t] = tv.x;
     tv3[3 * t + 1] = tv.y;
     tv3[3 * t + 2] = tv.z;

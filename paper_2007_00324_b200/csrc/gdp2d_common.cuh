@@ -81,6 +81,8 @@ struct DevMesh {
 
 // ts[t] for a triangle whose corners record tv is already loaded: the load is
 // skipped (all NONE) when no edge carries a subsegment -- most triangles.
+// Every reader of ts goes through the bits: a rewrite that leaves a triangle
+// without subsegments does not store its ts record, so ts[t] is stale then.
 __device__ __forceinline__ uint4 load_ts(const DevMesh& m, u32 t, const uint4& tv) {
     return any_seg(tv) ? m.ts[t] : make_uint4(NONE, NONE, NONE, 0u);
 }

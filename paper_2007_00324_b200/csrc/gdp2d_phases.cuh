@@ -50,7 +50,7 @@ __device__ __forceinline__ u32 locate_one(const DevMesh& m, const DevCands& c, u
             done = true;
             break;
         case 1: {  // OnEdge
-            const u32 s = comp(m.ts[loc.tri], loc.edge);
+            const u32 s = has_seg(m.tv[loc.tri], loc.edge) ? comp(m.ts[loc.tri], loc.edge) : NONE;
             if (s == NONE) {
                 c.loc[i] = loc.tri;
                 c.lkind[i] = 1;
@@ -261,7 +261,7 @@ __device__ __forceinline__ bool cavity_bfs_into(const DevMesh& m, u32 seed, bool
         if (len >= rs) return false;
         reg[len++] = t;
         const uint4 tn = m.tn[t];
-        const uint4 ts = m.ts[t];
+        const uint4 ts = load_ts(m, t, m.tv[t]);
         for (int e = 0; e < 3; ++e) {
             if (comp(ts, e) != NONE) continue;
             const u32 cc = comp(tn, e);
@@ -299,7 +299,7 @@ __device__ __forceinline__ u32 cavity_claims_one(const DevMesh& m, const DevCand
             u32 red = NONE;
             if (c.kind[i] == 1) {
                 for (u32 k = 0; k < blen; ++k) {
-                    const uint4 ts = m.ts[reg[k]];
+                    const uint4 ts = load_ts(m, reg[k], m.tv[reg[k]]);
                     for (int e = 0; e < 3; ++e) {
                         const u32 s = comp(ts, e);
                         if (s == NONE || s >= red) continue;
@@ -329,7 +329,7 @@ __device__ __forceinline__ u32 cavity_claims_one(const DevMesh& m, const DevCand
         for (u32 k = 0; k < blen && ok; ++k) {
             const u32 t = reg[k];
             const uint4 tn = m.tn[t];
-            const uint4 ts = m.ts[t];
+            const uint4 ts = load_ts(m, t, m.tv[t]);
             for (int e = 0; e < 3; ++e) {
                 const u32 s = comp(ts, e);
                 if (s != NONE) {

@@ -20,9 +20,11 @@ namespace gdp2d {
 
 __device__ __forceinline__ void write_tri(const DevMesh& m, u32 t, u32 a, u32 b, u32 c, u32 n0,
                                           u32 n1, u32 n2, u32 pend, u32 s0, u32 s1, u32 s2) {
-    m.tv[t] = make_uint4(a, b, c, tri_flags(s0, s1, s2));
+    const u32 fl = tri_flags(s0, s1, s2);
+    m.tv[t] = make_uint4(a, b, c, fl);
     m.tn[t] = make_uint4(n0, n1, n2, pend);
-    m.ts[t] = make_uint4(s0, s1, s2, 0u);
+    // ts is read only behind the tv.w subsegment bits (load_ts / has_seg)
+    if (fl != 1u) m.ts[t] = make_uint4(s0, s1, s2, 0u);
     m.tflag[t] = 2;
     m.vtri[a] = NONE;
     m.vtri[b] = NONE;

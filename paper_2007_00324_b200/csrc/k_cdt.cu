@@ -416,7 +416,7 @@ __device__ int pipe_walk(const DevMesh& m, u32 u, u32 w, u32 t, int e, u32* out,
     for (u32 guard = 0; guard < (1u << 26); ++guard) {
         if (out) out[len] = t;
         ++len;
-        if (comp(m.ts[t], e) != NONE) {
+        if (has_seg(m.tv[t], e)) {
             info = DERR_SEG_CROSS;
             return PIPE_ERR;
         }
@@ -539,9 +539,9 @@ __device__ bool recover_pipe(const CdtArgs& a, u32 p, const u32* gid, u32 len, u
         const u32 g = gid[j];
         CdtLocal T;
         T.v = m.tv[g];
+        T.s = load_ts(m, g, T.v);
         T.v.w = 0;
         const uint4 tn = m.tn[g];
-        T.s = m.ts[g];
         T.n = make_uint4(0, 0, 0, 0);
 #pragma unroll
         for (int e = 0; e < 3; ++e) {
@@ -675,9 +675,14 @@ __global__ void __launch_bounds__(CDT_BLOCK) k_cdt_recover(const __grid_constant
     const bool leader = tid == 0;
     const DevMesh& m = a.m;
     u32* tsw = reinterpret_cast<u32*>(m.ts);
+    u32* tvw = reinterpret_cast<u32*>(m.tv);
     u32 n = n0, cur = 0, step = 0, rounds = 0;
     u32 found = 0, pipes = 0, splits = 0, pmax = 0;
     ring_next(a, step + 3u, leader);
+    // rewrites do not store the ts record of a triangle without subsegments
+    // (write_tri): make every such record NONE before edges get flagged
+    for (u32 t = tid; t < m.nT; t += nthr)
+        if (!any_seg(m.tv[t])) m.ts[t] = make_uint4(NONE, NONE, NONE, 0u);
     g.sync();
     while (n > 0 && rounds < (1u << 16)) {
         RoundCtr* rc = ring_slot(a, step);
@@ -697,7 +702,11 @@ __global__ void __launch_bounds__(CDT_BLOCK) k_cdt_recover(const __grid_constant
                 // flag_edge (cdt.hpp:273-284); the lower piece keeps a shared edge
                 const u32 far = comp(m.tn[t], e);
                 atomicMin(&tsw[4 * (size_t)t + e], p);
-                if (far != NONE) atomicMin(&tsw[4 * (size_t)etri(far) + eidx(far)], p);
+                atomicOr(&tvw[4 * (size_t)t + 3], 2u << e);   // the tv.w subsegment bit
+                if (far != NONE) {
+                    atomicMin(&tsw[4 * (size_t)etri(far) + eidx(far)], p);
+                    atomicOr(&tvw[4 * (size_t)etri(far) + 3], 2u << eidx(far));
+                }
                 a.plen[p] = 0;
                 ++found;
             } else if (r == PIPE_SPLIT) {
@@ -849,8 +858,9 @@ __global__ void k_alive_flags(DevMesh m, u32* flags) {
 __global__ void k_cdt_piece_live(DevMesh m, u32* plive) {
     const u32 t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= m.nT) return;
-    if (!m.tv[t].w) return;
-    const uint4 ts = m.ts[t];
+    const uint4 tv = m.tv[t];
+    if (!tv.w) return;
+    const uint4 ts = load_ts(m, t, tv);
     if (ts.x != NONE) plive[ts.x] = 1;
     if (ts.y != NONE) plive[ts.y] = 1;
     if (ts.z != NONE) plive[ts.z] = 1;
@@ -863,7 +873,7 @@ __global__ void k_cdt_compact_tris(DevMesh s, DevMesh d, const u32* __restrict__
     const uint4 tv = s.tv[t];
     if (!tv.w) return;
     const u32 nt = newid[t];
-    const uint4 tn = s.tn[t], ts = s.ts[t];
+    const uint4 tn = s.tn[t], ts = load_ts(s, t, tv);
     const auto mapn = [&](u32 r) { return r == NONE ? NONE : enc(newid[etri(r)], eidx(r)); };
     const auto maps = [&](u32 p) { return p == NONE ? NONE : pmap[p]; };
     const uint4 sn = make_uint4(maps(ts.x), maps(ts.y), maps(ts.z), 0u);

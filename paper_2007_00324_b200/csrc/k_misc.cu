@@ -215,8 +215,10 @@ __global__ void k_validate(DevMesh m, u32* out) {
     };
     if (tv.x >= m.nV || tv.y >= m.nV || tv.z >= m.nV) return fail(1, -1);
     if (orient2d(m.xy[tv.x], m.xy[tv.y], m.xy[tv.z]) <= 0) return fail(2, -1);
-    const uint4 tn = m.tn[t], ts = m.ts[t];
+    const uint4 tn = m.tn[t], ts = load_ts(m, t, tv);
     if (tn.w) return fail(3, -1);
+    for (int e = 0; e < 3; ++e)   // the subsegment bits of tv.w match the ts record
+        if (has_seg(tv, e) != (comp(ts, e) != NONE)) return fail(14, e);
     for (int e = 0; e < 3; ++e) {
         const u32 c = comp(tn, e);
         if (c == NONE) continue;
@@ -228,7 +230,7 @@ __global__ void k_validate(DevMesh m, u32* out) {
         if (comp(m.tn[u], f) != enc(t, e)) return fail(6, e);
         if (comp(uv, nxt(f)) != comp(tv, prv(e)) || comp(uv, prv(f)) != comp(tv, nxt(e)))
             return fail(7, e);
-        if (comp(m.ts[u], f) != comp(ts, e)) return fail(8, e);
+        if (comp(load_ts(m, u, uv), f) != comp(ts, e)) return fail(8, e);
     }
     for (int e = 0; e < 3; ++e) {
         const u32 s = comp(ts, e);
@@ -238,7 +240,8 @@ __global__ void k_validate(DevMesh m, u32* out) {
         const u32 x = comp(tv, nxt(e)), y = comp(tv, prv(e));
         if (!((sv.x == x && sv.y == y) || (sv.x == y && sv.y == x))) return fail(10, e);
         const u32 st = m.stri[s];
-        if (st == NONE || st >= m.nT || seg_slot(m.ts[st], s) < 0) return fail(11, e);
+        if (st == NONE || st >= m.nT || seg_slot(load_ts(m, st, m.tv[st]), s) < 0)
+            return fail(11, e);
     }
     for (int i = 0; i < 3; ++i) {
         const u32 v = comp(tv, i);

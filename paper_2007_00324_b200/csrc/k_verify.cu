@@ -59,10 +59,10 @@ __global__ void k_verify_tris(DevMesh m, Quality q, VerifyAcc* acc) {
             if (bin >= GDP2D_HIST_BINS) bin = GDP2D_HIST_BINS - 1;
             atomicAdd(&hist[bin], 1u);
             angle_fx = (ull)__double2ll_rn(ldexp(min_ang, kAngleFx));
-            const uint4 tn = m.tn[t], ts = m.ts[t];
+            const uint4 tn = m.tn[t];
             for (int e = 0; e < 3; ++e) {
                 const u32 c = comp(tn, e);
-                if (c == NONE || comp(ts, e) != NONE) continue;
+                if (c == NONE || has_seg(tv, e)) continue;
                 const u32 u = etri(c);
                 if (u < t) continue;   // each interior edge once
                 const u32 d = comp(m.tv[u], eidx(c));
