@@ -431,13 +431,15 @@ def main():
     dropin = None
     if a.dropin_steps > 0:
         host.time_dropin(meshes[0], cfg["theta"], 1, device)          # warm the cached context
-        ds, dst = host.time_dropin(meshes[0], cfg["theta"], a.dropin_steps, device)
+        ds, dst, parts = host.time_dropin(meshes[0], cfg["theta"], a.dropin_steps, device,
+                                          parts=True)
         dropin = {"value": dst * a.dropin_steps / ds, "unit": UNIT,
                   "wall_s_per_step": ds / a.dropin_steps, "steps": a.dropin_steps,
                   "path": "gdp2d::refine(cdtref::Mesh&, q, EngineConfig{}) from "
                           "include/gdp2d_cdtref.hpp: AoS->SoA pack, gdp2d_refine with pageable "
                           "host buffers (H2D + loop + D2H), unpack in place",
-                  "h2d_bytes_per_step": mesh_bytes(meshes[0]), "steiner": dst}
+                  "h2d_bytes_per_step": mesh_bytes(meshes[0]), "steiner": dst,
+                  "breakdown_s_per_step": parts}
 
     # ---- roofline: the dominant engine kernel (largest share of the step) ----
     peak, peak_kind = load_peaks()

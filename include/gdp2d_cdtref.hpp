@@ -37,6 +37,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <map>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -44,9 +45,52 @@
 
 #include "gdp2d.h"
 
+#ifdef __linux__
+#include <sys/mman.h>
+#endif
+
 namespace gdp2d {
 
 namespace detail {
+
+// Transparent-huge-page hint for [p, p + bytes) (the 2 MB pages inside it):
+// the first touch of a multi-GB mesh array then faults 2 MB pages.
+inline void hint_huge(const void* p, size_t bytes) {
+#if defined(__linux__) && defined(MADV_HUGEPAGE)
+    constexpr uintptr_t kHuge = uintptr_t(2) << 20;
+    const uintptr_t lo = (reinterpret_cast<uintptr_t>(p) + kHuge - 1) & ~(kHuge - 1);
+    const uintptr_t hi = (reinterpret_cast<uintptr_t>(p) + bytes) & ~(kHuge - 1);
+    if (hi > lo) madvise(reinterpret_cast<void*>(lo), hi - lo, MADV_HUGEPAGE);
+#else
+    (void)p;
+    (void)bytes;
+#endif
+}
+
+// Uninitialised host array (no value-initialisation pass: the parallel fill
+// below is its first touch, so page faults spread over the host cores).
+template <class T>
+inline std::unique_ptr<T[]> raw_array(size_t n) {
+    std::unique_ptr<T[]> a(new T[n ? n : 1]);
+    hint_huge(a.get(), sizeof(T) * n);
+    return a;
+}
+
+// Size a vector to n elements whose contents are about to be overwritten
+// wholesale: beyond its capacity a fresh (huge-page hinted) buffer replaces
+// it instead of reallocating and copying the old elements.
+template <class V>
+inline void resize_for_overwrite(V& v, size_t n) {
+    if (n > v.capacity()) {
+        V fresh;
+        fresh.reserve(n);
+        hint_huge(fresh.data(), sizeof(typename V::value_type) * n);
+        fresh.resize(n);
+        v.swap(fresh);
+    } else {
+        v.resize(n);
+    }
+}
 
 // The AoS <-> SoA conversion of a multi-million-element mesh is host work on
 // the drop-in path: split it over the host cores (contiguous blocks, so the
@@ -89,17 +133,17 @@ inline gdp2d_params make_params(const cdtref::QualityCriteria& q,
 
 // AoS Mesh -> SoA staging owned by the caller's stack frame.
 struct Packed {
-    std::vector<double> xy;
-    std::vector<uint8_t> vkind, valive, talive, senc, salive;
-    std::vector<uint32_t> vbirth, tv, tn, ts, sv, sparent;
+    std::unique_ptr<double[]> xy;
+    std::unique_ptr<uint8_t[]> vkind, valive, talive, senc, salive;
+    std::unique_ptr<uint32_t[]> vbirth, tv, tn, ts, sv, sparent;
     gdp2d_mesh_view view{};
 
     explicit Packed(const cdtref::Mesh& m) {
         const size_t V = m.vertices.size(), T = m.triangles.size(), S = m.subsegments.size();
-        xy.resize(2 * V);
-        vkind.resize(V);
-        valive.resize(V);
-        vbirth.resize(V);
+        xy = raw_array<double>(2 * V);
+        vkind = raw_array<uint8_t>(V);
+        valive = raw_array<uint8_t>(V);
+        vbirth = raw_array<uint32_t>(V);
         parallel_for(V, [&](size_t i) {
             const cdtref::Vertex& v = m.vertices[i];
             xy[2 * i] = v.pos.x;
@@ -108,10 +152,10 @@ struct Packed {
             vbirth[i] = v.birth_batch;
             valive[i] = v.alive ? 1 : 0;
         });
-        tv.resize(3 * T);
-        tn.resize(3 * T);
-        ts.resize(3 * T);
-        talive.resize(T);
+        tv = raw_array<uint32_t>(3 * T);
+        tn = raw_array<uint32_t>(3 * T);
+        ts = raw_array<uint32_t>(3 * T);
+        talive = raw_array<uint8_t>(T);
         parallel_for(T, [&](size_t t) {
             const cdtref::Triangle& tr = m.triangles[t];
             for (int i = 0; i < 3; ++i) {
@@ -121,35 +165,35 @@ struct Packed {
             }
             talive[t] = tr.alive ? 1 : 0;
         });
-        sv.resize(2 * S);
-        sparent.resize(S);
-        senc.resize(S);
-        salive.resize(S);
-        for (size_t s = 0; s < S; ++s) {
+        sv = raw_array<uint32_t>(2 * S);
+        sparent = raw_array<uint32_t>(S);
+        senc = raw_array<uint8_t>(S);
+        salive = raw_array<uint8_t>(S);
+        parallel_for(S, [&](size_t s) {
             const cdtref::Subsegment& sg = m.subsegments[s];
             sv[2 * s] = sg.v[0];
             sv[2 * s + 1] = sg.v[1];
             sparent[s] = sg.parent;
             senc[s] = sg.encroached ? 1 : 0;
             salive[s] = sg.alive ? 1 : 0;
-        }
+        });
         view.n_vertices = static_cast<uint32_t>(V);
         view.n_triangles = static_cast<uint32_t>(T);
         view.n_subsegments = static_cast<uint32_t>(S);
         view.batch_epoch = m.batch_epoch;
-        view.xy = xy.data();
-        view.vert_kind = vkind.data();
-        view.vert_birth = vbirth.data();
-        view.vert_alive = valive.data();
+        view.xy = xy.get();
+        view.vert_kind = vkind.get();
+        view.vert_birth = vbirth.get();
+        view.vert_alive = valive.get();
         view.vert_tri = m.vert_tri.data();
-        view.tri_v = tv.data();
-        view.tri_n = tn.data();
-        view.tri_seg = ts.data();
-        view.tri_alive = talive.data();
-        view.seg_v = sv.data();
-        view.seg_parent = sparent.data();
-        view.seg_encroached = senc.data();
-        view.seg_alive = salive.data();
+        view.tri_v = tv.get();
+        view.tri_n = tn.get();
+        view.tri_seg = ts.get();
+        view.tri_alive = talive.get();
+        view.seg_v = sv.get();
+        view.seg_parent = sparent.get();
+        view.seg_encroached = senc.get();
+        view.seg_alive = salive.get();
         view.seg_tri = m.seg_tri.data();
     }
 };
@@ -157,7 +201,7 @@ struct Packed {
 // SoA result -> the caller's Mesh, in place (ids preserved).
 inline void unpack(const gdp2d_mesh_buf& b, cdtref::Mesh& m) {
     const size_t V = b.n_vertices, T = b.n_triangles, S = b.n_subsegments;
-    m.vertices.resize(V);
+    resize_for_overwrite(m.vertices, V);
     m.vert_tri.assign(b.vert_tri, b.vert_tri + V);
     parallel_for(V, [&](size_t i) {
         cdtref::Vertex& v = m.vertices[i];
@@ -166,7 +210,7 @@ inline void unpack(const gdp2d_mesh_buf& b, cdtref::Mesh& m) {
         v.birth_batch = b.vert_birth[i];
         v.alive = b.vert_alive[i] != 0;
     });
-    m.triangles.resize(T);
+    resize_for_overwrite(m.triangles, T);
     parallel_for(T, [&](size_t t) {
         cdtref::Triangle& tr = m.triangles[t];
         for (int i = 0; i < 3; ++i) {
@@ -176,15 +220,15 @@ inline void unpack(const gdp2d_mesh_buf& b, cdtref::Mesh& m) {
         }
         tr.alive = b.tri_alive[t] != 0;
     });
-    m.subsegments.resize(S);
+    resize_for_overwrite(m.subsegments, S);
     m.seg_tri.assign(b.seg_tri, b.seg_tri + S);
-    for (size_t s = 0; s < S; ++s) {
+    parallel_for(S, [&](size_t s) {
         cdtref::Subsegment& sg = m.subsegments[s];
         sg.v = {b.seg_v[2 * s], b.seg_v[2 * s + 1]};
         sg.parent = b.seg_parent[s];
         sg.encroached = b.seg_encroached[s] != 0;
         sg.alive = b.seg_alive[s] != 0;
-    }
+    });
     m.batch_epoch = b.batch_epoch;
 }
 

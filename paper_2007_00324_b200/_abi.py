@@ -190,7 +190,8 @@ HOST_SIGNATURES = {
     "gdp2d_host_free_buf": (None, [C.POINTER(MeshBuf)]),
     "gdp2d_host_last_error": (C.c_char_p, []),
     "gdp2d_host_time_dropin": (C.c_int, [C.POINTER(MeshView), C.c_double, C.c_int, C.c_int,
-                                         C.POINTER(C.c_double), C.POINTER(C.c_uint64)]),
+                                         C.POINTER(C.c_double), C.POINTER(C.c_uint64),
+                                         C.c_void_p]),
 }
 
 _LIBS: dict[str, C.CDLL] = {}

@@ -17,6 +17,8 @@
 #include <vector>
 #include <thread>
 
+#include <sys/mman.h>
+
 #include "engine.h"
 #include "gdp2d.h"
 #include "scan.cuh"
@@ -966,11 +968,25 @@ void download_into(gdp2d_ctx* x, gdp2d_mesh_buf* b) {
     CK(cudaGetLastError());
 }
 
+// Library-owned output arrays (freed by gdp2d_free): 2 MB aligned, with a
+// transparent-huge-page hint for the big ones, so the first touch by the
+// staged D2H copy faults 2 MB pages, not 4 KB ones.
+void* host_out_alloc(size_t bytes) {
+    constexpr size_t kHuge = 2u << 20;
+    if (bytes < kHuge) return std::malloc(bytes ? bytes : 1);
+    const size_t n = (bytes + kHuge - 1) / kHuge * kHuge;
+    void* p = std::aligned_alloc(kHuge, n);
+#ifdef MADV_HUGEPAGE
+    if (p) madvise(p, n, MADV_HUGEPAGE);
+#endif
+    return p;
+}
+
 void download(gdp2d_ctx* x, gdp2d_mesh_buf* b) {
     const DevMesh& m = x->work.m;
     const u32 V = m.nV, T = m.nT, S = m.nS;
     std::memset(b, 0, sizeof *b);
-    auto hm = [](size_t bytes) { return std::malloc(bytes ? bytes : 1); };
+    auto hm = [](size_t bytes) { return host_out_alloc(bytes); };
     b->xy = (double*)hm(16ull * V);
     b->vert_kind = (uint8_t*)hm(V);
     b->vert_birth = (u32*)hm(4ull * V);

@@ -297,9 +297,11 @@ void gdp2d_host_free_buf(gdp2d_mesh_buf* b) {
 // place -- exactly what a cdtref caller gets after swapping the namespace.
 // The reference Mesh is built from *in once; each of `steps` calls refines a
 // fresh copy of it (the copy is untimed).  Writes the summed call time and
-// the last call's Steiner count.
+// the last call's Steiner count.  parts (optional, 4 doubles): summed seconds
+// of the shim's steps, timed separately on a further copy -- AoS->SoA pack,
+// gdp2d_refine (H2D + loop + D2H), SoA->AoS unpack, gdp2d_free.
 int gdp2d_host_time_dropin(const gdp2d_mesh_view* in, double theta_deg, int steps, int device,
-                           double* seconds, uint64_t* steiner) {
+                           double* seconds, uint64_t* steiner, double* parts) {
     try {
         const Mesh base = view_to_mesh(in);
         QualityCriteria q;
@@ -314,6 +316,36 @@ int gdp2d_host_time_dropin(const gdp2d_mesh_view* in, double theta_deg, int step
             *steiner = rep.steiner_points;
         }
         *seconds = total;
+        if (parts) {
+            using clk = std::chrono::steady_clock;
+            auto sec = [](clk::time_point a, clk::time_point b) {
+                return std::chrono::duration<double>(b - a).count();
+            };
+            for (int k = 0; k < 4; ++k) parts[k] = 0.0;
+            for (int i = 0; i < steps; ++i) {
+                Mesh m = base;
+                const gdp2d_params p = gdp2d::detail::make_params(q, cfg);
+                const auto t0 = clk::now();
+                gdp2d::detail::Packed pk(m);
+                const auto t1 = clk::now();
+                std::vector<gdp2d_batch_metrics> bm(cfg.iteration_cap + 1);
+                gdp2d_report r{};
+                r.batches = bm.data();
+                r.batches_capacity = (uint32_t)bm.size();
+                gdp2d_mesh_buf out{};
+                if (gdp2d_refine(&pk.view, &out, &p, &r, device) != GDP2D_OK)
+                    throw std::runtime_error(gdp2d_last_error());
+                const auto t2 = clk::now();
+                gdp2d::detail::unpack(out, m);
+                const auto t3 = clk::now();
+                gdp2d_free(&out);
+                const auto t4 = clk::now();
+                parts[0] += sec(t0, t1);
+                parts[1] += sec(t1, t2);
+                parts[2] += sec(t2, t3);
+                parts[3] += sec(t3, t4);
+            }
+        }
         return 0;
     } catch (const std::exception& e) {
         g_err = e.what();

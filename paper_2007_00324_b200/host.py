@@ -50,18 +50,24 @@ def build_cdt(points: np.ndarray, segments: np.ndarray, close_hull: bool = True)
     return Mesh.from_buf(out, lib.gdp2d_host_free_buf), closed
 
 
-def time_dropin(mesh: Mesh, theta: float, steps: int, device: int = 0):
+def time_dropin(mesh: Mesh, theta: float, steps: int, device: int = 0, parts: bool = False):
     """The drop-in caller's path (include/gdp2d_cdtref.hpp): `steps` calls of
     gdp2d::refine(cdtref::Mesh&, q, EngineConfig{}) on copies of the mesh as
     a reference AoS Mesh in pageable memory.  Returns (seconds summed over
-    the calls, Steiner count of the last call)."""
+    the calls, Steiner count of the last call[, per-step breakdown dict of
+    the shim's pack / gdp2d_refine / unpack / free when parts])."""
     lib = A.host()
     v = mesh.view()
     secs = C.c_double()
     st = C.c_uint64()
-    if lib.gdp2d_host_time_dropin(C.byref(v), theta, steps, device, C.byref(secs), C.byref(st)):
+    pv = (C.c_double * 4)()
+    if lib.gdp2d_host_time_dropin(C.byref(v), theta, steps, device, C.byref(secs), C.byref(st),
+                                  pv if parts else None):
         raise RuntimeError("gdp2d::refine: " + lib.gdp2d_host_last_error().decode())
-    return secs.value, int(st.value)
+    if not parts:
+        return secs.value, int(st.value)
+    names = ("pack_s", "gdp2d_refine_s", "unpack_s", "free_s")
+    return secs.value, int(st.value), {k: pv[i] / steps for i, k in enumerate(names)}
 
 
 def close_hull(points: np.ndarray, segments: np.ndarray, check: bool = True) -> np.ndarray:
