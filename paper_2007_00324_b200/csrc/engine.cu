@@ -1097,6 +1097,7 @@ bool insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, int prefiltered, u32
         L.small_c = x->small_c;
         L.resume = started ? 1 : 0;
         L.prefiltered = prefiltered;
+        L.planned = prefiltered && !isolate;
         L.reg_cap = reg_cap;
         if (x->tr.on) {
             L.trace = x->tr.d_trace;
@@ -1319,7 +1320,8 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
                                            x->region_len, x->ins_state + 8, x->d_ctr, st);
                 else
                     launch_cavity(m, x->c, na, ncav, 2, x->aux, x->regions,
-                                  x->region_len, nullptr, x->d_ctr, st);
+                                  x->region_len, nullptr, x->d_ctr, st, &x->ib,
+                                  p->split_depth_cap);
                 CK(cudaEventRecord(x->ev[5], st));
                 filtered_events = true;
             }

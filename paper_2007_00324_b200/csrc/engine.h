@@ -98,12 +98,25 @@ inline void launch_claim(const DevMesh& m, DevCands c, u32 n, TriAux a, Counters
                          cudaStream_t st) {
     launch_claim(m, c, NArg::host(n), a, d_ctr, st);
 }
+struct InsertBufs {
+    u32* nv = nullptr;  // per-candidate needs / offsets
+    u32* nt = nullptr;
+    u32* ns = nullptr;
+    u32* ov = nullptr;
+    u32* ot = nullptr;
+    u32* os = nullptr;
+    u32* totals = nullptr;   // device [3]
+    u32 cap = 0;
+};
+
 // Cavity filter (refine.hpp:382-429).  extras: 0 parity (the reference's
 // claims only), 2 refinement: the rewrite table also guards each split
 // (rw_*_one, gdp2d_phases.cuh).
+// plan != null: the survivors' phase-1 plan (plan_one) is written to
+// plan->nv / nt / ns by the last filter kernel (InsertLaunch::planned).
 void launch_cavity(const DevMesh& m, DevCands c, NArg n, u32 ncav, int extras, TriAux a,
                    u32* regions, u32* region_len, u32* bfs_len, Counters* d_ctr,
-                   cudaStream_t st);
+                   cudaStream_t st, const InsertBufs* plan = nullptr, u64 depth_cap = 0);
 inline void launch_cavity(const DevMesh& m, DevCands c, u32 n, u32 ncav, int extras, TriAux a,
                           u32* regions, u32* region_len, u32* bfs_len, Counters* d_ctr,
                           cudaStream_t st) {
@@ -120,16 +133,6 @@ void launch_cavity_isolated(const DevMesh& m, DevCands c, NArg n, u32 ncav, u32 
 
 // ---- insertion ---------------------------------------------------------------------
 
-struct InsertBufs {
-    u32* nv = nullptr;  // per-candidate needs / offsets
-    u32* nt = nullptr;
-    u32* ns = nullptr;
-    u32* ov = nullptr;
-    u32* ot = nullptr;
-    u32* os = nullptr;
-    u32* totals = nullptr;   // device [3]
-    u32 cap = 0;
-};
 
 struct FreshInfo {
     u64* key = nullptr;
@@ -203,6 +206,7 @@ struct InsertLaunch {
     u32 small_c = 0;
     int resume = 0;
     int prefiltered = 0;        // standalone Lines 5-7 kernels ran (they skip C <= small_c)
+    int planned = 0;            // ... and made the phase-1 plan (launch_cavity's plan)
     u32 reg_cap = 0xFFFFFFFFu;  // candidates the region buffers hold (INS_REGIONS beyond)
     int isolate = 1;            // claims: 0 reference cavity, 1 isolated (ring), 2 precedence
     int dep_mis = 0;            // dependent pairs by the priority-MIS rule

@@ -97,16 +97,29 @@ __global__ void k_cavity_check(DevCands c, NArg na, u32 rs, const u32* __restric
     block_add<u32>(&ctr->surv_cavity, surv);
 }
 
-__global__ void k_cavity_reset(DevCands c, NArg na, u32 nT, u32 rs,
+// plan.nv != null: the phase-1 plan of each survivor (plan_one) is made here,
+// by every candidate's thread at full occupancy, instead of inside the
+// persistent insertion kernel (InsertLaunch::planned).
+__global__ void k_cavity_reset(const __grid_constant__ DevMesh m, DevCands c, NArg na, u32 rs,
                                const u32* __restrict__ regions,
                                const u32* __restrict__ region_len, u64* __restrict__ ckey,
                                u64* __restrict__ ctie, u64* __restrict__ fkey,
-                               u64* __restrict__ ftie) {
+                               u64* __restrict__ ftie, InsertBufs plan, u64 depth_cap,
+                               Counters* ctr) {
     const u32 n = narg(na);
+    u32 dropped = 0;
     GRID_STRIDE(i, n) {
         cavity_reset_one(i, rs, regions, region_len, ckey, ctie);
-        if (fkey) rw_reset_one(c, i, nT, fkey, ftie);
+        if (fkey) rw_reset_one(c, i, m.nT, fkey, ftie);
+        if (plan.nv) {
+            u32 nv, nt, ns;
+            dropped += plan_one(m, c, i, depth_cap, nv, nt, ns);
+            plan.nv[i] = nv;
+            plan.nt[i] = nt;
+            plan.ns[i] = ns;
+        }
     }
+    if (plan.nv) warp_add_u32(&ctr->dropped, dropped);
 }
 
 // ---- isolated claims (GDP2D_INSERT_ISOLATED, gdp2d_phases.cuh) ----
@@ -160,12 +173,12 @@ void launch_cavity_isolated(const DevMesh& m, DevCands c, NArg n, u32 ncav, u32 
     note_launch(), k_cavity_tie<<<g, 256, 0, st>>>(c, n, rs, regions, region_len, a.ckey, a.ctie);
     note_launch(), k_rw_tie<<<g, 256, 0, st>>>(c, n, a.fkey, a.ftie);
     note_launch(), k_isolated_check<<<g, 256, 0, st>>>(m, c, n, rs, regions, region_len, a.ckey, a.ctie, a.fkey, a.ftie, unsafe_flag, d_ctr);
-    note_launch(), k_cavity_reset<<<g, 256, 0, st>>>(c, n, m.nT, rs, regions, region_len, a.ckey, a.ctie, a.fkey, a.ftie);
+    note_launch(), k_cavity_reset<<<g, 256, 0, st>>>(m, c, n, rs, regions, region_len, a.ckey, a.ctie, a.fkey, a.ftie, InsertBufs{}, 0, d_ctr);
 }
 
 void launch_cavity(const DevMesh& m, DevCands c, NArg n, u32 ncav, int extras, TriAux a,
                    u32* regions, u32* region_len, u32* bfs_len, Counters* d_ctr,
-                   cudaStream_t st) {
+                   cudaStream_t st, const InsertBufs* plan, u64 depth_cap) {
     if (!n.grid_n) return;
     const u32 rs = ncav + 1 + MAX_CLAIM_EXTRA;
     const bool rw = extras >= 2;   // refinement: the rewrite table
@@ -178,9 +191,11 @@ void launch_cavity(const DevMesh& m, DevCands c, NArg n, u32 ncav, int extras, T
     note_launch(), k_cavity_check<<<g, 256, 0, st>>>(c, n, rs, regions, region_len, a.ckey, a.ctie,
                                                      rw ? a.fkey : nullptr, rw ? a.ftie : nullptr,
                                                      d_ctr);
-    note_launch(), k_cavity_reset<<<g, 256, 0, st>>>(c, n, m.nT, rs, regions, region_len, a.ckey,
+    note_launch(), k_cavity_reset<<<g, 256, 0, st>>>(m, c, n, rs, regions, region_len, a.ckey,
                                                      a.ctie, rw ? a.fkey : nullptr,
-                                                     rw ? a.ftie : nullptr);
+                                                     rw ? a.ftie : nullptr,
+                                                     plan ? *plan : InsertBufs{}, depth_cap,
+                                                     d_ctr);
 }
 
 // Little's law against measured occupancy: the number of candidates the

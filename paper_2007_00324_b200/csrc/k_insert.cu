@@ -668,6 +668,7 @@ struct InsertArgs {
     u32 small_c;          // block mode for the whole batch when C <= small_c
     int resume;           // 1: candidates are planned, start at the capacity check
     int prefiltered;      // standalone Lines 5-7 ran (for C > small_c)
+    int planned;          // ... including the phase-1 plan (b.nv / nt / ns written)
     u32 reg_cap;          // candidates the region buffers hold
     int isolate;          // claims: 0 reference, 1 isolated (rollback only if state[8]), 2 precedence
     int dep_mis;          // dependent pairs: 1 = priority-MIS rule, 0 = any-higher-neighbour rule
@@ -872,7 +873,9 @@ __device__ void filter(const InsertArgs& a, const Exec& ex, u32 C) {
     warp_add_u32(&a.ctr->surv_cavity, surv2);
 }
 
-__device__ void plan_and_scan(const InsertArgs& a, const Exec& ex, u32 C) {
+// planned: the standalone filter already wrote b.nv / nt / ns (and counted
+// the dropped candidates); only the scan is left.
+__device__ void plan_and_scan(const InsertArgs& a, const Exec& ex, u32 C, bool planned) {
     const DevMesh& m = a.m;
     u32 dropped = 0;
 
@@ -886,10 +889,16 @@ __device__ void plan_and_scan(const InsertArgs& a, const Exec& ex, u32 C) {
     unsigned long long local = 0;
     for (u32 i = lo + threadIdx.x; i < hi; i += INSERT_BLOCK) {
         u32 nv, nt, ns;
-        dropped += plan_one(m, a.c, i, a.depth_cap, nv, nt, ns);
-        a.b.nv[i] = nv;
-        a.b.nt[i] = nt;
-        a.b.ns[i] = ns;
+        if (planned) {
+            nv = a.b.nv[i];
+            nt = a.b.nt[i];
+            ns = a.b.ns[i];
+        } else {
+            dropped += plan_one(m, a.c, i, a.depth_cap, nv, nt, ns);
+            a.b.nv[i] = nv;
+            a.b.nt[i] = nt;
+            a.b.ns[i] = ns;
+        }
         local += (unsigned long long)nv | ((unsigned long long)(nt - nv) << 21) |
                  ((unsigned long long)(ns >> 1) << 42);
     }
@@ -1186,8 +1195,9 @@ __global__ void __launch_bounds__(INSERT_BLOCK, GDP2D_SPLIT_MINB) k_batch_split(
     const Exec ex = block ? block_exec(sring) : grid_exec(a.ring);
     if (!a.resume) {
         trace(a, ex.leader(), TR_START);
-        if (block || !a.prefiltered) filter<MODE>(a, ex, C);
-        plan_and_scan(a, ex, C);
+        const bool here = block || !a.prefiltered;   // Lines 5-7 in this kernel
+        if (here) filter<MODE>(a, ex, C);
+        plan_and_scan(a, ex, C, !here && a.planned);
     }
     const u32 nv = vload(&a.b.totals[0]), nt = vload(&a.b.totals[1]), ns = vload(&a.b.totals[2]);
     if (!fits_and_status(a, nv, nt, ns)) return;   // uniform
@@ -1258,6 +1268,7 @@ static InsertArgs make_args(const InsertLaunch& L) {
     a.small_c = L.small_c;
     a.resume = L.resume;
     a.prefiltered = L.prefiltered;
+    a.planned = L.planned;
     a.reg_cap = L.reg_cap;
     a.isolate = L.isolate;
     a.dep_mis = L.dep_mis;
