@@ -421,6 +421,8 @@ struct gdp2d_ctx {
     bool dep_mis = false;         // GDP2D_DEP=mis: dependent pairs by the priority-MIS rule
     bool check = false;           // GDP2D_CHECK=1: validate after each insertion kernel
     u32* scan_part = nullptr;     // [3 * insert_grid] plan chunk sums
+    u32* small_list = nullptr;    // [SMALL_LIST_CAP] + count: the small-list collect
+    u32 small_collect_c = 2048;   // GDP2D_SMALL_COLLECT: previous batch at or below -> small-list collect
     RoundCtr* rcs = nullptr;      // per-round counters of the persistent kernel
     u32* d_res = nullptr;
     u32* d_val = nullptr;
@@ -682,6 +684,9 @@ void ctx_init(gdp2d_ctx* x, int device) {
     if (const char* e = std::getenv("GDP2D_DEP")) x->dep_mis = std::string(e) == "mis";
     if (const char* e = std::getenv("GDP2D_CHECK")) x->check = e[0] == '1';
     dalloc(x->scan_part, 3ull * x->insert_grid + 3);
+    dalloc(x->small_list, SMALL_LIST_CAP + 1);
+    CK(cudaMemsetAsync(x->small_list + SMALL_LIST_CAP, 0, sizeof(u32), x->st));
+    if (const char* e = std::getenv("GDP2D_SMALL_COLLECT")) x->small_collect_c = (u32)std::atoll(e);
     const char* fc = std::getenv("GDP2D_COLLECT");
     x->full_collect = fc && std::string(fc) == "full";
     dalloc(x->rcs, 1024);
@@ -723,6 +728,7 @@ void ctx_release(gdp2d_ctx* x) {
     dfree(x->d_res);
     dfree(x->ring);
     dfree(x->scan_part);
+    dfree(x->small_list);
     {
         auto& c = x->cdt;
         dfree(c.ptri); dfree(c.pedge); dfree(c.pother); dfree(c.pkey); dfree(c.pwin);
@@ -1250,9 +1256,12 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
         const bool ncs = !x->sync_collect && x->have_c_prev &&
                          p->rule4_unified_collection != 0 && p->batch_size_cap == 0 &&
                          !little_sync;
+        const bool small = ncs && x->c_prev <= x->small_collect_c;
         u32 C = launch_collect(m, q, p->rule4_unified_collection != 0, x->flags, x->c, x->ccap,
                                x->scan, x->d_ctr, st, cache, &tris_scanned, x->d_C,
-                               nullptr, ncs ? nullptr : x->ev[GDP2D_NPHASES + 3], !ncs);
+                               nullptr, ncs ? nullptr : x->ev[GDP2D_NPHASES + 3], !ncs,
+                               small ? x->small_list : nullptr,
+                               small ? x->small_list + SMALL_LIST_CAP : nullptr);
         // the no-round-trip collect is timed to ev[1], scatter included (one
         // event record less per batch)
         const cudaEvent_t scan_end = ncs ? x->ev[1] : x->ev[GDP2D_NPHASES + 3];
@@ -1332,10 +1341,11 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
                                    standalone ? x->ev[5] : x->ev[1])) {
                 // the list outgrew the region buffers: grow them, redo the batch
                 // (collect recomputes the same list from its cached verdicts)
-                // (the redo takes the synchronous path: it knows C exactly)
-                ensure_regions(x, x->h_tot[3], ncav, rs);
+                // (the redo takes the synchronous path: it knows C exactly);
+                // C = NONE: the small-list collect overflowed, nothing to grow
+                if (x->h_tot[3] != NONE) ensure_regions(x, x->h_tot[3], ncav, rs);
                 --x->epoch;
-                x->c_prev = x->h_tot[3];
+                x->c_prev = x->h_tot[3] != NONE ? x->h_tot[3] : x->c_prev;
                 x->have_c_prev = false;
                 --iter;
                 continue;

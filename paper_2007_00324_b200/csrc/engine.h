@@ -70,7 +70,12 @@ u32 launch_collect(const DevMesh& m, const Quality& q, bool rule4, uint8_t* flag
                    u32 ccap, ScanScratch& s, Counters* d_ctr, cudaStream_t st,
                    const CollectCache& cache, bool* tris_scanned, u32* d_count,
                    cudaEvent_t ev_scan0 = nullptr,
-                   cudaEvent_t ev_scan1 = nullptr, bool sync = true);
+                   cudaEvent_t ev_scan1 = nullptr, bool sync = true,
+                   u32* small_list = nullptr, u32* small_list_n = nullptr);
+// small_list (SMALL_LIST_CAP keys) + small_list_n (zeroed): the no-round-trip
+// collect of a small list (k_collect_append + k_collect_small, k_collect.cu);
+// *d_count = NONE when the list outgrew it.
+constexpr u32 SMALL_LIST_CAP = 4096;
 void launch_split_points(const DevMesh& m, DevCands c, u32 n, Counters* d_ctr, cudaStream_t st);
 // batch_size_cap (refine.hpp:252-261): keep the k highest-priority alive
 // candidates of the list (others marked dead), device-side radix select.

@@ -139,6 +139,31 @@ __device__ __forceinline__ double2 split_point(const DevMesh& m, int kind, u32 i
     return midpoint2(v3[nxt(best)], v3[prv(best)]);
 }
 
+// One candidate record (refine.hpp:236-248 + compute_splitting_points):
+// list position o, element i of kind 0 (subsegment) / 1 (triangle).
+__device__ __forceinline__ u32 write_candidate(const DevMesh& m, const DevCands& c, u32 o,
+                                               int kind, u32 i) {
+    uint8_t fb;
+    c.pt[o] = split_point(m, kind, i, fb);
+    double measure;
+    if (kind == 0) {
+        measure = subseg_len(m, i);
+    } else {
+        const uint4 tv = m.tv[i];
+        measure = area_pts(m.xy[tv.x], m.xy[tv.y], m.xy[tv.z]);
+    }
+    c.key[o] = make_key(kind == 0 ? 1 : 0, measure);
+    c.id[o] = i;
+    c.tie[o] = o;
+    c.loc[o] = PENDING;
+    c.kind[o] = (uint8_t)kind;
+    c.alive[o] = 1;
+    c.lkind[o] = 0;
+    c.ledge[o] = -1;
+    c.fb[o] = fb;
+    return fb;
+}
+
 __global__ void __launch_bounds__(SCAN_BLOCK) k_collect_scatter(DevMesh m, CollectRange r,
                                                              const uint8_t* __restrict__ flags,
                                                              const u32* __restrict__ partial,
@@ -160,43 +185,172 @@ __global__ void __launch_bounds__(SCAN_BLOCK) k_collect_scatter(DevMesh m, Colle
     const int kind = is_sub ? 0 : 1;
     for (int j = 0; j < SCAN_ITEMS; ++j) {
         if (!((f8 >> (8 * j)) & 1ull)) continue;
-        const u32 i = i0 + j;
-        if (o < ccap) {
-            uint8_t fb;
-            c.pt[o] = split_point(m, kind, i, fb);
-            nfb += fb;
-            double measure;
-            if (is_sub) {
-                measure = subseg_len(m, i);
-            } else {
-                const uint4 tv = m.tv[i];
-                measure = area_pts(m.xy[tv.x], m.xy[tv.y], m.xy[tv.z]);
-            }
-            c.key[o] = make_key(is_sub ? 1 : 0, measure);
-            c.id[o] = i;
-            c.tie[o] = o;
-            c.loc[o] = PENDING;
-            c.kind[o] = (uint8_t)kind;
-            c.alive[o] = 1;
-            c.lkind[o] = 0;
-            c.ledge[o] = -1;
-            c.fb[o] = fb;
-        }
+        if (o < ccap) nfb += write_candidate(m, c, o, kind, i0 + j);
         ++o;
     }
     warp_add_u32(&ctr->fallbacks, nfb);
 }
 
+// ---- small lists (the tail of a refinement) -------------------------------------
+//
+// When the previous batch had at most SMALL_LIST candidates, the flags pass
+// appends the candidate elements' keys (bit 31 = triangle, then the id: the
+// list order of refine.hpp:226-263, subsegments first, each by id) to a
+// short unordered list instead of writing a flag per element, and ONE CTA
+// sorts it and writes the records -- two launches instead of flags + scan +
+// scatter over every tile of a 20M-triangle mesh.  Same list, same records.
+// A list that outgrew SMALL_LIST sets the count to NONE: every filter kernel
+// and the insertion kernel then skip the batch, and the host redoes it with
+// the full collect.
+constexpr u32 SMALL_LIST = SMALL_LIST_CAP;
+constexpr int SMALL_BLOCK = 1024;
+
+template <int MODE>
+__global__ void __launch_bounds__(SCAN_BLOCK) k_collect_append(DevMesh m, Quality q, CollectRange r,
+                                                            u32* __restrict__ list,
+                                                            u32* __restrict__ list_n, int full,
+                                                            Counters* ctr, u32* z0, u32 n0,
+                                                            u32* z1, u32 n1) {
+    __shared__ u32 sh[SCAN_BLOCK / 32 + 1];
+    if (blockIdx.x == 0) {
+        for (u32 k = threadIdx.x; k < n0; k += blockDim.x) z0[k] = 0;
+        for (u32 k = threadIdx.x; k < n1; k += blockDim.x) z1[k] = 0;
+    }
+    const bool is_sub = blockIdx.x < r.tilesS;
+    const u32 tile = is_sub ? blockIdx.x : blockIdx.x - r.tilesS;
+    const u32 n = is_sub ? r.nS : r.nT;
+    const u32 i0 = tile * (u32)SCAN_TILE + threadIdx.x * (u32)SCAN_ITEMS;
+    u32 dirty = 0;
+    unsigned long long out = 0;
+    if (!is_sub && !full && i0 + SCAN_ITEMS <= n) {
+        unsigned long long v = *reinterpret_cast<const unsigned long long*>(m.tflag + i0);
+        if (v & 0x0202020202020202ull) {
+#pragma unroll
+            for (int j = 0; j < SCAN_ITEMS; ++j) {
+                const uint8_t tf = (uint8_t)(v >> (8 * j));
+                if (tf & 2) {
+                    const uint8_t f = eval_tri(m, q, i0 + j);
+                    ++dirty;
+                    v = (v & ~(0xFFull << (8 * j))) | ((unsigned long long)f << (8 * j));
+                }
+            }
+        }
+        out = v & 0x0101010101010101ull;
+    } else {
+        for (int j = 0; j < SCAN_ITEMS; ++j) {
+            const u32 i = i0 + j;
+            if (i >= n) break;
+            uint8_t f;
+            if (is_sub) {
+                f = eval_sub<MODE>(m, i, full, dirty);
+            } else {
+                const uint8_t tf = full ? 2 : m.tflag[i];
+                if (tf & 2) {
+                    f = eval_tri(m, q, i);
+                    ++dirty;
+                } else {
+                    f = tf & 1;
+                }
+            }
+            out |= (unsigned long long)f << (8 * j);
+        }
+    }
+    const u32 cnt = __popcll(out);
+    if (__any_sync(0xFFFFFFFFu, cnt != 0)) {
+        // warp-aggregated append
+        u32 pre = cnt;
+        for (int d = 1; d < 32; d <<= 1) {
+            const u32 y = __shfl_up_sync(0xFFFFFFFFu, pre, d);
+            if ((threadIdx.x & 31) >= (u32)d) pre += y;
+        }
+        const u32 wtot = __shfl_sync(0xFFFFFFFFu, pre, 31);
+        u32 base = 0;
+        if ((threadIdx.x & 31) == 31) base = atomicAdd(list_n, wtot);
+        base = __shfl_sync(0xFFFFFFFFu, base, 31) + pre - cnt;
+        const u32 kbit = is_sub ? 0u : 0x80000000u;
+        for (int j = 0; j < SCAN_ITEMS; ++j)
+            if ((out >> (8 * j)) & 1ull) {
+                if (base < SMALL_LIST) list[base] = kbit | (i0 + j);
+                ++base;
+            }
+    }
+    const u32 t = block_sum<SCAN_BLOCK>(dirty, sh);
+    if (threadIdx.x == 0 && t) atomicAdd(&ctr->scan_dirty, t);
+}
+
+// One CTA: sort the appended keys (bitonic, in shared memory) and write the
+// candidate records in list order.
+__global__ void __launch_bounds__(SMALL_BLOCK) k_collect_small(DevMesh m, u32* __restrict__ list,
+                                                            u32* __restrict__ list_n, DevCands c,
+                                                            u32 ccap, u32* __restrict__ d_count,
+                                                            Counters* ctr) {
+    __shared__ u32 key[SMALL_LIST];
+    const u32 n = *list_n;
+    if (n > SMALL_LIST || n > ccap) {
+        if (threadIdx.x == 0) {
+            *d_count = NONE;   // the host redoes the batch (full collect)
+            *list_n = 0;
+        }
+        return;
+    }
+    u32 np = 1;
+    while (np < n) np <<= 1;
+    for (u32 k = threadIdx.x; k < np; k += blockDim.x) key[k] = k < n ? list[k] : NONE;
+    __syncthreads();
+    for (u32 size = 2; size <= np; size <<= 1)
+        for (u32 stride = size >> 1; stride > 0; stride >>= 1) {
+            for (u32 k = threadIdx.x; k < np / 2; k += blockDim.x) {
+                const u32 lo = 2 * k - (k & (stride - 1));
+                const u32 hi = lo + stride;
+                const bool up = (lo & size) == 0;
+                const u32 a = key[lo], b = key[hi];
+                if ((a > b) == up) {
+                    key[lo] = b;
+                    key[hi] = a;
+                }
+            }
+            __syncthreads();
+        }
+    u32 nfb = 0;
+    for (u32 o = threadIdx.x; o < n; o += blockDim.x) {
+        const u32 k = key[o];
+        nfb += write_candidate(m, c, o, k >> 31 ? 1 : 0, k & 0x7FFFFFFFu);
+    }
+    warp_add_u32(&ctr->fallbacks, nfb);
+    if (threadIdx.x == 0) {
+        *d_count = n;
+        *list_n = 0;   // ready for the next batch
+    }
+}
+
 u32 launch_collect(const DevMesh& m, const Quality& q, bool rule4, uint8_t* flags, DevCands c,
                    u32 ccap, ScanScratch& s, Counters* d_ctr, cudaStream_t st,
                    const CollectCache& cache, bool* tris_scanned, u32* d_count,
-                   cudaEvent_t ev_scan0, cudaEvent_t ev_scan1, bool sync) {
+                   cudaEvent_t ev_scan0, cudaEvent_t ev_scan1, bool sync, u32* small_list,
+                   u32* small_list_n) {
     *tris_scanned = false;
     u32 *zp0 = cache.zero[0], *zp1 = cache.zero[1];
     u32 zn0 = cache.zero_n[0], zn1 = cache.zero_n[1];
     // sync == false (rule 4 only): no host round trip -- the scatter runs
     // unconditionally and the count stays on the device (*d_count)
     if (!sync && !rule4) sync = true;
+    if (!sync && small_list && small_list_n && m.nS + m.nT > 0) {
+        // the previous batch was small: append + one-CTA sort (see above)
+        *tris_scanned = true;
+        CollectRange r;
+        r.nS = m.nS;
+        r.nT = m.nT;
+        r.tilesS = (r.nS + SCAN_TILE - 1) / SCAN_TILE;
+        r.tilesT = (r.nT + SCAN_TILE - 1) / SCAN_TILE;
+        const u32 tiles = r.tilesS + r.tilesT;
+        if (ev_scan0) cudaEventRecord(ev_scan0, st);
+        if (q.mode == 0)
+            note_launch(), k_collect_append<0><<<tiles, SCAN_BLOCK, 0, st>>>(m, q, r, small_list, small_list_n, cache.full, d_ctr, zp0, zn0, zp1, zn1);
+        else
+            note_launch(), k_collect_append<1><<<tiles, SCAN_BLOCK, 0, st>>>(m, q, r, small_list, small_list_n, cache.full, d_ctr, zp0, zn0, zp1, zn1);
+        note_launch(), k_collect_small<<<1, SMALL_BLOCK, 0, st>>>(m, small_list, small_list_n, c, ccap, d_count, d_ctr);
+        return NONE;
+    }
     auto run = [&](bool sub, bool tri) -> u32 {
         if (tri) *tris_scanned = true;
         CollectRange r;

@@ -158,14 +158,17 @@ def test_collect_round_trip_paths_identical(built, monkeypatch):
     """The candidate count stays on the device between collect and insertion;
     the synchronous path (GDP2D_SYNC_COLLECT=1) and the region-overflow redo
     (GDP2D_REGIONS_TIGHT=1 makes every no-round-trip batch overflow and redo)
-    must give bit-identical meshes."""
+    must give bit-identical meshes.  So must the small-list collect (append +
+    one-CTA sort) switched off (GDP2D_SMALL_COLLECT=0) or forced onto every
+    no-round-trip batch, big ones overflowing into the full-collect redo."""
     from paper_2007_00324_b200 import Engine, QualityCriteria, host
     pts, segs = host.generate_pslg(40_000, 4_000, "gaussian", 13)
     m, closed = host.build_cdt(pts, segs)
     q = QualityCriteria(B_SQRT2_THETA)
     outs = []
-    for env in ({}, {"GDP2D_SYNC_COLLECT": "1"}, {"GDP2D_REGIONS_TIGHT": "1"}):
-        for k in ("GDP2D_SYNC_COLLECT", "GDP2D_REGIONS_TIGHT"):
+    for env in ({}, {"GDP2D_SYNC_COLLECT": "1"}, {"GDP2D_REGIONS_TIGHT": "1"},
+                {"GDP2D_SMALL_COLLECT": "0"}, {"GDP2D_SMALL_COLLECT": "1000000000"}):
+        for k in ("GDP2D_SYNC_COLLECT", "GDP2D_REGIONS_TIGHT", "GDP2D_SMALL_COLLECT"):
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)
