@@ -1027,6 +1027,7 @@ void check_structure_now(gdp2d_ctx* x, u32 nV, u32 nT, u32 nS, const char* where
     m.nV = nV + x->h_tot[0];
     m.nT = nT + x->h_tot[1];
     m.nS = nS + x->h_tot[2];
+    launch_vtri_rebuild(m, x->st);   // batches keep vert_tri for fresh vertices only
     launch_validate(m, x->d_val, x->st);
     u32 h[4];
     CK(cudaMemcpyAsync(h, x->d_val, sizeof h, cudaMemcpyDeviceToHost, x->st));
@@ -1079,6 +1080,7 @@ bool insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, int prefiltered, u32
         L.w.fresh_cc = x->fresh.cc;
         L.w.fresh_v0 = x->work.m.nV;          // fresh ids start here ...
         L.w.fresh_n = x->fresh.cap;           // ... and never exceed the buffer
+        L.w.vtri_from = x->work.m.nV;         // vert_tri kept for the fresh ids only
         L.ring = x->ring;
         L.state = x->ins_state;
         L.ctr = x->d_ctr;
@@ -1429,6 +1431,8 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
         r->sum_subsegs_alive += bm.subsegs_alive;
         if (retained == 0 && h.marked == 0) break;
     }
+    // the batches kept vert_tri for their own fresh vertices only
+    launch_vtri_rebuild(x->work.m, st);
     CK(cudaEventRecord(x->ev[GDP2D_NPHASES], st));
     CK(cudaEventSynchronize(x->ev[GDP2D_NPHASES]));
     if (const char* dbg = std::getenv("GDP2D_DEBUG"); dbg && dbg[0] == '1') {

@@ -172,6 +172,11 @@ struct WorkLists {
     uint8_t* vdirty = nullptr;
     const uint8_t* fresh_cc = nullptr;   // FreshInfo::cc
     u32 fresh_v0 = 0, fresh_n = 0;
+    // vert_tri is maintained for vertex ids >= vtri_from only (0 = every
+    // vertex).  A refinement batch reads vert_tri of its own fresh vertices
+    // alone (detection and removal stars), so it passes its first fresh id and
+    // refine_loop rebuilds the whole array once at the end (launch_vtri_rebuild).
+    u32 vtri_from = 0;
 };
 
 // The whole Lawson fixpoint as one persistent cooperative kernel (see
@@ -256,6 +261,8 @@ void launch_export(const DevMesh& m, u32* fv, u32* ov, u32* ft, u32* ot, double2
 
 // Debug structural validator (out: 4 u32 device words).
 void launch_validate(const DevMesh& m, u32* out, cudaStream_t st);
+// vert_tri of every vertex = its lowest alive incident triangle (k_misc.cu).
+void launch_vtri_rebuild(const DevMesh& m, cudaStream_t st);
 
 // Line 1 on the device (k_cdt.cu): Delaunay triangulation of the input
 // points inside a super triangle (vertices N..N+2), then segment recovery by

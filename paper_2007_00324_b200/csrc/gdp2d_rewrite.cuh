@@ -18,17 +18,19 @@ namespace gdp2d {
 
 // ---- shared phase-A helpers ----------------------------------------------------
 
+// vfrom: vert_tri is invalidated only for corner ids >= vfrom (WorkLists::vtri_from)
 __device__ __forceinline__ void write_tri(const DevMesh& m, u32 t, u32 a, u32 b, u32 c, u32 n0,
-                                          u32 n1, u32 n2, u32 pend, u32 s0, u32 s1, u32 s2) {
+                                          u32 n1, u32 n2, u32 pend, u32 s0, u32 s1, u32 s2,
+                                          u32 vfrom = 0) {
     const u32 fl = tri_flags(s0, s1, s2);
     m.tv[t] = make_uint4(a, b, c, fl);
     m.tn[t] = make_uint4(n0, n1, n2, pend);
     // ts is read only behind the tv.w subsegment bits (load_ts / has_seg)
     if (fl != 1u) m.ts[t] = make_uint4(s0, s1, s2, 0u);
     m.tflag[t] = 2;
-    m.vtri[a] = NONE;
-    m.vtri[b] = NONE;
-    m.vtri[c] = NONE;
+    if (a >= vfrom) m.vtri[a] = NONE;
+    if (b >= vfrom) m.vtri[b] = NONE;
+    if (c >= vfrom) m.vtri[c] = NONE;
     if (s0 != NONE) m.stri[s0] = NONE, m.sflag[s0] = 2;
     if (s1 != NONE) m.stri[s1] = NONE, m.sflag[s1] = 2;
     if (s2 != NONE) m.stri[s2] = NONE, m.sflag[s2] = 2;
@@ -61,9 +63,9 @@ static __device__ void split_triangle_A(const DevMesh& m, const TriAux& x, const
                                  int seed = 0, Counters* ctr = nullptr) {
     const uint4 ov = m.tv[t], on = m.tn[t], os = load_ts(m, t, ov);
     x.stamp[t] = round;
-    write_tri(m, t, ov.x, ov.y, wv, enc(t1, 1), enc(t2, 0), on.z, 4u, NONE, NONE, os.z);
-    write_tri(m, t1, ov.y, ov.z, wv, enc(t2, 1), enc(t, 0), on.x, 4u, NONE, NONE, os.x);
-    write_tri(m, t2, ov.z, ov.x, wv, enc(t, 1), enc(t1, 0), on.y, 4u, NONE, NONE, os.y);
+    write_tri(m, t, ov.x, ov.y, wv, enc(t1, 1), enc(t2, 0), on.z, 4u, NONE, NONE, os.z, w.vtri_from);
+    write_tri(m, t1, ov.y, ov.z, wv, enc(t2, 1), enc(t, 0), on.x, 4u, NONE, NONE, os.x, w.vtri_from);
+    write_tri(m, t2, ov.z, ov.x, wv, enc(t, 1), enc(t1, 0), on.y, 4u, NONE, NONE, os.y, w.vtri_from);
     x.emap[3 * t + 0] = enc(t1, 2);
     x.emap[3 * t + 1] = enc(t2, 2);
     x.emap[3 * t + 2] = enc(t, 2);
@@ -90,9 +92,9 @@ static __device__ void split_edge_A(const DevMesh& m, const TriAux& x, const Wor
     if (uc == NONE) {
         // t := (a,b,w) {-, t2, n_prev}, t2 := (a,w,c) {-, n_next, t}
         write_tri(m, t, a, b, wv, NONE, enc(t2, 2), comp(on, prv(e)), 4u, s_bw, NONE,
-                  comp(os, prv(e)));
+                  comp(os, prv(e)), w.vtri_from);
         write_tri(m, t2, a, wv, c, NONE, comp(on, nxt(e)), enc(t, 1), 2u, s_wc,
-                  comp(os, nxt(e)), NONE);
+                  comp(os, nxt(e)), NONE, w.vtri_from);
         x.emap[3 * t + nxt(e)] = enc(t2, 1);
         x.emap[3 * t + prv(e)] = enc(t, 2);
         x.emap[3 * t + e] = NONE;
@@ -116,14 +118,14 @@ static __device__ void split_edge_A(const DevMesh& m, const TriAux& x, const Wor
     x.stamp[u] = round;
     // t := (a,b,w) {u2, t2, n_ab}; t2 := (a,w,c) {u, n_ca, t}
     write_tri(m, t, a, b, wv, enc(u2, 0), enc(t2, 2), comp(on, prv(e)), 4u, s_bw, NONE,
-              comp(os, prv(e)));
+              comp(os, prv(e)), w.vtri_from);
     write_tri(m, t2, a, wv, c, enc(u, 0), comp(on, nxt(e)), enc(t, 1), 2u, s_wc,
-              comp(os, nxt(e)), NONE);
+              comp(os, nxt(e)), NONE, w.vtri_from);
     // u := (d,c,w) {t2, u2, n_dc}; u2 := (d,w,b) {t, n_bd, u}
     write_tri(m, u, d, c, wv, enc(t2, 0), enc(u2, 2), comp(un, prv(f)), 4u, s_wc, NONE,
-              comp(us, prv(f)));
+              comp(us, prv(f)), w.vtri_from);
     write_tri(m, u2, d, wv, b, enc(t, 0), comp(un, nxt(f)), enc(u, 1), 2u, s_bw,
-              comp(us, nxt(f)), NONE);
+              comp(us, nxt(f)), NONE, w.vtri_from);
     x.emap[3 * t + nxt(e)] = enc(t2, 1);
     x.emap[3 * t + prv(e)] = enc(t, 2);
     x.emap[3 * t + e] = NONE;
@@ -172,9 +174,9 @@ __device__ __forceinline__ void fixup_one(const DevMesh& m, u32 round, const Tri
     }
     tn.w = 0;
     m.tn[t] = tn;
-    atomicMin(&m.vtri[tv.x], t);
-    atomicMin(&m.vtri[tv.y], t);
-    atomicMin(&m.vtri[tv.z], t);
+    if (tv.x >= w.vtri_from) atomicMin(&m.vtri[tv.x], t);
+    if (tv.y >= w.vtri_from) atomicMin(&m.vtri[tv.y], t);
+    if (tv.z >= w.vtri_from) atomicMin(&m.vtri[tv.z], t);
     if (w.vdirty) {
         // Suspects for the redundancy detection (refine.hpp:551-608): a
         // same-batch circumcenter can only be redundant as the apex of a
@@ -279,9 +281,9 @@ __device__ __forceinline__ u32 flip_apply_one(const DevMesh& m, u32 i, u32 round
         return 0;
     }
     write_tri(m, t, a, b, d, comp(un, nxt(f)), enc(u, 2), comp(tn, prv(e)), 5u,
-              comp(us, nxt(f)), NONE, comp(ts, prv(e)));
+              comp(us, nxt(f)), NONE, comp(ts, prv(e)), w.vtri_from);
     write_tri(m, u, a, d, c, comp(un, prv(f)), comp(tn, nxt(e)), enc(t, 1), 3u,
-              comp(us, prv(f)), comp(ts, nxt(e)), NONE);
+              comp(us, prv(f)), comp(ts, nxt(e)), NONE, w.vtri_from);
     x.emap[3 * t + nxt(e)] = enc(u, 1);
     x.emap[3 * t + prv(e)] = enc(t, 2);
     x.emap[3 * t + e] = NONE;

@@ -556,7 +556,7 @@ __device__ __noinline__ u32 rm_apply_one(const DevMesh& m, const u32* __restrict
                     const u32 pend = (CK[ci][0] == 1 ? 1u : 0u) | (CK[ci][1] == 1 ? 2u : 0u) |
                                      (CK[ci][2] == 1 ? 4u : 0u);
                     write_tri(m, st[ci], CV[ci][0], CV[ci][1], CV[ci][2], CN[ci][0], CN[ci][1],
-                              CN[ci][2], pend, CS[ci][0], CS[ci][1], CS[ci][2]);
+                              CN[ci][2], pend, CS[ci][0], CS[ci][1], CS[ci][2], w.vtri_from);
                 }
                 u32* tv_words = reinterpret_cast<u32*>(m.tv);
                 for (int q = created; q < k; ++q) {

@@ -257,4 +257,22 @@ void launch_validate(const DevMesh& m, u32* out, cudaStream_t st) {
     if (m.nT) note_launch(), k_validate<<<(m.nT + 255) / 256, 256, 0, st>>>(m, out);
 }
 
+// vert_tri rebuilt from scratch: the lowest alive incident triangle id of every
+// vertex (Mesh::vert_tri, mesh.hpp:73; refinement batches maintain it only for
+// their fresh vertices, WorkLists::vtri_from).
+__global__ void k_vtri_min(DevMesh m) {
+    const u32 t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= m.nT) return;
+    const uint4 tv = m.tv[t];
+    if (!tv.w) return;
+    atomicMin(&m.vtri[tv.x], t);
+    atomicMin(&m.vtri[tv.y], t);
+    atomicMin(&m.vtri[tv.z], t);
+}
+
+void launch_vtri_rebuild(const DevMesh& m, cudaStream_t st) {
+    if (m.nV) cudaMemsetAsync(m.vtri, 0xFF, 4ull * m.nV, st);
+    if (m.nT) note_launch(), k_vtri_min<<<(m.nT + 255) / 256, 256, 0, st>>>(m);
+}
+
 }  // namespace gdp2d
