@@ -683,6 +683,7 @@ void ctx_init(gdp2d_ctx* x, int device) {
     if (const char* e = std::getenv("GDP2D_SMALL_C")) x->small_c = (u32)std::strtoul(e, nullptr, 10);
     if (const char* e = std::getenv("GDP2D_DEP")) x->dep_mis = std::string(e) == "mis";
     if (const char* e = std::getenv("GDP2D_CHECK")) x->check = e[0] == '1';
+    if (const char* e = std::getenv("GDP2D_EAR_DL_MAX")) x->wl.ear_dl_max = (u32)std::atoll(e);
     dalloc(x->scan_part, 3ull * x->insert_grid + 3);
     dalloc(x->small_list, SMALL_LIST_CAP + 1);
     CK(cudaMemsetAsync(x->small_list + SMALL_LIST_CAP, 0, sizeof(u32), x->st));

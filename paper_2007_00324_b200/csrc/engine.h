@@ -177,6 +177,7 @@ struct WorkLists {
     // alone (detection and removal stars), so it passes its first fresh id and
     // refine_loop rebuilds the whole array once at the end (launch_vtri_rebuild).
     u32 vtri_from = 0;
+    u32 ear_dl_max = 0xFFFFFFFFu;   // experiment: Delaunay-ear pass only while the polygon has <= this many vertices
 };
 
 // The whole Lawson fixpoint as one persistent cooperative kernel (see

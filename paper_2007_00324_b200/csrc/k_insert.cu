@@ -401,10 +401,15 @@ __device__ __forceinline__ void rm_claim_one(const DevMesh& m, const u32* __rest
 // (ids reused in star order), the last two die.
 // Lawson seeds of the rebuilt star go to seed_rc->wl_next (so successive
 // removal rounds can accumulate one list for a single Lawson pass).
-__device__ __noinline__ u32 rm_apply_one(const DevMesh& m, const u32* __restrict__ list, u32 i,
-                                         u32 round, u32 V0, u32 widx, u32 next_list,
-                                         const TriAux& x, const FreshInfo& f, const WorkLists& w,
-                                         RoundCtr* rc, Counters* ctr, RoundCtr* seed_rc) {
+// N: capacity of the thread-local link arrays.  The common small star runs
+// with N = 16 (a compact local frame that stays in L1); larger stars take the
+// MAX_STAR instantiation (rm_apply_one dispatches on the star size).
+template <int N>
+__device__ __noinline__ u32 rm_apply_one_n(const DevMesh& m, const u32* __restrict__ list, u32 i,
+                                           u32 round, u32 V0, u32 widx, u32 next_list,
+                                           const TriAux& x, const FreshInfo& f,
+                                           const WorkLists& w, RoundCtr* rc, Counters* ctr,
+                                           RoundCtr* seed_rc) {
     u32 done = 0;
     {
         const u32 v = list[i];
@@ -419,10 +424,10 @@ __device__ __noinline__ u32 rm_apply_one(const DevMesh& m, const u32* __restrict
             if (o < w.rm_cap) w.rm[next_list][o] = v;
         } else if (own) {
             // Link polygon, CCW: L[j] = p_j; link edge j = (L[j], L[j+1]).
-            u32 L[MAX_STAR], R[MAX_STAR], SG[MAX_STAR], ORG[MAX_STAR];
-            uint8_t PK[MAX_STAR];  // 1 = old outer ref, 2 = local (idx<<2|slot), 0 = none
-            int NX[MAX_STAR], PV[MAX_STAR];
-            double2 XY[MAX_STAR];  // link vertex coordinates, gathered once
+            u32 L[N], R[N], SG[N], ORG[N];
+            uint8_t PK[N];  // 1 = old outer ref, 2 = local (idx<<2|slot), 0 = none
+            int NX[N], PV[N];
+            double2 XY[N];  // link vertex coordinates, gathered once
             // records of the whole star first (independent loads), then the
             // link coordinates: two dependent levels instead of 2k
 #pragma unroll 4
@@ -441,10 +446,10 @@ __device__ __noinline__ u32 rm_apply_one(const DevMesh& m, const u32* __restrict
 #pragma unroll 4
             for (int q = 0; q < k; ++q) XY[q] = m.xy[L[q]];
             // created triangles (local): vertices, refs, kinds, segs
-            u32 CV[MAX_STAR][3];
-            u32 CN[MAX_STAR][3];
-            uint8_t CK[MAX_STAR][3];
-            u32 CS[MAX_STAR][3];
+            u32 CV[N][3];
+            u32 CN[N][3];
+            uint8_t CK[N][3];
+            u32 CS[N][3];
             const double2 pv = m.xy[v];
             int cnt = k, head = 0, created = 0;
             bool ok = true;
@@ -477,7 +482,7 @@ __device__ __noinline__ u32 rm_apply_one(const DevMesh& m, const u32* __restrict
                 // Pass 1 (degenerate stars only, e.g. a point that was inserted
                 // exactly on an edge): v may lie ON the new diagonal -- the
                 // final hole triangulation is still valid because v leaves.
-                for (int pass = -1; pass < 2 && !found; ++pass) {
+                for (int pass = (u32)cnt <= w.ear_dl_max ? -1 : 0; pass < 2 && !found; ++pass) {
                     j = head;
                     for (int it = 0; it < cnt; ++it) {
                         const int a = PV[j], c = NX[j];
@@ -584,6 +589,18 @@ __device__ __noinline__ u32 rm_apply_one(const DevMesh& m, const u32* __restrict
         }
     }
     return done;
+}
+
+__device__ __forceinline__ u32 rm_apply_one(const DevMesh& m, const u32* __restrict__ list, u32 i,
+                                            u32 round, u32 V0, u32 widx, u32 next_list,
+                                            const TriAux& x, const FreshInfo& f,
+                                            const WorkLists& w, RoundCtr* rc, Counters* ctr,
+                                            RoundCtr* seed_rc) {
+    if (w.star_len[i] <= 16u)
+        return rm_apply_one_n<16>(m, list, i, round, V0, widx, next_list, x, f, w, rc, ctr,
+                                  seed_rc);
+    return rm_apply_one_n<MAX_STAR>(m, list, i, round, V0, widx, next_list, x, f, w, rc, ctr,
+                                    seed_rc);
 }
 
 __device__ __forceinline__ void rm_post_one(u32 i, const TriAux& x, const WorkLists& w) {

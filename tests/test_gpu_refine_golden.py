@@ -50,9 +50,13 @@ def _pslg_sha(pts, segs) -> str:
     return h.hexdigest()[:32]
 
 
-@pytest.mark.parametrize("config", ["cfg1", "cfg2", "cfg3", "cfg4"])
-def test_refine_matches_reference_at_baseline_size(built, config):
-    from paper_2007_00324_b200 import Engine, QualityCriteria, host
+@pytest.mark.parametrize("config,insert_mode", [
+    ("cfg1", 1), ("cfg2", 1), ("cfg3", 1), ("cfg4", 1),
+    # pre-insertion encroachment precedence (GDP2D_INSERT_PRECEDENCE): the GPU
+    # design difference SURVEY 8(c) budgets inside the 10% band
+    ("cfg1", 2), ("cfg2", 2), ("cfg3", 2)])
+def test_refine_matches_reference_at_baseline_size(built, config, insert_mode):
+    from paper_2007_00324_b200 import Engine, EngineConfig, QualityCriteria, host
     gold = json.loads(GOLDEN.read_text())[config]
     pts, segs = host.generate_pslg(gold["n"], gold["m"], gold["dist"], gold["seed"])
     mesh, closed = host.build_cdt(pts, segs)
@@ -62,7 +66,7 @@ def test_refine_matches_reference_at_baseline_size(built, config):
     q = QualityCriteria(gold["theta"])
     with Engine() as eng:
         eng.upload(mesh)
-        rep = eng.refine(q)
+        rep = eng.refine(q, EngineConfig(insert_mode=insert_mode))
         v = eng.validate(q)
     assert not rep.iteration_cap_hit
     assert v["structure_failure"] == 0, v
@@ -76,7 +80,7 @@ def test_refine_matches_reference_at_baseline_size(built, config):
     assert tv <= HIST_TV_MAX, tv
     assert abs(v["mean_min_angle_deg"] - gold["mean_min_angle_deg"]) <= MEAN_ANGLE_TOL, \
         (v["mean_min_angle_deg"], gold["mean_min_angle_deg"])
-    print(f"{config}: steiner {rep.steiner_points} vs {gold['steiner_points']} ({ratio:.4f}), "
+    print(f"{config} mode {insert_mode}: steiner {rep.steiner_points} vs {gold['steiner_points']} ({ratio:.4f}), "
           f"hist TV {tv:.4f}, mean min angle {v['mean_min_angle_deg']:.3f} vs "
           f"{gold['mean_min_angle_deg']:.3f}, {len(rep.batches)} vs {gold['batches']} batches")
 
