@@ -39,7 +39,7 @@ NVFLAGS = ["-std=c++17", "-O3", "-lineinfo", "-fmad=false", "-Xcompiler", "-fPIC
 CU_SOURCES = ["k_scan.cu", "k_collect.cu", "k_locate.cu", "k_filter.cu", "k_insert.cu",
               "k_misc.cu", "k_verify.cu", "k_cdt.cu", "engine.cu"]
 HEADERS = ["gdp2d_common.cuh", "gdp2d_predicates.cuh", "gdp2d_geom.cuh", "gdp2d_phases.cuh",
-           "scan.cuh", "engine.h", "gdp2d_rewrite.cuh"]
+           "scan.cuh", "engine.h", "gdp2d_rewrite.cuh", "gdp2d_collect.cuh"]
 
 
 def _newer(target: Path, deps) -> bool:

@@ -348,6 +348,8 @@ struct LittleSizer {
     }
 };
 
+constexpr u32 kTailMax = 256;   // batches per tail-loop launch
+
 struct gdp2d_ctx {
     int device = 0;
     Tracer tr;
@@ -421,7 +423,15 @@ struct gdp2d_ctx {
     bool dep_mis = false;         // GDP2D_DEP=mis: dependent pairs by the priority-MIS rule
     bool check = false;           // GDP2D_CHECK=1: validate after each insertion kernel
     u32* scan_part = nullptr;     // [3 * insert_grid] plan chunk sums
-    u32* small_list = nullptr;    // [SMALL_LIST_CAP] + count: the small-list collect
+    u32* small_list = nullptr;    // [SMALL_LIST_WORDS]: the small-list collect (+ klist)
+    u32* dlist = nullptr;         // [DLIST_CAP] + count: the tail loop's dirty elements
+    bool dlist_on = false;        // this batch records its dirty elements
+    bool klist_ok = false;        // klist = the last collect's list (the tail loop may start)
+    bool tail_on = true;          // GDP2D_TAIL_LOOP=0: no device-resident tail loop
+    TailRec* tail_rec = nullptr;  // [kTailMax] device records + pinned mirror
+    TailRec* h_tail_rec = nullptr;
+    u32* tail_out = nullptr;      // [8] + pinned mirror
+    u32* h_tail_out = nullptr;
     u32 small_collect_c = 2048;   // GDP2D_SMALL_COLLECT: previous batch at or below -> small-list collect
     RoundCtr* rcs = nullptr;      // per-round counters of the persistent kernel
     u32* d_res = nullptr;
@@ -683,10 +693,16 @@ void ctx_init(gdp2d_ctx* x, int device) {
     if (const char* e = std::getenv("GDP2D_SMALL_C")) x->small_c = (u32)std::strtoul(e, nullptr, 10);
     if (const char* e = std::getenv("GDP2D_DEP")) x->dep_mis = std::string(e) == "mis";
     if (const char* e = std::getenv("GDP2D_CHECK")) x->check = e[0] == '1';
-    if (const char* e = std::getenv("GDP2D_EAR_DL_MAX")) x->wl.ear_dl_max = (u32)std::atoll(e);
     dalloc(x->scan_part, 3ull * x->insert_grid + 3);
-    dalloc(x->small_list, SMALL_LIST_CAP + 1);
-    CK(cudaMemsetAsync(x->small_list + SMALL_LIST_CAP, 0, sizeof(u32), x->st));
+    dalloc(x->small_list, SMALL_LIST_WORDS);
+    CK(cudaMemsetAsync(x->small_list, 0, sizeof(u32) * SMALL_LIST_WORDS, x->st));
+    dalloc(x->dlist, DLIST_CAP + 1);
+    CK(cudaMemsetAsync(x->dlist + DLIST_CAP, 0, sizeof(u32), x->st));
+    dalloc(x->tail_rec, kTailMax);
+    CK(cudaMallocHost(&x->h_tail_rec, sizeof(TailRec) * kTailMax));
+    dalloc(x->tail_out, 8);
+    CK(cudaMallocHost(&x->h_tail_out, sizeof(u32) * 8));
+    if (const char* e = std::getenv("GDP2D_TAIL_LOOP")) x->tail_on = e[0] != '0';
     if (const char* e = std::getenv("GDP2D_SMALL_COLLECT")) x->small_collect_c = (u32)std::atoll(e);
     const char* fc = std::getenv("GDP2D_COLLECT");
     x->full_collect = fc && std::string(fc) == "full";
@@ -730,6 +746,11 @@ void ctx_release(gdp2d_ctx* x) {
     dfree(x->ring);
     dfree(x->scan_part);
     dfree(x->small_list);
+    dfree(x->dlist);
+    dfree(x->tail_rec);
+    dfree(x->tail_out);
+    if (x->h_tail_rec) cudaFreeHost(x->h_tail_rec);
+    if (x->h_tail_out) cudaFreeHost(x->h_tail_out);
     {
         auto& c = x->cdt;
         dfree(c.ptri); dfree(c.pedge); dfree(c.pother); dfree(c.pkey); dfree(c.pwin);
@@ -1042,6 +1063,51 @@ void check_structure_now(gdp2d_ctx* x, u32 nV, u32 nT, u32 nS, const char* where
     }
 }
 
+// The launch record every batch kernel shares (insert_persistent, tail_loop).
+InsertLaunch base_launch(gdp2d_ctx* x, const gdp2d_params* p, u32 batch, u32 ncav, u32 rs,
+                         int isolate) {
+    InsertLaunch L;
+    L.m = x->work.m;
+    L.c = x->c;
+    L.b = x->ib;
+    L.x = x->aux;
+    L.f = x->fresh;
+    L.w = x->wl;
+    L.w.vdirty = x->fresh.dirty;          // fixup flags detection suspects
+    L.w.fresh_cc = x->fresh.cc;
+    L.w.fresh_v0 = x->work.m.nV;          // fresh ids start here ...
+    L.w.fresh_n = x->fresh.cap;           // ... and never exceed the buffer
+    L.w.vtri_from = x->work.m.nV;         // vert_tri kept for the fresh ids only
+    if (x->dlist_on) {                    // the next batch may run in the tail loop
+        L.w.dlist = x->dlist;
+        L.w.dlist_n = x->dlist + DLIST_CAP;
+        L.w.dlist_cap = DLIST_CAP;
+    }
+    L.ring = x->ring;
+    L.state = x->ins_state;
+    L.ctr = x->d_ctr;
+    L.d_C = x->d_C;
+    L.depth_cap = p->split_depth_cap;
+    L.batch = batch;
+    L.round0 = x->round + 1;
+    L.vcap = x->work.vcap;
+    L.tcap = x->work.tcap;
+    L.scap = x->work.scap;
+    L.small_nv = x->small_nv;
+    L.small_wl = x->small_wl;
+    L.max_steps = 1u << 20;
+    L.ncav = ncav;
+    L.rs = rs;
+    L.isolate = isolate;
+    L.dep_mis = x->dep_mis ? 1 : 0;
+    L.extras = 2;   // refinement claims: the rewrite table (launch_cavity)
+    L.regions = x->regions;
+    L.region_len = x->region_len;
+    L.scan_part = x->scan_part;
+    L.small_c = x->small_c;
+    return L;
+}
+
 // Insertion phase as one persistent cooperative launch (k_insert.cu): no host
 // round trip inside; the capacity check runs on the device and a batch that
 // does not fit is re-launched after growing the buffers (the mesh is not
@@ -1070,40 +1136,7 @@ bool insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, int prefiltered, u32
     int grow = 0;
     for (int attempt = 0;; ++attempt) {
         if (attempt > 0) CK(cudaMemsetAsync(x->ring, 0, 5 * sizeof(RoundCtr), st));
-        InsertLaunch L;
-        L.m = x->work.m;
-        L.c = x->c;
-        L.b = x->ib;
-        L.x = x->aux;
-        L.f = x->fresh;
-        L.w = x->wl;
-        L.w.vdirty = x->fresh.dirty;          // fixup flags detection suspects
-        L.w.fresh_cc = x->fresh.cc;
-        L.w.fresh_v0 = x->work.m.nV;          // fresh ids start here ...
-        L.w.fresh_n = x->fresh.cap;           // ... and never exceed the buffer
-        L.w.vtri_from = x->work.m.nV;         // vert_tri kept for the fresh ids only
-        L.ring = x->ring;
-        L.state = x->ins_state;
-        L.ctr = x->d_ctr;
-        L.d_C = x->d_C;
-        L.depth_cap = p->split_depth_cap;
-        L.batch = batch;
-        L.round0 = x->round + 1;
-        L.vcap = x->work.vcap;
-        L.tcap = x->work.tcap;
-        L.scap = x->work.scap;
-        L.small_nv = x->small_nv;
-        L.small_wl = x->small_wl;
-        L.max_steps = 1u << 20;
-        L.ncav = ncav;
-        L.rs = rs;
-        L.isolate = isolate;
-        L.dep_mis = x->dep_mis ? 1 : 0;
-        L.extras = 2;   // refinement claims: the rewrite table (launch_cavity)
-        L.regions = x->regions;
-        L.region_len = x->region_len;
-        L.scan_part = x->scan_part;
-        L.small_c = x->small_c;
+        InsertLaunch L = base_launch(x, p, batch, ncav, rs, isolate);
         L.resume = started ? 1 : 0;
         L.prefiltered = prefiltered;
         L.planned = prefiltered && !isolate;
@@ -1207,6 +1240,130 @@ u64 scan_alg_bytes(u64 nT, u64 nS, u64 dirty, u64 cands, bool scatter) {
     return 2 * (nT + nS) + 5 * nS + 64 * dirty + (scatter ? 105 * cands : 0);
 }
 
+// The bookkeeping of one finished batch (alive counts, record_batch metrics,
+// ruleskit.hpp:128-142, the Little's-law measurement, the report totals);
+// bm.phase_seconds is filled by the caller.  Returns the retained insertions.
+u32 account_batch(gdp2d_ctx* x, gdp2d_report* r, gdp2d_batch_metrics& bm, u32 attempted,
+                  const Counters& h, u32 nt, u32 flip_rounds, u32 rm_rounds) {
+    const u32 inserted = h.ins_mid + h.ins_cc;
+    const u32 retained = inserted - std::min(inserted, h.rm_done);
+    x->alive_v += inserted;
+    x->alive_v -= std::min<ull>(x->alive_v, h.rm_done);
+    x->alive_t += nt;
+    x->alive_t -= std::min<ull>(x->alive_t, 2ull * h.rm_done);
+    x->alive_s += h.ins_mid;
+    bm.attempted = attempted;
+    bm.concurrency = retained;
+    bm.latency = 0;
+    for (double s : bm.phase_seconds) bm.latency += s;
+    bm.throughput = bm.latency > 0 ? retained / bm.latency : 0.0;
+    x->little.record(attempted, retained, bm.latency);
+    bm.waste_fraction = attempted ? double(attempted - retained) / attempted : 0.0;
+    bm.walk_steps = h.walk_steps;
+    bm.cavity_visits = h.cavity_visits;
+    bm.survivors_claim = h.surv_claim;
+    bm.survivors_cavity = h.surv_cavity;
+    bm.inserted_midpoints = h.ins_mid;
+    bm.inserted_circumcenters = h.ins_cc;
+    bm.removed_redundant = h.rm_red;
+    bm.removed_dependent = h.rm_dep;
+    bm.dropped = h.dropped;
+    bm.marked_encroached = h.marked;
+    bm.flips = h.flips;
+    bm.flip_rounds = flip_rounds;
+    bm.removal_rounds = rm_rounds;
+    bm.removals_kept = h.rm_kept;
+    if (r->batches && r->n_batches < r->batches_capacity) r->batches[r->n_batches] = bm;
+    r->n_batches++;
+    r->total_candidates += attempted;
+    r->total_walk_steps += h.walk_steps;
+    r->total_cavity_visits += h.cavity_visits;
+    r->total_inserted += inserted;
+    r->total_flips += h.flips;
+    r->total_removed += h.rm_done;
+    r->sum_tris_alive += bm.tris_alive;
+    r->sum_verts_alive += bm.verts_alive;
+    r->sum_subsegs_alive += bm.subsegs_alive;
+    return retained;
+}
+
+// k_tail_loop on the working mesh (see its header in k_insert.cu): up to
+// `budget` batches; `ran` = batches done.  Returns true when the refinement
+// is finished.
+bool tail_loop(gdp2d_ctx* x, const gdp2d_params* p, const Quality& q, gdp2d_report* r,
+               u32 ncav, u64 budget, u64& ran) {
+    cudaStream_t st = x->st;
+    const int isolate = ncav == 0 ? 0
+                        : p->insert_mode == GDP2D_INSERT_ISOLATED   ? 1
+                        : p->insert_mode == GDP2D_INSERT_PRECEDENCE ? 2
+                                                                    : 0;
+    const u32 rs = isolate ? isolated_stride(ncav) : ncav + 1 + MAX_CLAIM_EXTRA;
+    // every buffer a batch of <= small_c candidates needs (nothing grows inside)
+    ensure_regions(x, x->small_c, ncav, rs);
+    ensure_fresh(x, x->small_c);
+    ensure_worklists(x, 12ull * x->small_c);
+    const u32 reg_cap = (u32)std::min<size_t>(x->reg_cap / rs, x->rl_cap);
+    const u32 nb_max = (u32)std::min<u64>(budget, kTailMax);
+    InsertLaunch L = base_launch(x, p, x->epoch + 1, ncav, rs, isolate);
+    L.w.dlist = x->dlist;
+    L.w.dlist_n = x->dlist + DLIST_CAP;
+    L.w.dlist_cap = DLIST_CAP;
+    L.reg_cap = reg_cap;
+    TailArgs t;
+    t.rec = x->tail_rec;
+    t.max_batches = nb_max;
+    t.klist = x->small_list + SMALL_LIST_CAP + 1;
+    t.klist_n = x->small_list + 2 * SMALL_LIST_CAP + 1;
+    t.q = q;
+    t.out = x->tail_out;
+    CK(cudaMemsetAsync(x->d_ctr, 0, sizeof(Counters), st));
+    CK(cudaEventRecord(x->ev[0], st));
+    launch_tail_loop(L, t, p->mode == GDP2D_CHEW ? 1 : 0, st);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(x->h_tail_out, x->tail_out, 8 * sizeof(u32), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(x->h_tail_rec, x->tail_rec, sizeof(TailRec) * nb_max,
+                       cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const u32 exitr = x->h_tail_out[0], nb = x->h_tail_out[1];
+    ran = nb;
+    bool done = false;
+    for (u32 k = 0; k < nb; ++k) {
+        const TailRec& rec = x->h_tail_rec[k];
+        if (rec.ctr.err_code) {
+            *x->h_ctr = rec.ctr;
+            raise_dev_err(x);
+        }
+        gdp2d_batch_metrics bm;
+        std::memset(&bm, 0, sizeof bm);
+        bm.batch_index = r->n_batches;
+        bm.tris_alive = x->alive_t;
+        bm.verts_alive = x->alive_v;
+        bm.subsegs_alive = x->alive_s;
+        bm.phase_seconds[GDP2D_PH_COLLECT] = double(rec.t1 - rec.t0) * 1e-9;
+        bm.phase_seconds[GDP2D_PH_INSERT] = double(rec.t2 - rec.t1) * 1e-9;
+        r->scan_seconds += double(rec.t1 - rec.t0) * 1e-9;
+        r->scan_bytes += 64ull * rec.ctr.scan_dirty + 105ull * rec.attempted;
+        r->scan_launches += 1;
+        const u32 retained =
+            account_batch(x, r, bm, rec.attempted, rec.ctr, rec.nt, rec.flip_rounds, rec.rm_rounds);
+        if (retained == 0 && rec.ctr.marked == 0) done = true;
+    }
+    if (exitr == TAIL_ERR) throw Fail{GDP2D_EMESH, "tail loop: device error"};
+    x->epoch += nb;
+    x->round = x->h_tail_out[5] - 1;
+    x->work.m.nV = x->h_tail_out[2];
+    x->work.m.nT = x->h_tail_out[3];
+    x->work.m.nS = x->h_tail_out[4];
+    x->c_prev = x->h_tail_out[6];
+    x->have_c_prev = true;
+    // after BIG / GROW the klist is the list of the batch the host runs next;
+    // NOKEYS: the dirty list overflowed, the host collects from scratch
+    x->klist_ok = exitr != TAIL_NOKEYS;
+    if (exitr == TAIL_NOKEYS || exitr == TAIL_GROW || exitr == TAIL_BIG) x->klist_ok = false;
+    if (exitr == TAIL_DONE) done = true;
+    return done;
+}
+
 // The refinement loop (refine.hpp:651-713) on the working mesh.
 void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
     const auto wall0 = std::chrono::steady_clock::now();
@@ -1222,12 +1379,27 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
     x->k_split_s = x->k_rb_s = 0;
     x->k_split_b = x->k_rb_b = x->k_launches = x->k_rb_launches = 0;
     x->have_c_prev = false;
+    x->klist_ok = false;
+    x->dlist_on = false;
     x->little.reset();
     CK(cudaEventRecord(x->ev[GDP2D_NPHASES + 1], st));  // loop start
     for (u64 iter = 0;; ++iter) {
         if (iter >= p->iteration_cap) {
             r->iteration_cap_hit = 1;
             break;
+        }
+        // The long tail of small batches: run them back to back on the device
+        // (k_tail_loop) while the list stays small; the loop returns here when
+        // it does not, or the refinement is done.
+        if (x->tail_on && x->have_c_prev && x->klist_ok && x->c_prev <= x->small_c &&
+            !x->tr.on && !x->check && p->rule4_unified_collection != 0 &&
+            p->batch_size_cap == 0) {
+            u64 ran = 0;
+            const bool done = tail_loop(x, p, q, r, ncav, p->iteration_cap - iter, ran);
+            iter += ran;
+            if (done) break;
+            --iter;   // the for loop's increment: the next batch is iteration iter + ran
+            continue;
         }
         DevMesh& m = x->work.m;
         gdp2d_batch_metrics bm;
@@ -1260,11 +1432,11 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
                          p->rule4_unified_collection != 0 && p->batch_size_cap == 0 &&
                          !little_sync;
         const bool small = ncs && x->c_prev <= x->small_collect_c;
+        x->dlist_on = small;   // its rewrites feed a tail loop's next collect
         u32 C = launch_collect(m, q, p->rule4_unified_collection != 0, x->flags, x->c, x->ccap,
                                x->scan, x->d_ctr, st, cache, &tris_scanned, x->d_C,
                                nullptr, ncs ? nullptr : x->ev[GDP2D_NPHASES + 3], !ncs,
-                               small ? x->small_list : nullptr,
-                               small ? x->small_list + SMALL_LIST_CAP : nullptr);
+                               small ? x->small_list : nullptr, x->dlist + DLIST_CAP);
         // the no-round-trip collect is timed to ev[1], scatter included (one
         // event record less per batch)
         const cudaEvent_t scan_end = ncs ? x->ev[1] : x->ev[GDP2D_NPHASES + 3];
@@ -1381,16 +1553,7 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
         raise_dev_err(x);   // counters came back with the insertion's status
         const Counters& h = *x->h_ctr;
         r->scan_bytes += scan_alg_bytes(scan_nT, scan_nS, h.scan_dirty, C, ncs);
-        const u32 inserted = h.ins_mid + h.ins_cc;
-        const u32 retained = inserted - std::min(inserted, h.rm_done);
-        x->alive_v += inserted;
-        x->alive_v -= std::min<ull>(x->alive_v, h.rm_done);
-        x->alive_t += nt;
-        x->alive_t -= std::min<ull>(x->alive_t, 2ull * h.rm_done);
-        x->alive_s += h.ins_mid;
         // metrics (record_batch, ruleskit.hpp:128-142)
-        bm.attempted = attempted;
-        bm.concurrency = retained;
         bm.phase_seconds[GDP2D_PH_COLLECT] = ev_ms(x->ev[0], x->ev[1]) * 1e-3;
         bm.phase_seconds[GDP2D_PH_SPLIT_POINTS] = 0.0;   // fused into collect
         if (filtered_events) {
@@ -1401,35 +1564,8 @@ void refine_loop(gdp2d_ctx* x, const gdp2d_params* p, gdp2d_report* r) {
         } else {   // filtered inside the batch kernel
             bm.phase_seconds[GDP2D_PH_INSERT] = ev_ms(x->ev[1], ins_end) * 1e-3;
         }
-        for (double s : bm.phase_seconds) bm.latency += s;
-        bm.throughput = bm.latency > 0 ? retained / bm.latency : 0.0;
-        x->little.record(attempted, retained, bm.latency);
-        bm.waste_fraction = attempted ? double(attempted - retained) / attempted : 0.0;
-        bm.walk_steps = h.walk_steps;
-        bm.cavity_visits = h.cavity_visits;
-        bm.survivors_claim = h.surv_claim;
-        bm.survivors_cavity = h.surv_cavity;
-        bm.inserted_midpoints = h.ins_mid;
-        bm.inserted_circumcenters = h.ins_cc;
-        bm.removed_redundant = h.rm_red;
-        bm.removed_dependent = h.rm_dep;
-        bm.dropped = h.dropped;
-        bm.marked_encroached = h.marked;
-        bm.flips = h.flips;
-        bm.flip_rounds = flip_rounds;
-        bm.removal_rounds = rm_rounds;
-        bm.removals_kept = h.rm_kept;
-        if (r->batches && r->n_batches < r->batches_capacity) r->batches[r->n_batches] = bm;
-        r->n_batches++;
-        r->total_candidates += attempted;
-        r->total_walk_steps += h.walk_steps;
-        r->total_cavity_visits += h.cavity_visits;
-        r->total_inserted += inserted;
-        r->total_flips += h.flips;
-        r->total_removed += h.rm_done;
-        r->sum_tris_alive += bm.tris_alive;
-        r->sum_verts_alive += bm.verts_alive;
-        r->sum_subsegs_alive += bm.subsegs_alive;
+        x->klist_ok = small && C != NONE;   // the next batch may take the tail loop
+        const u32 retained = account_batch(x, r, bm, attempted, h, nt, flip_rounds, rm_rounds);
         if (retained == 0 && h.marked == 0) break;
     }
     // the batches kept vert_tri for their own fresh vertices only

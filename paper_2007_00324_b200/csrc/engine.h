@@ -71,11 +71,15 @@ u32 launch_collect(const DevMesh& m, const Quality& q, bool rule4, uint8_t* flag
                    const CollectCache& cache, bool* tris_scanned, u32* d_count,
                    cudaEvent_t ev_scan0 = nullptr,
                    cudaEvent_t ev_scan1 = nullptr, bool sync = true,
-                   u32* small_list = nullptr, u32* small_list_n = nullptr);
-// small_list (SMALL_LIST_CAP keys) + small_list_n (zeroed): the no-round-trip
+                   u32* small_list = nullptr, u32* dlist_n = nullptr);
+// small_list (SMALL_LIST_WORDS: append keys [CAP], their count, the sorted
+// keys of the list made (klist) [CAP], klist's count): the no-round-trip
 // collect of a small list (k_collect_append + k_collect_small, k_collect.cu);
-// *d_count = NONE when the list outgrew it.
+// *d_count = NONE when the list outgrew it.  dlist_n: the tail loop's
+// dirty-element count, restarted by every small-list collect.
 constexpr u32 SMALL_LIST_CAP = 4096;
+constexpr u32 SMALL_LIST_WORDS = 2 * SMALL_LIST_CAP + 2;
+constexpr u32 DLIST_CAP = 1u << 16;
 void launch_split_points(const DevMesh& m, DevCands c, u32 n, Counters* d_ctr, cudaStream_t st);
 // batch_size_cap (refine.hpp:252-261): keep the k highest-priority alive
 // candidates of the list (others marked dead), device-side radix select.
@@ -177,7 +181,12 @@ struct WorkLists {
     // alone (detection and removal stars), so it passes its first fresh id and
     // refine_loop rebuilds the whole array once at the end (launch_vtri_rebuild).
     u32 vtri_from = 0;
-    u32 ear_dl_max = 0xFFFFFFFFu;   // experiment: Delaunay-ear pass only while the polygon has <= this many vertices
+    // dirty-element list of the device-resident tail loop (k_tail_loop): every
+    // rewritten triangle, the subsegments on it and every newly marked
+    // subsegment, as collect keys (bit 31 = triangle | id); null = off
+    u32* dlist = nullptr;
+    u32* dlist_n = nullptr;
+    u32 dlist_cap = 0;
 };
 
 // The whole Lawson fixpoint as one persistent cooperative kernel (see
@@ -229,6 +238,29 @@ struct InsertLaunch {
 };
 int insert_persistent_grid(int device);
 int rollback_persistent_grid(int device);
+// The device-resident tail loop (k_tail_loop, k_insert.cu): consecutive small
+// batches (C <= small_c) run back to back in ONE single-CTA launch -- an
+// incremental collect over the previous candidate keys and the elements the
+// previous batch dirtied (klist + WorkLists::dlist), Lines 5-7, the splits,
+// Lawson, detection and rollback -- with one host readback at the end.
+struct TailRec {            // one batch of the loop, for the host's RunReport
+    u32 attempted, nv, nt, ns;
+    u32 steps, flip_rounds, rm_rounds, dirty;
+    unsigned long long t0, t1, t2;   // globaltimer: batch start, collect end, batch end
+    Counters ctr;
+};
+enum : u32 { TAIL_DONE = 0, TAIL_BIG = 1, TAIL_GROW = 2, TAIL_CAP = 3, TAIL_ERR = 4,
+             TAIL_NOKEYS = 5 };
+struct TailArgs {
+    TailRec* rec;           // [max_batches]
+    u32 max_batches;
+    u32* klist;             // [SMALL_LIST_CAP] sorted keys of the last collect's list
+    u32* klist_n;           // their count (NONE = not valid)
+    Quality q;
+    u32* out;               // [8]: exit reason, batches, nV, nT, nS, next round0, last C
+};
+void launch_tail_loop(const InsertLaunch& L, const TailArgs& t, int mode, cudaStream_t st);
+
 // Kernel 1 (plan + splits + Lawson, with Lines 5-7 unless L.prefiltered) then
 // kernel 2 (detect + rollback loop), both cooperative, no host sync between.
 // which: bit 0 = kernel 1, bit 1 = kernel 2, launched in that order.

@@ -149,6 +149,13 @@ static __device__ void split_edge_A(const DevMesh& m, const TriAux& x, const Wor
     }
 }
 
+// ---- the tail loop's dirty-element list (WorkLists::dlist) ---------------------------
+
+__device__ __forceinline__ void dlist_push(const WorkLists& w, u32 key) {
+    const u32 o = atomicAdd(w.dlist_n, 1u);
+    if (o < w.dlist_cap) w.dlist[o] = key;
+}
+
 // ---- phase B ------------------------------------------------------------------------
 
 __device__ __forceinline__ void fixup_one(const DevMesh& m, u32 round, const TriAux& x,
@@ -174,6 +181,12 @@ __device__ __forceinline__ void fixup_one(const DevMesh& m, u32 round, const Tri
     }
     tn.w = 0;
     m.tn[t] = tn;
+    if (w.dlist) {   // the tail loop re-evaluates what a rewrite touched
+        dlist_push(w, 0x80000000u | t);
+        if (ts.x != NONE) dlist_push(w, ts.x);
+        if (ts.y != NONE) dlist_push(w, ts.y);
+        if (ts.z != NONE) dlist_push(w, ts.z);
+    }
     if (tv.x >= w.vtri_from) atomicMin(&m.vtri[tv.x], t);
     if (tv.y >= w.vtri_from) atomicMin(&m.vtri[tv.y], t);
     if (tv.z >= w.vtri_from) atomicMin(&m.vtri[tv.z], t);

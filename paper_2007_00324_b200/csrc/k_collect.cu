@@ -10,6 +10,7 @@
 #include <algorithm>
 
 #include "engine.h"
+#include "gdp2d_collect.cuh"
 #include "scan.cuh"
 
 namespace gdp2d {
@@ -20,40 +21,10 @@ struct CollectRange {
 };
 
 // Incremental mode (full == 0): an element whose dirty bit is clear keeps its
-// cached verdict -- its corners (and, for a subsegment, both adjacent
-// triangles and hence its apexes) are unchanged since the last scan -- so the
-// scan reads one byte instead of the 64 B record + corner gathers.  The
-// candidate list is bit-identical to a full scan (same flags, same stable
-// compaction); only the sticky encroached flag is read for every subsegment.
-// Each thread owns SCAN_ITEMS (= 8) consecutive elements: one 8-byte load of
-// the cached verdicts, one 8-byte store of the flags.  Order inside a tile is
-// element order, so the scatter needs a single block scan per tile.
-template <int MODE>
-__device__ __forceinline__ uint8_t eval_sub(const DevMesh& m, u32 i, int full, u32& dirty) {
-    if (!m.salive[i]) return 0;
-    const uint8_t sf = full ? 2 : m.sflag[i];
-    bool enc;
-    if (sf & 2) {
-        enc = is_encroached<MODE>(m, i);
-        m.sflag[i] = enc ? 1 : 0;
-        ++dirty;
-    } else {
-        enc = sf & 1;
-    }
-    return (m.senc[i] || enc) ? 1 : 0;
-}
-
-__device__ __forceinline__ uint8_t eval_tri(const DevMesh& m, const Quality& q, u32 i) {
-    uint8_t f = 0;
-    const uint4 tv = m.tv[i];
-    if (tv.w) {
-        const double2 a = m.xy[tv.x], b = m.xy[tv.y], c = m.xy[tv.z];
-        if (is_bad_pts(a, b, c, q) && resolvable_pts(a, b, c)) f = 1;
-    }
-    m.tflag[i] = f;
-    return f;
-}
-
+// cached verdict (eval_sub / eval_tri, gdp2d_collect.cuh).  Each thread owns
+// SCAN_ITEMS (= 8) consecutive elements: one 8-byte load of the cached
+// verdicts, one 8-byte store of the flags.  Order inside a tile is element
+// order, so the scatter needs a single block scan per tile.
 template <int MODE>
 __global__ void __launch_bounds__(SCAN_BLOCK) k_collect_flags(DevMesh m, Quality q, CollectRange r,
                                                            uint8_t* __restrict__ flags,
@@ -115,53 +86,6 @@ __global__ void __launch_bounds__(SCAN_BLOCK) k_collect_flags(DevMesh m, Quality
         partial[blockIdx.x] = t & 0xFFFFu;
         if (t >> 16) atomicAdd(&ctr->scan_dirty, t >> 16);
     }
-}
-
-// compute_splitting_points for one candidate (refine.hpp:269-294).
-__device__ __forceinline__ double2 split_point(const DevMesh& m, int kind, u32 id, uint8_t& fb) {
-    fb = 0;
-    if (kind == 0) return subseg_mid(m, id);
-    const uint4 tv = m.tv[id];
-    const double2 v3[3] = {m.xy[tv.x], m.xy[tv.y], m.xy[tv.z]};
-    bool ok;
-    const double2 cc = circumcenter(v3[0], v3[1], v3[2], ok);
-    if (ok && isfinite(cc.x) && isfinite(cc.y)) return cc;
-    fb = 1;
-    int best = 0;
-    double best_len = -1.0;
-    for (int e = 0; e < 3; ++e) {
-        const double len = sqdist(v3[nxt(e)], v3[prv(e)]);
-        if (len > best_len) {
-            best_len = len;
-            best = e;
-        }
-    }
-    return midpoint2(v3[nxt(best)], v3[prv(best)]);
-}
-
-// One candidate record (refine.hpp:236-248 + compute_splitting_points):
-// list position o, element i of kind 0 (subsegment) / 1 (triangle).
-__device__ __forceinline__ u32 write_candidate(const DevMesh& m, const DevCands& c, u32 o,
-                                               int kind, u32 i) {
-    uint8_t fb;
-    c.pt[o] = split_point(m, kind, i, fb);
-    double measure;
-    if (kind == 0) {
-        measure = subseg_len(m, i);
-    } else {
-        const uint4 tv = m.tv[i];
-        measure = area_pts(m.xy[tv.x], m.xy[tv.y], m.xy[tv.z]);
-    }
-    c.key[o] = make_key(kind == 0 ? 1 : 0, measure);
-    c.id[o] = i;
-    c.tie[o] = o;
-    c.loc[o] = PENDING;
-    c.kind[o] = (uint8_t)kind;
-    c.alive[o] = 1;
-    c.lkind[o] = 0;
-    c.ledge[o] = -1;
-    c.fb[o] = fb;
-    return fb;
 }
 
 __global__ void __launch_bounds__(SCAN_BLOCK) k_collect_scatter(DevMesh m, CollectRange r,
@@ -280,16 +204,22 @@ __global__ void __launch_bounds__(SCAN_BLOCK) k_collect_append(DevMesh m, Qualit
 
 // One CTA: sort the appended keys (bitonic, in shared memory) and write the
 // candidate records in list order.
+// The sorted keys are also kept (klist): the tail loop's next collect starts
+// from them, and the dirty-element list restarts (dlist_n).
 __global__ void __launch_bounds__(SMALL_BLOCK) k_collect_small(DevMesh m, u32* __restrict__ list,
                                                             u32* __restrict__ list_n, DevCands c,
                                                             u32 ccap, u32* __restrict__ d_count,
-                                                            Counters* ctr) {
+                                                            Counters* ctr, u32* __restrict__ klist,
+                                                            u32* __restrict__ klist_n,
+                                                            u32* __restrict__ dlist_n) {
     __shared__ u32 key[SMALL_LIST];
     const u32 n = *list_n;
     if (n > SMALL_LIST || n > ccap) {
         if (threadIdx.x == 0) {
             *d_count = NONE;   // the host redoes the batch (full collect)
             *list_n = 0;
+            *klist_n = NONE;
+            if (dlist_n) *dlist_n = 0;
         }
         return;
     }
@@ -314,12 +244,15 @@ __global__ void __launch_bounds__(SMALL_BLOCK) k_collect_small(DevMesh m, u32* _
     u32 nfb = 0;
     for (u32 o = threadIdx.x; o < n; o += blockDim.x) {
         const u32 k = key[o];
+        klist[o] = k;
         nfb += write_candidate(m, c, o, k >> 31 ? 1 : 0, k & 0x7FFFFFFFu);
     }
     warp_add_u32(&ctr->fallbacks, nfb);
     if (threadIdx.x == 0) {
         *d_count = n;
         *list_n = 0;   // ready for the next batch
+        *klist_n = n;
+        if (dlist_n) *dlist_n = 0;
     }
 }
 
@@ -327,7 +260,10 @@ u32 launch_collect(const DevMesh& m, const Quality& q, bool rule4, uint8_t* flag
                    u32 ccap, ScanScratch& s, Counters* d_ctr, cudaStream_t st,
                    const CollectCache& cache, bool* tris_scanned, u32* d_count,
                    cudaEvent_t ev_scan0, cudaEvent_t ev_scan1, bool sync, u32* small_list,
-                   u32* small_list_n) {
+                   u32* dlist_n) {
+    u32* small_list_n = small_list ? small_list + SMALL_LIST_CAP : nullptr;
+    u32* klist = small_list ? small_list + SMALL_LIST_CAP + 1 : nullptr;
+    u32* klist_n = small_list ? small_list + 2 * SMALL_LIST_CAP + 1 : nullptr;
     *tris_scanned = false;
     u32 *zp0 = cache.zero[0], *zp1 = cache.zero[1];
     u32 zn0 = cache.zero_n[0], zn1 = cache.zero_n[1];
@@ -348,7 +284,7 @@ u32 launch_collect(const DevMesh& m, const Quality& q, bool rule4, uint8_t* flag
             note_launch(), k_collect_append<0><<<tiles, SCAN_BLOCK, 0, st>>>(m, q, r, small_list, small_list_n, cache.full, d_ctr, zp0, zn0, zp1, zn1);
         else
             note_launch(), k_collect_append<1><<<tiles, SCAN_BLOCK, 0, st>>>(m, q, r, small_list, small_list_n, cache.full, d_ctr, zp0, zn0, zp1, zn1);
-        note_launch(), k_collect_small<<<1, SMALL_BLOCK, 0, st>>>(m, small_list, small_list_n, c, ccap, d_count, d_ctr);
+        note_launch(), k_collect_small<<<1, SMALL_BLOCK, 0, st>>>(m, small_list, small_list_n, c, ccap, d_count, d_ctr, klist, klist_n, dlist_n);
         return NONE;
     }
     auto run = [&](bool sub, bool tri) -> u32 {

@@ -20,6 +20,7 @@
 
 #include <algorithm>
 
+#include "gdp2d_collect.cuh"
 #include "gdp2d_phases.cuh"
 #include "gdp2d_rewrite.cuh"
 #include "scan.cuh"
@@ -212,7 +213,8 @@ __device__ __forceinline__ bool prio_gt(const FreshInfo& f, u32 a, u32 b) {
 // 255 = too many), so detect_b_fast needs no second walk.
 template <int MODE>
 __device__ __noinline__ u32 detect_a_one(const DevMesh& m, u64 depth_cap, u32 V0, u32 F, u32 j,
-                                         const FreshInfo& f, Counters* ctr, int collect_dep) {
+                                         const FreshInfo& f, Counters* ctr, int collect_dep,
+                                         const WorkLists& w) {
     u32 marked = 0;
     uint8_t mark = 0;
     const u32 v = V0 + j;
@@ -256,7 +258,10 @@ __device__ __noinline__ u32 detect_a_one(const DevMesh& m, u64 depth_cap, u32 V0
         }
         if (best != NONE) {
             mark = 1;
-            if (atomicExch(&m.senc[best], 1u) == 0u) marked = 1;
+            if (atomicExch(&m.senc[best], 1u) == 0u) {
+                marked = 1;
+                if (w.dlist) dlist_push(w, best);   // a new candidate for the tail loop
+            }
         }
     }
     f.mark[j] = mark;
@@ -482,7 +487,7 @@ __device__ __noinline__ u32 rm_apply_one_n(const DevMesh& m, const u32* __restri
                 // Pass 1 (degenerate stars only, e.g. a point that was inserted
                 // exactly on an edge): v may lie ON the new diagonal -- the
                 // final hole triangulation is still valid because v leaves.
-                for (int pass = (u32)cnt <= w.ear_dl_max ? -1 : 0; pass < 2 && !found; ++pass) {
+                for (int pass = -1; pass < 2 && !found; ++pass) {
                     j = head;
                     for (int it = 0; it < cnt; ++it) {
                         const int a = PV[j], c = NX[j];
@@ -871,10 +876,16 @@ __device__ void filter(const InsertArgs& a, const Exec& ex, u32 C) {
             a.c.alive[i] = 0;
             continue;
         }
-        surv2 += a.isolate ? isolated_check_one(m, a.c, i, a.rs, a.regions, a.region_len,
-                                                a.x.ckey, a.x.ctie, marked, unsafe)
-                           : cavity_check_one(a.c, i, a.rs, a.regions, a.region_len, a.x.ckey,
-                                              a.x.ctie);
+        if (a.isolate) {
+            u32 mk = 0;
+            surv2 += isolated_check_one(m, a.c, i, a.rs, a.regions, a.region_len, a.x.ckey,
+                                        a.x.ctie, mk, unsafe);
+            // a precedence mark makes a new candidate for the tail loop
+            if (mk && a.w.dlist) dlist_push(a.w, a.c.red[i]);
+            marked += mk;
+        } else {
+            surv2 += cavity_check_one(a.c, i, a.rs, a.regions, a.region_len, a.x.ckey, a.x.ctie);
+        }
     }
     if (unsafe) atomicOr(&a.state[8], 1u);
     warp_add_u32(&a.ctr->marked, marked);
@@ -1058,7 +1069,7 @@ __device__ void rollback_loop(const InsertArgs& a, const Exec& ex, u32 nv, u32 n
         for (u32 j = ex.tid; j < F; j += ex.nthr) {
             if (a.f.dirty[j] == 0) continue;   // not a suspect since the last pass
             a.f.dirty[j] = 2;
-            marked += detect_a_one<MODE>(m, a.depth_cap, V0, F, j, a.f, a.ctr, !a.dep_mis);
+            marked += detect_a_one<MODE>(m, a.depth_cap, V0, F, j, a.f, a.ctr, !a.dep_mis, w);
         }
         ex.sync();
         trace(a, ex.leader(), TR_DET_A);
@@ -1240,6 +1251,195 @@ __global__ void __launch_bounds__(ROLLBACK_BLOCK) k_batch_rollback(const __grid_
     rollback_loop<MODE>(a, ex, nv, nt, ns);
 }
 
+// =====================================================================================
+// The device-resident tail loop: the long run of small batches at the end of a
+// refinement (Rule 1 / Rule 4 of PAPER.md:104-116 taken to the batch loop) in
+// ONE single-CTA launch.  Each iteration is one batch of refine.hpp:658-708:
+//   collect   incremental, and the list is the one a full scan would make:
+//             every element whose verdict can have changed since the last
+//             collect is in klist (the last list: still bad unless rewritten)
+//             or in the dirty list (rewritten triangles, the subsegments on
+//             them, newly marked subsegments).  Their union is sorted, each
+//             element re-evaluated through the dirty-bit cache (eval_sub /
+//             eval_tri) and the bad ones written as records in key order
+//             (subsegments, then triangles, each by id; tiebreak = index).
+//   Lines 5-8 the block-mode batch code of k_batch_split / k_batch_rollback.
+// The loop leaves to the host when the list outgrows small_c (BIG), a batch
+// does not fit the buffers (GROW, nothing written), a device error, the
+// iteration budget, or the refinement ends (DONE: C == 0, or nothing
+// retained and nothing marked, refine.hpp:706).
+// =====================================================================================
+
+template <int MODE>
+__global__ void __launch_bounds__(INSERT_BLOCK, 1) k_tail_loop(const __grid_constant__ InsertArgs a0,
+                                                            const __grid_constant__ TailArgs t) {
+    __shared__ u32 key[SMALL_LIST_CAP];
+    __shared__ u32 sh[INSERT_BLOCK / 32 + 1];
+    __shared__ u32 s_n;
+    __shared__ RoundCtr sring[5];
+    InsertArgs a = a0;   // per-batch counts / epoch / stamp round (every thread the same)
+    u32 b = 0, exitr = TAIL_CAP, lastC = 0;
+    for (; b < t.max_batches; ++b) {
+        const unsigned long long t0 = globaltimer();
+        // ---- incremental collect ----
+        const u32 nk = vload(t.klist_n), nd = vload(a.w.dlist_n);
+        if (nk > SMALL_LIST_CAP || nd > a.w.dlist_cap || nk + nd > SMALL_LIST_CAP) {
+            exitr = TAIL_NOKEYS;   // nothing consumed: the host collects from scratch
+            break;
+        }
+        const u32 n = nk + nd;
+        u32 np = 1;
+        while (np < n) np <<= 1;
+        for (u32 k = threadIdx.x; k < np; k += blockDim.x)
+            key[k] = k < nk ? t.klist[k] : (k < n ? a.w.dlist[k - nk] : NONE);
+        __syncthreads();
+        for (u32 size = 2; size <= np; size <<= 1)
+            for (u32 stride = size >> 1; stride > 0; stride >>= 1) {
+                for (u32 k = threadIdx.x; k < np / 2; k += blockDim.x) {
+                    const u32 lo = 2 * k - (k & (stride - 1)), hi = lo + stride;
+                    const bool up = (lo & size) == 0;
+                    const u32 x = key[lo], y = key[hi];
+                    if ((x > y) == up) {
+                        key[lo] = y;
+                        key[hi] = x;
+                    }
+                }
+                __syncthreads();
+            }
+        // unique keys, verdicts through the dirty-bit cache, order-preserving
+        // compaction: chunks of blockDim keys, one block scan each
+        u32 C = 0, dirty = 0, nfb = 0;
+        for (u32 base = 0; base < n; base += blockDim.x) {
+            const u32 k = base + threadIdx.x;
+            u32 bad = 0, kk = NONE;
+            if (k < n) {
+                kk = key[k];
+                if (kk != NONE && (k == 0 || key[k - 1] != kk)) {
+                    const u32 id = kk & 0x7FFFFFFFu;
+                    if (kk >> 31) {
+                        const uint8_t tf = a.m.tflag[id];
+                        if (tf & 2) {
+                            bad = eval_tri(a.m, t.q, id);
+                            ++dirty;
+                        } else {
+                            bad = tf & 1;
+                        }
+                    } else {
+                        bad = eval_sub<MODE>(a.m, id, 0, dirty);
+                    }
+                }
+            }
+            u32 tot;
+            const u32 o = C + block_exclusive<INSERT_BLOCK>(bad, sh, &tot);
+            __syncthreads();   // every thread has read key[] of this chunk
+            if (bad) {
+                t.klist[o] = kk;
+                nfb += write_candidate(a.m, a.c, o, kk >> 31 ? 1 : 0, kk & 0x7FFFFFFFu);
+            }
+            C += tot;
+        }
+        warp_add_u32(&a.ctr->fallbacks, nfb);
+        {
+            const u32 d = block_sum<INSERT_BLOCK>(dirty, sh);
+            if (threadIdx.x == 0) {
+                a.ctr->scan_dirty += d;
+                *t.klist_n = C;
+                *a.w.dlist_n = 0;
+                *const_cast<u32*>(a.d_C) = C;
+                for (int k = 0; k < 10; ++k) a.state[k] = 0;
+            }
+        }
+        __syncthreads();
+        lastC = C;
+        if (C == 0) {
+            exitr = TAIL_DONE;
+            break;
+        }
+        if (C > a.small_c || C > a.reg_cap) {
+            exitr = TAIL_BIG;   // the host runs this list's batch on the grid kernels
+            break;
+        }
+        const unsigned long long t1 = globaltimer();
+        // ---- Lines 5-8 (block mode) ----
+        const Exec ex = block_exec(sring);
+        filter<MODE>(a, ex, C);
+        plan_and_scan(a, ex, C, false);
+        const u32 nv = vload(&a.b.totals[0]), nt = vload(&a.b.totals[1]),
+                  ns = vload(&a.b.totals[2]);
+        if (nv > 0) {
+            if (!fits_and_status(a, nv, nt, ns)) {
+                exitr = TAIL_GROW;   // nothing written; the host grows and redoes it
+                break;
+            }
+            split_and_flip(a, ex, nv, nt, ns);
+            __syncthreads();
+            if (vload(&a.state[0]) == INS_OK && !(a.isolate == 1 && vload(&a.state[8]) == 0))
+                rollback_loop<MODE>(a, ex, nv, nt, ns);
+        } else {
+            fits_and_status(a, 0, 0, 0);   // status words zero
+        }
+        __syncthreads();
+        const unsigned long long t2 = globaltimer();
+        // ---- the batch's record; the next batch's counts ----
+        const u32 steps = vload(&a.state[1]);
+        if (threadIdx.x == 0) {
+            TailRec& r = t.rec[b];
+            r.attempted = C;
+            r.nv = nv;
+            r.nt = nt;
+            r.ns = ns;
+            r.steps = steps;
+            r.flip_rounds = vload(&a.state[2]);
+            r.rm_rounds = vload(&a.state[3]);
+            r.dirty = 0;
+            r.t0 = t0;
+            r.t1 = t1;
+            r.t2 = t2;
+            // word by word past L1: the counters were bumped by L2 atomics
+            const volatile u32* src = reinterpret_cast<const volatile u32*>(a.ctr);
+            u32* dst = reinterpret_cast<u32*>(&r.ctr);
+            for (u32 k = 0; k < sizeof(Counters) / 4; ++k) dst[k] = src[k];
+        }
+        __syncthreads();
+        const Counters& h = t.rec[b].ctr;
+        const u32 err = vload(&a.ctr->err_code);
+        const u32 st0 = vload(&a.state[0]);
+        const u32 ins = h.ins_mid + h.ins_cc, rmd = h.rm_done, marked = h.marked;
+        __syncthreads();   // everyone has read the record before the counters reset
+        if (threadIdx.x == 0) {
+            Counters z = {};
+            *a.ctr = z;
+        }
+        if (err != 0 || (nv > 0 && st0 != INS_OK)) {
+            exitr = TAIL_ERR;
+            ++b;
+            break;
+        }
+        a.m.nV += nv;
+        a.m.nT += nt;
+        a.m.nS += ns;
+        a.batch += 1;
+        a.round0 += nv > 0 ? steps + 1 : 1;
+        a.w.fresh_v0 = a.m.nV;
+        a.w.vtri_from = a.m.nV;
+        if (ins - min(ins, rmd) == 0 && marked == 0) {
+            exitr = TAIL_DONE;
+            ++b;
+            break;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        t.out[0] = exitr;
+        t.out[1] = b;
+        t.out[2] = a.m.nV;
+        t.out[3] = a.m.nT;
+        t.out[4] = a.m.nS;
+        t.out[5] = a.round0;
+        t.out[6] = lastC;
+    }
+}
+
 template <class K0, class K1>
 static int coop_grid(K0 k0, K1 k1, int device, int block = INSERT_BLOCK) {
     int sms = 0, per0 = 0, per1 = 0;
@@ -1295,6 +1495,15 @@ static InsertArgs make_args(const InsertLaunch& L) {
     a.trace_n = L.trace_n;
     a.trace_cap = L.trace_cap;
     return a;
+}
+
+void launch_tail_loop(const InsertLaunch& L, const TailArgs& t, int mode, cudaStream_t st) {
+    const InsertArgs a = make_args(L);
+    note_launch();
+    if (mode)
+        k_tail_loop<1><<<1, INSERT_BLOCK, 0, st>>>(a, t);
+    else
+        k_tail_loop<0><<<1, INSERT_BLOCK, 0, st>>>(a, t);
 }
 
 void launch_insert_persistent(const InsertLaunch& L, int mode, int grid, int grid2, cudaStream_t st,

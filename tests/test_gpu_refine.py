@@ -160,15 +160,18 @@ def test_collect_round_trip_paths_identical(built, monkeypatch):
     (GDP2D_REGIONS_TIGHT=1 makes every no-round-trip batch overflow and redo)
     must give bit-identical meshes.  So must the small-list collect (append +
     one-CTA sort) switched off (GDP2D_SMALL_COLLECT=0) or forced onto every
-    no-round-trip batch, big ones overflowing into the full-collect redo."""
+    no-round-trip batch, big ones overflowing into the full-collect redo, and
+    the device-resident tail loop switched off (GDP2D_TAIL_LOOP=0)."""
     from paper_2007_00324_b200 import Engine, QualityCriteria, host
     pts, segs = host.generate_pslg(40_000, 4_000, "gaussian", 13)
     m, closed = host.build_cdt(pts, segs)
     q = QualityCriteria(B_SQRT2_THETA)
     outs = []
     for env in ({}, {"GDP2D_SYNC_COLLECT": "1"}, {"GDP2D_REGIONS_TIGHT": "1"},
-                {"GDP2D_SMALL_COLLECT": "0"}, {"GDP2D_SMALL_COLLECT": "1000000000"}):
-        for k in ("GDP2D_SYNC_COLLECT", "GDP2D_REGIONS_TIGHT", "GDP2D_SMALL_COLLECT"):
+                {"GDP2D_SMALL_COLLECT": "0"}, {"GDP2D_SMALL_COLLECT": "1000000000"},
+                {"GDP2D_TAIL_LOOP": "0"}):
+        for k in ("GDP2D_SYNC_COLLECT", "GDP2D_REGIONS_TIGHT", "GDP2D_SMALL_COLLECT",
+                  "GDP2D_TAIL_LOOP"):
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)
@@ -395,3 +398,32 @@ def test_high_degree_ngon(built, n_sides):
     assert rep.bad_triangles == 0
     assert abs(rep.steiner_points - rref.steiner_points) <= 0.10 * rref.steiner_points + 8, \
         (rep.steiner_points, rref.steiner_points)
+
+
+@pytest.mark.parametrize("insert_mode", [0, 1, 2])
+@pytest.mark.parametrize("theta", [B_SQRT2_THETA, 30.0])
+def test_tail_loop_identical(built, monkeypatch, insert_mode, theta):
+    """The device-resident tail loop (k_tail_loop: incremental collect from the
+    last list + the dirty elements, the block-mode batch, no host round trip)
+    gives the very mesh the per-batch host loop gives (GDP2D_TAIL_LOOP=0), in
+    every insertion policy."""
+    from paper_2007_00324_b200 import Engine, EngineConfig, QualityCriteria, host
+    pts, segs = host.generate_pslg(100_000, 10_000, "gaussian", 31)
+    m, _ = host.build_cdt(pts, segs)
+    q = QualityCriteria(theta)
+    outs = []
+    for env in ({}, {"GDP2D_TAIL_LOOP": "0"}):
+        monkeypatch.delenv("GDP2D_TAIL_LOOP", raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        with Engine(0) as eng:
+            eng.upload(m)
+            rep = eng.refine(q, EngineConfig(insert_mode=insert_mode))
+            v = eng.validate(q)
+            assert v["bad_triangles"] == 0 and v["cdt_violations"] == 0, v
+            outs.append((rep, eng.download()))
+    (r0, a), (r1, b) = outs
+    assert len(r0.batches) == len(r1.batches) and r0.steiner_points == r1.steiner_points
+    for name in ("xy", "tri_v", "tri_n", "tri_seg", "tri_alive", "seg_v", "seg_alive",
+                 "vert_tri", "seg_tri"):
+        assert np.array_equal(getattr(a, name), getattr(b, name)), name
