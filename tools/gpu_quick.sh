@@ -4,8 +4,8 @@
 #   gpurun -- 'bash tools/gpu_quick.sh TAG [KEXPR]'
 TAG=${1:-rXX}; K=${2:-golden}
 O=gpurun_out
-if [ "$K" = "all" ]; then KA=""; else KA="-k $K"; fi
-timeout 1500 python -m pytest tests -m gpu -q --timeout 900 -x $KA > $O/${TAG}_pytest.log 2>&1
+if [ "$K" = "all" ]; then KA=""; else KA="-k"; fi
+timeout 1500 python -m pytest tests -m gpu -q --timeout 900 -x $KA ${KA:+"$K"} > $O/${TAG}_pytest.log 2>&1
 echo "pytest rc=$?"; tail -1 $O/${TAG}_pytest.log; grep -E "^FAILED|Error" $O/${TAG}_pytest.log | head -5
 for c in 3 2 4; do
   timeout 600 python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline --dropin-steps 0 > $O/${TAG}_bench_c$c.json 2>$O/${TAG}_bench_c$c.err
