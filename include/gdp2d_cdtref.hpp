@@ -24,6 +24,8 @@
  *     iteration_cap_hit, and the quality summary of refine.hpp:614-645);
  *   - cfg.execution / executor_count / seed are accepted and ignored (the GPU
  *     is the executor), as rule3_gamma / rule5 are ignored by the reference;
+ *   - on an error the mesh's element vectors are left unspecified (the
+ *     reference leaves a partially refined mesh behind a MeshError too);
  *   - errors: a device structural failure throws cdtref::MeshError
  *     (MeshErrc::StaleHandle), capacity / CUDA / argument failures throw
  *     std::runtime_error carrying gdp2d_last_error().  There is no CPU
@@ -232,6 +234,27 @@ inline void unpack(const gdp2d_mesh_buf& b, cdtref::Mesh& m) {
     m.batch_epoch = b.batch_epoch;
 }
 
+// Expected output/input size ratio of a refinement: ~2x at radius-edge
+// sqrt(2), ~5x at 30 degrees (BASELINE configs 2-4).  Only a hint: a larger
+// output just grows again in unpack.
+inline double growth_hint(const cdtref::QualityCriteria& q) {
+    return q.theta >= 28.0 ? 5.5 : q.theta >= 24.0 ? 3.5 : 2.2;
+}
+
+// While the GPU refines, grow the caller's element vectors to the expected
+// output size on a host thread: std::vector's value-initialisation of the new
+// tail is serial, and this way it runs during gdp2d_refine instead of after
+// it.  Their contents are already packed, so they are not copied.
+inline void pregrow(cdtref::Mesh& m, double g) {
+    auto grow = [g](auto& v) {
+        const size_t n = static_cast<size_t>(static_cast<double>(v.size()) * g);
+        if (n > v.capacity()) resize_for_overwrite(v, n);
+    };
+    grow(m.vertices);
+    grow(m.triangles);
+    grow(m.subsegments);
+}
+
 inline void throw_status(int rc) {
     const std::string what = std::string("gdp2d_refine: ") + gdp2d_last_error();
     if (rc == GDP2D_EMESH) throw cdtref::MeshError(cdtref::MeshErrc::StaleHandle, what);
@@ -252,7 +275,17 @@ inline cdtref::RunReport refine(cdtref::Mesh& m, const cdtref::QualityCriteria& 
     r.batches = bm.data();
     r.batches_capacity = static_cast<uint32_t>(bm.size());
     gdp2d_mesh_buf out{};
-    const int rc = gdp2d_refine(&in.view, &out, &p, &r, device);
+    int rc;
+    {
+        // the element vectors are packed: grow them while the device works
+        // (vert_tri / seg_tri stay untouched: the view reads them in place)
+        std::thread grow([&m, g = detail::growth_hint(q)] { detail::pregrow(m, g); });
+        struct Join {
+            std::thread& t;
+            ~Join() { t.join(); }
+        } join{grow};
+        rc = gdp2d_refine(&in.view, &out, &p, &r, device);
+    }
     if (rc != GDP2D_OK) detail::throw_status(rc);
     detail::unpack(out, m);
     gdp2d_free(&out);

@@ -299,7 +299,8 @@ void gdp2d_host_free_buf(gdp2d_mesh_buf* b) {
 // fresh copy of it (the copy is untimed).  Writes the summed call time and
 // the last call's Steiner count.  parts (optional, 4 doubles): summed seconds
 // of the shim's steps, timed separately on a further copy -- AoS->SoA pack,
-// gdp2d_refine (H2D + loop + D2H), SoA->AoS unpack, gdp2d_free.
+// gdp2d_refine (H2D + loop + D2H, with the vectors' pre-growth beside it),
+// SoA->AoS unpack, gdp2d_free.
 int gdp2d_host_time_dropin(const gdp2d_mesh_view* in, double theta_deg, int steps, int device,
                            double* seconds, uint64_t* steiner, double* parts) {
     try {
@@ -333,8 +334,12 @@ int gdp2d_host_time_dropin(const gdp2d_mesh_view* in, double theta_deg, int step
                 r.batches = bm.data();
                 r.batches_capacity = (uint32_t)bm.size();
                 gdp2d_mesh_buf out{};
-                if (gdp2d_refine(&pk.view, &out, &p, &r, device) != GDP2D_OK)
-                    throw std::runtime_error(gdp2d_last_error());
+                std::thread grow([&m, g = gdp2d::detail::growth_hint(q)] {
+                    gdp2d::detail::pregrow(m, g);
+                });
+                const int rc = gdp2d_refine(&pk.view, &out, &p, &r, device);
+                grow.join();
+                if (rc != GDP2D_OK) throw std::runtime_error(gdp2d_last_error());
                 const auto t2 = clk::now();
                 gdp2d::detail::unpack(out, m);
                 const auto t3 = clk::now();
