@@ -224,17 +224,19 @@ __device__ __forceinline__ void fixup_one(const DevMesh& m, u32 round, const Tri
 // Test one work item (is_non_delaunay_edge mesh.hpp:430-437) on its canonical
 // side (lower triangle id) and claim both triangles with the edge code as key:
 // the minimum key wins, so a round's flip set is deterministic.
-__device__ __forceinline__ void flip_test_one(const DevMesh& m, u32 code, const TriAux& x,
-                                              const WorkLists& w, RoundCtr* rc, Counters* ctr) {
+// The test itself: true for a flip candidate (claims made), with its key
+// (canonical side) and the far side's code.
+__device__ __forceinline__ bool flip_test_eval(const DevMesh& m, u32 code, const TriAux& x,
+                                               u32& key_out, u32& uc_out) {
     u32 t = etri(code);
     int e = eidx(code);
-    if (t >= m.nT) return;
+    if (t >= m.nT) return false;
     // record loads issued together: the dependent chain is t's record ->
     // the neighbour's corners -> the four coordinates
     const uint4 tv0 = m.tv[t], tn0 = m.tn[t];
-    if (!tv0.w) return;
+    if (!tv0.w) return false;
     const u32 c = comp(tn0, e);
-    if (c == NONE || has_seg(tv0, e)) return;
+    if (c == NONE || has_seg(tv0, e)) return false;
     u32 u = etri(c);
     int f = eidx(c);
     const uint4 tvu = m.tv[u];
@@ -250,23 +252,39 @@ __device__ __forceinline__ void flip_test_one(const DevMesh& m, u32 code, const 
         u = tt;
         f = ee;
     }
-    if (incircle(m.xy[tv.x], m.xy[tv.y], m.xy[tv.z], m.xy[d]) <= 0) return;
+    if (incircle(m.xy[tv.x], m.xy[tv.y], m.xy[tv.z], m.xy[d]) <= 0) return false;
     const u32 key = enc(t, e);
     atomicMin(&x.owner[t], key);
     atomicMin(&x.owner[u], key);
-    const u32 o = agg_reserve(&rc->cand, 1u);
+    key_out = key;
+    uc_out = enc(u, f);
+    return true;
+}
+
+__device__ __forceinline__ void flip_cand_store(const WorkLists& w, u32 o, u32 key, u32 uc,
+                                                Counters* ctr) {
     if (o < w.cap) {
         w.fc[o] = key;
-        w.fu[o] = enc(u, f);
+        w.fu[o] = uc;
     } else {
         raise_err(ctr, DERR_WORKLIST_OVERFLOW, o);
     }
 }
 
+__device__ __forceinline__ void flip_test_one(const DevMesh& m, u32 code, const TriAux& x,
+                                              const WorkLists& w, RoundCtr* rc, Counters* ctr) {
+    u32 key, uc;
+    if (!flip_test_eval(m, code, x, key, uc)) return;
+    flip_cand_store(w, agg_reserve(&rc->cand, 1u), key, uc, ctr);
+}
+
 // flip (mesh.hpp:210-258) as a phase-A rewrite: t := (a,b,d), u := (a,d,c).
-__device__ __forceinline__ u32 flip_apply_one(const DevMesh& m, u32 i, u32 round, u32 widx,
-                                              const TriAux& x, const WorkLists& w, RoundCtr* rc,
-                                              Counters* ctr) {
+// Everything but the two list appends (the rewritten pair -> touched, its four
+// outer edges -> the next work list); returns true when it flipped (t_out,
+// u_out = the pair).
+__device__ __forceinline__ bool flip_apply_core(const DevMesh& m, u32 i, u32 round,
+                                                const TriAux& x, const WorkLists& w,
+                                                Counters* ctr, u32& t_out, u32& u_out) {
     const u32 key = w.fc[i], uc = w.fu[i];
     const u32 t = etri(key), u = etri(uc);
     const int e = eidx(key), f = eidx(uc);
@@ -279,7 +297,7 @@ __device__ __forceinline__ u32 flip_apply_one(const DevMesh& m, u32 i, u32 round
     const bool won = ot == key && ou == key;
     w.fwin[i] = won;
     // exactly one duplicate performs the flip
-    if (!won || atomicExch(&x.stamp[t], round) == round) return 0;
+    if (!won || atomicExch(&x.stamp[t], round) == round) return false;
     const u32 a = comp(tv, e), b = comp(tv, nxt(e)), c = comp(tv, prv(e));
     const u32 d = comp(uv, f);
     const double2 pa = m.xy[a], pb = m.xy[b], pc = m.xy[c], pd = m.xy[d];
@@ -291,7 +309,7 @@ __device__ __forceinline__ u32 flip_apply_one(const DevMesh& m, u32 i, u32 round
             ctr->dbg[0] = pa.x; ctr->dbg[1] = pa.y; ctr->dbg[2] = pb.x; ctr->dbg[3] = pb.y;
             ctr->dbg[4] = pc.x; ctr->dbg[5] = pc.y; ctr->dbg[6] = pd.x; ctr->dbg[7] = pd.y;
         }
-        return 0;
+        return false;
     }
     write_tri(m, t, a, b, d, comp(un, nxt(f)), enc(u, 2), comp(tn, prv(e)), 5u,
               comp(us, nxt(f)), NONE, comp(ts, prv(e)), w.vtri_from);
@@ -303,6 +321,33 @@ __device__ __forceinline__ u32 flip_apply_one(const DevMesh& m, u32 i, u32 round
     x.emap[3 * u + nxt(f)] = enc(t, 0);
     x.emap[3 * u + prv(f)] = enc(u, 0);
     x.emap[3 * u + f] = NONE;
+    t_out = t;
+    u_out = u;
+    return true;
+}
+
+// The appends of a flip at reserved slots: touched [ot, ot+2), work [ow, ow+4).
+__device__ __forceinline__ void flip_appends(const WorkLists& w, u32 widx, u32 t, u32 u, u32 ot,
+                                             u32 ow, Counters* ctr) {
+    if (ot + 2 <= w.cap) {
+        w.touched[ot] = t;
+        w.touched[ot + 1] = u;
+    }
+    if (ow + 4 > w.cap) {
+        raise_err(ctr, DERR_WORKLIST_OVERFLOW, ow);
+        return;
+    }
+    w.w[widx][ow] = enc(t, 0);
+    w.w[widx][ow + 1] = enc(t, 2);
+    w.w[widx][ow + 2] = enc(u, 0);
+    w.w[widx][ow + 3] = enc(u, 1);
+}
+
+__device__ __forceinline__ u32 flip_apply_one(const DevMesh& m, u32 i, u32 round, u32 widx,
+                                              const TriAux& x, const WorkLists& w, RoundCtr* rc,
+                                              Counters* ctr) {
+    u32 t, u;
+    if (!flip_apply_core(m, i, round, x, w, ctr, t, u)) return 0;
     const u32 tl[2] = {t, u};
     push_touched(w, tl, 2, rc);
     const u32 codes[4] = {enc(t, 0), enc(t, 2), enc(u, 0), enc(u, 1)};
@@ -310,14 +355,21 @@ __device__ __forceinline__ u32 flip_apply_one(const DevMesh& m, u32 i, u32 round
     return 1;
 }
 
-// Release claims; a loser whose triangles were both left untouched retries.
-__device__ __forceinline__ void flip_post_one(u32 i, u32 round, u32 widx, const TriAux& x,
-                                              const WorkLists& w, RoundCtr* rc, Counters* ctr) {
+// Release claims; a loser whose triangles were both left untouched retries
+// (returns its key to re-queue, or NONE).
+__device__ __forceinline__ u32 flip_post_core(u32 i, u32 round, const TriAux& x,
+                                              const WorkLists& w) {
     const u32 key = w.fc[i], uc = w.fu[i];
     const u32 t = etri(key), u = etri(uc);
     x.owner[t] = NONE;
     x.owner[u] = NONE;
-    if (!w.fwin[i] && x.stamp[t] != round && x.stamp[u] != round) {
+    return (!w.fwin[i] && x.stamp[t] != round && x.stamp[u] != round) ? key : NONE;
+}
+
+__device__ __forceinline__ void flip_post_one(u32 i, u32 round, u32 widx, const TriAux& x,
+                                              const WorkLists& w, RoundCtr* rc, Counters* ctr) {
+    const u32 key = flip_post_core(i, round, x, w);
+    if (key != NONE) {
         const u32 codes[1] = {key};
         push_work(w, widx, codes, 1, ctr, rc);
     }

@@ -60,6 +60,24 @@ __device__ __forceinline__ u32 block_sum(u32 v, u32* sh) {
     return t;  // valid in thread 0 only
 }
 
+// Block-aggregated reservation of k slots per thread in a global work list:
+// one atomicAdd per CTA (instead of one per warp, agg_reserve) on the list's
+// counter, whose same-address atomics otherwise queue thousands deep at mesh
+// scale.  Returns the thread's first slot.  Every thread of the block must call
+// it (k may be 0).
+template <int BLOCK>
+__device__ __forceinline__ u32 block_reserve(u32* ctr, u32 k) {
+    __shared__ u32 sh[BLOCK / 32 + 1];
+    __shared__ u32 base;
+    u32 tot;
+    const u32 pre = block_exclusive_t<BLOCK, u32>(k, sh, &tot);
+    if (threadIdx.x == 0 && tot) base = atomicAdd(ctr, tot);
+    __syncthreads();
+    const u32 b = base;
+    __syncthreads();   // the next call's write of base must not overtake this read
+    return b + pre;
+}
+
 // Block-aggregated counter add: one global atomic per CTA instead of one per
 // warp (a same-address atomic per warp still serialises ~10^4 deep at mesh
 // scale).  Every thread of the block must call it.
