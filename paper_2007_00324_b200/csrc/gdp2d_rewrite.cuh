@@ -36,16 +36,17 @@ __device__ __forceinline__ void write_tri(const DevMesh& m, u32 t, u32 a, u32 b,
     if (s2 != NONE) m.stri[s2] = NONE, m.sflag[s2] = 2;
 }
 
+// slot: a slot reserved beforehand (block_reserve), or NONE to reserve here
 __device__ __forceinline__ void push_touched(const WorkLists& w, const u32* ts, int k,
-                                             RoundCtr* rc = nullptr) {
-    const u32 o = agg_reserve(&(rc ? rc : w.rc)->touched, (u32)k);
+                                             RoundCtr* rc = nullptr, u32 slot = NONE) {
+    const u32 o = slot != NONE ? slot : agg_reserve(&(rc ? rc : w.rc)->touched, (u32)k);
     for (int j = 0; j < k; ++j)
         if (o + j < w.cap) w.touched[o + j] = ts[j];
 }
 
 __device__ __forceinline__ void push_work(const WorkLists& w, u32 widx, const u32* codes, int k,
-                                          Counters* ctr, RoundCtr* rc = nullptr) {
-    const u32 o = agg_reserve(&(rc ? rc : w.rc)->wl_next, (u32)k);
+                                          Counters* ctr, RoundCtr* rc = nullptr, u32 slot = NONE) {
+    const u32 o = slot != NONE ? slot : agg_reserve(&(rc ? rc : w.rc)->wl_next, (u32)k);
     if (o + k > w.cap) {
         raise_err(ctr, DERR_WORKLIST_OVERFLOW, o);
         return;
@@ -58,9 +59,11 @@ __device__ __forceinline__ void push_work(const WorkLists& w, u32 widx, const u3
 // spokes (wv, a) need no test: an empty circle through wv and a exists inside
 // the old circumcircle, so they are Delaunay edges (Lawson insertion); the
 // flips that later change a spoke's quad push it again (flip_apply_one).
+// slots (optional): [touched, work] slots reserved by the caller (block_reserve)
 static __device__ void split_triangle_A(const DevMesh& m, const TriAux& x, const WorkLists& w, u32 t,
                                  u32 wv, u32 t1, u32 t2, u32 round, RoundCtr* rc = nullptr,
-                                 int seed = 0, Counters* ctr = nullptr) {
+                                 int seed = 0, Counters* ctr = nullptr,
+                                 const u32* slots = nullptr) {
     const uint4 ov = m.tv[t], on = m.tn[t], os = load_ts(m, t, ov);
     x.stamp[t] = round;
     write_tri(m, t, ov.x, ov.y, wv, enc(t1, 1), enc(t2, 0), on.z, 4u, NONE, NONE, os.z, w.vtri_from);
@@ -71,10 +74,10 @@ static __device__ void split_triangle_A(const DevMesh& m, const TriAux& x, const
     x.emap[3 * t + 2] = enc(t, 2);
     m.vtri[wv] = NONE;
     const u32 tl[3] = {t, t1, t2};
-    push_touched(w, tl, 3, rc);
+    push_touched(w, tl, 3, rc, slots ? slots[0] : NONE);
     if (seed) {
         const u32 codes[3] = {enc(t, 2), enc(t1, 2), enc(t2, 2)};
-        push_work(w, 0, codes, 3, ctr, rc);
+        push_work(w, 0, codes, 3, ctr, rc, slots ? slots[1] : NONE);
     }
 }
 
@@ -84,7 +87,8 @@ static __device__ void split_triangle_A(const DevMesh& m, const TriAux& x, const
 // empty-circle guarantee for the edge halves).
 static __device__ void split_edge_A(const DevMesh& m, const TriAux& x, const WorkLists& w, u32 t, int e,
                              u32 wv, u32 t2, u32 u2, u32 s_bw, u32 s_wc, u32 round,
-                             RoundCtr* rc = nullptr, int seed = 0, Counters* ctr = nullptr) {
+                             RoundCtr* rc = nullptr, int seed = 0, Counters* ctr = nullptr,
+                             const u32* slots = nullptr) {
     const uint4 ov = m.tv[t], on = m.tn[t], os = load_ts(m, t, ov);
     const u32 a = comp(ov, e), b = comp(ov, nxt(e)), c = comp(ov, prv(e));
     const u32 uc = comp(on, e);
@@ -100,14 +104,14 @@ static __device__ void split_edge_A(const DevMesh& m, const TriAux& x, const Wor
         x.emap[3 * t + e] = NONE;
         m.vtri[wv] = NONE;
         const u32 tl[2] = {t, t2};
-        push_touched(w, tl, 2, rc);
+        push_touched(w, tl, 2, rc, slots ? slots[0] : NONE);
         if (seed && s_bw != NONE) {
             const u32 codes[2] = {enc(t, 2), enc(t2, 1)};
-            push_work(w, 0, codes, 2, ctr, rc);
+            push_work(w, 0, codes, 2, ctr, rc, slots ? slots[1] : NONE);
         } else if (seed) {
             const u32 codes[6] = {enc(t, 0), enc(t, 1), enc(t, 2), enc(t2, 0), enc(t2, 1),
                                   enc(t2, 2)};
-            push_work(w, 0, codes, 6, ctr, rc);
+            push_work(w, 0, codes, 6, ctr, rc, slots ? slots[1] : NONE);
         }
         return;
     }
@@ -134,18 +138,18 @@ static __device__ void split_edge_A(const DevMesh& m, const TriAux& x, const Wor
     x.emap[3 * u + f] = NONE;
     m.vtri[wv] = NONE;
     const u32 tl[4] = {t, t2, u, u2};
-    push_touched(w, tl, 4, rc);
+    push_touched(w, tl, 4, rc, slots ? slots[0] : NONE);
     if (seed && s_bw != NONE) {
         // subsegment midpoint: the halves are constrained and the spokes
         // (w,a), (w,d) are constrained-Delaunay (a circle through a and w
         // inside the empty circumcircle of (a,b,c)); only the link edges
         const u32 codes[4] = {enc(t, 2), enc(t2, 1), enc(u, 2), enc(u2, 1)};
-        push_work(w, 0, codes, 4, ctr, rc);
+        push_work(w, 0, codes, 4, ctr, rc, slots ? slots[1] : NONE);
     } else if (seed) {
         const u32 codes[12] = {enc(t, 0), enc(t, 1), enc(t, 2), enc(t2, 0), enc(t2, 1),
                                enc(t2, 2), enc(u, 0), enc(u, 1), enc(u, 2), enc(u2, 0),
                                enc(u2, 1), enc(u2, 2)};
-        push_work(w, 0, codes, 12, ctr, rc);
+        push_work(w, 0, codes, 12, ctr, rc, slots ? slots[1] : NONE);
     }
 }
 

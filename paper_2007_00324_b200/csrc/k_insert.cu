@@ -39,10 +39,12 @@ namespace gdp2d {
 
 // One surviving candidate's phase-1 insertion (refine.hpp:492-539).
 // Returns 1 = midpoint, 2 = circumcenter, 0 = nothing.
+// slots (optional): the [touched, work] list slots reserved for it
+// (split_appends gives the sizes).
 __device__ __forceinline__ int apply_one(const DevMesh& m, const DevCands& c, u32 i, u32 batch,
                                          u32 round, const InsertBufs& b, const TriAux& x,
                                          const FreshInfo& f, const WorkLists& w, RoundCtr* rc,
-                                         int seed, Counters* ctr) {
+                                         int seed, Counters* ctr, const u32* slots = nullptr) {
     if (!b.nv[i]) return 0;
     const u32 wv = m.nV + b.ov[i];
     const u32 nt0 = m.nT + b.ot[i];
@@ -80,15 +82,35 @@ __device__ __forceinline__ int apply_one(const DevMesh& m, const DevCands& c, u3
         m.stri[s_wc] = NONE;
         m.salive[s] = 0;
         m.senc[s] = 0;
-        split_edge_A(m, x, w, t, e, wv, nt0, nt0 + 1, s_bw, s_wc, round, rc, seed, ctr);
+        split_edge_A(m, x, w, t, e, wv, nt0, nt0 + 1, s_bw, s_wc, round, rc, seed, ctr, slots);
         return 1;
     }
     if (c.lkind[i] == 0) {
-        split_triangle_A(m, x, w, t, wv, nt0, nt0 + 1, round, rc, seed, ctr);
+        split_triangle_A(m, x, w, t, wv, nt0, nt0 + 1, round, rc, seed, ctr, slots);
     } else {
-        split_edge_A(m, x, w, t, c.ledge[i], wv, nt0, nt0 + 1, NONE, NONE, round, rc, seed, ctr);
+        split_edge_A(m, x, w, t, c.ledge[i], wv, nt0, nt0 + 1, NONE, NONE, round, rc, seed, ctr,
+                     slots);
     }
     return 2;
+}
+
+// The list appends apply_one(seed = 1) makes for candidate i: touched
+// triangles and Lawson seeds (split_triangle_A / split_edge_A).
+__device__ __forceinline__ void split_appends(const DevCands& c, u32 i, const InsertBufs& b,
+                                              u32& nt_out, u32& nw_out) {
+    nt_out = nw_out = 0;
+    if (!b.nv[i]) return;
+    const u32 nt = b.nt[i];   // 2: the split edge has a far side (or 1 -> 3)
+    if (c.kind[i] == 0) {             // subsegment midpoint: the link edges only
+        nt_out = 2 * nt;
+        nw_out = 2 * nt;
+    } else if (c.lkind[i] == 0) {     // 1 -> 3
+        nt_out = 3;
+        nw_out = 3;
+    } else {                          // point on an edge: every edge of the new triangles
+        nt_out = 2 * nt;
+        nw_out = 6 * nt;
+    }
 }
 
 // Whole Lawson fixpoint in ONE persistent cooperative launch: each round is
@@ -1023,10 +1045,28 @@ __device__ void split_and_flip(const InsertArgs& a, const Exec& ex, u32 nv, u32 
     ring_advance(a, ex, step);
     {
         const u32 round = a.round0 + step;
-        for (u32 i = ex.tid; i < C; i += ex.nthr) {
-            const int r = apply_one(m, a.c, i, a.batch, round, a.b, a.x, a.f, w, rc, 1, a.ctr);
-            mid += r == 1;
-            cc += r == 2;
+        if (ex.block) {
+            for (u32 i = ex.tid; i < C; i += ex.nthr) {
+                const int r = apply_one(m, a.c, i, a.batch, round, a.b, a.x, a.f, w, rc, 1, a.ctr);
+                mid += r == 1;
+                cc += r == 2;
+            }
+        } else {
+            // waves: one touched / seed reservation per CTA (block_reserve)
+            for (u32 base = ex.tid - threadIdx.x; base < C; base += ex.nthr) {
+                const u32 i = base + threadIdx.x;
+                u32 ntc = 0, nwc = 0;
+                if (i < C) split_appends(a.c, i, a.b, ntc, nwc);
+                u32 slots[2];
+                slots[0] = block_reserve<INSERT_BLOCK>(&rc->touched, ntc);
+                slots[1] = block_reserve<INSERT_BLOCK>(&rc->wl_next, nwc);
+                if (i < C) {
+                    const int r = apply_one(m, a.c, i, a.batch, round, a.b, a.x, a.f, w, rc, 1,
+                                            a.ctr, slots);
+                    mid += r == 1;
+                    cc += r == 2;
+                }
+            }
         }
         m.nV += nv;
         m.nT += nt;
