@@ -428,6 +428,30 @@ __device__ __forceinline__ void rm_claim_one(const DevMesh& m, const u32* __rest
 // (ids reused in star order), the last two die.
 // Lawson seeds of the rebuilt star go to seed_rc->wl_next (so successive
 // removal rounds can accumulate one list for a single Lawson pass).
+// What a removal leaves for the caller to append when it reserves the list
+// slots itself (grid mode, block_reserve): deferred, or `created` rebuilt
+// triangles (touched + their 3 * created edges as Lawson seeds).
+struct RmOut {
+    u32 defer;
+    int created;
+};
+
+// touched slot ot (NONE: already pushed) and seed slot os of a removal's
+// rebuilt star st[0..created).
+__device__ __forceinline__ void rm_appends(const WorkLists& w, u32 widx, const u32* st,
+                                           int created, u32 ot, u32 os, Counters* ctr) {
+    if (ot != NONE)
+        for (int ci = 0; ci < created; ++ci)
+            if (ot + ci < w.cap) w.touched[ot + ci] = st[ci];
+    const u32 ns = 3u * (u32)created;
+    if (os + ns > w.cap) {
+        raise_err(ctr, DERR_WORKLIST_OVERFLOW, os);
+        return;
+    }
+    for (int ci = 0; ci < created; ++ci)
+        for (int e = 0; e < 3; ++e) w.w[widx][os + 3 * ci + e] = enc(st[ci], e);
+}
+
 // N: capacity of the thread-local link arrays.  The common small star runs
 // with N = 16 (a compact local frame that stays in L1); larger stars take the
 // MAX_STAR instantiation (rm_apply_one dispatches on the star size).
@@ -436,7 +460,7 @@ __device__ __noinline__ u32 rm_apply_one_n(const DevMesh& m, const u32* __restri
                                            u32 round, u32 V0, u32 widx, u32 next_list,
                                            const TriAux& x, const FreshInfo& f,
                                            const WorkLists& w, RoundCtr* rc, Counters* ctr,
-                                           RoundCtr* seed_rc) {
+                                           RoundCtr* seed_rc, RmOut* out) {
     u32 done = 0;
     {
         const u32 v = list[i];
@@ -447,8 +471,12 @@ __device__ __noinline__ u32 rm_apply_one_n(const DevMesh& m, const u32* __restri
 #pragma unroll 8
         for (int q = 0; q < k; ++q) own &= x.owner[st[q]] == v;
         if (k >= 3 && !own) {
-            const u32 o = agg_reserve(&rc->rm_next, 1u);
-            if (o < w.rm_cap) w.rm[next_list][o] = v;
+            if (out) {
+                out->defer = 1;
+            } else {
+                const u32 o = agg_reserve(&rc->rm_next, 1u);
+                if (o < w.rm_cap) w.rm[next_list][o] = v;
+            }
         } else if (own) {
             // Link polygon, CCW: L[j] = p_j; link edge j = (L[j], L[j+1]).
             u32 L[N], R[N], SG[N], ORG[N];
@@ -598,18 +626,15 @@ __device__ __noinline__ u32 rm_apply_one_n(const DevMesh& m, const u32* __restri
                 m.valive[v] = 0;
                 m.vtri[v] = NONE;
                 f.removed[v - V0] = 1;
-                push_touched(w, st, created, rc);
-                {
+                if (out) {
+                    out->created = created;   // the caller appends (rm_appends)
+                } else {
+                    push_touched(w, st, created, rc);
                     // every edge of the rebuilt hole seeds the Lawson pass: one
                     // reservation for all of them
                     const u32 ns = 3u * (u32)created;
-                    const u32 o = agg_reserve(&seed_rc->wl_next, ns);
-                    if (o + ns > w.cap) {
-                        raise_err(ctr, DERR_WORKLIST_OVERFLOW, o);
-                    } else {
-                        for (int ci = 0; ci < created; ++ci)
-                            for (int e = 0; e < 3; ++e) w.w[widx][o + 3 * ci + e] = enc(st[ci], e);
-                    }
+                    rm_appends(w, widx, st, created, NONE, agg_reserve(&seed_rc->wl_next, ns),
+                               ctr);
                 }
                 done = 1;
             }
@@ -622,12 +647,12 @@ __device__ __forceinline__ u32 rm_apply_one(const DevMesh& m, const u32* __restr
                                             u32 round, u32 V0, u32 widx, u32 next_list,
                                             const TriAux& x, const FreshInfo& f,
                                             const WorkLists& w, RoundCtr* rc, Counters* ctr,
-                                            RoundCtr* seed_rc) {
+                                            RoundCtr* seed_rc, RmOut* out = nullptr) {
     if (w.star_len[i] <= 16u)
         return rm_apply_one_n<16>(m, list, i, round, V0, widx, next_list, x, f, w, rc, ctr,
-                                  seed_rc);
+                                  seed_rc, out);
     return rm_apply_one_n<MAX_STAR>(m, list, i, round, V0, widx, next_list, x, f, w, rc, ctr,
-                                    seed_rc);
+                                    seed_rc, out);
 }
 
 __device__ __forceinline__ void rm_post_one(u32 i, const TriAux& x, const WorkLists& w) {
@@ -1218,9 +1243,28 @@ __device__ void rollback_loop(const InsertArgs& a, const Exec& ex, u32 nv, u32 n
             for (u32 i = ex.tid; i < nrm; i += ex.nthr) rm_claim_one(m, list, i, V0, a.x, a.f, w, a.ctr);
             ex.sync();
             trace(a, ex.leader(), TR_RM_CLAIM, nrm);
-            for (u32 i = ex.tid; i < nrm; i += ex.nthr)
-                done += rm_apply_one(m, list, i, round, V0, 0, rcur ^ 1u, a.x, a.f, w, rc, a.ctr,
-                                     seed_rc);
+            if (ex.block) {
+                for (u32 i = ex.tid; i < nrm; i += ex.nthr)
+                    done += rm_apply_one(m, list, i, round, V0, 0, rcur ^ 1u, a.x, a.f, w, rc,
+                                         a.ctr, seed_rc);
+            } else {
+                // waves: one reservation per CTA for each list (block_reserve)
+                for (u32 base = ex.tid - threadIdx.x; base < nrm; base += ex.nthr) {
+                    const u32 i = base + threadIdx.x;
+                    RmOut ro{0u, 0};
+                    if (i < nrm)
+                        done += rm_apply_one(m, list, i, round, V0, 0, rcur ^ 1u, a.x, a.f, w, rc,
+                                             a.ctr, seed_rc, &ro);
+                    const u32 od = block_reserve<ROLLBACK_BLOCK>(&rc->rm_next, ro.defer);
+                    const u32 ot = block_reserve<ROLLBACK_BLOCK>(&rc->touched, (u32)ro.created);
+                    const u32 os =
+                        block_reserve<ROLLBACK_BLOCK>(&seed_rc->wl_next, 3u * (u32)ro.created);
+                    if (ro.defer && od < w.rm_cap) w.rm[rcur ^ 1u][od] = list[i];
+                    if (ro.created)
+                        rm_appends(w, 0, w.star + (size_t)i * MAX_STAR, ro.created, ot, os,
+                                   a.ctr);
+                }
+            }
             ex.sync();
             trace(a, ex.leader(), TR_RM_APPLY);
             for (u32 i = ex.tid; i < nrm; i += ex.nthr) rm_post_one(i, a.x, w);
