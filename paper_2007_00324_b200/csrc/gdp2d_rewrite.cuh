@@ -13,6 +13,7 @@
 
 #include "engine.h"
 #include "gdp2d_geom.cuh"
+#include "scan.cuh"
 
 namespace gdp2d {
 
@@ -376,6 +377,62 @@ __device__ __forceinline__ void flip_post_one(u32 i, u32 round, u32 widx, const 
     if (key != NONE) {
         const u32 codes[1] = {key};
         push_work(w, widx, codes, 1, ctr, rc);
+    }
+}
+
+// ---- grid-wide Lawson phases in waves --------------------------------------------
+//
+// The grid-mode rounds (refinement, device CDT, the parity hook) process their
+// lists in waves of one item per thread, and every wave reserves the slots it
+// appends with ONE atomic per CTA (block_reserve) instead of one per warp:
+// the list counters are single addresses, and their same-address atomics
+// queue thousands deep at mesh scale.  tid0 = the CTA's first grid thread,
+// nthr = grid threads.  Every thread of every CTA calls these.
+
+template <int BLOCK>
+__device__ __forceinline__ void flip_test_waves(const DevMesh& m, const u32* wl, u32 n, u32 tid0,
+                                                u32 nthr, const TriAux& x, const WorkLists& w,
+                                                RoundCtr* rc, Counters* ctr) {
+    for (u32 base = tid0; base < n; base += nthr) {
+        const u32 i = base + threadIdx.x;
+        u32 key = 0, uc = 0;
+        const bool cand = i < n && flip_test_eval(m, wl[i], x, key, uc);
+        const u32 o = block_reserve<BLOCK>(&rc->cand, cand ? 1u : 0u);
+        if (cand) flip_cand_store(w, o, key, uc, ctr);
+    }
+}
+
+template <int BLOCK>
+__device__ __forceinline__ u32 flip_apply_waves(const DevMesh& m, u32 nc, u32 round, u32 widx,
+                                                u32 tid0, u32 nthr, const TriAux& x,
+                                                const WorkLists& w, RoundCtr* rc, Counters* ctr) {
+    u32 flipped = 0;
+    for (u32 base = tid0; base < nc; base += nthr) {
+        const u32 i = base + threadIdx.x;
+        u32 t = 0, u = 0;
+        const bool fl = i < nc && flip_apply_core(m, i, round, x, w, ctr, t, u);
+        const u32 ot = block_reserve<BLOCK>(&rc->touched, fl ? 2u : 0u);
+        const u32 ow = block_reserve<BLOCK>(&rc->wl_next, fl ? 4u : 0u);
+        if (fl) flip_appends(w, widx, t, u, ot, ow, ctr);
+        flipped += fl;
+    }
+    return flipped;
+}
+
+template <int BLOCK>
+__device__ __forceinline__ void flip_post_waves(u32 nc, u32 round, u32 widx, u32 tid0, u32 nthr,
+                                                const TriAux& x, const WorkLists& w,
+                                                RoundCtr* rc, Counters* ctr) {
+    for (u32 base = tid0; base < nc; base += nthr) {
+        const u32 i = base + threadIdx.x;
+        const u32 key = i < nc ? flip_post_core(i, round, x, w) : NONE;
+        const u32 o = block_reserve<BLOCK>(&rc->wl_next, key != NONE ? 1u : 0u);
+        if (key != NONE) {
+            if (o < w.cap)
+                w.w[widx][o] = key;
+            else
+                raise_err(ctr, DERR_WORKLIST_OVERFLOW, o);
+        }
     }
 }
 

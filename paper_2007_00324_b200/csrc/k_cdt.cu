@@ -282,12 +282,14 @@ __global__ void __launch_bounds__(CDT_BLOCK, GDP2D_CDT_MINB) k_cdt_delaunay(cons
             ring_next(a, step, leader);
             const u32 round = a.round0 + step;
             const u32* wl = a.w.w[cur];
-            for (u32 i = tid; i < n; i += nthr) flip_test_one(m, wl[i], a.x, a.w, fr, a.ctr);
+            const u32 tid0 = tid - threadIdx.x;   // waves (flip_*_waves)
+            flip_test_waves<CDT_BLOCK>(m, wl, n, tid0, nthr, a.x, a.w, fr, a.ctr);
             g.sync();
             const u32 nc = min(vld(&fr->cand), a.w.cap);
-            for (u32 i = tid; i < nc; i += nthr) flipped += flip_apply_one(m, i, round, cur ^ 1u, a.x, a.w, fr, a.ctr);
+            flipped += flip_apply_waves<CDT_BLOCK>(m, nc, round, cur ^ 1u, tid0, nthr, a.x, a.w, fr,
+                                                   a.ctr);
             g.sync();
-            for (u32 i = tid; i < nc; i += nthr) flip_post_one(i, round, cur ^ 1u, a.x, a.w, fr, a.ctr);
+            flip_post_waves<CDT_BLOCK>(nc, round, cur ^ 1u, tid0, nthr, a.x, a.w, fr, a.ctr);
             const u32 nt = min(vld(&fr->touched), a.w.cap);
             for (u32 i = tid; i < nt; i += nthr) fixup_one(m, round, a.x, a.w, a.w.touched[i], 0, 0, fr, a.ctr);
             g.sync();

@@ -130,12 +130,13 @@ __global__ void __launch_bounds__(LAWSON_BLOCK) k_lawson_persistent(
         RoundCtr* rc = rcs + r;
         const u32 round = round0 + r;
         const u32* wl = w.w[cur];
-        for (u32 i = tid; i < n; i += nthr) flip_test_one(m, wl[i], x, w, rc, ctr);
+        const u32 tid0 = tid - threadIdx.x;
+        flip_test_waves<LAWSON_BLOCK>(m, wl, n, tid0, nthr, x, w, rc, ctr);
         g.sync();
         const u32 nc = min(*(volatile u32*)&rc->cand, w.cap);
-        for (u32 i = tid; i < nc; i += nthr) flipped += flip_apply_one(m, i, round, cur ^ 1u, x, w, rc, ctr);
+        flipped += flip_apply_waves<LAWSON_BLOCK>(m, nc, round, cur ^ 1u, tid0, nthr, x, w, rc, ctr);
         g.sync();
-        for (u32 i = tid; i < nc; i += nthr) flip_post_one(i, round, cur ^ 1u, x, w, rc, ctr);
+        flip_post_waves<LAWSON_BLOCK>(nc, round, cur ^ 1u, tid0, nthr, x, w, rc, ctr);
         const u32 nt = min(*(volatile u32*)&rc->touched, w.cap);
         for (u32 i = tid; i < nt; i += nthr) fixup_one(m, round, x, w, w.touched[i], 0, 0, rc, ctr);
         g.sync();
@@ -855,40 +856,17 @@ __device__ void lawson_fixpoint_dev(const InsertArgs& a, const Exec& ex, const D
         ring_advance(a, ex, step);
         const u32 round = a.round0 + step;
         const u32* wl = a.w.w[cur];
-        // waves of one item per thread: one candidate-list reservation per CTA
-        // and wave (block_reserve) instead of one per warp
-        for (u32 base = ex.tid - threadIdx.x; base < n; base += ex.nthr) {
-            const u32 i = base + threadIdx.x;
-            u32 key = 0, uc = 0;
-            const bool cand = i < n && flip_test_eval(m, wl[i], a.x, key, uc);
-            const u32 o = block_reserve<INSERT_BLOCK>(&rc->cand, cand ? 1u : 0u);
-            if (cand) flip_cand_store(a.w, o, key, uc, a.ctr);
-        }
+        // waves: one list reservation per CTA (flip_*_waves, gdp2d_rewrite.cuh)
+        const u32 tid0 = ex.tid - threadIdx.x;
+        flip_test_waves<INSERT_BLOCK>(m, wl, n, tid0, ex.nthr, a.x, a.w, rc, a.ctr);
         ex.sync();
         trace(a, ex.leader(), TR_FTEST, n);
         const u32 nc = min(vload(&rc->cand), a.w.cap);
-        for (u32 base = ex.tid - threadIdx.x; base < nc; base += ex.nthr) {
-            const u32 i = base + threadIdx.x;
-            u32 t = 0, u = 0;
-            const bool fl = i < nc && flip_apply_core(m, i, round, a.x, a.w, a.ctr, t, u);
-            const u32 ot = block_reserve<INSERT_BLOCK>(&rc->touched, fl ? 2u : 0u);
-            const u32 ow = block_reserve<INSERT_BLOCK>(&rc->wl_next, fl ? 4u : 0u);
-            if (fl) flip_appends(a.w, cur ^ 1u, t, u, ot, ow, a.ctr);
-            flipped += fl;
-        }
+        flipped += flip_apply_waves<INSERT_BLOCK>(m, nc, round, cur ^ 1u, tid0, ex.nthr, a.x, a.w,
+                                                  rc, a.ctr);
         ex.sync();
         trace(a, ex.leader(), TR_FAPPLY, nc);
-        for (u32 base = ex.tid - threadIdx.x; base < nc; base += ex.nthr) {
-            const u32 i = base + threadIdx.x;
-            const u32 key = i < nc ? flip_post_core(i, round, a.x, a.w) : NONE;
-            const u32 o = block_reserve<INSERT_BLOCK>(&rc->wl_next, key != NONE ? 1u : 0u);
-            if (key != NONE) {
-                if (o < a.w.cap)
-                    a.w.w[cur ^ 1u][o] = key;
-                else
-                    raise_err(a.ctr, DERR_WORKLIST_OVERFLOW, o);
-            }
-        }
+        flip_post_waves<INSERT_BLOCK>(nc, round, cur ^ 1u, tid0, ex.nthr, a.x, a.w, rc, a.ctr);
         const u32 nt = min(vload(&rc->touched), a.w.cap);
         for (u32 i = ex.tid; i < nt; i += ex.nthr)
             fixup_one(m, round, a.x, a.w, a.w.touched[i], 0, 0, rc, a.ctr);
