@@ -186,14 +186,15 @@ __device__ __forceinline__ int walk_star(const DevMesh& m, u32 v, u32* st, int* 
     u32 cur = t0;
     int k = 0;
     do {
-        const uint4 tv = m.tv[cur];
+        // both records at once: the step's only dependent level
+        const uint4 tv = m.tv[cur], tn = m.tn[cur];
         const int i = tv.x == v ? 0 : (tv.y == v ? 1 : (tv.z == v ? 2 : -1));
         if (i < 0) return 0;
         if (k >= cap) return -1;
         st[k] = cur;
         si[k] = i;
         ++k;
-        const u32 c = comp(m.tn[cur], nxt(i));
+        const u32 c = comp(tn, nxt(i));
         if (c == NONE) return 0;
         cur = etri(c);
     } while (cur != t0);
@@ -212,12 +213,13 @@ __device__ __forceinline__ int stream_star(const DevMesh& m, u32 v, Fn&& fn) {
     u32 cur = t0;
     int k = 0;
     do {
-        const uint4 tv = m.tv[cur];
+        // both records at once (fn's own loads cannot delay the next step)
+        const uint4 tv = m.tv[cur], tn = m.tn[cur];
         const int i = tv.x == v ? 0 : (tv.y == v ? 1 : (tv.z == v ? 2 : -1));
         if (i < 0 || k >= STAR_WALK_LIMIT) return 0;
         fn(cur, i, tv);
         ++k;
-        const u32 c = comp(m.tn[cur], nxt(i));
+        const u32 c = comp(tn, nxt(i));
         if (c == NONE) return 0;
         cur = etri(c);
     } while (cur != t0);
