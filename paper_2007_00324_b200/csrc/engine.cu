@@ -83,7 +83,8 @@ struct MeshStore {
 void mesh_free(MeshStore& s) {
     DevMesh& m = s.m;
     dfree(m.xy); dfree(m.vkind); dfree(m.vbirth); dfree(m.valive); dfree(m.vtri);
-    dfree(m.tv); dfree(m.tn); dfree(m.ts);
+    dfree(m.tr); dfree(m.ts);
+    bind_tris(m);
     dfree(m.sv); dfree(m.sparent); dfree(m.senc); dfree(m.salive); dfree(m.stri); dfree(m.sdepth);
     dfree(m.tflag); dfree(m.sflag);
     s.vcap = s.tcap = s.scap = 0;
@@ -100,8 +101,8 @@ void mesh_reserve(MeshStore& s, u32 V, u32 T, u32 S, cudaStream_t st) {
         s.vcap = V;
     }
     if (T > s.tcap) {
-        dgrow(m.tv, m.nT, T, st);
-        dgrow(m.tn, m.nT, T, st);
+        dgrow(m.tr, m.nT, T, st);
+        bind_tris(m);
         dgrow(m.ts, m.nT, T, st);
         dgrow(m.tflag, m.nT, T, st);
         s.tcap = T;
@@ -130,8 +131,7 @@ void mesh_copy(MeshStore& dst, const MeshStore& src, cudaStream_t st) {
     cp(b.vbirth, a.vbirth, 4ull * a.nV);
     cp(b.valive, a.valive, a.nV);
     cp(b.vtri, a.vtri, 4ull * a.nV);
-    cp(b.tv, a.tv, sizeof(uint4) * a.nT);
-    cp(b.tn, a.tn, sizeof(uint4) * a.nT);
+    cp(b.tr, a.tr, sizeof(TriRec) * a.nT);
     cp(b.ts, a.ts, sizeof(uint4) * a.nT);
     cp(b.sv, a.sv, sizeof(uint2) * a.nS);
     cp(b.sparent, a.sparent, 4ull * a.nS);
@@ -1682,8 +1682,8 @@ void build_cdt(gdp2d_ctx* x, const double* xy, u32 N, const u32* seg, u32 M,
     CK(cudaMemsetAsync(m.vtri, 0xFF, 4ull * (N + 3), st));
     const uint4 t0v[3] = {make_uint4(N, N + 1, N + 2, 1u), make_uint4(NONE, NONE, NONE, 0u),
                           make_uint4(NONE, NONE, NONE, 0u)};
-    CK(cudaMemcpyAsync(m.tv, &t0v[0], 16, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(m.tn, &t0v[1], 16, cudaMemcpyHostToDevice, st));
+    const TriRec t0r = {t0v[0], t0v[1]};
+    CK(cudaMemcpyAsync(m.tr, &t0r, sizeof t0r, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(m.ts, &t0v[2], 16, cudaMemcpyHostToDevice, st));
     m.nV = N + 3;
     m.nT = T;

@@ -4,6 +4,9 @@
 // HBM layout (structure of arrays, one mesh per GPU, pre-allocated with
 // headroom and grown by the host between batches):
 //   double2 xy[V]                       vertex coordinates (16 B, one LDG.128)
+//   TriRec  tr[T] = {tv, tn}            one 32-byte record per triangle, so the
+//                                       corners and the neighbours that nearly every
+//                                       step reads together share one DRAM burst:
 //   uint4   tv[T] = {v0, v1, v2, flags} triangle corners   (reference Triangle::v);
 //                                       flags = 0 dead, else bit 0 (alive) | bit 1+e
 //                                       when edge e carries a subsegment, so the hot
@@ -55,14 +58,27 @@ __host__ __device__ __forceinline__ u32 tri_flags(u32 s0, u32 s1, u32 s2) {
 __device__ __forceinline__ bool has_seg(const uint4& tv, int e) { return (tv.w >> (1 + e)) & 1u; }
 __device__ __forceinline__ bool any_seg(const uint4& tv) { return (tv.w & 14u) != 0u; }
 
+// tv / tn are views into the triangle records tr: element t at p[2 t].
+struct TriRec {
+    uint4 v, n;
+};
+struct RecField {
+    uint4* p;
+    __host__ __device__ __forceinline__ uint4& operator[](size_t t) const { return p[2 * t]; }
+    __host__ __device__ __forceinline__ u32* words(size_t t) const {
+        return reinterpret_cast<u32*>(p + 2 * t);
+    }
+};
+
 struct DevMesh {
     double2* xy;
     uint8_t* vkind;
     u32* vbirth;
     uint8_t* valive;
     u32* vtri;
-    uint4* tv;
-    uint4* tn;
+    TriRec* tr;
+    RecField tv;     // = {&tr->v}
+    RecField tn;     // = {&tr->n}
     uint4* ts;
     uint2* sv;
     u32* sparent;
@@ -78,6 +94,12 @@ struct DevMesh {
     uint8_t* sflag;
     u32 nV, nT, nS;
 };
+
+// re-point the tv / tn views after tr was (re)allocated
+__host__ __forceinline__ void bind_tris(DevMesh& m) {
+    m.tv.p = m.tr ? &m.tr->v : nullptr;
+    m.tn.p = m.tr ? &m.tr->n : nullptr;
+}
 
 // ts[t] for a triangle whose corners record tv is already loaded: the load is
 // skipped (all NONE) when no edge carries a subsegment -- most triangles.

@@ -171,7 +171,6 @@ __device__ __forceinline__ void fixup_one(const DevMesh& m, u32 round, const Tri
     if (!tv.w) return;
     const uint4 ts = load_ts(m, t, tv);
     const u32 pend = tn.w;
-    u32* tn_words = reinterpret_cast<u32*>(m.tn);
 #pragma unroll
     for (int e = 0; e < 3; ++e) {
         if (!((pend >> e) & 1u)) continue;
@@ -181,7 +180,7 @@ __device__ __forceinline__ void fixup_one(const DevMesh& m, u32 round, const Tri
         if (x.stamp[X] == round) {
             set_comp(tn, e, x.emap[3 * X + eidx(r)]);
         } else {
-            tn_words[4 * (size_t)X + eidx(r)] = enc(t, e);
+            m.tn.words(X)[eidx(r)] = enc(t, e);
         }
     }
     tn.w = 0;

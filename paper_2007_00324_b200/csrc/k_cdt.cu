@@ -677,7 +677,6 @@ __global__ void __launch_bounds__(CDT_BLOCK) k_cdt_recover(const __grid_constant
     const bool leader = tid == 0;
     const DevMesh& m = a.m;
     u32* tsw = reinterpret_cast<u32*>(m.ts);
-    u32* tvw = reinterpret_cast<u32*>(m.tv);
     u32 n = n0, cur = 0, step = 0, rounds = 0;
     u32 found = 0, pipes = 0, splits = 0, pmax = 0;
     ring_next(a, step + 3u, leader);
@@ -704,10 +703,10 @@ __global__ void __launch_bounds__(CDT_BLOCK) k_cdt_recover(const __grid_constant
                 // flag_edge (cdt.hpp:273-284); the lower piece keeps a shared edge
                 const u32 far = comp(m.tn[t], e);
                 atomicMin(&tsw[4 * (size_t)t + e], p);
-                atomicOr(&tvw[4 * (size_t)t + 3], 2u << e);   // the tv.w subsegment bit
+                atomicOr(&m.tv.words(t)[3], 2u << e);   // the tv.w subsegment bit
                 if (far != NONE) {
                     atomicMin(&tsw[4 * (size_t)etri(far) + eidx(far)], p);
-                    atomicOr(&tvw[4 * (size_t)etri(far) + 3], 2u << eidx(far));
+                    atomicOr(&m.tv.words(etri(far))[3], 2u << eidx(far));
                 }
                 a.plen[p] = 0;
                 ++found;

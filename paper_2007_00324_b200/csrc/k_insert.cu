@@ -621,9 +621,8 @@ __device__ __noinline__ u32 rm_apply_one_n(const DevMesh& m, const u32* __restri
                     write_tri(m, st[ci], CV[ci][0], CV[ci][1], CV[ci][2], CN[ci][0], CN[ci][1],
                               CN[ci][2], pend, CS[ci][0], CS[ci][1], CS[ci][2], w.vtri_from);
                 }
-                u32* tv_words = reinterpret_cast<u32*>(m.tv);
                 for (int q = created; q < k; ++q) {
-                    tv_words[4 * (size_t)st[q] + 3] = 0;   // dead (no read-modify-write)
+                    m.tv.words(st[q])[3] = 0;   // dead (no read-modify-write)
                     m.tflag[st[q]] = 2;
                 }
                 m.valive[v] = 0;
