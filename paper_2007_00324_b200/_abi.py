@@ -2,6 +2,7 @@
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 LIB_DIR = Path(__file__).resolve().parent / "lib"
@@ -201,6 +202,8 @@ def _load(name: str, sigs: dict) -> C.CDLL:
     if name in _LIBS:
         return _LIBS[name]
     path = LIB_DIR / name
+    if name == "libgdp2d.so" and os.environ.get("GDP2D_ENGINE_LIB"):
+        path = Path(os.environ["GDP2D_ENGINE_LIB"])   # A/B builds (tools/ab_bench.sh)
     if not path.exists():
         raise RuntimeError(
             f"{path} is missing: build it with `python -m paper_2007_00324_b200.build` "
