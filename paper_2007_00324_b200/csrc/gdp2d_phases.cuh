@@ -117,6 +117,8 @@ __device__ __forceinline__ void claim_reset_one(const DevCands& c, u32 i, u32 nT
     }
 }
 
+__device__ __forceinline__ ull bloom_bit(u32 t) { return 1ull << ((t * 0x9E3779B1u) >> 26); }
+
 // Per candidate: FIFO BFS of triangles whose circumcircle strictly contains
 // the point (the located triangle always belongs), never crossing a
 // subsegment, at most ncav+1 triangles.  Processing a FIFO queue item by item
@@ -138,6 +140,9 @@ __device__ __forceinline__ u32 cavity_bfs_one(const DevMesh& m, const DevCands& 
         u32 lreg[MAX_CAVITY_N + 1 + MAX_CLAIM_EXTRA];
         u32 queue[1 + 3 * (MAX_CAVITY_N + 1)];
         u32 head = 0, tail = 0;
+        // 64-bit membership filter of lreg: a triangle whose bit is clear is
+        // not in the region, so most membership scans of lreg are skipped
+        ull bloom = 0;
         const u32 located = c.loc[i];
         const double2 p = c.pt[i];
         const u64 key = c.key[i];
@@ -151,19 +156,25 @@ __device__ __forceinline__ u32 cavity_bfs_one(const DevMesh& m, const DevCands& 
             bool pred = t == located;
             if (!pred && tv.w) pred = incircle(m.xy[tv.x], m.xy[tv.y], m.xy[tv.z], p) > 0;
             if (!pred) continue;
-            bool in = false;
-            for (u32 k = 0; k < len; ++k) in |= lreg[k] == t;
-            if (in) continue;
+            const ull tb = bloom_bit(t);
+            if (bloom & tb) {
+                bool in = false;
+                for (u32 k = 0; k < len; ++k) in |= lreg[k] == t;
+                if (in) continue;
+            }
             lreg[len++] = t;
+            bloom |= tb;
             atomicMax((ull*)&ckey[t], (ull)key);
             for (int e = 0; e < 3; ++e) {
                 if (has_seg(tv, e)) continue;
                 const u32 cc = comp(tn, e);
                 if (cc == NONE) continue;
                 const u32 nb = etri(cc);
-                bool seen = false;
-                for (u32 k = 0; k < len; ++k) seen |= lreg[k] == nb;
-                if (seen) continue;
+                if (bloom & bloom_bit(nb)) {
+                    bool seen = false;
+                    for (u32 k = 0; k < len; ++k) seen |= lreg[k] == nb;
+                    if (seen) continue;
+                }
                 queue[tail++] = nb;
             }
         }
