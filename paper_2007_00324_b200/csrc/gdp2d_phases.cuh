@@ -194,9 +194,15 @@ __device__ __forceinline__ void cavity_tie_one(const DevCands& c, u32 i, u32 rs,
     const u64 key = c.key[i];
     const u64 tie = tie_of(c, i);
     const u32* reg = regions + (size_t)i * rs;
-    for (u32 k = 0; k < len; ++k) {
-        const u32 t = reg[k];
-        if (ckey[t] == key) atomicMin((ull*)&ctie[t], (ull)tie);
+    // the key loads first (independent, issued together), then the atomics:
+    // interleaved, every load would wait behind the previous atomic
+    for (u32 k0 = 0; k0 < len; k0 += 64) {
+        const u32 n = min(len - k0, 64u);
+        ull hold = 0;   // bit k: this candidate holds the key of reg[k0 + k]
+#pragma unroll 4
+        for (u32 k = 0; k < n; ++k) hold |= (ull)(ckey[reg[k0 + k]] == key) << k;
+        for (u32 k = 0; k < n; ++k)
+            if ((hold >> k) & 1ull) atomicMin((ull*)&ctie[reg[k0 + k]], (ull)tie);
     }
 }
 
@@ -210,9 +216,11 @@ __device__ __forceinline__ u32 cavity_check_one(const DevCands& c, u32 i, u32 rs
     const u64 tie = tie_of(c, i);
     const u32* reg = regions + (size_t)i * rs;
     bool own = true;
-    for (u32 k = 0; k < len && own; ++k) {
+    // no early exit: the loads of the whole region are issued together
+#pragma unroll 4
+    for (u32 k = 0; k < len; ++k) {
         const u32 t = reg[k];
-        own = ckey[t] == key && ctie[t] == tie;
+        own &= (ckey[t] == key) & (ctie[t] == tie);
     }
     if (!own) c.alive[i] = 0;
     return own ? 1u : 0u;
