@@ -171,16 +171,30 @@ __device__ __forceinline__ void fixup_one(const DevMesh& m, u32 round, const Tri
     if (!tv.w) return;
     const uint4 ts = load_ts(m, t, tv);
     const u32 pend = tn.w;
+    // the far sides' stamps are loaded together before any store (a store
+    // between them would order each load behind it)
+    u32 sx[3];
+#pragma unroll
+    for (int e = 0; e < 3; ++e) {
+        const u32 r = comp(tn, e);
+        sx[e] = (((pend >> e) & 1u) && r != NONE) ? x.stamp[etri(r)] : 0u;
+    }
+    u32 em[3];
+#pragma unroll
+    for (int e = 0; e < 3; ++e) {
+        const u32 r = comp(tn, e);
+        em[e] = (((pend >> e) & 1u) && r != NONE && sx[e] == round)
+                    ? x.emap[3 * etri(r) + eidx(r)] : NONE;
+    }
 #pragma unroll
     for (int e = 0; e < 3; ++e) {
         if (!((pend >> e) & 1u)) continue;
         const u32 r = comp(tn, e);
         if (r == NONE) continue;
-        const u32 X = etri(r);
-        if (x.stamp[X] == round) {
-            set_comp(tn, e, x.emap[3 * X + eidx(r)]);
+        if (sx[e] == round) {
+            set_comp(tn, e, em[e]);
         } else {
-            m.tn.words(X)[eidx(r)] = enc(t, e);
+            m.tn.words(etri(r))[eidx(r)] = enc(t, e);
         }
     }
     tn.w = 0;

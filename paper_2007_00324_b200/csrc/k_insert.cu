@@ -212,16 +212,21 @@ __device__ __forceinline__ int stream_star(const DevMesh& m, u32 v, Fn&& fn) {
     if (t0 == NONE) return 0;
     u32 cur = t0;
     int k = 0;
+    uint4 tv = m.tv[cur], tn = m.tn[cur];
     do {
-        // both records at once (fn's own loads cannot delay the next step)
-        const uint4 tv = m.tv[cur], tn = m.tn[cur];
         const int i = tv.x == v ? 0 : (tv.y == v ? 1 : (tv.z == v ? 2 : -1));
         if (i < 0 || k >= STAR_WALK_LIMIT) return 0;
+        const u32 c = comp(tn, nxt(i));
+        // the next step's records (both at once) are loaded before fn runs:
+        // fn's own loads and stores cannot delay the walk
+        const u32 nx = c == NONE ? t0 : etri(c);
+        const uint4 ntv = m.tv[nx], ntn = m.tn[nx];
         fn(cur, i, tv);
         ++k;
-        const u32 c = comp(tn, nxt(i));
         if (c == NONE) return 0;
-        cur = etri(c);
+        cur = nx;
+        tv = ntv;
+        tn = ntn;
     } while (cur != t0);
     return k;
 }
