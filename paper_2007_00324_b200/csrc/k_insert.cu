@@ -463,12 +463,20 @@ __device__ __forceinline__ void rm_appends(const WorkLists& w, u32 widx, const u
 // N: capacity of the thread-local link arrays.  The common small star runs
 // with N = 16 (a compact local frame that stays in L1); larger stars take the
 // MAX_STAR instantiation (rm_apply_one dispatches on the star size).
-template <int N>
+// WARP (a round of few removals, so latency-bound): the 32 lanes of a warp
+// remove ONE vertex.  Every lane holds the link polygon and does the same
+// bookkeeping; the ear search tests the first 32 ears from head in parallel
+// (lane l: the l-th) and takes the first that passes -- the serial order,
+// so the mesh is identical -- and lane 0 alone writes.
+template <int N, bool WARP>
 __device__ __noinline__ u32 rm_apply_one_n(const DevMesh& m, const u32* __restrict__ list, u32 i,
                                            u32 round, u32 V0, u32 widx, u32 next_list,
                                            const TriAux& x, const FreshInfo& f,
                                            const WorkLists& w, RoundCtr* rc, Counters* ctr,
                                            RoundCtr* seed_rc, RmOut* out) {
+    static_assert(!WARP || N <= 32, "warp-mode link polygons fit one alive mask");
+    const u32 lane = WARP ? (threadIdx.x & 31u) : 0u;
+    const bool lead = lane == 0;
     u32 done = 0;
     {
         const u32 v = list[i];
@@ -479,7 +487,8 @@ __device__ __noinline__ u32 rm_apply_one_n(const DevMesh& m, const u32* __restri
 #pragma unroll 8
         for (int q = 0; q < k; ++q) own &= x.owner[st[q]] == v;
         if (k >= 3 && !own) {
-            if (out) {
+            if (!lead) {
+            } else if (out) {
                 out->defer = 1;
             } else {
                 const u32 o = agg_reserve(&rc->rm_next, 1u);
@@ -529,11 +538,46 @@ __device__ __noinline__ u32 rm_apply_one_n(const DevMesh& m, const u32* __restri
                     CN[ci][slot] = R[le];
                     CK[ci][slot] = PK[le];
                 }
-                if (ORG[le] != NONE) x.emap[ORG[le]] = enc(tid, slot);
+                if (lead && ORG[le] != NONE) x.emap[ORG[le]] = enc(tid, slot);
             };
+            u32 alive = N >= 32 ? ~0u : ((1u << k) - 1u);   // WARP: link positions left
             while (cnt > 3 && ok) {
                 int j = head;
                 bool found = false;
+                if (WARP) {
+                    // the first passing ear from head, 32 ears at a time: the
+                    // l-th remaining position from head is the l-th set bit of
+                    // the alive mask rotated to head
+                    const u32 rot = head == 0 ? alive
+                                              : ((alive >> head) | (alive << (k - head))) &
+                                                    (k >= 32 ? ~0u : ((1u << k) - 1u));
+                    for (int pass = -1; pass < 2 && !found; ++pass) {
+                        bool pl = false;
+                        int jl = 0;
+                        if ((int)lane < cnt) {
+                            const int sb = (int)__fns(rot, 0, (int)lane + 1);
+                            jl = head + sb >= k ? head + sb - k : head + sb;
+                            const int a = PV[jl], c = NX[jl];
+                            const double2 pa = XY[a], pj = XY[jl], pc = XY[c];
+                            const int side = orient2d(pa, pc, pv);
+                            if (orient2d(pa, pj, pc) > 0 && (side > 0 || (pass == 1 && side == 0))) {
+                                pl = true;
+                                if (pass < 0)
+                                    for (int q = NX[c]; q != a && pl; q = NX[q])
+                                        pl = incircle(pa, pj, pc, XY[q]) <= 0;
+                            }
+                        }
+                        const u32 bal = __ballot_sync(0xFFFFFFFFu, pl);
+                        if (bal) {
+                            j = __shfl_sync(0xFFFFFFFFu, jl, __ffs(bal) - 1);
+                            found = true;
+                        }
+                    }
+                    if (!found) {
+                        ok = false;
+                        break;
+                    }
+                }
                 // Pass -1: a strict ear whose circumcircle holds no other
                 // vertex of the remaining link polygon -- an edge of the
                 // polygon's Delaunay triangulation.  Clipping only such ears
@@ -545,7 +589,7 @@ __device__ __noinline__ u32 rm_apply_one_n(const DevMesh& m, const u32* __restri
                 // Pass 1 (degenerate stars only, e.g. a point that was inserted
                 // exactly on an edge): v may lie ON the new diagonal -- the
                 // final hole triangulation is still valid because v leaves.
-                for (int pass = -1; pass < 2 && !found; ++pass) {
+                for (int pass = -1; pass < 2 && !found && !WARP; ++pass) {
                     j = head;
                     for (int it = 0; it < cnt; ++it) {
                         const int a = PV[j], c = NX[j];
@@ -587,6 +631,7 @@ __device__ __noinline__ u32 rm_apply_one_n(const DevMesh& m, const u32* __restri
                 NX[a] = c;
                 PV[c] = a;
                 if (head == j) head = c;
+                alive &= ~(1u << (j & 31));
                 --cnt;
             }
             if (ok) {
@@ -600,7 +645,8 @@ __device__ __noinline__ u32 rm_apply_one_n(const DevMesh& m, const u32* __restri
                 bind(ci, 2, a);
                 ok = orient2d(XY[a], XY[b], XY[c]) > 0;
             }
-            if (!ok) {
+            if (!lead) {
+            } else if (!ok) {
                 // No flippable incident edge (degenerate star): like
                 // remove_free_vertex returning false (mesh.hpp:462), keep the
                 // vertex; it is never selected again.
@@ -656,10 +702,24 @@ __device__ __forceinline__ u32 rm_apply_one(const DevMesh& m, const u32* __restr
                                             const WorkLists& w, RoundCtr* rc, Counters* ctr,
                                             RoundCtr* seed_rc, RmOut* out = nullptr) {
     if (w.star_len[i] <= 16u)
-        return rm_apply_one_n<16>(m, list, i, round, V0, widx, next_list, x, f, w, rc, ctr,
-                                  seed_rc, out);
-    return rm_apply_one_n<MAX_STAR>(m, list, i, round, V0, widx, next_list, x, f, w, rc, ctr,
-                                    seed_rc, out);
+        return rm_apply_one_n<16, false>(m, list, i, round, V0, widx, next_list, x, f, w, rc, ctr,
+                                         seed_rc, out);
+    return rm_apply_one_n<MAX_STAR, false>(m, list, i, round, V0, widx, next_list, x, f, w, rc,
+                                           ctr, seed_rc, out);
+}
+
+// Removal i by the whole calling warp (every lane calls; lane 0 returns the count).
+__device__ __forceinline__ u32 rm_apply_warp(const DevMesh& m, const u32* __restrict__ list, u32 i,
+                                             u32 round, u32 V0, u32 widx, u32 next_list,
+                                             const TriAux& x, const FreshInfo& f,
+                                             const WorkLists& w, RoundCtr* rc, Counters* ctr,
+                                             RoundCtr* seed_rc) {
+    if (w.star_len[i] <= 16u)
+        return rm_apply_one_n<16, true>(m, list, i, round, V0, widx, next_list, x, f, w, rc, ctr,
+                                        seed_rc, nullptr);
+    if ((threadIdx.x & 31u) != 0u) return 0;
+    return rm_apply_one_n<MAX_STAR, false>(m, list, i, round, V0, widx, next_list, x, f, w, rc,
+                                           ctr, seed_rc, nullptr);
 }
 
 __device__ __forceinline__ void rm_post_one(u32 i, const TriAux& x, const WorkLists& w) {
@@ -1227,7 +1287,13 @@ __device__ void rollback_loop(const InsertArgs& a, const Exec& ex, u32 nv, u32 n
             for (u32 i = ex.tid; i < nrm; i += ex.nthr) rm_claim_one(m, list, i, V0, a.x, a.f, w, a.ctr);
             ex.sync();
             trace(a, ex.leader(), TR_RM_CLAIM, nrm);
-            if (ex.block) {
+            if (nrm <= (ex.nthr >> 5)) {
+                // few removals: one warp each (latency), direct list appends
+                const u32 wi = ex.tid >> 5;
+                if (wi < nrm)
+                    done += rm_apply_warp(m, list, wi, round, V0, 0, rcur ^ 1u, a.x, a.f, w, rc,
+                                          a.ctr, seed_rc);
+            } else if (ex.block) {
                 for (u32 i = ex.tid; i < nrm; i += ex.nthr)
                     done += rm_apply_one(m, list, i, round, V0, 0, rcur ^ 1u, a.x, a.f, w, rc,
                                          a.ctr, seed_rc);
