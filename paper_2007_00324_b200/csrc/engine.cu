@@ -417,6 +417,7 @@ struct gdp2d_ctx {
                                   // capacity to no-round-trip batches, forcing the redo path
     u32 small_nv = 256;           // GDP2D_SMALL_NV: block-mode insertion at or below
     u32 small_wl = 256;           // GDP2D_SMALL_WL: block-mode Lawson below this list size
+    u32 rm_warp = 4;              // GDP2D_RM_WARP: warp-per-removal rounds up to this many per warp
     u32 small_c = 256;            // GDP2D_SMALL_C: whole batch in one CTA at or below
     u32 standalone_c = 30000;     // GDP2D_STANDALONE_C: Lines 5-7 as standalone kernels only above this
                                   // (smaller batches filter inside the grid-mode batch kernel)
@@ -690,6 +691,7 @@ void ctx_init(gdp2d_ctx* x, int device) {
     }
     if (const char* e = std::getenv("GDP2D_SMALL_NV")) x->small_nv = (u32)std::strtoul(e, nullptr, 10);
     if (const char* e = std::getenv("GDP2D_SMALL_WL")) x->small_wl = (u32)std::strtoul(e, nullptr, 10);
+    if (const char* e = std::getenv("GDP2D_RM_WARP")) x->rm_warp = (u32)std::strtoul(e, nullptr, 10);
     if (const char* e = std::getenv("GDP2D_SMALL_C")) x->small_c = (u32)std::strtoul(e, nullptr, 10);
     if (const char* e = std::getenv("GDP2D_DEP")) x->dep_mis = std::string(e) == "mis";
     if (const char* e = std::getenv("GDP2D_CHECK")) x->check = e[0] == '1';
@@ -1095,6 +1097,7 @@ InsertLaunch base_launch(gdp2d_ctx* x, const gdp2d_params* p, u32 batch, u32 nca
     L.scap = x->work.scap;
     L.small_nv = x->small_nv;
     L.small_wl = x->small_wl;
+    L.rm_warp = x->rm_warp;
     L.max_steps = 1u << 20;
     L.ncav = ncav;
     L.rs = rs;

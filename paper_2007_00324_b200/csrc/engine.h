@@ -219,6 +219,7 @@ struct InsertLaunch {
     u32 batch, round0;
     u32 vcap, tcap, scap;
     u32 small_nv, small_wl, max_steps;
+    u32 rm_warp;
     u32 ncav = 32, rs = 35;
     u32* regions = nullptr;
     u32* region_len = nullptr;

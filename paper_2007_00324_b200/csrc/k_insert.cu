@@ -795,6 +795,7 @@ struct InsertArgs {
     u32 vcap, tcap, scap; // mesh capacities
     u32 small_nv;         // block mode when the batch inserts <= small_nv points
     u32 small_wl;         // Lawson switches to block mode below this many work items
+    u32 rm_warp;          // removal rounds of <= rm_warp * warps run one warp per removal
     u32 max_steps;        // safety bound on barrier steps
     // Lines 5-7 (locate / claim / cavity) + the phase-1 plan and its scan
     u32 ncav, rs;         // cavity bound and region stride
@@ -1287,10 +1288,9 @@ __device__ void rollback_loop(const InsertArgs& a, const Exec& ex, u32 nv, u32 n
             for (u32 i = ex.tid; i < nrm; i += ex.nthr) rm_claim_one(m, list, i, V0, a.x, a.f, w, a.ctr);
             ex.sync();
             trace(a, ex.leader(), TR_RM_CLAIM, nrm);
-            if (nrm <= (ex.nthr >> 5)) {
+            if (nrm <= a.rm_warp * (ex.nthr >> 5)) {
                 // few removals: one warp each (latency), direct list appends
-                const u32 wi = ex.tid >> 5;
-                if (wi < nrm)
+                for (u32 wi = ex.tid >> 5; wi < nrm; wi += ex.nthr >> 5)
                     done += rm_apply_warp(m, list, wi, round, V0, 0, rcur ^ 1u, a.x, a.f, w, rc,
                                           a.ctr, seed_rc);
             } else if (ex.block) {
@@ -1634,6 +1634,7 @@ static InsertArgs make_args(const InsertLaunch& L) {
     a.scap = L.scap;
     a.small_nv = L.small_nv;
     a.small_wl = L.small_wl;
+    a.rm_warp = L.rm_warp;
     a.max_steps = L.max_steps;
     a.ncav = L.ncav;
     a.rs = L.rs;
