@@ -427,3 +427,34 @@ def test_tail_loop_identical(built, monkeypatch, insert_mode, theta):
     for name in ("xy", "tri_v", "tri_n", "tri_seg", "tri_alive", "seg_v", "seg_alive",
                  "vert_tri", "seg_tri"):
         assert np.array_equal(getattr(a, name), getattr(b, name)), name
+
+
+@pytest.mark.parametrize("insert_mode", [1, 2])
+def test_warp_removal_identical(built, monkeypatch, insert_mode):
+    """Removal rounds with one warp per removal (lanes test the ears from head
+    in parallel, GDP2D_RM_WARP) clip the same ears in the same order as one
+    thread per removal: the refined mesh is identical whether no round
+    (GDP2D_RM_WARP=0), the default few-removal rounds, or every round runs in
+    warp mode."""
+    from paper_2007_00324_b200 import Engine, EngineConfig, QualityCriteria, host
+    pts, segs = host.generate_pslg(100_000, 10_000, "gaussian", 37)
+    m, _ = host.build_cdt(pts, segs)
+    q = QualityCriteria(B_SQRT2_THETA)
+    outs = []
+    for val in ("0", None, "1000000"):
+        monkeypatch.delenv("GDP2D_RM_WARP", raising=False)
+        if val is not None:
+            monkeypatch.setenv("GDP2D_RM_WARP", val)
+        with Engine(0) as eng:
+            eng.upload(m)
+            rep = eng.refine(q, EngineConfig(insert_mode=insert_mode))
+            v = eng.validate(q)
+            assert v["bad_triangles"] == 0 and v["cdt_violations"] == 0, v
+            assert rep.totals["total_removed"] > 0
+            outs.append((rep, eng.download()))
+    (r0, a) = outs[0]
+    for r1, b in outs[1:]:
+        assert len(r0.batches) == len(r1.batches) and r0.steiner_points == r1.steiner_points
+        for name in ("xy", "tri_v", "tri_n", "tri_seg", "tri_alive", "seg_v", "seg_alive",
+                     "vert_tri", "seg_tri"):
+            assert np.array_equal(getattr(a, name), getattr(b, name)), name
