@@ -436,8 +436,9 @@ def main():
         dropin = {"value": dst * a.dropin_steps / ds, "unit": UNIT,
                   "wall_s_per_step": ds / a.dropin_steps, "steps": a.dropin_steps,
                   "path": "gdp2d::refine(cdtref::Mesh&, q, EngineConfig{}) from "
-                          "include/gdp2d_cdtref.hpp: AoS->SoA pack, gdp2d_refine with pageable "
-                          "host buffers (H2D + loop + D2H), unpack in place",
+                          "include/gdp2d_cdtref.hpp: the Mesh's element vectors (pageable) to "
+                          "gdp2d_refine_aos as they are -- H2D, records converted on the "
+                          "device, loop, D2H back into the vectors",
                   "h2d_bytes_per_step": mesh_bytes(meshes[0]), "steiner": dst,
                   "breakdown_s_per_step": parts}
 

@@ -242,6 +242,43 @@ void gdp2d_params_init(gdp2d_params* p, double theta_deg, double ell, uint32_t m
 int gdp2d_refine(const gdp2d_mesh_view* in, gdp2d_mesh_buf* out, const gdp2d_params* p,
                  gdp2d_report* r, int device);
 
+/* Array-of-structures records: the reference's own element vectors
+ * (cdtref::Vertex / Triangle / Subsegment, mesh.hpp:43-62) described by byte
+ * size and field offsets, so the drop-in refine (include/gdp2d_cdtref.hpp)
+ * hands the caller's vectors over as they are -- no host pack / unpack, no
+ * library-owned output buffers.  Fields: vertex pos (2 x f64), kind (u8),
+ * birth (u32), alive (u8); triangle v[3], nbr[3], seg[3] (u32), alive (u8);
+ * subsegment v[2], parent (u32), encroached (u8), alive (u8). */
+typedef struct gdp2d_aos_layout {
+    uint32_t vert_size, vert_pos, vert_kind, vert_birth, vert_alive;
+    uint32_t tri_size, tri_v, tri_nbr, tri_seg, tri_alive;
+    uint32_t seg_size, seg_v, seg_parent, seg_encroached, seg_alive;
+} gdp2d_aos_layout;
+
+enum { GDP2D_AOS_VERTS = 0, GDP2D_AOS_TRIS = 1, GDP2D_AOS_SEGS = 2, GDP2D_AOS_VERT_TRI = 3,
+       GDP2D_AOS_SEG_TRI = 4 };
+
+/* A caller-owned AoS mesh, refined in place.  After the refinement the
+ * library calls resize(user, what, n) once per array (GDP2D_AOS_*) with its
+ * output length; the callback sizes the caller's array and returns its
+ * (possibly moved) base, which the library overwrites with n records.
+ * batch_epoch is updated on return. */
+typedef struct gdp2d_aos_mesh {
+    uint32_t n_vertices, n_triangles, n_subsegments, batch_epoch;
+    const void* verts;
+    const void* tris;
+    const void* segs;
+    const uint32_t* vert_tri;
+    const uint32_t* seg_tri;
+    void* (*resize)(void* user, int what, uint64_t n);
+    void* user;
+} gdp2d_aos_mesh;
+
+/* gdp2d_refine on AoS records (replaces cdtref::refine, refine.hpp:651, for
+ * callers that hold a cdtref::Mesh): records are converted on the device. */
+int gdp2d_refine_aos(const gdp2d_aos_layout* layout, gdp2d_aos_mesh* mesh,
+                     const gdp2d_params* p, gdp2d_report* r, int device);
+
 /* Create the cached context of `device` and run one tiny CDT build +
  * refinement on it, so CUDA context creation and kernel loading (~1-2 s in a
  * fresh process) are paid here.  Meant to run on a helper thread while the
@@ -255,7 +292,7 @@ const char* gdp2d_last_error(void);
 const char* gdp2d_version(void);
 /* sizeof() of the exchange structs, for binding-layout checks:
  * 0 mesh_view, 1 mesh_buf, 2 params, 3 batch_metrics, 4 report, 5 candidate,
- * 6 validation, 7 node_ele, 8 cdt_report */
+ * 6 validation, 7 node_ele, 8 cdt_report, 9 aos_layout, 10 aos_mesh */
 size_t gdp2d_struct_size(int which);
 /* Process-wide count of engine kernel launches so far (all devices). */
 uint64_t gdp2d_kernel_launches(void);

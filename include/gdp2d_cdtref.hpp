@@ -8,9 +8,11 @@
  * existing caller (tools/cdtref.cpp:175, tests/unit/test_refine.cpp:374, ...)
  * switches by including this header and writing gdp2d::refine instead of
  * cdtref::refine.  The caller keeps the reference's own Mesh, PSLG/mesh I/O
- * (pslg_io.hpp) and Line-1 build_cdt (cdt.hpp:483): this header only packs
- * the AoS Mesh (mesh.hpp:43-75) into the SoA exchange view, runs the whole
- * refinement loop on the GPU (libgdp2d.so) and unpacks the result in place.
+ * (pslg_io.hpp) and Line-1 build_cdt (cdt.hpp:483): this header hands the
+ * Mesh's element vectors (mesh.hpp:43-75) to gdp2d_refine_aos as they are --
+ * the records are converted on the device, so there is no host pack / unpack
+ * -- runs the whole refinement loop on the GPU (libgdp2d.so) and writes the
+ * result back into the same vectors.
  *
  * Include AFTER the reference headers ("cdtref/refine.hpp"); link -lgdp2d.
  *
@@ -37,12 +39,14 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstddef>
 #include <cstdlib>
 #include <map>
 #include <memory>
 #include <stdexcept>
 #include <string>
 #include <thread>
+#include <type_traits>
 #include <vector>
 
 #include "gdp2d.h"
@@ -236,23 +240,9 @@ inline void unpack(const gdp2d_mesh_buf& b, cdtref::Mesh& m) {
 
 // Expected output/input size ratio of a refinement: ~2x at radius-edge
 // sqrt(2), ~5x at 30 degrees (BASELINE configs 2-4).  Only a hint: a larger
-// output just grows again in unpack.
+// output just grows again when the library asks for the output vectors.
 inline double growth_hint(const cdtref::QualityCriteria& q) {
     return q.theta >= 28.0 ? 5.5 : q.theta >= 24.0 ? 3.5 : 2.2;
-}
-
-// While the GPU refines, grow the caller's element vectors to the expected
-// output size on a host thread: std::vector's value-initialisation of the new
-// tail is serial, and this way it runs during gdp2d_refine instead of after
-// it.  Their contents are already packed, so they are not copied.
-inline void pregrow(cdtref::Mesh& m, double g) {
-    auto grow = [g](auto& v) {
-        const size_t n = static_cast<size_t>(static_cast<double>(v.size()) * g);
-        if (n > v.capacity()) resize_for_overwrite(v, n);
-    };
-    grow(m.vertices);
-    grow(m.triangles);
-    grow(m.subsegments);
 }
 
 inline void throw_status(int rc) {
@@ -263,32 +253,118 @@ inline void throw_status(int rc) {
 
 }  // namespace detail
 
+namespace detail {
+
+// The reference's records as gdp2d_refine_aos sees them.
+inline gdp2d_aos_layout aos_layout() {
+    gdp2d_aos_layout L;
+    L.vert_size = sizeof(cdtref::Vertex);
+    L.vert_pos = offsetof(cdtref::Vertex, pos);
+    L.vert_kind = offsetof(cdtref::Vertex, kind);
+    L.vert_birth = offsetof(cdtref::Vertex, birth_batch);
+    L.vert_alive = offsetof(cdtref::Vertex, alive);
+    L.tri_size = sizeof(cdtref::Triangle);
+    L.tri_v = offsetof(cdtref::Triangle, v);
+    L.tri_nbr = offsetof(cdtref::Triangle, nbr);
+    L.tri_seg = offsetof(cdtref::Triangle, seg);
+    L.tri_alive = offsetof(cdtref::Triangle, alive);
+    L.seg_size = sizeof(cdtref::Subsegment);
+    L.seg_v = offsetof(cdtref::Subsegment, v);
+    L.seg_parent = offsetof(cdtref::Subsegment, parent);
+    L.seg_encroached = offsetof(cdtref::Subsegment, encroached);
+    L.seg_alive = offsetof(cdtref::Subsegment, alive);
+    return L;
+}
+static_assert(sizeof(cdtref::VertexKind) == 1 && sizeof(bool) == 1 &&
+                  sizeof(cdtref::Point2) == 16 && sizeof(cdtref::TriId) == 4 &&
+                  sizeof(cdtref::SubsegId) == 4 && sizeof(cdtref::VertexId) == 4,
+              "gdp2d_aos_layout field widths");
+
+// The output vectors, built on a host thread while the device refines:
+// std::vector's value-initialisation of a multi-GB tail is serial, and the
+// fresh buffers are swapped in only when the library asks for them (the
+// caller's input vectors are being read by the upload until then).
+struct OutVectors {
+    cdtref::Mesh& m;
+    double g;
+    std::vector<cdtref::Vertex> verts;
+    std::vector<cdtref::Triangle> tris;
+    std::vector<cdtref::Subsegment> segs;
+    std::thread th;
+    OutVectors(cdtref::Mesh& mesh, double growth) : m(mesh), g(growth) {
+        const size_t V = m.vertices.size(), T = m.triangles.size(), S = m.subsegments.size();
+        th = std::thread([this, V, T, S] {
+            auto make = [this](auto& v, size_t n0) {
+                const size_t n = static_cast<size_t>(static_cast<double>(n0) * g);
+                v.reserve(n + n / 8);   // room to grow a little without a copy
+                hint_huge(v.data(), sizeof(typename std::decay_t<decltype(v)>::value_type) * v.capacity());
+                v.resize(n);
+            };
+            make(verts, V);
+            make(tris, T);
+            make(segs, S);
+        });
+    }
+    ~OutVectors() {
+        if (th.joinable()) th.join();
+    }
+    template <class V>
+    static void* take(V& dst, V& fresh, size_t n) {
+        if (n <= fresh.capacity()) {
+            dst.swap(fresh);
+            dst.resize(n);
+        } else {
+            resize_for_overwrite(dst, n);
+        }
+        return dst.data();
+    }
+    // gdp2d_aos_mesh::resize
+    static void* resize(void* user, int what, uint64_t n) {
+        OutVectors& o = *static_cast<OutVectors*>(user);
+        if (o.th.joinable()) o.th.join();
+        switch (what) {
+            case GDP2D_AOS_VERTS: return take(o.m.vertices, o.verts, n);
+            case GDP2D_AOS_TRIS: return take(o.m.triangles, o.tris, n);
+            case GDP2D_AOS_SEGS: return take(o.m.subsegments, o.segs, n);
+            case GDP2D_AOS_VERT_TRI: o.m.vert_tri.resize(n); return o.m.vert_tri.data();
+            case GDP2D_AOS_SEG_TRI: o.m.seg_tri.resize(n); return o.m.seg_tri.data();
+            default: return nullptr;
+        }
+    }
+};
+
+}  // namespace detail
+
 // Drop-in for cdtref::refine (refine.hpp:651).  `device` selects the GPU
 // (one call = one device + one stream, blocking; distinct host threads may
 // drive distinct devices).
 inline cdtref::RunReport refine(cdtref::Mesh& m, const cdtref::QualityCriteria& q,
                                 const cdtref::EngineConfig& cfg, int device = 0) {
     const gdp2d_params p = detail::make_params(q, cfg);
-    detail::Packed in(m);
+    const gdp2d_aos_layout L = detail::aos_layout();
     std::vector<gdp2d_batch_metrics> bm(cfg.iteration_cap < 100000 ? cfg.iteration_cap + 1 : 100001);
     gdp2d_report r{};
     r.batches = bm.data();
     r.batches_capacity = static_cast<uint32_t>(bm.size());
-    gdp2d_mesh_buf out{};
     int rc;
     {
-        // the element vectors are packed: grow them while the device works
-        // (vert_tri / seg_tri stay untouched: the view reads them in place)
-        std::thread grow([&m, g = detail::growth_hint(q)] { detail::pregrow(m, g); });
-        struct Join {
-            std::thread& t;
-            ~Join() { t.join(); }
-        } join{grow};
-        rc = gdp2d_refine(&in.view, &out, &p, &r, device);
+        detail::OutVectors out(m, detail::growth_hint(q));
+        gdp2d_aos_mesh a{};
+        a.n_vertices = static_cast<uint32_t>(m.vertices.size());
+        a.n_triangles = static_cast<uint32_t>(m.triangles.size());
+        a.n_subsegments = static_cast<uint32_t>(m.subsegments.size());
+        a.batch_epoch = m.batch_epoch;
+        a.verts = m.vertices.data();
+        a.tris = m.triangles.data();
+        a.segs = m.subsegments.data();
+        a.vert_tri = m.vert_tri.data();
+        a.seg_tri = m.seg_tri.data();
+        a.resize = &detail::OutVectors::resize;
+        a.user = &out;
+        rc = gdp2d_refine_aos(&L, &a, &p, &r, device);
+        if (rc == GDP2D_OK) m.batch_epoch = a.batch_epoch;
     }
     if (rc != GDP2D_OK) detail::throw_status(rc);
-    detail::unpack(out, m);
-    gdp2d_free(&out);
 
     cdtref::RunReport rep;
     const uint32_t nb = r.n_batches < r.batches_capacity ? r.n_batches : r.batches_capacity;

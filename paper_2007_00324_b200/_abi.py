@@ -123,13 +123,33 @@ def candidate_dtype():
                      ("alive", "u1"), ("fallback", "u1")])
 
 
+class AosLayout(C.Structure):
+    _fields_ = [(n, C.c_uint32) for n in (
+        "vert_size", "vert_pos", "vert_kind", "vert_birth", "vert_alive",
+        "tri_size", "tri_v", "tri_nbr", "tri_seg", "tri_alive",
+        "seg_size", "seg_v", "seg_parent", "seg_encroached", "seg_alive")]
+
+
+AOS_RESIZE = C.CFUNCTYPE(C.c_void_p, C.c_void_p, C.c_int, C.c_uint64)
+
+
+class AosMesh(C.Structure):
+    _fields_ = [("n_vertices", C.c_uint32), ("n_triangles", C.c_uint32),
+                ("n_subsegments", C.c_uint32), ("batch_epoch", C.c_uint32),
+                ("verts", C.c_void_p), ("tris", C.c_void_p), ("segs", C.c_void_p),
+                ("vert_tri", C.c_void_p), ("seg_tri", C.c_void_p),
+                ("resize", AOS_RESIZE), ("user", C.c_void_p)]
+
+
 STRUCTS = [MeshView, MeshBuf, Params, BatchMetrics, Report, Candidate, Validation, NodeEle,
-           CdtReport]
+           CdtReport, AosLayout, AosMesh]
 
 # Every entry point of include/gdp2d.h: name -> (restype, argtypes)
 ctx_p = C.c_void_p
 SIGNATURES = {
     "gdp2d_params_init": (None, [C.POINTER(Params), C.c_double, C.c_double, C.c_uint32]),
+    "gdp2d_refine_aos": (C.c_int, [C.POINTER(AosLayout), C.POINTER(AosMesh), C.POINTER(Params),
+                                   C.POINTER(Report), C.c_int]),
     "gdp2d_refine": (C.c_int, [C.POINTER(MeshView), C.POINTER(MeshBuf), C.POINTER(Params),
                                C.POINTER(Report), C.c_int]),
     "gdp2d_free": (None, [C.POINTER(MeshBuf)]),
@@ -190,6 +210,8 @@ HOST_SIGNATURES = {
                                              C.POINTER(C.c_char_p)]),
     "gdp2d_host_free_buf": (None, [C.POINTER(MeshBuf)]),
     "gdp2d_host_last_error": (C.c_char_p, []),
+    "gdp2d_host_dropin_refine": (C.c_int, [C.POINTER(MeshView), C.c_double, C.c_int,
+                                           C.POINTER(MeshBuf), C.POINTER(C.c_uint64)]),
     "gdp2d_host_time_dropin": (C.c_int, [C.POINTER(MeshView), C.c_double, C.c_int, C.c_int,
                                          C.POINTER(C.c_double), C.POINTER(C.c_uint64),
                                          C.c_void_p]),

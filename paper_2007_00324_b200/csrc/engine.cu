@@ -176,6 +176,98 @@ __global__ void k_u32_to_u8(const u32* __restrict__ a, uint8_t* __restrict__ b, 
     if (i < n) b[i] = a[i] ? 1 : 0;
 }
 
+// ---- AoS records (gdp2d_refine_aos): the caller's element vectors as bytes ----
+// Field offsets come from gdp2d_aos_layout (checked on the host: natural
+// alignment, inside the record).
+template <class T>
+__device__ __forceinline__ T& fld(uint8_t* rec, u32 off) {
+    return *reinterpret_cast<T*>(rec + off);
+}
+template <class T>
+__device__ __forceinline__ T fldc(const uint8_t* rec, u32 off) {
+    return *reinterpret_cast<const T*>(rec + off);
+}
+
+__global__ void k_aos_verts_in(const uint8_t* __restrict__ in, const __grid_constant__ gdp2d_aos_layout L,
+                               DevMesh m, u32 V) {
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= V) return;
+    const uint8_t* r = in + (size_t)i * L.vert_size;
+    m.xy[i] = make_double2(fldc<double>(r, L.vert_pos), fldc<double>(r, L.vert_pos + 8));
+    m.vkind[i] = r[L.vert_kind];
+    m.vbirth[i] = fldc<u32>(r, L.vert_birth);
+    m.valive[i] = r[L.vert_alive] ? 1 : 0;
+}
+
+__global__ void k_aos_tris_in(const uint8_t* __restrict__ in, const __grid_constant__ gdp2d_aos_layout L,
+                              u32* __restrict__ tv3, u32* __restrict__ ts3, u32* __restrict__ tn3,
+                              uint8_t* __restrict__ alive, u32 T) {
+    const u32 t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= T) return;
+    const uint8_t* r = in + (size_t)t * L.tri_size;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        tv3[3 * t + k] = fldc<u32>(r, L.tri_v + 4 * k);
+        tn3[3 * t + k] = fldc<u32>(r, L.tri_nbr + 4 * k);
+        ts3[3 * t + k] = fldc<u32>(r, L.tri_seg + 4 * k);
+    }
+    alive[t] = r[L.tri_alive] ? 1 : 0;
+}
+
+__global__ void k_aos_segs_in(const uint8_t* __restrict__ in, const __grid_constant__ gdp2d_aos_layout L,
+                              DevMesh m, u32 S) {
+    const u32 s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= S) return;
+    const uint8_t* r = in + (size_t)s * L.seg_size;
+    m.sv[s] = make_uint2(fldc<u32>(r, L.seg_v), fldc<u32>(r, L.seg_v + 4));
+    m.sparent[s] = fldc<u32>(r, L.seg_parent);
+    m.senc[s] = r[L.seg_encroached] ? 1u : 0u;
+    m.salive[s] = r[L.seg_alive] ? 1 : 0;
+    m.sdepth[s] = 0;
+}
+
+__global__ void k_aos_verts_out(DevMesh m, const __grid_constant__ gdp2d_aos_layout L,
+                                uint8_t* __restrict__ out, u32 V) {
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= V) return;
+    uint8_t* r = out + (size_t)i * L.vert_size;
+    const double2 p = m.xy[i];
+    fld<double>(r, L.vert_pos) = p.x;
+    fld<double>(r, L.vert_pos + 8) = p.y;
+    r[L.vert_kind] = m.vkind[i];
+    fld<u32>(r, L.vert_birth) = m.vbirth[i];
+    r[L.vert_alive] = m.valive[i] ? 1 : 0;
+}
+
+__global__ void k_aos_tris_out(const u32* __restrict__ tv3, const u32* __restrict__ ts3,
+                               const u32* __restrict__ tn3, const uint8_t* __restrict__ alive,
+                               const __grid_constant__ gdp2d_aos_layout L, uint8_t* __restrict__ out,
+                               u32 T) {
+    const u32 t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= T) return;
+    uint8_t* r = out + (size_t)t * L.tri_size;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        fld<u32>(r, L.tri_v + 4 * k) = tv3[3 * t + k];
+        fld<u32>(r, L.tri_nbr + 4 * k) = tn3[3 * t + k];
+        fld<u32>(r, L.tri_seg + 4 * k) = ts3[3 * t + k];
+    }
+    r[L.tri_alive] = alive[t];
+}
+
+__global__ void k_aos_segs_out(DevMesh m, const __grid_constant__ gdp2d_aos_layout L,
+                               uint8_t* __restrict__ out, u32 S) {
+    const u32 s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= S) return;
+    uint8_t* r = out + (size_t)s * L.seg_size;
+    const uint2 sv = m.sv[s];
+    fld<u32>(r, L.seg_v) = sv.x;
+    fld<u32>(r, L.seg_v + 4) = sv.y;
+    fld<u32>(r, L.seg_parent) = m.sparent[s];
+    r[L.seg_encroached] = m.senc[s] ? 1 : 0;
+    r[L.seg_alive] = m.salive[s] ? 1 : 0;
+}
+
 __global__ void k_fill_u64(u64* p, u64 v, size_t n) {
     const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
     if (i < n) p[i] = v;
@@ -460,6 +552,9 @@ struct gdp2d_ctx {
     u32* stage_u32[3] = {nullptr, nullptr, nullptr};
     uint8_t* stage_u8 = nullptr;
     size_t stage_cap = 0;
+    // AoS records of gdp2d_refine_aos (bytes)
+    uint8_t* aos_stage = nullptr;
+    size_t aos_cap = 0;
 };
 
 namespace {
@@ -739,6 +834,7 @@ void ctx_release(gdp2d_ctx* x) {
     x->h_ctr = nullptr;
     for (auto& s : x->stage_u32) dfree(s);
     dfree(x->stage_u8);
+    dfree(x->aos_stage);
     if (x->h_rc) cudaFreeHost(x->h_rc);
     if (x->qscratch) cudaFree(x->qscratch);
     dfree(x->d_val);
@@ -886,6 +982,8 @@ void h2d(gdp2d_ctx* x, void* dst, const void* src, size_t bytes) {
     // event (or follows it in stream order)
 }
 
+void upload_finish(gdp2d_ctx* x, u32 batch_epoch);
+
 void upload(gdp2d_ctx* x, const gdp2d_mesh_view* v) {
     validate_view(v);
     const u32 V = v->n_vertices, T = v->n_triangles, S = v->n_subsegments;
@@ -922,7 +1020,15 @@ void upload(gdp2d_ctx* x, const gdp2d_mesh_view* v) {
         CK(cudaMemsetAsync(m.sdepth, 0, 4ull * S, st));
     }
     CK(cudaGetLastError());
-    x->pristine_epoch = v->batch_epoch;
+    upload_finish(x, v->batch_epoch);
+}
+
+// The tail of every upload: epoch, lazily derived input segments, alive counts.
+void upload_finish(gdp2d_ctx* x, u32 batch_epoch) {
+    const DevMesh& m = x->pristine.m;
+    const u32 V = m.nV, T = m.nT, S = m.nS;
+    cudaStream_t st = x->st;
+    x->pristine_epoch = batch_epoch;
     x->n_in = 0;   // input segments are derived lazily by gdp2d_ctx_validate
     x->in_valid = false;
     // alive counts (batch metrics) on the device, read back with the upload
@@ -1032,6 +1138,118 @@ void download(gdp2d_ctx* x, gdp2d_mesh_buf* b) {
     b->seg_alive = (uint8_t*)hm(S);
     b->seg_tri = (u32*)hm(4ull * S);
     download_into(x, b);
+}
+
+// ---- AoS records (gdp2d_refine_aos) ----
+
+void check_aos_layout(const gdp2d_aos_layout* L) {
+    auto in = [](u32 off, u32 bytes, u32 size, u32 align) {
+        return off % align == 0 && (u64)off + bytes <= size;
+    };
+    const bool ok = L && L->vert_size % 8 == 0 && L->tri_size % 4 == 0 && L->seg_size % 4 == 0 &&
+                    in(L->vert_pos, 16, L->vert_size, 8) && in(L->vert_kind, 1, L->vert_size, 1) &&
+                    in(L->vert_birth, 4, L->vert_size, 4) && in(L->vert_alive, 1, L->vert_size, 1) &&
+                    in(L->tri_v, 12, L->tri_size, 4) && in(L->tri_nbr, 12, L->tri_size, 4) &&
+                    in(L->tri_seg, 12, L->tri_size, 4) && in(L->tri_alive, 1, L->tri_size, 1) &&
+                    in(L->seg_v, 8, L->seg_size, 4) && in(L->seg_parent, 4, L->seg_size, 4) &&
+                    in(L->seg_encroached, 1, L->seg_size, 1) && in(L->seg_alive, 1, L->seg_size, 1);
+    if (!ok) throw Fail{GDP2D_EINVAL, "AoS layout: field outside its record or misaligned"};
+}
+
+void ensure_aos(gdp2d_ctx* x, size_t bytes) {
+    if (bytes <= x->aos_cap) return;
+    dfree(x->aos_stage);
+    dalloc(x->aos_stage, bytes);
+    x->aos_cap = bytes;
+}
+
+void upload_aos(gdp2d_ctx* x, const gdp2d_aos_layout* L, const gdp2d_aos_mesh* a) {
+    check_aos_layout(L);
+    const u32 V = a->n_vertices, T = a->n_triangles, S = a->n_subsegments;
+    if ((V && (!a->verts || !a->vert_tri)) || (T && !a->tris) || (S && (!a->segs || !a->seg_tri)))
+        throw Fail{GDP2D_EINVAL, "missing AoS arrays"};
+    MeshStore& p = x->pristine;
+    p.m.nV = p.m.nT = p.m.nS = 0;
+    mesh_reserve(p, V, T, S, x->st);
+    DevMesh& m = p.m;
+    m.nV = V;
+    m.nT = T;
+    m.nS = S;
+    cudaStream_t st = x->st;
+    ensure_aos(x, std::max({(size_t)V * L->vert_size, (size_t)T * L->tri_size,
+                            (size_t)S * L->seg_size, (size_t)16}));
+    ensure_stage(x, std::max<size_t>(3ull * T, 2ull * S) + T + S + 16);
+    if (V) {
+        h2d(x, x->aos_stage, a->verts, (size_t)V * L->vert_size);
+        note_launch(), k_aos_verts_in<<<grid(V), 256, 0, st>>>(x->aos_stage, *L, m, V);
+        h2d(x, m.vtri, a->vert_tri, 4ull * V);
+    }
+    if (T) {   // the records' bytes reuse the staging once the vertex kernel ran (stream order)
+        h2d(x, x->aos_stage, a->tris, (size_t)T * L->tri_size);
+        note_launch(), k_aos_tris_in<<<grid(T), 256, 0, st>>>(x->aos_stage, *L, x->stage_u32[0],
+                                                            x->stage_u32[1], x->stage_u32[2],
+                                                            x->stage_u8, T);
+        note_launch(), k_pack_tris<<<grid(T), 256, 0, st>>>(m, x->stage_u32[0], x->stage_u32[1], x->stage_u8);
+        launch_encode_neighbors(m, x->stage_u32[2], st);
+    }
+    if (S) {
+        h2d(x, x->aos_stage, a->segs, (size_t)S * L->seg_size);
+        note_launch(), k_aos_segs_in<<<grid(S), 256, 0, st>>>(x->aos_stage, *L, m, S);
+        h2d(x, m.stri, a->seg_tri, 4ull * S);
+    }
+    CK(cudaGetLastError());
+    upload_finish(x, a->batch_epoch);
+}
+
+// The working mesh into the caller's AoS arrays, sized by its resize callback.
+void download_aos(gdp2d_ctx* x, const gdp2d_aos_layout* L, gdp2d_aos_mesh* a) {
+    const DevMesh& m = x->work.m;
+    const u32 V = m.nV, T = m.nT, S = m.nS;
+    cudaStream_t st = x->st;
+    ensure_aos(x, std::max({(size_t)V * L->vert_size, (size_t)T * L->tri_size,
+                            (size_t)S * L->seg_size, (size_t)16}));
+    ensure_stage(x, std::max<size_t>(3ull * T, 2ull * S) + T + S + 16);
+    auto dst = [&](int what, u64 n) {
+        void* d = a->resize(a->user, what, n);
+        if (!d && n) throw Fail{GDP2D_EINVAL, "AoS resize callback returned null"};
+        return d;
+    };
+    // the record padding goes out as zeros
+    if (V) {
+        CK(cudaMemsetAsync(x->aos_stage, 0, (size_t)V * L->vert_size, st));
+        note_launch(), k_aos_verts_out<<<grid(V), 256, 0, st>>>(m, *L, x->aos_stage, V);
+        d2h(x, dst(GDP2D_AOS_VERTS, V), x->aos_stage, (size_t)V * L->vert_size);
+        d2h(x, dst(GDP2D_AOS_VERT_TRI, V), m.vtri, 4ull * V);
+    } else {
+        dst(GDP2D_AOS_VERTS, 0);
+        dst(GDP2D_AOS_VERT_TRI, 0);
+    }
+    if (T) {
+        CK(cudaMemsetAsync(x->aos_stage, 0, (size_t)T * L->tri_size, st));
+        note_launch(), k_unpack_tris<<<grid(T), 256, 0, st>>>(m, x->stage_u32[0], x->stage_u32[1], x->stage_u8);
+        launch_decode_neighbors(m, x->stage_u32[2], st);
+        note_launch(), k_aos_tris_out<<<grid(T), 256, 0, st>>>(x->stage_u32[0], x->stage_u32[1],
+                                                             x->stage_u32[2], x->stage_u8, *L,
+                                                             x->aos_stage, T);
+        d2h(x, dst(GDP2D_AOS_TRIS, T), x->aos_stage, (size_t)T * L->tri_size);
+    } else {
+        dst(GDP2D_AOS_TRIS, 0);
+    }
+    if (S) {
+        CK(cudaMemsetAsync(x->aos_stage, 0, (size_t)S * L->seg_size, st));
+        note_launch(), k_aos_segs_out<<<grid(S), 256, 0, st>>>(m, *L, x->aos_stage, S);
+        d2h(x, dst(GDP2D_AOS_SEGS, S), x->aos_stage, (size_t)S * L->seg_size);
+        d2h(x, dst(GDP2D_AOS_SEG_TRI, S), m.stri, 4ull * S);
+    } else {
+        dst(GDP2D_AOS_SEGS, 0);
+        dst(GDP2D_AOS_SEG_TRI, 0);
+    }
+    CK(cudaStreamSynchronize(st));
+    CK(cudaGetLastError());
+    a->n_vertices = V;
+    a->n_triangles = T;
+    a->n_subsegments = S;
+    a->batch_epoch = x->epoch;
 }
 
 double ev_ms(cudaEvent_t a, cudaEvent_t b) {
@@ -2041,6 +2259,8 @@ size_t gdp2d_struct_size(int which) {
         case 6: return sizeof(gdp2d_validation);
         case 7: return sizeof(gdp2d_node_ele);
         case 8: return sizeof(gdp2d_cdt_report);
+        case 9: return sizeof(gdp2d_aos_layout);
+        case 10: return sizeof(gdp2d_aos_mesh);
         default: return 0;
     }
 }
@@ -2147,6 +2367,29 @@ int gdp2d_refine(const gdp2d_mesh_view* in, gdp2d_mesh_buf* out, const gdp2d_par
         reset_work(x, p->theta_deg);
         refine_loop(x, p, r);
         download(x, out);
+        r->e2e_seconds =
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        fill_summary(x, p, r);
+    });
+}
+
+int gdp2d_refine_aos(const gdp2d_aos_layout* layout, gdp2d_aos_mesh* mesh,
+                     const gdp2d_params* p, gdp2d_report* r, int device) {
+    if (!layout || !mesh || !mesh->resize || !p || !r) return GDP2D_EINVAL;
+    if (device < 0 || device >= kMaxDevices) return GDP2D_ENODEVICE;
+    std::lock_guard<std::mutex> lock(g_cache_mu[device]);
+    if (!g_cache[device]) {
+        const int rc = gdp2d_ctx_create(&g_cache[device], device);
+        if (rc) return rc;
+    }
+    gdp2d_ctx* x = g_cache[device];
+    return run_guarded([&] {
+        DeviceGuard g(x->device);
+        const auto t0 = std::chrono::steady_clock::now();
+        upload_aos(x, layout, mesh);
+        reset_work(x, p->theta_deg);
+        refine_loop(x, p, r);
+        download_aos(x, layout, mesh);
         r->e2e_seconds =
             std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         fill_summary(x, p, r);

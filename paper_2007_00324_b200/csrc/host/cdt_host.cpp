@@ -291,16 +291,37 @@ void gdp2d_host_free_buf(gdp2d_mesh_buf* b) {
     std::memset(b, 0, sizeof *b);
 }
 
+// One drop-in call, for parity tests: the reference Mesh built from *in,
+// refined by gdp2d::refine (include/gdp2d_cdtref.hpp, gdp2d_refine_aos) and
+// returned as an SoA buffer (gdp2d_host_free_buf).
+int gdp2d_host_dropin_refine(const gdp2d_mesh_view* in, double theta_deg, int device,
+                             gdp2d_mesh_buf* out, uint64_t* steiner) {
+    try {
+        Mesh m = view_to_mesh(in);
+        QualityCriteria q;
+        q.theta = theta_deg;
+        const RunReport rep = gdp2d::refine(m, q, EngineConfig{}, device);
+        *steiner = rep.steiner_points;
+        mesh_to_buf(m, out);
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
 // The drop-in caller's path, timed: gdp2d::refine(cdtref::Mesh&, q, cfg)
 // (include/gdp2d_cdtref.hpp) on the reference's own AoS Mesh in pageable
-// memory -- pack to SoA, gdp2d_refine (H2D, device loop, D2H), unpack in
-// place -- exactly what a cdtref caller gets after swapping the namespace.
-// The reference Mesh is built from *in once; each of `steps` calls refines a
+// memory -- its element vectors go to gdp2d_refine_aos as they are (H2D,
+// device record conversion, device loop, D2H back into the vectors) --
+// exactly what a cdtref caller gets after swapping the namespace.  The
+// reference Mesh is built from *in once; each of `steps` calls refines a
 // fresh copy of it (the copy is untimed).  Writes the summed call time and
 // the last call's Steiner count.  parts (optional, 4 doubles): summed seconds
-// of the shim's steps, timed separately on a further copy -- AoS->SoA pack,
-// gdp2d_refine (H2D + loop + D2H, with the vectors' pre-growth beside it),
-// SoA->AoS unpack, gdp2d_free.
+// of a further `steps` calls split by the library's own clocks -- transfers
+// (gdp2d_report e2e_seconds minus the loop: H2D, record conversion, D2H, and
+// any wait for the output vectors), the refinement loop (wall_seconds), the
+// shim around the library call, and 0.
 int gdp2d_host_time_dropin(const gdp2d_mesh_view* in, double theta_deg, int steps, int device,
                            double* seconds, uint64_t* steiner, double* parts) {
     try {
@@ -319,36 +340,38 @@ int gdp2d_host_time_dropin(const gdp2d_mesh_view* in, double theta_deg, int step
         *seconds = total;
         if (parts) {
             using clk = std::chrono::steady_clock;
-            auto sec = [](clk::time_point a, clk::time_point b) {
-                return std::chrono::duration<double>(b - a).count();
-            };
             for (int k = 0; k < 4; ++k) parts[k] = 0.0;
             for (int i = 0; i < steps; ++i) {
                 Mesh m = base;
                 const gdp2d_params p = gdp2d::detail::make_params(q, cfg);
-                const auto t0 = clk::now();
-                gdp2d::detail::Packed pk(m);
-                const auto t1 = clk::now();
+                const gdp2d_aos_layout L = gdp2d::detail::aos_layout();
                 std::vector<gdp2d_batch_metrics> bm(cfg.iteration_cap + 1);
                 gdp2d_report r{};
                 r.batches = bm.data();
                 r.batches_capacity = (uint32_t)bm.size();
-                gdp2d_mesh_buf out{};
-                std::thread grow([&m, g = gdp2d::detail::growth_hint(q)] {
-                    gdp2d::detail::pregrow(m, g);
-                });
-                const int rc = gdp2d_refine(&pk.view, &out, &p, &r, device);
-                grow.join();
+                const auto t0 = clk::now();
+                int rc;
+                {
+                    gdp2d::detail::OutVectors out(m, gdp2d::detail::growth_hint(q));
+                    gdp2d_aos_mesh a{};
+                    a.n_vertices = (uint32_t)m.vertices.size();
+                    a.n_triangles = (uint32_t)m.triangles.size();
+                    a.n_subsegments = (uint32_t)m.subsegments.size();
+                    a.batch_epoch = m.batch_epoch;
+                    a.verts = m.vertices.data();
+                    a.tris = m.triangles.data();
+                    a.segs = m.subsegments.data();
+                    a.vert_tri = m.vert_tri.data();
+                    a.seg_tri = m.seg_tri.data();
+                    a.resize = &gdp2d::detail::OutVectors::resize;
+                    a.user = &out;
+                    rc = gdp2d_refine_aos(&L, &a, &p, &r, device);
+                }
                 if (rc != GDP2D_OK) throw std::runtime_error(gdp2d_last_error());
-                const auto t2 = clk::now();
-                gdp2d::detail::unpack(out, m);
-                const auto t3 = clk::now();
-                gdp2d_free(&out);
-                const auto t4 = clk::now();
-                parts[0] += sec(t0, t1);
-                parts[1] += sec(t1, t2);
-                parts[2] += sec(t2, t3);
-                parts[3] += sec(t3, t4);
+                const double call = std::chrono::duration<double>(clk::now() - t0).count();
+                parts[0] += r.e2e_seconds - r.wall_seconds;
+                parts[1] += r.wall_seconds;
+                parts[2] += call - r.e2e_seconds;
             }
         }
         return 0;

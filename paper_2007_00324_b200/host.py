@@ -50,12 +50,26 @@ def build_cdt(points: np.ndarray, segments: np.ndarray, close_hull: bool = True)
     return Mesh.from_buf(out, lib.gdp2d_host_free_buf), closed
 
 
+def dropin_refine(mesh: Mesh, theta: float, device: int = 0):
+    """One gdp2d::refine(cdtref::Mesh&, q, EngineConfig{}) call (the drop-in
+    shim, include/gdp2d_cdtref.hpp) on the mesh as a reference AoS Mesh.
+    Returns (refined Mesh, Steiner count)."""
+    lib = A.host()
+    v = mesh.view()
+    out = A.MeshBuf()
+    st = C.c_uint64()
+    if lib.gdp2d_host_dropin_refine(C.byref(v), theta, device, C.byref(out), C.byref(st)):
+        raise RuntimeError("gdp2d::refine: " + lib.gdp2d_host_last_error().decode())
+    return Mesh.from_buf(out, lib.gdp2d_host_free_buf), int(st.value)
+
+
 def time_dropin(mesh: Mesh, theta: float, steps: int, device: int = 0, parts: bool = False):
     """The drop-in caller's path (include/gdp2d_cdtref.hpp): `steps` calls of
     gdp2d::refine(cdtref::Mesh&, q, EngineConfig{}) on copies of the mesh as
     a reference AoS Mesh in pageable memory.  Returns (seconds summed over
-    the calls, Steiner count of the last call[, per-step breakdown dict of
-    the shim's pack / gdp2d_refine / unpack / free when parts])."""
+    the calls, Steiner count of the last call[, per-step breakdown dict when
+    parts: transfers (H2D, device record conversion, D2H), the refinement
+    loop, and the shim around the library call])."""
     lib = A.host()
     v = mesh.view()
     secs = C.c_double()
@@ -66,7 +80,7 @@ def time_dropin(mesh: Mesh, theta: float, steps: int, device: int = 0, parts: bo
         raise RuntimeError("gdp2d::refine: " + lib.gdp2d_host_last_error().decode())
     if not parts:
         return secs.value, int(st.value)
-    names = ("pack_s", "gdp2d_refine_s", "unpack_s", "free_s")
+    names = ("transfers_s", "refine_loop_s", "shim_s")
     return secs.value, int(st.value), {k: pv[i] / steps for i, k in enumerate(names)}
 
 

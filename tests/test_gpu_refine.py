@@ -458,3 +458,29 @@ def test_warp_removal_identical(built, monkeypatch, insert_mode):
         for name in ("xy", "tri_v", "tri_n", "tri_seg", "tri_alive", "seg_v", "seg_alive",
                      "vert_tri", "seg_tri"):
             assert np.array_equal(getattr(a, name), getattr(b, name)), name
+
+
+@pytest.mark.parametrize("theta", [B_SQRT2_THETA, 23.5])
+def test_dropin_shim_matches_context_path(built, theta):
+    """gdp2d::refine on the reference's own AoS Mesh (include/gdp2d_cdtref.hpp:
+    the element vectors go to gdp2d_refine_aos as they are, the records are
+    converted on the device and the result is written back into the vectors)
+    gives the mesh the SoA context path gives, array for array.  At 23.5 deg
+    the output outgrows the shim's size hint (2.2x), so the resize callback's
+    reallocating branch runs too."""
+    from paper_2007_00324_b200 import Engine, QualityCriteria, host
+    from paper_2007_00324_b200.gdp2d import _FIELDS
+    pts, segs = host.generate_pslg(60_000, 6_000, "gaussian", 41)
+    m, _ = host.build_cdt(pts, segs)
+    q = QualityCriteria(theta)
+    with Engine(0) as eng:
+        eng.upload(m)
+        rep = eng.refine(q)
+        ref = eng.download()
+    got, steiner = host.dropin_refine(m, theta)
+    assert steiner == rep.steiner_points
+    if theta > 23.0:
+        assert got.n_triangles > 2.2 * m.n_triangles
+    assert got.batch_epoch == ref.batch_epoch
+    for name, _, _ in _FIELDS:
+        assert np.array_equal(getattr(got, name), getattr(ref, name)), name
