@@ -290,24 +290,32 @@ struct OutVectors {
     std::vector<cdtref::Vertex> verts;
     std::vector<cdtref::Triangle> tris;
     std::vector<cdtref::Subsegment> segs;
-    std::thread th;
+    std::vector<cdtref::TriId> vtri, stri;
+    std::thread th[3];
     OutVectors(cdtref::Mesh& mesh, double growth) : m(mesh), g(growth) {
+        auto make = [this](auto* v, size_t n0) {
+            const size_t n = static_cast<size_t>(static_cast<double>(n0) * g);
+            v->reserve(n + n / 8);   // room to grow a little without a copy
+            hint_huge(v->data(), sizeof(typename std::decay_t<decltype(*v)>::value_type) * v->capacity());
+            v->resize(n);
+        };
         const size_t V = m.vertices.size(), T = m.triangles.size(), S = m.subsegments.size();
-        th = std::thread([this, V, T, S] {
-            auto make = [this](auto& v, size_t n0) {
-                const size_t n = static_cast<size_t>(static_cast<double>(n0) * g);
-                v.reserve(n + n / 8);   // room to grow a little without a copy
-                hint_huge(v.data(), sizeof(typename std::decay_t<decltype(v)>::value_type) * v.capacity());
-                v.resize(n);
-            };
-            make(verts, V);
-            make(tris, T);
-            make(segs, S);
+        // one thread per big vector (the triangle records dominate)
+        th[0] = std::thread([=] { make(&tris, T); });
+        th[1] = std::thread([=] {
+            make(&verts, V);
+            make(&vtri, V);
+        });
+        th[2] = std::thread([=] {
+            make(&segs, S);
+            make(&stri, S);
         });
     }
-    ~OutVectors() {
-        if (th.joinable()) th.join();
+    void join() {
+        for (auto& t : th)
+            if (t.joinable()) t.join();
     }
+    ~OutVectors() { join(); }
     template <class V>
     static void* take(V& dst, V& fresh, size_t n) {
         if (n <= fresh.capacity()) {
@@ -321,13 +329,15 @@ struct OutVectors {
     // gdp2d_aos_mesh::resize
     static void* resize(void* user, int what, uint64_t n) {
         OutVectors& o = *static_cast<OutVectors*>(user);
-        if (o.th.joinable()) o.th.join();
+        // wait only for the thread that builds the requested vector
+        std::thread& t = o.th[what == GDP2D_AOS_TRIS ? 0 : (what == GDP2D_AOS_VERTS || what == GDP2D_AOS_VERT_TRI) ? 1 : 2];
+        if (t.joinable()) t.join();
         switch (what) {
             case GDP2D_AOS_VERTS: return take(o.m.vertices, o.verts, n);
             case GDP2D_AOS_TRIS: return take(o.m.triangles, o.tris, n);
             case GDP2D_AOS_SEGS: return take(o.m.subsegments, o.segs, n);
-            case GDP2D_AOS_VERT_TRI: o.m.vert_tri.resize(n); return o.m.vert_tri.data();
-            case GDP2D_AOS_SEG_TRI: o.m.seg_tri.resize(n); return o.m.seg_tri.data();
+            case GDP2D_AOS_VERT_TRI: return take(o.m.vert_tri, o.vtri, n);
+            case GDP2D_AOS_SEG_TRI: return take(o.m.seg_tri, o.stri, n);
             default: return nullptr;
         }
     }
