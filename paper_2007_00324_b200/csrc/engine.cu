@@ -505,6 +505,9 @@ struct gdp2d_ctx {
                                   // persistent kernels on one CTA per SM (cheaper grid barriers)
     u32 quarter_grid_c = 10000;   // GDP2D_QUARTER_GRID_C: ... below this on half the SMs
     u32 eighth_grid_c = 0;        // GDP2D_EIGHTH_GRID_C: ... below this on a quarter of the SMs
+    u32 cluster_c = 4096;         // GDP2D_CLUSTER_C: ... below this as ONE thread-block cluster
+                                  // (barrier.cluster instead of grid barriers)
+    int cluster_size = 0;         // GDP2D_CLUSTER (default 16): CTAs of that cluster (0 = off)
     bool regions_tight = false;   // GDP2D_REGIONS_TIGHT=1 (tests): advertise half the region
                                   // capacity to no-round-trip batches, forcing the redo path
     u32 small_nv = 256;           // GDP2D_SMALL_NV: block-mode insertion at or below
@@ -766,6 +769,11 @@ void ctx_init(gdp2d_ctx* x, int device) {
     if (const char* e = std::getenv("GDP2D_HALF_GRID_C")) x->half_grid_c = (u32)std::atoll(e);
     if (const char* e = std::getenv("GDP2D_QUARTER_GRID_C")) x->quarter_grid_c = (u32)std::atoll(e);
     if (const char* e = std::getenv("GDP2D_EIGHTH_GRID_C")) x->eighth_grid_c = (u32)std::atoll(e);
+    if (const char* e = std::getenv("GDP2D_CLUSTER_C")) x->cluster_c = (u32)std::atoll(e);
+    {
+        const char* e = std::getenv("GDP2D_CLUSTER");
+        x->cluster_size = insert_cluster_size(device, e ? std::atoi(e) : 16);
+    }
     x->lawson_grid = lawson_persistent_grid(device);
     x->insert_grid = insert_persistent_grid(device);
     x->rollback_grid = rollback_persistent_grid(device);
@@ -1347,12 +1355,18 @@ bool insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, int prefiltered, u32
                     : c_est < x->quarter_grid_c ? 4
                     : c_est < x->half_grid_c    ? 2
                                                 : 1;
-    const int g_ins = std::max(1, x->insert_grid / div);
+    // Mid-size batches: both kernels as ONE thread-block cluster, whose
+    // barriers are hardware cluster barriers (~0.2 us) instead of grid
+    // barriers (~1.2 us); same output for any grid size or launch shape.
+    const bool as_cluster = x->cluster_size > 0 && c_est < x->cluster_c;
+    const int g_ins =
+        as_cluster ? x->cluster_size : std::max(1, x->insert_grid / div);
     static const int rb_div = [] {
         const char* e = std::getenv("GDP2D_RB_DIV");   // experiments: extra divisor, rollback kernel
         return e ? std::max(1, std::atoi(e)) : 1;
     }();
-    const int g_rb = std::max(1, x->rollback_grid / (div * rb_div));
+    const int g_rb =
+        as_cluster ? x->cluster_size : std::max(1, x->rollback_grid / (div * rb_div));
     bool started = false;   // an earlier attempt got past the filter and plan
     int grow = 0;
     for (int attempt = 0;; ++attempt) {
@@ -1362,6 +1376,7 @@ bool insert_persistent(gdp2d_ctx* x, const gdp2d_params* p, int prefiltered, u32
         L.prefiltered = prefiltered;
         L.planned = prefiltered && !isolate;
         L.reg_cap = reg_cap;
+        L.cluster = as_cluster ? 1 : 0;
         if (x->tr.on) {
             L.trace = x->tr.d_trace;
             L.trace_val = x->tr.d_trace_val;

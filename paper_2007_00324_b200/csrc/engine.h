@@ -229,6 +229,7 @@ struct InsertLaunch {
     int prefiltered = 0;        // standalone Lines 5-7 kernels ran (they skip C <= small_c)
     int planned = 0;            // ... and made the phase-1 plan (launch_cavity's plan)
     u32 reg_cap = 0xFFFFFFFFu;  // candidates the region buffers hold (INS_REGIONS beyond)
+    int cluster = 0;            // launch both kernels as ONE cluster of `grid` CTAs
     int isolate = 1;            // claims: 0 reference cavity, 1 isolated (ring), 2 precedence
     int dep_mis = 0;            // dependent pairs by the priority-MIS rule
     int extras = 2;             // cavity extras mode (see launch_cavity)
@@ -239,6 +240,9 @@ struct InsertLaunch {
 };
 int insert_persistent_grid(int device);
 int rollback_persistent_grid(int device);
+// Largest cluster size <= want (a power of two, <= 16) the persistent kernels can
+// be launched with as one thread-block cluster; 0 if none.
+int insert_cluster_size(int device, int want);
 // The device-resident tail loop (k_tail_loop, k_insert.cu): consecutive small
 // batches (C <= small_c) run back to back in ONE single-CTA launch -- an
 // incremental collect over the previous candidate keys and the elements the

@@ -752,18 +752,24 @@ struct Exec {
     bool block;      // block mode: CTA 0 only
     RoundCtr* ring;  // step counters: global ring (grid mode) or shared memory (block mode,
                      // so the work-list atomics and the post-barrier count reads stay on-SM)
+    bool cluster;    // cluster mode: the whole launch is ONE thread-block cluster
+                     // (mid-size batches): barrier.cluster instead of a grid barrier
     __device__ __forceinline__ void sync() const {
         if (block)
             __syncthreads();
+        else if (cluster)
+            cg::this_cluster().sync();   // hardware barrier, release/acquire at cluster scope
         else
             cg::this_grid().sync();
     }
     __device__ __forceinline__ bool leader() const { return tid == 0; }
 };
 
-__device__ __forceinline__ Exec grid_exec(RoundCtr* ring) {
+// Grid mode over every CTA of the launch; when the launch is one cluster
+// (InsertArgs::cluster) its barriers are cluster barriers.
+__device__ __forceinline__ Exec grid_exec(RoundCtr* ring, bool cluster = false) {
     cg::grid_group g = cg::this_grid();
-    return Exec{(u32)g.thread_rank(), (u32)g.size(), false, ring};
+    return Exec{(u32)g.thread_rank(), (u32)g.size(), false, ring, cluster};
 }
 // Block mode with its counters in shared memory: sring[5] is zeroed here
 // (every thread of the CTA must call it).
@@ -773,7 +779,7 @@ __device__ __forceinline__ Exec block_exec(RoundCtr* sring) {
         sring[threadIdx.x] = z;
     }
     __syncthreads();
-    return Exec{threadIdx.x, blockDim.x, true, sring};
+    return Exec{threadIdx.x, blockDim.x, true, sring, false};
 }
 
 __device__ __forceinline__ u32 vload(const u32* p) { return *(const volatile u32*)p; }
@@ -807,6 +813,7 @@ struct InsertArgs {
     int prefiltered;      // standalone Lines 5-7 ran (for C > small_c)
     int planned;          // ... including the phase-1 plan (b.nv / nt / ns written)
     u32 reg_cap;          // candidates the region buffers hold
+    int cluster;          // the launch is one thread-block cluster (Exec::cluster)
     int isolate;          // claims: 0 reference, 1 isolated (rollback only if state[8]), 2 precedence
     int dep_mis;          // dependent pairs: 1 = priority-MIS rule, 0 = any-higher-neighbour rule
     int extras;           // refine cavity claims: 2 = the rewrite table (launch_cavity)
@@ -1378,7 +1385,7 @@ __global__ void __launch_bounds__(INSERT_BLOCK, GDP2D_SPLIT_MINB) k_batch_split(
     const bool block = C <= a.small_c;
     if (block && blockIdx.x != 0) return;
     __shared__ RoundCtr sring[5];
-    const Exec ex = block ? block_exec(sring) : grid_exec(a.ring);
+    const Exec ex = block ? block_exec(sring) : grid_exec(a.ring, a.cluster != 0);
     if (!a.resume) {
         trace(a, ex.leader(), TR_START);
         const bool here = block || !a.prefiltered;   // Lines 5-7 in this kernel
@@ -1404,7 +1411,7 @@ __global__ void __launch_bounds__(ROLLBACK_BLOCK) k_batch_rollback(const __grid_
     const bool block = nv <= a.small_c;
     if (block && blockIdx.x != 0) return;
     __shared__ RoundCtr sring[5];
-    const Exec ex = block ? block_exec(sring) : grid_exec(a.ring);
+    const Exec ex = block ? block_exec(sring) : grid_exec(a.ring, a.cluster != 0);
     trace(a, ex.leader(), TR_RB_START);
     rollback_loop<MODE>(a, ex, nv, nt, ns);
 }
@@ -1646,6 +1653,7 @@ static InsertArgs make_args(const InsertLaunch& L) {
     a.prefiltered = L.prefiltered;
     a.planned = L.planned;
     a.reg_cap = L.reg_cap;
+    a.cluster = L.cluster;
     a.isolate = L.isolate;
     a.dep_mis = L.dep_mis;
     a.extras = L.extras;
@@ -1665,20 +1673,90 @@ void launch_tail_loop(const InsertLaunch& L, const TailArgs& t, int mode, cudaSt
         k_tail_loop<0><<<1, INSERT_BLOCK, 0, st>>>(a, t);
 }
 
+// Cluster launch: the grid is ONE cluster of `grid` CTAs (non-portable sizes
+// up to 16 are enabled once per kernel), no cooperative attribute -- the
+// kernels' barriers are then barrier.cluster (Exec::cluster).
+static cudaError_t launch_as_cluster(const void* fn, int grid, int block, void** args,
+                                     cudaStream_t st) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = grid;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelExC(&cfg, fn, args);
+}
+
+static const void* split_fn(int mode) {
+    return mode ? (const void*)k_batch_split<1> : (const void*)k_batch_split<0>;
+}
+static const void* rollback_fn(int mode) {
+    return mode ? (const void*)k_batch_rollback<1> : (const void*)k_batch_rollback<0>;
+}
+
+int insert_cluster_size(int device, int want) {
+    // largest cluster <= want that both persistent kernels can place (0 = none)
+    static int cached[64][17];
+    if (want < 2) return 0;
+    want = std::min(want, 16);
+    if (device >= 0 && device < 64 && cached[device][want]) return cached[device][want] - 1;
+    int got = 0;
+    for (int cs = want; cs >= 2 && !got; cs /= 2) {
+        bool ok = true;
+        for (int mode = 0; mode < 2 && ok; ++mode)
+            for (int k = 0; k < 2 && ok; ++k) {
+                const void* fn = k ? rollback_fn(mode) : split_fn(mode);
+                if (cs > 8 &&
+                    cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+                        cudaSuccess) {
+                    ok = false;
+                    break;
+                }
+                cudaLaunchConfig_t cfg = {};
+                cfg.gridDim = dim3(cs);
+                cfg.blockDim = dim3(k ? ROLLBACK_BLOCK : INSERT_BLOCK);
+                cudaLaunchAttribute at[1];
+                at[0].id = cudaLaunchAttributeClusterDimension;
+                at[0].val.clusterDim.x = cs;
+                at[0].val.clusterDim.y = 1;
+                at[0].val.clusterDim.z = 1;
+                cfg.attrs = at;
+                cfg.numAttrs = 1;
+                int n = 0;
+                if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) != cudaSuccess || n < 1) ok = false;
+            }
+        if (ok) got = cs;
+    }
+    cudaGetLastError();
+    if (device >= 0 && device < 64) cached[device][want] = got + 1;
+    return got;
+}
+
 void launch_insert_persistent(const InsertLaunch& L, int mode, int grid, int grid2, cudaStream_t st,
                               cudaEvent_t between, int which) {
     InsertArgs a = make_args(L);
     void* args[] = {&a};
     if (which & 1) {
         note_launch();
-        cudaLaunchCooperativeKernel(mode ? (void*)k_batch_split<1> : (void*)k_batch_split<0>,
-                                    dim3(grid), dim3(INSERT_BLOCK), args, 0, st);
+        if (L.cluster)
+            launch_as_cluster(split_fn(mode), grid, INSERT_BLOCK, args, st);
+        else
+            cudaLaunchCooperativeKernel(split_fn(mode), dim3(grid), dim3(INSERT_BLOCK), args, 0, st);
     }
     if (between) cudaEventRecord(between, st);
     if (which & 2) {
         note_launch();
-        cudaLaunchCooperativeKernel(mode ? (void*)k_batch_rollback<1> : (void*)k_batch_rollback<0>,
-                                    dim3(grid2), dim3(ROLLBACK_BLOCK), args, 0, st);
+        if (L.cluster)
+            launch_as_cluster(rollback_fn(mode), grid2, ROLLBACK_BLOCK, args, st);
+        else
+            cudaLaunchCooperativeKernel(rollback_fn(mode), dim3(grid2), dim3(ROLLBACK_BLOCK), args,
+                                        0, st);
     }
 }
 

@@ -460,6 +460,38 @@ def test_warp_removal_identical(built, monkeypatch, insert_mode):
             assert np.array_equal(getattr(a, name), getattr(b, name)), name
 
 
+@pytest.mark.parametrize("insert_mode", [0, 1])
+@pytest.mark.parametrize("theta", [B_SQRT2_THETA, 30.0])
+def test_cluster_mode_identical(built, monkeypatch, insert_mode, theta):
+    """Batches run as ONE thread-block cluster (barrier.cluster instead of grid
+    barriers, GDP2D_CLUSTER_C) give the very mesh the cooperative grid gives:
+    cluster mode off, the default mid-size band, and every batch that does not
+    run in block mode forced into a cluster (16 or 8 CTAs)."""
+    from paper_2007_00324_b200 import Engine, EngineConfig, QualityCriteria, host
+    pts, segs = host.generate_pslg(100_000, 10_000, "gaussian", 41)
+    m, _ = host.build_cdt(pts, segs)
+    q = QualityCriteria(theta)
+    outs = []
+    for env in ({"GDP2D_CLUSTER_C": "0"}, {}, {"GDP2D_CLUSTER_C": "1000000000"},
+                {"GDP2D_CLUSTER_C": "1000000000", "GDP2D_CLUSTER": "8"}):
+        for k in ("GDP2D_CLUSTER_C", "GDP2D_CLUSTER"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        with Engine(0) as eng:
+            eng.upload(m)
+            rep = eng.refine(q, EngineConfig(insert_mode=insert_mode))
+            v = eng.validate(q)
+            assert v["bad_triangles"] == 0 and v["cdt_violations"] == 0, v
+            outs.append((rep, eng.download()))
+    (r0, a) = outs[0]
+    for r1, b in outs[1:]:
+        assert len(r0.batches) == len(r1.batches) and r0.steiner_points == r1.steiner_points
+        for name in ("xy", "tri_v", "tri_n", "tri_seg", "tri_alive", "seg_v", "seg_alive",
+                     "vert_tri", "seg_tri"):
+            assert np.array_equal(getattr(a, name), getattr(b, name)), name
+
+
 @pytest.mark.parametrize("theta", [B_SQRT2_THETA, 23.5])
 def test_dropin_shim_matches_context_path(built, theta):
     """gdp2d::refine on the reference's own AoS Mesh (include/gdp2d_cdtref.hpp:
