@@ -605,7 +605,8 @@ void ensure_aux(gdp2d_ctx* x) {
     const u32 T = x->work.tcap;
     if (T > x->aux_cap) {
         dfree(x->aux.ckey); dfree(x->aux.ctie); dfree(x->aux.owner); dfree(x->aux.stamp);
-        dfree(x->aux.emap); dfree(x->aux.fkey); dfree(x->aux.ftie);
+        dfree(x->aux.emap); dfree(x->aux.fkey); dfree(x->aux.ftie); dfree(x->aux.fown);
+        dalloc(x->aux.fown, T);
         dalloc(x->aux.ckey, T); dalloc(x->aux.ctie, T); dalloc(x->aux.owner, T);
         dalloc(x->aux.stamp, T); dalloc(x->aux.emap, 3ull * T);
         dalloc(x->aux.fkey, T); dalloc(x->aux.ftie, T);
@@ -615,6 +616,8 @@ void ensure_aux(gdp2d_ctx* x) {
         CK(cudaMemsetAsync(x->aux.ftie, 0xFF, sizeof(u64) * T, x->st));
         CK(cudaMemsetAsync(x->aux.owner, 0xFF, sizeof(u32) * T, x->st));
         CK(cudaMemsetAsync(x->aux.stamp, 0, sizeof(u32) * T, x->st));
+        // flip claims are tagged with the round, which restarts here
+        CK(cudaMemsetAsync(x->aux.fown, 0, sizeof(u64) * T, x->st));
         x->aux_cap = T;
         x->round = 0;
     }
@@ -822,7 +825,8 @@ void ctx_release(gdp2d_ctx* x) {
     mesh_free(x->work);
     mesh_free(x->pristine);
     dfree(x->aux.ckey); dfree(x->aux.ctie); dfree(x->aux.owner); dfree(x->aux.stamp);
-    dfree(x->aux.emap); dfree(x->aux.fkey); dfree(x->aux.ftie); dfree(x->flags);
+    dfree(x->aux.emap); dfree(x->aux.fkey); dfree(x->aux.ftie); dfree(x->aux.fown);
+    dfree(x->flags);
     cands_free(x->c);
     dfree(x->regions); dfree(x->region_len); dfree(x->bfs_len);
     dfree(x->ib.nv); dfree(x->ib.nt); dfree(x->ib.ns); dfree(x->ib.ov); dfree(x->ib.ot);

@@ -241,11 +241,17 @@ __device__ __forceinline__ void fixup_one(const DevMesh& m, u32 round, const Tri
 
 // Test one work item (is_non_delaunay_edge mesh.hpp:430-437) on its canonical
 // side (lower triangle id) and claim both triangles with the edge code as key:
-// the minimum key wins, so a round's flip set is deterministic.
+// the minimum key wins, so a round's flip set is deterministic.  The claim is
+// round-tagged, fown = max over (round << 32 | ~key): a later round's claim
+// beats any stale one, so the claims are never reset.
 // The test itself: true for a flip candidate (claims made), with its key
 // (canonical side) and the far side's code.
-__device__ __forceinline__ bool flip_test_eval(const DevMesh& m, u32 code, const TriAux& x,
-                                               u32& key_out, u32& uc_out) {
+__device__ __forceinline__ u64 flip_tag(u32 round, u32 key) {
+    return ((u64)round << 32) | (u64)(~key);
+}
+
+__device__ __forceinline__ bool flip_test_eval(const DevMesh& m, u32 code, u32 round,
+                                               const TriAux& x, u32& key_out, u32& uc_out) {
     u32 t = etri(code);
     int e = eidx(code);
     if (t >= m.nT) return false;
@@ -272,8 +278,9 @@ __device__ __forceinline__ bool flip_test_eval(const DevMesh& m, u32 code, const
     }
     if (incircle(m.xy[tv.x], m.xy[tv.y], m.xy[tv.z], m.xy[d]) <= 0) return false;
     const u32 key = enc(t, e);
-    atomicMin(&x.owner[t], key);
-    atomicMin(&x.owner[u], key);
+    const u64 tag = flip_tag(round, key);
+    atomicMax((ull*)&x.fown[t], (ull)tag);
+    atomicMax((ull*)&x.fown[u], (ull)tag);
     key_out = key;
     uc_out = enc(u, f);
     return true;
@@ -289,10 +296,11 @@ __device__ __forceinline__ void flip_cand_store(const WorkLists& w, u32 o, u32 k
     }
 }
 
-__device__ __forceinline__ void flip_test_one(const DevMesh& m, u32 code, const TriAux& x,
-                                              const WorkLists& w, RoundCtr* rc, Counters* ctr) {
+__device__ __forceinline__ void flip_test_one(const DevMesh& m, u32 code, u32 round,
+                                              const TriAux& x, const WorkLists& w, RoundCtr* rc,
+                                              Counters* ctr) {
     u32 key, uc;
-    if (!flip_test_eval(m, code, x, key, uc)) return;
+    if (!flip_test_eval(m, code, round, x, key, uc)) return;
     flip_cand_store(w, agg_reserve(&rc->cand, 1u), key, uc, ctr);
 }
 
@@ -309,10 +317,11 @@ __device__ __forceinline__ bool flip_apply_core(const DevMesh& m, u32 i, u32 rou
     // the pair's records are loaded together with the claims; a duplicate
     // work item (same key, all "win") that loses the stamp exchange below
     // discards them, and the winner's reads precede any write to the pair
-    const u32 ot = x.owner[t], ou = x.owner[u];
+    const u64 ot = x.fown[t], ou = x.fown[u];
     const uint4 tv = m.tv[t], tn = m.tn[t];
     const uint4 uv = m.tv[u], un = m.tn[u];
-    const bool won = ot == key && ou == key;
+    const u64 tag = flip_tag(round, key);
+    const bool won = ot == tag && ou == tag;
     w.fwin[i] = won;
     // exactly one duplicate performs the flip
     if (!won || atomicExch(&x.stamp[t], round) == round) return false;
@@ -373,14 +382,12 @@ __device__ __forceinline__ u32 flip_apply_one(const DevMesh& m, u32 i, u32 round
     return 1;
 }
 
-// Release claims; a loser whose triangles were both left untouched retries
-// (returns its key to re-queue, or NONE).
+// A loser whose triangles were both left untouched retries (returns its key
+// to re-queue, or NONE).  The claims need no release (round-tagged).
 __device__ __forceinline__ u32 flip_post_core(u32 i, u32 round, const TriAux& x,
                                               const WorkLists& w) {
     const u32 key = w.fc[i], uc = w.fu[i];
     const u32 t = etri(key), u = etri(uc);
-    x.owner[t] = NONE;
-    x.owner[u] = NONE;
     return (!w.fwin[i] && x.stamp[t] != round && x.stamp[u] != round) ? key : NONE;
 }
 
@@ -403,13 +410,13 @@ __device__ __forceinline__ void flip_post_one(u32 i, u32 round, u32 widx, const 
 // nthr = grid threads.  Every thread of every CTA calls these.
 
 template <int BLOCK>
-__device__ __forceinline__ void flip_test_waves(const DevMesh& m, const u32* wl, u32 n, u32 tid0,
-                                                u32 nthr, const TriAux& x, const WorkLists& w,
-                                                RoundCtr* rc, Counters* ctr) {
+__device__ __forceinline__ void flip_test_waves(const DevMesh& m, const u32* wl, u32 n, u32 round,
+                                                u32 tid0, u32 nthr, const TriAux& x,
+                                                const WorkLists& w, RoundCtr* rc, Counters* ctr) {
     for (u32 base = tid0; base < n; base += nthr) {
         const u32 i = base + threadIdx.x;
         u32 key = 0, uc = 0;
-        const bool cand = i < n && flip_test_eval(m, wl[i], x, key, uc);
+        const bool cand = i < n && flip_test_eval(m, wl[i], round, x, key, uc);
         const u32 o = block_reserve<BLOCK>(&rc->cand, cand ? 1u : 0u);
         if (cand) flip_cand_store(w, o, key, uc, ctr);
     }

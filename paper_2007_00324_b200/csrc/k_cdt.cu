@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(CDT_BLOCK, GDP2D_CDT_MINB) k_cdt_delaunay(cons
             const u32 round = a.round0 + step;
             const u32* wl = a.w.w[cur];
             const u32 tid0 = tid - threadIdx.x;   // waves (flip_*_waves)
-            flip_test_waves<CDT_BLOCK>(m, wl, n, tid0, nthr, a.x, a.w, fr, a.ctr);
+            flip_test_waves<CDT_BLOCK>(m, wl, n, round, tid0, nthr, a.x, a.w, fr, a.ctr);
             g.sync();
             const u32 nc = min(vld(&fr->cand), a.w.cap);
             flipped += flip_apply_waves<CDT_BLOCK>(m, nc, round, cur ^ 1u, tid0, nthr, a.x, a.w, fr,

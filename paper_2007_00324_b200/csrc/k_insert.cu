@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(LAWSON_BLOCK) k_lawson_persistent(
         const u32 round = round0 + r;
         const u32* wl = w.w[cur];
         const u32 tid0 = tid - threadIdx.x;
-        flip_test_waves<LAWSON_BLOCK>(m, wl, n, tid0, nthr, x, w, rc, ctr);
+        flip_test_waves<LAWSON_BLOCK>(m, wl, n, round, tid0, nthr, x, w, rc, ctr);
         g.sync();
         const u32 nc = min(*(volatile u32*)&rc->cand, w.cap);
         flipped += flip_apply_waves<LAWSON_BLOCK>(m, nc, round, cur ^ 1u, tid0, nthr, x, w, rc, ctr);
@@ -867,7 +867,7 @@ __device__ void lawson_rounds(const InsertArgs& a, const Exec& ex, const DevMesh
         ring_advance(a, ex, step);
         const u32 round = a.round0 + step;
         const u32* wl = w.w[cur];
-        for (u32 i = ex.tid; i < n; i += ex.nthr) flip_test_one(m, wl[i], a.x, w, rc, a.ctr);
+        for (u32 i = ex.tid; i < n; i += ex.nthr) flip_test_one(m, wl[i], round, a.x, w, rc, a.ctr);
         ex.sync();
         trace(a, ex.leader(), TR_FTEST, n);
         const u32 nc = min(vload(&rc->cand), w.cap);
@@ -932,7 +932,7 @@ __device__ void lawson_fixpoint_dev(const InsertArgs& a, const Exec& ex, const D
         const u32* wl = a.w.w[cur];
         // waves: one list reservation per CTA (flip_*_waves, gdp2d_rewrite.cuh)
         const u32 tid0 = ex.tid - threadIdx.x;
-        flip_test_waves<INSERT_BLOCK>(m, wl, n, tid0, ex.nthr, a.x, a.w, rc, a.ctr);
+        flip_test_waves<INSERT_BLOCK>(m, wl, n, round, tid0, ex.nthr, a.x, a.w, rc, a.ctr);
         ex.sync();
         trace(a, ex.leader(), TR_FTEST, n);
         const u32 nc = min(vload(&rc->cand), a.w.cap);
