@@ -37,8 +37,8 @@ void scan_partials(u32* partial, u32 ntiles, u32* d_total, cudaStream_t st);
 struct TriAux {
     u64* ckey = nullptr;     // claim key (band|measure)
     u64* ctie = nullptr;     // claim tie  (tiebreak << 32 | list index)
-    u32* owner = nullptr;    // removal / device-CDT pipe claim
-    u64* fown = nullptr;     // flip claim: max (round << 32 | ~edge key), never reset
+    u32* owner = nullptr;    // device-CDT pipe claim
+    u64* fown = nullptr;     // flip / removal claim: max (round << 32 | ~key), never reset
     u32* stamp = nullptr;    // round in which the triangle was rewritten
     u32* emap = nullptr;     // 3 per triangle: old edge slot -> new (tri<<2|edge)
     // rewrite table: every candidate claims the triangles its split REWRITES

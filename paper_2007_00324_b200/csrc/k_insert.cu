@@ -406,9 +406,13 @@ __device__ __forceinline__ void detect_collect_one(u32 V0, u32 j, const FreshInf
 
 // ---- parallel vertex removal (remove_free_vertex + flop, mesh.hpp:261-304,442-466) ----
 
+// The star claims share the flips' round-tagged claim array (fown, tag
+// round << 32 | ~v, atomicMax: the lowest vertex id of the round wins) and
+// are never released.
 __device__ __forceinline__ void rm_claim_one(const DevMesh& m, const u32* __restrict__ list, u32 i,
-                                             u32 V0, const TriAux& x, const FreshInfo& f,
-                                             const WorkLists& w, Counters* ctr) {
+                                             u32 V0, u32 round, const TriAux& x,
+                                             const FreshInfo& f, const WorkLists& w,
+                                             Counters* ctr) {
     const u32 v = list[i];
     u32* st = w.star + (size_t)i * MAX_STAR;
     int si[MAX_STAR];
@@ -427,7 +431,8 @@ __device__ __forceinline__ void rm_claim_one(const DevMesh& m, const u32* __rest
         w.star_len[i] = 0;
         return;
     }
-    for (int q = 0; q < k; ++q) atomicMin(&x.owner[st[q]], v);
+    const u64 tag = flip_tag(round, v);
+    for (int q = 0; q < k; ++q) atomicMax((ull*)&x.fown[st[q]], (ull)tag);
 }
 
 // Remove v by ear-clipping its link polygon: each ear is one degree-reducing
@@ -483,9 +488,10 @@ __device__ __noinline__ u32 rm_apply_one_n(const DevMesh& m, const u32* __restri
         const u32* st = w.star + (size_t)i * MAX_STAR;
         const int k = (int)w.star_len[i];
         bool own = k >= 3;
+        const u64 tag = flip_tag(round, v);
         // independent loads, no early exit: the claims arrive together
 #pragma unroll 8
-        for (int q = 0; q < k; ++q) own &= x.owner[st[q]] == v;
+        for (int q = 0; q < k; ++q) own &= x.fown[st[q]] == tag;
         if (k >= 3 && !own) {
             if (!lead) {
             } else if (out) {
@@ -720,12 +726,6 @@ __device__ __forceinline__ u32 rm_apply_warp(const DevMesh& m, const u32* __rest
     if ((threadIdx.x & 31u) != 0u) return 0;
     return rm_apply_one_n<MAX_STAR, false>(m, list, i, round, V0, widx, next_list, x, f, w, rc,
                                            ctr, seed_rc, nullptr);
-}
-
-__device__ __forceinline__ void rm_post_one(u32 i, const TriAux& x, const WorkLists& w) {
-    const u32* st = w.star + (size_t)i * MAX_STAR;
-    const u32 k = w.star_len[i];
-    for (u32 q = 0; q < k; ++q) x.owner[st[q]] = NONE;
 }
 
 // =====================================================================================
@@ -1292,7 +1292,7 @@ __device__ void rollback_loop(const InsertArgs& a, const Exec& ex, u32 nv, u32 n
             ring_advance(a, ex, step);
             const u32 round = a.round0 + step;
             const u32* list = w.rm[rcur];
-            for (u32 i = ex.tid; i < nrm; i += ex.nthr) rm_claim_one(m, list, i, V0, a.x, a.f, w, a.ctr);
+            for (u32 i = ex.tid; i < nrm; i += ex.nthr) rm_claim_one(m, list, i, V0, round, a.x, a.f, w, a.ctr);
             ex.sync();
             trace(a, ex.leader(), TR_RM_CLAIM, nrm);
             if (nrm <= a.rm_warp * (ex.nthr >> 5)) {
@@ -1324,7 +1324,6 @@ __device__ void rollback_loop(const InsertArgs& a, const Exec& ex, u32 nv, u32 n
             }
             ex.sync();
             trace(a, ex.leader(), TR_RM_APPLY);
-            for (u32 i = ex.tid; i < nrm; i += ex.nthr) rm_post_one(i, a.x, w);
             const u32 ntouch = min(vload(&rc->touched), w.cap);
             for (u32 i = ex.tid; i < ntouch; i += ex.nthr)
                 fixup_one(m, round, a.x, w, w.touched[i], 0, 0, rc, a.ctr);
