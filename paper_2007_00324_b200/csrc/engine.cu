@@ -604,18 +604,18 @@ void ensure_regions(gdp2d_ctx* x, u32 n, u32 ncav, u32 stride = 0) {
 void ensure_aux(gdp2d_ctx* x) {
     const u32 T = x->work.tcap;
     if (T > x->aux_cap) {
-        dfree(x->aux.ckey); dfree(x->aux.ctie); dfree(x->aux.owner); dfree(x->aux.stamp);
-        dfree(x->aux.emap); dfree(x->aux.fkey); dfree(x->aux.ftie); dfree(x->aux.fown);
+        dfree(x->aux.ckey); dfree(x->aux.ctie); dfree(x->aux.owner); dfree(x->aux.se);
+        dfree(x->aux.fkey); dfree(x->aux.ftie); dfree(x->aux.fown);
         dalloc(x->aux.fown, T);
         dalloc(x->aux.ckey, T); dalloc(x->aux.ctie, T); dalloc(x->aux.owner, T);
-        dalloc(x->aux.stamp, T); dalloc(x->aux.emap, 3ull * T);
+        dalloc(x->aux.se, 4ull * T);
         dalloc(x->aux.fkey, T); dalloc(x->aux.ftie, T);
         CK(cudaMemsetAsync(x->aux.ckey, 0, sizeof(u64) * T, x->st));
         CK(cudaMemsetAsync(x->aux.ctie, 0xFF, sizeof(u64) * T, x->st));
         CK(cudaMemsetAsync(x->aux.fkey, 0, sizeof(u64) * T, x->st));
         CK(cudaMemsetAsync(x->aux.ftie, 0xFF, sizeof(u64) * T, x->st));
         CK(cudaMemsetAsync(x->aux.owner, 0xFF, sizeof(u32) * T, x->st));
-        CK(cudaMemsetAsync(x->aux.stamp, 0, sizeof(u32) * T, x->st));
+        CK(cudaMemsetAsync(x->aux.se, 0, sizeof(u32) * 4ull * T, x->st));
         // flip claims are tagged with the round, which restarts here
         CK(cudaMemsetAsync(x->aux.fown, 0, sizeof(u64) * T, x->st));
         x->aux_cap = T;
@@ -824,8 +824,8 @@ void ctx_release(gdp2d_ctx* x) {
     cudaSetDevice(x->device);
     mesh_free(x->work);
     mesh_free(x->pristine);
-    dfree(x->aux.ckey); dfree(x->aux.ctie); dfree(x->aux.owner); dfree(x->aux.stamp);
-    dfree(x->aux.emap); dfree(x->aux.fkey); dfree(x->aux.ftie); dfree(x->aux.fown);
+    dfree(x->aux.ckey); dfree(x->aux.ctie); dfree(x->aux.owner); dfree(x->aux.se);
+    dfree(x->aux.fkey); dfree(x->aux.ftie); dfree(x->aux.fown);
     dfree(x->flags);
     cands_free(x->c);
     dfree(x->regions); dfree(x->region_len); dfree(x->bfs_len);

@@ -39,8 +39,10 @@ struct TriAux {
     u64* ctie = nullptr;     // claim tie  (tiebreak << 32 | list index)
     u32* owner = nullptr;    // device-CDT pipe claim
     u64* fown = nullptr;     // flip / removal claim: max (round << 32 | ~key), never reset
-    u32* stamp = nullptr;    // round in which the triangle was rewritten
-    u32* emap = nullptr;     // 3 per triangle: old edge slot -> new (tri<<2|edge)
+    // one 16-byte record per triangle: se[4t] = stamp (round in which the
+    // triangle was rewritten), se[4t + 1 + k] = emap (old edge slot k -> new
+    // tri<<2|edge); fixup reads a far side's stamp and emap in one load
+    u32* se = nullptr;
     // rewrite table: every candidate claims the triangles its split REWRITES
     // (located, + the far side of a split edge); see gdp2d_phases.cuh
     u64* fkey = nullptr;

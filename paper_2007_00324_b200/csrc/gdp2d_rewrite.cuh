@@ -4,7 +4,8 @@
 // Phase A: the owner of a claimed region rewrites its triangles in place
 // (write_tri), marks the edges whose far side is outside the region as
 // pending (tn.w bits) and records, per old edge slot, where that edge now
-// lives (emap) together with stamp[t] = round.  Phase B (fixup_one, after a
+// lives (emap) together with stamp[t] = round -- one 16-byte record per
+// triangle, TriAux::se = {stamp, emap[0..2]}.  Phase B (fixup_one, after a
 // barrier): each rewritten triangle resolves its pending edges -- a far side
 // rewritten in the same round is followed through its emap, any other far
 // side gets its back-pointer written.  Regions of one round must be disjoint;
@@ -66,13 +67,13 @@ static __device__ void split_triangle_A(const DevMesh& m, const TriAux& x, const
                                  int seed = 0, Counters* ctr = nullptr,
                                  const u32* slots = nullptr) {
     const uint4 ov = m.tv[t], on = m.tn[t], os = load_ts(m, t, ov);
-    x.stamp[t] = round;
+    x.se[4 * t] = round;
     write_tri(m, t, ov.x, ov.y, wv, enc(t1, 1), enc(t2, 0), on.z, 4u, NONE, NONE, os.z, w.vtri_from);
     write_tri(m, t1, ov.y, ov.z, wv, enc(t2, 1), enc(t, 0), on.x, 4u, NONE, NONE, os.x, w.vtri_from);
     write_tri(m, t2, ov.z, ov.x, wv, enc(t, 1), enc(t1, 0), on.y, 4u, NONE, NONE, os.y, w.vtri_from);
-    x.emap[3 * t + 0] = enc(t1, 2);
-    x.emap[3 * t + 1] = enc(t2, 2);
-    x.emap[3 * t + 2] = enc(t, 2);
+    x.se[4 * t + 1 + 0] = enc(t1, 2);
+    x.se[4 * t + 1 + 1] = enc(t2, 2);
+    x.se[4 * t + 1 + 2] = enc(t, 2);
     m.vtri[wv] = NONE;
     const u32 tl[3] = {t, t1, t2};
     push_touched(w, tl, 3, rc, slots ? slots[0] : NONE);
@@ -93,16 +94,16 @@ static __device__ void split_edge_A(const DevMesh& m, const TriAux& x, const Wor
     const uint4 ov = m.tv[t], on = m.tn[t], os = load_ts(m, t, ov);
     const u32 a = comp(ov, e), b = comp(ov, nxt(e)), c = comp(ov, prv(e));
     const u32 uc = comp(on, e);
-    x.stamp[t] = round;
+    x.se[4 * t] = round;
     if (uc == NONE) {
         // t := (a,b,w) {-, t2, n_prev}, t2 := (a,w,c) {-, n_next, t}
         write_tri(m, t, a, b, wv, NONE, enc(t2, 2), comp(on, prv(e)), 4u, s_bw, NONE,
                   comp(os, prv(e)), w.vtri_from);
         write_tri(m, t2, a, wv, c, NONE, comp(on, nxt(e)), enc(t, 1), 2u, s_wc,
                   comp(os, nxt(e)), NONE, w.vtri_from);
-        x.emap[3 * t + nxt(e)] = enc(t2, 1);
-        x.emap[3 * t + prv(e)] = enc(t, 2);
-        x.emap[3 * t + e] = NONE;
+        x.se[4 * t + 1 + nxt(e)] = enc(t2, 1);
+        x.se[4 * t + 1 + prv(e)] = enc(t, 2);
+        x.se[4 * t + 1 + e] = NONE;
         m.vtri[wv] = NONE;
         const u32 tl[2] = {t, t2};
         push_touched(w, tl, 2, rc, slots ? slots[0] : NONE);
@@ -120,7 +121,7 @@ static __device__ void split_edge_A(const DevMesh& m, const TriAux& x, const Wor
     const int f = eidx(uc);
     const uint4 uv = m.tv[u], un = m.tn[u], us = load_ts(m, u, uv);
     const u32 d = comp(uv, f);
-    x.stamp[u] = round;
+    x.se[4 * u] = round;
     // t := (a,b,w) {u2, t2, n_ab}; t2 := (a,w,c) {u, n_ca, t}
     write_tri(m, t, a, b, wv, enc(u2, 0), enc(t2, 2), comp(on, prv(e)), 4u, s_bw, NONE,
               comp(os, prv(e)), w.vtri_from);
@@ -131,12 +132,12 @@ static __device__ void split_edge_A(const DevMesh& m, const TriAux& x, const Wor
               comp(us, prv(f)), w.vtri_from);
     write_tri(m, u2, d, wv, b, enc(t, 0), comp(un, nxt(f)), enc(u, 1), 2u, s_bw,
               comp(us, nxt(f)), NONE, w.vtri_from);
-    x.emap[3 * t + nxt(e)] = enc(t2, 1);
-    x.emap[3 * t + prv(e)] = enc(t, 2);
-    x.emap[3 * t + e] = NONE;
-    x.emap[3 * u + prv(f)] = enc(u, 2);
-    x.emap[3 * u + nxt(f)] = enc(u2, 1);
-    x.emap[3 * u + f] = NONE;
+    x.se[4 * t + 1 + nxt(e)] = enc(t2, 1);
+    x.se[4 * t + 1 + prv(e)] = enc(t, 2);
+    x.se[4 * t + 1 + e] = NONE;
+    x.se[4 * u + 1 + prv(f)] = enc(u, 2);
+    x.se[4 * u + 1 + nxt(f)] = enc(u2, 1);
+    x.se[4 * u + 1 + f] = NONE;
     m.vtri[wv] = NONE;
     const u32 tl[4] = {t, t2, u, u2};
     push_touched(w, tl, 4, rc, slots ? slots[0] : NONE);
@@ -171,20 +172,18 @@ __device__ __forceinline__ void fixup_one(const DevMesh& m, u32 round, const Tri
     if (!tv.w) return;
     const uint4 ts = load_ts(m, t, tv);
     const u32 pend = tn.w;
-    // the far sides' stamps are loaded together before any store (a store
-    // between them would order each load behind it)
-    u32 sx[3];
+    // each far side's {stamp, emap[3]} record in one 16-byte load, all three
+    // issued together before any store (a store between them would order
+    // each load behind it)
+    u32 sx[3], em[3];
 #pragma unroll
     for (int e = 0; e < 3; ++e) {
         const u32 r = comp(tn, e);
-        sx[e] = (((pend >> e) & 1u) && r != NONE) ? x.stamp[etri(r)] : 0u;
-    }
-    u32 em[3];
-#pragma unroll
-    for (int e = 0; e < 3; ++e) {
-        const u32 r = comp(tn, e);
-        em[e] = (((pend >> e) & 1u) && r != NONE && sx[e] == round)
-                    ? x.emap[3 * etri(r) + eidx(r)] : NONE;
+        uint4 se = make_uint4(0u, NONE, NONE, NONE);
+        if (((pend >> e) & 1u) && r != NONE) se = reinterpret_cast<const uint4*>(x.se)[etri(r)];
+        sx[e] = se.x;
+        const int k = r != NONE ? eidx(r) : 0;   // emap slot k is word 1 + k
+        em[e] = k == 0 ? se.y : (k == 1 ? se.z : se.w);
     }
 #pragma unroll
     for (int e = 0; e < 3; ++e) {
@@ -324,12 +323,12 @@ __device__ __forceinline__ bool flip_apply_core(const DevMesh& m, u32 i, u32 rou
     const bool won = ot == tag && ou == tag;
     w.fwin[i] = won;
     // exactly one duplicate performs the flip
-    if (!won || atomicExch(&x.stamp[t], round) == round) return false;
+    if (!won || atomicExch(&x.se[4 * t], round) == round) return false;
     const u32 a = comp(tv, e), b = comp(tv, nxt(e)), c = comp(tv, prv(e));
     const u32 d = comp(uv, f);
     const double2 pa = m.xy[a], pb = m.xy[b], pc = m.xy[c], pd = m.xy[d];
     const uint4 ts = load_ts(m, t, tv), us = load_ts(m, u, uv);
-    x.stamp[u] = round;
+    x.se[4 * u] = round;
     if (orient2d(pa, pb, pd) <= 0 || orient2d(pa, pd, pc) <= 0) {
         if (atomicCAS(&ctr->err_code, 0u, (u32)DERR_NONCONVEX_FLIP) == 0u) {
             ctr->err_info = t;
@@ -342,12 +341,12 @@ __device__ __forceinline__ bool flip_apply_core(const DevMesh& m, u32 i, u32 rou
               comp(us, nxt(f)), NONE, comp(ts, prv(e)), w.vtri_from);
     write_tri(m, u, a, d, c, comp(un, prv(f)), comp(tn, nxt(e)), enc(t, 1), 3u,
               comp(us, prv(f)), comp(ts, nxt(e)), NONE, w.vtri_from);
-    x.emap[3 * t + nxt(e)] = enc(u, 1);
-    x.emap[3 * t + prv(e)] = enc(t, 2);
-    x.emap[3 * t + e] = NONE;
-    x.emap[3 * u + nxt(f)] = enc(t, 0);
-    x.emap[3 * u + prv(f)] = enc(u, 0);
-    x.emap[3 * u + f] = NONE;
+    x.se[4 * t + 1 + nxt(e)] = enc(u, 1);
+    x.se[4 * t + 1 + prv(e)] = enc(t, 2);
+    x.se[4 * t + 1 + e] = NONE;
+    x.se[4 * u + 1 + nxt(f)] = enc(t, 0);
+    x.se[4 * u + 1 + prv(f)] = enc(u, 0);
+    x.se[4 * u + 1 + f] = NONE;
     t_out = t;
     u_out = u;
     return true;
@@ -388,7 +387,7 @@ __device__ __forceinline__ u32 flip_post_core(u32 i, u32 round, const TriAux& x,
                                               const WorkLists& w) {
     const u32 key = w.fc[i], uc = w.fu[i];
     const u32 t = etri(key), u = etri(uc);
-    return (!w.fwin[i] && x.stamp[t] != round && x.stamp[u] != round) ? key : NONE;
+    return (!w.fwin[i] && x.se[4 * t] != round && x.se[4 * u] != round) ? key : NONE;
 }
 
 __device__ __forceinline__ void flip_post_one(u32 i, u32 round, u32 widx, const TriAux& x,

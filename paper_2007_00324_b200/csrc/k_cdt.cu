@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(CDT_BLOCK, GDP2D_CDT_MINB) k_cdt_delaunay(cons
             const u32 t = a.ptri[i];
             if (t >= PT_DEFER) continue;
             ++left;
-            if (a.x.stamp[t] >= R) relocate(a, i, t);
+            if (a.x.se[4 * t] >= R) relocate(a, i, t);
         }
         block_add(&lr->detect, left);
         g.sync();
@@ -649,10 +649,10 @@ __device__ bool recover_pipe(const CdtArgs& a, u32 p, const u32* gid, u32 len, u
                 nn[e2] = r;
                 if (r != NONE) pend |= 1u << e2;
                 const u32 o = comp(T.o, e2);
-                a.x.emap[3 * etri(o) + eidx(o)] = enc(g, e2);
+                a.x.se[4 * (etri(o)) + 1 + eidx(o)] = enc(g, e2);
             }
         }
-        a.x.stamp[g] = R;
+        a.x.se[4 * g] = R;
         write_tri(m, g, T.v.x, T.v.y, T.v.z, nn[0], nn[1], nn[2], pend, T.s.x, T.s.y, T.s.z);
     }
     {

@@ -7,7 +7,7 @@
 //   phase A (owner thread): rewrite the owned triangles + allocate new ones;
 //     references leaving the owned set keep the OLD outer (tri<<2|edge) and
 //     are flagged pending in tn.w; every old boundary slot records where its
-//     edge went in emap[3*t+e]; owned triangles are stamped with the round.
+//     edge went in emap (TriAux::se); owned triangles are stamped with the round.
 //   phase B (launch_fixup, one thread per touched triangle): a pending ref to
 //     a triangle stamped this round is translated through its emap; a ref to
 //     an untouched triangle stays and gets its back-pointer written (single
@@ -517,7 +517,7 @@ __device__ __noinline__ u32 rm_apply_one_n(const DevMesh& m, const u32* __restri
                 R[q] = comp(tn, iv);
                 PK[q] = R[q] == NONE ? 0 : 1;
                 SG[q] = comp(ts, iv);
-                ORG[q] = 3 * t + iv;
+                ORG[q] = 4 * t + 1 + iv;   // word of emap slot iv in TriAux::se
                 NX[q] = q + 1 == k ? 0 : q + 1;
                 PV[q] = q == 0 ? k - 1 : q - 1;
             }
@@ -544,7 +544,7 @@ __device__ __noinline__ u32 rm_apply_one_n(const DevMesh& m, const u32* __restri
                     CN[ci][slot] = R[le];
                     CK[ci][slot] = PK[le];
                 }
-                if (lead && ORG[le] != NONE) x.emap[ORG[le]] = enc(tid, slot);
+                if (lead && ORG[le] != NONE) x.se[ORG[le]] = enc(tid, slot);
             };
             u32 alive = N >= 32 ? ~0u : ((1u << k) - 1u);   // WARP: link positions left
             while (cnt > 3 && ok) {
@@ -671,7 +671,7 @@ __device__ __noinline__ u32 rm_apply_one_n(const DevMesh& m, const u32* __restri
                     }
                 }
             } else {
-                for (int q = 0; q < k; ++q) x.stamp[st[q]] = round;
+                for (int q = 0; q < k; ++q) x.se[4 * (st[q])] = round;
                 for (int ci = 0; ci < created; ++ci) {
                     const u32 pend = (CK[ci][0] == 1 ? 1u : 0u) | (CK[ci][1] == 1 ? 2u : 0u) |
                                      (CK[ci][2] == 1 ? 4u : 0u);
