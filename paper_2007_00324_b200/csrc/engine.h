@@ -35,8 +35,11 @@ void scan_partials(u32* partial, u32 ntiles, u32* d_total, cudaStream_t st);
 
 // Per-triangle scratch (claims, stamps, edge maps).
 struct TriAux {
-    u64* ckey = nullptr;     // claim key (band|measure)
-    u64* ctie = nullptr;     // claim tie  (tiebreak << 32 | list index)
+    // claim key (band|measure) and tie (tiebreak << 32 | list index) of
+    // triangle t at ckey[cslot(t)] / ctie[cslot(t)]: one allocation of 2T
+    // words, ctie = ckey + 1 (interleaved 16-byte records)
+    u64* ckey = nullptr;
+    u64* ctie = nullptr;
     u32* owner = nullptr;    // device-CDT pipe claim
     u64* fown = nullptr;     // flip / removal claim: max (round << 32 | ~key), never reset
     // one 16-byte record per triangle: se[4t] = stamp (round in which the

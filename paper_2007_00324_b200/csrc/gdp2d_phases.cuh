@@ -86,15 +86,20 @@ __device__ __forceinline__ u64 tie_of(const DevCands& c, u32 i) {
     return ((u64)c.tie[i] << 32) | (u64)i;
 }
 
+// The claim tables: ckey and ctie of triangle t share one 16-byte record
+// (TriAux: ctie = ckey + 1, both indexed by cslot(t)), so a check reads one
+// sector and a reset writes one.
+__device__ __forceinline__ size_t cslot(u32 t) { return 2ull * t; }
+
 __device__ __forceinline__ void claim_max_one(const DevCands& c, u32 i, u64* ckey) {
-    if (c.alive[i]) atomicMax((ull*)&ckey[c.loc[i]], (ull)c.key[i]);
+    if (c.alive[i]) atomicMax((ull*)&ckey[cslot(c.loc[i])], (ull)c.key[i]);
 }
 
 __device__ __forceinline__ void claim_tie_one(const DevCands& c, u32 i, const u64* ckey,
                                               u64* ctie) {
     if (c.alive[i]) {
         const u32 t = c.loc[i];
-        if (ckey[t] == c.key[i]) atomicMin((ull*)&ctie[t], (ull)tie_of(c, i));
+        if (ckey[cslot(t)] == c.key[i]) atomicMin((ull*)&ctie[cslot(t)], (ull)tie_of(c, i));
     }
 }
 
@@ -103,7 +108,7 @@ __device__ __forceinline__ u32 claim_check_one(const DevCands& c, u32 i, const u
                                                const u64* ctie) {
     if (!c.alive[i]) return 0;
     const u32 t = c.loc[i];
-    const bool own = ckey[t] == c.key[i] && ctie[t] == tie_of(c, i);
+    const bool own = ckey[cslot(t)] == c.key[i] && ctie[cslot(t)] == tie_of(c, i);
     if (!own) c.alive[i] = 0;
     return own ? 1u : 0u;
 }
@@ -112,8 +117,8 @@ __device__ __forceinline__ void claim_reset_one(const DevCands& c, u32 i, u32 nT
                                                 u64* ctie) {
     const u32 t = c.loc[i];
     if (t < nT) {
-        ckey[t] = 0;
-        ctie[t] = ~0ull;
+        ckey[cslot(t)] = 0;
+        ctie[cslot(t)] = ~0ull;
     }
 }
 
@@ -164,7 +169,7 @@ __device__ __forceinline__ u32 cavity_bfs_one(const DevMesh& m, const DevCands& 
             }
             lreg[len++] = t;
             bloom |= tb;
-            atomicMax((ull*)&ckey[t], (ull)key);
+            atomicMax((ull*)&ckey[cslot(t)], (ull)key);
             for (int e = 0; e < 3; ++e) {
                 if (has_seg(tv, e)) continue;
                 const u32 cc = comp(tn, e);
@@ -200,9 +205,9 @@ __device__ __forceinline__ void cavity_tie_one(const DevCands& c, u32 i, u32 rs,
         const u32 n = min(len - k0, 64u);
         ull hold = 0;   // bit k: this candidate holds the key of reg[k0 + k]
 #pragma unroll 4
-        for (u32 k = 0; k < n; ++k) hold |= (ull)(ckey[reg[k0 + k]] == key) << k;
+        for (u32 k = 0; k < n; ++k) hold |= (ull)(ckey[cslot(reg[k0 + k])] == key) << k;
         for (u32 k = 0; k < n; ++k)
-            if ((hold >> k) & 1ull) atomicMin((ull*)&ctie[reg[k0 + k]], (ull)tie);
+            if ((hold >> k) & 1ull) atomicMin((ull*)&ctie[cslot(reg[k0 + k])], (ull)tie);
     }
 }
 
@@ -220,7 +225,7 @@ __device__ __forceinline__ u32 cavity_check_one(const DevCands& c, u32 i, u32 rs
 #pragma unroll 4
     for (u32 k = 0; k < len; ++k) {
         const u32 t = reg[k];
-        own &= (ckey[t] == key) & (ctie[t] == tie);
+        own &= (ckey[cslot(t)] == key) & (ctie[cslot(t)] == tie);
     }
     if (!own) c.alive[i] = 0;
     return own ? 1u : 0u;
@@ -231,8 +236,8 @@ __device__ __forceinline__ void cavity_reset_one(u32 i, u32 rs, const u32* regio
     const u32 len = region_len[i];
     const u32* reg = regions + (size_t)i * rs;
     for (u32 k = 0; k < len; ++k) {
-        ckey[reg[k]] = 0;
-        ctie[reg[k]] = ~0ull;
+        ckey[cslot(reg[k])] = 0;
+        ctie[cslot(reg[k])] = ~0ull;
     }
 }
 
@@ -383,7 +388,7 @@ __device__ __forceinline__ u32 cavity_claims_one(const DevMesh& m, const DevCand
             blen = len;
         }
         const u64 key = c.key[i];
-        for (u32 k = 0; k < len; ++k) atomicMax((ull*)&ckey[reg[k]], (ull)key);
+        for (u32 k = 0; k < len; ++k) atomicMax((ull*)&ckey[cslot(reg[k])], (ull)key);
     }
     region_len[i] = len;
     return blen;
