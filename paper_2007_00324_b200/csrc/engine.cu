@@ -605,16 +605,16 @@ void ensure_aux(gdp2d_ctx* x) {
     const u32 T = x->work.tcap;
     if (T > x->aux_cap) {
         dfree(x->aux.ckey); x->aux.ctie = nullptr; dfree(x->aux.owner); dfree(x->aux.se);
-        dfree(x->aux.fkey); dfree(x->aux.ftie); dfree(x->aux.fown);
+        dfree(x->aux.fkey); x->aux.ftie = nullptr; dfree(x->aux.fown);
         dalloc(x->aux.fown, T);
         dalloc(x->aux.ckey, 2ull * T); x->aux.ctie = x->aux.ckey + 1; dalloc(x->aux.owner, T);
         dalloc(x->aux.se, 4ull * T);
-        dalloc(x->aux.fkey, T); dalloc(x->aux.ftie, T);
+        dalloc(x->aux.fkey, 2ull * T); x->aux.ftie = x->aux.fkey + 1;
         // interleaved records: keys 0, ties ~0
         CK(cudaMemset2DAsync(x->aux.ckey, 2 * sizeof(u64), 0, sizeof(u64), T, x->st));
         CK(cudaMemset2DAsync(x->aux.ctie, 2 * sizeof(u64), 0xFF, sizeof(u64), T, x->st));
-        CK(cudaMemsetAsync(x->aux.fkey, 0, sizeof(u64) * T, x->st));
-        CK(cudaMemsetAsync(x->aux.ftie, 0xFF, sizeof(u64) * T, x->st));
+        CK(cudaMemset2DAsync(x->aux.fkey, 2 * sizeof(u64), 0, sizeof(u64), T, x->st));
+        CK(cudaMemset2DAsync(x->aux.ftie, 2 * sizeof(u64), 0xFF, sizeof(u64), T, x->st));
         CK(cudaMemsetAsync(x->aux.owner, 0xFF, sizeof(u32) * T, x->st));
         CK(cudaMemsetAsync(x->aux.se, 0, sizeof(u32) * 4ull * T, x->st));
         // flip claims are tagged with the round, which restarts here
@@ -826,7 +826,7 @@ void ctx_release(gdp2d_ctx* x) {
     mesh_free(x->work);
     mesh_free(x->pristine);
     dfree(x->aux.ckey); x->aux.ctie = nullptr; dfree(x->aux.owner); dfree(x->aux.se);
-    dfree(x->aux.fkey); dfree(x->aux.ftie); dfree(x->aux.fown);
+    dfree(x->aux.fkey); x->aux.ftie = nullptr; dfree(x->aux.fown);
     dfree(x->flags);
     cands_free(x->c);
     dfree(x->regions); dfree(x->region_len); dfree(x->bfs_len);

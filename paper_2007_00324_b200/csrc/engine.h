@@ -48,7 +48,7 @@ struct TriAux {
     u32* se = nullptr;
     // rewrite table: every candidate claims the triangles its split REWRITES
     // (located, + the far side of a split edge); see gdp2d_phases.cuh
-    u64* fkey = nullptr;
+    u64* fkey = nullptr;     // interleaved like ckey / ctie: ftie = fkey + 1, cslot(t)
     u64* ftie = nullptr;
 };
 

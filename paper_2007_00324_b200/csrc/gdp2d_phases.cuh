@@ -88,7 +88,7 @@ __device__ __forceinline__ u64 tie_of(const DevCands& c, u32 i) {
 
 // The claim tables: ckey and ctie of triangle t share one 16-byte record
 // (TriAux: ctie = ckey + 1, both indexed by cslot(t)), so a check reads one
-// sector and a reset writes one.
+// sector and a reset writes one; the rewrite table's fkey / ftie likewise.
 __device__ __forceinline__ size_t cslot(u32 t) { return 2ull * t; }
 
 __device__ __forceinline__ void claim_max_one(const DevCands& c, u32 i, u64* ckey) {
@@ -444,8 +444,8 @@ __device__ __forceinline__ void rw_claim_one(const DevMesh& m, const DevCands& c
     if (c.alive[i]) {
         u32 t;
         rw_set(m, c, i, t, far);
-        atomicMax((ull*)&fkey[t], (ull)c.key[i]);
-        if (far != NONE) atomicMax((ull*)&fkey[far], (ull)c.key[i]);
+        atomicMax((ull*)&fkey[cslot(t)], (ull)c.key[i]);
+        if (far != NONE) atomicMax((ull*)&fkey[cslot(far)], (ull)c.key[i]);
     }
     c.far[i] = far;
 }
@@ -454,16 +454,16 @@ __device__ __forceinline__ void rw_tie_one(const DevCands& c, u32 i, const u64* 
     if (!c.alive[i]) return;
     const u64 key = c.key[i], tie = tie_of(c, i);
     const u32 t = c.loc[i], far = c.far[i];
-    if (fkey[t] == key) atomicMin((ull*)&ftie[t], (ull)tie);
-    if (far != NONE && fkey[far] == key) atomicMin((ull*)&ftie[far], (ull)tie);
+    if (fkey[cslot(t)] == key) atomicMin((ull*)&ftie[cslot(t)], (ull)tie);
+    if (far != NONE && fkey[cslot(far)] == key) atomicMin((ull*)&ftie[cslot(far)], (ull)tie);
 }
 
 __device__ __forceinline__ bool rw_owns(const DevCands& c, u32 i, const u64* fkey,
                                         const u64* ftie) {
     const u64 key = c.key[i], tie = tie_of(c, i);
     const u32 t = c.loc[i], far = c.far[i];
-    if (fkey[t] != key || ftie[t] != tie) return false;
-    if (far != NONE && (fkey[far] != key || ftie[far] != tie)) return false;
+    if (fkey[cslot(t)] != key || ftie[cslot(t)] != tie) return false;
+    if (far != NONE && (fkey[cslot(far)] != key || ftie[cslot(far)] != tie)) return false;
     return true;
 }
 
@@ -471,12 +471,12 @@ __device__ __forceinline__ void rw_reset_one(const DevCands& c, u32 i, u32 nT, u
                                              u64* ftie) {
     const u32 t = c.loc[i], far = c.far[i];
     if (t < nT) {
-        fkey[t] = 0;
-        ftie[t] = ~0ull;
+        fkey[cslot(t)] = 0;
+        ftie[cslot(t)] = ~0ull;
     }
     if (far != NONE && far < nT) {
-        fkey[far] = 0;
-        ftie[far] = ~0ull;
+        fkey[cslot(far)] = 0;
+        ftie[cslot(far)] = ~0ull;
     }
 }
 
