@@ -90,6 +90,13 @@ __device__ __forceinline__ u64 tie_of(const DevCands& c, u32 i) {
 // (TriAux: ctie = ckey + 1, both indexed by cslot(t)), so a check reads one
 // sector and a reset writes one; the rewrite table's fkey / ftie likewise.
 __device__ __forceinline__ size_t cslot(u32 t) { return 2ull * t; }
+// the whole {key, tie} record of t: one 16-byte load / store
+__device__ __forceinline__ ulonglong2 claim_rec(const u64* key_tab, u32 t) {
+    return reinterpret_cast<const ulonglong2*>(key_tab)[t];
+}
+__device__ __forceinline__ void claim_clear(u64* key_tab, u32 t) {
+    reinterpret_cast<ulonglong2*>(key_tab)[t] = make_ulonglong2(0ull, ~0ull);
+}
 
 __device__ __forceinline__ void claim_max_one(const DevCands& c, u32 i, u64* ckey) {
     if (c.alive[i]) atomicMax((ull*)&ckey[cslot(c.loc[i])], (ull)c.key[i]);
@@ -108,7 +115,9 @@ __device__ __forceinline__ u32 claim_check_one(const DevCands& c, u32 i, const u
                                                const u64* ctie) {
     if (!c.alive[i]) return 0;
     const u32 t = c.loc[i];
-    const bool own = ckey[cslot(t)] == c.key[i] && ctie[cslot(t)] == tie_of(c, i);
+    (void)ctie;
+    const ulonglong2 r = claim_rec(ckey, t);
+    const bool own = r.x == c.key[i] && r.y == tie_of(c, i);
     if (!own) c.alive[i] = 0;
     return own ? 1u : 0u;
 }
@@ -116,10 +125,8 @@ __device__ __forceinline__ u32 claim_check_one(const DevCands& c, u32 i, const u
 __device__ __forceinline__ void claim_reset_one(const DevCands& c, u32 i, u32 nT, u64* ckey,
                                                 u64* ctie) {
     const u32 t = c.loc[i];
-    if (t < nT) {
-        ckey[cslot(t)] = 0;
-        ctie[cslot(t)] = ~0ull;
-    }
+    (void)ctie;
+    if (t < nT) claim_clear(ckey, t);
 }
 
 __device__ __forceinline__ ull bloom_bit(u32 t) { return 1ull << ((t * 0x9E3779B1u) >> 26); }
@@ -224,8 +231,8 @@ __device__ __forceinline__ u32 cavity_check_one(const DevCands& c, u32 i, u32 rs
     // no early exit: the loads of the whole region are issued together
 #pragma unroll 4
     for (u32 k = 0; k < len; ++k) {
-        const u32 t = reg[k];
-        own &= (ckey[cslot(t)] == key) & (ctie[cslot(t)] == tie);
+        const ulonglong2 r = claim_rec(ckey, reg[k]);
+        own &= (r.x == key) & (r.y == tie);
     }
     if (!own) c.alive[i] = 0;
     return own ? 1u : 0u;
@@ -235,10 +242,8 @@ __device__ __forceinline__ void cavity_reset_one(u32 i, u32 rs, const u32* regio
                                                  const u32* region_len, u64* ckey, u64* ctie) {
     const u32 len = region_len[i];
     const u32* reg = regions + (size_t)i * rs;
-    for (u32 k = 0; k < len; ++k) {
-        ckey[cslot(reg[k])] = 0;
-        ctie[cslot(reg[k])] = ~0ull;
-    }
+    (void)ctie;
+    for (u32 k = 0; k < len; ++k) claim_clear(ckey, reg[k]);
 }
 
 // ---- isolated insertion claims (GDP2D_INSERT_ISOLATED) ------------------------
@@ -462,22 +467,18 @@ __device__ __forceinline__ bool rw_owns(const DevCands& c, u32 i, const u64* fke
                                         const u64* ftie) {
     const u64 key = c.key[i], tie = tie_of(c, i);
     const u32 t = c.loc[i], far = c.far[i];
-    if (fkey[cslot(t)] != key || ftie[cslot(t)] != tie) return false;
-    if (far != NONE && (fkey[cslot(far)] != key || ftie[cslot(far)] != tie)) return false;
-    return true;
+    (void)ftie;
+    const ulonglong2 r = claim_rec(fkey, t);
+    const ulonglong2 rf = far != NONE ? claim_rec(fkey, far) : make_ulonglong2(key, tie);
+    return r.x == key && r.y == tie && rf.x == key && rf.y == tie;
 }
 
 __device__ __forceinline__ void rw_reset_one(const DevCands& c, u32 i, u32 nT, u64* fkey,
                                              u64* ftie) {
     const u32 t = c.loc[i], far = c.far[i];
-    if (t < nT) {
-        fkey[cslot(t)] = 0;
-        ftie[cslot(t)] = ~0ull;
-    }
-    if (far != NONE && far < nT) {
-        fkey[cslot(far)] = 0;
-        ftie[cslot(far)] = ~0ull;
-    }
+    (void)ftie;
+    if (t < nT) claim_clear(fkey, t);
+    if (far != NONE && far < nT) claim_clear(fkey, far);
 }
 
 // Needs of one surviving candidate (refine.hpp:493-539): subsegments that hit
